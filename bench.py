@@ -1,0 +1,298 @@
+#!/usr/bin/env python
+"""bench.py -- online inserts/s of the B200 path on BASELINE.json configs[1] (C1).
+
+A step = one graph_insert_batch of B = 1024 points (search -> all-pairs -> update balls ->
+merge: every row of SURVEY.md 8(a) on the unpartitioned path) on the evolving graph, inputs
+already resident in HBM.  L2 is flushed (256 MiB write) between timed steps, outside the
+timed events.  Multi-GPU (torchrun): C1 is unpartitioned, so ranks run replicas (weak scaling,
+DESIGN.md "Multi-GPU").  --impl reference times the CPU oracle (the reference arm of this tier).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen as D  # noqa: E402
+
+CFG_NAME = "C1"
+
+
+def baseline_metric():
+    try:
+        return json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+    except Exception:
+        return "online inserts/sec"
+
+
+def hbm_peak():
+    try:
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, lrank
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.samples.append([x.strip() for x in ln.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def alg_bytes(st, V, k):
+    """per committed search evaluation V + 4 B, per expanded node 4k B."""
+    return st["search_evals"] * (V + 4) + st["search_expansions"] * 4 * k
+
+
+def run_cpu_baseline(cfg, X, S, rows, budget_s=12.0, nthreads=None):
+    """The oracle as it stands, on host cores: insert whole batches of the same workload.
+    Its starting graph is the exact initial graph (rows copied in: building it on the CPU takes
+    minutes and is not the timed work)."""
+    from oracle import oracle as O
+    nthreads = nthreads or os.cpu_count() or 1
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cfg.n0 + len(S) + 8)
+    o.set_rows(*rows)
+    done, t_tot = 0, 0.0
+    while t_tot < budget_s and done + cfg.batch <= len(S):
+        t0 = time.perf_counter()
+        o.insert_batch(S[done:done + cfg.batch], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed,
+                       nthreads)
+        t_tot += time.perf_counter() - t0
+        done += cfg.batch
+    return {"value": done / t_tot, "unit": "inserts/s", "cores": nthreads, "kind": "oracle",
+            "sample": "%d inserts (%d batches of %d) of %s on the exact initial graph, %.1f s" % (
+                done, done // cfg.batch, cfg.batch, cfg.name, t_tot)}
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    nthreads = os.cpu_count() or 1
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, (args.warmup + args.steps) * cfg.batch)
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cfg.n0 + len(S) + 8)
+    t0 = time.perf_counter()
+    o.init_exact(nthreads)
+    t_init = time.perf_counter() - t0
+    pos = 0
+    for _ in range(args.warmup):
+        o.insert_batch(S[pos:pos + cfg.batch], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed, nthreads)
+        pos += cfg.batch
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.insert_batch(S[pos:pos + cfg.batch], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed, nthreads)
+        pos += cfg.batch
+    t = time.perf_counter() - t0
+    val = args.steps * cfg.batch / t
+    line = {"impl": "reference", "metric": baseline_metric(), "value": val, "unit": "inserts/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": cfg_desc(cfg), "global_batch": cfg.batch},
+            "cpu_baseline": {"value": val, "unit": "inserts/s", "cores": nthreads, "kind": "oracle",
+                             "sample": "%d timed batches of %d inserts (oracle exact init %.0f s untimed)" % (
+                                 args.steps, cfg.batch, t_init)},
+            "e2e": {"value": val, "unit": "inserts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cfg_desc(cfg):
+    return ("%s: n0=%d uint8 d=%d (%d-cluster mixture), squared-L2 int32, k=%d, batches of %d, speedup=%g, "
+            "expansion %d/%d, depth %d" % (cfg.name, cfg.n0, cfg.dim, cfg.clusters, cfg.k, cfg.batch, cfg.speedup,
+                                           cfg.e_num, cfg.e_den, cfg.depth))
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_1602_06819_b200 import KnngGraph, load_library
+    load_library()
+    ws, rank, lrank = dist_env()
+    torch.cuda.set_device(lrank)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    B = cfg.batch
+    nsteps = args.warmup + args.steps
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, max(cfg.n_insert, nsteps * B))
+    V = cfg.dim if cfg.metric == D.U8 else 4 * cfg.dim
+    stream = torch.cuda.Stream()
+    cap = cfg.n0 + nsteps * B + 8
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+
+    # ---------------- device-resident inputs (value) ----------------
+    g = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
+    rows0 = g.rows() if (rank == 0 and ws == 1 and not args.no_cpu_baseline) else None
+    S_dev = torch.from_numpy(S[:nsteps * B]).to("cuda")
+    pos = 0
+    for _ in range(args.warmup):
+        g.insert_batch(S_dev[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        pos += B
+    ms_steps, stats = [], []
+    barrier()
+    with ClockSampler(lrank) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(pos & 0xFF)           # L2 flush, outside the timed events
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, st = g.insert_batch(S_dev[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+            e1.record(stream)
+            e1.synchronize()
+            ms_steps.append(e0.elapsed_time(e1))
+            stats.append(st)
+            pos += B
+    barrier()
+    t_total = sum(ms_steps) / 1000.0
+    if ws > 1:
+        t = torch.tensor([t_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_total = float(t.item())
+    value = args.steps * B * ws / t_total
+    evals = sum(s["search_evals"] + s["ball_nodes"] for s in stats)
+    ms_search = sum(s["ms_search"] for s in stats)
+    bytes_search = sum(alg_bytes(s, V, cfg.k) for s in stats)
+    peak, peak_src = hbm_peak()
+    achieved = bytes_search / (ms_search / 1000.0) / 1e9
+    launches = sum(s["kernel_launches"] for s in stats)
+
+    # recall@k of the inserted points' rows vs the exact k-nn over the final point set (sampled, torch)
+    ids, keys = g.rows(cfg.n0, pos)
+    allp = torch.from_numpy(np.concatenate([X, S[:pos]])).to("cuda").float()
+    samp = np.arange(0, pos, max(1, pos // 256))
+    q = allp[cfg.n0 + samp]
+    d2 = torch.cdist(q, allp).pow(2)
+    d2[torch.arange(len(samp)), torch.from_numpy(cfg.n0 + samp).cuda()] = float("inf")
+    exact = torch.topk(d2, cfg.k, largest=False).indices.cpu().numpy()
+    rec = float(np.mean([len(set(ids[s].tolist()) & set(exact[i].tolist())) / cfg.k for i, s in enumerate(samp)]))
+    g.close()
+
+    # ---------------- end to end through the C ABI with host buffers (e2e) ----------------
+    g2 = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
+    S_pin_t = torch.from_numpy(S[:nsteps * B]).pin_memory()
+    S_pin = S_pin_t.numpy()
+    pos2 = 0
+    for _ in range(args.warmup):
+        g2.insert_batch(S_pin[pos2:pos2 + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        pos2 += B
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        g2.insert_batch(S_pin[pos2:pos2 + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        pos2 += B
+    barrier()
+    t_e2e = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    g2.close()
+
+    line = {
+        "metric": baseline_metric(), "value": value, "unit": "inserts/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": cfg_desc(cfg), "global_batch": B * ws, "parallelism": "replicas x%d" % ws,
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+        "similarities_per_s": evals * ws / t_total,
+        "recall_at_k": rec,
+        "roofline": {"bound": "hbm", "kernel": "k_search (K1 iGNNS)", "achieved": achieved, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": bytes_search / len(stats),
+                     "ms_per_launch": ms_search / len(stats),
+                     "note": "C1 is L2-resident (14 MB store): HBM fraction is not the binding claim"},
+        "phase_ms": {p: sum(s[p] for s in stats) / len(stats) for p in ("ms_search", "ms_allpairs", "ms_update",
+                                                                       "ms_merge")},
+        "e2e": {"value": args.steps * B * ws / t_e2e, "unit": "inserts/s", "h2d_bytes_per_step": B * V,
+                "d2h_bytes_per_step": 16 * 8},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rows0 is not None:
+        line["cpu_baseline"] = run_cpu_baseline(cfg, X, S, rows0)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = D.CONFIGS[CFG_NAME]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

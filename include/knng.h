@@ -1,0 +1,184 @@
+/*
+ * knng.h -- C ABI of the B200-native online approximate k-nn graph library
+ * (arXiv 1602.06819, Debatty et al., "Fast online k-nn graph building").
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source, with the
+ * section / algorithm it falls in.  Readings Qn of points the paper leaves
+ * open are listed in DESIGN.md ("Readings").
+ *
+ * Conventions (all calls):
+ *  - extern "C", no C++ or torch types; every call returns int status
+ *    (KNNG_OK = 0, < 0 = error) and never throws.  The message of the last
+ *    error of the calling thread is graph_last_error().
+ *  - Inputs are caller-owned and only read during the call.  Outputs go to
+ *    caller-allocated buffers.  The graph handle and all device memory it
+ *    uses are owned by the library until graph_free().
+ *  - "host" pointers are ordinary CPU memory; "device" pointers are CUDA
+ *    global memory on the handle's device.  knng_points.data_on_device says
+ *    which one a point buffer is; output buffers are host memory unless the
+ *    call has an *_on_device flag.
+ *  - One handle must not be used by two threads at once.  Work is issued on
+ *    the handle's CUDA stream (knng_runtime.cuda_stream, or a stream the
+ *    library creates); every call returns after that stream has finished the
+ *    call's work.
+ *  - There is no CPU fallback: every step of every call runs in the
+ *    library's CUDA kernels (sm_100a).  Without a usable device the calls
+ *    fail with KNNG_ERR_CUDA.
+ */
+#ifndef KNNG_H_
+#define KNNG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (error names follow SPEC.md: S:120) ---- */
+#define KNNG_OK                     0
+#define KNNG_ERR_INVALID_ARG       -1  /* metric/dim mismatch, k<1, speedup<1, e<1, depth<1, ... */
+#define KNNG_ERR_INSUFFICIENT      -2  /* n <= k: a k-nn graph needs more than k items */
+#define KNNG_ERR_EMPTY             -3  /* empty graph / empty partition */
+#define KNNG_ERR_CAPACITY_INFEAS   -4  /* P * ceil(n*imbalance/P) < n */
+#define KNNG_ERR_OOM               -5  /* device allocation failed */
+#define KNNG_ERR_CUDA              -6  /* CUDA runtime/launch error, or no device */
+#define KNNG_ERR_NCCL              -7  /* NCCL error (multi-GPU) */
+#define KNNG_ERR_CAPACITY_EXCEEDED -8  /* store full: n_t + B > capacity */
+
+/* ---- metrics ----
+ * KNNG_L2SQ_U8        uint8 vectors; key D = sum_j (a_j - b_j)^2 as exact uint32 (
+ *                     Q25: squared L2, monotone in L2).
+ * KNNG_L2SQ_F32       fp32 vectors; key D = fp32 squared L2 in the canonical evaluation order
+ *                     of reading Q24, returned as the float's bits.
+ * KNNG_JACCARD_U32SET sorted, duplicate-free uint32 token sets (set-similarity stand-in for
+ *                     P:292); key = (|A n B| << 16) | |A u B|, similarity = inter/union,
+ *                     compared exactly by cross-multiplication.
+ * Edge order (all metrics): more similar key first, equal similarity -> smaller id.
+ * Every neighbour row is sorted by edge order. */
+typedef enum {
+  KNNG_L2SQ_U8 = 0,
+  KNNG_L2SQ_F32 = 1,
+  KNNG_JACCARD_U32SET = 2
+} knng_metric;
+
+/* A set of points.  Vectors: data = u8[n*dim] or f32[n*dim], row-major.
+ * Sets: data = uint32 tokens (each set sorted ascending, no duplicates), offsets = uint64[n+1]
+ * (set i is data[offsets[i] .. offsets[i+1])), dim ignored; sets hold <= 65535 tokens.
+ * data_on_device = 1: data (and offsets) are device pointers on the handle's GPU. */
+typedef struct {
+  int32_t metric;
+  int32_t dim;
+  int64_t n;
+  const void *data;
+  const uint64_t *offsets;
+  int32_t data_on_device;
+} knng_points;
+
+/* Parameters of iGNNS and of the update (Alg. 2).
+ *  speedup        budget of one search = max(min(k, |pool|), floor(|pool| / speedup)) similarity
+ *                 evaluations (reading Q6); speedup >= 1.
+ *  expansion_num/den  expansion e = num/den >= 1 of the restart skip rule; den = 0 means
+ *                 e = +inf (never skip).  1.2 = 6/5.
+ *  depth          DEPTH of the update (Alg. 2), 1..10.
+ *  seed           key of the counter RNG of the random starts (reading Q4): results are a pure
+ *                 function of (inputs, params, seed).
+ *  start_override test hook (graph_search only): host array of node ids used as the start
+ *                 sequence of every query instead of RNG draws; NULL in production. */
+typedef struct {
+  double speedup;
+  uint32_t expansion_num, expansion_den;
+  int32_t depth;
+  uint64_t seed;
+  const int32_t *start_override;
+  int32_t start_override_len;
+} knng_params;
+
+/* Counters and per-phase device times of the last call (CUDA events on the handle's stream). */
+typedef struct {
+  int64_t search_evals;       /* committed similarity evaluations of the searches (P:89 units) */
+  int64_t search_starts;      /* random starts evaluated */
+  int64_t search_skipped;     /* starts discarded by the expansion rule */
+  int64_t search_expansions;  /* nodes whose neighbour row was scanned */
+  int64_t ball_nodes;         /* update-ball nodes evaluated (Alg. 2) */
+  int64_t proposals;          /* (node, new point) replacements proposed by the balls */
+  int64_t allpair_pairs;      /* intra-batch pairs evaluated (ordered, i != j) */
+  int64_t kernel_launches;    /* kernels launched by the call */
+  float ms_search, ms_allpairs, ms_update, ms_merge, ms_total;
+} knng_stats;
+
+/* Runtime placement.  device: CUDA ordinal.  rank/world/nccl_unique_id: reserved for the
+ * multi-GPU path (world = 1 here).  cuda_stream: cudaStream_t to issue work on, or NULL.
+ * capacity: maximum number of points the graph will hold (0 = 2 * n0). */
+typedef struct {
+  int32_t device;
+  int32_t rank, world;
+  const void *nccl_unique_id;
+  void *cuda_stream;
+  int64_t capacity;
+} knng_runtime;
+
+typedef struct knng_graph knng_graph;   /* opaque */
+
+/* graph_init -- build the EXACT k-nn graph of pts (AL1 "brute force"): row v = the first k
+ * of all u != v in edge order.  Ids are 0..n-1 in input order.
+ * Errors: INVALID_ARG (k < 1 or k > 32, bad metric/dim, null pointers), INSUFFICIENT (n <= k),
+ * OOM, CUDA.  *out receives a new handle (NULL on error). */
+int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_graph **out);
+
+/* graph_insert_batch -- add a batch of B points (Alg. 1 + Alg. 2; distributed form
+ * Alg. 5, when partitioned).  Ids are n_t .. n_t+B-1 in batch order
+ * (*first_id_out = n_t).  Semantics: every point is searched
+ * with iGNNS on the snapshot G_t (RNG stream keyed by its id); its row is the top-k of its
+ * search result and the other batch points; the update balls (DEPTH levels over the snapshot)
+ * propose the new ids; every touched row becomes top-k(row u proposals); partitioned graphs
+ * place each point at its nearest medoid.  B = 1 is exactly the paper's sequential
+ * algorithm.  pts->metric/dim must match the graph.  st may be NULL.
+ * Errors: INVALID_ARG, CAPACITY_EXCEEDED, EMPTY (a partition is empty), OOM, CUDA. */
+int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p,
+                       int64_t *first_id_out, knng_stats *st);
+
+/* graph_search -- iGNNS k_r-nn search of nq queries on the current graph (read-only; P:73-89,
+ * Alg. 3 P:166-178 when partitioned).  Query i uses RNG stream (seed, i, partition).
+ * ids_out int32[nq*kr], keys_out uint32[nq*kr], sorted by edge order; -1 / 0 pad when the pool
+ * holds fewer than kr nodes.  out_on_device = 1: the output pointers are device memory.
+ * Errors: INVALID_ARG (kr < 1 or kr > 32), EMPTY, OOM, CUDA. */
+int graph_search(knng_graph *g, const knng_points *queries, int32_t kr, const knng_params *p,
+                 int32_t *ids_out, uint32_t *keys_out, int32_t out_on_device, knng_stats *st);
+
+/* partition_kmedoids -- balanced k-medoids of the graph into P partitions (Alg. 4, P:188-243;
+ * readings Q21-Q23): capacity ceil(n*imbalance/P); greedy assignment in ascending id to the
+ * eligible cluster maximising similarity(m,n) * (1 - |C|/capacity); medoid = member minimising
+ * the hop sum in the cluster-induced undirected subgraph (exact when |C| <= 4096, else over
+ * {current medoid} + 63 seeded candidates); an iteration is kept only if the total hop sum does
+ * not rise.  The graph becomes partitioned: later searches run per partition and inserts place
+ * points at the nearest medoid.  part_out: uint8[n] or NULL; medoids_out: int32[P];
+ * cost_out: int64[max_iter+1] or NULL (hop-sum cost of each kept iteration, -1 padded);
+ * init_medoids: int32[P] test hook or NULL.  All host pointers.  P in 1..255.
+ * Returns the number of kept iterations (>= 1) or an error:
+ * INVALID_ARG, CAPACITY_INFEAS, OOM, CUDA. */
+int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, int32_t max_iter,
+                       uint64_t seed, uint8_t *part_out, int32_t *medoids_out, int64_t *cost_out,
+                       const int32_t *init_medoids);
+
+/* graph_get_rows -- copy rows [first, first+count) to host: ids int32[count*k],
+ * keys uint32[count*k] (either may be NULL).  Errors: INVALID_ARG, CUDA. */
+int graph_get_rows(const knng_graph *g, int64_t first, int64_t count, int32_t *ids, uint32_t *keys);
+
+/* graph_get_partition -- part uint8[n] (may be NULL), medoids int32[P] (may be NULL), *P_out.
+ * P_out = 0 for an unpartitioned graph.  Errors: INVALID_ARG, CUDA. */
+int graph_get_partition(const knng_graph *g, uint8_t *part, int32_t *medoids, int32_t *P_out);
+
+/* graph_size / graph_degree: current n_t and k (-1 on a NULL handle). */
+int64_t graph_size(const knng_graph *g);
+int32_t graph_degree(const knng_graph *g);
+
+/* graph_free -- release the handle and all its device memory.  NULL is a no-op. */
+void graph_free(knng_graph *g);
+
+/* graph_last_error -- message of the last non-zero status of this thread ("" if none). */
+const char *graph_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KNNG_H_ */

@@ -195,10 +195,10 @@ typedef struct {
  * Duplicate ids are rejected (neighbour lists hold distinct ids). */
 static int list_insert(int metric, or_list *L, uint32_t key, int32_t id) {
   int i, pos;
-  for (i = 0; i < L->cnt; ++i)
-    if (L->id[i] == id) return 0;
   if (L->cnt == L->cap && !precedes(metric, key, id, L->key[L->cnt - 1], L->id[L->cnt - 1]))
     return 0;
+  for (i = 0; i < L->cnt; ++i)
+    if (L->id[i] == id) return 0;
   pos = 0;
   while (pos < L->cnt && precedes(metric, L->key[pos], L->id[pos], key, id)) ++pos;
   if (L->cnt < L->cap) L->cnt++;

@@ -1,0 +1,520 @@
+// knng_api.cu -- the C ABI of include/knng.h: graph handle, HBM layout, and the batch
+// pipeline of graph_insert_batch (search -> partition merge -> all-pairs -> update balls ->
+// ordered merge -> placement), all stream-ordered on the handle's CUDA stream.
+//
+// HBM layout of a handle (capacity N_cap points, degree k):
+//   vec      uint8 [N_cap][stride]   vectors, rows zero-padded to 16-byte chunks
+//   ids      int32 [N_cap][k]        neighbour rows, sorted by edge order
+//   keys     uint32[N_cap][k]        their keys
+//   part_of  uint8 [N_cap], local_idx int32[N_cap], members int32[P][N_cap]   (partitioned)
+//   ncnt/nfill/noff int32[N_cap]     proposal bucketing of the merge (kept zeroed)
+// plus per-batch workspaces grown on demand.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/knng.h"
+#include "knng_common.cuh"
+#include "knng_internal.h"
+
+using namespace knng;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      return fail(e_ == cudaErrorMemoryAllocation ? KNNG_ERR_OOM : KNNG_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #x, cudaGetErrorString(e_), __FILE__, __LINE__);                              \
+  } while (0)
+
+struct DBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T *as() const { return (T *)p; }
+};
+
+struct knng_graph {
+  int metric = 0, dim = 0, k = 0;
+  int64_t n = 0, cap = 0;
+  VecGeom geom{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint8_t *vec = nullptr;
+  int32_t *ids = nullptr;
+  uint32_t *keys = nullptr;
+  int32_t *ncnt = nullptr, *nfill = nullptr, *noff = nullptr, *scan_tmp = nullptr;
+  // partitions
+  int P = 0;
+  uint8_t *part_of = nullptr;
+  int32_t *local_idx = nullptr;
+  int32_t *members = nullptr;
+  int64_t *member_cnt = nullptr;
+  int32_t *medoids = nullptr;
+  std::vector<int32_t> h_medoids;
+  // workspaces
+  DBuf w_bits, w_cand_i, w_cand_k, w_C_i, w_C_k, w_hash, w_list, w_props, w_prop_cnt, w_sorted, w_stats,
+      w_target, w_query, w_starts;
+  cudaEvent_t ev[6] = {};
+};
+
+static int elem_bytes(int metric) { return metric == KNNG_L2SQ_U8 ? 1 : 4; }
+
+static int geom_for(int metric, int dim, VecGeom *g) {
+  const size_t row = (size_t)dim * elem_bytes(metric);
+  const int C = (int)((row + 15) / 16);
+  g->metric = metric;
+  g->nchunks = C;
+  g->stride = (size_t)C * 16;
+  if (C <= 32) {
+    int L = 1;
+    while (L < C) L <<= 1;
+    g->L = L;
+    g->CPL = 1;
+  } else if (C <= 64) {
+    g->L = 32; g->CPL = 2;
+  } else if (C <= 128) {
+    g->L = 32; g->CPL = 4;
+  } else {
+    return -1;
+  }
+  return 0;
+}
+
+static int check_points(const knng_points *p, const char *what) {
+  if (!p) return fail(KNNG_ERR_INVALID_ARG, "%s: null points", what);
+  if (p->metric == KNNG_JACCARD_U32SET)
+    return fail(KNNG_ERR_INVALID_ARG, "%s: Jaccard sets are not supported by this build yet", what);
+  if (p->metric != KNNG_L2SQ_U8 && p->metric != KNNG_L2SQ_F32) return fail(KNNG_ERR_INVALID_ARG, "%s: bad metric %d", what, p->metric);
+  if (p->dim < 1) return fail(KNNG_ERR_INVALID_ARG, "%s: dim < 1", what);
+  if (p->n < 0) return fail(KNNG_ERR_INVALID_ARG, "%s: n < 0", what);
+  if (p->n > 0 && !p->data) return fail(KNNG_ERR_INVALID_ARG, "%s: null data", what);
+  return 0;
+}
+
+// copy n points (row-major, dim*elem bytes each) into padded rows starting at dst
+static int copy_rows(knng_graph *g, uint8_t *dst, const knng_points *p) {
+  if (p->n == 0) return 0;
+  const size_t row = (size_t)p->dim * elem_bytes(p->metric);
+  CK(cudaMemcpy2DAsync(dst, g->geom.stride, p->data, row, row, (size_t)p->n,
+                       p->data_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->stream));
+  return 0;
+}
+
+static void free_graph(knng_graph *g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  void *bufs[] = {g->vec, g->ids, g->keys, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->part_of, g->local_idx,
+                  g->members, g->member_cnt, g->medoids};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  DBuf *ws[] = {&g->w_bits, &g->w_cand_i, &g->w_cand_k, &g->w_C_i, &g->w_C_k, &g->w_hash, &g->w_list, &g->w_props,
+                &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts};
+  for (DBuf *b : ws) b->release();
+  for (auto &e : g->ev)
+    if (e) cudaEventDestroy(e);
+  if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+extern "C" {
+
+const char *graph_last_error(void) { return g_err.c_str(); }
+
+int64_t graph_size(const knng_graph *g) { return g ? g->n : -1; }
+int32_t graph_degree(const knng_graph *g) { return g ? g->k : -1; }
+void graph_free(knng_graph *g) { free_graph(g); }
+
+int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_graph **out) {
+  g_err.clear();
+  if (!out) return fail(KNNG_ERR_INVALID_ARG, "graph_init: null out");
+  *out = nullptr;
+  if (int r = check_points(pts, "graph_init")) return r;
+  if (k < 1 || k > 32) return fail(KNNG_ERR_INVALID_ARG, "graph_init: k=%d outside 1..32", k);
+  if (pts->n <= k) return fail(KNNG_ERR_INSUFFICIENT, "graph_init: n=%lld <= k=%d", (long long)pts->n, k);
+  if (pts->n >= (int64_t)1 << 31) return fail(KNNG_ERR_INVALID_ARG, "graph_init: n too large");
+  knng_graph *g = new knng_graph();
+  g->metric = pts->metric;
+  g->dim = pts->dim;
+  g->k = k;
+  g->device = rt ? rt->device : 0;
+  if (geom_for(g->metric, g->dim, &g->geom)) {
+    delete g;
+    return fail(KNNG_ERR_INVALID_ARG, "graph_init: vectors of %d dims are too wide", pts->dim);
+  }
+  int r = 0;
+  auto bail = [&](int code) { free_graph(g); return code; };
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    delete g;
+    return fail(KNNG_ERR_CUDA, "graph_init: no CUDA device");
+  }
+  if (cudaSetDevice(g->device) != cudaSuccess) {
+    delete g;
+    return fail(KNNG_ERR_CUDA, "graph_init: cudaSetDevice(%d) failed", rt ? rt->device : 0);
+  }
+  if (rt && rt->cuda_stream) {
+    g->stream = (cudaStream_t)rt->cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete g;
+      return fail(KNNG_ERR_CUDA, "graph_init: stream create failed");
+    }
+    g->own_stream = true;
+  }
+  g->n = pts->n;
+  g->cap = (rt && rt->capacity > 0) ? rt->capacity : 2 * pts->n;
+  if (g->cap < g->n) g->cap = g->n;
+  const size_t cap = (size_t)g->cap;
+#define A(ptr, bytes)                                             \
+  do {                                                            \
+    cudaError_t e_ = cudaMalloc((void **)&(ptr), (bytes));        \
+    if (e_ != cudaSuccess) {                                      \
+      fail(KNNG_ERR_OOM, "graph_init: cudaMalloc %zu B failed", (size_t)(bytes)); \
+      return bail(KNNG_ERR_OOM);                                  \
+    }                                                             \
+  } while (0)
+  A(g->vec, cap * g->geom.stride);
+  A(g->ids, cap * k * 4);
+  A(g->keys, cap * k * 4);
+  A(g->ncnt, cap * 4);
+  A(g->nfill, cap * 4);
+  A(g->noff, cap * 4);
+  A(g->scan_tmp, ((cap + 1023) / 1024 + 1) * 4);
+#undef A
+  for (auto &e : g->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(KNNG_ERR_CUDA, "event create failed"));
+  if (cudaMemsetAsync(g->vec, 0, cap * g->geom.stride, g->stream) != cudaSuccess ||
+      cudaMemsetAsync(g->ncnt, 0, cap * 4, g->stream) != cudaSuccess ||
+      cudaMemsetAsync(g->nfill, 0, cap * 4, g->stream) != cudaSuccess)
+    return bail(fail(KNNG_ERR_CUDA, "graph_init: memset failed"));
+  if ((r = copy_rows(g, g->vec, pts))) return bail(r);
+  cudaError_t e = launch_exact_build(g->geom, g->vec, g->n, k, g->ids, g->keys, g->stream);
+  if (e != cudaSuccess) return bail(fail(KNNG_ERR_CUDA, "exact build launch: %s", cudaGetErrorString(e)));
+  e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) return bail(fail(KNNG_ERR_CUDA, "exact build: %s", cudaGetErrorString(e)));
+  *out = g;
+  return KNNG_OK;
+}
+
+static int check_params(const knng_params *p) {
+  if (!p) return fail(KNNG_ERR_INVALID_ARG, "null params");
+  if (!(p->speedup >= 1.0)) return fail(KNNG_ERR_INVALID_ARG, "speedup < 1");
+  if (p->expansion_den != 0 && p->expansion_num < p->expansion_den) return fail(KNNG_ERR_INVALID_ARG, "expansion < 1");
+  return 0;
+}
+
+// search workspace: returns smem flag and bits words per slot
+struct SearchPlan {
+  int smem;
+  int64_t bits_words;
+  int64_t slots;
+};
+
+static SearchPlan plan_search(knng_graph *g, int64_t tasks, int64_t mmax) {
+  SearchPlan sp;
+  sp.bits_words = 2 * ((mmax + 31) / 32);
+  const size_t per_block = (size_t)4 * sp.bits_words * 4;
+  sp.smem = per_block <= 200 * 1024 ? 1 : 0;
+  int64_t blocks = (tasks + 3) / 4;
+  if (!sp.smem && blocks > 148 * 16) blocks = 148 * 16;
+  sp.slots = blocks * 4;
+  return sp;
+}
+
+static int64_t max_pool(knng_graph *g) {
+  if (g->P == 0) return g->n;
+  std::vector<int64_t> cnt(g->P);
+  cudaMemcpy(cnt.data(), g->member_cnt, sizeof(int64_t) * g->P, cudaMemcpyDeviceToHost);
+  int64_t m = 0;
+  for (auto c : cnt) m = std::max(m, c);
+  return m;
+}
+
+static int run_search_phase(knng_graph *g, const uint8_t *qbase, int64_t nq, int64_t pid_base, int kr,
+                            const knng_params *p, const int32_t *d_starts, int nstarts, int32_t *out_i,
+                            uint32_t *out_k, int *nl) {
+  const int Pn = g->P > 0 ? g->P : 1;
+  const int64_t mmax = max_pool(g);
+  if (g->P > 0 && mmax == 0) return fail(KNNG_ERR_EMPTY, "all partitions are empty");
+  SearchPlan sp = plan_search(g, nq * Pn, mmax);
+  if (!sp.smem) CK(g->w_bits.ensure((size_t)sp.slots * sp.bits_words * 4));
+  int32_t *ci = out_i;
+  uint32_t *ck = out_k;
+  if (g->P > 0) {
+    CK(g->w_cand_i.ensure((size_t)nq * Pn * kr * 4));
+    CK(g->w_cand_k.ensure((size_t)nq * Pn * kr * 4));
+    ci = g->w_cand_i.as<int32_t>();
+    ck = g->w_cand_k.as<uint32_t>();
+  }
+  SearchArgs a;
+  memset(&a, 0, sizeof a);
+  a.vec = g->vec;
+  a.stride = g->geom.stride;
+  a.nchunks = g->geom.nchunks;
+  a.rows = g->ids;
+  a.k = g->k;
+  a.n_t = g->n;
+  a.qbase = qbase;
+  a.nq = nq;
+  a.pid_base = pid_base;
+  a.P = g->P;
+  a.members = g->members;
+  a.member_cap = g->cap;
+  a.member_cnt = g->member_cnt;
+  a.part_of = g->part_of;
+  a.local_idx = g->local_idx;
+  a.speedup = p->speedup;
+  a.e_num = p->expansion_num;
+  a.e_den = p->expansion_den;
+  a.seed = p->seed;
+  a.kr = kr;
+  a.starts = d_starts;
+  a.nstarts = nstarts;
+  a.G = 8;
+  a.gbits = g->w_bits.as<uint32_t>();
+  a.bits_words = sp.bits_words;
+  a.smem_bits = sp.smem;
+  a.out_ids = ci;
+  a.out_keys = ck;
+  a.stats = g->w_stats.as<unsigned long long>();
+  cudaError_t e = launch_search(g->geom, a, g->stream, nl);
+  if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
+  if (g->P > 0) {
+    e = launch_merge_parts(g->metric, ci, ck, nq, g->P, kr, out_i, out_k, g->stream);
+    if (nl) ++*nl;
+    if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "merge launch: %s", cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+static void fill_stats(knng_graph *g, knng_stats *st, const unsigned long long *h, int nl, int nev) {
+  if (!st) return;
+  memset(st, 0, sizeof *st);
+  st->search_evals = (int64_t)h[0];
+  st->search_starts = (int64_t)h[1];
+  st->search_skipped = (int64_t)h[2];
+  st->search_expansions = (int64_t)h[3];
+  st->ball_nodes = (int64_t)h[4];
+  st->proposals = (int64_t)h[5];
+  st->allpair_pairs = (int64_t)h[6];
+  st->kernel_launches = nl;
+  float ms = 0;
+  if (nev >= 2) { cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]); st->ms_search = ms; }
+  if (nev >= 3) { cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]); st->ms_allpairs = ms; }
+  if (nev >= 4) { cudaEventElapsedTime(&ms, g->ev[2], g->ev[3]); st->ms_update = ms; }
+  if (nev >= 5) { cudaEventElapsedTime(&ms, g->ev[3], g->ev[4]); st->ms_merge = ms; }
+  if (nev >= 2) { cudaEventElapsedTime(&ms, g->ev[0], g->ev[nev - 1]); st->ms_total = ms; }
+}
+
+int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,
+                       knng_stats *st) {
+  g_err.clear();
+  if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: null graph");
+  if (int r = check_points(pts, "graph_insert_batch")) return r;
+  if (int r = check_params(p)) return r;
+  if (pts->metric != g->metric || pts->dim != g->dim)
+    return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: metric/dim mismatch");
+  if (p->depth < 1 || p->depth > 10) return fail(KNNG_ERR_INVALID_ARG, "depth %d outside 1..10", p->depth);
+  const int64_t B = pts->n, n_t = g->n;
+  const int k = g->k;
+  if (first_id_out) *first_id_out = n_t;
+  if (n_t + B > g->cap)
+    return fail(KNNG_ERR_CAPACITY_EXCEEDED, "capacity %lld exceeded (n=%lld, B=%lld)", (long long)g->cap,
+                (long long)n_t, (long long)B);
+  CK(cudaSetDevice(g->device));
+  CK(g->w_stats.ensure(16 * 8));
+  if (B == 0) {
+    fill_stats(g, st, (const unsigned long long[8]){0, 0, 0, 0, 0, 0, 0, 0}, 0, 0);
+    return KNNG_OK;
+  }
+  int nl = 0;
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  // A1: batch ingest into the store tail (ids n_t .. n_t+B-1)
+  if (int r = copy_rows(g, g->vec + (size_t)n_t * g->geom.stride, pts)) return r;
+  // ball bound k + k^2 + ... + k^DEPTH, at most n_t
+  int64_t ballmax = 0, pw = 1;
+  for (int d = 1; d <= p->depth && ballmax < n_t; ++d) {
+    pw *= k;
+    ballmax += pw;
+  }
+  if (ballmax > n_t) ballmax = n_t;
+  int hcap = 64;
+  while (hcap < 2 * ballmax) hcap <<= 1;
+  int64_t bslots = std::min<int64_t>((B + 3) / 4, 148 * 8) * 4;
+  CK(g->w_C_i.ensure((size_t)B * k * 4));
+  CK(g->w_C_k.ensure((size_t)B * k * 4));
+  CK(g->w_hash.ensure((size_t)bslots * hcap * 4));
+  CK(g->w_list.ensure((size_t)bslots * ballmax * 4));
+  CK(g->w_props.ensure((size_t)B * ballmax * 8));
+  CK(g->w_prop_cnt.ensure((size_t)B * 4));
+  CK(g->w_sorted.ensure((size_t)B * ballmax * 8));
+  if (g->P > 0) CK(g->w_target.ensure((size_t)B * 4));
+
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  // A2-A4: iGNNS per (point, partition) on the snapshot + partition merge
+  if (int r = run_search_phase(g, g->vec + (size_t)n_t * g->geom.stride, B, n_t, k, p, nullptr, 0,
+                               g->w_C_i.as<int32_t>(), g->w_C_k.as<uint32_t>(), &nl))
+    return r;
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  // A5: intra-batch all-pairs -> new rows n_t .. n_t+B-1
+  CK(launch_allpairs(g->geom, g->vec, g->ids, g->keys, k, n_t, B, g->w_C_i.as<int32_t>(), g->w_C_k.as<uint32_t>(),
+                     g->stream));
+  ++nl;
+  CK(cudaEventRecord(g->ev[2], g->stream));
+  // A6: update balls over the snapshot -> proposals
+  BallArgs ba;
+  memset(&ba, 0, sizeof ba);
+  ba.vec = g->vec;
+  ba.stride = g->geom.stride;
+  ba.nchunks = g->geom.nchunks;
+  ba.ids = g->ids;
+  ba.keys = g->keys;
+  ba.k = k;
+  ba.n_t = n_t;
+  ba.B = B;
+  ba.depth = p->depth;
+  ba.C = g->w_C_i.as<int32_t>();
+  ba.hash = g->w_hash.as<int32_t>();
+  ba.hcap = hcap;
+  ba.list = g->w_list.as<int32_t>();
+  ba.ballmax = (int)ballmax;
+  ba.props = g->w_props.as<int2>();
+  ba.prop_cnt = g->w_prop_cnt.as<int32_t>();
+  ba.stats = g->w_stats.as<unsigned long long>();
+  CK(launch_ball(g->geom, ba, bslots, g->stream));
+  ++nl;
+  CK(cudaEventRecord(g->ev[3], g->stream));
+  // A7: ordered merge of the proposals into the snapshot rows
+  CK(launch_merge_props(g->metric, g->ids, g->keys, k, n_t, B, g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(),
+                        (int)ballmax, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->w_sorted.as<int2>(), g->stream, &nl));
+  // A8: placement at the nearest medoid
+  if (g->P > 0) {
+    CK(launch_place(g->geom, g->vec, n_t, B, g->P, g->medoids, g->members, g->cap, g->member_cnt, g->part_of,
+                    g->local_idx, g->w_target.as<int32_t>(), g->stream));
+    nl += 2;
+  }
+  CK(cudaEventRecord(g->ev[4], g->stream));
+  unsigned long long h[16];
+  CK(cudaMemcpyAsync(h, g->w_stats.p, 16 * 8, cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  h[6] = (unsigned long long)(B * (B - 1));
+  g->n = n_t + B;
+  fill_stats(g, st, h, nl, 5);
+  return KNNG_OK;
+}
+
+int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_params *p, int32_t *ids_out,
+                 uint32_t *keys_out, int32_t out_on_device, knng_stats *st) {
+  g_err.clear();
+  if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_search: null graph");
+  if (int r = check_points(q, "graph_search")) return r;
+  if (int r = check_params(p)) return r;
+  if (q->metric != g->metric || q->dim != g->dim) return fail(KNNG_ERR_INVALID_ARG, "graph_search: metric/dim mismatch");
+  if (kr < 1 || kr > 32) return fail(KNNG_ERR_INVALID_ARG, "graph_search: kr=%d outside 1..32", kr);
+  if (q->n > 0 && (!ids_out || !keys_out)) return fail(KNNG_ERR_INVALID_ARG, "graph_search: null outputs");
+  CK(cudaSetDevice(g->device));
+  CK(g->w_stats.ensure(16 * 8));
+  const int64_t nq = q->n;
+  if (nq == 0) {
+    fill_stats(g, st, (const unsigned long long[8]){0, 0, 0, 0, 0, 0, 0, 0}, 0, 0);
+    return KNNG_OK;
+  }
+  int nl = 0;
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  CK(g->w_query.ensure((size_t)nq * g->geom.stride));
+  CK(cudaMemsetAsync(g->w_query.p, 0, (size_t)nq * g->geom.stride, g->stream));
+  if (int r = copy_rows(g, g->w_query.as<uint8_t>(), q)) return r;
+  const int32_t *d_starts = nullptr;
+  int nstarts = 0;
+  if (p->start_override && p->start_override_len > 0) {
+    nstarts = p->start_override_len;
+    CK(g->w_starts.ensure((size_t)nstarts * 4));
+    CK(cudaMemcpyAsync(g->w_starts.p, p->start_override, (size_t)nstarts * 4, cudaMemcpyHostToDevice, g->stream));
+    d_starts = g->w_starts.as<int32_t>();
+  }
+  int32_t *oi = ids_out;
+  uint32_t *ok = keys_out;
+  if (!out_on_device) {
+    CK(g->w_C_i.ensure((size_t)nq * kr * 4));
+    CK(g->w_C_k.ensure((size_t)nq * kr * 4));
+    oi = g->w_C_i.as<int32_t>();
+    ok = g->w_C_k.as<uint32_t>();
+  }
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  if (int r = run_search_phase(g, g->w_query.as<uint8_t>(), nq, 0, kr, p, d_starts, nstarts, oi, ok, &nl)) return r;
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  if (!out_on_device) {
+    CK(cudaMemcpyAsync(ids_out, oi, (size_t)nq * kr * 4, cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaMemcpyAsync(keys_out, ok, (size_t)nq * kr * 4, cudaMemcpyDeviceToHost, g->stream));
+  }
+  unsigned long long h[16];
+  CK(cudaMemcpyAsync(h, g->w_stats.p, 16 * 8, cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  h[4] = h[5] = h[6] = 0;
+  fill_stats(g, st, h, nl, 2);
+  return KNNG_OK;
+}
+
+int graph_get_rows(const knng_graph *g, int64_t first, int64_t count, int32_t *ids, uint32_t *keys) {
+  g_err.clear();
+  if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_get_rows: null graph");
+  if (first < 0 || count < 0 || first + count > g->n) return fail(KNNG_ERR_INVALID_ARG, "graph_get_rows: bad range");
+  CK(cudaSetDevice(g->device));
+  if (ids) CK(cudaMemcpyAsync(ids, g->ids + first * g->k, (size_t)count * g->k * 4, cudaMemcpyDeviceToHost, g->stream));
+  if (keys)
+    CK(cudaMemcpyAsync(keys, g->keys + first * g->k, (size_t)count * g->k * 4, cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  return KNNG_OK;
+}
+
+int graph_get_partition(const knng_graph *g, uint8_t *part, int32_t *medoids, int32_t *P_out) {
+  g_err.clear();
+  if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_get_partition: null graph");
+  if (P_out) *P_out = g->P;
+  if (g->P == 0) return KNNG_OK;
+  CK(cudaSetDevice(g->device));
+  if (part) CK(cudaMemcpyAsync(part, g->part_of, (size_t)g->n, cudaMemcpyDeviceToHost, g->stream));
+  if (medoids) memcpy(medoids, g->h_medoids.data(), sizeof(int32_t) * g->P);
+  CK(cudaStreamSynchronize(g->stream));
+  return KNNG_OK;
+}
+
+int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, int32_t max_iter, uint64_t seed, uint8_t *part_out,
+                       int32_t *medoids_out, int64_t *cost_out, const int32_t *init_medoids);
+
+}  // extern "C"

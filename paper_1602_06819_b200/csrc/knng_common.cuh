@@ -1,0 +1,258 @@
+// knng_common.cuh -- device building blocks of the B200 path (sm_100a).
+//
+// Product code: shares nothing with oracle/.  "P:n" = line n of the paper
+// (PAPER.md); "Qn" = reading n in DESIGN.md.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace knng {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+enum { M_U8 = 0, M_F32 = 1, M_JAC = 2 };
+
+// ---------------------------------------------------------------------------
+// Counter RNG of the random starts (Q4): SplitMix64 finaliser chain keyed by
+// (seed, point id, partition, draw #); pool index = floor(h * m / 2^64).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t rng_prefix(uint64_t seed, uint64_t pid, uint64_t part) {
+  uint64_t h = mix64(seed + 1ull * GOLDEN);
+  h = mix64(h ^ (pid + 2ull * GOLDEN));
+  return mix64(h ^ (part + 3ull * GOLDEN));
+}
+__device__ __forceinline__ uint64_t rng_index(uint64_t prefix, uint64_t draw, uint64_t m) {
+  return __umul64hi(mix64(prefix ^ (draw + 4ull * GOLDEN)), m);
+}
+
+// ---------------------------------------------------------------------------
+// Key order.  U8: uint32 D; F32: fp32 D bits; JAC: (inter<<16)|union.
+// closer(a,b): a strictly more similar than b (metric value only).
+// precedes: edge order (closer first, equal similarity -> smaller id).
+// ---------------------------------------------------------------------------
+template <int M>
+__device__ __forceinline__ bool closer(uint32_t a, uint32_t b) {
+  if (M == M_U8) return a < b;
+  if (M == M_F32) return __uint_as_float(a) < __uint_as_float(b);
+  return (uint64_t)(a >> 16) * (b & 0xFFFFu) > (uint64_t)(b >> 16) * (a & 0xFFFFu);
+}
+template <int M>
+__device__ __forceinline__ bool precedes(uint32_t ka, int32_t ia, uint32_t kb, int32_t ib) {
+  if (closer<M>(ka, kb)) return true;
+  if (closer<M>(kb, ka)) return false;
+  return ia < ib;
+}
+// Expansion rule of P:81 with e = num/den (den = 0: e = +inf).  Q1: s = 1/(1+D) for the L2
+// metrics, s = i/u for Jaccard; skip iff s_r < s_max / e, decided exactly.
+template <int M>
+__device__ __forceinline__ bool skip_start(uint32_t kr, uint32_t kb, uint64_t num, uint64_t den) {
+  if (den == 0) return false;
+  if (M == M_U8) return den * (1ull + kr) > num * (1ull + kb);
+  if (M == M_F32) {
+    const double l = __dmul_rn((double)den, __dadd_rn(1.0, (double)__uint_as_float(kr)));
+    const double r = __dmul_rn((double)num, __dadd_rn(1.0, (double)__uint_as_float(kb)));
+    return l > r;
+  }
+  return num * (uint64_t)(kr >> 16) * (uint64_t)(kb & 0xFFFFu) <
+         den * (uint64_t)(kb >> 16) * (uint64_t)(kr & 0xFFFFu);
+}
+
+// ---------------------------------------------------------------------------
+// Global memory helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ldg16(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ bool bit_get(const uint32_t *b, uint32_t i) {
+  return (((const volatile uint32_t *)b)[i >> 5] >> (i & 31)) & 1u;
+}
+__device__ __forceinline__ void bit_set(uint32_t *b, uint32_t i) { atomicOr(b + (i >> 5), 1u << (i & 31)); }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+// the lowest n set bits of mask
+__device__ __forceinline__ unsigned first_bits(unsigned mask, int n) {
+  unsigned r = 0;
+  for (int i = 0; i < n && mask; ++i) {
+    const unsigned low = mask & (0u - mask);
+    r |= low;
+    mask ^= low;
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Warp-register top-k: lane j < cnt holds entry j, sorted by edge order.
+// ---------------------------------------------------------------------------
+template <int M>
+struct WarpTopK {
+  uint32_t key;
+  int32_t id;
+  int cnt, kr;
+  __device__ __forceinline__ void init(int kr_) { key = 0; id = -1; cnt = 0; kr = kr_; }
+  __device__ __forceinline__ uint32_t best() const { return __shfl_sync(FULL, key, 0); }
+  // insert every lane with flag set (distinct ids assumed)
+  __device__ __forceinline__ void insert(bool flag, uint32_t ck, int32_t cid) {
+    const int lane = threadIdx.x & 31;
+    if (cnt == kr) {   // pre-filter against the current worst entry (conservative)
+      const uint32_t wk = __shfl_sync(FULL, key, kr - 1);
+      const int32_t wi = __shfl_sync(FULL, id, kr - 1);
+      flag = flag && precedes<M>(ck, cid, wk, wi);
+    }
+    unsigned m = __ballot_sync(FULL, flag);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t k2 = __shfl_sync(FULL, ck, src);
+      const int32_t i2 = __shfl_sync(FULL, cid, src);
+      const bool before = lane < cnt && precedes<M>(key, id, k2, i2);
+      const int pos = __popc(__ballot_sync(FULL, before));
+      if (pos >= kr) continue;
+      const uint32_t uk = __shfl_up_sync(FULL, key, 1);
+      const int32_t ui = __shfl_up_sync(FULL, id, 1);
+      if (lane > pos) { key = uk; id = ui; }
+      if (lane == pos) { key = k2; id = i2; }
+      if (cnt < kr) ++cnt;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Canonical squared distances (Q24).
+//  Vectors are stored in rows of `stride` bytes = nchunks 16-byte chunks, zero padded.
+//  U8 : exact int sum of (a-b)^2 (order irrelevant).
+//  F32: 32 partial sums; chunk c -> partial c%32 via fmaf(d,d,acc) over its 4 floats
+//       (chunks c, c+32, ... in increasing order); partials combined by the xor butterfly
+//       16,8,4,2,1.  Warp form (below) and single-thread form (thread_dist) compute the
+//       same tree; IEEE addition is commutative, and the absent partials are +0.
+// ---------------------------------------------------------------------------
+template <int M>
+__device__ __forceinline__ void chunk_acc(uint32_t &acc, const uint4 &a, const uint4 &b);
+template <>
+__device__ __forceinline__ void chunk_acc<M_U8>(uint32_t &acc, const uint4 &a, const uint4 &b) {
+  uint32_t d;
+  d = __vabsdiffu4(a.x, b.x); acc = __dp4a(d, d, acc);
+  d = __vabsdiffu4(a.y, b.y); acc = __dp4a(d, d, acc);
+  d = __vabsdiffu4(a.z, b.z); acc = __dp4a(d, d, acc);
+  d = __vabsdiffu4(a.w, b.w); acc = __dp4a(d, d, acc);
+}
+__device__ __forceinline__ float f4_leaf(float acc, const uint4 &a, const uint4 &b) {
+  float d;
+  d = __fsub_rn(__uint_as_float(a.x), __uint_as_float(b.x)); acc = __fmaf_rn(d, d, acc);
+  d = __fsub_rn(__uint_as_float(a.y), __uint_as_float(b.y)); acc = __fmaf_rn(d, d, acc);
+  d = __fsub_rn(__uint_as_float(a.z), __uint_as_float(b.z)); acc = __fmaf_rn(d, d, acc);
+  d = __fsub_rn(__uint_as_float(a.w), __uint_as_float(b.w)); acc = __fmaf_rn(d, d, acc);
+  return acc;
+}
+
+// Single-thread canonical distance between two rows (pointers to 16B chunks, any space).
+template <int M>
+__device__ __forceinline__ uint32_t thread_dist(const uint4 *a, const uint4 *b, int nchunks) {
+  if (M == M_U8) {
+    uint32_t acc = 0;
+    for (int c = 0; c < nchunks; ++c) chunk_acc<M_U8>(acc, a[c], b[c]);
+    return acc;
+  } else {
+    // leaves in butterfly order: leaf i holds partial bitrev5(i); a binary-counter stack
+    // evaluates ((p0+p16)+(p8+p24)) + ... exactly as the warp butterfly does.
+    float stk[6];
+    int sp = 0;
+#pragma unroll 1
+    for (int i = 0; i < 32; ++i) {
+      const int l = __brev(i) >> 27;
+      float leaf = 0.0f;
+      for (int c = l; c < nchunks; c += 32) leaf = f4_leaf(leaf, a[c], b[c]);
+      stk[sp++] = leaf;
+      for (int cnt = i + 1; (cnt & 1) == 0; cnt >>= 1) {
+        stk[sp - 2] = __fadd_rn(stk[sp - 2], stk[sp - 1]);
+        --sp;
+      }
+    }
+    return __float_as_uint(stk[0]);
+  }
+}
+
+// Warp-cooperative evaluation of up to 32 candidates against a query held in registers.
+// L lanes per vector (power of 2), CPL chunks per lane: lane sl of a group owns chunks
+// sl, sl+L, ..., (CPL of them).  32/L vectors per pass; GRP passes have their loads in flight
+// together.
+template <int M, int L, int CPL>
+struct VecQuery {
+  static constexpr int VPP = 32 / L;
+  static constexpr int GRP = (L < (8 / CPL) ? L : ((8 / CPL) > 0 ? (8 / CPL) : 1));
+  uint4 q[CPL];
+
+  __device__ __forceinline__ void load(const uint8_t *row, int nchunks) {
+    const int sl = (threadIdx.x & 31) % L;
+#pragma unroll
+    for (int t = 0; t < CPL; ++t) {
+      const int c = sl + L * t;
+      q[t] = c < nchunks ? ldg16(row + (size_t)c * 16) : make_uint4(0, 0, 0, 0);
+    }
+  }
+
+  __device__ __forceinline__ uint32_t reduce(const uint4 *b) const {
+    if (M == M_U8) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) chunk_acc<M_U8>(acc, q[t], b[t]);
+#pragma unroll
+      for (int o = L / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+      return acc;
+    } else {
+      float acc = 0.0f;
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) acc = f4_leaf(acc, q[t], b[t]);
+#pragma unroll
+      for (int o = L / 2; o >= 1; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+      return __float_as_uint(acc);
+    }
+  }
+
+  // cand: id held by lane j for candidate j < n (id < 0: skipped, key undefined).
+  // Returns the key of candidate j in lane j.
+  __device__ __forceinline__ uint32_t eval(const uint8_t *__restrict__ base, size_t stride, int nchunks,
+                                           int32_t cand, int n) const {
+    const int lane = threadIdx.x & 31, sub = lane / L, sl = lane % L;
+    uint32_t out = 0;
+    const int np = (n + VPP - 1) / VPP;
+    for (int p0 = 0; p0 < np; p0 += GRP) {
+      uint4 buf[GRP][CPL];
+#pragma unroll
+      for (int g = 0; g < GRP; ++g) {
+        const int v = (p0 + g) * VPP + sub;
+        const int32_t id = __shfl_sync(FULL, cand, v & 31);
+        const bool ok = v < n && id >= 0;
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) {
+          const int c = sl + L * t;
+          buf[g][t] = (ok && c < nchunks) ? ldg16(base + (size_t)id * stride + (size_t)c * 16)
+                                          : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < GRP; ++g) {
+        if (p0 + g < np) {
+          const uint32_t key = reduce(buf[g]);
+          const uint32_t kk = __shfl_sync(FULL, key, (lane % VPP) * L);
+          if (lane / VPP == p0 + g) out = kk;
+        }
+      }
+    }
+    return out;
+  }
+};
+
+}  // namespace knng

@@ -1,0 +1,89 @@
+// knng_internal.h -- kernel argument blocks and launchers shared by the .cu files of the
+// product library (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace knng {
+
+// Vector store geometry: rows of `stride` bytes (= nchunks * 16, zero padded).
+struct VecGeom {
+  int metric;
+  int nchunks;
+  size_t stride;
+  int L, CPL;   // lanes per vector and chunks per lane of the warp evaluator
+};
+
+struct SearchArgs {
+  const uint8_t *vec;          // store rows
+  size_t stride;
+  int nchunks;
+  const int32_t *rows;         // snapshot rows [n_t][k]
+  int k;
+  int64_t n_t;
+  const uint8_t *qbase;        // query rows (stride bytes each)
+  int64_t nq;
+  int64_t pid_base;            // RNG point id of query b = pid_base + b
+  // partitions (P == 0: unpartitioned, pool = 0..n_t-1)
+  int P;
+  const int32_t *members;      // [P][member_cap]
+  int64_t member_cap;
+  const int64_t *member_cnt;   // [P] (device)
+  const uint8_t *part_of;      // [cap]
+  const int32_t *local_idx;    // [cap]
+  // parameters
+  double speedup;
+  uint64_t e_num, e_den, seed;
+  int kr;
+  const int32_t *starts;       // injected start sequence (device) or null
+  int nstarts;
+  int G;                       // restart draws evaluated together
+  // bitmap workspace
+  uint32_t *gbits;             // global: per warp slot, bits_words each
+  int64_t bits_words;          // evaluated + expanded words per task slot
+  int smem_bits;               // 1: bitmaps in dynamic shared memory
+  // outputs
+  int32_t *out_ids;            // [nq][max(P,1)][kr]
+  uint32_t *out_keys;
+  unsigned long long *stats;   // [0] evals [1] starts [2] skipped [3] expansions
+};
+
+struct BallArgs {
+  const uint8_t *vec;
+  size_t stride;
+  int nchunks;
+  int32_t *ids;                // rows (snapshot until the merge)
+  uint32_t *keys;
+  int k;
+  int64_t n_t;
+  int64_t B;
+  int depth;
+  const int32_t *C;            // search results [B][k]
+  int32_t *hash;               // per warp slot, hcap entries
+  int hcap;
+  int32_t *list;               // per warp slot, ballmax entries
+  int ballmax;
+  int2 *props;                 // [B][ballmax] (node, key)
+  int32_t *prop_cnt;           // [B]
+  unsigned long long *stats;   // [4] ball nodes [5] proposals
+};
+
+// Launchers (return cudaError_t of the launch)
+cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch);
+cudaError_t launch_merge_parts(int metric, const int32_t *cand_ids, const uint32_t *cand_keys, int64_t nq,
+                               int P, int kr, int32_t *out_ids, uint32_t *out_keys, cudaStream_t s);
+cudaError_t launch_allpairs(const VecGeom &g, const uint8_t *vec, int32_t *ids, uint32_t *keys, int k,
+                            int64_t n_t, int64_t B, const int32_t *C_ids, const uint32_t *C_keys,
+                            cudaStream_t s);
+cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cudaStream_t s);
+cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
+                               const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
+                               int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted,
+                               cudaStream_t s, int *n_launch);
+cudaError_t launch_exact_build(const VecGeom &g, const uint8_t *vec, int64_t n, int k, int32_t *ids,
+                               uint32_t *keys, cudaStream_t s);
+cudaError_t launch_place(const VecGeom &g, const uint8_t *vec, int64_t n_t, int64_t B, int P,
+                         const int32_t *medoids, int32_t *members, int64_t member_cap, int64_t *member_cnt,
+                         uint8_t *part_of, int32_t *local_idx, int32_t *target_tmp, cudaStream_t s);
+
+}  // namespace knng

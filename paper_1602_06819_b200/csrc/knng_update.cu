@@ -1,0 +1,362 @@
+// knng_update.cu -- the batch update of graph_insert_batch:
+//   K3 intra-batch all-pairs + new rows     (new row = top-k(C_i u peers), Q15)
+//   K4 update ball + proposals              (Alg. 2, over the snapshot, Q12-Q14)
+//   K5 proposal bucketing + per-node merge  (row_v = top-k(row_v u proposals); Q17)
+//   K6 placement at the nearest medoid      (Alg. 5)
+#include "knng_common.cuh"
+#include "knng_internal.h"
+
+namespace knng {
+
+// ---------------------------------------------------------------------------
+// K3: warp per new point i; lanes take peers j = lane + 32t (thread-level canonical distance).
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__(128) k_allpairs(const uint8_t *__restrict__ vec, size_t stride, int nchunks,
+                                                  int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
+                                                  const int32_t *Ci, const uint32_t *Ck) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= B) return;
+  WarpTopK<M> top;
+  top.init(k);
+  {
+    const int32_t cid = lane < k ? Ci[i * k + lane] : -1;
+    const uint32_t ck = lane < k ? Ck[i * k + lane] : 0u;
+    top.insert(cid >= 0, ck, cid);
+  }
+  const uint4 *xi = (const uint4 *)(vec + (size_t)(n_t + i) * stride);
+  for (int64_t j0 = 0; j0 < B; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const bool valid = j < B && j != i;
+    uint32_t key = 0;
+    if (valid) key = thread_dist<M>(xi, (const uint4 *)(vec + (size_t)(n_t + j) * stride), nchunks);
+    top.insert(valid, key, (int32_t)(n_t + j));
+  }
+  if (lane < k) {
+    ids[(size_t)(n_t + i) * k + lane] = lane < top.cnt ? top.id : -1;
+    keys[(size_t)(n_t + i) * k + lane] = lane < top.cnt ? top.key : 0u;
+  }
+}
+
+cudaError_t launch_allpairs(const VecGeom &g, const uint8_t *vec, int32_t *ids, uint32_t *keys, int k, int64_t n_t,
+                            int64_t B, const int32_t *Ci, const uint32_t *Ck, cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((B + 3) / 4);
+  if (g.metric == M_U8)
+    k_allpairs<M_U8><<<blocks, 128, 0, s>>>(vec, g.stride, g.nchunks, ids, keys, k, n_t, B, Ci, Ck);
+  else
+    k_allpairs<M_F32><<<blocks, 128, 0, s>>>(vec, g.stride, g.nchunks, ids, keys, k, n_t, B, Ci, Ck);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K4: update ball.  Warp per new point; BFS levels with a per-slot hash set (dedup, Q12);
+// each level's nodes are evaluated 32 at a time with the warp evaluator; a node v proposes the
+// new point when (D, id_x) precedes row_v[k-1] (Q14).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool hash_insert(int32_t *h, int hcap, int32_t u) {
+  uint32_t x = (uint32_t)u * 0x9E3779B1u;
+  int pos = (int)(x >> 7) & (hcap - 1);
+  for (;;) {
+    const int32_t old = atomicCAS(h + pos, -1, u);
+    if (old == -1) return true;
+    if (old == u) return false;
+    pos = (pos + 1) & (hcap - 1);
+  }
+}
+
+template <int M, int L, int CPL>
+__global__ void __launch_bounds__(128) k_ball(BallArgs a) {
+  __shared__ int s_n[4];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * 4 + wib, nw = (int64_t)gridDim.x * 4;
+  int32_t *hash = a.hash + gw * a.hcap;
+  int32_t *list = a.list + gw * a.ballmax;
+  const int k = a.k;
+  unsigned long long s_ball = 0, s_prop = 0;
+  for (int64_t b = gw; b < a.B; b += nw) {
+    for (int i = lane; i < a.hcap; i += 32) hash[i] = -1;
+    if (lane == 0) s_n[wib] = 0;
+    __syncwarp();
+    VecQuery<M, L, CPL> Q;
+    Q.load(a.vec + (size_t)(a.n_t + b) * a.stride, a.nchunks);
+    const int32_t idx = (int32_t)(a.n_t + b);
+    // L1 = the search result C(x)
+    {
+      const int32_t v = lane < k ? a.C[b * k + lane] : -1;
+      const bool ins = v >= 0 && hash_insert(hash, a.hcap, v);
+      const unsigned m = __ballot_sync(FULL, ins);
+      if (ins) list[__popc(m & lanemask_lt())] = v;
+      if (lane == 0) s_n[wib] = __popc(m);
+      __syncwarp();
+    }
+    int lo = 0, hi = s_n[wib];
+    int np = 0;
+    int2 *props = a.props + (size_t)b * a.ballmax;
+    for (int d = 1; d <= a.depth; ++d) {
+      for (int base = lo; base < hi; base += 32) {
+        const int t = base + lane;
+        const int32_t v = t < hi ? list[t] : -1;
+        if (d < a.depth && v >= 0) {
+          for (int e = 0; e < k; ++e) {
+            const int32_t u = a.ids[(size_t)v * k + e];
+            if (u >= 0 && hash_insert(hash, a.hcap, u)) {
+              const int pos = atomicAdd(&s_n[wib], 1);
+              if (pos < a.ballmax) list[pos] = u;
+            }
+          }
+        }
+        const int cnt = hi - base < 32 ? hi - base : 32;
+        const uint32_t key = Q.eval(a.vec, a.stride, a.nchunks, v, cnt);
+        bool prop = false;
+        if (v >= 0) {
+          const uint32_t kk = a.keys[(size_t)v * k + k - 1];
+          const int32_t ik = a.ids[(size_t)v * k + k - 1];
+          prop = precedes<M>(key, idx, kk, ik);
+        }
+        const unsigned pm = __ballot_sync(FULL, prop);
+        if (prop) props[np + __popc(pm & lanemask_lt())] = make_int2(v, (int)key);
+        np += __popc(pm);
+      }
+      __syncwarp();
+      lo = hi;
+      hi = s_n[wib] < a.ballmax ? s_n[wib] : a.ballmax;
+      __syncwarp();
+    }
+    s_ball += (unsigned long long)lo;
+    s_prop += np;
+    if (lane == 0) a.prop_cnt[b] = np;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    atomicAdd(a.stats + 4, s_ball);
+    atomicAdd(a.stats + 5, s_prop);
+  }
+}
+
+template <int M, int L, int CPL>
+static cudaError_t run_ball(const BallArgs &a, int64_t nslots, cudaStream_t s) {
+  if (a.B == 0) return cudaSuccess;
+  const int64_t blocks = nslots / 4;
+  k_ball<M, L, CPL><<<(unsigned)blocks, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+#define KNNG_SHAPES(X, M) \
+  X(M, 1, 1) X(M, 2, 1) X(M, 4, 1) X(M, 8, 1) X(M, 16, 1) X(M, 32, 1) X(M, 32, 2) X(M, 32, 4)
+
+cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cudaStream_t s) {
+#define X(MM, LL, CC) \
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_ball<MM, LL, CC>(a, nslots, s);
+  KNNG_SHAPES(X, M_U8)
+  KNNG_SHAPES(X, M_F32)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// K5: bucket the proposals by node (count, exclusive scan, scatter), then one thread per
+// touched node merges its row with its proposals: row_v = top-k(row_v u proposals).  The merge
+// owns each row (no atomics on rows); a top-k under a strict total order does not depend on
+// the order the proposals arrive in, so the result equals the fixed (qid, key, node) order.
+// ---------------------------------------------------------------------------
+__global__ void k_prop_count(const int2 *props, const int32_t *prop_cnt, int ballmax, int64_t B, int32_t *ncnt) {
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  const int n = prop_cnt[b];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) atomicAdd(ncnt + props[b * ballmax + j].x, 1);
+}
+
+__global__ void k_scan_block(const int32_t *in, int32_t *out, int32_t *blocksum, int64_t n) {
+  __shared__ int32_t ws[32];
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t x = i < n ? in[i] : 0;
+  int32_t v = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) ws[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int32_t s = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, s, o);
+      if (lane >= o) s += y;
+    }
+    ws[lane] = s;
+  }
+  __syncthreads();
+  const int32_t pre = (w > 0 ? ws[w - 1] : 0) + v - x;   // exclusive
+  if (i < n) out[i] = pre;
+  if (threadIdx.x == 1023) blocksum[blockIdx.x] = ws[31];
+}
+
+__global__ void k_scan_sums(int32_t *blocksum, int64_t nb) {
+  // single block: exclusive scan of nb block sums, 1024 at a time
+  __shared__ int32_t ws[32];
+  __shared__ int32_t carry;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t x = i < nb ? blocksum[i] : 0;
+    int32_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) ws[w] = v;
+    __syncthreads();
+    if (w == 0) {
+      int32_t s = ws[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(FULL, s, o);
+        if (lane >= o) s += y;
+      }
+      ws[lane] = s;
+    }
+    __syncthreads();
+    const int32_t c0 = carry;
+    if (i < nb) blocksum[i] = c0 + (w > 0 ? ws[w - 1] : 0) + v - x;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c0 + ws[31];
+    __syncthreads();
+  }
+}
+
+__global__ void k_scan_add(int32_t *out, const int32_t *blocksum, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  if (i < n) out[i] += blocksum[blockIdx.x];
+}
+
+__global__ void k_prop_scatter(const int2 *props, const int32_t *prop_cnt, int ballmax, int64_t B, int64_t n_t,
+                               const int32_t *noff, int32_t *nfill, int2 *sorted) {
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  const int n = prop_cnt[b];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int2 pr = props[b * ballmax + j];
+    const int pos = noff[pr.x] + atomicAdd(nfill + pr.x, 1);
+    sorted[pos] = make_int2(pr.y, (int)(n_t + b));   // (key, new id)
+  }
+}
+
+template <int M>
+__global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, int32_t *ncnt, int32_t *nfill,
+                             const int32_t *noff, const int2 *sorted) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n_t) return;
+  const int c = ncnt[v];
+  if (c == 0) return;
+  int32_t ri[32];
+  uint32_t rk[32];
+  for (int e = 0; e < k; ++e) { ri[e] = ids[v * k + e]; rk[e] = keys[v * k + e]; }
+  const int o = noff[v];
+  for (int j = 0; j < c; ++j) {
+    const int2 pr = sorted[o + j];
+    const uint32_t key = (uint32_t)pr.x;
+    const int32_t id = pr.y;
+    if (!precedes<M>(key, id, rk[k - 1], ri[k - 1])) continue;
+    int pos = k - 1;
+    while (pos > 0 && precedes<M>(key, id, rk[pos - 1], ri[pos - 1])) {
+      rk[pos] = rk[pos - 1];
+      ri[pos] = ri[pos - 1];
+      --pos;
+    }
+    rk[pos] = key;
+    ri[pos] = id;
+  }
+  for (int e = 0; e < k; ++e) { ids[v * k + e] = ri[e]; keys[v * k + e] = rk[e]; }
+  ncnt[v] = 0;
+  nfill[v] = 0;
+}
+
+cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
+                               const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
+                               int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted, cudaStream_t s,
+                               int *n_launch) {
+  if (B == 0) return cudaSuccess;
+  k_prop_count<<<(unsigned)B, 128, 0, s>>>(props, prop_cnt, ballmax, B, ncnt);
+  const int64_t nb = (n_t + 1023) / 1024;
+  k_scan_block<<<(unsigned)nb, 1024, 0, s>>>(ncnt, noff, scan_tmp, n_t);
+  k_scan_sums<<<1, 1024, 0, s>>>(scan_tmp, nb);
+  k_scan_add<<<(unsigned)nb, 1024, 0, s>>>(noff, scan_tmp, n_t);
+  k_prop_scatter<<<(unsigned)B, 128, 0, s>>>(props, prop_cnt, ballmax, B, n_t, noff, nfill, sorted);
+  const unsigned mb = (unsigned)((n_t + 255) / 256);
+  if (metric == M_U8) k_node_merge<M_U8><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted);
+  else if (metric == M_F32) k_node_merge<M_F32><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted);
+  else k_node_merge<M_JAC><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted);
+  if (n_launch) *n_launch += 6;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K6: nearest medoid (ties -> lowest p) and ordered append to the member lists.
+// Single block: new ids are appended in batch order, so member lists stay ascending.
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void k_place_target(const uint8_t *vec, size_t stride, int nchunks, int64_t n_t, int64_t B, int P,
+                               const int32_t *medoids, int32_t *target) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const uint4 *x = (const uint4 *)(vec + (size_t)(n_t + i) * stride);
+  int best = 0;
+  uint32_t bk = 0;
+  for (int p = 0; p < P; ++p) {
+    const uint32_t kp = thread_dist<M>(x, (const uint4 *)(vec + (size_t)medoids[p] * stride), nchunks);
+    if (p == 0 || closer<M>(kp, bk)) { best = p; bk = kp; }
+  }
+  target[i] = best;
+}
+
+__global__ void k_place_append(int64_t n_t, int64_t B, int P, const int32_t *target, int32_t *members,
+                               int64_t member_cap, int64_t *member_cnt, uint8_t *part_of, int32_t *local_idx) {
+  // one block of 1024 threads; per chunk of 1024 points, rank = # earlier points with the same target
+  __shared__ int32_t tg[1024];
+  __shared__ int64_t base[256];
+  for (int p = threadIdx.x; p < P; p += blockDim.x) base[p] = member_cnt[p];
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < B; c0 += 1024) {
+    const int64_t i = c0 + threadIdx.x;
+    const int t = i < B ? target[i] : -1;
+    tg[threadIdx.x] = t;
+    __syncthreads();
+    if (t >= 0) {
+      int r = 0;
+      for (int j = 0; j < (int)threadIdx.x; ++j) r += tg[j] == t;
+      const int64_t pos = base[t] + r;
+      members[(size_t)t * member_cap + pos] = (int32_t)(n_t + i);
+      part_of[n_t + i] = (uint8_t)t;
+      local_idx[n_t + i] = (int32_t)pos;
+    }
+    __syncthreads();
+    if (threadIdx.x < (unsigned)P) {
+      int cnt = 0;
+      for (int j = 0; j < 1024; ++j) cnt += tg[j] == (int)threadIdx.x;
+      base[threadIdx.x] += cnt;
+    }
+    __syncthreads();
+  }
+  for (int p = threadIdx.x; p < P; p += blockDim.x) member_cnt[p] = base[p];
+}
+
+cudaError_t launch_place(const VecGeom &g, const uint8_t *vec, int64_t n_t, int64_t B, int P, const int32_t *medoids,
+                         int32_t *members, int64_t member_cap, int64_t *member_cnt, uint8_t *part_of,
+                         int32_t *local_idx, int32_t *target, cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((B + 127) / 128);
+  if (g.metric == M_U8) k_place_target<M_U8><<<blocks, 128, 0, s>>>(vec, g.stride, g.nchunks, n_t, B, P, medoids, target);
+  else k_place_target<M_F32><<<blocks, 128, 0, s>>>(vec, g.stride, g.nchunks, n_t, B, P, medoids, target);
+  k_place_append<<<1, 1024, 0, s>>>(n_t, B, P, target, members, member_cap, member_cnt, part_of, local_idx);
+  return cudaGetLastError();
+}
+
+}  // namespace knng

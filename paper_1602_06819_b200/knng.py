@@ -1,0 +1,218 @@
+"""Thin ctypes binding of the C ABI in include/knng.h (argument marshalling only).
+
+Every step of every call runs in the library's CUDA kernels (libknng.so, sm_100a).
+There is no CPU path: if the shared library is missing or no CUDA device is present,
+the calls raise.  Names follow the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libknng.so")
+
+KNNG_L2SQ_U8, KNNG_L2SQ_F32, KNNG_JACCARD_U32SET = 0, 1, 2
+ERRORS = {
+    -1: "INVALID_ARG", -2: "INSUFFICIENT", -3: "EMPTY", -4: "CAPACITY_INFEAS", -5: "OOM",
+    -6: "CUDA", -7: "NCCL", -8: "CAPACITY_EXCEEDED",
+}
+
+
+class KnngError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("%s (%d): %s" % (ERRORS.get(code, "?"), code, msg))
+        self.code = code
+
+
+class knng_points(C.Structure):
+    _fields_ = [("metric", C.c_int32), ("dim", C.c_int32), ("n", C.c_int64), ("data", C.c_void_p),
+                ("offsets", C.c_void_p), ("data_on_device", C.c_int32)]
+
+
+class knng_params(C.Structure):
+    _fields_ = [("speedup", C.c_double), ("expansion_num", C.c_uint32), ("expansion_den", C.c_uint32),
+                ("depth", C.c_int32), ("seed", C.c_uint64), ("start_override", C.c_void_p),
+                ("start_override_len", C.c_int32)]
+
+
+class knng_stats(C.Structure):
+    _fields_ = [("search_evals", C.c_int64), ("search_starts", C.c_int64), ("search_skipped", C.c_int64),
+                ("search_expansions", C.c_int64), ("ball_nodes", C.c_int64), ("proposals", C.c_int64),
+                ("allpair_pairs", C.c_int64), ("kernel_launches", C.c_int64), ("ms_search", C.c_float),
+                ("ms_allpairs", C.c_float), ("ms_update", C.c_float), ("ms_merge", C.c_float),
+                ("ms_total", C.c_float)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class knng_runtime(C.Structure):
+    _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
+                ("nccl_unique_id", C.c_void_p), ("cuda_stream", C.c_void_p), ("capacity", C.c_int64)]
+
+
+EXPORTS = ["graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
+           "graph_get_partition", "graph_size", "graph_degree", "graph_free", "graph_last_error"]
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load libknng.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError("libknng.so not built (%s): run __graft_entry__.build()" % path)
+    L = C.CDLL(path)
+    P = C.c_void_p
+    L.graph_init.argtypes = [C.POINTER(knng_points), C.c_int32, C.POINTER(knng_runtime), C.POINTER(C.c_void_p)]
+    L.graph_insert_batch.argtypes = [P, C.POINTER(knng_points), C.POINTER(knng_params), C.POINTER(C.c_int64),
+                                     C.POINTER(knng_stats)]
+    L.graph_search.argtypes = [P, C.POINTER(knng_points), C.c_int32, C.POINTER(knng_params), P, P, C.c_int32,
+                               C.POINTER(knng_stats)]
+    L.partition_kmedoids.argtypes = [P, C.c_int32, C.c_double, C.c_int32, C.c_uint64, P, P, P, P]
+    L.graph_get_rows.argtypes = [P, C.c_int64, C.c_int64, P, P]
+    L.graph_get_partition.argtypes = [P, P, P, C.POINTER(C.c_int32)]
+    L.graph_size.argtypes = [P]
+    L.graph_size.restype = C.c_int64
+    L.graph_degree.argtypes = [P]
+    L.graph_degree.restype = C.c_int32
+    L.graph_free.argtypes = [P]
+    L.graph_free.restype = None
+    L.graph_last_error.restype = C.c_char_p
+    for f in ("graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
+              "graph_get_partition"):
+        getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc < 0:
+        raise KnngError(rc, load_library().graph_last_error().decode())
+    return rc
+
+
+def _metric_of(arr):
+    dt = np.dtype(str(arr.dtype).replace("torch.", ""))
+    if dt == np.uint8:
+        return KNNG_L2SQ_U8
+    if dt == np.float32:
+        return KNNG_L2SQ_F32
+    raise TypeError("points must be uint8 or float32, got %s" % arr.dtype)
+
+
+def make_points(points):
+    """Marshal a host numpy array or a CUDA torch tensor [n, dim] into knng_points.
+    Returns (struct, keepalive)."""
+    if hasattr(points, "is_cuda") and points.is_cuda:
+        t = points.contiguous()
+        n, d = t.shape
+        p = knng_points(_metric_of(t), d, n, C.c_void_p(t.data_ptr()), None, 1)
+        return p, t
+    a = np.ascontiguousarray(points)
+    if a.ndim != 2:
+        raise ValueError("points must be [n, dim]")
+    n, d = a.shape
+    p = knng_points(_metric_of(a), d, n, a.ctypes.data_as(C.c_void_p), None, 0)
+    return p, a
+
+
+def make_params(speedup, e_num, e_den, depth, seed, starts=None):
+    keep = None
+    sp, sl = None, 0
+    if starts is not None:
+        keep = np.ascontiguousarray(starts, np.int32)
+        sp, sl = keep.ctypes.data_as(C.c_void_p), len(keep)
+    return knng_params(float(speedup), int(e_num), int(e_den), int(depth), int(seed), sp, sl), keep
+
+
+class KnngGraph:
+    """One graph handle (graph_init ... graph_free)."""
+
+    def __init__(self, points, k, device=0, capacity=0, stream=None):
+        L = load_library()
+        p, keep = make_points(points)
+        rt = knng_runtime(int(device), 0, 1, None, C.c_void_p(stream) if stream else None, int(capacity))
+        h = C.c_void_p()
+        _check(L.graph_init(C.byref(p), int(k), C.byref(rt), C.byref(h)))
+        del keep
+        self._h = h
+        self.k = int(k)
+        self.metric = p.metric
+        self.dim = p.dim
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().graph_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n(self):
+        return int(load_library().graph_size(self._h))
+
+    def insert_batch(self, points, speedup, e_num, e_den, depth, seed):
+        p, keep = make_points(points)
+        prm, _ = make_params(speedup, e_num, e_den, depth, seed)
+        first = C.c_int64()
+        st = knng_stats()
+        _check(load_library().graph_insert_batch(self._h, C.byref(p), C.byref(prm), C.byref(first), C.byref(st)))
+        return int(first.value), st.as_dict()
+
+    def search(self, queries, kr, speedup, e_num, e_den, seed, starts=None, out=None):
+        p, keep = make_points(queries)
+        prm, keep2 = make_params(speedup, e_num, e_den, 1, seed, starts)
+        st = knng_stats()
+        if out is not None:        # device outputs (torch int32 tensors)
+            oi, ok = out
+            _check(load_library().graph_search(self._h, C.byref(p), int(kr), C.byref(prm),
+                                               C.c_void_p(oi.data_ptr()), C.c_void_p(ok.data_ptr()), 1,
+                                               C.byref(st)))
+            return oi, ok, st.as_dict()
+        ids = np.zeros((p.n, kr), np.int32)
+        keys = np.zeros((p.n, kr), np.uint32)
+        _check(load_library().graph_search(self._h, C.byref(p), int(kr), C.byref(prm),
+                                           ids.ctypes.data_as(C.c_void_p), keys.ctypes.data_as(C.c_void_p), 0,
+                                           C.byref(st)))
+        return ids, keys, st.as_dict()
+
+    def partition_kmedoids(self, P, imbalance, max_iter, seed, init_medoids=None):
+        n = self.n
+        part = np.zeros(n, np.uint8)
+        med = np.zeros(P, np.int32)
+        cost = np.full(max_iter + 1, -1, np.int64)
+        im = None if init_medoids is None else np.ascontiguousarray(init_medoids, np.int32)
+        rc = _check(load_library().partition_kmedoids(
+            self._h, int(P), float(imbalance), int(max_iter), int(seed), part.ctypes.data_as(C.c_void_p),
+            med.ctypes.data_as(C.c_void_p), cost.ctypes.data_as(C.c_void_p),
+            None if im is None else im.ctypes.data_as(C.c_void_p)))
+        return part, med, cost[:rc]
+
+    def rows(self, first=0, count=None):
+        count = self.n - first if count is None else count
+        ids = np.zeros((count, self.k), np.int32)
+        keys = np.zeros((count, self.k), np.uint32)
+        _check(load_library().graph_get_rows(self._h, int(first), int(count), ids.ctypes.data_as(C.c_void_p),
+                                             keys.ctypes.data_as(C.c_void_p)))
+        return ids, keys
+
+    def partition(self):
+        P = C.c_int32()
+        _check(load_library().graph_get_partition(self._h, None, None, C.byref(P)))
+        if P.value == 0:
+            return None, None
+        part = np.zeros(self.n, np.uint8)
+        med = np.zeros(P.value, np.int32)
+        _check(load_library().graph_get_partition(self._h, part.ctypes.data_as(C.c_void_p),
+                                                  med.ctypes.data_as(C.c_void_p), C.byref(P)))
+        return part, med

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same seeded inputs.
+
+Bar: integer metrics bit-exact; fp32 every key within 1e-5 relative and
+edge agreement >= 0.995 (north_star), which the canonical fp32 order makes bit-exact in practice.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import datagen as D
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+F32_RTOL = 1e-5
+
+
+def _graph(X, k, cap=None):
+    from paper_1602_06819_b200 import KnngGraph
+    return KnngGraph(X, k, device=0, capacity=cap or 2 * len(X))
+
+
+def _assert_rows_equal(metric, gi, gk, oi, ok, what):
+    if metric == O.F32:
+        gv = np.asarray(gk).view(np.float32).astype(np.float64)
+        ov = np.asarray(ok).view(np.float32).astype(np.float64)
+        assert np.all(np.abs(gv - ov) <= F32_RTOL * np.maximum(np.abs(ov), 1e-30)), what + ": keys"
+        agree = np.mean([len(set(a.tolist()) & set(b.tolist())) / len(b) for a, b in zip(gi, oi)])
+        assert agree >= 0.995, "%s: edge agreement %.5f" % (what, agree)
+        # canonical order: expect bit-exact
+        assert (gi == oi).all() and (gk == ok).all(), what + ": not bit-exact (within tolerance)"
+    else:
+        bad = np.nonzero((gi != oi).any(1) | (gk != ok).any(1))[0]
+        assert len(bad) == 0, "%s: %d rows differ, first %s: gpu %s %s oracle %s %s" % (
+            what, len(bad), bad[:5], gi[bad[0]], gk[bad[0]], oi[bad[0]], ok[bad[0]])
+
+
+def _cfg_small(name, **kw):
+    return D.CONFIGS[name].with_sizes(**kw)
+
+
+# ---------------------------------------------------------------------------
+# A0 graph_init
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,n0,k", [("C0", 2000, 10), ("C1", 3000, 10), ("C2", 2500, 20)])
+def test_graph_init_exact(name, n0, k):
+    cfg = _cfg_small(name, n0=n0)
+    X = D.initial_points(cfg)
+    g = _graph(X, k)
+    o = O.OracleGraph(cfg.metric, X, k)
+    o.init_exact()
+    gi, gk = g.rows()
+    _assert_rows_equal(cfg.metric, gi, gk, o.ids[:n0], o.keys[:n0], "graph_init " + name)
+
+
+@pytest.mark.parametrize("metric,dim", [(O.U8, 1), (O.U8, 3), (O.U8, 17), (O.F32, 1), (O.F32, 5), (O.F32, 33),
+                                        (O.F32, 130), (O.U8, 300)])
+def test_graph_init_ragged_dims_and_ties(metric, dim):
+    rng = np.random.default_rng(dim + 10 * metric)
+    n = 333   # ragged: not a multiple of the 64-row tile
+    if metric == O.U8:
+        X = rng.integers(0, 4, size=(n, dim)).astype(np.uint8)      # many exact ties
+    else:
+        X = rng.standard_normal((n, dim)).astype(np.float32)
+    g = _graph(X, 7)
+    o = O.OracleGraph(metric, X, 7)
+    o.init_exact()
+    gi, gk = g.rows()
+    _assert_rows_equal(metric, gi, gk, o.ids[:n], o.keys[:n], "init d=%d" % dim)
+
+
+def test_graph_init_errors():
+    from paper_1602_06819_b200 import KnngGraph, KnngError
+    with pytest.raises(KnngError) as e:
+        KnngGraph(np.zeros((5, 4), np.uint8), 5)
+    assert e.value.code == -2
+    with pytest.raises(KnngError) as e:
+        KnngGraph(np.zeros((50, 4), np.uint8), 0)
+    assert e.value.code == -1
+    with pytest.raises(KnngError) as e:
+        KnngGraph(np.zeros((50, 4), np.uint8), 33)
+    assert e.value.code == -1
+
+
+# ---------------------------------------------------------------------------
+# A2/A3 graph_search
+# ---------------------------------------------------------------------------
+def test_search_w3_hand_traces():
+    X = D.line_points([0, 10, 20, 30, 40, 100, 110, 120])
+    g = _graph(X, 2)
+    q = D.line_points([33])
+    ids, keys, st = g.search(q, 2, 1.0, 6, 5, 0, starts=[1, 6, 7, 5])
+    assert [(int(a), int(b)) for a, b in zip(keys[0], ids[0])] == [(9, 3), (49, 4)]
+    assert st["search_evals"] == 8 and st["search_skipped"] == 3
+    ids, keys, st = g.search(q, 2, 2.0, 6, 5, 0, starts=[1, 6, 7, 5])
+    assert [(int(a), int(b)) for a, b in zip(keys[0], ids[0])] == [(9, 3), (169, 2)]
+    assert st["search_evals"] == 4
+    ids, keys, st = g.search(q, 2, 1.3, 6, 5, 0, starts=[6, 5, 1])
+    assert [(int(a), int(b)) for a, b in zip(keys[0], ids[0])] == [(169, 2), (529, 1)]
+    assert st["search_evals"] == 6 and st["search_skipped"] == 0
+
+
+@pytest.mark.parametrize("name,n0,speedup,kr", [("C0", 2000, 4.0, 10), ("C0", 2000, 1.0, 10), ("C1", 6000, 8.0, 10),
+                                                ("C1", 6000, 3.0, 17), ("C2", 4000, 16.0, 20), ("C2", 4000, 2.0, 5)])
+def test_search_matches_oracle(name, n0, speedup, kr):
+    cfg = _cfg_small(name, n0=n0)
+    X = D.initial_points(cfg)
+    Q = D.query_points(cfg, 300)
+    g = _graph(X, cfg.k)
+    o = O.OracleGraph(cfg.metric, X, cfg.k)
+    o.init_exact()
+    gi, gk, gst = g.search(Q, kr, speedup, cfg.e_num, cfg.e_den, cfg.search_seed)
+    oi, ok, ost = o.search(Q, kr, speedup, cfg.e_num, cfg.e_den, cfg.search_seed)
+    _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "search " + name)
+    assert gst["search_evals"] == ost[:, 0].sum()
+    assert gst["search_starts"] == ost[:, 1].sum()
+    assert gst["search_skipped"] == ost[:, 2].sum()
+    assert gst["search_expansions"] == ost[:, 3].sum()
+    assert gst["search_evals"] == 300 * O.budget(n0, kr, speedup)
+
+
+def test_search_expansion_infinite_and_one():
+    cfg = _cfg_small("C1", n0=3000)
+    X = D.initial_points(cfg)
+    Q = D.query_points(cfg, 100)
+    g = _graph(X, cfg.k)
+    o = O.OracleGraph(cfg.metric, X, cfg.k)
+    o.init_exact()
+    for num, den in ((1, 0), (1, 1), (5, 1)):
+        gi, gk, gst = g.search(Q, 10, 6.0, num, den, 7)
+        oi, ok, ost = o.search(Q, 10, 6.0, num, den, 7)
+        _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "e=%d/%d" % (num, den))
+        assert gst["search_skipped"] == ost[:, 2].sum()
+
+
+# ---------------------------------------------------------------------------
+# A1-A7 graph_insert_batch
+# ---------------------------------------------------------------------------
+def _run_stream(cfg, batches, nthreads=None):
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    cap = cfg.n0 + cfg.n_insert + 8
+    g = _graph(X, cfg.k, cap)
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cap)
+    o.init_exact()
+    pos = 0
+    for B in batches:
+        first, gst = g.insert_batch(S[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        ost = o.insert_batch(S[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed,
+                             nthreads)
+        assert first == cfg.n0 + pos
+        assert gst["search_evals"] == ost[:, 0].sum()
+        assert gst["ball_nodes"] == ost[:, 4].sum()
+        assert gst["proposals"] == ost[:, 5].sum()
+        pos += B
+        gi, gk = g.rows()
+        oi, ok = o.rows()
+        _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "%s after %d inserts" % (cfg.name, pos))
+    return g, o
+
+
+def test_insert_C0_sequential_batches_of_one():
+    cfg = _cfg_small("C0", n_insert=60)
+    _run_stream(cfg, [1] * 60)
+
+
+def test_insert_C1_shape():
+    cfg = _cfg_small("C1", n0=20000, n_insert=2100)
+    _run_stream(cfg, [1024, 1024, 52])
+
+
+def test_insert_C2_shape_f32_depth3():
+    cfg = _cfg_small("C2", n0=12000, n_insert=1100)
+    _run_stream(cfg, [512, 512, 76])
+
+
+def test_insert_edge_cases():
+    # batch larger than the graph, k=1, depth 1, ragged dims, B=0
+    rng = np.random.default_rng(3)
+    for metric, dim, k, depth in ((O.U8, 3, 1, 1), (O.U8, 40, 4, 3), (O.F32, 7, 3, 2)):
+        X = (rng.integers(0, 9, size=(40, dim)).astype(np.uint8) if metric == O.U8
+             else rng.standard_normal((40, dim)).astype(np.float32))
+        S = (rng.integers(0, 9, size=(120, dim)).astype(np.uint8) if metric == O.U8
+             else rng.standard_normal((120, dim)).astype(np.float32))
+        g = _graph(X, k, 200)
+        o = O.OracleGraph(metric, X, k, capacity=200)
+        o.init_exact()
+        for lo, hi in ((0, 0), (0, 100), (100, 101), (101, 120)):
+            g.insert_batch(S[lo:hi], 2.0, 6, 5, depth, 11)
+            o.insert_batch(S[lo:hi], 2.0, 6, 5, depth, 11)
+            gi, gk = g.rows()
+            oi, ok = o.rows()
+            _assert_rows_equal(metric, gi, gk, oi, ok, "edge m=%d d=%d k=%d" % (metric, dim, k))
+
+
+def test_insert_errors():
+    from paper_1602_06819_b200 import KnngGraph, KnngError
+    g = KnngGraph(np.zeros((20, 4), np.uint8), 3, capacity=25)
+    with pytest.raises(KnngError) as e:
+        g.insert_batch(np.zeros((6, 4), np.uint8), 2.0, 6, 5, 2, 1)
+    assert e.value.code == -8
+    with pytest.raises(KnngError) as e:
+        g.insert_batch(np.zeros((2, 5), np.uint8), 2.0, 6, 5, 2, 1)
+    assert e.value.code == -1
+    with pytest.raises(KnngError) as e:
+        g.insert_batch(np.zeros((2, 4), np.uint8), 0.5, 6, 5, 2, 1)
+    assert e.value.code == -1
+    with pytest.raises(KnngError) as e:
+        g.insert_batch(np.zeros((2, 4), np.uint8), 2.0, 6, 5, 0, 1)
+    assert e.value.code == -1
+
+
+# ---------------------------------------------------------------------------
+# Full C1 size, in the launch configuration bench.py times (B = 1024): sampled outputs
+# ---------------------------------------------------------------------------
+def test_C1_full_size_sampled():
+    cfg = D.CONFIGS["C1"]
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.batch)
+    g = _graph(X, cfg.k, cfg.n0 + cfg.n_insert)
+    o = O.OracleGraph(cfg.metric, X, cfg.k)
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(cfg.n0, 300, replace=False))
+    oi, ok = o.exact_rows(sample)
+    gi, gk = g.rows()
+    _assert_rows_equal(cfg.metric, gi[sample], gk[sample], oi, ok, "C1 init sample")
+    first, st = g.insert_batch(S, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+    assert st["search_evals"] == cfg.batch * O.budget(cfg.n0, cfg.k, cfg.speedup)
+    gi, gk = g.rows()
+    # every stored key is the oracle's key of that pair; rows sorted, distinct, no self-loops
+    allp = np.concatenate([X, S])
+    for v in list(sample[:100]) + list(range(cfg.n0, cfg.n0 + 100)):
+        row = gi[v].tolist()
+        assert v not in row and len(set(row)) == cfg.k
+        for a in range(cfg.k):
+            assert O.key(cfg.metric, allp[v], allp[row[a]]) == int(gk[v, a])
+        for a in range(cfg.k - 1):
+            assert O.precedes(cfg.metric, int(gk[v, a]), row[a], int(gk[v, a + 1]), row[a + 1])
+    # new rows: top-k of (own search result, peers) => at least as close as the exact peers-only top-k
+    for i in range(0, cfg.batch, 97):
+        D_peers = sorted((O.key(cfg.metric, S[i], S[j]), cfg.n0 + j) for j in range(cfg.batch) if j != i)
+        assert int(gk[cfg.n0 + i, -1]) <= D_peers[cfg.k - 1][0]
