@@ -100,8 +100,7 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
       // committable: fresh draws in order up to the first one without a key
       const unsigned miss = fm & ~hm;
       unsigned cm = miss ? (fm & ((1u << (__ffs(miss) - 1)) - 1u)) : fm;
-      bool hit = false;
-      if ((int64_t)__popc(cm) > budget - c) { cm = first_bits(cm, (int)(budget - c)); hit = true; }
+      if ((int64_t)__popc(cm) > budget - c) cm = first_bits(cm, (int)(budget - c));
       const bool inc = (cm >> lane) & 1u;
       // s_max before each draw: best of top-k and of the earlier committed draws
       uint32_t run = wkey;
@@ -135,7 +134,9 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
       s_starts += ncm;
       s_skip += ncm - (am ? 1 : 0);
       __syncwarp();
-      if (hit) break;
+      // budget reached: stop, unless a start was accepted -- then, as in the sequential
+      // algorithm, its walk begins and ends at the first fresh evaluation it needs
+      if (c >= budget && !am) break;
       if (!am) {
         wpos = miss ? (__ffs(miss) - 1) : 32;
         continue;
