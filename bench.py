@@ -262,8 +262,8 @@ def run_ours(args, cfg):
                      "alg_bytes_per_launch": bytes_search / len(stats),
                      "ms_per_launch": ms_search / len(stats),
                      "note": "C1 is L2-resident (14 MB store): HBM fraction is not the binding claim"},
-        "phase_ms": {p: sum(s[p] for s in stats) / len(stats) for p in ("ms_search", "ms_allpairs", "ms_update",
-                                                                       "ms_merge")},
+        "phase_ms": {p: sum(s[p] for s in stats) / len(stats) for p in ("ms_search", "ms_allpairs",
+                                                                       "ms_update", "ms_merge")},
         "e2e": {"value": args.steps * B * ws / t_e2e, "unit": "inserts/s", "h2d_bytes_per_step": B * V,
                 "d2h_bytes_per_step": 16 * 8},
         "gpu_launches": launches,

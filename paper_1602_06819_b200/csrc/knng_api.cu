@@ -50,6 +50,7 @@ struct DBuf {
   size_t bytes = 0;
   cudaError_t ensure(size_t need) {
     if (need <= bytes) return cudaSuccess;
+    need += need / 4;             // grow geometrically: batches grow the pool a little each time
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -248,11 +249,9 @@ struct SearchPlan {
 static SearchPlan plan_search(knng_graph *g, int64_t tasks, int64_t mmax) {
   SearchPlan sp;
   sp.bits_words = 2 * ((mmax + 31) / 32);
-  const size_t per_block = (size_t)4 * sp.bits_words * 4;
-  sp.smem = per_block <= 200 * 1024 ? 1 : 0;
-  int64_t blocks = (tasks + 3) / 4;
-  if (!sp.smem && blocks > 148 * 16) blocks = 148 * 16;
-  sp.slots = blocks * 4;
+  // visited + expanded bitmaps in shared memory when a CTA still fits >= 4 times per SM
+  sp.smem = (size_t)sp.bits_words * 4 <= 40 * 1024 ? 1 : 0;
+  sp.slots = sp.smem ? tasks : std::min<int64_t>(tasks, 148 * 8);
   return sp;
 }
 
@@ -307,12 +306,14 @@ static int run_search_phase(knng_graph *g, const uint8_t *qbase, int64_t nq, int
   a.nstarts = nstarts;
   a.G = 8;
   a.gbits = g->w_bits.as<uint32_t>();
+  a.gslots = sp.slots;
   a.bits_words = sp.bits_words;
   a.smem_bits = sp.smem;
   a.out_ids = ci;
   a.out_keys = ck;
   a.stats = g->w_stats.as<unsigned long long>();
-  cudaError_t e = launch_search(g->geom, a, g->stream, nl);
+  cudaError_t e;
+  e = launch_search(g->geom, a, g->stream, nl);
   if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
   if (g->P > 0) {
     e = launch_merge_parts(g->metric, ci, ck, nq, g->P, kr, out_i, out_k, g->stream);

@@ -39,7 +39,8 @@ struct SearchArgs {
   int nstarts;
   int G;                       // restart draws evaluated together
   // bitmap workspace
-  uint32_t *gbits;             // global: per warp slot, bits_words each
+  uint32_t *gbits;             // global: per CTA slot, bits_words each
+  int64_t gslots;              // CTA slots of gbits (grid cap when bitmaps are global)
   int64_t bits_words;          // evaluated + expanded words per task slot
   int smem_bits;               // 1: bitmaps in dynamic shared memory
   // outputs

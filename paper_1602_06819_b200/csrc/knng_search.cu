@@ -17,40 +17,86 @@
 
 namespace knng {
 
+constexpr int RING_CHUNKS = 16;   // smem ring of 16 x 32 precomputed draws per CTA
+
+struct RingHdr {
+  int seq[RING_CHUNKS];   // seq[s] = c + 1 once chunk c is in slot s
+  int consumed;           // chunks < consumed are free
+  int done;               // consumer finished the task
+};
+
+// Producer warp(s): speculative evaluation of the random starts.  The draw sequence of a search
+// is fixed by the counter RNG (Q4) and the key of a draw is a pure function of (query, node), so
+// producers evaluate draws ahead of the consumer, 32 per chunk, into the CTA's smem ring.
+// Nothing here touches a counter, the visited sets or the top-k.
+template <int M, int L, int CPL>
+__device__ __forceinline__ void produce(const SearchArgs &a, const VecQuery<M, L, CPL> &Q, volatile RingHdr *hdr,
+                                        int2 *ring, int pw, int nprod, int64_t nch, uint64_t h3, int64_t m,
+                                        const int32_t *pool) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t c = pw; c < nch; c += nprod) {
+    while (c - hdr->consumed >= RING_CHUNKS && !hdr->done) __nanosleep(64);
+    if (hdr->done) break;
+    const uint64_t idx = rng_index(h3, (uint64_t)(c * 32 + lane), (uint64_t)m);
+    const int32_t node = pool ? pool[idx] : (int32_t)idx;
+    const uint32_t key = Q.eval(a.vec, a.stride, a.nchunks, node, 32);
+    volatile int *rs = (volatile int *)(ring + (c % RING_CHUNKS) * 32 + lane);
+    rs[0] = node;
+    rs[1] = (int)key;
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) hdr->seq[c % RING_CHUNKS] = (int)(c + 1);
+  }
+}
+
+// K1: one CTA per (query, partition) task: warp 0 runs the search in the paper's sequential
+// order, warps 1.. produce its random-start keys ahead of it.
 template <int M, int L, int CPL>
 __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
-  extern __shared__ uint32_t smem_bits[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int wpb = blockDim.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * wpb + wib, nw = (int64_t)gridDim.x * wpb;
+  extern __shared__ __align__(16) uint8_t smem[];
+  volatile RingHdr *hdr = (volatile RingHdr *)smem;
+  int2 *ring = (int2 *)(smem + 128);
+  int32_t *rowbuf = (int32_t *)(smem + 128 + RING_CHUNKS * 32 * 8);
+  uint32_t *sbits = (uint32_t *)(smem + 128 + RING_CHUNKS * 32 * 8 + 32 * 32 * 4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nprod = (blockDim.x >> 5) - 1;
   const int Pn = a.P > 0 ? a.P : 1;
   const int64_t T = a.nq * Pn;
-  uint32_t *bits = a.smem_bits ? smem_bits + (size_t)wib * a.bits_words : a.gbits + gw * a.bits_words;
+  uint32_t *bits = a.smem_bits ? sbits : a.gbits + (int64_t)blockIdx.x * a.bits_words;
   const int k = a.k;
   unsigned long long s_evals = 0, s_starts = 0, s_skip = 0, s_exp = 0;
 
-  for (int64_t task = gw; task < T; task += nw) {
+  for (int64_t task = blockIdx.x; task < T; task += gridDim.x) {
     const int64_t b = task / Pn;
     const int p = (int)(task % Pn);
     const int64_t m = a.P > 0 ? a.member_cnt[p] : a.n_t;
     const int32_t *pool = a.P > 0 ? a.members + (size_t)p * a.member_cap : nullptr;
     const int64_t words = (m + 31) >> 5;
     uint32_t *ev = bits, *ex = bits + words;
-    for (int64_t w = lane; w < 2 * words; w += 32) bits[w] = 0;
-    __syncwarp();
+    __syncthreads();
+    for (int64_t w = threadIdx.x; w < 2 * words; w += blockDim.x) bits[w] = 0;
+    if (threadIdx.x < RING_CHUNKS) hdr->seq[threadIdx.x] = 0;
+    if (threadIdx.x == 0) { hdr->consumed = 0; hdr->done = 0; }
+    __syncthreads();
 
     // budget (Q6) -- never more than the pool (Q7)
     int64_t budget = (int64_t)floor((double)m / a.speedup);
     const int64_t lo = m < a.kr ? m : a.kr;
     if (budget < lo) budget = lo;
     if (budget > m) budget = m;
+    const int64_t nch = a.starts ? 0 : (budget + 31) / 32;   // chunks the producers evaluate
 
     VecQuery<M, L, CPL> Q;
     Q.load(a.qbase + (size_t)b * a.stride, a.nchunks);
+    const uint64_t h3 = rng_prefix(a.seed, (uint64_t)(a.pid_base + b), (uint64_t)p);
+    if (warp > 0) {
+      if (budget > 0) produce<M, L, CPL>(a, Q, hdr, ring, warp - 1, nprod, nch, h3, m, pool);
+      continue;
+    }
+
+    // ================================ consumer ================================
     WarpTopK<M> top;
     top.init(a.kr);
-    const uint64_t h3 = rng_prefix(a.seed, (uint64_t)(a.pid_base + b), (uint64_t)p);
-
     int64_t c = 0, jbase = 0;
     int32_t wnode = -1;
     uint32_t wkey = 0, wl = 0;
@@ -61,15 +107,28 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
       // ------------------------------ restart ------------------------------
       if (wpos >= 32) {
         const int64_t j = jbase + lane;
-        if (a.starts) {
-          wnode = j < a.nstarts ? a.starts[j] : -1;
+        const int64_t ch = jbase / 32;
+        if (ch < nch && nprod > 0) {                 // produced ahead into the ring
+          const int slot = (int)(ch % RING_CHUNKS);
+          while (hdr->seq[slot] != (int)(ch + 1)) __nanosleep(20);
+          __threadfence_block();
+          const volatile int *rs = (const volatile int *)(ring + slot * 32 + lane);
+          wnode = rs[0];
+          wkey = (uint32_t)rs[1];
+          whave = true;
+          __syncwarp();
+          if (lane == 0) hdr->consumed = (int)(ch + 1);
         } else {
-          const uint64_t idx = rng_index(h3, (uint64_t)j, (uint64_t)m);
-          wnode = pool ? pool[idx] : (int32_t)idx;
+          if (a.starts) {
+            wnode = j < a.nstarts ? a.starts[j] : -1;
+          } else {
+            const uint64_t idx = rng_index(h3, (uint64_t)j, (uint64_t)m);
+            wnode = pool ? pool[idx] : (int32_t)idx;
+          }
+          whave = false;
         }
         wl = wnode >= 0 ? (a.P > 0 ? (uint32_t)a.local_idx[wnode] : (uint32_t)wnode) : 0u;
         jbase += 32;
-        whave = false;
         wpos = 0;
       }
       const unsigned active = FULL << wpos;
@@ -84,10 +143,11 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
         wpos = 32;
         continue;
       }
-      // evaluate the next G fresh draws that have no cached key
+      // evaluate the next G fresh draws that have no key yet (beyond the produced range)
       unsigned hm = __ballot_sync(FULL, whave);
-      const unsigned need = first_bits(fm, a.G) & ~hm;
-      if (need) {
+      const unsigned nokey = fm & ~hm;
+      if (nokey) {
+        const unsigned need = first_bits(nokey, a.G);
         const int nn = __popc(need);
         const int src = lane < nn ? (int)__fns(need, 0, lane + 1) : 0;
         const int32_t cid = __shfl_sync(FULL, wnode, src);
@@ -147,14 +207,23 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
       int32_t cur = __shfl_sync(FULL, wnode, al);
       uint32_t kcur = __shfl_sync(FULL, wkey, al);
       uint32_t curl = __shfl_sync(FULL, wl, al);
+      int pf = -1;                 // row of cur prefetched into rowbuf[pf*k ..] by the last step
       bool stop = false;
       for (;;) {
         if (lane == 0) bit_set(ex, curl);
         ++s_exp;
-        const int32_t v = lane < k ? a.rows[(size_t)cur * k + lane] : -1;
+        int32_t v = -1;
+        if (lane < k) v = pf >= 0 ? rowbuf[pf * k + lane] : a.rows[(size_t)cur * k + lane];
         const bool inpool = v >= 0 && (a.P == 0 || a.part_of[v] == p);   // Q10
         const uint32_t lv = inpool ? (a.P > 0 ? (uint32_t)a.local_idx[v] : (uint32_t)v) : 0u;
         __syncwarp();
+        // prefetch the rows of the in-pool neighbours: the next cur is one of them
+        for (int base = 0; base < k * k; base += 32) {
+          const int idx = base + lane;
+          const int t = idx / k;
+          const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t < 32 ? t : 31);
+          if (idx < k * k && vt >= 0) rowbuf[idx] = a.rows[(size_t)vt * k + (idx - t * k)];
+        }
         const bool evb2 = inpool ? bit_get(ev, lv) : true;
         const bool exb2 = inpool ? bit_get(ex, lv) : false;
         const uint32_t key = Q.eval(a.vec, a.stride, a.nchunks, inpool ? v : -1, k);
@@ -175,10 +244,12 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
         cur = __shfl_sync(FULL, v, fi);
         kcur = __shfl_sync(FULL, key, fi);
         curl = __shfl_sync(FULL, lv, fi);
+        pf = fi;
         if (__shfl_sync(FULL, exb2, fi)) break;   // Q9: moving onto an expanded node restarts
       }
       if (stop) break;
     }
+    if (lane == 0) hdr->done = 1;
     s_evals += c;
     if (lane < a.kr) {
       const size_t o = ((size_t)b * Pn + p) * a.kr + lane;
@@ -187,7 +258,7 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
     }
     __syncwarp();
   }
-  if (lane == 0) {
+  if (lane == 0 && warp == 0) {
     atomicAdd(a.stats + 0, s_evals);
     atomicAdd(a.stats + 1, s_starts);
     atomicAdd(a.stats + 2, s_skip);
@@ -216,26 +287,21 @@ __global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq,
   }
 }
 
-// ---------------------------------------------------------------------------
 template <int M, int L, int CPL>
-static cudaError_t run_search(const SearchArgs &a0, cudaStream_t s) {
-  SearchArgs a = a0;
+static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int Pn = a.P > 0 ? a.P : 1;
   const int64_t T = a.nq * Pn;
   if (T == 0) return cudaSuccess;
-  const int wpb = 4;
-  size_t smem = 0;
-  if (a.smem_bits) smem = (size_t)wpb * a.bits_words * 4;
+  const int warps = a.starts ? 1 : 2;          // consumer + producer(s)
+  size_t smem = 128 + RING_CHUNKS * 32 * 8 + 32 * 32 * 4;
+  if (a.smem_bits) smem += (size_t)a.bits_words * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  int64_t blocks = (T + wpb - 1) / wpb;
-  if (!a.smem_bits) {
-    const int64_t cap = (int64_t)a.bits_words > 0 ? 148 * 16 : blocks;
-    if (blocks > cap) blocks = cap;
-  }
-  k_search<M, L, CPL><<<(unsigned)blocks, wpb * 32, smem, s>>>(a);
+  int64_t blocks = T;
+  if (!a.smem_bits && blocks > a.gslots) blocks = a.gslots;
+  k_search<M, L, CPL><<<(unsigned)blocks, warps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 
