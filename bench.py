@@ -257,6 +257,9 @@ def run_ours(args, cfg):
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "similarities_per_s": evals * ws / t_total,
         "recall_at_k": rec,
+        "search_per_query": {f: sum(s_[f] for s_ in stats) / (len(stats) * B) for f in
+                             ("search_evals", "search_starts", "search_skipped", "search_expansions", "ball_nodes",
+                              "proposals")},
         "roofline": {"bound": "hbm", "kernel": "k_search (K1 iGNNS)", "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "alg_bytes_per_launch": bytes_search / len(stats),

@@ -13,6 +13,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -312,6 +313,7 @@ static int run_search_phase(knng_graph *g, const uint8_t *qbase, int64_t nq, int
   a.out_ids = ci;
   a.out_keys = ck;
   a.stats = g->w_stats.as<unsigned long long>();
+  a.prof = getenv("KNNG_PROFILE") ? a.stats + 8 : nullptr;   // cycle counters -> stats[8..13]
   cudaError_t e;
   e = launch_search(g->geom, a, g->stream, nl);
   if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
@@ -434,6 +436,9 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   CK(cudaMemcpyAsync(h, g->w_stats.p, 16 * 8, cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
   h[6] = (unsigned long long)(B * (B - 1));
+  if (getenv("KNNG_PROFILE"))
+    fprintf(stderr, "KNNG_PROFILE cycles/task: consumer %.0f ring-wait %.0f walk %.0f | producer work %.0f wait %.0f | windows/task %.1f\n",
+            (double)h[8] / B, (double)h[9] / B, (double)h[10] / B, (double)h[11] / B, (double)h[12] / B, (double)h[13] / B);
   g->n = n_t + B;
   fill_stats(g, st, h, nl, 5);
   return KNNG_OK;

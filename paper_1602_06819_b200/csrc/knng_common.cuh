@@ -77,6 +77,13 @@ __device__ __forceinline__ bool bit_get(const uint32_t *b, uint32_t i) {
 }
 __device__ __forceinline__ void bit_set(uint32_t *b, uint32_t i) { atomicOr(b + (i >> 5), 1u << (i & 31)); }
 
+// asynchronous 4-byte global -> shared copy (LDGSTS): the warp does not wait for the load
+__device__ __forceinline__ void cp_async4(void *smem_dst, const void *gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -101,7 +108,8 @@ struct WarpTopK {
   uint32_t key;
   int32_t id;
   int cnt, kr;
-  __device__ __forceinline__ void init(int kr_) { key = 0; id = -1; cnt = 0; kr = kr_; }
+  uint32_t key_at0;   // warp-uniform copy of the best key (valid when cnt > 0)
+  __device__ __forceinline__ void init(int kr_) { key = 0; id = -1; cnt = 0; kr = kr_; key_at0 = 0; }
   __device__ __forceinline__ uint32_t best() const { return __shfl_sync(FULL, key, 0); }
   // insert every lane with flag set (distinct ids assumed)
   __device__ __forceinline__ void insert(bool flag, uint32_t ck, int32_t cid) {
@@ -125,6 +133,7 @@ struct WarpTopK {
       if (lane > pos) { key = uk; id = ui; }
       if (lane == pos) { key = k2; id = i2; }
       if (cnt < kr) ++cnt;
+      if (pos == 0) key_at0 = k2;
     }
   }
 };

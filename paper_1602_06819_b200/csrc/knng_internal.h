@@ -47,6 +47,7 @@ struct SearchArgs {
   int32_t *out_ids;            // [nq][max(P,1)][kr]
   uint32_t *out_keys;
   unsigned long long *stats;   // [0] evals [1] starts [2] skipped [3] expansions
+  unsigned long long *prof;    // optional cycle counters (KNNG_PROFILE=1), else null
 };
 
 struct BallArgs {

@@ -17,7 +17,7 @@
 
 namespace knng {
 
-constexpr int RING_CHUNKS = 16;   // smem ring of 16 x 32 precomputed draws per CTA
+constexpr int RING_CHUNKS = 8;    // smem ring of 8 x 32 precomputed draws per CTA
 
 struct RingHdr {
   int seq[RING_CHUNKS];   // seq[s] = c + 1 once chunk c is in slot s
@@ -34,8 +34,12 @@ __device__ __forceinline__ void produce(const SearchArgs &a, const VecQuery<M, L
                                         int2 *ring, int pw, int nprod, int64_t nch, uint64_t h3, int64_t m,
                                         const int32_t *pool) {
   const int lane = threadIdx.x & 31;
+  long long p_wait = 0, p_work = 0;
   for (int64_t c = pw; c < nch; c += nprod) {
+    const long long t0 = a.prof ? clock64() : 0;
     while (c - hdr->consumed >= RING_CHUNKS && !hdr->done) __nanosleep(64);
+    const long long t1 = a.prof ? clock64() : 0;
+    p_wait += t1 - t0;
     if (hdr->done) break;
     const uint64_t idx = rng_index(h3, (uint64_t)(c * 32 + lane), (uint64_t)m);
     const int32_t node = pool ? pool[idx] : (int32_t)idx;
@@ -46,24 +50,31 @@ __device__ __forceinline__ void produce(const SearchArgs &a, const VecQuery<M, L
     __threadfence_block();
     __syncwarp();
     if (lane == 0) hdr->seq[c % RING_CHUNKS] = (int)(c + 1);
+    if (a.prof) p_work += clock64() - t1;
+  }
+  if (a.prof && lane == 0) {
+    atomicAdd(a.prof + 3, (unsigned long long)p_work);
+    atomicAdd(a.prof + 4, (unsigned long long)p_wait);
   }
 }
 
 // K1: one CTA per (query, partition) task: warp 0 runs the search in the paper's sequential
 // order, warps 1.. produce its random-start keys ahead of it.
 template <int M, int L, int CPL>
-__global__ void __launch_bounds__(128) k_search(SearchArgs a) {
+__global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   volatile RingHdr *hdr = (volatile RingHdr *)smem;
   int2 *ring = (int2 *)(smem + 128);
-  int32_t *rowbuf = (int32_t *)(smem + 128 + RING_CHUNKS * 32 * 8);
-  uint32_t *sbits = (uint32_t *)(smem + 128 + RING_CHUNKS * 32 * 8 + 32 * 32 * 4);
+  int32_t *rowbuf = (int32_t *)(smem + 128 + RING_CHUNKS * 32 * 8);          // [k][k]
+  int32_t *rowbuf2 = rowbuf + a.k * a.k;                                      // [32][k]
+  uint32_t *sbits = (uint32_t *)(rowbuf2 + 32 * a.k);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nprod = (blockDim.x >> 5) - 1;
   const int Pn = a.P > 0 ? a.P : 1;
   const int64_t T = a.nq * Pn;
   uint32_t *bits = a.smem_bits ? sbits : a.gbits + (int64_t)blockIdx.x * a.bits_words;
   const int k = a.k;
+  const float rk = 1.0f / (float)k;
   unsigned long long s_evals = 0, s_starts = 0, s_skip = 0, s_exp = 0;
 
   for (int64_t task = blockIdx.x; task < T; task += gridDim.x) {
@@ -100,9 +111,11 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
     int64_t c = 0, jbase = 0;
     int32_t wnode = -1;
     uint32_t wkey = 0, wl = 0;
-    bool whave = false;
+    bool whave = false, wpf = false;
     int wpos = 32;
 
+    const long long tc0 = a.prof ? clock64() : 0;
+    long long p_wait = 0, p_walk = 0, p_win = 0;
     while (c < budget) {
       // ------------------------------ restart ------------------------------
       if (wpos >= 32) {
@@ -110,7 +123,10 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
         const int64_t ch = jbase / 32;
         if (ch < nch && nprod > 0) {                 // produced ahead into the ring
           const int slot = (int)(ch % RING_CHUNKS);
+          const long long tw = a.prof ? clock64() : 0;
           while (hdr->seq[slot] != (int)(ch + 1)) __nanosleep(20);
+          if (a.prof) p_wait += clock64() - tw;
+          ++p_win;
           __threadfence_block();
           const volatile int *rs = (const volatile int *)(ring + slot * 32 + lane);
           wnode = rs[0];
@@ -130,6 +146,17 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
         wl = wnode >= 0 ? (a.P > 0 ? (uint32_t)a.local_idx[wnode] : (uint32_t)wnode) : 0u;
         jbase += 32;
         wpos = 0;
+        // prefetch the rows of the draws that could still be accepted: the skip threshold only
+        // tightens as s_max improves, so "passes against the current best" is a superset
+        wpf = false;
+        if (whave && wnode >= 0) {
+          wpf = top.cnt == 0 ? lane == 0 : !skip_start<M>(wkey, top.key_at0, a.e_num, a.e_den);
+          if (__ballot_sync(FULL, wpf)) {
+            cp_async_wait_all();      // older copies into rowbuf2 must land first
+            if (wpf)
+              for (int e = 0; e < k; ++e) cp_async4(rowbuf2 + lane * k + e, a.rows + (size_t)wnode * k + e);
+          }
+        }
       }
       const unsigned active = FULL << wpos;
       const unsigned invm = __ballot_sync(FULL, wnode < 0) & active;
@@ -162,6 +189,10 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
       unsigned cm = miss ? (fm & ((1u << (__ffs(miss) - 1)) - 1u)) : fm;
       if ((int64_t)__popc(cm) > budget - c) cm = first_bits(cm, (int)(budget - c));
       const bool inc = (cm >> lane) & 1u;
+      unsigned am;
+      if (top.cnt > 0 && __ballot_sync(FULL, inc && !skip_start<M>(wkey, top.key_at0, a.e_num, a.e_den)) == 0) {
+        am = 0;   // every committable draw is skipped even against the current s_max
+      } else {
       // s_max before each draw: best of top-k and of the earlier committed draws
       uint32_t run = wkey;
       bool rv = inc;
@@ -183,7 +214,8 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
       }
       // first start never skipped (Q3): it is the only draw with no best before it
       const bool acc = inc && (!bv || !skip_start<M>(wkey, bk, a.e_num, a.e_den));
-      const unsigned am = __ballot_sync(FULL, acc);
+      am = __ballot_sync(FULL, acc);
+      }
       const int al = am ? __ffs(am) - 1 : -1;
       const unsigned commit = am ? (cm & (al == 31 ? FULL : ((2u << al) - 1u))) : cm;
       const bool cmt = (commit >> lane) & 1u;
@@ -204,25 +236,34 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
       wpos = al + 1;
 
       // ------------------- hill climbing, eager first improvement -------------------
+      const long long tk0 = a.prof ? clock64() : 0;
       int32_t cur = __shfl_sync(FULL, wnode, al);
       uint32_t kcur = __shfl_sync(FULL, wkey, al);
       uint32_t curl = __shfl_sync(FULL, wl, al);
       int pf = -1;                 // row of cur prefetched into rowbuf[pf*k ..] by the last step
+      int pf2 = al;                // ... or into rowbuf2[pf2*k ..] when the window was loaded
+      if (!__shfl_sync(FULL, wpf, al)) pf2 = -1;
       bool stop = false;
       for (;;) {
         if (lane == 0) bit_set(ex, curl);
         ++s_exp;
         int32_t v = -1;
-        if (lane < k) v = pf >= 0 ? rowbuf[pf * k + lane] : a.rows[(size_t)cur * k + lane];
+        if (pf >= 0 || pf2 >= 0) {
+          cp_async_wait_all();
+          __syncwarp();
+        }
+        if (lane < k)
+          v = pf >= 0 ? rowbuf[pf * k + lane] : (pf2 >= 0 ? rowbuf2[pf2 * k + lane] : a.rows[(size_t)cur * k + lane]);
+        pf2 = -1;
         const bool inpool = v >= 0 && (a.P == 0 || a.part_of[v] == p);   // Q10
         const uint32_t lv = inpool ? (a.P > 0 ? (uint32_t)a.local_idx[v] : (uint32_t)v) : 0u;
         __syncwarp();
         // prefetch the rows of the in-pool neighbours: the next cur is one of them
         for (int base = 0; base < k * k; base += 32) {
           const int idx = base + lane;
-          const int t = idx / k;
+          const int t = __float2int_rz(__fmul_rn(__int2float_rn(idx) + 0.5f, rk));   // idx / k
           const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t < 32 ? t : 31);
-          if (idx < k * k && vt >= 0) rowbuf[idx] = a.rows[(size_t)vt * k + (idx - t * k)];
+          if (idx < k * k && vt >= 0) cp_async4(rowbuf + idx, a.rows + (size_t)vt * k + (idx - t * k));
         }
         const bool evb2 = inpool ? bit_get(ev, lv) : true;
         const bool exb2 = inpool ? bit_get(ex, lv) : false;
@@ -247,7 +288,14 @@ __global__ void __launch_bounds__(128) k_search(SearchArgs a) {
         pf = fi;
         if (__shfl_sync(FULL, exb2, fi)) break;   // Q9: moving onto an expanded node restarts
       }
+      if (a.prof) p_walk += clock64() - tk0;
       if (stop) break;
+    }
+    if (a.prof && lane == 0) {
+      atomicAdd(a.prof + 0, (unsigned long long)(clock64() - tc0));
+      atomicAdd(a.prof + 1, (unsigned long long)p_wait);
+      atomicAdd(a.prof + 2, (unsigned long long)p_walk);
+      atomicAdd(a.prof + 5, (unsigned long long)p_win);
     }
     if (lane == 0) hdr->done = 1;
     s_evals += c;
@@ -292,8 +340,8 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int Pn = a.P > 0 ? a.P : 1;
   const int64_t T = a.nq * Pn;
   if (T == 0) return cudaSuccess;
-  const int warps = a.starts ? 1 : 2;          // consumer + producer(s)
-  size_t smem = 128 + RING_CHUNKS * 32 * 8 + 32 * 32 * 4;
+  const int warps = a.starts ? 1 : 2;          // consumer + producers
+  size_t smem = 128 + RING_CHUNKS * 32 * 8 + (size_t)(a.k * a.k + 32 * a.k) * 4;
   if (a.smem_bits) smem += (size_t)a.bits_words * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

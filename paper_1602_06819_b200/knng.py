@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libknng.so")
+LIB_PATH = os.environ.get("KNNG_LIB") or os.path.join(_HERE, "libknng.so")
 
 KNNG_L2SQ_U8, KNNG_L2SQ_F32, KNNG_JACCARD_U32SET = 0, 1, 2
 ERRORS = {
