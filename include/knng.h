@@ -78,7 +78,7 @@ typedef struct {
  *  speedup        budget of one search = max(min(k, |pool|), floor(|pool| / speedup)) similarity
  *                 evaluations (reading Q6); speedup >= 1.
  *  expansion_num/den  expansion e = num/den >= 1 of the restart skip rule; den = 0 means
- *                 e = +inf (never skip).  1.2 = 6/5.
+ *                 e = +inf (never skip).  1.2 = 6/5.  num, den <= 65535.
  *  depth          DEPTH of the update (Alg. 2), 1..10.
  *  seed           key of the counter RNG of the random starts (reading Q4): results are a pure
  *                 function of (inputs, params, seed).

@@ -237,6 +237,8 @@ static int check_params(const knng_params *p) {
   if (!p) return fail(KNNG_ERR_INVALID_ARG, "null params");
   if (!(p->speedup >= 1.0)) return fail(KNNG_ERR_INVALID_ARG, "speedup < 1");
   if (p->expansion_den != 0 && p->expansion_num < p->expansion_den) return fail(KNNG_ERR_INVALID_ARG, "expansion < 1");
+  if (p->expansion_num > 65535 || p->expansion_den > 65535)
+    return fail(KNNG_ERR_INVALID_ARG, "expansion num/den must be <= 65535");
   return 0;
 }
 

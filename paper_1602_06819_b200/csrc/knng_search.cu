@@ -44,8 +44,10 @@ __device__ __forceinline__ void produce(const SearchArgs &a, const VecQuery<M, L
     const uint64_t idx = rng_index(h3, (uint64_t)(c * 32 + lane), (uint64_t)m);
     const int32_t node = pool ? pool[idx] : (int32_t)idx;
     const uint32_t key = Q.eval(a.vec, a.stride, a.nchunks, node, 32);
+    // a repeat of an earlier draw of the same chunk can never be fresh (Q4): flag it (bit 31)
+    const bool dup = (__ffs(__match_any_sync(FULL, node)) - 1) != lane;
     volatile int *rs = (volatile int *)(ring + (c % RING_CHUNKS) * 32 + lane);
-    rs[0] = node;
+    rs[0] = dup ? (int)(0x80000000u | (uint32_t)node) : node;
     rs[1] = (int)key;
     __threadfence_block();
     __syncwarp();
@@ -95,7 +97,9 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
     const int64_t lo = m < a.kr ? m : a.kr;
     if (budget < lo) budget = lo;
     if (budget > m) budget = m;
-    const int64_t nch = a.starts ? 0 : (budget + 31) / 32;   // chunks the producers evaluate
+    // chunks the producers may evaluate: they run until the consumer is done (redraws push the
+    // consumed draws past the budget), capped for degenerate cases (speedup ~ 1)
+    const int64_t nch = a.starts ? 0 : (8 * budget + 31) / 32 + 8;
 
     VecQuery<M, L, CPL> Q;
     Q.load(a.qbase + (size_t)b * a.stride, a.nchunks);
@@ -111,7 +115,10 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
     int64_t c = 0, jbase = 0;
     int32_t wnode = -1;
     uint32_t wkey = 0, wl = 0;
-    bool whave = false, wpf = false;
+    bool whave = false, wpf = false, wdup = false;
+    SkipThr<M> thr;              // skip rule prepared against the current best key
+    uint32_t thr_key = 0;
+    bool thr_ok = false;
     int wpos = 32;
 
     const long long tc0 = a.prof ? clock64() : 0;
@@ -129,7 +136,9 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
           ++p_win;
           __threadfence_block();
           const volatile int *rs = (const volatile int *)(ring + slot * 32 + lane);
-          wnode = rs[0];
+          const int w0 = rs[0];
+          wnode = w0 & 0x7FFFFFFF;
+          wdup = w0 < 0;
           wkey = (uint32_t)rs[1];
           whave = true;
           __syncwarp();
@@ -142,6 +151,7 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
             wnode = pool ? pool[idx] : (int32_t)idx;
           }
           whave = false;
+          wdup = false;
         }
         wl = wnode >= 0 ? (a.P > 0 ? (uint32_t)a.local_idx[wnode] : (uint32_t)wnode) : 0u;
         jbase += 32;
@@ -150,7 +160,12 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
         // tightens as s_max improves, so "passes against the current best" is a superset
         wpf = false;
         if (whave && wnode >= 0) {
-          wpf = top.cnt == 0 ? lane == 0 : !skip_start<M>(wkey, top.key_at0, a.e_num, a.e_den);
+          if (top.cnt > 0 && (!thr_ok || thr_key != top.key_at0)) {
+            thr.set(top.key_at0, a.e_num, a.e_den);
+            thr_key = top.key_at0;
+            thr_ok = true;
+          }
+          wpf = top.cnt == 0 ? lane == 0 : !thr.skip(wkey);
           if (__ballot_sync(FULL, wpf)) {
             cp_async_wait_all();      // older copies into rowbuf2 must land first
             if (wpf)
@@ -162,8 +177,13 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
       const unsigned invm = __ballot_sync(FULL, wnode < 0) & active;
       const unsigned lim = invm ? ((1u << (__ffs(invm) - 1)) - 1u) : FULL;
       const bool evb = wnode >= 0 ? bit_get(ev, wl) : true;
-      const unsigned same = __match_any_sync(FULL, wnode) & active;
-      const bool fresh = lane >= wpos && !evb && (__ffs(same) - 1) == lane;   // redraws are free (Q4)
+      bool fresh;
+      if (__all_sync(FULL, whave)) {     // produced window: repeats are flagged by the producer
+        fresh = lane >= wpos && !evb && !wdup;
+      } else {
+        const unsigned same = __match_any_sync(FULL, wnode) & active;
+        fresh = lane >= wpos && !evb && (__ffs(same) - 1) == lane;   // redraws are free (Q4)
+      }
       const unsigned fm = __ballot_sync(FULL, fresh) & active & lim;
       if (fm == 0) {
         if (invm) break;          // injected start sequence exhausted
@@ -190,7 +210,12 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
       if ((int64_t)__popc(cm) > budget - c) cm = first_bits(cm, (int)(budget - c));
       const bool inc = (cm >> lane) & 1u;
       unsigned am;
-      if (top.cnt > 0 && __ballot_sync(FULL, inc && !skip_start<M>(wkey, top.key_at0, a.e_num, a.e_den)) == 0) {
+      if (top.cnt > 0 && (!thr_ok || thr_key != top.key_at0)) {
+        thr.set(top.key_at0, a.e_num, a.e_den);
+        thr_key = top.key_at0;
+        thr_ok = true;
+      }
+      if (top.cnt > 0 && __ballot_sync(FULL, inc && !thr.skip(wkey)) == 0) {
         am = 0;   // every committable draw is skipped even against the current s_max
       } else {
       // s_max before each draw: best of top-k and of the earlier committed draws
