@@ -216,6 +216,11 @@ def run_ours(args, cfg):
     peak, peak_src = hbm_peak()
     achieved = bytes_search / (ms_search / 1000.0) / 1e9
     launches = sum(s["kernel_launches"] for s in stats)
+    traffic = None       # DRAM bytes per launch of k_search from the committed ncu --set full capture
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "k_search_ncu.json")))["dram_bytes_per_launch"]
+    except Exception:
+        pass
 
     # recall@k of the inserted points' rows vs the exact k-nn over the final point set (sampled, torch)
     ids, keys = g.rows(cfg.n0, pos)
@@ -261,7 +266,7 @@ def run_ours(args, cfg):
                              ("search_evals", "search_starts", "search_skipped", "search_expansions", "ball_nodes",
                               "proposals")},
         "roofline": {"bound": "hbm", "kernel": "k_search (K1 iGNNS)", "achieved": achieved, "peak": peak,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": bytes_search / len(stats),
                      "ms_per_launch": ms_search / len(stats),
                      "note": "C1 is L2-resident (14 MB store): HBM fraction is not the binding claim"},
@@ -273,7 +278,8 @@ def run_ours(args, cfg):
         "clocks": clk.summary(),
     }
     if rows0 is not None:
-        line["cpu_baseline"] = run_cpu_baseline(cfg, X, S, rows0)
+        S_cpu = D.stream_points(cfg, 0, 48 * B)      # enough whole batches for ~10 s of oracle work
+        line["cpu_baseline"] = run_cpu_baseline(cfg, X, S_cpu, rows0)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
