@@ -24,74 +24,24 @@
 #include "knng_common.cuh"
 #include "knng_internal.h"
 
+#include "knng_handle.h"
+
 using namespace knng;
 
-static thread_local std::string g_err;
+std::string &knng_err_slot() {
+  static thread_local std::string e;
+  return e;
+}
 
-static int fail(int code, const char *fmt, ...) {
+int knng_fail(int code, const char *fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(buf, sizeof buf, fmt, ap);
   va_end(ap);
-  g_err = buf;
+  knng_err_slot() = buf;
   return code;
 }
-
-#define CK(x)                                                                                   \
-  do {                                                                                          \
-    cudaError_t e_ = (x);                                                                       \
-    if (e_ != cudaSuccess)                                                                      \
-      return fail(e_ == cudaErrorMemoryAllocation ? KNNG_ERR_OOM : KNNG_ERR_CUDA, "%s: %s (%s:%d)", \
-                  #x, cudaGetErrorString(e_), __FILE__, __LINE__);                              \
-  } while (0)
-
-struct DBuf {
-  void *p = nullptr;
-  size_t bytes = 0;
-  cudaError_t ensure(size_t need) {
-    if (need <= bytes) return cudaSuccess;
-    need += need / 4;             // grow geometrically: batches grow the pool a little each time
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMalloc(&p, need);
-    if (e == cudaSuccess) bytes = need;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  template <class T>
-  T *as() const { return (T *)p; }
-};
-
-struct knng_graph {
-  int metric = 0, dim = 0, k = 0;
-  int64_t n = 0, cap = 0;
-  VecGeom geom{};
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  uint8_t *vec = nullptr;
-  int32_t *ids = nullptr;
-  uint32_t *keys = nullptr;
-  int32_t *ncnt = nullptr, *nfill = nullptr, *noff = nullptr, *scan_tmp = nullptr;
-  // partitions
-  int P = 0;
-  uint8_t *part_of = nullptr;
-  int32_t *local_idx = nullptr;
-  int32_t *members = nullptr;
-  int64_t *member_cnt = nullptr;
-  int32_t *medoids = nullptr;
-  std::vector<int32_t> h_medoids;
-  // workspaces
-  DBuf w_bits, w_cand_i, w_cand_k, w_C_i, w_C_k, w_hash, w_list, w_props, w_prop_cnt, w_sorted, w_stats,
-      w_target, w_query, w_starts;
-  cudaEvent_t ev[6] = {};
-};
 
 static int elem_bytes(int metric) { return metric == KNNG_L2SQ_U8 ? 1 : 4; }
 
@@ -155,14 +105,14 @@ static void free_graph(knng_graph *g) {
 
 extern "C" {
 
-const char *graph_last_error(void) { return g_err.c_str(); }
+const char *graph_last_error(void) { return knng_err_slot().c_str(); }
 
 int64_t graph_size(const knng_graph *g) { return g ? g->n : -1; }
 int32_t graph_degree(const knng_graph *g) { return g ? g->k : -1; }
 void graph_free(knng_graph *g) { free_graph(g); }
 
 int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_graph **out) {
-  g_err.clear();
+  knng_err_slot().clear();
   if (!out) return fail(KNNG_ERR_INVALID_ARG, "graph_init: null out");
   *out = nullptr;
   if (int r = check_points(pts, "graph_init")) return r;
@@ -348,7 +298,7 @@ static void fill_stats(knng_graph *g, knng_stats *st, const unsigned long long *
 
 int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,
                        knng_stats *st) {
-  g_err.clear();
+  knng_err_slot().clear();
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: null graph");
   if (int r = check_points(pts, "graph_insert_batch")) return r;
   if (int r = check_params(p)) return r;
@@ -448,7 +398,7 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
 
 int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_params *p, int32_t *ids_out,
                  uint32_t *keys_out, int32_t out_on_device, knng_stats *st) {
-  g_err.clear();
+  knng_err_slot().clear();
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_search: null graph");
   if (int r = check_points(q, "graph_search")) return r;
   if (int r = check_params(p)) return r;
@@ -499,7 +449,7 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
 }
 
 int graph_get_rows(const knng_graph *g, int64_t first, int64_t count, int32_t *ids, uint32_t *keys) {
-  g_err.clear();
+  knng_err_slot().clear();
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_get_rows: null graph");
   if (first < 0 || count < 0 || first + count > g->n) return fail(KNNG_ERR_INVALID_ARG, "graph_get_rows: bad range");
   CK(cudaSetDevice(g->device));
@@ -511,7 +461,7 @@ int graph_get_rows(const knng_graph *g, int64_t first, int64_t count, int32_t *i
 }
 
 int graph_get_partition(const knng_graph *g, uint8_t *part, int32_t *medoids, int32_t *P_out) {
-  g_err.clear();
+  knng_err_slot().clear();
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_get_partition: null graph");
   if (P_out) *P_out = g->P;
   if (g->P == 0) return KNNG_OK;

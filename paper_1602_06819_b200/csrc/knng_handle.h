@@ -1,0 +1,70 @@
+// knng_handle.h -- the graph handle and host helpers shared by the C-ABI implementation files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/knng.h"
+#include "knng_internal.h"
+
+std::string &knng_err_slot();
+int knng_fail(int code, const char *fmt, ...);
+#define fail knng_fail
+
+#define CK(x)                                                                                       \
+  do {                                                                                              \
+    cudaError_t e_ = (x);                                                                           \
+    if (e_ != cudaSuccess)                                                                          \
+      return fail(e_ == cudaErrorMemoryAllocation ? KNNG_ERR_OOM : KNNG_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #x, cudaGetErrorString(e_), __FILE__, __LINE__);                                  \
+  } while (0)
+
+struct DBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    need += need / 4;             // grow geometrically: batches grow the pool a little each time
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T *as() const { return (T *)p; }
+};
+
+struct knng_graph {
+  int metric = 0, dim = 0, k = 0;
+  int64_t n = 0, cap = 0;
+  knng::VecGeom geom{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint8_t *vec = nullptr;
+  int32_t *ids = nullptr;
+  uint32_t *keys = nullptr;
+  int32_t *ncnt = nullptr, *nfill = nullptr, *noff = nullptr, *scan_tmp = nullptr;
+  // partitions
+  int P = 0;
+  uint8_t *part_of = nullptr;
+  int32_t *local_idx = nullptr;
+  int32_t *members = nullptr;
+  int64_t *member_cnt = nullptr;
+  int32_t *medoids = nullptr;
+  std::vector<int32_t> h_medoids;
+  // workspaces
+  DBuf w_bits, w_cand_i, w_cand_k, w_C_i, w_C_k, w_hash, w_list, w_props, w_prop_cnt, w_sorted, w_stats,
+      w_target, w_query, w_starts;
+  cudaEvent_t ev[6] = {};
+};

@@ -237,6 +237,15 @@ __global__ void k_scan_add(int32_t *out, const int32_t *blocksum, int64_t n) {
   if (i < n) out[i] += blocksum[blockIdx.x];
 }
 
+cudaError_t exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t *tmp, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t nb = (n + 1023) / 1024;
+  k_scan_block<<<(unsigned)nb, 1024, 0, s>>>(in, out, tmp, n);
+  k_scan_sums<<<1, 1024, 0, s>>>(tmp, nb);
+  k_scan_add<<<(unsigned)nb, 1024, 0, s>>>(out, tmp, n);
+  return cudaGetLastError();
+}
+
 __global__ void k_prop_scatter(const int2 *props, const int32_t *prop_cnt, int ballmax, int64_t B, int64_t n_t,
                                const int32_t *noff, int32_t *nfill, int2 *sorted) {
   const int64_t b = blockIdx.x;

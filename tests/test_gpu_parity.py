@@ -241,3 +241,71 @@ def test_C1_full_size_sampled():
     for i in range(0, cfg.batch, 97):
         D_peers = sorted((O.key(cfg.metric, S[i], S[j]), cfg.n0 + j) for j in range(cfg.batch) if j != i)
         assert int(gk[cfg.n0 + i, -1]) <= D_peers[cfg.k - 1][0]
+
+
+# ---------------------------------------------------------------------------
+# A9 partition_kmedoids, A4 partitioned search (Alg. 3), A8 placement (Alg. 5)
+# ---------------------------------------------------------------------------
+def test_partition_w7_hand_trace():
+    X = D.line_points([0, 1, 2, 3, 10, 11, 12, 13])
+    g = _graph(X, 2, 16)
+    part, med, cost = g.partition_kmedoids(2, 1.0, 10, 0, init_medoids=[1, 5])
+    assert part.tolist() == [0, 0, 0, 0, 1, 1, 1, 1]
+    assert med.tolist() == [1, 5] and cost.tolist() == [6]
+    p2, m2 = g.partition()
+    assert p2.tolist() == part.tolist() and m2.tolist() == [1, 5]
+
+
+@pytest.mark.parametrize("name,n0,P,imb", [("C3", 3000, 2, 1.0), ("C3", 5000, 8, 1.05), ("C2", 4000, 4, 1.1),
+                                           ("C3", 12000, 2, 1.05), ("C0", 2000, 8, 1.05)])
+def test_partition_matches_oracle(name, n0, P, imb):
+    cfg = _cfg_small(name, n0=n0)
+    X = D.initial_points(cfg)
+    g = _graph(X, cfg.k)
+    o = O.OracleGraph(cfg.metric, X, cfg.k)
+    o.init_exact()
+    gp, gm, gc = g.partition_kmedoids(P, imb, 6, cfg.part_seed)
+    op, om, oc = o.partition_kmedoids(P, imb, 6, cfg.part_seed)
+    assert gm.tolist() == om.tolist() and gc.tolist() == oc.tolist()
+    assert (gp == op).all()
+    assert np.bincount(gp, minlength=P).max() <= math.ceil(n0 * imb / P)
+
+
+def test_partitioned_search_and_stream_C3_shape():
+    cfg = _cfg_small("C3", n0=20000, n_insert=2200)
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    Q = D.query_points(cfg, 200)
+    cap = cfg.n0 + cfg.n_insert + 8
+    g = _graph(X, cfg.k, cap)
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cap)
+    o.init_exact()
+    gp, gm, _ = g.partition_kmedoids(cfg.P, cfg.imbalance, 4, cfg.part_seed)
+    op, om, _ = o.partition_kmedoids(cfg.P, cfg.imbalance, 4, cfg.part_seed)
+    assert (gp == op).all() and gm.tolist() == om.tolist()
+    o.set_partition(op, om)
+    gi, gk, gst = g.search(Q, cfg.k, cfg.speedup, cfg.e_num, cfg.e_den, cfg.search_seed)
+    oi, ok, ost = o.search(Q, cfg.k, cfg.speedup, cfg.e_num, cfg.e_den, cfg.search_seed)
+    _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "partitioned search")
+    assert gst["search_evals"] == ost[:, 0].sum() and gst["search_expansions"] == ost[:, 3].sum()
+    pos = 0
+    for B in (1024, 1024, 152):
+        g.insert_batch(S[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        o.insert_batch(S[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        pos += B
+        gi, gk = g.rows()
+        oi, ok = o.rows()
+        _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "partitioned stream after %d" % pos)
+        gpart, _ = g.partition()
+        assert (gpart == o.part_of[:o.n]).all()
+
+
+def test_partition_errors():
+    from paper_1602_06819_b200 import KnngError
+    g = _graph(np.random.default_rng(0).integers(0, 255, (100, 4)).astype(np.uint8), 3)
+    with pytest.raises(KnngError):
+        g.partition_kmedoids(0, 1.0, 3, 0)
+    with pytest.raises(KnngError):
+        g.partition_kmedoids(300, 1.0, 3, 0)
+    with pytest.raises(KnngError):
+        g.partition_kmedoids(4, 0.5, 3, 0)
