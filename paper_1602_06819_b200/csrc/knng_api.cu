@@ -46,6 +46,14 @@ int knng_fail(int code, const char *fmt, ...) {
 static int elem_bytes(int metric) { return metric == KNNG_L2SQ_U8 ? 1 : 4; }
 
 static int geom_for(int metric, int dim, VecGeom *g) {
+  if (metric == KNNG_JACCARD_U32SET) {   // sets: L = 8 lanes per candidate in the warp evaluator
+    g->metric = metric;
+    g->nchunks = 0;
+    g->stride = 0;
+    g->L = 8;
+    g->CPL = 1;
+    return 0;
+  }
   const size_t row = (size_t)dim * elem_bytes(metric);
   const int C = (int)((row + 15) / 16);
   g->metric = metric;
@@ -68,12 +76,12 @@ static int geom_for(int metric, int dim, VecGeom *g) {
 
 static int check_points(const knng_points *p, const char *what) {
   if (!p) return fail(KNNG_ERR_INVALID_ARG, "%s: null points", what);
-  if (p->metric == KNNG_JACCARD_U32SET)
-    return fail(KNNG_ERR_INVALID_ARG, "%s: Jaccard sets are not supported by this build yet", what);
-  if (p->metric != KNNG_L2SQ_U8 && p->metric != KNNG_L2SQ_F32) return fail(KNNG_ERR_INVALID_ARG, "%s: bad metric %d", what, p->metric);
-  if (p->dim < 1) return fail(KNNG_ERR_INVALID_ARG, "%s: dim < 1", what);
+  if (p->metric != KNNG_L2SQ_U8 && p->metric != KNNG_L2SQ_F32 && p->metric != KNNG_JACCARD_U32SET)
+    return fail(KNNG_ERR_INVALID_ARG, "%s: bad metric %d", what, p->metric);
+  if (p->metric != KNNG_JACCARD_U32SET && p->dim < 1) return fail(KNNG_ERR_INVALID_ARG, "%s: dim < 1", what);
   if (p->n < 0) return fail(KNNG_ERR_INVALID_ARG, "%s: n < 0", what);
   if (p->n > 0 && !p->data) return fail(KNNG_ERR_INVALID_ARG, "%s: null data", what);
+  if (p->metric == KNNG_JACCARD_U32SET && !p->offsets) return fail(KNNG_ERR_INVALID_ARG, "%s: null offsets", what);
   return 0;
 }
 
@@ -86,16 +94,77 @@ static int copy_rows(knng_graph *g, uint8_t *dst, const knng_points *p) {
   return 0;
 }
 
+__global__ void k_rebase_offsets(const uint64_t *in, int64_t n, uint64_t base, uint64_t *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= n) out[i] = base + (in[i] - in[0]);
+}
+
+// append n sets (CSR, host or device) to a token/offset store: off[row0 .. row0+n] and
+// tok[tok_n ..]; grows the token buffer geometrically.  Returns the tokens appended.
+static int append_sets(knng_graph *g, const knng_points *p, uint64_t **off_dst_base, uint32_t **tok_buf,
+                       int64_t *tok_cap, int64_t row0, int64_t tok0, int64_t *ntok_out) {
+  uint64_t first = 0, last = 0;
+  if (p->data_on_device) {
+    CK(cudaMemcpyAsync(&first, p->offsets, 8, cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaMemcpyAsync(&last, p->offsets + p->n, 8, cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+  } else {
+    first = p->offsets[0];
+    last = p->offsets[p->n];
+    for (int64_t i = 0; i < p->n; ++i)
+      if (p->offsets[i + 1] - p->offsets[i] > 65535) return fail(KNNG_ERR_INVALID_ARG, "set longer than 65535");
+  }
+  const int64_t nt = (int64_t)(last - first);
+  if (tok0 + nt > *tok_cap) {
+    const int64_t ncap = std::max<int64_t>(tok0 + nt, *tok_cap + *tok_cap / 2) + 1024;
+    uint32_t *nb = nullptr;
+    CK(cudaMalloc((void **)&nb, (size_t)ncap * 4));
+    if (*tok_buf && tok0 > 0) CK(cudaMemcpyAsync(nb, *tok_buf, (size_t)tok0 * 4, cudaMemcpyDeviceToDevice, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    if (*tok_buf) cudaFree(*tok_buf);
+    *tok_buf = nb;
+    *tok_cap = ncap;
+  }
+  if (nt > 0)
+    CK(cudaMemcpyAsync(*tok_buf + tok0, (const uint32_t *)p->data + first, (size_t)nt * 4,
+                       p->data_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->stream));
+  // offsets rebased to tok0
+  uint64_t *dst = *off_dst_base + row0;
+  if (p->data_on_device) {
+    k_rebase_offsets<<<(unsigned)((p->n + 256) / 256), 256, 0, g->stream>>>(p->offsets, p->n, (uint64_t)tok0, dst);
+    CK(cudaGetLastError());
+  } else {
+    std::vector<uint64_t> h((size_t)p->n + 1);
+    for (int64_t i = 0; i <= p->n; ++i) h[i] = (uint64_t)tok0 + (p->offsets[i] - first);
+    CK(cudaMemcpyAsync(dst, h.data(), h.size() * 8, cudaMemcpyHostToDevice, g->stream));
+    CK(cudaStreamSynchronize(g->stream));   // h is a local buffer
+  }
+  *ntok_out = nt;
+  return 0;
+}
+
+// store the batch's points at rows [row0, row0+n) of the graph's store
+static int store_points(knng_graph *g, const knng_points *p, int64_t row0) {
+  if (g->metric == KNNG_JACCARD_U32SET) {
+    int64_t nt = 0;
+    if (int r = append_sets(g, p, &g->off, &g->tok, &g->tok_cap, row0, g->tok_n, &nt)) return r;
+    g->tok_n += nt;
+    return 0;
+  }
+  return copy_rows(g, g->vec + (size_t)row0 * g->geom.stride, p);
+}
+
 static void free_graph(knng_graph *g) {
   if (!g) return;
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
   void *bufs[] = {g->vec, g->ids, g->keys, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->part_of, g->local_idx,
-                  g->members, g->member_cnt, g->medoids};
+                  g->members, g->member_cnt, g->medoids, g->off, g->tok};
   for (void *b : bufs)
     if (b) cudaFree(b);
   DBuf *ws[] = {&g->w_bits, &g->w_cand_i, &g->w_cand_k, &g->w_C_i, &g->w_C_k, &g->w_hash, &g->w_list, &g->w_props,
-                &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts};
+                &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts,
+                &g->w_qoff, &g->w_qtok};
   for (DBuf *b : ws) b->release();
   for (auto &e : g->ev)
     if (e) cudaEventDestroy(e);
@@ -160,7 +229,11 @@ int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_g
       return bail(KNNG_ERR_OOM);                                  \
     }                                                             \
   } while (0)
-  A(g->vec, cap * g->geom.stride);
+  if (g->metric == KNNG_JACCARD_U32SET) {
+    A(g->off, (cap + 1) * 8);
+  } else {
+    A(g->vec, cap * g->geom.stride);
+  }
   A(g->ids, cap * k * 4);
   A(g->keys, cap * k * 4);
   A(g->ncnt, cap * 4);
@@ -170,12 +243,12 @@ int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_g
 #undef A
   for (auto &e : g->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(KNNG_ERR_CUDA, "event create failed"));
-  if (cudaMemsetAsync(g->vec, 0, cap * g->geom.stride, g->stream) != cudaSuccess ||
+  if ((g->vec && cudaMemsetAsync(g->vec, 0, cap * g->geom.stride, g->stream) != cudaSuccess) ||
       cudaMemsetAsync(g->ncnt, 0, cap * 4, g->stream) != cudaSuccess ||
       cudaMemsetAsync(g->nfill, 0, cap * 4, g->stream) != cudaSuccess)
     return bail(fail(KNNG_ERR_CUDA, "graph_init: memset failed"));
-  if ((r = copy_rows(g, g->vec, pts))) return bail(r);
-  cudaError_t e = launch_exact_build(g->geom, g->vec, g->n, k, g->ids, g->keys, g->stream);
+  if ((r = store_points(g, pts, 0))) return bail(r);
+  cudaError_t e = launch_exact_build(g->geom, graph_store_view(g), g->n, k, g->ids, g->keys, g->stream);
   if (e != cudaSuccess) return bail(fail(KNNG_ERR_CUDA, "exact build launch: %s", cudaGetErrorString(e)));
   e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return bail(fail(KNNG_ERR_CUDA, "exact build: %s", cudaGetErrorString(e)));
@@ -217,7 +290,7 @@ static int64_t max_pool(knng_graph *g) {
   return m;
 }
 
-static int run_search_phase(knng_graph *g, const uint8_t *qbase, int64_t nq, int64_t pid_base, int kr,
+static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, int64_t nq, int64_t pid_base, int kr,
                             const knng_params *p, const int32_t *d_starts, int nstarts, int32_t *out_i,
                             uint32_t *out_k, int *nl) {
   const int Pn = g->P > 0 ? g->P : 1;
@@ -235,13 +308,12 @@ static int run_search_phase(knng_graph *g, const uint8_t *qbase, int64_t nq, int
   }
   SearchArgs a;
   memset(&a, 0, sizeof a);
-  a.vec = g->vec;
-  a.stride = g->geom.stride;
-  a.nchunks = g->geom.nchunks;
+  a.st = graph_store_view(g);
+  a.qs = qs;
+  a.qrow0 = qrow0;
   a.rows = g->ids;
   a.k = g->k;
   a.n_t = g->n;
-  a.qbase = qbase;
   a.nq = nq;
   a.pid_base = pid_base;
   a.P = g->P;
@@ -320,7 +392,8 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   int nl = 0;
   CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
   // A1: batch ingest into the store tail (ids n_t .. n_t+B-1)
-  if (int r = copy_rows(g, g->vec + (size_t)n_t * g->geom.stride, pts)) return r;
+  if (int r = store_points(g, pts, n_t)) return r;
+  const StoreView sv = graph_store_view(g);
   // ball bound k + k^2 + ... + k^DEPTH, at most n_t
   int64_t ballmax = 0, pw = 1;
   for (int d = 1; d <= p->depth && ballmax < n_t; ++d) {
@@ -342,21 +415,19 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
 
   CK(cudaEventRecord(g->ev[0], g->stream));
   // A2-A4: iGNNS per (point, partition) on the snapshot + partition merge
-  if (int r = run_search_phase(g, g->vec + (size_t)n_t * g->geom.stride, B, n_t, k, p, nullptr, 0,
+  if (int r = run_search_phase(g, sv, n_t, B, n_t, k, p, nullptr, 0,
                                g->w_C_i.as<int32_t>(), g->w_C_k.as<uint32_t>(), &nl))
     return r;
   CK(cudaEventRecord(g->ev[1], g->stream));
   // A5: intra-batch all-pairs -> new rows n_t .. n_t+B-1
-  CK(launch_allpairs(g->geom, g->vec, g->ids, g->keys, k, n_t, B, g->w_C_i.as<int32_t>(), g->w_C_k.as<uint32_t>(),
+  CK(launch_allpairs(g->geom, sv, g->ids, g->keys, k, n_t, B, g->w_C_i.as<int32_t>(), g->w_C_k.as<uint32_t>(),
                      g->stream));
   ++nl;
   CK(cudaEventRecord(g->ev[2], g->stream));
   // A6: update balls over the snapshot -> proposals
   BallArgs ba;
   memset(&ba, 0, sizeof ba);
-  ba.vec = g->vec;
-  ba.stride = g->geom.stride;
-  ba.nchunks = g->geom.nchunks;
+  ba.st = sv;
   ba.ids = g->ids;
   ba.keys = g->keys;
   ba.k = k;
@@ -379,7 +450,7 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
                         (int)ballmax, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->w_sorted.as<int2>(), g->stream, &nl));
   // A8: placement at the nearest medoid
   if (g->P > 0) {
-    CK(launch_place(g->geom, g->vec, n_t, B, g->P, g->medoids, g->members, g->cap, g->member_cnt, g->part_of,
+    CK(launch_place(g->geom, sv, n_t, B, g->P, g->medoids, g->members, g->cap, g->member_cnt, g->part_of,
                     g->local_idx, g->w_target.as<int32_t>(), g->stream));
     nl += 2;
   }
@@ -414,9 +485,26 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
   }
   int nl = 0;
   CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
-  CK(g->w_query.ensure((size_t)nq * g->geom.stride));
-  CK(cudaMemsetAsync(g->w_query.p, 0, (size_t)nq * g->geom.stride, g->stream));
-  if (int r = copy_rows(g, g->w_query.as<uint8_t>(), q)) return r;
+  StoreView qs = graph_store_view(g);
+  if (g->metric == KNNG_JACCARD_U32SET) {
+    CK(g->w_qoff.ensure((size_t)(nq + 1) * 8));
+    uint32_t *qt = g->w_qtok.as<uint32_t>();
+    int64_t qcap = (int64_t)(g->w_qtok.bytes / 4), ntok = 0;
+    uint64_t *qo = g->w_qoff.as<uint64_t>();
+    if (int r = append_sets(g, q, &qo, &qt, &qcap, 0, 0, &ntok)) return r;
+    if (qt != g->w_qtok.p) {   // append_sets reallocated the token buffer
+      g->w_qtok.release();
+      g->w_qtok.p = qt;
+      g->w_qtok.bytes = (size_t)qcap * 4;
+    }
+    qs.off = g->w_qoff.as<uint64_t>();
+    qs.tok = g->w_qtok.as<uint32_t>();
+  } else {
+    CK(g->w_query.ensure((size_t)nq * g->geom.stride));
+    CK(cudaMemsetAsync(g->w_query.p, 0, (size_t)nq * g->geom.stride, g->stream));
+    if (int r = copy_rows(g, g->w_query.as<uint8_t>(), q)) return r;
+    qs.vec = g->w_query.as<uint8_t>();
+  }
   const int32_t *d_starts = nullptr;
   int nstarts = 0;
   if (p->start_override && p->start_override_len > 0) {
@@ -434,7 +522,7 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
     ok = g->w_C_k.as<uint32_t>();
   }
   CK(cudaEventRecord(g->ev[0], g->stream));
-  if (int r = run_search_phase(g, g->w_query.as<uint8_t>(), nq, 0, kr, p, d_starts, nstarts, oi, ok, &nl)) return r;
+  if (int r = run_search_phase(g, qs, 0, nq, 0, kr, p, d_starts, nstarts, oi, ok, &nl)) return r;
   CK(cudaEventRecord(g->ev[1], g->stream));
   if (!out_on_device) {
     CK(cudaMemcpyAsync(ids_out, oi, (size_t)nq * kr * 4, cudaMemcpyDeviceToHost, g->stream));

@@ -57,8 +57,32 @@ __global__ void __launch_bounds__(256) k_exact_build(const uint8_t *__restrict__
   }
 }
 
-cudaError_t launch_exact_build(const VecGeom &g, const uint8_t *vec, int64_t n, int k, int32_t *ids, uint32_t *keys,
+// Jaccard sets: warp per row, lanes over all columns (single-thread sorted-list intersection).
+__global__ void __launch_bounds__(128) k_exact_build_sets(StoreView st, int64_t n, int k, int32_t *ids, uint32_t *keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  WarpTopK<M_JAC> top;
+  top.init(k);
+  for (int64_t c0 = 0; c0 < n; c0 += 32) {
+    const int64_t col = c0 + lane;
+    const bool valid = col < n && col != row;
+    const uint32_t key = valid ? pair_key<M_JAC>(st, row, col) : 0u;
+    top.insert(valid, key, (int32_t)col);
+  }
+  if (lane < k) {
+    ids[(size_t)row * k + lane] = lane < top.cnt ? top.id : -1;
+    keys[(size_t)row * k + lane] = lane < top.cnt ? top.key : 0u;
+  }
+}
+
+cudaError_t launch_exact_build(const VecGeom &g, const StoreView &st, int64_t n, int k, int32_t *ids, uint32_t *keys,
                                cudaStream_t s) {
+  if (g.metric == M_JAC) {
+    k_exact_build_sets<<<(unsigned)((n + 3) / 4), 128, 0, s>>>(st, n, k, ids, keys);
+    return cudaGetLastError();
+  }
+  const uint8_t *vec = st.vec;
   const size_t smem = (size_t)128 * (g.nchunks + 1) * 16;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   const unsigned blocks = (unsigned)((n + 63) / 64);

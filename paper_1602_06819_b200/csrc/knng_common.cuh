@@ -216,6 +216,38 @@ __device__ __forceinline__ uint32_t thread_dist(const uint4 *a, const uint4 *b, 
   }
 }
 
+// Where the points live: vector rows (stride bytes, zero padded) or Jaccard sets in CSR.
+struct StoreView {
+  const uint8_t *vec;
+  size_t stride;
+  int nchunks;
+  const uint64_t *off;   // sets: [n+1]
+  const uint32_t *tok;   // sets: sorted, unique tokens
+};
+
+// Single-thread Jaccard key of two sorted token lists: (|A n B| << 16) | |A u B|.
+__device__ __forceinline__ uint32_t set_key(const uint32_t *a, int la, const uint32_t *b, int lb) {
+  int i = 0, j = 0, inter = 0;
+  while (i < la && j < lb) {
+    const uint32_t x = a[i], y = b[j];
+    inter += x == y;
+    i += x <= y;
+    j += y <= x;
+  }
+  return ((uint32_t)inter << 16) | (uint32_t)(la + lb - inter);
+}
+
+// Key of rows i and j of a store (single thread).
+template <int M>
+__device__ __forceinline__ uint32_t pair_key(const StoreView &s, int64_t i, int64_t j) {
+  if (M == M_JAC) {
+    const uint64_t ai = s.off[i], bi = s.off[j];
+    return set_key(s.tok + ai, (int)(s.off[i + 1] - ai), s.tok + bi, (int)(s.off[j + 1] - bi));
+  }
+  return thread_dist<M>((const uint4 *)(s.vec + (size_t)i * s.stride), (const uint4 *)(s.vec + (size_t)j * s.stride),
+                        s.nchunks);
+}
+
 // Warp-cooperative evaluation of up to 32 candidates against a query held in registers.
 // L lanes per vector (power of 2), CPL chunks per lane: lane sl of a group owns chunks
 // sl, sl+L, ..., (CPL of them).  32/L vectors per pass; GRP passes have their loads in flight
@@ -226,7 +258,9 @@ struct VecQuery {
   static constexpr int GRP = (L < (8 / CPL) ? L : ((8 / CPL) > 0 ? (8 / CPL) : 1));
   uint4 q[CPL];
 
-  __device__ __forceinline__ void load(const uint8_t *row, int nchunks) {
+  __device__ __forceinline__ void load(const StoreView &s, int64_t r, uint32_t * /*scratch*/) {
+    const uint8_t *row = s.vec + (size_t)r * s.stride;
+    const int nchunks = s.nchunks;
     const int sl = (threadIdx.x & 31) % L;
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
@@ -255,8 +289,10 @@ struct VecQuery {
 
   // cand: id held by lane j for candidate j < n (id < 0: skipped, key undefined).
   // Returns the key of candidate j in lane j.
-  __device__ __forceinline__ uint32_t eval(const uint8_t *__restrict__ base, size_t stride, int nchunks,
-                                           int32_t cand, int n) const {
+  __device__ __forceinline__ uint32_t eval(const StoreView &s, int32_t cand, int n) const {
+    const uint8_t *__restrict__ base = s.vec;
+    const size_t stride = s.stride;
+    const int nchunks = s.nchunks;
     const int lane = threadIdx.x & 31, sub = lane / L, sl = lane % L;
     uint32_t out = 0;
     const int np = (n + VPP - 1) / VPP;
@@ -286,5 +322,66 @@ struct VecQuery {
     return out;
   }
 };
+
+// Jaccard sets: the query's sorted tokens in per-warp shared scratch (global when longer than
+// QMAX); L lanes per candidate each take every L-th candidate token and binary-search it in the
+// query; intersections are summed over the L lanes.
+constexpr int QMAX = 256;
+template <int L>
+struct SetQuery {
+  static constexpr int VPP = 32 / L;
+  const uint32_t *q;
+  int qn;
+
+  __device__ __forceinline__ void load(const StoreView &s, int64_t r, uint32_t *scratch) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t b = s.off[r];
+    qn = (int)(s.off[r + 1] - b);
+    if (qn <= QMAX && scratch) {
+      for (int i = lane; i < qn; i += 32) scratch[i] = s.tok[b + i];
+      __syncwarp();
+      q = scratch;
+    } else {
+      q = s.tok + b;
+    }
+  }
+
+  __device__ __forceinline__ int has(uint32_t t) const {
+    int lo = 0, hi = qn;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (q[mid] < t) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo < qn && q[lo] == t;
+  }
+
+  __device__ __forceinline__ uint32_t eval(const StoreView &s, int32_t cand, int n) const {
+    const int lane = threadIdx.x & 31, sub = lane / L, sl = lane % L;
+    uint32_t out = 0;
+    const int np = (n + VPP - 1) / VPP;
+    for (int p = 0; p < np; ++p) {
+      const int v = p * VPP + sub;
+      const int32_t id = __shfl_sync(FULL, cand, v & 31);
+      int inter = 0, cl = 0;
+      if (v < n && id >= 0) {
+        const uint64_t b0 = s.off[id];
+        cl = (int)(s.off[id + 1] - b0);
+        for (int j = sl; j < cl; j += L) inter += has(s.tok[b0 + j]);
+      }
+#pragma unroll
+      for (int o = L / 2; o >= 1; o >>= 1) inter += __shfl_xor_sync(FULL, inter, o);
+      const uint32_t key = ((uint32_t)inter << 16) | (uint32_t)(qn + cl - inter);
+      const uint32_t kk = __shfl_sync(FULL, key, (lane % VPP) * L);
+      if (lane / VPP == p) out = kk;
+    }
+    return out;
+  }
+};
+
+template <int M, int L, int CPL>
+struct QuerySel { typedef VecQuery<M, L, CPL> T; };
+template <int L, int CPL>
+struct QuerySel<M_JAC, L, CPL> { typedef SetQuery<L> T; };
 
 }  // namespace knng

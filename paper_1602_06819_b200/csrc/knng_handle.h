@@ -51,7 +51,10 @@ struct knng_graph {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  uint8_t *vec = nullptr;
+  uint8_t *vec = nullptr;                       // vectors (u8 / f32 rows)
+  uint64_t *off = nullptr;                      // sets: [cap+1] offsets into tok
+  uint32_t *tok = nullptr;                      // sets: tokens
+  int64_t tok_cap = 0, tok_n = 0;               // token capacity / tokens in use (host mirror)
   int32_t *ids = nullptr;
   uint32_t *keys = nullptr;
   int32_t *ncnt = nullptr, *nfill = nullptr, *noff = nullptr, *scan_tmp = nullptr;
@@ -66,5 +69,16 @@ struct knng_graph {
   // workspaces
   DBuf w_bits, w_cand_i, w_cand_k, w_C_i, w_C_k, w_hash, w_list, w_props, w_prop_cnt, w_sorted, w_stats,
       w_target, w_query, w_starts;
+  DBuf w_qoff, w_qtok;
   cudaEvent_t ev[6] = {};
 };
+
+inline knng::StoreView graph_store_view(const knng_graph *g) {
+  knng::StoreView v;
+  v.vec = g->vec;
+  v.stride = g->geom.stride;
+  v.nchunks = g->geom.nchunks;
+  v.off = g->off;
+  v.tok = g->tok;
+  return v;
+}

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "knng_common.cuh"
+
 namespace knng {
 
 // Vector store geometry: rows of `stride` bytes (= nchunks * 16, zero padded).
@@ -15,13 +17,12 @@ struct VecGeom {
 };
 
 struct SearchArgs {
-  const uint8_t *vec;          // store rows
-  size_t stride;
-  int nchunks;
+  StoreView st;                // the graph's points
+  StoreView qs;                // the queries (== st for inserts)
+  int64_t qrow0;               // query b is row qrow0 + b of qs
   const int32_t *rows;         // snapshot rows [n_t][k]
   int k;
   int64_t n_t;
-  const uint8_t *qbase;        // query rows (stride bytes each)
   int64_t nq;
   int64_t pid_base;            // RNG point id of query b = pid_base + b
   // partitions (P == 0: unpartitioned, pool = 0..n_t-1)
@@ -51,9 +52,7 @@ struct SearchArgs {
 };
 
 struct BallArgs {
-  const uint8_t *vec;
-  size_t stride;
-  int nchunks;
+  StoreView st;
   int32_t *ids;                // rows (snapshot until the merge)
   uint32_t *keys;
   int k;
@@ -74,7 +73,7 @@ struct BallArgs {
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch);
 cudaError_t launch_merge_parts(int metric, const int32_t *cand_ids, const uint32_t *cand_keys, int64_t nq,
                                int P, int kr, int32_t *out_ids, uint32_t *out_keys, cudaStream_t s);
-cudaError_t launch_allpairs(const VecGeom &g, const uint8_t *vec, int32_t *ids, uint32_t *keys, int k,
+cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int32_t *ids, uint32_t *keys, int k,
                             int64_t n_t, int64_t B, const int32_t *C_ids, const uint32_t *C_keys,
                             cudaStream_t s);
 cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cudaStream_t s);
@@ -82,9 +81,10 @@ cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, 
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
                                int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted,
                                cudaStream_t s, int *n_launch);
-cudaError_t launch_exact_build(const VecGeom &g, const uint8_t *vec, int64_t n, int k, int32_t *ids,
+cudaError_t exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t *tmp, int64_t n, cudaStream_t s);
+cudaError_t launch_exact_build(const VecGeom &g, const StoreView &st, int64_t n, int k, int32_t *ids,
                                uint32_t *keys, cudaStream_t s);
-cudaError_t launch_place(const VecGeom &g, const uint8_t *vec, int64_t n_t, int64_t B, int P,
+cudaError_t launch_place(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int P,
                          const int32_t *medoids, int32_t *members, int64_t member_cap, int64_t *member_cnt,
                          uint8_t *part_of, int32_t *local_idx, int32_t *target_tmp, cudaStream_t s);
 

@@ -38,13 +38,10 @@ __global__ void k_init_medoids(uint64_t seed, int64_t n, int P, int32_t *med) {
 }
 
 template <int M>
-__global__ void k_medoid_keys(const uint8_t *vec, size_t stride, int nchunks, int64_t n, int P, const int32_t *med,
-                              uint32_t *D) {
+__global__ void k_medoid_keys(StoreView st, int64_t n, int P, const int32_t *med, uint32_t *D) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint4 *x = (const uint4 *)(vec + (size_t)i * stride);
-  for (int p = 0; p < P; ++p)
-    D[(size_t)i * P + p] = thread_dist<M>(x, (const uint4 *)(vec + (size_t)med[p] * stride), nchunks);
+  for (int p = 0; p < P; ++p) D[(size_t)i * P + p] = pair_key<M>(st, i, med[p]);
 }
 
 // assign comparison: cluster a (key ka, size sa) strictly above b (P:188 score sim * w)
@@ -312,8 +309,6 @@ extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, in
   if (!(imbalance >= 1.0)) return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: imbalance < 1");
   if (max_iter < 1) return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: max_iter < 1");
   if (!medoids_out) return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: null medoids_out");
-  if (g->metric != KNNG_L2SQ_U8 && g->metric != KNNG_L2SQ_F32)
-    return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: metric not supported yet");
   const int64_t n = g->n;
   if (n < P) return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: n < P");
   const int64_t cap = (int64_t)ceil((double)n * imbalance / (double)P);   // F4, ceil
@@ -390,15 +385,18 @@ extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, in
   for (int it = 0; it < max_iter; ++it) {
     // ---------------- assign ----------------
     CK(cudaMemcpyAsync(wmed.p, med.data(), (size_t)P * 4, cudaMemcpyHostToDevice, s));
+    const StoreView st = graph_store_view(g);
     if (g->metric == KNNG_L2SQ_U8) {
-      k_medoid_keys<M_U8><<<nb, 256, 0, s>>>(g->vec, g->geom.stride, g->geom.nchunks, n, P, wmed.as<int32_t>(),
-                                             wD.as<uint32_t>());
+      k_medoid_keys<M_U8><<<nb, 256, 0, s>>>(st, n, P, wmed.as<int32_t>(), wD.as<uint32_t>());
       k_greedy_assign<M_U8><<<1, 32, 0, s>>>(wD.as<uint32_t>(), n, P, wmed.as<int32_t>(), cap, g->part_of,
                                              wsz.as<int64_t>());
-    } else {
-      k_medoid_keys<M_F32><<<nb, 256, 0, s>>>(g->vec, g->geom.stride, g->geom.nchunks, n, P, wmed.as<int32_t>(),
-                                              wD.as<uint32_t>());
+    } else if (g->metric == KNNG_L2SQ_F32) {
+      k_medoid_keys<M_F32><<<nb, 256, 0, s>>>(st, n, P, wmed.as<int32_t>(), wD.as<uint32_t>());
       k_greedy_assign<M_F32><<<1, 32, 0, s>>>(wD.as<uint32_t>(), n, P, wmed.as<int32_t>(), cap, g->part_of,
+                                              wsz.as<int64_t>());
+    } else {
+      k_medoid_keys<M_JAC><<<nb, 256, 0, s>>>(st, n, P, wmed.as<int32_t>(), wD.as<uint32_t>());
+      k_greedy_assign<M_JAC><<<1, 32, 0, s>>>(wD.as<uint32_t>(), n, P, wmed.as<int32_t>(), cap, g->part_of,
                                               wsz.as<int64_t>());
     }
     CK(cudaGetLastError());

@@ -29,8 +29,8 @@ struct RingHdr {
 // is fixed by the counter RNG (Q4) and the key of a draw is a pure function of (query, node), so
 // producers evaluate draws ahead of the consumer, 32 per chunk, into the CTA's smem ring.
 // Nothing here touches a counter, the visited sets or the top-k.
-template <int M, int L, int CPL>
-__device__ __forceinline__ void produce(const SearchArgs &a, const VecQuery<M, L, CPL> &Q, volatile RingHdr *hdr,
+template <class QT>
+__device__ __forceinline__ void produce(const SearchArgs &a, const QT &Q, volatile RingHdr *hdr,
                                         int2 *ring, int pw, int nprod, int64_t nch, uint64_t h3, int64_t m,
                                         const int32_t *pool) {
   const int lane = threadIdx.x & 31;
@@ -43,7 +43,7 @@ __device__ __forceinline__ void produce(const SearchArgs &a, const VecQuery<M, L
     if (hdr->done) break;
     const uint64_t idx = rng_index(h3, (uint64_t)(c * 32 + lane), (uint64_t)m);
     const int32_t node = pool ? pool[idx] : (int32_t)idx;
-    const uint32_t key = Q.eval(a.vec, a.stride, a.nchunks, node, 32);
+    const uint32_t key = Q.eval(a.st, node, 32);
     // a repeat of an earlier draw of the same chunk can never be fresh (Q4): flag it (bit 31)
     const bool dup = (__ffs(__match_any_sync(FULL, node)) - 1) != lane;
     volatile int *rs = (volatile int *)(ring + (c % RING_CHUNKS) * 32 + lane);
@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
   int2 *ring = (int2 *)(smem + 128);
   int32_t *rowbuf = (int32_t *)(smem + 128 + RING_CHUNKS * 32 * 8);          // [k][k]
   int32_t *rowbuf2 = rowbuf + a.k * a.k;                                      // [32][k]
-  uint32_t *sbits = (uint32_t *)(rowbuf2 + 32 * a.k);
+  uint32_t *qscr = (uint32_t *)(rowbuf2 + 32 * a.k);                          // [2][QMAX] (sets)
+  uint32_t *sbits = qscr + (M == M_JAC ? 2 * QMAX : 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nprod = (blockDim.x >> 5) - 1;
   const int Pn = a.P > 0 ? a.P : 1;
@@ -101,11 +102,11 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
     // consumed draws past the budget), capped for degenerate cases (speedup ~ 1)
     const int64_t nch = a.starts ? 0 : (8 * budget + 31) / 32 + 8;
 
-    VecQuery<M, L, CPL> Q;
-    Q.load(a.qbase + (size_t)b * a.stride, a.nchunks);
+    typename QuerySel<M, L, CPL>::T Q;
+    Q.load(a.qs, a.qrow0 + b, M == M_JAC ? qscr + (warp < 2 ? warp : 1) * QMAX : nullptr);
     const uint64_t h3 = rng_prefix(a.seed, (uint64_t)(a.pid_base + b), (uint64_t)p);
     if (warp > 0) {
-      if (budget > 0) produce<M, L, CPL>(a, Q, hdr, ring, warp - 1, nprod, nch, h3, m, pool);
+      if (budget > 0) produce(a, Q, hdr, ring, warp - 1, nprod, nch, h3, m, pool);
       continue;
     }
 
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
         const int nn = __popc(need);
         const int src = lane < nn ? (int)__fns(need, 0, lane + 1) : 0;
         const int32_t cid = __shfl_sync(FULL, wnode, src);
-        const uint32_t kk = Q.eval(a.vec, a.stride, a.nchunks, lane < nn ? cid : -1, nn);
+        const uint32_t kk = Q.eval(a.st, lane < nn ? cid : -1, nn);
         const int rank = __popc(need & lanemask_lt());
         const uint32_t mine = __shfl_sync(FULL, kk, rank & 31);
         if ((need >> lane) & 1u) { wkey = mine; whave = true; }
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
         }
         const bool evb2 = inpool ? bit_get(ev, lv) : true;
         const bool exb2 = inpool ? bit_get(ex, lv) : false;
-        const uint32_t key = Q.eval(a.vec, a.stride, a.nchunks, inpool ? v : -1, k);
+        const uint32_t key = Q.eval(a.st, inpool ? v : -1, k);
         const bool imp = inpool && closer<M>(key, kcur);
         const unsigned im = __ballot_sync(FULL, imp);
         const int fi = im ? __ffs(im) - 1 : 31;
@@ -366,7 +367,7 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int64_t T = a.nq * Pn;
   if (T == 0) return cudaSuccess;
   const int warps = a.starts ? 1 : 2;          // consumer + producers
-  size_t smem = 128 + RING_CHUNKS * 32 * 8 + (size_t)(a.k * a.k + 32 * a.k) * 4;
+  size_t smem = 128 + RING_CHUNKS * 32 * 8 + (size_t)(a.k * a.k + 32 * a.k) * 4 + (M == M_JAC ? 2 * QMAX * 4 : 0);
   if (a.smem_bits) smem += (size_t)a.bits_words * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -387,6 +388,7 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
   if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC>(a, s);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES(X, M_F32)
+  X(M_JAC, 8, 1)
 #undef X
   return cudaErrorInvalidValue;
 }

@@ -12,9 +12,8 @@ namespace knng {
 // K3: warp per new point i; lanes take peers j = lane + 32t (thread-level canonical distance).
 // ---------------------------------------------------------------------------
 template <int M>
-__global__ void __launch_bounds__(128) k_allpairs(const uint8_t *__restrict__ vec, size_t stride, int nchunks,
-                                                  int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
-                                                  const int32_t *Ci, const uint32_t *Ck) {
+__global__ void __launch_bounds__(128) k_allpairs(StoreView st, int32_t *ids, uint32_t *keys, int k, int64_t n_t,
+                                                  int64_t B, const int32_t *Ci, const uint32_t *Ck) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= B) return;
@@ -25,12 +24,11 @@ __global__ void __launch_bounds__(128) k_allpairs(const uint8_t *__restrict__ ve
     const uint32_t ck = lane < k ? Ck[i * k + lane] : 0u;
     top.insert(cid >= 0, ck, cid);
   }
-  const uint4 *xi = (const uint4 *)(vec + (size_t)(n_t + i) * stride);
   for (int64_t j0 = 0; j0 < B; j0 += 32) {
     const int64_t j = j0 + lane;
     const bool valid = j < B && j != i;
     uint32_t key = 0;
-    if (valid) key = thread_dist<M>(xi, (const uint4 *)(vec + (size_t)(n_t + j) * stride), nchunks);
+    if (valid) key = pair_key<M>(st, n_t + i, n_t + j);
     top.insert(valid, key, (int32_t)(n_t + j));
   }
   if (lane < k) {
@@ -39,14 +37,13 @@ __global__ void __launch_bounds__(128) k_allpairs(const uint8_t *__restrict__ ve
   }
 }
 
-cudaError_t launch_allpairs(const VecGeom &g, const uint8_t *vec, int32_t *ids, uint32_t *keys, int k, int64_t n_t,
+cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int32_t *ids, uint32_t *keys, int k, int64_t n_t,
                             int64_t B, const int32_t *Ci, const uint32_t *Ck, cudaStream_t s) {
   if (B == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((B + 3) / 4);
-  if (g.metric == M_U8)
-    k_allpairs<M_U8><<<blocks, 128, 0, s>>>(vec, g.stride, g.nchunks, ids, keys, k, n_t, B, Ci, Ck);
-  else
-    k_allpairs<M_F32><<<blocks, 128, 0, s>>>(vec, g.stride, g.nchunks, ids, keys, k, n_t, B, Ci, Ck);
+  if (g.metric == M_U8) k_allpairs<M_U8><<<blocks, 128, 0, s>>>(st, ids, keys, k, n_t, B, Ci, Ck);
+  else if (g.metric == M_F32) k_allpairs<M_F32><<<blocks, 128, 0, s>>>(st, ids, keys, k, n_t, B, Ci, Ck);
+  else k_allpairs<M_JAC><<<blocks, 128, 0, s>>>(st, ids, keys, k, n_t, B, Ci, Ck);
   return cudaGetLastError();
 }
 
@@ -69,6 +66,7 @@ __device__ __forceinline__ bool hash_insert(int32_t *h, int hcap, int32_t u) {
 template <int M, int L, int CPL>
 __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
   __shared__ int s_n[4];
+  __shared__ uint32_t qscr[M == M_JAC ? 4 * QMAX : 1];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * 4 + wib, nw = (int64_t)gridDim.x * 4;
   int32_t *hash = a.hash + gw * a.hcap;
@@ -79,8 +77,8 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
     for (int i = lane; i < a.hcap; i += 32) hash[i] = -1;
     if (lane == 0) s_n[wib] = 0;
     __syncwarp();
-    VecQuery<M, L, CPL> Q;
-    Q.load(a.vec + (size_t)(a.n_t + b) * a.stride, a.nchunks);
+    typename QuerySel<M, L, CPL>::T Q;
+    Q.load(a.st, a.n_t + b, M == M_JAC ? qscr + wib * QMAX : nullptr);
     const int32_t idx = (int32_t)(a.n_t + b);
     // L1 = the search result C(x)
     {
@@ -108,7 +106,7 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
           }
         }
         const int cnt = hi - base < 32 ? hi - base : 32;
-        const uint32_t key = Q.eval(a.vec, a.stride, a.nchunks, v, cnt);
+        const uint32_t key = Q.eval(a.st, v, cnt);
         bool prop = false;
         if (v >= 0) {
           const uint32_t kk = a.keys[(size_t)v * k + k - 1];
@@ -151,6 +149,7 @@ cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cud
   if (g.metric == MM && g.L == LL && g.CPL == CC) return run_ball<MM, LL, CC>(a, nslots, s);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES(X, M_F32)
+  X(M_JAC, 8, 1)
 #undef X
   return cudaErrorInvalidValue;
 }
@@ -312,15 +311,13 @@ cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, 
 // Single block: new ids are appended in batch order, so member lists stay ascending.
 // ---------------------------------------------------------------------------
 template <int M>
-__global__ void k_place_target(const uint8_t *vec, size_t stride, int nchunks, int64_t n_t, int64_t B, int P,
-                               const int32_t *medoids, int32_t *target) {
+__global__ void k_place_target(StoreView st, int64_t n_t, int64_t B, int P, const int32_t *medoids, int32_t *target) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
-  const uint4 *x = (const uint4 *)(vec + (size_t)(n_t + i) * stride);
   int best = 0;
   uint32_t bk = 0;
   for (int p = 0; p < P; ++p) {
-    const uint32_t kp = thread_dist<M>(x, (const uint4 *)(vec + (size_t)medoids[p] * stride), nchunks);
+    const uint32_t kp = pair_key<M>(st, n_t + i, medoids[p]);
     if (p == 0 || closer<M>(kp, bk)) { best = p; bk = kp; }
   }
   target[i] = best;
@@ -357,13 +354,14 @@ __global__ void k_place_append(int64_t n_t, int64_t B, int P, const int32_t *tar
   for (int p = threadIdx.x; p < P; p += blockDim.x) member_cnt[p] = base[p];
 }
 
-cudaError_t launch_place(const VecGeom &g, const uint8_t *vec, int64_t n_t, int64_t B, int P, const int32_t *medoids,
+cudaError_t launch_place(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int P, const int32_t *medoids,
                          int32_t *members, int64_t member_cap, int64_t *member_cnt, uint8_t *part_of,
                          int32_t *local_idx, int32_t *target, cudaStream_t s) {
   if (B == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((B + 127) / 128);
-  if (g.metric == M_U8) k_place_target<M_U8><<<blocks, 128, 0, s>>>(vec, g.stride, g.nchunks, n_t, B, P, medoids, target);
-  else k_place_target<M_F32><<<blocks, 128, 0, s>>>(vec, g.stride, g.nchunks, n_t, B, P, medoids, target);
+  if (g.metric == M_U8) k_place_target<M_U8><<<blocks, 128, 0, s>>>(st, n_t, B, P, medoids, target);
+  else if (g.metric == M_F32) k_place_target<M_F32><<<blocks, 128, 0, s>>>(st, n_t, B, P, medoids, target);
+  else k_place_target<M_JAC><<<blocks, 128, 0, s>>>(st, n_t, B, P, medoids, target);
   k_place_append<<<1, 1024, 0, s>>>(n_t, B, P, target, members, member_cap, member_cnt, part_of, local_idx);
   return cudaGetLastError();
 }

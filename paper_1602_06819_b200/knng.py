@@ -106,9 +106,44 @@ def _metric_of(arr):
     raise TypeError("points must be uint8 or float32, got %s" % arr.dtype)
 
 
+class TokenSets:
+    """Jaccard sets in CSR form: offsets uint64[n+1], tokens uint32 (each set sorted, unique).
+    Both host numpy arrays, or both CUDA torch tensors (int64 / int32 views are accepted)."""
+
+    def __init__(self, offsets, tokens):
+        self.offsets = offsets
+        self.tokens = tokens
+
+    @staticmethod
+    def from_list(sets):
+        off = np.zeros(len(sets) + 1, np.uint64)
+        off[1:] = np.cumsum([len(x) for x in sets])
+        tok = (np.concatenate([np.asarray(x, np.uint32) for x in sets]) if len(sets) else np.zeros(0, np.uint32))
+        return TokenSets(off, np.ascontiguousarray(tok, np.uint32))
+
+    def __len__(self):
+        return len(self.offsets) - 1
+
+
 def make_points(points):
-    """Marshal a host numpy array or a CUDA torch tensor [n, dim] into knng_points.
-    Returns (struct, keepalive)."""
+    """Marshal host numpy [n, dim] / CUDA torch [n, dim] vectors, or Jaccard sets (a list of sorted
+    uint32 arrays or a TokenSets), into knng_points.  Returns (struct, keepalive)."""
+    if isinstance(points, list):
+        points = TokenSets.from_list(points)
+    if isinstance(points, TokenSets):
+        o, t = points.offsets, points.tokens
+        if hasattr(o, "is_cuda") and o.is_cuda:
+            o, t = o.contiguous(), t.contiguous()
+            p = knng_points(KNNG_JACCARD_U32SET, 0, len(o) - 1, C.c_void_p(t.data_ptr() if t.numel() else 0),
+                            C.c_void_p(o.data_ptr()), 1)
+            return p, (o, t)
+        o = np.ascontiguousarray(o, np.uint64)
+        t = np.ascontiguousarray(t, np.uint32)
+        if len(t) == 0:
+            t = np.zeros(1, np.uint32)
+        p = knng_points(KNNG_JACCARD_U32SET, 0, len(o) - 1, t.ctypes.data_as(C.c_void_p),
+                        o.ctypes.data_as(C.c_void_p), 0)
+        return p, (o, t)
     if hasattr(points, "is_cuda") and points.is_cuda:
         t = points.contiguous()
         n, d = t.shape

@@ -309,3 +309,61 @@ def test_partition_errors():
         g.partition_kmedoids(300, 1.0, 3, 0)
     with pytest.raises(KnngError):
         g.partition_kmedoids(4, 0.5, 3, 0)
+
+
+# ---------------------------------------------------------------------------
+# Jaccard token sets (C4 shape): exact cross-multiplied keys, bit-exact
+# ---------------------------------------------------------------------------
+def test_jaccard_init_search_stream_and_partition():
+    cfg = _cfg_small("C4", n0=3000, n_insert=900)
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    Q = D.query_points(cfg, 150)
+    cap = cfg.n0 + cfg.n_insert + 8
+    g = _graph(X, cfg.k, cap)
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cap)
+    o.init_exact()
+    gi, gk = g.rows()
+    _assert_rows_equal(cfg.metric, gi, gk, o.ids[:cfg.n0], o.keys[:cfg.n0], "jaccard init")
+    gi, gk, gst = g.search(Q, cfg.k, 4.0, cfg.e_num, cfg.e_den, cfg.search_seed)
+    oi, ok, ost = o.search(Q, cfg.k, 4.0, cfg.e_num, cfg.e_den, cfg.search_seed)
+    _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "jaccard search")
+    assert gst["search_evals"] == ost[:, 0].sum() and gst["search_skipped"] == ost[:, 2].sum()
+    # unpartitioned batches, then partition and continue (Alg. 5 placement)
+    g.insert_batch(S[:300], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+    o.insert_batch(S[:300], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+    gi, gk = g.rows()
+    oi, ok = o.rows()
+    _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "jaccard stream")
+    gp, gm, gc = g.partition_kmedoids(cfg.P, cfg.imbalance, 4, cfg.part_seed)
+    op, om, oc = o.partition_kmedoids(cfg.P, cfg.imbalance, 4, cfg.part_seed)
+    assert (gp == op).all() and gm.tolist() == om.tolist() and gc.tolist() == oc.tolist()
+    o.set_partition(op, om)
+    for lo, hi in ((300, 812), (812, 900)):
+        g.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        o.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        gi, gk = g.rows()
+        oi, ok = o.rows()
+        _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "jaccard partitioned stream")
+    gpart, _ = g.partition()
+    assert (gpart == o.part_of[:o.n]).all()
+
+
+def test_jaccard_edge_sets():
+    # identical sets (ties -> id), disjoint sets (key 0/u), single-token sets, a long set (> QMAX tokens)
+    rng = np.random.default_rng(5)
+    sets = [np.array([1, 2, 3], np.uint32)] * 6 + [np.array([100 + i], np.uint32) for i in range(10)]
+    sets += [np.sort(rng.choice(5000, size=int(rng.integers(1, 40)), replace=False)).astype(np.uint32)
+             for _ in range(80)]
+    sets += [np.arange(0, 900, 2, dtype=np.uint32), np.arange(0, 600, 3, dtype=np.uint32)]
+    g = _graph(sets, 4, 200)
+    o = O.OracleGraph(O.JAC, sets, 4, capacity=200)
+    o.init_exact()
+    gi, gk = g.rows()
+    _assert_rows_equal(O.JAC, gi, gk, o.ids[:len(sets)], o.keys[:len(sets)], "jaccard edge init")
+    new = [np.arange(0, 700, 2, dtype=np.uint32), np.array([1, 2, 3], np.uint32), np.array([7], np.uint32)]
+    g.insert_batch(new, 1.5, 6, 5, 2, 3)
+    o.insert_batch(new, 1.5, 6, 5, 2, 3)
+    gi, gk = g.rows()
+    oi, ok = o.rows()
+    _assert_rows_equal(O.JAC, gi, gk, oi, ok, "jaccard edge insert")
