@@ -160,6 +160,33 @@ int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, int32_t max_i
                        uint64_t seed, uint8_t *part_out, int32_t *medoids_out, int64_t *cost_out,
                        const int32_t *init_medoids);
 
+/* ---- Staged insert: the multi-GPU building blocks (all buffers are DEVICE pointers) ----
+ * graph_insert_batch == stage_search(all partitions) + stage_update(world 1, all queries) +
+ * stage_commit.  With G ranks each holding a full replica of the graph (same inputs, same calls),
+ * the distributed insert of Alg. 5 is, on every rank r:
+ *   1. graph_insert_stage_search over the rank's partitions [r*P/G, (r+1)*P/G): it ingests the batch
+ *      (rows n_t..n_t+B-1) and writes cand [B][P/G][k] (ids int32, keys uint32; -1/0 padded);
+ *   2. all-gather cand over the ranks -> [G][B][P/G][k] (rank-major) ("the compute nodes send the
+ *      k.p candidates", Alg. 3);
+ *   3. graph_insert_stage_update(world = G, gathered cand, query shard [q_lo, q_hi)): merges the
+ *      candidates (identical on every rank), writes the B new rows, and runs the update balls of the
+ *      shard into props int2[q_hi-q_lo][ballmax] (node, key) and prop_cnt int32[q_hi-q_lo];
+ *   4. all-gather props / prop_cnt over equal-size shards (S = ceil(B/G) slots per rank, counts 0 in
+ *      the padding) -> [G*S][ballmax], [G*S];
+ *   5. graph_insert_stage_commit(nq_slots = G*S): applies every proposal (slot b proposes id n_t + b)
+ *      and places the new points; the replicas stay bit-identical, and the result equals the single-GPU
+ *      call for every G.
+ * ballmax = graph_ball_bound(g, depth) evaluated BEFORE stage_search (it depends on n_t).
+ * Errors: INVALID_ARG (bad ranges, a pending batch, P % G != 0), CAPACITY_EXCEEDED, OOM, CUDA. */
+int64_t graph_ball_bound(const knng_graph *g, int32_t depth);
+int graph_insert_stage_search(knng_graph *g, const knng_points *pts, const knng_params *p, int32_t part_lo,
+                              int32_t part_hi, int32_t *cand_ids, uint32_t *cand_keys, knng_stats *st);
+int graph_insert_stage_update(knng_graph *g, const knng_params *p, int32_t world, const int32_t *cand_ids_all,
+                              const uint32_t *cand_keys_all, int64_t q_lo, int64_t q_hi, int32_t *props,
+                              int32_t *prop_cnt, knng_stats *st);
+int graph_insert_stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, const int32_t *props_all,
+                              const int32_t *prop_cnt_all, knng_stats *st);
+
 /* graph_get_rows -- copy rows [first, first+count) to host: ids int32[count*k],
  * keys uint32[count*k] (either may be NULL).  Errors: INVALID_ARG, CUDA. */
 int graph_get_rows(const knng_graph *g, int64_t first, int64_t count, int32_t *ids, uint32_t *keys);

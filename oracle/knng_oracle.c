@@ -1017,3 +1017,109 @@ int or_nearest_medoid(int metric, int dim, const void *data, const uint64_t *off
   px.u8 = (const uint8_t *)x; px.f32 = (const float *)x; px.tok = (const uint32_t *)x; px.ntok = nx;
   return nearest_medoid(&G, px);
 }
+
+/* ------------------------------------------------------------------ */
+/* Staged batch (the same steps as or_insert_batch, split the way a     */
+/* distributed run splits them: searches per partition range, balls    */
+/* per query range, then one commit).  Used by the multi-process tests. */
+/* ------------------------------------------------------------------ */
+/* per-partition candidates of batch points stored at rows n_t+b, b in [0,B), for partitions
+ * [plo, phi): out [B][phi-plo][k] (-1/0 padded) */
+int or_stage_search(int metric, int dim, void *data, uint64_t *off, int k, int64_t n_t, int32_t *ids,
+                    uint32_t *keys, int P, uint8_t *part_of, int32_t *members, int64_t *member_cnt,
+                    int64_t member_cap, int64_t B, int plo, int phi, double speedup, uint64_t e_num,
+                    uint64_t e_den, uint64_t seed, int32_t *out_ids, uint32_t *out_keys, int64_t *out_evals) {
+  or_graph G;
+  or_store S;
+  or_scratch W;
+  int64_t b;
+  int p, t, np = phi - plo;
+  memset(&G, 0, sizeof G);
+  G.metric = metric; G.dim = dim; G.k = k; G.data = data; G.off = off; G.n = n_t;
+  G.ids = ids; G.keys = keys; G.P = P; G.part_of = part_of; G.members = members;
+  G.member_cnt = member_cnt; G.member_cap = member_cap;
+  S = graph_store(&G);
+  if (!scratch_init(&W, n_t)) return -5;
+  for (b = 0; b < B; ++b) {
+    for (p = plo; p < phi; ++p) {
+      or_search_cfg C;
+      or_list T;
+      or_search_stats st;
+      memset(&C, 0, sizeof C);
+      C.S = &S; C.k = k; C.rows = ids;
+      if (P > 0) {
+        C.pool = members + (size_t)p * member_cap; C.m = member_cnt[p]; C.part_of = part_of; C.part = p;
+      } else {
+        C.pool = NULL; C.m = n_t; C.part_of = NULL; C.part = 0;
+      }
+      C.speedup = speedup; C.e_num = e_num; C.e_den = e_den; C.seed = seed;
+      T.cap = k; T.cnt = 0;
+      T.key = out_keys + ((size_t)b * np + (p - plo)) * k;
+      T.id = out_ids + ((size_t)b * np + (p - plo)) * k;
+      ignns(&C, store_point(&S, n_t + b), n_t + b, k, &W, &T, &st);
+      for (t = T.cnt; t < k; ++t) { T.id[t] = -1; T.key[t] = 0; }
+      if (out_evals) *out_evals += st.evals;
+    }
+  }
+  scratch_free(&W);
+  return 0;
+}
+
+/* update balls of queries [qlo, qhi) given their search results C [B][k] (all B):
+ * props [qhi-qlo][ballmax] as (node, key) int pairs, counts [qhi-qlo] */
+int or_stage_ball(int metric, int dim, void *data, uint64_t *off, int k, int64_t n_t, int32_t *ids,
+                  uint32_t *keys, const int32_t *C_ids, int64_t qlo, int64_t qhi, int depth, int64_t ballmax,
+                  int32_t *props, int32_t *prop_cnt) {
+  or_graph G;
+  or_store S;
+  uint8_t *seen;
+  int32_t *buf;
+  or_prop *tmp;
+  int64_t q, i;
+  memset(&G, 0, sizeof G);
+  G.metric = metric; G.dim = dim; G.k = k; G.data = data; G.off = off; G.n = n_t;
+  G.ids = ids; G.keys = keys;
+  S = graph_store(&G);
+  seen = (uint8_t *)calloc((size_t)n_t + 1, 1);
+  buf = (int32_t *)malloc(sizeof(int32_t) * (size_t)(ballmax + 1));
+  tmp = (or_prop *)malloc(sizeof(or_prop) * (size_t)(ballmax + 1));
+  for (q = qlo; q < qhi; ++q) {
+    int64_t np = 0;
+    update_ball(&G, store_point(&S, n_t + q), (int32_t)(n_t + q), C_ids + q * k, depth, seen, buf, ballmax, tmp,
+                &np, (int32_t)q);
+    prop_cnt[q - qlo] = (int32_t)np;
+    for (i = 0; i < np; ++i) {
+      props[((q - qlo) * ballmax + i) * 2 + 0] = tmp[i].node;
+      props[((q - qlo) * ballmax + i) * 2 + 1] = (int32_t)tmp[i].key;
+    }
+  }
+  free(seen); free(buf); free(tmp);
+  return 0;
+}
+
+/* apply proposals of nslots query slots (slot b proposes id n_t + b), in (qid, key, node) order */
+int or_stage_apply(int metric, int k, int64_t n_t, int32_t *ids, uint32_t *keys, int64_t nslots, int64_t ballmax,
+                   const int32_t *props, const int32_t *prop_cnt) {
+  int64_t b, i, n = 0;
+  or_prop *all;
+  for (b = 0; b < nslots; ++b) n += prop_cnt[b];
+  all = (or_prop *)malloc(sizeof(or_prop) * (size_t)(n + 1));
+  n = 0;
+  for (b = 0; b < nslots; ++b)
+    for (i = 0; i < prop_cnt[b]; ++i) {
+      all[n].node = props[(b * ballmax + i) * 2 + 0];
+      all[n].key = (uint32_t)props[(b * ballmax + i) * 2 + 1];
+      all[n].qid = (int32_t)b;
+      ++n;
+    }
+  g_sort_metric = metric;
+  qsort(all, (size_t)n, sizeof(or_prop), prop_cmp);
+  for (i = 0; i < n; ++i) {
+    or_list L;
+    int32_t v = all[i].node;
+    L.cap = k; L.cnt = k; L.key = keys + (size_t)v * k; L.id = ids + (size_t)v * k;
+    list_insert(metric, &L, all[i].key, (int32_t)(n_t + all[i].qid));
+  }
+  free(all);
+  return 0;
+}

@@ -72,6 +72,13 @@ def lib():
                                                 P, P, P, i64, i32, P]
             L.or_nearest_medoid.restype = i32
             L.or_nearest_medoid.argtypes = [i32, i32, P, P, P, i32, P, i64]
+            L.or_stage_search.restype = i32
+            L.or_stage_search.argtypes = [i32, i32, P, P, i32, i64, P, P, i32, P, P, P, i64, i64, i32, i32, dbl,
+                                          u64, u64, u64, P, P, P]
+            L.or_stage_ball.restype = i32
+            L.or_stage_ball.argtypes = [i32, i32, P, P, i32, i64, P, P, P, i64, i64, i32, i64, P, P]
+            L.or_stage_apply.restype = i32
+            L.or_stage_apply.argtypes = [i32, i32, i64, P, P, i64, i64, P, P]
             _lib = L
     return _lib
 
@@ -383,3 +390,85 @@ class OracleGraph:
 
     def rows(self):
         return self.ids[:self.n].copy(), self.keys[:self.n].copy()
+
+    # -- the batch split the way a distributed run splits it (tests of the multi-GPU design) --
+    def ball_bound(self, depth):
+        b, pw = 0, 1
+        for _ in range(depth):
+            if b >= self.n:
+                break
+            pw *= self.k
+            b += pw
+        return min(b, self.n)
+
+    def stage_search(self, pts, plo, phi, speedup, e_num, e_den, seed):
+        """Ingest the batch (rows n..n+B-1, n unchanged) and search partitions [plo, phi)."""
+        B = len(pts)
+        self._append_points(pts)
+        self.pend_B = B
+        oi = np.full((B, phi - plo, self.k), -1, np.int32)
+        ok = np.zeros((B, phi - plo, self.k), np.uint32)
+        ev = np.zeros(1, np.int64)
+        rc = lib().or_stage_search(self.metric, self.dim, _p(self.data), _p(self.off), self.k, self.n, _p(self.ids),
+                                   _p(self.keys), self.P, _p(self.part_of), _p(self.members), _p(self.member_cnt),
+                                   self.member_cap, B, plo, phi, speedup, e_num, e_den, seed, _p(oi), _p(ok), _p(ev))
+        if rc:
+            raise RuntimeError("or_stage_search rc=%d" % rc)
+        return oi, ok
+
+    def stage_update(self, C_ids, C_keys, qlo, qhi, depth, ballmax):
+        """New rows of the whole batch (top-k of C_i and the peers, Q15), then the balls of
+        queries [qlo, qhi) -> props [qhi-qlo][ballmax][2], counts."""
+        import functools
+        B, n_t, k = self.pend_B, self.n, self.k
+
+        def cmp(a, b):
+            return -1 if precedes(self.metric, a[0], a[1], b[0], b[1]) else 1
+        for i in range(B):
+            cand = [(int(C_keys[i, t]), int(C_ids[i, t])) for t in range(k) if C_ids[i, t] >= 0]
+            cand += [(key(self.metric, self.point(n_t + i), self.point(n_t + j)), n_t + j) for j in range(B) if j != i]
+            cand.sort(key=functools.cmp_to_key(cmp))
+            cand = cand[:k] + [(0, -1)] * (k - len(cand[:k]))
+            self.keys[n_t + i] = [c[0] for c in cand]
+            self.ids[n_t + i] = [c[1] for c in cand]
+        props = np.zeros((max(qhi - qlo, 0), ballmax, 2), np.int32)
+        cnt = np.zeros(max(qhi - qlo, 0), np.int32)
+        Ci = np.ascontiguousarray(C_ids, np.int32)
+        rc = lib().or_stage_ball(self.metric, self.dim, _p(self.data), _p(self.off), k, n_t, _p(self.ids),
+                                 _p(self.keys), _p(Ci), qlo, qhi, depth, ballmax, _p(props), _p(cnt))
+        if rc:
+            raise RuntimeError("or_stage_ball rc=%d" % rc)
+        return props, cnt
+
+    def stage_commit(self, props_all, cnt_all, ballmax):
+        B, n_t = self.pend_B, self.n
+        pa = np.ascontiguousarray(props_all, np.int32)
+        ca = np.ascontiguousarray(cnt_all, np.int32)
+        lib().or_stage_apply(self.metric, self.k, n_t, _p(self.ids), _p(self.keys), len(ca), ballmax, _p(pa), _p(ca))
+        if self.P > 0:       # placement at the nearest medoid, batch order (Alg. 5)
+            for i in range(B):
+                p = self.nearest_medoid(self.point(n_t + i))
+                self.part_of[n_t + i] = p
+                self.members[p, self.member_cnt[p]] = n_t + i
+                self.member_cnt[p] += 1
+        self.n = n_t + B
+        self.pend_B = 0
+
+
+def merge_candidates(metric, cand_ids, cand_keys, world, P, k):
+    """Alg. 3 'keep the k most similar' over rank-major gathered candidates [world][B][P/world][k]."""
+    import functools
+    ci = np.asarray(cand_ids).reshape(world, -1, P // world, k)
+    ck = np.asarray(cand_keys).reshape(world, -1, P // world, k)
+    B = ci.shape[1]
+    out_i = np.full((B, k), -1, np.int32)
+    out_k = np.zeros((B, k), np.uint32)
+
+    def cmp(a, b):
+        return -1 if precedes(metric, a[0], a[1], b[0], b[1]) else 1
+    for b in range(B):
+        c = sorted(((int(ck[r, b, j, t]), int(ci[r, b, j, t])) for r in range(world) for j in range(P // world)
+                    for t in range(k) if ci[r, b, j, t] >= 0), key=functools.cmp_to_key(cmp))[:k]
+        for t, (kk, ii) in enumerate(c):
+            out_i[b, t], out_k[b, t] = ii, kk
+    return out_i, out_k

@@ -290,22 +290,16 @@ static int64_t max_pool(knng_graph *g) {
   return m;
 }
 
+// K1 over partitions [part_lo, part_hi) (unpartitioned: [0, 1)): raw per-partition candidates
+// [nq][part_hi-part_lo][kr] into out_i / out_k.
 static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, int64_t nq, int64_t pid_base, int kr,
-                            const knng_params *p, const int32_t *d_starts, int nstarts, int32_t *out_i,
-                            uint32_t *out_k, int *nl) {
-  const int Pn = g->P > 0 ? g->P : 1;
+                            const knng_params *p, const int32_t *d_starts, int nstarts, int part_lo, int part_hi,
+                            int32_t *out_i, uint32_t *out_k, int *nl) {
   const int64_t mmax = max_pool(g);
   if (g->P > 0 && mmax == 0) return fail(KNNG_ERR_EMPTY, "all partitions are empty");
-  SearchPlan sp = plan_search(g, nq * Pn, mmax);
+  const int pc = part_hi - part_lo;
+  SearchPlan sp = plan_search(g, nq * pc, mmax);
   if (!sp.smem) CK(g->w_bits.ensure((size_t)sp.slots * sp.bits_words * 4));
-  int32_t *ci = out_i;
-  uint32_t *ck = out_k;
-  if (g->P > 0) {
-    CK(g->w_cand_i.ensure((size_t)nq * Pn * kr * 4));
-    CK(g->w_cand_k.ensure((size_t)nq * Pn * kr * 4));
-    ci = g->w_cand_i.as<int32_t>();
-    ck = g->w_cand_k.as<uint32_t>();
-  }
   SearchArgs a;
   memset(&a, 0, sizeof a);
   a.st = graph_store_view(g);
@@ -317,6 +311,8 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.nq = nq;
   a.pid_base = pid_base;
   a.P = g->P;
+  a.part_lo = part_lo;
+  a.part_cnt = pc;
   a.members = g->members;
   a.member_cap = g->cap;
   a.member_cnt = g->member_cnt;
@@ -334,18 +330,12 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.gslots = sp.slots;
   a.bits_words = sp.bits_words;
   a.smem_bits = sp.smem;
-  a.out_ids = ci;
-  a.out_keys = ck;
+  a.out_ids = out_i;
+  a.out_keys = out_k;
   a.stats = g->w_stats.as<unsigned long long>();
   a.prof = getenv("KNNG_PROFILE") ? a.stats + 8 : nullptr;   // cycle counters -> stats[8..13]
-  cudaError_t e;
-  e = launch_search(g->geom, a, g->stream, nl);
+  cudaError_t e = launch_search(g->geom, a, g->stream, nl);
   if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
-  if (g->P > 0) {
-    e = launch_merge_parts(g->metric, ci, ck, nq, g->P, kr, out_i, out_k, g->stream);
-    if (nl) ++*nl;
-    if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "merge launch: %s", cudaGetErrorString(e));
-  }
   return 0;
 }
 
@@ -368,63 +358,75 @@ static void fill_stats(knng_graph *g, knng_stats *st, const unsigned long long *
   if (nev >= 2) { cudaEventElapsedTime(&ms, g->ev[0], g->ev[nev - 1]); st->ms_total = ms; }
 }
 
-int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,
-                       knng_stats *st) {
-  knng_err_slot().clear();
-  if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: null graph");
-  if (int r = check_points(pts, "graph_insert_batch")) return r;
-  if (int r = check_params(p)) return r;
-  if (pts->metric != g->metric || pts->dim != g->dim)
-    return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: metric/dim mismatch");
-  if (p->depth < 1 || p->depth > 10) return fail(KNNG_ERR_INVALID_ARG, "depth %d outside 1..10", p->depth);
-  const int64_t B = pts->n, n_t = g->n;
-  const int k = g->k;
-  if (first_id_out) *first_id_out = n_t;
-  if (n_t + B > g->cap)
-    return fail(KNNG_ERR_CAPACITY_EXCEEDED, "capacity %lld exceeded (n=%lld, B=%lld)", (long long)g->cap,
-                (long long)n_t, (long long)B);
-  CK(cudaSetDevice(g->device));
-  CK(g->w_stats.ensure(16 * 8));
-  if (B == 0) {
-    fill_stats(g, st, (const unsigned long long[8]){0, 0, 0, 0, 0, 0, 0, 0}, 0, 0);
-    return KNNG_OK;
-  }
-  int nl = 0;
-  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
-  // A1: batch ingest into the store tail (ids n_t .. n_t+B-1)
-  if (int r = store_points(g, pts, n_t)) return r;
-  const StoreView sv = graph_store_view(g);
-  // ball bound k + k^2 + ... + k^DEPTH, at most n_t
+// ---------------------------------------------------------------------------------------------
+// graph_insert_batch in three stages.  One GPU runs them back to back; the multi-GPU driver
+// (paper_1602_06819_b200/dist.py) runs them on every rank with two all-gathers in between:
+//   search : ingest the batch (rows n_t..), K1 over this rank's partitions   -> candidates
+//   update : K2 merge of all ranks' candidates, K3 all-pairs (all B), K4 balls of this rank's
+//            query shard                                                      -> proposals
+//   commit : K5 merge of all ranks' proposals, K6 placement, n_t += B  (identical on every rank)
+// ---------------------------------------------------------------------------------------------
+static int64_t ball_bound(int64_t n_t, int k, int depth) {   // k + k^2 + ... + k^DEPTH, <= n_t
   int64_t ballmax = 0, pw = 1;
-  for (int d = 1; d <= p->depth && ballmax < n_t; ++d) {
+  for (int d = 1; d <= depth && ballmax < n_t; ++d) {
     pw *= k;
     ballmax += pw;
   }
-  if (ballmax > n_t) ballmax = n_t;
+  return ballmax > n_t ? n_t : ballmax;
+}
+
+static int stage_search(knng_graph *g, const knng_points *pts, const knng_params *p, int part_lo, int part_hi,
+                        int32_t *ci, uint32_t *ck, int *nl) {
+  if (int r = check_points(pts, "insert")) return r;
+  if (int r = check_params(p)) return r;
+  if (pts->metric != g->metric || (g->metric != KNNG_JACCARD_U32SET && pts->dim != g->dim))
+    return fail(KNNG_ERR_INVALID_ARG, "insert: metric/dim mismatch");
+  if (p->depth < 1 || p->depth > 10) return fail(KNNG_ERR_INVALID_ARG, "depth %d outside 1..10", p->depth);
+  const int Pn = g->P > 0 ? g->P : 1;
+  if (part_lo < 0 || part_hi > Pn || part_lo >= part_hi) return fail(KNNG_ERR_INVALID_ARG, "bad partition range");
+  const int64_t B = pts->n, n_t = g->n;
+  if (n_t + B > g->cap)
+    return fail(KNNG_ERR_CAPACITY_EXCEEDED, "capacity %lld exceeded (n=%lld, B=%lld)", (long long)g->cap,
+                (long long)n_t, (long long)B);
+  g->pend_B = B;
+  if (B == 0) return 0;
+  // A1: batch ingest into the store tail (ids n_t .. n_t+B-1)
+  if (int r = store_points(g, pts, n_t)) return r;
+  // A2-A3: iGNNS per (point, partition) on the snapshot
+  return run_search_phase(g, graph_store_view(g), n_t, B, n_t, g->k, p, nullptr, 0, part_lo, part_hi, ci, ck, nl);
+}
+
+static int stage_update(knng_graph *g, const knng_params *p, int world, const int32_t *ci_all, const uint32_t *ck_all,
+                        int64_t q_lo, int64_t q_hi, int2 *props, int32_t *prop_cnt, int *nl, bool timed) {
+  const int64_t B = g->pend_B, n_t = g->n;
+  const int k = g->k;
+  if (B == 0) return 0;
+  const StoreView sv = graph_store_view(g);
+  // A4: keep the k best of the P*k per-partition candidates (all-gathered, rank-major)
+  int32_t *Ci = (int32_t *)ci_all;
+  uint32_t *Ck = (uint32_t *)ck_all;
+  if (g->P > 0) {
+    if (g->P % world) return fail(KNNG_ERR_INVALID_ARG, "P=%d not divisible by world=%d", g->P, world);
+    CK(g->w_C_i.ensure((size_t)B * k * 4));
+    CK(g->w_C_k.ensure((size_t)B * k * 4));
+    Ci = g->w_C_i.as<int32_t>();
+    Ck = g->w_C_k.as<uint32_t>();
+    CK(launch_merge_parts(g->metric, ci_all, ck_all, B, g->P, world, k, Ci, Ck, g->stream));
+    ++*nl;
+  }
+  if (timed) CK(cudaEventRecord(g->ev[1], g->stream));
+  // A5: intra-batch all-pairs -> new rows n_t .. n_t+B-1
+  CK(launch_allpairs(g->geom, sv, g->ids, g->keys, k, n_t, B, Ci, Ck, g->stream));
+  ++*nl;
+  if (timed) CK(cudaEventRecord(g->ev[2], g->stream));
+  // A6: update balls of queries [q_lo, q_hi) over the snapshot -> proposals
+  const int64_t ballmax = ball_bound(n_t, k, p->depth);
   int hcap = 64;
   while (hcap < 2 * ballmax) hcap <<= 1;
-  int64_t bslots = std::min<int64_t>((B + 3) / 4, 148 * 8) * 4;
-  CK(g->w_C_i.ensure((size_t)B * k * 4));
-  CK(g->w_C_k.ensure((size_t)B * k * 4));
+  const int64_t nqb = q_hi - q_lo;
+  const int64_t bslots = std::max<int64_t>(1, std::min<int64_t>((nqb + 3) / 4, 148 * 8)) * 4;
   CK(g->w_hash.ensure((size_t)bslots * hcap * 4));
   CK(g->w_list.ensure((size_t)bslots * ballmax * 4));
-  CK(g->w_props.ensure((size_t)B * ballmax * 8));
-  CK(g->w_prop_cnt.ensure((size_t)B * 4));
-  CK(g->w_sorted.ensure((size_t)B * ballmax * 8));
-  if (g->P > 0) CK(g->w_target.ensure((size_t)B * 4));
-
-  CK(cudaEventRecord(g->ev[0], g->stream));
-  // A2-A4: iGNNS per (point, partition) on the snapshot + partition merge
-  if (int r = run_search_phase(g, sv, n_t, B, n_t, k, p, nullptr, 0,
-                               g->w_C_i.as<int32_t>(), g->w_C_k.as<uint32_t>(), &nl))
-    return r;
-  CK(cudaEventRecord(g->ev[1], g->stream));
-  // A5: intra-batch all-pairs -> new rows n_t .. n_t+B-1
-  CK(launch_allpairs(g->geom, sv, g->ids, g->keys, k, n_t, B, g->w_C_i.as<int32_t>(), g->w_C_k.as<uint32_t>(),
-                     g->stream));
-  ++nl;
-  CK(cudaEventRecord(g->ev[2], g->stream));
-  // A6: update balls over the snapshot -> proposals
   BallArgs ba;
   memset(&ba, 0, sizeof ba);
   ba.st = sv;
@@ -433,38 +435,138 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   ba.k = k;
   ba.n_t = n_t;
   ba.B = B;
+  ba.q0 = q_lo;
+  ba.nqb = nqb;
   ba.depth = p->depth;
-  ba.C = g->w_C_i.as<int32_t>();
+  ba.C = Ci;
   ba.hash = g->w_hash.as<int32_t>();
   ba.hcap = hcap;
   ba.list = g->w_list.as<int32_t>();
   ba.ballmax = (int)ballmax;
-  ba.props = g->w_props.as<int2>();
-  ba.prop_cnt = g->w_prop_cnt.as<int32_t>();
+  ba.props = props;
+  ba.prop_cnt = prop_cnt;
   ba.stats = g->w_stats.as<unsigned long long>();
   CK(launch_ball(g->geom, ba, bslots, g->stream));
-  ++nl;
-  CK(cudaEventRecord(g->ev[3], g->stream));
-  // A7: ordered merge of the proposals into the snapshot rows
-  CK(launch_merge_props(g->metric, g->ids, g->keys, k, n_t, B, g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(),
-                        (int)ballmax, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->w_sorted.as<int2>(), g->stream, &nl));
+  ++*nl;
+  return 0;
+}
+
+static int stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, const int2 *props_all,
+                        const int32_t *prop_cnt_all, int *nl) {
+  const int64_t B = g->pend_B, n_t = g->n;
+  if (B == 0) return 0;
+  const int64_t ballmax = ball_bound(n_t, g->k, p->depth);
+  CK(g->w_sorted.ensure((size_t)nq_slots * ballmax * 8));
+  // A7: row_v = top-k(row_v u proposals), proposal (slot b) carries the new id n_t + b
+  CK(launch_merge_props(g->metric, g->ids, g->keys, g->k, n_t, nq_slots, props_all, prop_cnt_all, (int)ballmax,
+                        g->ncnt, g->nfill, g->noff, g->scan_tmp, g->w_sorted.as<int2>(), g->stream, nl));
   // A8: placement at the nearest medoid
   if (g->P > 0) {
-    CK(launch_place(g->geom, sv, n_t, B, g->P, g->medoids, g->members, g->cap, g->member_cnt, g->part_of,
-                    g->local_idx, g->w_target.as<int32_t>(), g->stream));
-    nl += 2;
+    CK(g->w_target.ensure((size_t)B * 4));
+    CK(launch_place(g->geom, graph_store_view(g), n_t, B, g->P, g->medoids, g->members, g->cap, g->member_cnt,
+                    g->part_of, g->local_idx, g->w_target.as<int32_t>(), g->stream));
+    *nl += 2;
   }
-  CK(cudaEventRecord(g->ev[4], g->stream));
+  g->n = n_t + B;
+  g->pend_B = 0;
+  return 0;
+}
+
+static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t B) {
   unsigned long long h[16];
   CK(cudaMemcpyAsync(h, g->w_stats.p, 16 * 8, cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
   h[6] = (unsigned long long)(B * (B - 1));
-  if (getenv("KNNG_PROFILE"))
+  if (getenv("KNNG_PROFILE") && B > 0)
     fprintf(stderr, "KNNG_PROFILE cycles/task: consumer %.0f ring-wait %.0f walk %.0f | producer work %.0f wait %.0f | windows/task %.1f\n",
             (double)h[8] / B, (double)h[9] / B, (double)h[10] / B, (double)h[11] / B, (double)h[12] / B, (double)h[13] / B);
-  g->n = n_t + B;
-  fill_stats(g, st, h, nl, 5);
-  return KNNG_OK;
+  fill_stats(g, st, h, nl, nev);
+  return 0;
+}
+
+int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,
+                       knng_stats *st) {
+  knng_err_slot().clear();
+  if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: null graph");
+  if (first_id_out) *first_id_out = g->n;
+  CK(cudaSetDevice(g->device));
+  CK(g->w_stats.ensure(16 * 8));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  const int64_t B = pts ? pts->n : 0, k = g->k;
+  const int Pn = g->P > 0 ? g->P : 1;
+  CK(g->w_cand_i.ensure((size_t)std::max<int64_t>(B, 1) * Pn * k * 4));
+  CK(g->w_cand_k.ensure((size_t)std::max<int64_t>(B, 1) * Pn * k * 4));
+  int nl = 0;
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  if (int r = stage_search(g, pts, p, 0, Pn, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl)) return r;
+  if (B == 0) {
+    g->pend_B = 0;
+    return finish_stats(g, st, 0, 0, 0);
+  }
+  const int64_t ballmax = ball_bound(g->n, g->k, p->depth);
+  CK(g->w_props.ensure((size_t)B * ballmax * 8));
+  CK(g->w_prop_cnt.ensure((size_t)B * 4));
+  if (int r = stage_update(g, p, 1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), 0, B,
+                           g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), &nl, true))
+    return r;
+  CK(cudaEventRecord(g->ev[3], g->stream));
+  if (int r = stage_commit(g, p, B, g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), &nl)) return r;
+  CK(cudaEventRecord(g->ev[4], g->stream));
+  return finish_stats(g, st, nl, 5, B);
+}
+
+// ---- the stages as C-ABI calls (multi-GPU building blocks; device buffers) ----
+int64_t graph_ball_bound(const knng_graph *g, int32_t depth) {
+  if (!g || depth < 1) return -1;
+  return ball_bound(g->n, g->k, depth);
+}
+
+int graph_insert_stage_search(knng_graph *g, const knng_points *pts, const knng_params *p, int32_t part_lo,
+                              int32_t part_hi, int32_t *cand_ids, uint32_t *cand_keys, knng_stats *st) {
+  knng_err_slot().clear();
+  if (!g) return fail(KNNG_ERR_INVALID_ARG, "stage_search: null graph");
+  if (g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_search: a staged batch is pending");
+  CK(cudaSetDevice(g->device));
+  CK(g->w_stats.ensure(16 * 8));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  int nl = 0;
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  if (int r = stage_search(g, pts, p, part_lo, part_hi, cand_ids, cand_keys, &nl)) {
+    g->pend_B = 0;
+    return r;
+  }
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  return finish_stats(g, st, nl, 2, 0);
+}
+
+int graph_insert_stage_update(knng_graph *g, const knng_params *p, int32_t world, const int32_t *cand_ids_all,
+                              const uint32_t *cand_keys_all, int64_t q_lo, int64_t q_hi, int32_t *props,
+                              int32_t *prop_cnt, knng_stats *st) {
+  knng_err_slot().clear();
+  if (!g || !p) return fail(KNNG_ERR_INVALID_ARG, "stage_update: null argument");
+  if (world < 1 || q_lo < 0 || q_hi < q_lo || q_hi > g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_update: bad range");
+  CK(cudaSetDevice(g->device));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  int nl = 0;
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  if (int r = stage_update(g, p, world, cand_ids_all, cand_keys_all, q_lo, q_hi, (int2 *)props, prop_cnt, &nl, false))
+    return r;
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  return finish_stats(g, st, nl, 2, 0);
+}
+
+int graph_insert_stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, const int32_t *props_all,
+                              const int32_t *prop_cnt_all, knng_stats *st) {
+  knng_err_slot().clear();
+  if (!g || !p) return fail(KNNG_ERR_INVALID_ARG, "stage_commit: null argument");
+  if (nq_slots < g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_commit: fewer query slots than the batch");
+  CK(cudaSetDevice(g->device));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  int nl = 0;
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  if (int r = stage_commit(g, p, nq_slots, (const int2 *)props_all, prop_cnt_all, &nl)) return r;
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  return finish_stats(g, st, nl, 2, 0);
 }
 
 int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_params *p, int32_t *ids_out,
@@ -522,7 +624,18 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
     ok = g->w_C_k.as<uint32_t>();
   }
   CK(cudaEventRecord(g->ev[0], g->stream));
-  if (int r = run_search_phase(g, qs, 0, nq, 0, kr, p, d_starts, nstarts, oi, ok, &nl)) return r;
+  if (g->P > 0) {
+    CK(g->w_cand_i.ensure((size_t)nq * g->P * kr * 4));
+    CK(g->w_cand_k.ensure((size_t)nq * g->P * kr * 4));
+    if (int r = run_search_phase(g, qs, 0, nq, 0, kr, p, d_starts, nstarts, 0, g->P, g->w_cand_i.as<int32_t>(),
+                                 g->w_cand_k.as<uint32_t>(), &nl))
+      return r;
+    CK(launch_merge_parts(g->metric, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), nq, g->P, 1, kr, oi, ok,
+                          g->stream));
+    ++nl;
+  } else {
+    if (int r = run_search_phase(g, qs, 0, nq, 0, kr, p, d_starts, nstarts, 0, 1, oi, ok, &nl)) return r;
+  }
   CK(cudaEventRecord(g->ev[1], g->stream));
   if (!out_on_device) {
     CK(cudaMemcpyAsync(ids_out, oi, (size_t)nq * kr * 4, cudaMemcpyDeviceToHost, g->stream));

@@ -47,6 +47,7 @@ struct DBuf {
 struct knng_graph {
   int metric = 0, dim = 0, k = 0;
   int64_t n = 0, cap = 0;
+  int64_t pend_B = 0;                           // batch ingested by stage_search, not yet committed
   knng::VecGeom geom{};
   int device = 0;
   cudaStream_t stream = nullptr;

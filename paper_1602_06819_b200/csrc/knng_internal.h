@@ -25,8 +25,10 @@ struct SearchArgs {
   int64_t n_t;
   int64_t nq;
   int64_t pid_base;            // RNG point id of query b = pid_base + b
-  // partitions (P == 0: unpartitioned, pool = 0..n_t-1)
+  // partitions (P == 0: unpartitioned, pool = 0..n_t-1); this launch searches partitions
+  // [part_lo, part_lo + part_cnt) (part_lo = 0, part_cnt = 1 when unpartitioned)
   int P;
+  int part_lo, part_cnt;
   const int32_t *members;      // [P][member_cap]
   int64_t member_cap;
   const int64_t *member_cnt;   // [P] (device)
@@ -45,7 +47,7 @@ struct SearchArgs {
   int64_t bits_words;          // evaluated + expanded words per task slot
   int smem_bits;               // 1: bitmaps in dynamic shared memory
   // outputs
-  int32_t *out_ids;            // [nq][max(P,1)][kr]
+  int32_t *out_ids;            // [nq][part_cnt][kr]
   uint32_t *out_keys;
   unsigned long long *stats;   // [0] evals [1] starts [2] skipped [3] expansions
   unsigned long long *prof;    // optional cycle counters (KNNG_PROFILE=1), else null
@@ -59,7 +61,9 @@ struct BallArgs {
   int64_t n_t;
   int64_t B;
   int depth;
-  const int32_t *C;            // search results [B][k]
+  const int32_t *C;            // search results [B][k] (all B queries of the batch)
+  int64_t q0;                  // this launch handles queries q0 .. q0+nqb-1 (props index is local)
+  int64_t nqb;
   int32_t *hash;               // per warp slot, hcap entries
   int hcap;
   int32_t *list;               // per warp slot, ballmax entries
@@ -71,8 +75,9 @@ struct BallArgs {
 
 // Launchers (return cudaError_t of the launch)
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch);
+// gathered candidates: rank-major [world][nq][P/world][kr]
 cudaError_t launch_merge_parts(int metric, const int32_t *cand_ids, const uint32_t *cand_keys, int64_t nq,
-                               int P, int kr, int32_t *out_ids, uint32_t *out_keys, cudaStream_t s);
+                               int P, int world, int kr, int32_t *out_ids, uint32_t *out_keys, cudaStream_t s);
 cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int32_t *ids, uint32_t *keys, int k,
                             int64_t n_t, int64_t B, const int32_t *C_ids, const uint32_t *C_keys,
                             cudaStream_t s);

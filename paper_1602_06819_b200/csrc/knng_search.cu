@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
   uint32_t *sbits = qscr + (M == M_JAC ? 2 * QMAX : 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nprod = (blockDim.x >> 5) - 1;
-  const int Pn = a.P > 0 ? a.P : 1;
+  const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   uint32_t *bits = a.smem_bits ? sbits : a.gbits + (int64_t)blockIdx.x * a.bits_words;
   const int k = a.k;
@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
 
   for (int64_t task = blockIdx.x; task < T; task += gridDim.x) {
     const int64_t b = task / Pn;
-    const int p = (int)(task % Pn);
+    const int pl = (int)(task % Pn);          // output slot
+    const int p = a.part_lo + pl;             // partition searched
     const int64_t m = a.P > 0 ? a.member_cnt[p] : a.n_t;
     const int32_t *pool = a.P > 0 ? a.members + (size_t)p * a.member_cap : nullptr;
     const int64_t words = (m + 31) >> 5;
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
     if (lane == 0) hdr->done = 1;
     s_evals += c;
     if (lane < a.kr) {
-      const size_t o = ((size_t)b * Pn + p) * a.kr + lane;
+      const size_t o = ((size_t)b * Pn + pl) * a.kr + lane;
       a.out_ids[o] = lane < top.cnt ? top.id : -1;
       a.out_keys[o] = lane < top.cnt ? top.key : 0u;
     }
@@ -340,17 +341,21 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
   }
 }
 
-// K2: keep the k_r best of the P*k_r per-partition candidates (Alg. 3 "Keep k most similar").
+// K2: keep the k_r best of the P*k_r per-partition candidates (Alg. 3 "Keep k most similar",
+// P:176).  Input is rank-major [world][nq][P/world][kr] (world = 1: [nq][P][kr]), the layout an
+// all-gather of the per-rank candidate buffers produces.
 template <int M>
-__global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq, int P, int kr,
+__global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq, int P, int world, int kr,
                               int32_t *oi, uint32_t *ok) {
   const int lane = threadIdx.x & 31;
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
+  const int Pown = P / world;
   WarpTopK<M> top;
   top.init(kr);
   for (int p = 0; p < P; ++p) {
-    const size_t o = ((size_t)q * P + p) * kr;
+    const int r = p / Pown, j = p % Pown;
+    const size_t o = (((size_t)r * nq + q) * Pown + j) * kr;
     const int32_t id = lane < kr ? ci[o + lane] : -1;
     const uint32_t key = lane < kr ? ck[o + lane] : 0u;
     top.insert(id >= 0, key, id);
@@ -363,7 +368,7 @@ __global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq,
 
 template <int M, int L, int CPL>
 static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
-  const int Pn = a.P > 0 ? a.P : 1;
+  const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   if (T == 0) return cudaSuccess;
   const int warps = a.starts ? 1 : 2;          // consumer + producers
@@ -393,13 +398,13 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_merge_parts(int metric, const int32_t *ci, const uint32_t *ck, int64_t nq, int P, int kr,
+cudaError_t launch_merge_parts(int metric, const int32_t *ci, const uint32_t *ck, int64_t nq, int P, int world, int kr,
                                int32_t *oi, uint32_t *ok, cudaStream_t s) {
   if (nq == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((nq + 3) / 4);
-  if (metric == M_U8) k_merge_parts<M_U8><<<blocks, 128, 0, s>>>(ci, ck, nq, P, kr, oi, ok);
-  else if (metric == M_F32) k_merge_parts<M_F32><<<blocks, 128, 0, s>>>(ci, ck, nq, P, kr, oi, ok);
-  else k_merge_parts<M_JAC><<<blocks, 128, 0, s>>>(ci, ck, nq, P, kr, oi, ok);
+  if (metric == M_U8) k_merge_parts<M_U8><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
+  else if (metric == M_F32) k_merge_parts<M_F32><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
+  else k_merge_parts<M_JAC><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
   return cudaGetLastError();
 }
 

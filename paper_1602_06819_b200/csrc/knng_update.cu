@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
   int32_t *list = a.list + gw * a.ballmax;
   const int k = a.k;
   unsigned long long s_ball = 0, s_prop = 0;
-  for (int64_t b = gw; b < a.B; b += nw) {
+  for (int64_t bl = gw; bl < a.nqb; bl += nw) {
+    const int64_t b = a.q0 + bl;             // query of the batch; proposals are stored at slot bl
     for (int i = lane; i < a.hcap; i += 32) hash[i] = -1;
     if (lane == 0) s_n[wib] = 0;
     __syncwarp();
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
     }
     int lo = 0, hi = s_n[wib];
     int np = 0;
-    int2 *props = a.props + (size_t)b * a.ballmax;
+    int2 *props = a.props + (size_t)bl * a.ballmax;
     for (int d = 1; d <= a.depth; ++d) {
       for (int base = lo; base < hi; base += 32) {
         const int t = base + lane;
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
     }
     s_ball += (unsigned long long)lo;
     s_prop += np;
-    if (lane == 0) a.prop_cnt[b] = np;
+    if (lane == 0) a.prop_cnt[bl] = np;
     __syncwarp();
   }
   if (lane == 0) {
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
 
 template <int M, int L, int CPL>
 static cudaError_t run_ball(const BallArgs &a, int64_t nslots, cudaStream_t s) {
-  if (a.B == 0) return cudaSuccess;
+  if (a.nqb == 0) return cudaSuccess;
   const int64_t blocks = nslots / 4;
   k_ball<M, L, CPL><<<(unsigned)blocks, 128, 0, s>>>(a);
   return cudaGetLastError();

@@ -1,0 +1,140 @@
+"""Multi-GPU online insert for partitioned graphs (Alg. 3 + Alg. 5 across ranks).
+
+One process per GPU (torchrun), every rank holding a full replica of the graph and making the same
+calls with the same inputs.  A batch is inserted in the three C-ABI stages of include/knng.h with
+two all-gathers in between (torch.distributed, NCCL over NVLink on a GPU box):
+
+  1. graph_insert_stage_search  -- this rank's partitions [r P/G, (r+1) P/G)      -> cand [B][P/G][k]
+  2. all-gather cand                                                          -> [G][B][P/G][k]
+  3. graph_insert_stage_update  -- merge (identical everywhere), new rows, balls of the query shard
+  4. all-gather proposals (S = ceil(B/G) slots per rank)                      -> [G*S][ballmax]
+  5. graph_insert_stage_commit  -- apply all proposals, place the points (identical everywhere)
+
+The exchange carries B*P*k*8 + G*S*ballmax*8 bytes per batch (C3: 5.2 MB + 7.2 MB), the only
+data-path collectives of the path.  Results are identical for every G (tested by emulating G ranks
+on one GPU, and the decomposition itself on CPU with gloo + the oracle).
+"""
+from __future__ import annotations
+
+import torch
+
+
+def owned_partitions(P, world, rank):
+    """Partitions [lo, hi) searched by `rank` (P must be a multiple of the world size)."""
+    if P % world:
+        raise ValueError("P=%d is not a multiple of the world size %d" % (P, world))
+    per = P // world
+    return rank * per, (rank + 1) * per
+
+
+def query_shard(B, world, rank):
+    """Queries [lo, hi) whose update balls `rank` runs, and the equal per-rank slot count S."""
+    S = -(-B // world) if B else 0
+    lo = min(rank * S, B)
+    return lo, min(lo + S, B), S
+
+
+class TorchComm:
+    """All-gather along dim 0 over a torch.distributed process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def allgather(self, t):
+        t = t.contiguous()
+        out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        if t.is_cuda:
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+        else:   # gloo (CPU tests)
+            parts = [torch.empty_like(t) for _ in range(self.world)]
+            self.dist.all_gather(parts, t, group=self.group)
+            out = torch.cat(parts, 0)
+        return out
+
+
+def _i32(n_elems_shape, device):
+    return torch.empty(n_elems_shape, dtype=torch.int32, device=device)
+
+
+def _sync():
+    """Buffers made by torch (its stream) are consumed by the library (its own stream)."""
+    if torch.cuda.is_available():
+        torch.cuda.current_stream().synchronize()
+
+
+class DistributedGraph:
+    """A rank's replica of a partitioned graph (KnngGraph) plus the communicator of the job."""
+
+    def __init__(self, graph, comm):
+        self.g = graph
+        self.comm = comm
+
+    def insert_batch(self, points, speedup, e_num, e_den, depth, seed):
+        _, med = self.g.partition()
+        if med is None:
+            raise ValueError("the multi-GPU insert needs a partitioned graph (partition_kmedoids)")
+        return insert_batch_staged([self.g], [self.comm.rank], self.comm.world, points, speedup, e_num, e_den,
+                                   depth, seed, len(med), allgather=self.comm.allgather)
+
+
+def insert_batch_staged(graphs, ranks, world, points, speedup, e_num, e_den, depth, seed, P, allgather=None):
+    """Run the three stages for the replicas `graphs` (one per entry of `ranks`) of a `world`-rank job.
+
+    With one replica per process, `allgather` is the communicator's all-gather.  With every rank's
+    replica in this process (emulation on one GPU: len(graphs) == world), the gathers are the
+    concatenation of the ranks' buffers in rank order -- the same layout an all-gather produces;
+    nothing waits on another launch.
+    Returns the per-replica stage stats.
+    """
+    B = len(points)
+    k = graphs[0].k
+    dev = "cuda"
+    Peff = P if P > 0 else 1
+    wsearch = world if P > 0 else 1           # unpartitioned graphs: every rank searches everything
+    ballmax = graphs[0].ball_bound(depth)
+    stats = [dict() for _ in graphs]
+
+    def gather(bufs):
+        if allgather is not None:
+            return allgather(bufs[0])
+        return torch.cat(bufs, 0)
+
+    # 1-2: per-rank partition searches, all-gather of the candidates
+    cis, cks = [], []
+    _sync()
+    for i, (g, r) in enumerate(zip(graphs, ranks)):
+        lo, hi = owned_partitions(Peff, wsearch, r % wsearch) if P > 0 else (0, 1)
+        ci = _i32((B, hi - lo, k), dev)
+        ck = _i32((B, hi - lo, k), dev)
+        stats[i]["search"] = g.stage_search(points, speedup, e_num, e_den, depth, seed, lo, hi, ci, ck)
+        cis.append(ci)
+        cks.append(ck)
+    if P > 0:
+        ci_all, ck_all = gather(cis), gather(cks)
+        _sync()
+    else:
+        ci_all, ck_all = cis[0], cks[0]
+    # 3-4: merge + new rows + balls of the query shard, all-gather of the proposals
+    props_l, cnt_l = [], []
+    S = query_shard(B, world, 0)[2]
+    bufs = [(torch.zeros((S, ballmax, 2), dtype=torch.int32, device=dev), torch.zeros((S,), dtype=torch.int32,
+                                                                                        device=dev)) for _ in graphs]
+    _sync()
+    for i, (g, r) in enumerate(zip(graphs, ranks)):
+        qlo, qhi, _ = query_shard(B, world, r)
+        props, cnt = bufs[i]
+        stats[i]["update"] = g.stage_update(speedup, e_num, e_den, depth, seed, wsearch if P > 0 else 1,
+                                            ci_all if P > 0 else cis[i], ck_all if P > 0 else cks[i], qlo, qhi,
+                                            props, cnt)
+        props_l.append(props)
+        cnt_l.append(cnt)
+    props_all, cnt_all = gather(props_l), gather(cnt_l)
+    _sync()
+    # 5: commit everywhere
+    for i, g in enumerate(graphs):
+        stats[i]["commit"] = g.stage_commit(speedup, e_num, e_den, depth, seed, props_all.shape[0], props_all, cnt_all)
+    return stats

@@ -55,7 +55,8 @@ class knng_runtime(C.Structure):
 
 
 EXPORTS = ["graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
-           "graph_get_partition", "graph_size", "graph_degree", "graph_free", "graph_last_error"]
+           "graph_get_partition", "graph_size", "graph_degree", "graph_free", "graph_last_error",
+           "graph_ball_bound", "graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit"]
 
 _lib = None
 
@@ -84,6 +85,15 @@ def load_library(path=LIB_PATH):
     L.graph_free.argtypes = [P]
     L.graph_free.restype = None
     L.graph_last_error.restype = C.c_char_p
+    L.graph_ball_bound.argtypes = [P, C.c_int32]
+    L.graph_ball_bound.restype = C.c_int64
+    L.graph_insert_stage_search.argtypes = [P, C.POINTER(knng_points), C.POINTER(knng_params), C.c_int32,
+                                            C.c_int32, P, P, C.POINTER(knng_stats)]
+    L.graph_insert_stage_update.argtypes = [P, C.POINTER(knng_params), C.c_int32, P, P, C.c_int64, C.c_int64, P, P,
+                                            C.POINTER(knng_stats)]
+    L.graph_insert_stage_commit.argtypes = [P, C.POINTER(knng_params), C.c_int64, P, P, C.POINTER(knng_stats)]
+    for f in ("graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit"):
+        getattr(L, f).restype = C.c_int
     for f in ("graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
               "graph_get_partition"):
         getattr(L, f).restype = C.c_int
@@ -220,6 +230,38 @@ class KnngGraph:
                                            ids.ctypes.data_as(C.c_void_p), keys.ctypes.data_as(C.c_void_p), 0,
                                            C.byref(st)))
         return ids, keys, st.as_dict()
+
+    # ---- staged insert (multi-GPU building blocks; torch CUDA tensors) ----
+    def ball_bound(self, depth):
+        return int(load_library().graph_ball_bound(self._h, int(depth)))
+
+    def stage_search(self, points, speedup, e_num, e_den, depth, seed, part_lo, part_hi, cand_ids, cand_keys):
+        p, keep = make_points(points)
+        prm, _ = make_params(speedup, e_num, e_den, depth, seed)
+        st = knng_stats()
+        _check(load_library().graph_insert_stage_search(self._h, C.byref(p), C.byref(prm), int(part_lo), int(part_hi),
+                                                        C.c_void_p(cand_ids.data_ptr()),
+                                                        C.c_void_p(cand_keys.data_ptr()), C.byref(st)))
+        return st.as_dict()
+
+    def stage_update(self, speedup, e_num, e_den, depth, seed, world, cand_ids_all, cand_keys_all, q_lo, q_hi, props,
+                     prop_cnt):
+        prm, _ = make_params(speedup, e_num, e_den, depth, seed)
+        st = knng_stats()
+        _check(load_library().graph_insert_stage_update(self._h, C.byref(prm), int(world),
+                                                        C.c_void_p(cand_ids_all.data_ptr()),
+                                                        C.c_void_p(cand_keys_all.data_ptr()), int(q_lo), int(q_hi),
+                                                        C.c_void_p(props.data_ptr()), C.c_void_p(prop_cnt.data_ptr()),
+                                                        C.byref(st)))
+        return st.as_dict()
+
+    def stage_commit(self, speedup, e_num, e_den, depth, seed, nq_slots, props_all, prop_cnt_all):
+        prm, _ = make_params(speedup, e_num, e_den, depth, seed)
+        st = knng_stats()
+        _check(load_library().graph_insert_stage_commit(self._h, C.byref(prm), int(nq_slots),
+                                                        C.c_void_p(props_all.data_ptr()),
+                                                        C.c_void_p(prop_cnt_all.data_ptr()), C.byref(st)))
+        return st.as_dict()
 
     def partition_kmedoids(self, P, imbalance, max_iter, seed, init_medoids=None):
         n = self.n

@@ -367,3 +367,44 @@ def test_jaccard_edge_sets():
     gi, gk = g.rows()
     oi, ok = o.rows()
     _assert_rows_equal(O.JAC, gi, gk, oi, ok, "jaccard edge insert")
+
+
+# ---------------------------------------------------------------------------
+# Multi-GPU decomposition (Alg. 3 + Alg. 5 over G ranks), G ranks emulated on one GPU: every
+# replica must equal the single-GPU graph (and the oracle) for G = 1, 2, 4, 8
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_multi_rank_stages_are_G_invariant(name):
+    from paper_1602_06819_b200.dist import insert_batch_staged
+    n0 = 6000 if name == "C3" else 2500
+    cfg = _cfg_small(name, n0=n0, n_insert=700)
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    cap = cfg.n0 + cfg.n_insert + 8
+    ref = _graph(X, cfg.k, cap)
+    ref.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cap)
+    o.init_exact()
+    op, om, _ = o.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+    o.set_partition(op, om)
+    batches = [(0, 300), (300, 301), (301, 700)]
+    for lo, hi in batches:
+        ref.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        o.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+    ri, rk = ref.rows()
+    oi, ok = o.rows()
+    _assert_rows_equal(cfg.metric, ri, rk, oi, ok, "single-GPU reference")
+    for G in (1, 2, 4, 8):
+        reps = [_graph(X, cfg.k, cap) for _ in range(G)]
+        for g in reps:
+            g.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+        for lo, hi in batches:
+            insert_batch_staged(reps, list(range(G)), G, S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth,
+                                cfg.search_seed, cfg.P)
+        for r, g in enumerate(reps):
+            gi, gk = g.rows()
+            _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "G=%d rank %d" % (G, r))
+            gpart, _ = g.partition()
+            assert (gpart == o.part_of[:o.n]).all()
+        for g in reps:
+            g.close()
