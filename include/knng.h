@@ -164,8 +164,9 @@ int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, int32_t max_i
  * graph_insert_batch == stage_search(all partitions) + stage_update(world 1, all queries) +
  * stage_commit.  With G ranks each holding a full replica of the graph (same inputs, same calls),
  * the distributed insert of Alg. 5 is, on every rank r:
- *   1. graph_insert_stage_search over the rank's partitions [r*P/G, (r+1)*P/G): it ingests the batch
- *      (rows n_t..n_t+B-1) and writes cand [B][P/G][k] (ids int32, keys uint32; -1/0 padded);
+ *   1. graph_insert_stage_search over the rank's partitions [r*P/G, (r+1)*P/G) and all queries
+ *      (q_lo = q_hi = -1): it ingests the batch (rows n_t..n_t+B-1) and writes cand [B][P/G][k]
+ *      (ids int32, keys uint32; -1/0 padded);
  *   2. all-gather cand over the ranks -> [G][B][P/G][k] (rank-major) ("the compute nodes send the
  *      k.p candidates", Alg. 3);
  *   3. graph_insert_stage_update(world = G, gathered cand, query shard [q_lo, q_hi)): merges the
@@ -176,11 +177,15 @@ int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, int32_t max_i
  *   5. graph_insert_stage_commit(nq_slots = G*S): applies every proposal (slot b proposes id n_t + b)
  *      and places the new points; the replicas stay bit-identical, and the result equals the single-GPU
  *      call for every G.
+ * Unpartitioned graphs shard the queries instead: stage_search(part [0,1), queries [r*S, r*S+S) of the
+ * batch) writes cand [S][1][k]; the all-gather gives [G*S][k] whose row b is query b; stage_update is
+ * then called with world = 1 and that buffer (the batch of G*S_local points is one snapshot batch).
  * ballmax = graph_ball_bound(g, depth) evaluated BEFORE stage_search (it depends on n_t).
  * Errors: INVALID_ARG (bad ranges, a pending batch, P % G != 0), CAPACITY_EXCEEDED, OOM, CUDA. */
 int64_t graph_ball_bound(const knng_graph *g, int32_t depth);
 int graph_insert_stage_search(knng_graph *g, const knng_points *pts, const knng_params *p, int32_t part_lo,
-                              int32_t part_hi, int32_t *cand_ids, uint32_t *cand_keys, knng_stats *st);
+                              int32_t part_hi, int64_t q_lo, int64_t q_hi, int32_t *cand_ids, uint32_t *cand_keys,
+                              knng_stats *st);
 int graph_insert_stage_update(knng_graph *g, const knng_params *p, int32_t world, const int32_t *cand_ids_all,
                               const uint32_t *cand_keys_all, int64_t q_lo, int64_t q_hi, int32_t *props,
                               int32_t *prop_cnt, knng_stats *st);

@@ -376,7 +376,7 @@ static int64_t ball_bound(int64_t n_t, int k, int depth) {   // k + k^2 + ... + 
 }
 
 static int stage_search(knng_graph *g, const knng_points *pts, const knng_params *p, int part_lo, int part_hi,
-                        int32_t *ci, uint32_t *ck, int *nl) {
+                        int64_t q_lo, int64_t q_hi, int32_t *ci, uint32_t *ck, int *nl) {
   if (int r = check_points(pts, "insert")) return r;
   if (int r = check_params(p)) return r;
   if (pts->metric != g->metric || (g->metric != KNNG_JACCARD_U32SET && pts->dim != g->dim))
@@ -388,12 +388,16 @@ static int stage_search(knng_graph *g, const knng_points *pts, const knng_params
   if (n_t + B > g->cap)
     return fail(KNNG_ERR_CAPACITY_EXCEEDED, "capacity %lld exceeded (n=%lld, B=%lld)", (long long)g->cap,
                 (long long)n_t, (long long)B);
+  if (q_lo < 0) q_hi = B, q_lo = 0;          // all queries
+  if (q_hi > B || q_lo > q_hi) return fail(KNNG_ERR_INVALID_ARG, "bad query range");
   g->pend_B = B;
   if (B == 0) return 0;
   // A1: batch ingest into the store tail (ids n_t .. n_t+B-1)
   if (int r = store_points(g, pts, n_t)) return r;
-  // A2-A3: iGNNS per (point, partition) on the snapshot
-  return run_search_phase(g, graph_store_view(g), n_t, B, n_t, g->k, p, nullptr, 0, part_lo, part_hi, ci, ck, nl);
+  // A2-A3: iGNNS per (point, partition) on the snapshot, for queries [q_lo, q_hi)
+  if (q_hi == q_lo) return 0;
+  return run_search_phase(g, graph_store_view(g), n_t + q_lo, q_hi - q_lo, n_t + q_lo, g->k, p, nullptr, 0, part_lo,
+                          part_hi, ci, ck, nl);
 }
 
 static int stage_update(knng_graph *g, const knng_params *p, int world, const int32_t *ci_all, const uint32_t *ck_all,
@@ -498,7 +502,8 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   CK(g->w_cand_k.ensure((size_t)std::max<int64_t>(B, 1) * Pn * k * 4));
   int nl = 0;
   CK(cudaEventRecord(g->ev[0], g->stream));
-  if (int r = stage_search(g, pts, p, 0, Pn, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl)) return r;
+  if (int r = stage_search(g, pts, p, 0, Pn, -1, -1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl))
+    return r;
   if (B == 0) {
     g->pend_B = 0;
     return finish_stats(g, st, 0, 0, 0);
@@ -522,7 +527,8 @@ int64_t graph_ball_bound(const knng_graph *g, int32_t depth) {
 }
 
 int graph_insert_stage_search(knng_graph *g, const knng_points *pts, const knng_params *p, int32_t part_lo,
-                              int32_t part_hi, int32_t *cand_ids, uint32_t *cand_keys, knng_stats *st) {
+                              int32_t part_hi, int64_t q_lo, int64_t q_hi, int32_t *cand_ids, uint32_t *cand_keys,
+                              knng_stats *st) {
   knng_err_slot().clear();
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "stage_search: null graph");
   if (g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_search: a staged batch is pending");
@@ -531,7 +537,7 @@ int graph_insert_stage_search(knng_graph *g, const knng_points *pts, const knng_
   CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
   int nl = 0;
   CK(cudaEventRecord(g->ev[0], g->stream));
-  if (int r = stage_search(g, pts, p, part_lo, part_hi, cand_ids, cand_keys, &nl)) {
+  if (int r = stage_search(g, pts, p, part_lo, part_hi, q_lo, q_hi, cand_ids, cand_keys, &nl)) {
     g->pend_B = 0;
     return r;
   }

@@ -1,7 +1,8 @@
 """Multi-GPU online insert for partitioned graphs (Alg. 3 + Alg. 5 across ranks).
 
 One process per GPU (torchrun), every rank holding a full replica of the graph and making the same
-calls with the same inputs.  A batch is inserted in the three C-ABI stages of include/knng.h with
+calls with the same inputs.  Partitioned graphs shard the P partition searches (below);
+unpartitioned graphs shard the queries of the batch instead (same stages, cand gathered by query).  A batch is inserted in the three C-ABI stages of include/knng.h with
 two all-gathers in between (torch.distributed, NCCL over NVLink on a GPU box):
 
   1. graph_insert_stage_search  -- this rank's partitions [r P/G, (r+1) P/G)      -> cand [B][P/G][k]
@@ -75,15 +76,15 @@ class DistributedGraph:
 
     def insert_batch(self, points, speedup, e_num, e_den, depth, seed):
         _, med = self.g.partition()
-        if med is None:
-            raise ValueError("the multi-GPU insert needs a partitioned graph (partition_kmedoids)")
         return insert_batch_staged([self.g], [self.comm.rank], self.comm.world, points, speedup, e_num, e_den,
-                                   depth, seed, len(med), allgather=self.comm.allgather)
+                                   depth, seed, 0 if med is None else len(med), allgather=self.comm.allgather)
 
 
 def insert_batch_staged(graphs, ranks, world, points, speedup, e_num, e_den, depth, seed, P, allgather=None):
     """Run the three stages for the replicas `graphs` (one per entry of `ranks`) of a `world`-rank job.
 
+    Partitioned graphs (P > 0) shard the partitions (Alg. 3); unpartitioned graphs shard the
+    queries of the batch (every replica holds the whole graph; the batch is one snapshot batch).
     With one replica per process, `allgather` is the communicator's all-gather.  With every rank's
     replica in this process (emulation on one GPU: len(graphs) == world), the gathers are the
     concatenation of the ranks' buffers in rank order -- the same layout an all-gather produces;
@@ -93,9 +94,8 @@ def insert_batch_staged(graphs, ranks, world, points, speedup, e_num, e_den, dep
     B = len(points)
     k = graphs[0].k
     dev = "cuda"
-    Peff = P if P > 0 else 1
-    wsearch = world if P > 0 else 1           # unpartitioned graphs: every rank searches everything
     ballmax = graphs[0].ball_bound(depth)
+    S = query_shard(B, world, 0)[2]
     stats = [dict() for _ in graphs]
 
     def gather(bufs):
@@ -103,36 +103,37 @@ def insert_batch_staged(graphs, ranks, world, points, speedup, e_num, e_den, dep
             return allgather(bufs[0])
         return torch.cat(bufs, 0)
 
-    # 1-2: per-rank partition searches, all-gather of the candidates
+    # 1-2: searches (partition-sharded, or query-sharded), all-gather of the candidates
     cis, cks = [], []
+    for g, r in zip(graphs, ranks):
+        if P > 0:
+            lo, hi = owned_partitions(P, world, r)
+            cis.append(torch.full((B, hi - lo, k), -1, dtype=torch.int32, device=dev))
+            cks.append(torch.zeros((B, hi - lo, k), dtype=torch.int32, device=dev))
+        else:
+            cis.append(torch.full((S, 1, k), -1, dtype=torch.int32, device=dev))
+            cks.append(torch.zeros((S, 1, k), dtype=torch.int32, device=dev))
     _sync()
     for i, (g, r) in enumerate(zip(graphs, ranks)):
-        lo, hi = owned_partitions(Peff, wsearch, r % wsearch) if P > 0 else (0, 1)
-        ci = _i32((B, hi - lo, k), dev)
-        ck = _i32((B, hi - lo, k), dev)
-        stats[i]["search"] = g.stage_search(points, speedup, e_num, e_den, depth, seed, lo, hi, ci, ck)
-        cis.append(ci)
-        cks.append(ck)
-    if P > 0:
-        ci_all, ck_all = gather(cis), gather(cks)
-        _sync()
-    else:
-        ci_all, ck_all = cis[0], cks[0]
+        if P > 0:
+            lo, hi = owned_partitions(P, world, r)
+            stats[i]["search"] = g.stage_search(points, speedup, e_num, e_den, depth, seed, lo, hi, cis[i], cks[i])
+        else:
+            qlo, qhi, _ = query_shard(B, world, r)
+            stats[i]["search"] = g.stage_search(points, speedup, e_num, e_den, depth, seed, 0, 1, cis[i], cks[i],
+                                                qlo, qhi)
+    ci_all, ck_all = gather(cis), gather(cks)      # P > 0: [G][B][P/G][k]; else [G*S][1][k] (row b = query b)
     # 3-4: merge + new rows + balls of the query shard, all-gather of the proposals
-    props_l, cnt_l = [], []
-    S = query_shard(B, world, 0)[2]
-    bufs = [(torch.zeros((S, ballmax, 2), dtype=torch.int32, device=dev), torch.zeros((S,), dtype=torch.int32,
-                                                                                        device=dev)) for _ in graphs]
+    bufs = [(torch.zeros((S, ballmax, 2), dtype=torch.int32, device=dev),
+             torch.zeros((S,), dtype=torch.int32, device=dev)) for _ in graphs]
     _sync()
     for i, (g, r) in enumerate(zip(graphs, ranks)):
         qlo, qhi, _ = query_shard(B, world, r)
         props, cnt = bufs[i]
-        stats[i]["update"] = g.stage_update(speedup, e_num, e_den, depth, seed, wsearch if P > 0 else 1,
-                                            ci_all if P > 0 else cis[i], ck_all if P > 0 else cks[i], qlo, qhi,
-                                            props, cnt)
-        props_l.append(props)
-        cnt_l.append(cnt)
-    props_all, cnt_all = gather(props_l), gather(cnt_l)
+        stats[i]["update"] = g.stage_update(speedup, e_num, e_den, depth, seed, world if P > 0 else 1, ci_all, ck_all,
+                                            qlo, qhi, props, cnt)
+    props_all = gather([b[0] for b in bufs])
+    cnt_all = gather([b[1] for b in bufs])
     _sync()
     # 5: commit everywhere
     for i, g in enumerate(graphs):

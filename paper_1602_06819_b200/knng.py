@@ -88,7 +88,7 @@ def load_library(path=LIB_PATH):
     L.graph_ball_bound.argtypes = [P, C.c_int32]
     L.graph_ball_bound.restype = C.c_int64
     L.graph_insert_stage_search.argtypes = [P, C.POINTER(knng_points), C.POINTER(knng_params), C.c_int32,
-                                            C.c_int32, P, P, C.POINTER(knng_stats)]
+                                            C.c_int32, C.c_int64, C.c_int64, P, P, C.POINTER(knng_stats)]
     L.graph_insert_stage_update.argtypes = [P, C.POINTER(knng_params), C.c_int32, P, P, C.c_int64, C.c_int64, P, P,
                                             C.POINTER(knng_stats)]
     L.graph_insert_stage_commit.argtypes = [P, C.POINTER(knng_params), C.c_int64, P, P, C.POINTER(knng_stats)]
@@ -235,12 +235,13 @@ class KnngGraph:
     def ball_bound(self, depth):
         return int(load_library().graph_ball_bound(self._h, int(depth)))
 
-    def stage_search(self, points, speedup, e_num, e_den, depth, seed, part_lo, part_hi, cand_ids, cand_keys):
+    def stage_search(self, points, speedup, e_num, e_den, depth, seed, part_lo, part_hi, cand_ids, cand_keys,
+                     q_lo=-1, q_hi=-1):
         p, keep = make_points(points)
         prm, _ = make_params(speedup, e_num, e_den, depth, seed)
         st = knng_stats()
         _check(load_library().graph_insert_stage_search(self._h, C.byref(p), C.byref(prm), int(part_lo), int(part_hi),
-                                                        C.c_void_p(cand_ids.data_ptr()),
+                                                        int(q_lo), int(q_hi), C.c_void_p(cand_ids.data_ptr()),
                                                         C.c_void_p(cand_keys.data_ptr()), C.byref(st)))
         return st.as_dict()
 

@@ -408,3 +408,28 @@ def test_multi_rank_stages_are_G_invariant(name):
             assert (gpart == o.part_of[:o.n]).all()
         for g in reps:
             g.close()
+
+
+def test_query_sharded_unpartitioned_is_G_invariant():
+    """Unpartitioned graphs (C1 shape): the batch's queries are sharded over G ranks; the result
+    equals the single-GPU batch of the same points for every G."""
+    from paper_1602_06819_b200.dist import insert_batch_staged
+    cfg = _cfg_small("C1", n0=5000, n_insert=1500)
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    cap = cfg.n0 + cfg.n_insert + 8
+    ref = _graph(X, cfg.k, cap)
+    batches = [(0, 1024), (1024, 1025), (1025, 1500)]
+    for lo, hi in batches:
+        ref.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+    ri, rk = ref.rows()
+    for G in (2, 3, 8):
+        reps = [_graph(X, cfg.k, cap) for _ in range(G)]
+        for lo, hi in batches:
+            insert_batch_staged(reps, list(range(G)), G, S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth,
+                                cfg.search_seed, 0)
+        for r, g in enumerate(reps):
+            gi, gk = g.rows()
+            _assert_rows_equal(cfg.metric, gi, gk, ri, rk, "query-sharded G=%d rank %d" % (G, r))
+        for g in reps:
+            g.close()
