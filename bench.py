@@ -163,31 +163,58 @@ def run_ours(args, cfg):
     from paper_1602_06819_b200 import KnngGraph, load_library
     load_library()
     ws, rank, lrank = dist_env()
+    lrank = lrank % torch.cuda.device_count()      # (more ranks than GPUs only in plumbing tests)
     torch.cuda.set_device(lrank)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
-    B = cfg.batch
+        backend = os.environ.get("KNNG_DIST_BACKEND", "nccl")   # gloo: host-staged, plumbing tests only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+        else:
+            dist.init_process_group(backend)
+    B = cfg.batch                      # per-rank batch; the global batch of a step is ws * B points
+    GB = ws * B
     nsteps = args.warmup + args.steps
     X = D.initial_points(cfg)
-    S = D.stream_points(cfg, 0, max(cfg.n_insert, nsteps * B))
+    S = D.stream_points(cfg, 0, max(cfg.n_insert, nsteps * GB))
     V = cfg.dim if cfg.metric == D.U8 else 4 * cfg.dim
     stream = torch.cuda.Stream()
-    cap = cfg.n0 + nsteps * B + 8
+    cap = cfg.n0 + nsteps * GB + 8
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    comm = None
+    if ws > 1:
+        from paper_1602_06819_b200.dist import TorchComm, insert_batch_staged
+        comm = TorchComm()
 
     def barrier():
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
 
+    def step(graph, pts):
+        """One global batch: 1 GPU -> graph_insert_batch; N GPUs -> the batch's queries sharded over the
+        ranks (replicated graph), stage_search / all-gather / stage_update / all-gather / stage_commit."""
+        if ws == 1:
+            return graph.insert_batch(pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)[1]
+        with torch.cuda.stream(stream):
+            st = insert_batch_staged([graph], [rank], ws, pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth,
+                                     cfg.search_seed, 0, allgather=comm.allgather)[0]
+        out = {f: st["search"][f] + st["update"][f] + st["commit"][f]
+               for f in ("search_evals", "search_starts", "search_skipped", "search_expansions", "ball_nodes",
+                         "proposals", "kernel_launches")}
+        out["ms_search"] = st["search"]["ms_total"]
+        out["ms_allpairs"] = st["update"]["ms_total"]
+        out["ms_update"] = 0.0
+        out["ms_merge"] = st["commit"]["ms_total"]
+        return out
+
     # ---------------- device-resident inputs (value) ----------------
     g = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
     rows0 = g.rows() if (rank == 0 and ws == 1 and not args.no_cpu_baseline) else None
-    S_dev = torch.from_numpy(S[:nsteps * B]).to("cuda")
+    S_dev = torch.from_numpy(S[:nsteps * GB]).to("cuda")
     pos = 0
     for _ in range(args.warmup):
-        g.insert_batch(S_dev[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
-        pos += B
+        step(g, S_dev[pos:pos + GB])
+        pos += GB
     ms_steps, stats = [], []
     barrier()
     with ClockSampler(lrank) as clk:
@@ -197,20 +224,20 @@ def run_ours(args, cfg):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            _, st = g.insert_batch(S_dev[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+            st = step(g, S_dev[pos:pos + GB])
             e1.record(stream)
             e1.synchronize()
             ms_steps.append(e0.elapsed_time(e1))
             stats.append(st)
-            pos += B
+            pos += GB
     barrier()
     t_total = sum(ms_steps) / 1000.0
     if ws > 1:
         t = torch.tensor([t_total], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_total = float(t.item())
-    value = args.steps * B * ws / t_total
-    evals = sum(s["search_evals"] + s["ball_nodes"] for s in stats)
+    value = args.steps * GB / t_total
+    evals = sum(s["search_evals"] + s["ball_nodes"] for s in stats) * ws
     ms_search = sum(s["ms_search"] for s in stats)
     bytes_search = sum(alg_bytes(s, V, cfg.k) for s in stats)
     peak, peak_src = hbm_peak()
@@ -235,17 +262,17 @@ def run_ours(args, cfg):
 
     # ---------------- end to end through the C ABI with host buffers (e2e) ----------------
     g2 = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
-    S_pin_t = torch.from_numpy(S[:nsteps * B]).pin_memory()
+    S_pin_t = torch.from_numpy(S[:nsteps * GB]).pin_memory()
     S_pin = S_pin_t.numpy()
     pos2 = 0
     for _ in range(args.warmup):
-        g2.insert_batch(S_pin[pos2:pos2 + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
-        pos2 += B
+        step(g2, S_pin[pos2:pos2 + GB])
+        pos2 += GB
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        g2.insert_batch(S_pin[pos2:pos2 + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
-        pos2 += B
+        step(g2, S_pin[pos2:pos2 + GB])
+        pos2 += GB
     barrier()
     t_e2e = time.perf_counter() - t0
     if ws > 1:
@@ -258,9 +285,12 @@ def run_ours(args, cfg):
         "metric": baseline_metric(), "value": value, "unit": "inserts/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": cfg_desc(cfg), "global_batch": B * ws, "parallelism": "replicas x%d" % ws,
+        "config": {"workload": cfg_desc(cfg), "global_batch": GB,
+                   "parallelism": "1 GPU" if ws == 1 else
+                   "dp%d: replicated graph, the global batch's queries sharded over ranks, NCCL all-gathers of "
+                   "candidates and proposals" % ws,
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
-        "similarities_per_s": evals * ws / t_total,
+        "similarities_per_s": evals / t_total,
         "recall_at_k": rec,
         "search_per_query": {f: sum(s_[f] for s_ in stats) / (len(stats) * B) for f in
                              ("search_evals", "search_starts", "search_skipped", "search_expansions", "ball_nodes",
@@ -272,7 +302,7 @@ def run_ours(args, cfg):
                      "note": "C1 is L2-resident (14 MB store): HBM fraction is not the binding claim"},
         "phase_ms": {p: sum(s[p] for s in stats) / len(stats) for p in ("ms_search", "ms_allpairs",
                                                                        "ms_update", "ms_merge")},
-        "e2e": {"value": args.steps * B * ws / t_e2e, "unit": "inserts/s", "h2d_bytes_per_step": B * V,
+        "e2e": {"value": args.steps * GB / t_e2e, "unit": "inserts/s", "h2d_bytes_per_step": GB * V,
                 "d2h_bytes_per_step": 16 * 8},
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -47,14 +47,15 @@ class TorchComm:
 
     def allgather(self, t):
         t = t.contiguous()
-        out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        if t.is_cuda:
+        if t.is_cuda and self.dist.get_backend(self.group) == "nccl":
+            out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
             self.dist.all_gather_into_tensor(out, t, group=self.group)
-        else:   # gloo (CPU tests)
-            parts = [torch.empty_like(t) for _ in range(self.world)]
-            self.dist.all_gather(parts, t, group=self.group)
-            out = torch.cat(parts, 0)
-        return out
+            return out
+        # gloo (CPU tests / plumbing tests): host-staged
+        h = t.cpu()
+        parts = [torch.empty_like(h) for _ in range(self.world)]
+        self.dist.all_gather(parts, h, group=self.group)
+        return torch.cat(parts, 0).to(t.device)
 
 
 def _i32(n_elems_shape, device):
