@@ -170,13 +170,15 @@ int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, int32_t max_i
  *   2. all-gather cand over the ranks -> [G][B][P/G][k] (rank-major) ("the compute nodes send the
  *      k.p candidates", Alg. 3);
  *   3. graph_insert_stage_update(world = G, gathered cand, query shard [q_lo, q_hi)): merges the
- *      candidates (identical on every rank), writes the B new rows, and runs the update balls of the
- *      shard into props int2[q_hi-q_lo][ballmax] (node, key) and prop_cnt int32[q_hi-q_lo];
- *   4. all-gather props / prop_cnt over equal-size shards (S = ceil(B/G) slots per rank, counts 0 in
- *      the padding) -> [G*S][ballmax], [G*S];
- *   5. graph_insert_stage_commit(nq_slots = G*S): applies every proposal (slot b proposes id n_t + b)
- *      and places the new points; the replicas stay bit-identical, and the result equals the single-GPU
- *      call for every G.
+ *      candidates (identical on every rank), computes the new rows of the shard's points (top-k of C_i
+ *      and the batch) into new_ids/new_keys [q_hi-q_lo][k] (NULL: straight into the graph, 1 GPU), and
+ *      runs the update balls of the shard into props int2[q_hi-q_lo][ballmax] (node, key) and
+ *      prop_cnt int32[q_hi-q_lo];
+ *   4. all-gather new rows, props, prop_cnt over equal-size shards (S = ceil(B/G) slots per rank,
+ *      counts 0 in the padding) -> [G*S][k], [G*S][ballmax], [G*S];
+ *   5. graph_insert_stage_commit(nq_slots = G*S, gathered buffers; new rows NULL if already in the
+ *      graph): writes the new rows, applies every proposal (slot b proposes id n_t + b) and places the
+ *      new points; the replicas stay bit-identical and equal the single-GPU call for every G.
  * Unpartitioned graphs shard the queries instead: stage_search(part [0,1), queries [r*S, r*S+S) of the
  * batch) writes cand [S][1][k]; the all-gather gives [G*S][k] whose row b is query b; stage_update is
  * then called with world = 1 and that buffer (the batch of G*S_local points is one snapshot batch).
@@ -188,9 +190,10 @@ int graph_insert_stage_search(knng_graph *g, const knng_points *pts, const knng_
                               knng_stats *st);
 int graph_insert_stage_update(knng_graph *g, const knng_params *p, int32_t world, const int32_t *cand_ids_all,
                               const uint32_t *cand_keys_all, int64_t q_lo, int64_t q_hi, int32_t *props,
-                              int32_t *prop_cnt, knng_stats *st);
+                              int32_t *prop_cnt, int32_t *new_ids, uint32_t *new_keys, knng_stats *st);
 int graph_insert_stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, const int32_t *props_all,
-                              const int32_t *prop_cnt_all, knng_stats *st);
+                              const int32_t *prop_cnt_all, const int32_t *new_ids_all, const uint32_t *new_keys_all,
+                              knng_stats *st);
 
 /* graph_get_rows -- copy rows [first, first+count) to host: ids int32[count*k],
  * keys uint32[count*k] (either may be NULL).  Errors: INVALID_ARG, CUDA. */

@@ -401,7 +401,8 @@ static int stage_search(knng_graph *g, const knng_points *pts, const knng_params
 }
 
 static int stage_update(knng_graph *g, const knng_params *p, int world, const int32_t *ci_all, const uint32_t *ck_all,
-                        int64_t q_lo, int64_t q_hi, int2 *props, int32_t *prop_cnt, int *nl, bool timed) {
+                        int64_t q_lo, int64_t q_hi, int2 *props, int32_t *prop_cnt, int32_t *new_ids,
+                        uint32_t *new_keys, int *nl, bool timed) {
   const int64_t B = g->pend_B, n_t = g->n;
   const int k = g->k;
   if (B == 0) return 0;
@@ -419,8 +420,12 @@ static int stage_update(knng_graph *g, const knng_params *p, int world, const in
     ++*nl;
   }
   if (timed) CK(cudaEventRecord(g->ev[1], g->stream));
-  // A5: intra-batch all-pairs -> new rows n_t .. n_t+B-1
-  CK(launch_allpairs(g->geom, sv, g->ids, g->keys, k, n_t, B, Ci, Ck, g->stream));
+  // A5: intra-batch all-pairs -> new rows of queries [q_lo, q_hi) (into the graph, or into new_ids/new_keys
+  // for the all-gather of a multi-GPU job)
+  int32_t *oi = new_ids ? new_ids : g->ids + (size_t)(n_t + q_lo) * k;
+  uint32_t *ok = new_keys ? new_keys : g->keys + (size_t)(n_t + q_lo) * k;
+  CK(launch_allpairs(g->geom, sv, n_t, B, q_lo, q_hi - q_lo, k, Ci + (size_t)q_lo * k, Ck + (size_t)q_lo * k, oi, ok,
+                     g->stream));
   ++*nl;
   if (timed) CK(cudaEventRecord(g->ev[2], g->stream));
   // A6: update balls of queries [q_lo, q_hi) over the snapshot -> proposals
@@ -456,9 +461,16 @@ static int stage_update(knng_graph *g, const knng_params *p, int world, const in
 }
 
 static int stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, const int2 *props_all,
-                        const int32_t *prop_cnt_all, int *nl) {
+                        const int32_t *prop_cnt_all, const int32_t *new_ids_all, const uint32_t *new_keys_all,
+                        int *nl) {
   const int64_t B = g->pend_B, n_t = g->n;
   if (B == 0) return 0;
+  if (new_ids_all) {   // the all-gathered new rows (slot b = query b)
+    CK(cudaMemcpyAsync(g->ids + (size_t)n_t * g->k, new_ids_all, (size_t)B * g->k * 4, cudaMemcpyDeviceToDevice,
+                       g->stream));
+    CK(cudaMemcpyAsync(g->keys + (size_t)n_t * g->k, new_keys_all, (size_t)B * g->k * 4, cudaMemcpyDeviceToDevice,
+                       g->stream));
+  }
   const int64_t ballmax = ball_bound(n_t, g->k, p->depth);
   CK(g->w_sorted.ensure((size_t)nq_slots * ballmax * 8));
   // A7: row_v = top-k(row_v u proposals), proposal (slot b) carries the new id n_t + b
@@ -512,10 +524,11 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   CK(g->w_props.ensure((size_t)B * ballmax * 8));
   CK(g->w_prop_cnt.ensure((size_t)B * 4));
   if (int r = stage_update(g, p, 1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), 0, B,
-                           g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), &nl, true))
+                           g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), nullptr, nullptr, &nl, true))
     return r;
   CK(cudaEventRecord(g->ev[3], g->stream));
-  if (int r = stage_commit(g, p, B, g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), &nl)) return r;
+  if (int r = stage_commit(g, p, B, g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), nullptr, nullptr, &nl))
+    return r;
   CK(cudaEventRecord(g->ev[4], g->stream));
   return finish_stats(g, st, nl, 5, B);
 }
@@ -547,7 +560,7 @@ int graph_insert_stage_search(knng_graph *g, const knng_points *pts, const knng_
 
 int graph_insert_stage_update(knng_graph *g, const knng_params *p, int32_t world, const int32_t *cand_ids_all,
                               const uint32_t *cand_keys_all, int64_t q_lo, int64_t q_hi, int32_t *props,
-                              int32_t *prop_cnt, knng_stats *st) {
+                              int32_t *prop_cnt, int32_t *new_ids, uint32_t *new_keys, knng_stats *st) {
   knng_err_slot().clear();
   if (!g || !p) return fail(KNNG_ERR_INVALID_ARG, "stage_update: null argument");
   if (world < 1 || q_lo < 0 || q_hi < q_lo || q_hi > g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_update: bad range");
@@ -555,14 +568,16 @@ int graph_insert_stage_update(knng_graph *g, const knng_params *p, int32_t world
   CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
   int nl = 0;
   CK(cudaEventRecord(g->ev[0], g->stream));
-  if (int r = stage_update(g, p, world, cand_ids_all, cand_keys_all, q_lo, q_hi, (int2 *)props, prop_cnt, &nl, false))
+  if (int r = stage_update(g, p, world, cand_ids_all, cand_keys_all, q_lo, q_hi, (int2 *)props, prop_cnt, new_ids,
+                           new_keys, &nl, false))
     return r;
   CK(cudaEventRecord(g->ev[1], g->stream));
   return finish_stats(g, st, nl, 2, 0);
 }
 
 int graph_insert_stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, const int32_t *props_all,
-                              const int32_t *prop_cnt_all, knng_stats *st) {
+                              const int32_t *prop_cnt_all, const int32_t *new_ids_all, const uint32_t *new_keys_all,
+                              knng_stats *st) {
   knng_err_slot().clear();
   if (!g || !p) return fail(KNNG_ERR_INVALID_ARG, "stage_commit: null argument");
   if (nq_slots < g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_commit: fewer query slots than the batch");
@@ -570,7 +585,8 @@ int graph_insert_stage_commit(knng_graph *g, const knng_params *p, int64_t nq_sl
   CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
   int nl = 0;
   CK(cudaEventRecord(g->ev[0], g->stream));
-  if (int r = stage_commit(g, p, nq_slots, (const int2 *)props_all, prop_cnt_all, &nl)) return r;
+  if (int r = stage_commit(g, p, nq_slots, (const int2 *)props_all, prop_cnt_all, new_ids_all, new_keys_all, &nl))
+    return r;
   CK(cudaEventRecord(g->ev[1], g->stream));
   return finish_stats(g, st, nl, 2, 0);
 }

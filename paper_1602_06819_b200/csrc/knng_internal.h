@@ -78,9 +78,8 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
 // gathered candidates: rank-major [world][nq][P/world][kr]
 cudaError_t launch_merge_parts(int metric, const int32_t *cand_ids, const uint32_t *cand_keys, int64_t nq,
                                int P, int world, int kr, int32_t *out_ids, uint32_t *out_keys, cudaStream_t s);
-cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int32_t *ids, uint32_t *keys, int k,
-                            int64_t n_t, int64_t B, const int32_t *C_ids, const uint32_t *C_keys,
-                            cudaStream_t s);
+cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int64_t q_lo, int64_t nq,
+                            int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi, uint32_t *ok, cudaStream_t s);
 cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cudaStream_t s);
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,

@@ -12,16 +12,18 @@ namespace knng {
 // K3: warp per new point i; lanes take peers j = lane + 32t (thread-level canonical distance).
 // ---------------------------------------------------------------------------
 template <int M>
-__global__ void __launch_bounds__(128) k_allpairs(StoreView st, int32_t *ids, uint32_t *keys, int k, int64_t n_t,
-                                                  int64_t B, const int32_t *Ci, const uint32_t *Ck) {
+__global__ void __launch_bounds__(128) k_allpairs(StoreView st, int64_t n_t, int64_t B, int64_t q_lo, int64_t nq,
+                                                  int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi,
+                                                  uint32_t *ok) {
   const int lane = threadIdx.x & 31;
-  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= B) return;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= nq) return;
+  const int64_t i = q_lo + r;
   WarpTopK<M> top;
   top.init(k);
   {
-    const int32_t cid = lane < k ? Ci[i * k + lane] : -1;
-    const uint32_t ck = lane < k ? Ck[i * k + lane] : 0u;
+    const int32_t cid = lane < k ? Ci[r * k + lane] : -1;
+    const uint32_t ck = lane < k ? Ck[r * k + lane] : 0u;
     top.insert(cid >= 0, ck, cid);
   }
   for (int64_t j0 = 0; j0 < B; j0 += 32) {
@@ -32,18 +34,23 @@ __global__ void __launch_bounds__(128) k_allpairs(StoreView st, int32_t *ids, ui
     top.insert(valid, key, (int32_t)(n_t + j));
   }
   if (lane < k) {
-    ids[(size_t)(n_t + i) * k + lane] = lane < top.cnt ? top.id : -1;
-    keys[(size_t)(n_t + i) * k + lane] = lane < top.cnt ? top.key : 0u;
+    oi[(size_t)r * k + lane] = lane < top.cnt ? top.id : -1;
+    ok[(size_t)r * k + lane] = lane < top.cnt ? top.key : 0u;
   }
 }
 
-cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int32_t *ids, uint32_t *keys, int k, int64_t n_t,
-                            int64_t B, const int32_t *Ci, const uint32_t *Ck, cudaStream_t s) {
-  if (B == 0) return cudaSuccess;
-  const unsigned blocks = (unsigned)((B + 3) / 4);
-  if (g.metric == M_U8) k_allpairs<M_U8><<<blocks, 128, 0, s>>>(st, ids, keys, k, n_t, B, Ci, Ck);
-  else if (g.metric == M_F32) k_allpairs<M_F32><<<blocks, 128, 0, s>>>(st, ids, keys, k, n_t, B, Ci, Ck);
-  else k_allpairs<M_JAC><<<blocks, 128, 0, s>>>(st, ids, keys, k, n_t, B, Ci, Ck);
+cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
+                             int64_t ncols, int k, const int32_t *seed_ids, const uint32_t *seed_keys, int32_t *out_ids,
+                             uint32_t *out_keys, cudaStream_t s);
+
+// A5: new rows of batch queries [q_lo, q_lo+nq): top-k(C_i u {(D(x_i, x_j), n_t+j) : j != i}).
+// Ci/Ck and the outputs are indexed by the local row (query - q_lo).
+cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int64_t q_lo, int64_t nq,
+                            int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi, uint32_t *ok, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  if (g.metric != M_JAC)   // vectors: the smem-tiled kernel of the exact build, seeded with C_i
+    return launch_tile_topk(g, st.vec, n_t + q_lo, nq, n_t, B, k, Ci, Ck, oi, ok, s);
+  k_allpairs<M_JAC><<<(unsigned)((nq + 3) / 4), 128, 0, s>>>(st, n_t, B, q_lo, nq, k, Ci, Ck, oi, ok);
   return cudaGetLastError();
 }
 

@@ -7,9 +7,9 @@ two all-gathers in between (torch.distributed, NCCL over NVLink on a GPU box):
 
   1. graph_insert_stage_search  -- this rank's partitions [r P/G, (r+1) P/G)      -> cand [B][P/G][k]
   2. all-gather cand                                                          -> [G][B][P/G][k]
-  3. graph_insert_stage_update  -- merge (identical everywhere), new rows, balls of the query shard
-  4. all-gather proposals (S = ceil(B/G) slots per rank)                      -> [G*S][ballmax]
-  5. graph_insert_stage_commit  -- apply all proposals, place the points (identical everywhere)
+  3. graph_insert_stage_update  -- merge (identical everywhere), new rows + balls of the query shard
+  4. all-gather new rows and proposals (S = ceil(B/G) slots per rank)    -> [G*S][k], [G*S][ballmax]
+  5. graph_insert_stage_commit  -- write the new rows, apply all proposals, place the points
 
 The exchange carries B*P*k*8 + G*S*ballmax*8 bytes per batch (C3: 5.2 MB + 7.2 MB), the only
 data-path collectives of the path.  Results are identical for every G (tested by emulating G ranks
@@ -126,17 +126,22 @@ def insert_batch_staged(graphs, ranks, world, points, speedup, e_num, e_den, dep
     ci_all, ck_all = gather(cis), gather(cks)      # P > 0: [G][B][P/G][k]; else [G*S][1][k] (row b = query b)
     # 3-4: merge + new rows + balls of the query shard, all-gather of the proposals
     bufs = [(torch.zeros((S, ballmax, 2), dtype=torch.int32, device=dev),
-             torch.zeros((S,), dtype=torch.int32, device=dev)) for _ in graphs]
+             torch.zeros((S,), dtype=torch.int32, device=dev),
+             torch.full((S, k), -1, dtype=torch.int32, device=dev),
+             torch.zeros((S, k), dtype=torch.int32, device=dev)) for _ in graphs]
     _sync()
     for i, (g, r) in enumerate(zip(graphs, ranks)):
         qlo, qhi, _ = query_shard(B, world, r)
-        props, cnt = bufs[i]
+        props, cnt, nid, nkey = bufs[i]
         stats[i]["update"] = g.stage_update(speedup, e_num, e_den, depth, seed, world if P > 0 else 1, ci_all, ck_all,
-                                            qlo, qhi, props, cnt)
+                                            qlo, qhi, props, cnt, nid, nkey)
     props_all = gather([b[0] for b in bufs])
     cnt_all = gather([b[1] for b in bufs])
+    nid_all = gather([b[2] for b in bufs])
+    nkey_all = gather([b[3] for b in bufs])
     _sync()
     # 5: commit everywhere
     for i, g in enumerate(graphs):
-        stats[i]["commit"] = g.stage_commit(speedup, e_num, e_den, depth, seed, props_all.shape[0], props_all, cnt_all)
+        stats[i]["commit"] = g.stage_commit(speedup, e_num, e_den, depth, seed, props_all.shape[0], props_all, cnt_all,
+                                            nid_all, nkey_all)
     return stats

@@ -90,8 +90,8 @@ def load_library(path=LIB_PATH):
     L.graph_insert_stage_search.argtypes = [P, C.POINTER(knng_points), C.POINTER(knng_params), C.c_int32,
                                             C.c_int32, C.c_int64, C.c_int64, P, P, C.POINTER(knng_stats)]
     L.graph_insert_stage_update.argtypes = [P, C.POINTER(knng_params), C.c_int32, P, P, C.c_int64, C.c_int64, P, P,
-                                            C.POINTER(knng_stats)]
-    L.graph_insert_stage_commit.argtypes = [P, C.POINTER(knng_params), C.c_int64, P, P, C.POINTER(knng_stats)]
+                                            P, P, C.POINTER(knng_stats)]
+    L.graph_insert_stage_commit.argtypes = [P, C.POINTER(knng_params), C.c_int64, P, P, P, P, C.POINTER(knng_stats)]
     for f in ("graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit"):
         getattr(L, f).restype = C.c_int
     for f in ("graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
@@ -246,22 +246,23 @@ class KnngGraph:
         return st.as_dict()
 
     def stage_update(self, speedup, e_num, e_den, depth, seed, world, cand_ids_all, cand_keys_all, q_lo, q_hi, props,
-                     prop_cnt):
+                     prop_cnt, new_ids=None, new_keys=None):
         prm, _ = make_params(speedup, e_num, e_den, depth, seed)
         st = knng_stats()
-        _check(load_library().graph_insert_stage_update(self._h, C.byref(prm), int(world),
-                                                        C.c_void_p(cand_ids_all.data_ptr()),
-                                                        C.c_void_p(cand_keys_all.data_ptr()), int(q_lo), int(q_hi),
-                                                        C.c_void_p(props.data_ptr()), C.c_void_p(prop_cnt.data_ptr()),
-                                                        C.byref(st)))
+        ptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())
+        _check(load_library().graph_insert_stage_update(self._h, C.byref(prm), int(world), ptr(cand_ids_all),
+                                                        ptr(cand_keys_all), int(q_lo), int(q_hi), ptr(props),
+                                                        ptr(prop_cnt), ptr(new_ids), ptr(new_keys), C.byref(st)))
         return st.as_dict()
 
-    def stage_commit(self, speedup, e_num, e_den, depth, seed, nq_slots, props_all, prop_cnt_all):
+    def stage_commit(self, speedup, e_num, e_den, depth, seed, nq_slots, props_all, prop_cnt_all, new_ids_all=None,
+                     new_keys_all=None):
         prm, _ = make_params(speedup, e_num, e_den, depth, seed)
         st = knng_stats()
-        _check(load_library().graph_insert_stage_commit(self._h, C.byref(prm), int(nq_slots),
-                                                        C.c_void_p(props_all.data_ptr()),
-                                                        C.c_void_p(prop_cnt_all.data_ptr()), C.byref(st)))
+        ptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())
+        _check(load_library().graph_insert_stage_commit(self._h, C.byref(prm), int(nq_slots), ptr(props_all),
+                                                        ptr(prop_cnt_all), ptr(new_ids_all), ptr(new_keys_all),
+                                                        C.byref(st)))
         return st.as_dict()
 
     def partition_kmedoids(self, P, imbalance, max_iter, seed, init_medoids=None):
