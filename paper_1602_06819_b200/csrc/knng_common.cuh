@@ -321,6 +321,44 @@ struct VecQuery {
     }
     return out;
   }
+
+  // Two full sets of 32 candidates with both sets' loads in flight together (producer warps).
+  __device__ __forceinline__ void eval2(const StoreView &s, int32_t ca, int32_t cb, uint32_t &oa, uint32_t &ob) const {
+    const uint8_t *__restrict__ base = s.vec;
+    const size_t stride = s.stride;
+    const int nchunks = s.nchunks;
+    const int lane = threadIdx.x & 31, sub = lane / L, sl = lane % L;
+    constexpr int NP = 32 / VPP;     // passes per 32 candidates
+    oa = 0;
+    ob = 0;
+    for (int p0 = 0; p0 < NP; p0 += GRP) {
+      uint4 ba[GRP][CPL], bb[GRP][CPL];
+#pragma unroll
+      for (int g = 0; g < GRP; ++g) {
+        const int v = (p0 + g) * VPP + sub;
+        const int32_t ida = __shfl_sync(FULL, ca, v & 31);
+        const int32_t idb = __shfl_sync(FULL, cb, v & 31);
+        const bool ok = p0 + g < NP;
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) {
+          const int c = sl + L * t;
+          const bool okc = ok && c < nchunks;
+          ba[g][t] = (okc && ida >= 0) ? ldg16(base + (size_t)ida * stride + (size_t)c * 16) : make_uint4(0, 0, 0, 0);
+          bb[g][t] = (okc && idb >= 0) ? ldg16(base + (size_t)idb * stride + (size_t)c * 16) : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < GRP; ++g) {
+        if (p0 + g < NP) {
+          const uint32_t ka = reduce(ba[g]);
+          const uint32_t kb = reduce(bb[g]);
+          const uint32_t xa = __shfl_sync(FULL, ka, (lane % VPP) * L);
+          const uint32_t xb = __shfl_sync(FULL, kb, (lane % VPP) * L);
+          if (lane / VPP == p0 + g) { oa = xa; ob = xb; }
+        }
+      }
+    }
+  }
 };
 
 // Jaccard sets: the query's sorted tokens in per-warp shared scratch (global when longer than
@@ -376,6 +414,11 @@ struct SetQuery {
       if (lane / VPP == p) out = kk;
     }
     return out;
+  }
+
+  __device__ __forceinline__ void eval2(const StoreView &s, int32_t ca, int32_t cb, uint32_t &oa, uint32_t &ob) const {
+    oa = eval(s, ca, 32);
+    ob = eval(s, cb, 32);
   }
 };
 
