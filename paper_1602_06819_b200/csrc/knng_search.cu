@@ -12,12 +12,16 @@
 //     so a run of skipped starts costs one round trip per G starts.
 // Visited / expanded sets are bitmaps over the pool-local index, in shared memory when the pool
 // is small enough, else in a per-warp-slot global workspace.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "knng_common.cuh"
 #include "knng_internal.h"
 
 namespace knng {
 
 constexpr int RING_CHUNKS = 8;    // smem ring of 8 x 32 precomputed draws per CTA
+constexpr int FASTC = 4;          // chunks the consumer's skip-only fast path commits at once
 
 struct RingHdr {
   int seq[RING_CHUNKS];   // seq[s] = c + 1 once chunk c is in slot s
@@ -35,23 +39,41 @@ __device__ __forceinline__ void produce(const SearchArgs &a, const QT &Q, volati
                                         const int32_t *pool) {
   const int lane = threadIdx.x & 31;
   long long p_wait = 0, p_work = 0;
-  for (int64_t c = pw; c < nch; c += nprod) {
+  // chunks c and c + nprod are produced together (both sets of loads in flight)
+  for (int64_t c = pw; c < nch; c += 2 * nprod) {
+    const int64_t c2 = c + nprod;
+    const bool two = c2 < nch;
+    const int64_t clast = two ? c2 : c;
     const long long t0 = a.prof ? clock64() : 0;
-    while (c - hdr->consumed >= RING_CHUNKS && !hdr->done) __nanosleep(64);
+    while (clast - hdr->consumed >= RING_CHUNKS && !hdr->done) __nanosleep(32);
     const long long t1 = a.prof ? clock64() : 0;
     p_wait += t1 - t0;
     if (hdr->done) break;
-    const uint64_t idx = rng_index(h3, (uint64_t)(c * 32 + lane), (uint64_t)m);
-    const int32_t node = pool ? pool[idx] : (int32_t)idx;
-    const uint32_t key = Q.eval(a.st, node, 32);
-    // a repeat of an earlier draw of the same chunk can never be fresh (Q4): flag it (bit 31)
-    const bool dup = (__ffs(__match_any_sync(FULL, node)) - 1) != lane;
-    volatile int *rs = (volatile int *)(ring + (c % RING_CHUNKS) * 32 + lane);
-    rs[0] = dup ? (int)(0x80000000u | (uint32_t)node) : node;
-    rs[1] = (int)key;
+    const uint64_t ia = rng_index(h3, (uint64_t)(c * 32 + lane), (uint64_t)m);
+    const int32_t na = pool ? pool[ia] : (int32_t)ia;
+    int32_t nb = -1;
+    if (two) {
+      const uint64_t ib = rng_index(h3, (uint64_t)(c2 * 32 + lane), (uint64_t)m);
+      nb = pool ? pool[ib] : (int32_t)ib;
+    }
+    uint32_t ka, kb;
+    Q.eval2(a.st, na, nb, ka, kb);
+    // repeats of a node inside a window are resolved by the consumer (the atomicOr that flips the
+    // node's visited bit decides which draw evaluates it)
+    volatile int *ra = (volatile int *)(ring + (c % RING_CHUNKS) * 32 + lane);
+    ra[0] = na;
+    ra[1] = (int)ka;
+    if (two) {
+      volatile int *rb = (volatile int *)(ring + (c2 % RING_CHUNKS) * 32 + lane);
+      rb[0] = nb;
+      rb[1] = (int)kb;
+    }
     __threadfence_block();
     __syncwarp();
-    if (lane == 0) hdr->seq[c % RING_CHUNKS] = (int)(c + 1);
+    if (lane == 0) {
+      hdr->seq[c % RING_CHUNKS] = (int)(c + 1);
+      if (two) hdr->seq[c2 % RING_CHUNKS] = (int)(c2 + 1);
+    }
     if (a.prof) p_work += clock64() - t1;
   }
   if (a.prof && lane == 0) {
@@ -107,7 +129,17 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
     Q.load(a.qs, a.qrow0 + b, M == M_JAC ? qscr + (warp < 2 ? warp : 1) * QMAX : nullptr);
     const uint64_t h3 = rng_prefix(a.seed, (uint64_t)(a.pid_base + b), (uint64_t)p);
     if (warp > 0) {
-      if (budget > 0) produce(a, Q, hdr, ring, warp - 1, nprod, nch, h3, m, pool);
+      if (budget > 0) {
+        if (M == M_U8 && a.st.nchunks <= 8 && a.qs.nchunks <= 8) {
+          // u8 rows of <= 128 B: 4 lanes x 2 chunks per candidate (2 shuffle levels), measured the
+          // fastest layout for 32-draw chunks (scripts/micro/eval_micro.cu)
+          VecQuery<M_U8, 4, 2> PQ;
+          PQ.load(a.qs, a.qrow0 + b, nullptr);
+          produce(a, PQ, hdr, ring, warp - 1, nprod, nch, h3, m, pool);
+        } else {
+          produce(a, Q, hdr, ring, warp - 1, nprod, nch, h3, m, pool);
+        }
+      }
       continue;
     }
 
@@ -117,7 +149,7 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
     int64_t c = 0, jbase = 0;
     int32_t wnode = -1;
     uint32_t wkey = 0, wl = 0;
-    bool whave = false, wpf = false, wdup = false;
+    bool whave = false, wpf = false;
     SkipThr<M> thr;              // skip rule prepared against the current best key
     uint32_t thr_key = 0;
     bool thr_ok = false;
@@ -128,6 +160,59 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
     while (c < budget) {
       // ------------------------------ restart ------------------------------
       if (wpos >= 32) {
+        // ---- fast path: FASTC whole produced chunks in which no draw can be accepted.  Against the
+        // current s_max every draw is skipped (so none is a new best and the threshold cannot move);
+        // each unevaluated node among them is evaluated once (the atomicOr that flips its bit) and
+        // skipped, exactly as the sequential loop would do draw by draw; the budget is not reached.
+        const int64_t ch0 = jbase / 32;
+        if (top.cnt > 0 && nprod > 0 && ch0 + FASTC <= nch && c + 32 * FASTC <= budget) {
+          const long long tw = a.prof ? clock64() : 0;
+          for (int t = 0; t < FASTC; ++t) {
+            const int slot = (int)((ch0 + t) % RING_CHUNKS);
+            while (hdr->seq[slot] != (int)(ch0 + t + 1)) __nanosleep(20);
+          }
+          if (a.prof) p_wait += clock64() - tw;
+          __threadfence_block();
+          if (!thr_ok || thr_key != top.key_at0) {
+            thr.set(top.key_at0, a.e_num, a.e_den);
+            thr_key = top.key_at0;
+            thr_ok = true;
+          }
+          int32_t fnode[FASTC];
+          uint32_t fkey[FASTC];
+          bool pass = false;
+#pragma unroll
+          for (int t = 0; t < FASTC; ++t) {
+            const volatile int *rs = (const volatile int *)(ring + ((ch0 + t) % RING_CHUNKS) * 32 + lane);
+            fnode[t] = rs[0];
+            fkey[t] = (uint32_t)rs[1];
+            pass |= !thr.skip(fkey[t]);
+          }
+          if (!__any_sync(FULL, pass)) {
+            bool fr[FASTC];
+#pragma unroll
+            for (int t = 0; t < FASTC; ++t) {
+              const uint32_t li = a.P > 0 ? (uint32_t)a.local_idx[fnode[t]] : (uint32_t)fnode[t];
+              const uint32_t bit = 1u << (li & 31);
+              fr[t] = !(atomicOr(ev + (li >> 5), bit) & bit);
+            }
+            __syncwarp();
+            int nf = 0;
+#pragma unroll
+            for (int t = 0; t < FASTC; ++t) {
+              top.insert(fr[t], fkey[t], fnode[t]);     // Q5: skipped starts enter the top-k
+              nf += __popc(__ballot_sync(FULL, fr[t]));
+            }
+            c += nf;
+            s_starts += nf;
+            s_skip += nf;
+            p_win += FASTC;
+            __syncwarp();
+            if (lane == 0) hdr->consumed = (int)(ch0 + FASTC);
+            jbase += 32 * FASTC;
+            continue;
+          }
+        }
         const int64_t j = jbase + lane;
         const int64_t ch = jbase / 32;
         if (ch < nch && nprod > 0) {                 // produced ahead into the ring
@@ -138,9 +223,7 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
           ++p_win;
           __threadfence_block();
           const volatile int *rs = (const volatile int *)(ring + slot * 32 + lane);
-          const int w0 = rs[0];
-          wnode = w0 & 0x7FFFFFFF;
-          wdup = w0 < 0;
+          wnode = rs[0];
           wkey = (uint32_t)rs[1];
           whave = true;
           __syncwarp();
@@ -153,7 +236,6 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
             wnode = pool ? pool[idx] : (int32_t)idx;
           }
           whave = false;
-          wdup = false;
         }
         wl = wnode >= 0 ? (a.P > 0 ? (uint32_t)a.local_idx[wnode] : (uint32_t)wnode) : 0u;
         jbase += 32;
@@ -179,13 +261,10 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
       const unsigned invm = __ballot_sync(FULL, wnode < 0) & active;
       const unsigned lim = invm ? ((1u << (__ffs(invm) - 1)) - 1u) : FULL;
       const bool evb = wnode >= 0 ? bit_get(ev, wl) : true;
-      bool fresh;
-      if (__all_sync(FULL, whave)) {     // produced window: repeats are flagged by the producer
-        fresh = lane >= wpos && !evb && !wdup;
-      } else {
-        const unsigned same = __match_any_sync(FULL, wnode) & active;
-        fresh = lane >= wpos && !evb && (__ffs(same) - 1) == lane;   // redraws are free (Q4)
-      }
+      // Redraws of evaluated nodes are free (Q4).  A node drawn twice inside the window looks fresh
+      // in both lanes: the later lane can never be accepted when the earlier one is skipped (same key,
+      // tighter s_max), and the commit's atomicOr lets only the first evaluation count.
+      const bool fresh = lane >= wpos && !evb;
       const unsigned fm = __ballot_sync(FULL, fresh) & active & lim;
       if (fm == 0) {
         if (invm) break;          // injected start sequence exhausted
@@ -208,7 +287,8 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
       }
       // committable: fresh draws in order up to the first one without a key
       const unsigned miss = fm & ~hm;
-      unsigned cm = miss ? (fm & ((1u << (__ffs(miss) - 1)) - 1u)) : fm;
+      const unsigned cmfull = miss ? (fm & ((1u << (__ffs(miss) - 1)) - 1u)) : fm;
+      unsigned cm = cmfull;
       if ((int64_t)__popc(cm) > budget - c) cm = first_bits(cm, (int)(budget - c));
       const bool inc = (cm >> lane) & 1u;
       unsigned am;
@@ -246,9 +326,13 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
       const int al = am ? __ffs(am) - 1 : -1;
       const unsigned commit = am ? (cm & (al == 31 ? FULL : ((2u << al) - 1u))) : cm;
       const bool cmt = (commit >> lane) & 1u;
-      if (cmt) bit_set(ev, wl);
-      top.insert(cmt, wkey, wnode);          // Q5: skipped starts enter the top-k too
-      const int ncm = __popc(commit);
+      bool newly = false;
+      if (cmt) {
+        const uint32_t bit = 1u << (wl & 31);
+        newly = !(atomicOr(ev + (wl >> 5), bit) & bit);
+      }
+      top.insert(newly, wkey, wnode);        // Q5: skipped starts enter the top-k too
+      const int ncm = __popc(__ballot_sync(FULL, newly));
       c += ncm;
       s_starts += ncm;
       s_skip += ncm - (am ? 1 : 0);
@@ -257,7 +341,8 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
       // algorithm, its walk begins and ends at the first fresh evaluation it needs
       if (c >= budget && !am) break;
       if (!am) {
-        wpos = miss ? (__ffs(miss) - 1) : 32;
+        const unsigned rest = cmfull & ~commit;   // truncated by the budget (repeats inside): resume there
+        wpos = rest ? (__ffs(rest) - 1) : (miss ? (__ffs(miss) - 1) : 32);
         continue;
       }
       wpos = al + 1;
@@ -380,6 +465,12 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   }
   int64_t blocks = T;
   if (!a.smem_bits && blocks > a.gslots) blocks = a.gslots;
+  if (getenv("KNNG_PROFILE")) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL>, warps * 32, smem);
+    fprintf(stderr, "KNNG_PROFILE k_search: %lld CTAs, %d per SM resident (%zu B smem each)\n", (long long)blocks,
+            per_sm, smem);
+  }
   k_search<M, L, CPL><<<(unsigned)blocks, warps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
