@@ -141,7 +141,7 @@ def run_reference(args, cfg):
     val = args.steps * cfg.batch / t
     line = {"impl": "reference", "metric": baseline_metric(), "value": val, "unit": "inserts/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_name(cfg), "data": "synthetic",
             "config": {"workload": cfg_desc(cfg), "global_batch": cfg.batch},
             "cpu_baseline": {"value": val, "unit": "inserts/s", "cores": nthreads, "kind": "oracle",
                              "sample": "%d timed batches of %d inserts (oracle exact init %.0f s untimed)" % (
@@ -152,9 +152,25 @@ def run_reference(args, cfg):
 
 
 def cfg_desc(cfg):
-    return ("%s: n0=%d uint8 d=%d (%d-cluster mixture), squared-L2 int32, k=%d, batches of %d, speedup=%g, "
-            "expansion %d/%d, depth %d" % (cfg.name, cfg.n0, cfg.dim, cfg.clusters, cfg.k, cfg.batch, cfg.speedup,
-                                           cfg.e_num, cfg.e_den, cfg.depth))
+    pts = {D.U8: "uint8 d=%d (%d-cluster mixture), squared-L2 int32" % (cfg.dim, cfg.clusters),
+           D.F32: "fp32 d=%d (%d-cluster mixture), squared-L2 fp32" % (cfg.dim, cfg.clusters),
+           D.JAC: "Zipf(1.1) token sets, Jaccard (exact cross-multiplied)"}[cfg.metric]
+    part = ", P=%d partitions (imbalance %g)" % (cfg.P, cfg.imbalance) if cfg.P else ""
+    return ("%s: n0=%d %s, k=%d, batches of %d, speedup=%g, expansion %d/%d, depth %d%s" % (
+        cfg.name, cfg.n0, pts, cfg.k, cfg.batch, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, part))
+
+
+def point_bytes(cfg, S=None):
+    """V of SURVEY 8(d): bytes of one point (sets: 4 per token of the mean set + 8 for its offsets)."""
+    if cfg.metric == D.U8:
+        return cfg.dim
+    if cfg.metric == D.F32:
+        return 4 * cfg.dim
+    return int(round(4 * float(np.mean([len(x) for x in S[:4096]])) + 8)) if S is not None else 118
+
+
+def dtype_name(cfg):
+    return {D.U8: "u8", D.F32: "f32", D.JAC: "u32 sets"}[cfg.metric]
 
 
 def run_ours(args, cfg):
@@ -176,7 +192,7 @@ def run_ours(args, cfg):
     nsteps = args.warmup + args.steps
     X = D.initial_points(cfg)
     S = D.stream_points(cfg, 0, max(cfg.n_insert, nsteps * GB))
-    V = cfg.dim if cfg.metric == D.U8 else 4 * cfg.dim
+    V = point_bytes(cfg, S)
     stream = torch.cuda.Stream()
     cap = cfg.n0 + nsteps * GB + 8
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
@@ -208,9 +224,20 @@ def run_ours(args, cfg):
         return out
 
     # ---------------- device-resident inputs (value) ----------------
-    g = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
-    rows0 = g.rows() if (rank == 0 and ws == 1 and not args.no_cpu_baseline) else None
-    S_dev = torch.from_numpy(S[:nsteps * GB]).to("cuda")
+    def new_graph():
+        gg = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
+        if cfg.P:     # Alg. 4 partitioning (setup, untimed)
+            gg.partition_kmedoids(cfg.P, cfg.imbalance, args.kmedoids_iters, cfg.part_seed)
+        return gg
+
+    t_setup = time.perf_counter()
+    g = new_graph()
+    t_setup = time.perf_counter() - t_setup
+    rows0 = g.rows() if (rank == 0 and ws == 1 and not args.no_cpu_baseline and not cfg.P) else None
+    if cfg.metric == D.JAC:     # sets stay in host CSR: the library copies each batch in (H2D inside the step)
+        S_dev = S[:nsteps * GB]
+    else:
+        S_dev = torch.from_numpy(S[:nsteps * GB]).to("cuda")
     pos = 0
     for _ in range(args.warmup):
         step(g, S_dev[pos:pos + GB])
@@ -245,25 +272,34 @@ def run_ours(args, cfg):
     launches = sum(s["kernel_launches"] for s in stats)
     traffic = None       # DRAM bytes per launch of k_search from the committed ncu --set full capture
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "k_search_ncu.json")))["dram_bytes_per_launch"]
+        prof = json.load(open(os.path.join(ROOT, "profiles", "k_search_ncu.json")))
+        if prof.get("config", "C1") == cfg.name and not args.n0:
+            traffic = prof["dram_bytes_per_launch"]
     except Exception:
         pass
 
     # recall@k of the inserted points' rows vs the exact k-nn over the final point set (sampled, torch)
-    ids, keys = g.rows(cfg.n0, pos)
-    allp = torch.from_numpy(np.concatenate([X, S[:pos]])).to("cuda").float()
-    samp = np.arange(0, pos, max(1, pos // 256))
-    q = allp[cfg.n0 + samp]
-    d2 = torch.cdist(q, allp).pow(2)
-    d2[torch.arange(len(samp)), torch.from_numpy(cfg.n0 + samp).cuda()] = float("inf")
-    exact = torch.topk(d2, cfg.k, largest=False).indices.cpu().numpy()
-    rec = float(np.mean([len(set(ids[s].tolist()) & set(exact[i].tolist())) / cfg.k for i, s in enumerate(samp)]))
+    rec = None
+    if cfg.metric != D.JAC:
+        ids, keys = g.rows(cfg.n0, pos)
+        samp = np.arange(0, pos, max(1, pos // 256))
+        allp = torch.from_numpy(np.concatenate([X, S[:pos]])).to("cuda").float()
+        q = allp[cfg.n0 + samp]
+        d2 = torch.cat([torch.cdist(q, allp[i:i + (1 << 20)]).pow(2) for i in range(0, len(allp), 1 << 20)], 1)
+        d2[torch.arange(len(samp)), torch.from_numpy(cfg.n0 + samp).cuda()] = float("inf")
+        exact = torch.topk(d2, cfg.k, largest=False).indices.cpu().numpy()
+        rec = float(np.mean([len(set(ids[s].tolist()) & set(exact[i].tolist())) / cfg.k
+                             for i, s in enumerate(samp)]))
+        del allp, d2
     g.close()
 
     # ---------------- end to end through the C ABI with host buffers (e2e) ----------------
-    g2 = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
-    S_pin_t = torch.from_numpy(S[:nsteps * GB]).pin_memory()
-    S_pin = S_pin_t.numpy()
+    g2 = new_graph()
+    if cfg.metric == D.JAC:
+        S_pin = S[:nsteps * GB]
+    else:
+        S_pin_t = torch.from_numpy(S[:nsteps * GB]).pin_memory()
+        S_pin = S_pin_t.numpy()
     pos2 = 0
     for _ in range(args.warmup):
         step(g2, S_pin[pos2:pos2 + GB])
@@ -284,8 +320,8 @@ def run_ours(args, cfg):
     line = {
         "metric": baseline_metric(), "value": value, "unit": "inserts/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": cfg_desc(cfg), "global_batch": GB,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype_name(cfg), "data": "synthetic",
+        "config": {"workload": cfg_desc(cfg), "global_batch": GB, "setup_s": t_setup,
                    "parallelism": "1 GPU" if ws == 1 else
                    "dp%d: replicated graph, the global batch's queries sharded over ranks, NCCL all-gathers of "
                    "candidates and proposals" % ws,
@@ -299,7 +335,8 @@ def run_ours(args, cfg):
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": bytes_search / len(stats),
                      "ms_per_launch": ms_search / len(stats),
-                     "note": "C1 is L2-resident (14 MB store): HBM fraction is not the binding claim"},
+                     "note": ("store + rows fit in L2 (126 MB): the HBM fraction is not the binding claim"
+                              if cap * (V + 8 * cfg.k) < 100e6 else "HBM-resident store")},
         "phase_ms": {p: sum(s[p] for s in stats) / len(stats) for p in ("ms_search", "ms_allpairs",
                                                                        "ms_update", "ms_merge")},
         "e2e": {"value": args.steps * GB / t_e2e, "unit": "inserts/s", "h2d_bytes_per_step": GB * V,
@@ -324,10 +361,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default=CFG_NAME, choices=sorted(D.CONFIGS),
+                    help="BASELINE.json config (default C1 = configs[1], the metric's workload)")
+    ap.add_argument("--n0", type=int, default=0, help="override the initial graph size (reduced runs)")
+    ap.add_argument("--kmedoids-iters", type=int, default=10)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = D.CONFIGS[CFG_NAME]
+    cfg = D.CONFIGS[args.config]
+    if args.n0:
+        cfg = cfg.with_sizes(n0=args.n0)
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

@@ -78,7 +78,8 @@ if os.path.exists(rep):
     dram = val("dram__bytes_read.sum", bscale) + val("dram__bytes_write.sum", bscale)
     tscale = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}
     ms = val("gpu__time_duration.sum", tscale)
-    json.dump({"kernel": "k_search", "dram_bytes_per_launch": dram, "ms": ms, "source": "ncu --set full, " + tag},
+    json.dump({"kernel": "k_search", "config": "C1", "dram_bytes_per_launch": dram, "ms": ms,
+               "source": "ncu --set full, " + tag},
               open(os.path.join(out, "k_search_ncu.json"), "w"), indent=1)
     md += ["", "DRAM traffic per launch: %.1f MB (the store is L2-resident)." % (dram / 1e6)]
     open(os.path.join(out, "%s_k_search_full.md" % tag), "w").write("\n".join(md) + "\n")
