@@ -59,7 +59,12 @@ static int geom_for(int metric, int dim, VecGeom *g) {
   g->metric = metric;
   g->nchunks = C;
   g->stride = (size_t)C * 16;
-  if (C <= 32) {
+  if (metric == KNNG_L2SQ_F32 && C <= 32) {   // <= 4 chunks per lane, in-lane canonical partials
+    int L = 1;
+    while (L * 4 < C) L <<= 1;
+    g->L = L;
+    g->CPL = (C + L - 1) / L;
+  } else if (C <= 32) {
     int L = 1;
     while (L < C) L <<= 1;
     g->L = L;

@@ -255,7 +255,10 @@ __device__ __forceinline__ uint32_t pair_key(const StoreView &s, int64_t i, int6
 template <int M, int L, int CPL>
 struct VecQuery {
   static constexpr int VPP = 32 / L;
-  static constexpr int GRP = (L < (8 / CPL) ? L : ((8 / CPL) > 0 ? (8 / CPL) : 1));
+  // passes whose loads are in flight together: up to 8 x 16 B per lane, 16 for wide vectors (one
+  // vector per pass, L = 32) so that a 32-candidate chunk needs 2 round trips, not 4
+  static constexpr int LIM = ((L == 32 && CPL == 1) || CPL >= 3) ? 16 : 8;
+  static constexpr int GRP = (L < (LIM / CPL) ? L : ((LIM / CPL) > 0 ? (LIM / CPL) : 1));
   uint4 q[CPL];
 
   __device__ __forceinline__ void load(const StoreView &s, int64_t r, uint32_t * /*scratch*/) {
@@ -277,10 +280,29 @@ struct VecQuery {
 #pragma unroll
       for (int o = L / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
       return acc;
-    } else {
+    } else if (L == 32 || CPL == 1) {
+      // chunks sl, sl+32, ... share partial sl: one fmaf chain in increasing chunk order (Q24)
       float acc = 0.0f;
 #pragma unroll
       for (int t = 0; t < CPL; ++t) acc = f4_leaf(acc, q[t], b[t]);
+#pragma unroll
+      for (int o = L / 2; o >= 1; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+      return __float_as_uint(acc);
+    } else {
+      // L*CPL <= 32: chunk sl + L*t is its own partial (index sl + L*t).  The butterfly levels
+      // o >= L pair partials held by the same lane (slots t and t + o/L; slots >= CPL are +0); the
+      // levels o < L cross lanes.  Same tree as the 32-lane canonical order (Q24).
+      float p[CPL];
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) p[t] = f4_leaf(0.0f, q[t], b[t]);
+#pragma unroll
+      for (int o = 16; o >= L; o >>= 1) {
+        const int st = o / L;
+#pragma unroll
+        for (int t = 0; t < CPL; ++t)
+          if (t < st && t + st < CPL) p[t] = __fadd_rn(p[t], p[t + st]);
+      }
+      float acc = p[0];
 #pragma unroll
       for (int o = L / 2; o >= 1; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
       return __float_as_uint(acc);
@@ -329,12 +351,13 @@ struct VecQuery {
     const int nchunks = s.nchunks;
     const int lane = threadIdx.x & 31, sub = lane / L, sl = lane % L;
     constexpr int NP = 32 / VPP;     // passes per 32 candidates
+    constexpr int G2 = (LIM == 16 && GRP > 1) ? GRP / 2 : GRP;   // per set (both sets together stay <= 16 loads)
     oa = 0;
     ob = 0;
-    for (int p0 = 0; p0 < NP; p0 += GRP) {
-      uint4 ba[GRP][CPL], bb[GRP][CPL];
+    for (int p0 = 0; p0 < NP; p0 += G2) {
+      uint4 ba[G2][CPL], bb[G2][CPL];
 #pragma unroll
-      for (int g = 0; g < GRP; ++g) {
+      for (int g = 0; g < G2; ++g) {
         const int v = (p0 + g) * VPP + sub;
         const int32_t ida = __shfl_sync(FULL, ca, v & 31);
         const int32_t idb = __shfl_sync(FULL, cb, v & 31);
@@ -348,7 +371,7 @@ struct VecQuery {
         }
       }
 #pragma unroll
-      for (int g = 0; g < GRP; ++g) {
+      for (int g = 0; g < G2; ++g) {
         if (p0 + g < NP) {
           const uint32_t ka = reduce(ba[g]);
           const uint32_t kb = reduce(bb[g]);

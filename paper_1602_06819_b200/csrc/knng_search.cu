@@ -456,7 +456,8 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   if (T == 0) return cudaSuccess;
-  const int warps = a.starts ? 1 : 2;          // consumer + producers
+  // consumer + producer (a second producer did not pay: measured on C2/C3)
+  const int warps = a.starts ? 1 : 2;
   size_t smem = 128 + RING_CHUNKS * 32 * 8 + (size_t)(a.k * a.k + 32 * a.k) * 4 + (M == M_JAC ? 2 * QMAX * 4 : 0);
   if (a.smem_bits) smem += (size_t)a.bits_words * 4;
   if (smem > 48 * 1024) {
@@ -477,13 +478,17 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
 
 #define KNNG_SHAPES(X, M) \
   X(M, 1, 1) X(M, 2, 1) X(M, 4, 1) X(M, 8, 1) X(M, 16, 1) X(M, 32, 1) X(M, 32, 2) X(M, 32, 4)
+// fp32 rows of <= 32 chunks: 4 chunks per lane at most, partials in-lane (see VecQuery::reduce)
+#define KNNG_SHAPES_F32(X) \
+  X(M_F32, 1, 1) X(M_F32, 1, 2) X(M_F32, 1, 3) X(M_F32, 1, 4) X(M_F32, 2, 3) X(M_F32, 2, 4) X(M_F32, 4, 3) \
+  X(M_F32, 4, 4) X(M_F32, 8, 3) X(M_F32, 8, 4) X(M_F32, 32, 2) X(M_F32, 32, 4)
 
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch) {
   if (n_launch) ++*n_launch;
 #define X(MM, LL, CC) \
   if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC>(a, s);
   KNNG_SHAPES(X, M_U8)
-  KNNG_SHAPES(X, M_F32)
+  KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
 #undef X
   return cudaErrorInvalidValue;

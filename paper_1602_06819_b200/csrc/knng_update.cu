@@ -151,12 +151,16 @@ static cudaError_t run_ball(const BallArgs &a, int64_t nslots, cudaStream_t s) {
 
 #define KNNG_SHAPES(X, M) \
   X(M, 1, 1) X(M, 2, 1) X(M, 4, 1) X(M, 8, 1) X(M, 16, 1) X(M, 32, 1) X(M, 32, 2) X(M, 32, 4)
+// fp32 rows of <= 32 chunks: 4 chunks per lane at most, partials in-lane (see VecQuery::reduce)
+#define KNNG_SHAPES_F32(X) \
+  X(M_F32, 1, 1) X(M_F32, 1, 2) X(M_F32, 1, 3) X(M_F32, 1, 4) X(M_F32, 2, 3) X(M_F32, 2, 4) X(M_F32, 4, 3) \
+  X(M_F32, 4, 4) X(M_F32, 8, 3) X(M_F32, 8, 4) X(M_F32, 32, 2) X(M_F32, 32, 4)
 
 cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cudaStream_t s) {
 #define X(MM, LL, CC) \
   if (g.metric == MM && g.L == LL && g.CPL == CC) return run_ball<MM, LL, CC>(a, nslots, s);
   KNNG_SHAPES(X, M_U8)
-  KNNG_SHAPES(X, M_F32)
+  KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
 #undef X
   return cudaErrorInvalidValue;
