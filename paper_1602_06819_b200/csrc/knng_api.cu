@@ -99,6 +99,14 @@ static int copy_rows(knng_graph *g, uint8_t *dst, const knng_points *p) {
   return 0;
 }
 
+__global__ void k_token_max(const uint32_t *tok, int64_t n, unsigned *out) {
+  unsigned m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, tok[i]);
+  m = __reduce_max_sync(0xFFFFFFFFu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 __global__ void k_rebase_offsets(const uint64_t *in, int64_t n, uint64_t base, uint64_t *out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i <= n) out[i] = base + (in[i] - in[0]);
@@ -107,7 +115,7 @@ __global__ void k_rebase_offsets(const uint64_t *in, int64_t n, uint64_t base, u
 // append n sets (CSR, host or device) to a token/offset store: off[row0 .. row0+n] and
 // tok[tok_n ..]; grows the token buffer geometrically.  Returns the tokens appended.
 static int append_sets(knng_graph *g, const knng_points *p, uint64_t **off_dst_base, uint32_t **tok_buf,
-                       int64_t *tok_cap, int64_t row0, int64_t tok0, int64_t *ntok_out) {
+                       int64_t *tok_cap, int64_t row0, int64_t tok0, int64_t *ntok_out, uint32_t *tok_max = nullptr) {
   uint64_t first = 0, last = 0;
   if (p->data_on_device) {
     CK(cudaMemcpyAsync(&first, p->offsets, 8, cudaMemcpyDeviceToHost, g->stream));
@@ -124,6 +132,8 @@ static int append_sets(knng_graph *g, const knng_points *p, uint64_t **off_dst_b
     const int64_t ncap = std::max<int64_t>(tok0 + nt, *tok_cap + *tok_cap / 2) + 1024;
     uint32_t *nb = nullptr;
     CK(cudaMalloc((void **)&nb, (size_t)ncap * 4));
+    // zeroed slack: the set evaluator reads whole 16-byte chunks around a set's tokens
+    CK(cudaMemsetAsync(nb + tok0, 0, (size_t)(ncap - tok0) * 4, g->stream));
     if (*tok_buf && tok0 > 0) CK(cudaMemcpyAsync(nb, *tok_buf, (size_t)tok0 * 4, cudaMemcpyDeviceToDevice, g->stream));
     CK(cudaStreamSynchronize(g->stream));
     if (*tok_buf) cudaFree(*tok_buf);
@@ -144,6 +154,23 @@ static int append_sets(knng_graph *g, const knng_points *p, uint64_t **off_dst_b
     CK(cudaMemcpyAsync(dst, h.data(), h.size() * 8, cudaMemcpyHostToDevice, g->stream));
     CK(cudaStreamSynchronize(g->stream));   // h is a local buffer
   }
+  if (tok_max && nt > 0) {   // largest token: sizes the search's vocabulary bitmap
+    unsigned m = 0;
+    if (p->data_on_device) {
+      unsigned *dm = nullptr;
+      CK(cudaMalloc((void **)&dm, 4));
+      CK(cudaMemsetAsync(dm, 0, 4, g->stream));
+      k_token_max<<<256, 256, 0, g->stream>>>(*tok_buf + tok0, nt, dm);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(&m, dm, 4, cudaMemcpyDeviceToHost, g->stream));
+      CK(cudaStreamSynchronize(g->stream));
+      cudaFree(dm);
+    } else {
+      const uint32_t *t = (const uint32_t *)p->data + first;
+      for (int64_t i = 0; i < nt; ++i) m = std::max(m, t[i]);
+    }
+    *tok_max = std::max(*tok_max, (uint32_t)m);
+  }
   *ntok_out = nt;
   return 0;
 }
@@ -152,7 +179,7 @@ static int append_sets(knng_graph *g, const knng_points *p, uint64_t **off_dst_b
 static int store_points(knng_graph *g, const knng_points *p, int64_t row0) {
   if (g->metric == KNNG_JACCARD_U32SET) {
     int64_t nt = 0;
-    if (int r = append_sets(g, p, &g->off, &g->tok, &g->tok_cap, row0, g->tok_n, &nt)) return r;
+    if (int r = append_sets(g, p, &g->off, &g->tok, &g->tok_cap, row0, g->tok_n, &nt, &g->tok_max)) return r;
     g->tok_n += nt;
     return 0;
   }
@@ -281,7 +308,9 @@ static SearchPlan plan_search(knng_graph *g, int64_t tasks, int64_t mmax) {
   SearchPlan sp;
   sp.bits_words = 2 * ((mmax + 31) / 32);
   // visited + expanded bitmaps in shared memory when a CTA still fits >= 4 times per SM
-  sp.smem = (size_t)sp.bits_words * 4 <= 40 * 1024 ? 1 : 0;
+  size_t lim = 40 * 1024;
+  if (const char *e = getenv("KNNG_SMEM_BITS_KB")) lim = (size_t)atoi(e) * 1024;
+  sp.smem = (size_t)sp.bits_words * 4 <= lim ? 1 : 0;
   sp.slots = sp.smem ? tasks : std::min<int64_t>(tasks, 148 * 8);
   return sp;
 }
@@ -339,6 +368,16 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.out_keys = out_k;
   a.stats = g->w_stats.as<unsigned long long>();
   a.prof = getenv("KNNG_PROFILE") ? a.stats + 8 : nullptr;   // cycle counters -> stats[8..13]
+  a.task_ctr = a.stats + 14;
+  a.pitch = g->metric == KNNG_JACCARD_U32SET ? 16 * 16 + 16 : (int)g->geom.stride + 16;
+  // producer shape (tuning knobs, overridable for measurement)
+  a.stages = g->metric == KNNG_JACCARD_U32SET ? 4 : 2;
+  a.nprod = 1;
+  a.lane_eval = 1;
+  if (const char *e = getenv("KNNG_STAGES")) a.stages = atoi(e) <= 2 ? 2 : 4;
+  if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
+  if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
+  if (g->metric == KNNG_JACCARD_U32SET) a.stages = 4;
   cudaError_t e = launch_search(g->geom, a, g->stream, nl);
   if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
   return 0;

@@ -106,6 +106,39 @@ __device__ __forceinline__ void cp_async4(void *smem_dst, const void *gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// asynchronous 16-byte global -> shared copy, L2 only (.cg): a staged gather holds no registers
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+// mbarrier (shared, CTA scope): the ring's "chunk published" signal without a memory fence
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_inval(uint64_t *bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -222,8 +255,10 @@ struct StoreView {
   size_t stride;
   int nchunks;
   const uint64_t *off;   // sets: [n+1]
-  const uint32_t *tok;   // sets: sorted, unique tokens
+  const uint32_t *tok;   // sets: sorted, unique tokens (16-byte aligned buffer, zeroed slack)
+  int vwords;            // sets: words of a vocabulary bitmap covering every stored token (0: none)
 };
+constexpr int VOCAB_SMEM_WORDS = 8192;   // vocabulary bitmaps up to 2^18 token ids live in smem
 
 // Single-thread Jaccard key of two sorted token lists: (|A n B| << 16) | |A u B|.
 __device__ __forceinline__ uint32_t set_key(const uint32_t *a, int la, const uint32_t *b, int lb) {
@@ -344,6 +379,36 @@ struct VecQuery {
     return out;
   }
 
+  // Keys of 32 candidates staged in shared memory (candidate j's row at sb + j * pitch, zero
+  // beyond nchunks not required); lane j gets candidate j's key.  Same reduction tree (Q24).
+  __device__ __forceinline__ uint32_t eval_smem(const uint8_t *sb, int pitch, int nchunks) const {
+    const int lane = threadIdx.x & 31, sub = lane / L, sl = lane % L;
+    constexpr int NP = 32 / VPP;
+    constexpr int GW = (8 / CPL) > 0 ? (8 / CPL) : 1;
+    constexpr int GS = NP < GW ? NP : (GW < 4 ? GW : 4);   // passes whose LDS are in flight together
+    uint32_t out = 0;
+#pragma unroll
+    for (int p0 = 0; p0 < NP; p0 += GS) {
+      uint4 buf[GS][CPL];
+#pragma unroll
+      for (int g = 0; g < GS; ++g) {
+        const uint8_t *row = sb + ((p0 + g) * VPP + sub) * pitch;
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) {
+          const int c = sl + L * t;
+          buf[g][t] = c < nchunks ? *(const uint4 *)(row + c * 16) : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < GS; ++g) {
+        const uint32_t key = reduce(buf[g]);
+        const uint32_t kk = __shfl_sync(FULL, key, (lane % VPP) * L);
+        if (lane / VPP == p0 + g) out = kk;
+      }
+    }
+    return out;
+  }
+
   // Two full sets of 32 candidates with both sets' loads in flight together (producer warps).
   __device__ __forceinline__ void eval2(const StoreView &s, int32_t ca, int32_t cb, uint32_t &oa, uint32_t &ob) const {
     const uint8_t *__restrict__ base = s.vec;
@@ -384,20 +449,26 @@ struct VecQuery {
   }
 };
 
-// Jaccard sets: the query's sorted tokens in per-warp shared scratch (global when longer than
-// QMAX); L lanes per candidate each take every L-th candidate token and binary-search it in the
-// query; intersections are summed over the L lanes.
+// Jaccard sets.  The query's sorted tokens sit in shared scratch (global when longer than QMAX);
+// membership of a candidate token is one bit test in a shared vocabulary bitmap when the store's
+// token range fits one (StoreView::vwords > 0, set up by the caller), else a binary search in the
+// sorted query.  One lane per candidate: the candidate's token range is read with aligned 16-byte
+// loads (the token buffer is 16-byte aligned and its slack is zeroed, so the chunks that straddle
+// the range hold valid tokens), and a 4-bit mask per chunk keeps only the candidate's own tokens.
+// Up to SU chunks per lane and set are in flight together.
 constexpr int QMAX = 256;
 template <int L>
 struct SetQuery {
-  static constexpr int VPP = 32 / L;
+  static constexpr int SU = 8;
   const uint32_t *q;
+  const uint32_t *bm;    // vocabulary bitmap of the query (shared) or null
   int qn;
 
   __device__ __forceinline__ void load(const StoreView &s, int64_t r, uint32_t *scratch) {
     const int lane = threadIdx.x & 31;
     const uint64_t b = s.off[r];
     qn = (int)(s.off[r + 1] - b);
+    bm = nullptr;
     if (qn <= QMAX && scratch) {
       for (int i = lane; i < qn; i += 32) scratch[i] = s.tok[b + i];
       __syncwarp();
@@ -408,6 +479,7 @@ struct SetQuery {
   }
 
   __device__ __forceinline__ int has(uint32_t t) const {
+    if (bm) return (bm[t >> 5] >> (t & 31)) & 1u;
     int lo = 0, hi = qn;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -417,31 +489,104 @@ struct SetQuery {
     return lo < qn && q[lo] == t;
   }
 
-  __device__ __forceinline__ uint32_t eval(const StoreView &s, int32_t cand, int n) const {
-    const int lane = threadIdx.x & 31, sub = lane / L, sl = lane % L;
-    uint32_t out = 0;
-    const int np = (n + VPP - 1) / VPP;
-    for (int p = 0; p < np; ++p) {
-      const int v = p * VPP + sub;
-      const int32_t id = __shfl_sync(FULL, cand, v & 31);
-      int inter = 0, cl = 0;
-      if (v < n && id >= 0) {
-        const uint64_t b0 = s.off[id];
-        cl = (int)(s.off[id + 1] - b0);
-        for (int j = sl; j < cl; j += L) inter += has(s.tok[b0 + j]);
-      }
+  // NS sets of up to 32 candidates (lane j holds candidate j of each set; id < 0: skipped, key 0)
+  template <int NS>
+  __device__ __forceinline__ void eval_n(const StoreView &s, const int32_t *cand, uint32_t *out) const {
+    uint64_t a0[NS];
+    int rb[NS], re[NS], nch[NS], inter[NS];
+    int mx = 0;
 #pragma unroll
-      for (int o = L / 2; o >= 1; o >>= 1) inter += __shfl_xor_sync(FULL, inter, o);
-      const uint32_t key = ((uint32_t)inter << 16) | (uint32_t)(qn + cl - inter);
-      const uint32_t kk = __shfl_sync(FULL, key, (lane % VPP) * L);
-      if (lane / VPP == p) out = kk;
+    for (int j = 0; j < NS; ++j) {
+      uint64_t b = 0, e = 0;
+      if (cand[j] >= 0) {
+        b = s.off[cand[j]];
+        e = s.off[cand[j] + 1];
+      }
+      a0[j] = b & ~3ull;
+      rb[j] = (int)(b - a0[j]);
+      re[j] = (int)(e - a0[j]);
+      nch[j] = cand[j] >= 0 ? (re[j] + 3) >> 2 : 0;
+      inter[j] = 0;
+      mx = max(mx, nch[j]);
     }
-    return out;
+    mx = __reduce_max_sync(FULL, mx);
+    for (int i0 = 0; i0 < mx; i0 += SU) {
+      uint4 buf[NS][SU];
+#pragma unroll
+      for (int j = 0; j < NS; ++j)
+#pragma unroll
+        for (int u = 0; u < SU; ++u)
+          buf[j][u] = i0 + u < nch[j] ? ldg16(s.tok + a0[j] + 4 * (i0 + u)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < NS; ++j)
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          const int c0 = 4 * (i0 + u);
+          if (i0 + u < nch[j]) {
+            const int lo = rb[j] > c0 ? rb[j] - c0 : 0;
+            const int hi = re[j] - c0 < 4 ? re[j] - c0 : 4;
+            const unsigned m = (0xFu >> (4 - hi)) & (0xFu << lo);
+            const unsigned h = (unsigned)has(buf[j][u].x) | ((unsigned)has(buf[j][u].y) << 1) |
+                               ((unsigned)has(buf[j][u].z) << 2) | ((unsigned)has(buf[j][u].w) << 3);
+            inter[j] += __popc(h & m);
+          }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+      out[j] = cand[j] >= 0 ? (((uint32_t)inter[j] << 16) | (uint32_t)(qn + (re[j] - rb[j]) - inter[j])) : 0u;
+  }
+
+  // Key of the candidate whose aligned token chunks are staged at slot (16 B each, SLOTCH at
+  // most; rb/re = first/end token relative to the first chunk).  Lane-local.
+  static constexpr int SLOTCH = 16;
+  __device__ __forceinline__ uint32_t eval_slot(const uint8_t *slot, int rb, int re) const {
+    const int nch = (re + 3) >> 2;
+    int inter = 0;
+#pragma unroll 4
+    for (int i = 0; i < nch; ++i) {
+      const uint4 t = *(const uint4 *)(slot + 16 * i);
+      const int c0 = 4 * i;
+      const int lo = rb > c0 ? rb - c0 : 0;
+      const int hi = re - c0 < 4 ? re - c0 : 4;
+      const unsigned m = (0xFu >> (4 - hi)) & (0xFu << lo);
+      const unsigned h = (unsigned)has(t.x) | ((unsigned)has(t.y) << 1) | ((unsigned)has(t.z) << 2) |
+                         ((unsigned)has(t.w) << 3);
+      inter += __popc(h & m);
+    }
+    return ((uint32_t)inter << 16) | (uint32_t)(qn + (re - rb) - inter);
+  }
+
+  __device__ __forceinline__ uint32_t eval_slot_global(const uint32_t *t0, int rb, int re) const {
+    const int nch = (re + 3) >> 2;
+    int inter = 0;
+    for (int i = 0; i < nch; ++i) {
+      const uint4 t = ldg16(t0 + 4 * i);
+      const int c0 = 4 * i;
+      const int lo = rb > c0 ? rb - c0 : 0;
+      const int hi = re - c0 < 4 ? re - c0 : 4;
+      const unsigned m = (0xFu >> (4 - hi)) & (0xFu << lo);
+      const unsigned h = (unsigned)has(t.x) | ((unsigned)has(t.y) << 1) | ((unsigned)has(t.z) << 2) |
+                         ((unsigned)has(t.w) << 3);
+      inter += __popc(h & m);
+    }
+    return ((uint32_t)inter << 16) | (uint32_t)(qn + (re - rb) - inter);
+  }
+
+  __device__ __forceinline__ uint32_t eval(const StoreView &s, int32_t cand, int n) const {
+    const int lane = threadIdx.x & 31;
+    const int32_t c[1] = {lane < n ? cand : -1};
+    uint32_t o[1];
+    eval_n<1>(s, c, o);
+    return o[0];
   }
 
   __device__ __forceinline__ void eval2(const StoreView &s, int32_t ca, int32_t cb, uint32_t &oa, uint32_t &ob) const {
-    oa = eval(s, ca, 32);
-    ob = eval(s, cb, 32);
+    const int32_t c[2] = {ca, cb};
+    uint32_t o[2];
+    eval_n<2>(s, c, o);
+    oa = o[0];
+    ob = o[1];
   }
 };
 

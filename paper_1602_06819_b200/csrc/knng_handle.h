@@ -56,6 +56,7 @@ struct knng_graph {
   uint64_t *off = nullptr;                      // sets: [cap+1] offsets into tok
   uint32_t *tok = nullptr;                      // sets: tokens
   int64_t tok_cap = 0, tok_n = 0;               // token capacity / tokens in use (host mirror)
+  uint32_t tok_max = 0;                         // largest stored token (valid when tok_n > 0)
   int32_t *ids = nullptr;
   uint32_t *keys = nullptr;
   int32_t *ncnt = nullptr, *nfill = nullptr, *noff = nullptr, *scan_tmp = nullptr;
@@ -81,5 +82,7 @@ inline knng::StoreView graph_store_view(const knng_graph *g) {
   v.nchunks = g->geom.nchunks;
   v.off = g->off;
   v.tok = g->tok;
+  const int64_t vw = g->tok_n > 0 ? ((int64_t)g->tok_max + 32) / 32 : 0;
+  v.vwords = (g->metric == KNNG_JACCARD_U32SET && vw > 0 && vw <= knng::VOCAB_SMEM_WORDS) ? (int)vw : 0;
   return v;
 }

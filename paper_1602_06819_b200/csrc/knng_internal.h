@@ -51,6 +51,11 @@ struct SearchArgs {
   uint32_t *out_keys;
   unsigned long long *stats;   // [0] evals [1] starts [2] skipped [3] expansions
   unsigned long long *prof;    // optional cycle counters (KNNG_PROFILE=1), else null
+  unsigned long long *task_ctr;  // dynamic task scheduler counter (zeroed by the launcher)
+  int pitch;                   // producer stage: bytes per staged row (vectors) / set slot
+  int stages;                  // producer gather pipeline depth (2 or 4; sets: 4)
+  int nprod;                   // producer warps per CTA (1..3)
+  int lane_eval;               // producers evaluate one row per lane where the width allows
 };
 
 struct BallArgs {

@@ -20,89 +20,379 @@
 
 namespace knng {
 
-constexpr int RING_CHUNKS = 8;    // smem ring of 8 x 32 precomputed draws per CTA
+constexpr int RING_CHUNKS = 32;   // smem ring of 32 x 32 evaluated draws per CTA (16 KB)
 constexpr int FASTC = 4;          // chunks the consumer's skip-only fast path commits at once
+constexpr int STAGES = 4;         // producer gather pipeline depth (chunks of 32 rows in flight)
+constexpr int HDR_BYTES = 128;
 
 struct RingHdr {
-  int seq[RING_CHUNKS];   // seq[s] = c + 1 once chunk c is in slot s
   int consumed;           // chunks < consumed are free
   int done;               // consumer finished the task
+  int next_task;          // dynamic task scheduler: the CTA's next task
+  int published;          // debug: last chunk a producer published
+  int pstate;             // debug: producer state
 };
 
 // Producer warp(s): speculative evaluation of the random starts.  The draw sequence of a search
 // is fixed by the counter RNG (Q4) and the key of a draw is a pure function of (query, node), so
 // producers evaluate draws ahead of the consumer, 32 per chunk, into the CTA's smem ring.
 // Nothing here touches a counter, the visited sets or the top-k.
-template <class QT>
-__device__ __forceinline__ void produce(const SearchArgs &a, const QT &Q, volatile RingHdr *hdr,
-                                        int2 *ring, int pw, int nprod, int64_t nch, uint64_t h3, int64_t m,
-                                        const int32_t *pool) {
+//
+// The rows of the drawn nodes are gathered into shared memory with 16-byte cp.async copies
+// (no registers held by loads in flight), STAGES chunks deep; the keys are computed from shared
+// memory.  Producer pw owns chunks pw, pw + nprod, ...; local iteration i <-> chunk pw + i*nprod.
+struct ProdCtx {
+  volatile RingHdr *hdr;
+  unsigned long long *ring;   // [RING_CHUNKS][32][2]: (tag << 32 | node), (tag << 32 | key), tag = chunk + 1
+  uint8_t *stg;       // this producer's STAGES x 32 rows (pitch bytes each)
+  int32_t *meta;      // this producer's STAGES x 32 x 4 ints (node, rb, re, -)
+  int pitch;
+  int pw, nprod;
+  int64_t nch;
+  uint64_t h3;
+  int64_t m;
+  const int32_t *pool;
+};
+
+__device__ __forceinline__ int32_t draw_node(const ProdCtx &x, int64_t i) {
+  const int64_t c = x.pw + i * x.nprod;
+  const uint64_t idx = rng_index(x.h3, (uint64_t)(c * 32 + (threadIdx.x & 31)), (uint64_t)x.m);
+  return x.pool ? x.pool[idx] : (int32_t)idx;
+}
+
+// publish chunk (local iteration i) to the ring; false when the consumer has finished
+__device__ __forceinline__ bool publish(const ProdCtx &x, int64_t i, int32_t node, uint32_t key, long long &p_wait,
+                                        bool prof) {
   const int lane = threadIdx.x & 31;
-  long long p_wait = 0, p_work = 0;
-  // chunks c and c + nprod are produced together (both sets of loads in flight)
-  for (int64_t c = pw; c < nch; c += 2 * nprod) {
-    const int64_t c2 = c + nprod;
-    const bool two = c2 < nch;
-    const int64_t clast = two ? c2 : c;
-    const long long t0 = a.prof ? clock64() : 0;
-    while (clast - hdr->consumed >= RING_CHUNKS && !hdr->done) __nanosleep(32);
-    const long long t1 = a.prof ? clock64() : 0;
-    p_wait += t1 - t0;
-    if (hdr->done) break;
-    const uint64_t ia = rng_index(h3, (uint64_t)(c * 32 + lane), (uint64_t)m);
-    const int32_t na = pool ? pool[ia] : (int32_t)ia;
-    int32_t nb = -1;
-    if (two) {
-      const uint64_t ib = rng_index(h3, (uint64_t)(c2 * 32 + lane), (uint64_t)m);
-      nb = pool ? pool[ib] : (int32_t)ib;
-    }
-    uint32_t ka, kb;
-    Q.eval2(a.st, na, nb, ka, kb);
-    // repeats of a node inside a window are resolved by the consumer (the atomicOr that flips the
-    // node's visited bit decides which draw evaluates it)
-    volatile int *ra = (volatile int *)(ring + (c % RING_CHUNKS) * 32 + lane);
-    ra[0] = na;
-    ra[1] = (int)ka;
-    if (two) {
-      volatile int *rb = (volatile int *)(ring + (c2 % RING_CHUNKS) * 32 + lane);
-      rb[0] = nb;
-      rb[1] = (int)kb;
-    }
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) {
-      hdr->seq[c % RING_CHUNKS] = (int)(c + 1);
-      if (two) hdr->seq[c2 % RING_CHUNKS] = (int)(c2 + 1);
-    }
-    if (a.prof) p_work += clock64() - t1;
+  const int64_t c = x.pw + i * x.nprod;
+  const long long t0 = prof ? clock64() : 0;
+  int dn = 0;
+  if (lane == 0)
+    while (c - x.hdr->consumed >= RING_CHUNKS && !(dn = x.hdr->done)) __nanosleep(32);
+  dn = __shfl_sync(FULL, dn, 0);
+  if (prof) p_wait += clock64() - t0;
+  if (dn) return false;
+  // Each entry word carries its chunk's tag next to the datum: an aligned 64-bit shared store is
+  // single-copy atomic, so the consumer sees a whole (tag, datum) pair and needs no fence or barrier.
+  const unsigned long long tag = (unsigned long long)(unsigned)(c + 1) << 32;
+  volatile unsigned long long *e = x.ring + ((c % RING_CHUNKS) * 32 + lane) * 2;
+  e[0] = tag | (uint32_t)node;
+  e[1] = tag | key;
+#ifdef KNNG_DEBUG_WAIT
+  if (lane == 0) x.hdr->published = (int)c;
+#endif
+  return true;
+}
+
+// consumer: wait until chunk ch is in its slot and read this lane's (node, key)
+__device__ __forceinline__ void ring_get(const unsigned long long *ring, volatile RingHdr *hdr, int64_t ch,
+                                         int32_t &node, uint32_t &key) {
+  const unsigned tag = (unsigned)(ch + 1);
+  const volatile unsigned long long *e = ring + ((ch % RING_CHUNKS) * 32 + (threadIdx.x & 31)) * 2;
+  unsigned long long w0, w1;
+#ifdef KNNG_DEBUG_WAIT
+  long long n = 0;
+#endif
+  for (;;) {
+    w0 = e[0];
+    w1 = e[1];
+    if (__all_sync(FULL, (unsigned)(w0 >> 32) == tag && (unsigned)(w1 >> 32) == tag)) break;
+#ifdef KNNG_DEBUG_WAIT
+    if (++n == (1ll << 22) && (threadIdx.x & 31) == 0)
+      printf("KNNG stuck wait: block %d chunk %lld consumed %d done %d published %d pstate %d\n", blockIdx.x,
+             (long long)ch, hdr->consumed, hdr->done, hdr->published, hdr->pstate);
+#endif
+    __nanosleep(16);
   }
-  if (a.prof && lane == 0) {
+  node = (int32_t)(uint32_t)w0;
+  key = (uint32_t)w1;
+}
+
+__device__ __forceinline__ bool consumer_done(const ProdCtx &x) {
+  int dn = (threadIdx.x & 31) == 0 ? x.hdr->done : 0;
+  return __shfl_sync(FULL, dn, 0) != 0;
+}
+
+// Evaluators of a staged chunk (32 rows at stage + j * pitch): key of candidate j in lane j.
+// Warp form: L lanes per row (VecQuery::eval_smem).
+template <class QT>
+struct EvalWarp {
+  static constexpr int NCH = 0;   // chunks per row known at run time only
+  const QT &Q;
+  __device__ __forceinline__ uint32_t key(const uint8_t *sb, int pitch, int nck) const {
+    return Q.eval_smem(sb, pitch, nck);
+  }
+};
+// Lane form: one lane per row, the whole distance in-lane (no shuffles; NCH independent chunk
+// chains), the query's chunks broadcast from shared memory.  F32 keeps the canonical tree (Q24):
+// with NCH <= 32 partial i is chunk i alone (f4_leaf from +0), partials >= NCH are +0, and the
+// levels o = 16..1 add partial i + o into partial i -- the xor butterfly's values.
+template <int M, int NCH_>
+struct EvalLane {
+  static constexpr int NCH = NCH_;
+  const uint8_t *qsm;   // the query's NCH chunks (shared)
+  __device__ __forceinline__ uint32_t key(const uint8_t *sb, int pitch, int) const {
+    const uint8_t *row = sb + (threadIdx.x & 31) * pitch;
+    if (M == M_U8) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+        chunk_acc<M_U8>(acc, *(const uint4 *)(qsm + 16 * c), *(const uint4 *)(row + 16 * c));
+      return acc;
+    } else {
+      static_assert(NCH <= 32, "lane form: one chunk per partial");
+      float p[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        p[i] = i < NCH ? f4_leaf(0.0f, *(const uint4 *)(qsm + 16 * i), *(const uint4 *)(row + 16 * i)) : 0.0f;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < o; ++i) p[i] = __fadd_rn(p[i], p[i + o]);
+      return __float_as_uint(p[0]);
+    }
+  }
+};
+
+// vectors: lane's copies within a stage are the 16-byte chunks e = lane + 32 j (j < nchunks) of the
+// 32 x nchunks stage, i.e. row e / nchunks, chunk e % nchunks (walked incrementally)
+template <int S, class EV>
+__device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
+  const int lane = threadIdx.x & 31;
+  const int nck = EV::NCH > 0 ? EV::NCH : a.st.nchunks;
+  const uint8_t *base = a.st.vec;
+  const size_t stride = a.st.stride;
+  const int r0 = lane / nck, c0 = lane % nck, rs = 32 / nck, cs = 32 % nck;
+  const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
+  const bool prof = a.prof != nullptr;
+  long long p_wait = 0, p_work = 0;
+  auto issue = [&](int st, int32_t node) {
+    x.meta[(st * 32 + lane) * 4] = node;
+    uint8_t *dst = x.stg + st * 32 * x.pitch;
+    int r = r0, cc = c0;
+#pragma unroll 8
+    for (int j = 0; j < nck; ++j) {
+      const int32_t id = __shfl_sync(FULL, node, r);
+      cp_async16(dst + r * x.pitch + cc * 16, base + (size_t)id * stride + (size_t)cc * 16);
+      cc += cs;
+      r += rs;
+      if (cc >= nck) { cc -= nck; ++r; }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < ni) issue(s, draw_node(x, s));
+    cp_async_commit();
+  }
+  int32_t pn = S - 1 < ni ? draw_node(x, S - 1) : 0;
+#ifdef KNNG_DEBUG_WAIT
+  if (lane == 0) { x.hdr->published = -1; x.hdr->pstate = 1000000 + (int)ni; }
+#endif
+  for (int64_t i = 0; i < ni; ++i) {
+    const long long t0 = prof ? clock64() : 0;
+#ifdef KNNG_DEBUG_WAIT
+    if (lane == 0) x.hdr->pstate = 1 + 10 * (int)i;
+#endif
+    if (consumer_done(x)) break;
+    const int64_t ii = i + S - 1;
+    if (ii < ni) {
+      issue((int)(ii % S), pn);
+      if (ii + 1 < ni) pn = draw_node(x, ii + 1);   // (pool load) in flight during this compute
+    }
+    cp_async_commit();
+#ifdef KNNG_DEBUG_WAIT
+    if (lane == 0) x.hdr->pstate = 2 + 10 * (int)i;
+#endif
+    cp_async_wait<S - 1>();
+    __syncwarp();
+#ifdef KNNG_DEBUG_WAIT
+    if (lane == 0) x.hdr->pstate = 3 + 10 * (int)i;
+#endif
+    const int st = (int)(i % S);
+    const uint32_t key = ev.key(x.stg + st * 32 * x.pitch, x.pitch, nck);
+    const int32_t node = x.meta[(st * 32 + lane) * 4];
+    __syncwarp();
+    if (prof) p_work += clock64() - t0;
+#ifdef KNNG_DEBUG_WAIT
+    if (lane == 0) x.hdr->pstate = 4 + 10 * (int)i;
+#endif
+    if (!publish(x, i, node, key, p_wait, prof)) break;
+  }
+#ifdef KNNG_DEBUG_WAIT
+  if (lane == 0) x.hdr->pstate = -x.hdr->pstate;
+#endif
+  cp_async_wait<0>();
+  __syncwarp();
+  if (prof && lane == 0) {
     atomicAdd(a.prof + 3, (unsigned long long)p_work);
     atomicAdd(a.prof + 4, (unsigned long long)p_wait);
   }
 }
 
+template <class EV>
+__device__ __forceinline__ void produce_vec_s(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
+  if (a.stages <= 2) produce_vec<2>(a, ev, x);
+  else produce_vec<4>(a, ev, x);
+}
+
+// the producer's evaluator: lane form for the configured row widths, else the warp form
+template <int M, int L, int CPL>
+__device__ __forceinline__ void produce_rows(const SearchArgs &a, const VecQuery<M, L, CPL> &Q, const ProdCtx &x,
+                                             uint8_t *qsm, int64_t qrow) {
+  const int lane = threadIdx.x & 31;
+  const int nck = a.st.nchunks;
+  const bool lane_form = a.lane_eval && ((M == M_U8 && (nck == 8 || nck == 2)) || (M == M_F32 && nck == 24));
+  if (lane_form) {
+    const uint8_t *qg = a.qs.vec + (size_t)qrow * a.qs.stride;
+    for (int c = lane; c < nck; c += 32) *(uint4 *)(qsm + 16 * c) = ldg16(qg + 16 * c);
+    __syncwarp();
+    if constexpr (M == M_U8) {
+      if (nck == 8) produce_vec_s(a, EvalLane<M_U8, 8>{qsm}, x);
+      else produce_vec_s(a, EvalLane<M_U8, 2>{qsm}, x);
+    } else if constexpr (M == M_F32) {
+      produce_vec_s(a, EvalLane<M_F32, 24>{qsm}, x);
+    }
+    return;
+  }
+  if (M == M_U8 && nck <= 8 && a.qs.nchunks <= 8) {
+    // u8 rows of <= 128 B: 4 lanes x 2 chunks per candidate (2 shuffle levels)
+    VecQuery<M_U8, 4, 2> PQ;
+    PQ.load(a.qs, qrow, nullptr);
+    produce_vec_s(a, EvalWarp<VecQuery<M_U8, 4, 2>>{PQ}, x);
+  } else {
+    produce_vec_s(a, EvalWarp<VecQuery<M, L, CPL>>{Q}, x);
+  }
+}
+
+// sets: lane j stages candidate j's token range (aligned 16-byte chunks, SLOTCH at most) in its own
+// slot; longer sets are evaluated from global memory.  Two prefetch levels: the node of chunk
+// i + STAGES and the offsets of chunk i + STAGES - 1 are loaded while chunk i is computed.
+template <int L>
+__device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<L> &Q, const ProdCtx &x) {
+  constexpr int SLOTCH = SetQuery<L>::SLOTCH;
+  const int lane = threadIdx.x & 31;
+  const uint32_t *tok = a.st.tok;
+  const uint64_t *off = a.st.off;
+  const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
+  const bool prof = a.prof != nullptr;
+  long long p_wait = 0, p_work = 0;
+  auto issue = [&](int st, int32_t node, uint64_t b, uint64_t e) {
+    const uint64_t a0 = b & ~3ull;
+    const int rb = (int)(b - a0), re = (int)(e - a0);
+    int4 *mt = (int4 *)(x.meta + (st * 32 + lane) * 4);
+    *mt = make_int4(node, rb, re, 0);
+    const int nch = (re + 3) >> 2;
+    if (nch <= SLOTCH) {
+      uint8_t *dst = x.stg + (st * 32 + lane) * x.pitch;
+      for (int j = 0; j < nch; ++j) cp_async16(dst + 16 * j, tok + a0 + 4 * j);
+    }
+  };
+  // prologue
+  int32_t n1 = 0;
+  uint64_t b1 = 0, e1 = 0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ni) {
+      const int32_t nd = draw_node(x, s);
+      issue(s, nd, off[nd], off[nd + 1]);
+    }
+    cp_async_commit();
+  }
+  if (STAGES - 1 < ni) {
+    n1 = draw_node(x, STAGES - 1);
+    b1 = off[n1];
+    e1 = off[n1 + 1];
+  }
+  int32_t n2 = STAGES < ni ? draw_node(x, STAGES) : 0;
+  for (int64_t i = 0; i < ni; ++i) {
+    const long long t0 = prof ? clock64() : 0;
+    if (consumer_done(x)) break;
+    const int64_t ii = i + STAGES - 1;
+    if (ii < ni) {
+      issue((int)(ii % STAGES), n1, b1, e1);
+      if (ii + 1 < ni) {
+        n1 = n2;
+        b1 = off[n1];
+        e1 = off[n1 + 1];
+        if (ii + 2 < ni) n2 = draw_node(x, ii + 2);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    __syncwarp();
+    const int st = (int)(i % STAGES);
+    const int4 mt = *(const int4 *)(x.meta + (st * 32 + lane) * 4);
+    uint32_t key;
+    if (((mt.z + 3) >> 2) <= SLOTCH) {
+      key = Q.eval_slot(x.stg + (st * 32 + lane) * x.pitch, mt.y, mt.z);
+    } else {   // long set: straight from global memory
+      const uint64_t b = off[mt.x];
+      key = Q.eval_slot_global(tok + (b & ~3ull), mt.y, mt.z);
+    }
+    __syncwarp();
+    if (prof) p_work += clock64() - t0;
+    if (!publish(x, i, mt.x, key, p_wait, prof)) break;
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  if (prof && lane == 0) {
+    atomicAdd(a.prof + 3, (unsigned long long)p_work);
+    atomicAdd(a.prof + 4, (unsigned long long)p_wait);
+  }
+}
+
+template <class QT>
+__device__ __forceinline__ void set_bitmap(QT &, const uint32_t *) {}
+template <int L>
+__device__ __forceinline__ void set_bitmap(SetQuery<L> &Q, const uint32_t *bm) { Q.bm = bm; }
+template <class QT>
+__device__ __forceinline__ int query_len(const QT &) { return 0; }
+template <int L>
+__device__ __forceinline__ int query_len(const SetQuery<L> &Q) { return Q.qn; }
+template <int M, int L, int CPL>
+__device__ __forceinline__ void produce_any(const SearchArgs &a, const VecQuery<M, L, CPL> &Q, const ProdCtx &x,
+                                            uint8_t *qsm, int64_t qrow) {
+  produce_rows(a, Q, x, qsm, qrow);
+}
+template <int L>
+__device__ __forceinline__ void produce_any(const SearchArgs &a, const SetQuery<L> &Q, const ProdCtx &x, uint8_t *,
+                                            int64_t) {
+  produce_set(a, Q, x);
+}
+
 // K1: one CTA per (query, partition) task: warp 0 runs the search in the paper's sequential
 // order, warps 1.. produce its random-start keys ahead of it.
 template <int M, int L, int CPL>
-__global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
+__global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  volatile RingHdr *hdr = (volatile RingHdr *)smem;
-  int2 *ring = (int2 *)(smem + 128);
-  int32_t *rowbuf = (int32_t *)(smem + 128 + RING_CHUNKS * 32 * 8);          // [k][k]
-  int32_t *rowbuf2 = rowbuf + a.k * a.k;                                      // [32][k]
-  uint32_t *qscr = (uint32_t *)(rowbuf2 + 32 * a.k);                          // [2][QMAX] (sets)
-  uint32_t *sbits = qscr + (M == M_JAC ? 2 * QMAX : 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nprod = (blockDim.x >> 5) - 1;
+  const int k = a.k;
+  volatile RingHdr *hdr = (volatile RingHdr *)smem;
+  unsigned long long *ring = (unsigned long long *)(smem + HDR_BYTES);
+  const int S = a.stages;
+  uint8_t *stg = smem + HDR_BYTES + RING_CHUNKS * 32 * 16;                    // [nprod][S][32] rows
+  int32_t *meta = (int32_t *)(stg + (size_t)nprod * S * 32 * a.pitch);        // [nprod][S][32][4]
+  uint8_t *qprod = (uint8_t *)(meta + nprod * S * 32 * 4);                   // [nprod][512 B] query copies
+  int32_t *rowbuf = (int32_t *)(qprod + nprod * 512);                         // [k][k]
+  int32_t *rowbuf2 = rowbuf + k * k;                                          // [32][k]
+  uint32_t *qscr = (uint32_t *)(rowbuf2 + 32 * k);                            // [2][QMAX] (sets)
+  uint32_t *vbm = qscr + (M == M_JAC ? 2 * QMAX : 0);                        // [vwords] (sets)
+  const int vwords = M == M_JAC ? a.st.vwords : 0;
+  uint32_t *sbits = vbm + vwords;
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   uint32_t *bits = a.smem_bits ? sbits : a.gbits + (int64_t)blockIdx.x * a.bits_words;
-  const int k = a.k;
   const float rk = 1.0f / (float)k;
   unsigned long long s_evals = 0, s_starts = 0, s_skip = 0, s_exp = 0;
+  int prev_qn = 0;                              // sets: tokens of the previous query (scratch 0)
+  for (int w = threadIdx.x; w < vwords; w += blockDim.x) vbm[w] = 0;
+  if (threadIdx.x == 0) hdr->next_task = (int)blockIdx.x;
 
-  for (int64_t task = blockIdx.x; task < T; task += gridDim.x) {
+  for (;;) {
+    __syncthreads();                          // previous task finished by every warp
+    const int64_t task = hdr->next_task;
+    if (task >= T) break;
     const int64_t b = task / Pn;
     const int pl = (int)(task % Pn);          // output slot
     const int p = a.part_lo + pl;             // partition searched
@@ -110,11 +400,18 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
     const int32_t *pool = a.P > 0 ? a.members + (size_t)p * a.member_cap : nullptr;
     const int64_t words = (m + 31) >> 5;
     uint32_t *ev = bits, *ex = bits + words;
-    __syncthreads();
     for (int64_t w = threadIdx.x; w < 2 * words; w += blockDim.x) bits[w] = 0;
-    if (threadIdx.x < RING_CHUNKS) hdr->seq[threadIdx.x] = 0;
+    for (int w = threadIdx.x; w < RING_CHUNKS * 32; w += blockDim.x)   // no stale tags from the last task
+      ((uint4 *)ring)[w] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) { hdr->consumed = 0; hdr->done = 0; }
+    if (M == M_JAC && vwords > 0 && warp == 0)   // clear the previous query's vocabulary bits
+      for (int i = lane; i < prev_qn; i += 32) {
+        const uint32_t t = qscr[i];
+        if ((t >> 5) < (uint32_t)vwords) vbm[t >> 5] = 0;
+      }
     __syncthreads();
+    // dynamic task scheduling: the CTA's next task (read after the next top barrier)
+    if (threadIdx.x == 0) hdr->next_task = (int)(gridDim.x + atomicAdd(a.task_ctr, 1ull));
 
     // budget (Q6) -- never more than the pool (Q7)
     int64_t budget = (int64_t)floor((double)m / a.speedup);
@@ -127,18 +424,38 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
 
     typename QuerySel<M, L, CPL>::T Q;
     Q.load(a.qs, a.qrow0 + b, M == M_JAC ? qscr + (warp < 2 ? warp : 1) * QMAX : nullptr);
+    if (M == M_JAC && vwords > 0) {
+      // vocabulary bitmap of the query: one bit test per candidate token (tokens beyond the store's
+      // largest token cannot match and are left out)
+      const int qn = query_len(Q);
+      if (warp == 0 && qn <= QMAX) {
+        for (int i = lane; i < qn; i += 32) {
+          const uint32_t t = qscr[i];
+          if ((t >> 5) < (uint32_t)vwords) atomicOr(vbm + (t >> 5), 1u << (t & 31));
+        }
+        prev_qn = qn;
+      } else if (warp == 0) {
+        prev_qn = 0;
+      }
+      __syncthreads();
+      if (qn <= QMAX) set_bitmap(Q, vbm);
+    }
     const uint64_t h3 = rng_prefix(a.seed, (uint64_t)(a.pid_base + b), (uint64_t)p);
     if (warp > 0) {
-      if (budget > 0) {
-        if (M == M_U8 && a.st.nchunks <= 8 && a.qs.nchunks <= 8) {
-          // u8 rows of <= 128 B: 4 lanes x 2 chunks per candidate (2 shuffle levels), measured the
-          // fastest layout for 32-draw chunks (scripts/micro/eval_micro.cu)
-          VecQuery<M_U8, 4, 2> PQ;
-          PQ.load(a.qs, a.qrow0 + b, nullptr);
-          produce(a, PQ, hdr, ring, warp - 1, nprod, nch, h3, m, pool);
-        } else {
-          produce(a, Q, hdr, ring, warp - 1, nprod, nch, h3, m, pool);
-        }
+      if (budget > 0 && nch > 0) {
+        ProdCtx x;
+        x.hdr = hdr;
+        x.ring = ring;
+        x.stg = stg + (size_t)(warp - 1) * S * 32 * a.pitch;
+        x.meta = meta + (warp - 1) * S * 32 * 4;
+        x.pitch = a.pitch;
+        x.pw = warp - 1;
+        x.nprod = nprod;
+        x.nch = nch;
+        x.h3 = h3;
+        x.m = m;
+        x.pool = pool;
+        produce_any(a, Q, x, qprod + (warp - 1) * 512, a.qrow0 + b);
       }
       continue;
     }
@@ -167,27 +484,19 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
         const int64_t ch0 = jbase / 32;
         if (top.cnt > 0 && nprod > 0 && ch0 + FASTC <= nch && c + 32 * FASTC <= budget) {
           const long long tw = a.prof ? clock64() : 0;
-          for (int t = 0; t < FASTC; ++t) {
-            const int slot = (int)((ch0 + t) % RING_CHUNKS);
-            while (hdr->seq[slot] != (int)(ch0 + t + 1)) __nanosleep(20);
-          }
+          int32_t fnode[FASTC];
+          uint32_t fkey[FASTC];
+#pragma unroll
+          for (int t = 0; t < FASTC; ++t) ring_get(ring, hdr, ch0 + t, fnode[t], fkey[t]);
           if (a.prof) p_wait += clock64() - tw;
-          __threadfence_block();
           if (!thr_ok || thr_key != top.key_at0) {
             thr.set(top.key_at0, a.e_num, a.e_den);
             thr_key = top.key_at0;
             thr_ok = true;
           }
-          int32_t fnode[FASTC];
-          uint32_t fkey[FASTC];
           bool pass = false;
 #pragma unroll
-          for (int t = 0; t < FASTC; ++t) {
-            const volatile int *rs = (const volatile int *)(ring + ((ch0 + t) % RING_CHUNKS) * 32 + lane);
-            fnode[t] = rs[0];
-            fkey[t] = (uint32_t)rs[1];
-            pass |= !thr.skip(fkey[t]);
-          }
+          for (int t = 0; t < FASTC; ++t) pass |= !thr.skip(fkey[t]);
           if (!__any_sync(FULL, pass)) {
             bool fr[FASTC];
 #pragma unroll
@@ -216,15 +525,12 @@ __global__ void __launch_bounds__(64, 8) k_search(SearchArgs a) {
         const int64_t j = jbase + lane;
         const int64_t ch = jbase / 32;
         if (ch < nch && nprod > 0) {                 // produced ahead into the ring
-          const int slot = (int)(ch % RING_CHUNKS);
           const long long tw = a.prof ? clock64() : 0;
-          while (hdr->seq[slot] != (int)(ch + 1)) __nanosleep(20);
+          uint32_t kk;
+          ring_get(ring, hdr, ch, wnode, kk);
+          wkey = kk;
           if (a.prof) p_wait += clock64() - tw;
           ++p_win;
-          __threadfence_block();
-          const volatile int *rs = (const volatile int *)(ring + slot * 32 + lane);
-          wnode = rs[0];
-          wkey = (uint32_t)rs[1];
           whave = true;
           __syncwarp();
           if (lane == 0) hdr->consumed = (int)(ch + 1);
@@ -456,22 +762,31 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   if (T == 0) return cudaSuccess;
-  // consumer + producer (a second producer did not pay: measured on C2/C3)
-  const int warps = a.starts ? 1 : 2;
-  size_t smem = 128 + RING_CHUNKS * 32 * 8 + (size_t)(a.k * a.k + 32 * a.k) * 4 + (M == M_JAC ? 2 * QMAX * 4 : 0);
+  // consumer + a.nprod producers (none when the starts are injected)
+  const int nprod = a.starts ? 0 : a.nprod;
+  const int warps = 1 + nprod;
+  size_t smem = HDR_BYTES + RING_CHUNKS * 32 * 16 + (size_t)nprod * (a.stages * 32 * (a.pitch + 16) + 512) +
+                (size_t)(a.k * a.k + 32 * a.k) * 4 + (M == M_JAC ? 2 * QMAX * 4 + (size_t)a.st.vwords * 4 : 0);
   if (a.smem_bits) smem += (size_t)a.bits_words * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  int64_t blocks = T;
+  // persistent grid: the CTAs that fit at once (dynamic task scheduling balances the tail)
+  int per_sm = 0;
+  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL>, warps * 32, smem);
+  if (oe != cudaSuccess) return oe;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int64_t blocks = T < (int64_t)per_sm * nsm ? T : (int64_t)per_sm * nsm;
   if (!a.smem_bits && blocks > a.gslots) blocks = a.gslots;
-  if (getenv("KNNG_PROFILE")) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL>, warps * 32, smem);
+  cudaError_t me = cudaMemsetAsync(a.task_ctr, 0, sizeof(unsigned long long), s);
+  if (me != cudaSuccess) return me;
+  if (getenv("KNNG_PROFILE"))
     fprintf(stderr, "KNNG_PROFILE k_search: %lld CTAs, %d per SM resident (%zu B smem each)\n", (long long)blocks,
             per_sm, smem);
-  }
   k_search<M, L, CPL><<<(unsigned)blocks, warps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
