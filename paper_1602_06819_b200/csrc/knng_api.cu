@@ -190,7 +190,7 @@ static void free_graph(knng_graph *g) {
   if (!g) return;
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
-  void *bufs[] = {g->vec, g->ids, g->keys, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->part_of, g->local_idx,
+  void *bufs[] = {g->vec, g->ids, g->keys, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->part_of, g->local_idx, g->lrows,
                   g->members, g->member_cnt, g->medoids, g->off, g->tok};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -297,22 +297,45 @@ static int check_params(const knng_params *p) {
   return 0;
 }
 
-// search workspace: returns smem flag and bits words per slot
-struct SearchPlan {
-  int smem;
-  int64_t bits_words;
-  int64_t slots;
-};
-
-static SearchPlan plan_search(knng_graph *g, int64_t tasks, int64_t mmax) {
-  SearchPlan sp;
-  sp.bits_words = 2 * ((mmax + 31) / 32);
-  // visited + expanded bitmaps in shared memory when a CTA still fits >= 4 times per SM
-  size_t lim = 40 * 1024;
-  if (const char *e = getenv("KNNG_SMEM_BITS_KB")) lim = (size_t)atoi(e) * 1024;
-  sp.smem = (size_t)sp.bits_words * 4 <= lim ? 1 : 0;
-  sp.slots = sp.smem ? tasks : std::min<int64_t>(tasks, 148 * 8);
-  return sp;
+// K1 launch shape.  Each CTA runs one (query, partition) task at a time: a consumer warp (the
+// sequential iGNNS) and a producer warp (the random starts, S chunks of rows in flight).  The walks
+// are latency chains, so the plan first makes room for every task at once (up to 8 CTAs per SM,
+// the register limit), then spends what shared memory is left on the visited bitmaps and a deeper
+// ring.  Knobs KNNG_STAGES / KNNG_NPROD / KNNG_LANE_EVAL / KNNG_RING / KNNG_SMEM_BITS override it
+// (measurement only).
+static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  a.bits_words = 2 * ((mmax + 31) / 32);
+  a.nprod = 1;
+  a.lane_eval = 1;
+  a.stages = 2;
+  const int need = (int)std::min<int64_t>(8, (tasks + nsm - 1) / nsm);
+  auto occ = [&](const SearchArgs &x) {
+    const size_t sm = search_smem_bytes(x, sets) + 1024;
+    return (int)std::min<size_t>(8, (228 * 1024) / sm);
+  };
+  // preference order: smem bitmaps + 32-chunk ring, global bitmaps + 32, smem + 16, global + 16
+  const int cand[4][2] = {{1, 32}, {0, 32}, {1, 16}, {0, 16}};
+  int best = -1, best_occ = -1;
+  for (int i = 0; i < 4; ++i) {
+    SearchArgs x = a;
+    x.smem_bits = cand[i][0];
+    x.ring = cand[i][1];
+    if (x.smem_bits && (size_t)x.bits_words * 4 > 64 * 1024) continue;
+    const int o = occ(x);
+    if (o >= need) { best = i; best_occ = o; break; }
+    if (o > best_occ) { best = i; best_occ = o; }
+  }
+  a.smem_bits = cand[best][0];
+  a.ring = cand[best][1];
+  if (const char *e = getenv("KNNG_STAGES")) a.stages = atoi(e) <= 2 ? 2 : 4;
+  if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
+  if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
+  if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 16 ? 16 : 32;
+  if (const char *e = getenv("KNNG_SMEM_BITS")) a.smem_bits = atoi(e) != 0;
+  a.gslots = a.smem_bits ? 0 : std::min<int64_t>(tasks, (int64_t)nsm * 8);
 }
 
 static int64_t max_pool(knng_graph *g) {
@@ -332,8 +355,6 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   const int64_t mmax = max_pool(g);
   if (g->P > 0 && mmax == 0) return fail(KNNG_ERR_EMPTY, "all partitions are empty");
   const int pc = part_hi - part_lo;
-  SearchPlan sp = plan_search(g, nq * pc, mmax);
-  if (!sp.smem) CK(g->w_bits.ensure((size_t)sp.slots * sp.bits_words * 4));
   SearchArgs a;
   memset(&a, 0, sizeof a);
   a.st = graph_store_view(g);
@@ -352,6 +373,7 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.member_cnt = g->member_cnt;
   a.part_of = g->part_of;
   a.local_idx = g->local_idx;
+  a.lrows = g->lrows;
   a.speedup = p->speedup;
   a.e_num = p->expansion_num;
   a.e_den = p->expansion_den;
@@ -360,24 +382,15 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.starts = d_starts;
   a.nstarts = nstarts;
   a.G = 8;
-  a.gbits = g->w_bits.as<uint32_t>();
-  a.gslots = sp.slots;
-  a.bits_words = sp.bits_words;
-  a.smem_bits = sp.smem;
   a.out_ids = out_i;
   a.out_keys = out_k;
   a.stats = g->w_stats.as<unsigned long long>();
   a.prof = getenv("KNNG_PROFILE") ? a.stats + 8 : nullptr;   // cycle counters -> stats[8..13]
   a.task_ctr = a.stats + 14;
   a.pitch = g->metric == KNNG_JACCARD_U32SET ? 16 * 16 + 16 : (int)g->geom.stride + 16;
-  // producer shape (tuning knobs, overridable for measurement)
-  a.stages = g->metric == KNNG_JACCARD_U32SET ? 4 : 2;
-  a.nprod = 1;
-  a.lane_eval = 1;
-  if (const char *e = getenv("KNNG_STAGES")) a.stages = atoi(e) <= 2 ? 2 : 4;
-  if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
-  if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
-  if (g->metric == KNNG_JACCARD_U32SET) a.stages = 4;
+  plan_k1(a, g->metric == KNNG_JACCARD_U32SET, nq * pc, mmax);
+  if (!a.smem_bits) CK(g->w_bits.ensure((size_t)a.gslots * a.bits_words * 4));
+  a.gbits = g->w_bits.as<uint32_t>();
   cudaError_t e = launch_search(g->geom, a, g->stream, nl);
   if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
   return 0;
@@ -517,15 +530,22 @@ static int stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, c
   }
   const int64_t ballmax = ball_bound(n_t, g->k, p->depth);
   CK(g->w_sorted.ensure((size_t)nq_slots * ballmax * 8));
-  // A7: row_v = top-k(row_v u proposals), proposal (slot b) carries the new id n_t + b
-  CK(launch_merge_props(g->metric, g->ids, g->keys, g->k, n_t, nq_slots, props_all, prop_cnt_all, (int)ballmax,
-                        g->ncnt, g->nfill, g->noff, g->scan_tmp, g->w_sorted.as<int2>(), g->stream, nl));
-  // A8: placement at the nearest medoid
+  // A8: placement at the nearest medoid.  It reads only the new points and the medoids, and the
+  // search of this batch is complete, so it runs before the merge: the merged rows' partition-local
+  // view (lrows) then sees the new ids' partitions.
   if (g->P > 0) {
     CK(g->w_target.ensure((size_t)B * 4));
     CK(launch_place(g->geom, graph_store_view(g), n_t, B, g->P, g->medoids, g->members, g->cap, g->member_cnt,
                     g->part_of, g->local_idx, g->w_target.as<int32_t>(), g->stream));
     *nl += 2;
+  }
+  // A7: row_v = top-k(row_v u proposals), proposal (slot b) carries the new id n_t + b
+  CK(launch_merge_props(g->metric, g->ids, g->keys, g->k, n_t, nq_slots, props_all, prop_cnt_all, (int)ballmax,
+                        g->ncnt, g->nfill, g->noff, g->scan_tmp, g->w_sorted.as<int2>(), g->stream, nl,
+                        g->P > 0 ? g->lrows : nullptr, g->part_of, g->local_idx));
+  if (g->P > 0) {   // the new rows' partition-local view
+    CK(launch_lrows(g->ids, g->k, n_t, B, g->part_of, g->local_idx, g->lrows, g->stream));
+    ++*nl;
   }
   g->n = n_t + B;
   g->pend_B = 0;

@@ -56,6 +56,7 @@ struct knng_graph {
   uint64_t *off = nullptr;                      // sets: [cap+1] offsets into tok
   uint32_t *tok = nullptr;                      // sets: tokens
   int64_t tok_cap = 0, tok_n = 0;               // token capacity / tokens in use (host mirror)
+  int32_t *lrows = nullptr;                     // partitioned: [cap][k] partition-local row entries (-1 across)
   uint32_t tok_max = 0;                         // largest stored token (valid when tok_n > 0)
   int32_t *ids = nullptr;
   uint32_t *keys = nullptr;

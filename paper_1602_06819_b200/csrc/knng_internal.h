@@ -34,6 +34,8 @@ struct SearchArgs {
   const int64_t *member_cnt;   // [P] (device)
   const uint8_t *part_of;      // [cap]
   const int32_t *local_idx;    // [cap]
+  const int32_t *lrows;        // [cap][k]: local index of each row entry in the row owner's partition, -1 if
+                               // the entry lies in another partition (P > 0)
   // parameters
   double speedup;
   uint64_t e_num, e_den, seed;
@@ -56,7 +58,9 @@ struct SearchArgs {
   int stages;                  // producer gather pipeline depth (2 or 4; sets: 4)
   int nprod;                   // producer warps per CTA (1..3)
   int lane_eval;               // producers evaluate one row per lane where the width allows
+  int ring;                    // ring chunks (16 or 32)
 };
+size_t search_smem_bytes(const SearchArgs &a, bool sets);
 
 struct BallArgs {
   StoreView st;
@@ -89,7 +93,11 @@ cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cud
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
                                int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted,
-                               cudaStream_t s, int *n_launch);
+                               cudaStream_t s, int *n_launch, int32_t *lrows = nullptr,
+                               const uint8_t *part_of = nullptr, const int32_t *local_idx = nullptr);
+// lrows of rows [first, first + count): partition-local index of each entry, -1 across partitions
+cudaError_t launch_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
+                         const int32_t *local_idx, int32_t *lrows, cudaStream_t s);
 cudaError_t exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t *tmp, int64_t n, cudaStream_t s);
 cudaError_t launch_exact_build(const VecGeom &g, const StoreView &st, int64_t n, int k, int32_t *ids,
                                uint32_t *keys, cudaStream_t s);

@@ -296,6 +296,9 @@ static int build_members(knng_graph *g, int32_t *flag, int32_t *scan, int32_t *t
     cnt[p] = (int64_t)last[0] + last[1];
   }
   CK(cudaMemcpyAsync(g->member_cnt, cnt.data(), sizeof(int64_t) * g->P, cudaMemcpyHostToDevice, g->stream));
+  // the rows' partition-local view, read by the partition-local walks of K1
+  if (!g->lrows) CK(cudaMalloc((void **)&g->lrows, (size_t)g->cap * g->k * 4));
+  CK(launch_lrows(g->ids, g->k, 0, n, g->part_of, g->local_idx, g->lrows, g->stream));
   CK(cudaStreamSynchronize(g->stream));
   return 0;
 }

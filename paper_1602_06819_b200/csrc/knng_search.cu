@@ -20,9 +20,8 @@
 
 namespace knng {
 
-constexpr int RING_CHUNKS = 32;   // smem ring of 32 x 32 evaluated draws per CTA (16 KB)
+constexpr int RING_MAX = 32;      // smem ring of a.ring (16 or 32) chunks x 32 evaluated draws per CTA
 constexpr int FASTC = 4;          // chunks the consumer's skip-only fast path commits at once
-constexpr int STAGES = 4;         // producer gather pipeline depth (chunks of 32 rows in flight)
 constexpr int HDR_BYTES = 128;
 
 struct RingHdr {
@@ -39,13 +38,14 @@ struct RingHdr {
 // Nothing here touches a counter, the visited sets or the top-k.
 //
 // The rows of the drawn nodes are gathered into shared memory with 16-byte cp.async copies
-// (no registers held by loads in flight), STAGES chunks deep; the keys are computed from shared
+// (no registers held by loads in flight), S chunks deep; the keys are computed from shared
 // memory.  Producer pw owns chunks pw, pw + nprod, ...; local iteration i <-> chunk pw + i*nprod.
 struct ProdCtx {
   volatile RingHdr *hdr;
-  unsigned long long *ring;   // [RING_CHUNKS][32][2]: (tag << 32 | node), (tag << 32 | key), tag = chunk + 1
-  uint8_t *stg;       // this producer's STAGES x 32 rows (pitch bytes each)
-  int32_t *meta;      // this producer's STAGES x 32 x 4 ints (node, rb, re, -)
+  unsigned long long *ring;   // [ring][32][2]: (tag << 32 | node), (tag << 32 | key), tag = chunk + 1
+  int ring_n;                 // ring chunks (power of 2)
+  uint8_t *stg;       // this producer's S x 32 rows (pitch bytes each)
+  int32_t *meta;      // this producer's S x 32 x 4 ints (node, rb, re, -)
   int pitch;
   int pw, nprod;
   int64_t nch;
@@ -68,14 +68,14 @@ __device__ __forceinline__ bool publish(const ProdCtx &x, int64_t i, int32_t nod
   const long long t0 = prof ? clock64() : 0;
   int dn = 0;
   if (lane == 0)
-    while (c - x.hdr->consumed >= RING_CHUNKS && !(dn = x.hdr->done)) __nanosleep(32);
+    while (c - x.hdr->consumed >= x.ring_n && !(dn = x.hdr->done)) __nanosleep(32);
   dn = __shfl_sync(FULL, dn, 0);
   if (prof) p_wait += clock64() - t0;
   if (dn) return false;
   // Each entry word carries its chunk's tag next to the datum: an aligned 64-bit shared store is
   // single-copy atomic, so the consumer sees a whole (tag, datum) pair and needs no fence or barrier.
   const unsigned long long tag = (unsigned long long)(unsigned)(c + 1) << 32;
-  volatile unsigned long long *e = x.ring + ((c % RING_CHUNKS) * 32 + lane) * 2;
+  volatile unsigned long long *e = x.ring + ((c & (x.ring_n - 1)) * 32 + lane) * 2;
   e[0] = tag | (uint32_t)node;
   e[1] = tag | key;
 #ifdef KNNG_DEBUG_WAIT
@@ -85,10 +85,10 @@ __device__ __forceinline__ bool publish(const ProdCtx &x, int64_t i, int32_t nod
 }
 
 // consumer: wait until chunk ch is in its slot and read this lane's (node, key)
-__device__ __forceinline__ void ring_get(const unsigned long long *ring, volatile RingHdr *hdr, int64_t ch,
+__device__ __forceinline__ void ring_get(const unsigned long long *ring, int ring_n, volatile RingHdr *hdr, int64_t ch,
                                          int32_t &node, uint32_t &key) {
   const unsigned tag = (unsigned)(ch + 1);
-  const volatile unsigned long long *e = ring + ((ch % RING_CHUNKS) * 32 + (threadIdx.x & 31)) * 2;
+  const volatile unsigned long long *e = ring + ((ch & (ring_n - 1)) * 32 + (threadIdx.x & 31)) * 2;
   unsigned long long w0, w1;
 #ifdef KNNG_DEBUG_WAIT
   long long n = 0;
@@ -266,8 +266,8 @@ __device__ __forceinline__ void produce_rows(const SearchArgs &a, const VecQuery
 
 // sets: lane j stages candidate j's token range (aligned 16-byte chunks, SLOTCH at most) in its own
 // slot; longer sets are evaluated from global memory.  Two prefetch levels: the node of chunk
-// i + STAGES and the offsets of chunk i + STAGES - 1 are loaded while chunk i is computed.
-template <int L>
+// i + S and the offsets of chunk i + S - 1 are loaded while chunk i is computed.
+template <int S, int L>
 __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<L> &Q, const ProdCtx &x) {
   constexpr int SLOTCH = SetQuery<L>::SLOTCH;
   const int lane = threadIdx.x & 31;
@@ -291,25 +291,25 @@ __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<
   int32_t n1 = 0;
   uint64_t b1 = 0, e1 = 0;
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < S - 1; ++s) {
     if (s < ni) {
       const int32_t nd = draw_node(x, s);
       issue(s, nd, off[nd], off[nd + 1]);
     }
     cp_async_commit();
   }
-  if (STAGES - 1 < ni) {
-    n1 = draw_node(x, STAGES - 1);
+  if (S - 1 < ni) {
+    n1 = draw_node(x, S - 1);
     b1 = off[n1];
     e1 = off[n1 + 1];
   }
-  int32_t n2 = STAGES < ni ? draw_node(x, STAGES) : 0;
+  int32_t n2 = S < ni ? draw_node(x, S) : 0;
   for (int64_t i = 0; i < ni; ++i) {
     const long long t0 = prof ? clock64() : 0;
     if (consumer_done(x)) break;
-    const int64_t ii = i + STAGES - 1;
+    const int64_t ii = i + S - 1;
     if (ii < ni) {
-      issue((int)(ii % STAGES), n1, b1, e1);
+      issue((int)(ii % S), n1, b1, e1);
       if (ii + 1 < ni) {
         n1 = n2;
         b1 = off[n1];
@@ -318,9 +318,9 @@ __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<
       }
     }
     cp_async_commit();
-    cp_async_wait<STAGES - 1>();
+    cp_async_wait<S - 1>();
     __syncwarp();
-    const int st = (int)(i % STAGES);
+    const int st = (int)(i % S);
     const int4 mt = *(const int4 *)(x.meta + (st * 32 + lane) * 4);
     uint32_t key;
     if (((mt.z + 3) >> 2) <= SLOTCH) {
@@ -357,7 +357,8 @@ __device__ __forceinline__ void produce_any(const SearchArgs &a, const VecQuery<
 template <int L>
 __device__ __forceinline__ void produce_any(const SearchArgs &a, const SetQuery<L> &Q, const ProdCtx &x, uint8_t *,
                                             int64_t) {
-  produce_set(a, Q, x);
+  if (a.stages <= 2) produce_set<2>(a, Q, x);
+  else produce_set<4>(a, Q, x);
 }
 
 // K1: one CTA per (query, partition) task: warp 0 runs the search in the paper's sequential
@@ -371,12 +372,16 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
   volatile RingHdr *hdr = (volatile RingHdr *)smem;
   unsigned long long *ring = (unsigned long long *)(smem + HDR_BYTES);
   const int S = a.stages;
-  uint8_t *stg = smem + HDR_BYTES + RING_CHUNKS * 32 * 16;                    // [nprod][S][32] rows
+  uint8_t *stg = smem + HDR_BYTES + a.ring * 32 * 16;                         // [nprod][S][32] rows
   int32_t *meta = (int32_t *)(stg + (size_t)nprod * S * 32 * a.pitch);        // [nprod][S][32][4]
   uint8_t *qprod = (uint8_t *)(meta + nprod * S * 32 * 4);                   // [nprod][512 B] query copies
   int32_t *rowbuf = (int32_t *)(qprod + nprod * 512);                         // [k][k]
   int32_t *rowbuf2 = rowbuf + k * k;                                          // [32][k]
-  uint32_t *qscr = (uint32_t *)(rowbuf2 + 32 * k);                            // [2][QMAX] (sets)
+  // partitioned: the same rows' partition-local indices (lrows, -1 = other partition)
+  const int lk = a.P > 0 ? k : 0;
+  int32_t *lrowbuf = rowbuf2 + 32 * k;                                        // [k][k] (P > 0)
+  int32_t *lrowbuf2 = lrowbuf + lk * k;                                       // [32][k] (P > 0)
+  uint32_t *qscr = (uint32_t *)(lrowbuf2 + 32 * lk);                          // [2][QMAX] (sets)
   uint32_t *vbm = qscr + (M == M_JAC ? 2 * QMAX : 0);                        // [vwords] (sets)
   const int vwords = M == M_JAC ? a.st.vwords : 0;
   uint32_t *sbits = vbm + vwords;
@@ -401,7 +406,7 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
     const int64_t words = (m + 31) >> 5;
     uint32_t *ev = bits, *ex = bits + words;
     for (int64_t w = threadIdx.x; w < 2 * words; w += blockDim.x) bits[w] = 0;
-    for (int w = threadIdx.x; w < RING_CHUNKS * 32; w += blockDim.x)   // no stale tags from the last task
+    for (int w = threadIdx.x; w < a.ring * 32; w += blockDim.x)   // no stale tags from the last task
       ((uint4 *)ring)[w] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) { hdr->consumed = 0; hdr->done = 0; }
     if (M == M_JAC && vwords > 0 && warp == 0)   // clear the previous query's vocabulary bits
@@ -446,6 +451,7 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
         ProdCtx x;
         x.hdr = hdr;
         x.ring = ring;
+        x.ring_n = a.ring;
         x.stg = stg + (size_t)(warp - 1) * S * 32 * a.pitch;
         x.meta = meta + (warp - 1) * S * 32 * 4;
         x.pitch = a.pitch;
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
           int32_t fnode[FASTC];
           uint32_t fkey[FASTC];
 #pragma unroll
-          for (int t = 0; t < FASTC; ++t) ring_get(ring, hdr, ch0 + t, fnode[t], fkey[t]);
+          for (int t = 0; t < FASTC; ++t) ring_get(ring, a.ring, hdr, ch0 + t, fnode[t], fkey[t]);
           if (a.prof) p_wait += clock64() - tw;
           if (!thr_ok || thr_key != top.key_at0) {
             thr.set(top.key_at0, a.e_num, a.e_den);
@@ -527,7 +533,7 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
         if (ch < nch && nprod > 0) {                 // produced ahead into the ring
           const long long tw = a.prof ? clock64() : 0;
           uint32_t kk;
-          ring_get(ring, hdr, ch, wnode, kk);
+          ring_get(ring, a.ring, hdr, ch, wnode, kk);
           wkey = kk;
           if (a.prof) p_wait += clock64() - tw;
           ++p_win;
@@ -559,7 +565,10 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
           if (__ballot_sync(FULL, wpf)) {
             cp_async_wait_all();      // older copies into rowbuf2 must land first
             if (wpf)
-              for (int e = 0; e < k; ++e) cp_async4(rowbuf2 + lane * k + e, a.rows + (size_t)wnode * k + e);
+              for (int e = 0; e < k; ++e) {
+                cp_async4(rowbuf2 + lane * k + e, a.rows + (size_t)wnode * k + e);
+                if (a.P > 0) cp_async4(lrowbuf2 + lane * k + e, a.lrows + (size_t)wnode * k + e);
+              }
           }
         }
       }
@@ -665,23 +674,31 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
       for (;;) {
         if (lane == 0) bit_set(ex, curl);
         ++s_exp;
-        int32_t v = -1;
+        int32_t v = -1, vl = -1;
         if (pf >= 0 || pf2 >= 0) {
           cp_async_wait_all();
           __syncwarp();
         }
-        if (lane < k)
+        if (lane < k) {
           v = pf >= 0 ? rowbuf[pf * k + lane] : (pf2 >= 0 ? rowbuf2[pf2 * k + lane] : a.rows[(size_t)cur * k + lane]);
+          if (a.P > 0)
+            vl = pf >= 0 ? lrowbuf[pf * k + lane]
+                         : (pf2 >= 0 ? lrowbuf2[pf2 * k + lane] : a.lrows[(size_t)cur * k + lane]);
+        }
         pf2 = -1;
-        const bool inpool = v >= 0 && (a.P == 0 || a.part_of[v] == p);   // Q10
-        const uint32_t lv = inpool ? (a.P > 0 ? (uint32_t)a.local_idx[v] : (uint32_t)v) : 0u;
+        // Q10: neighbours in another partition are skipped (lrows holds -1 for them)
+        const bool inpool = v >= 0 && (a.P == 0 || vl >= 0);
+        const uint32_t lv = inpool ? (a.P > 0 ? (uint32_t)vl : (uint32_t)v) : 0u;
         __syncwarp();
         // prefetch the rows of the in-pool neighbours: the next cur is one of them
         for (int base = 0; base < k * k; base += 32) {
           const int idx = base + lane;
           const int t = __float2int_rz(__fmul_rn(__int2float_rn(idx) + 0.5f, rk));   // idx / k
           const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t < 32 ? t : 31);
-          if (idx < k * k && vt >= 0) cp_async4(rowbuf + idx, a.rows + (size_t)vt * k + (idx - t * k));
+          if (idx < k * k && vt >= 0) {
+            cp_async4(rowbuf + idx, a.rows + (size_t)vt * k + (idx - t * k));
+            if (a.P > 0) cp_async4(lrowbuf + idx, a.lrows + (size_t)vt * k + (idx - t * k));
+          }
         }
         const bool evb2 = inpool ? bit_get(ev, lv) : true;
         const bool exb2 = inpool ? bit_get(ex, lv) : false;
@@ -757,6 +774,15 @@ __global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq,
   }
 }
 
+// dynamic shared memory of one K1 CTA (the kernel's carve-up above)
+size_t search_smem_bytes(const SearchArgs &a, bool sets) {
+  const int nprod = a.starts ? 0 : a.nprod;
+  size_t smem = HDR_BYTES + (size_t)a.ring * 32 * 16 + (size_t)nprod * (a.stages * 32 * (a.pitch + 16) + 512) +
+                (size_t)(a.k * a.k + 32 * a.k) * 4 * (a.P > 0 ? 2 : 1) + (sets ? 2 * QMAX * 4 + (size_t)a.st.vwords * 4 : 0);
+  if (a.smem_bits) smem += (size_t)a.bits_words * 4;
+  return smem;
+}
+
 template <int M, int L, int CPL>
 static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int Pn = a.part_cnt;
@@ -765,9 +791,7 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   // consumer + a.nprod producers (none when the starts are injected)
   const int nprod = a.starts ? 0 : a.nprod;
   const int warps = 1 + nprod;
-  size_t smem = HDR_BYTES + RING_CHUNKS * 32 * 16 + (size_t)nprod * (a.stages * 32 * (a.pitch + 16) + 512) +
-                (size_t)(a.k * a.k + 32 * a.k) * 4 + (M == M_JAC ? 2 * QMAX * 4 + (size_t)a.st.vwords * 4 : 0);
-  if (a.smem_bits) smem += (size_t)a.bits_words * 4;
+  const size_t smem = search_smem_bytes(a, M == M_JAC);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -271,7 +271,8 @@ __global__ void k_prop_scatter(const int2 *props, const int32_t *prop_cnt, int b
 
 template <int M>
 __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, int32_t *ncnt, int32_t *nfill,
-                             const int32_t *noff, const int2 *sorted) {
+                             const int32_t *noff, const int2 *sorted, int32_t *lrows, const uint8_t *part_of,
+                             const int32_t *local_idx) {
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n_t) return;
   const int c = ncnt[v];
@@ -295,6 +296,13 @@ __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, i
     ri[pos] = id;
   }
   for (int e = 0; e < k; ++e) { ids[v * k + e] = ri[e]; keys[v * k + e] = rk[e]; }
+  if (lrows) {   // partitioned: keep the row's partition-local view current (new ids are placed already)
+    const uint8_t pv = part_of[v];
+    for (int e = 0; e < k; ++e) {
+      const int32_t u = ri[e];
+      lrows[v * k + e] = (u >= 0 && part_of[u] == pv) ? local_idx[u] : -1;
+    }
+  }
   ncnt[v] = 0;
   nfill[v] = 0;
 }
@@ -302,7 +310,7 @@ __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, i
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
                                int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted, cudaStream_t s,
-                               int *n_launch) {
+                               int *n_launch, int32_t *lrows, const uint8_t *part_of, const int32_t *local_idx) {
   if (B == 0) return cudaSuccess;
   k_prop_count<<<(unsigned)B, 128, 0, s>>>(props, prop_cnt, ballmax, B, ncnt);
   const int64_t nb = (n_t + 1023) / 1024;
@@ -311,10 +319,31 @@ cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, 
   k_scan_add<<<(unsigned)nb, 1024, 0, s>>>(noff, scan_tmp, n_t);
   k_prop_scatter<<<(unsigned)B, 128, 0, s>>>(props, prop_cnt, ballmax, B, n_t, noff, nfill, sorted);
   const unsigned mb = (unsigned)((n_t + 255) / 256);
-  if (metric == M_U8) k_node_merge<M_U8><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted);
-  else if (metric == M_F32) k_node_merge<M_F32><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted);
-  else k_node_merge<M_JAC><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted);
+  if (metric == M_U8) k_node_merge<M_U8><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, lrows, part_of,
+                                                          local_idx);
+  else if (metric == M_F32) k_node_merge<M_F32><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, lrows, part_of,
+                                                          local_idx);
+  else k_node_merge<M_JAC><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, lrows, part_of,
+                                                          local_idx);
   if (n_launch) *n_launch += 6;
+  return cudaGetLastError();
+}
+
+__global__ void k_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
+                        const int32_t *local_idx, int32_t *lrows) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count * k) return;
+  const int64_t v = first + i / k;
+  const size_t o = (size_t)first * k + i;
+  const int32_t u = ids[o];
+  lrows[o] = (u >= 0 && part_of[u] == part_of[v]) ? local_idx[u] : -1;
+}
+
+cudaError_t launch_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
+                         const int32_t *local_idx, int32_t *lrows, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const int64_t n = count * k;
+  k_lrows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ids, k, first, count, part_of, local_idx, lrows);
   return cudaGetLastError();
 }
 

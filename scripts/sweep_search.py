@@ -1,7 +1,7 @@
 """Measurement helper: K1 (graph_search over one batch of stream points) under producer-shape
-knobs (KNNG_NPROD / KNNG_STAGES / KNNG_LANE_EVAL / KNNG_SMEM_BITS_KB), one graph per config.
+knobs (KNNG_NPROD / KNNG_STAGES / KNNG_LANE_EVAL / KNNG_RING / KNNG_SMEM_BITS), one graph per config.
 Every setting must return the same ids/keys (the knobs change the schedule, not the result).
-usage: python scripts/sweep_search.py C2 [--n0 N] [--reps R] [--settings "1,4,1,40 2,2,1,40"]"""
+usage: python scripts/sweep_search.py C2 [--n0 N] [--reps R] [--settings "plan RING=16 STAGES=4,NPROD=2"]"""
 import argparse
 import os
 import sys
@@ -20,7 +20,7 @@ def main():
     ap.add_argument("--n0", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--kmedoids-iters", type=int, default=2)
-    ap.add_argument("--settings", default="1,4,1,40 1,2,1,40 2,2,1,40 3,2,1,40 2,4,1,40 1,4,0,40 1,4,1,0 2,2,1,0")
+    ap.add_argument("--settings", default="plan RING=16 RING=32 SMEM_BITS=0 SMEM_BITS=1 STAGES=4 NPROD=2")
     args = ap.parse_args()
     import torch
     from paper_1602_06819_b200 import KnngGraph
@@ -37,9 +37,14 @@ def main():
     if cfg.metric != D.JAC:
         Q = torch.from_numpy(Q).cuda()
     ref = None
+    knobs = ("KNNG_NPROD", "KNNG_STAGES", "KNNG_LANE_EVAL", "KNNG_RING", "KNNG_SMEM_BITS")
     for s in args.settings.split():
-        npr, stg, lane, kb = s.split(",")
-        os.environ.update(KNNG_NPROD=npr, KNNG_STAGES=stg, KNNG_LANE_EVAL=lane, KNNG_SMEM_BITS_KB=kb)
+        for kn in knobs:
+            os.environ.pop(kn, None)
+        if s != "plan":
+            for kv in s.split(","):
+                kk, vv = kv.split("=")
+                os.environ["KNNG_" + kk] = vv
         ms = []
         for _ in range(args.reps):
             oi = torch.empty((cfg.batch, cfg.k), dtype=torch.int32, device="cuda")
@@ -55,8 +60,8 @@ def main():
         ev = st["search_evals"]
         V = {D.U8: cfg.dim, D.F32: 4 * cfg.dim, D.JAC: 118}[cfg.metric]
         gbs = (ev * (V + 4) + st["search_expansions"] * 4 * cfg.k) / (min(ms) / 1000) / 1e9
-        print("%-4s nprod=%s stages=%s lane=%s smem_bits_kb=%-3s  %8.2f ms (min of %d)  alg %.0f GB/s  same=%s" % (
-            args.config, npr, stg, lane, kb, min(ms), args.reps, gbs, same), flush=True)
+        print("%-4s %-22s %8.2f ms (min of %d)  alg %.0f GB/s  same=%s" % (
+            args.config, s, min(ms), args.reps, gbs, same), flush=True)
     g.close()
 
 
