@@ -311,31 +311,32 @@ static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
   a.nprod = 1;
   a.lane_eval = 1;
   a.stages = 2;
+  if (const char *e = getenv("KNNG_STAGES")) a.stages = atoi(e) <= 2 ? 2 : 4;
+  if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
   const int need = (int)std::min<int64_t>(8, (tasks + nsm - 1) / nsm);
   auto occ = [&](const SearchArgs &x) {
     const size_t sm = search_smem_bytes(x, sets) + 1024;
     return (int)std::min<size_t>(8, (228 * 1024) / sm);
   };
-  // preference order: smem bitmaps + 32-chunk ring, global bitmaps + 32, smem + 16, global + 16
-  const int cand[4][2] = {{1, 32}, {0, 32}, {1, 16}, {0, 16}};
+  // preference order: the evaluated bitmap in shared memory first (its test-and-set is on every
+  // draw), then the deeper ring
+  const int cand[6][2] = {{1, 32}, {1, 16}, {1, 8}, {0, 32}, {0, 16}, {0, 8}};
   int best = -1, best_occ = -1;
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 6; ++i) {
     SearchArgs x = a;
     x.smem_bits = cand[i][0];
     x.ring = cand[i][1];
-    if (x.smem_bits && (size_t)x.bits_words * 4 > 64 * 1024) continue;
+    if (x.smem_bits && (size_t)(x.bits_words / 2) * 4 > 96 * 1024) continue;
     const int o = occ(x);
     if (o >= need) { best = i; best_occ = o; break; }
     if (o > best_occ) { best = i; best_occ = o; }
   }
   a.smem_bits = cand[best][0];
   a.ring = cand[best][1];
-  if (const char *e = getenv("KNNG_STAGES")) a.stages = atoi(e) <= 2 ? 2 : 4;
-  if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
   if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
-  if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 16 ? 16 : 32;
+  if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 8 ? 8 : (atoi(e) <= 16 ? 16 : 32);
   if (const char *e = getenv("KNNG_SMEM_BITS")) a.smem_bits = atoi(e) != 0;
-  a.gslots = a.smem_bits ? 0 : std::min<int64_t>(tasks, (int64_t)nsm * 8);
+  a.gslots = std::min<int64_t>(tasks, (int64_t)nsm * 8);
 }
 
 static int64_t max_pool(knng_graph *g) {
@@ -389,7 +390,7 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.task_ctr = a.stats + 14;
   a.pitch = g->metric == KNNG_JACCARD_U32SET ? 16 * 16 + 16 : (int)g->geom.stride + 16;
   plan_k1(a, g->metric == KNNG_JACCARD_U32SET, nq * pc, mmax);
-  if (!a.smem_bits) CK(g->w_bits.ensure((size_t)a.gslots * a.bits_words * 4));
+  CK(g->w_bits.ensure((size_t)a.gslots * a.bits_words * 4));
   a.gbits = g->w_bits.as<uint32_t>();
   cudaError_t e = launch_search(g->geom, a, g->stream, nl);
   if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));

@@ -108,6 +108,40 @@ __device__ __forceinline__ void ring_get(const unsigned long long *ring, int rin
   key = (uint32_t)w1;
 }
 
+// Expanded set of the consumer warp (warp-uniform state): a shared open-addressing hash of
+// pool-local ids (+1; 0 = empty), filled to 3/4 at most; beyond that the global bitmap gex takes
+// the further entries (zeroed by the warp when first needed) and lookups consult both.
+constexpr int EXCAP = 512;
+__device__ __forceinline__ bool ex_has(const int32_t *exh, bool ovf, const uint32_t *gex, uint32_t lv) {
+  uint32_t h = (lv * 0x9E3779B1u) >> (32 - 9);
+  for (;;) {
+    const int32_t e = exh[h];
+    if (e == 0) break;
+    if (e == (int32_t)(lv + 1)) return true;
+    h = (h + 1) & (EXCAP - 1);
+  }
+  return ovf ? bit_get(gex, lv) : false;
+}
+__device__ __forceinline__ void ex_insert(int32_t *exh, int &cnt, bool &ovf, uint32_t *gex, int64_t words, uint32_t lv) {
+  const int lane = threadIdx.x & 31;
+  if (!ovf && cnt >= EXCAP * 3 / 4) {
+    for (int64_t w = lane; w < words; w += 32) gex[w] = 0;
+    __threadfence_block();
+    ovf = true;
+  }
+  if (ovf) {
+    if (lane == 0) bit_set(gex, lv);
+  } else {
+    if (lane == 0) {
+      uint32_t h = (lv * 0x9E3779B1u) >> (32 - 9);
+      while (exh[h] != 0 && exh[h] != (int32_t)(lv + 1)) h = (h + 1) & (EXCAP - 1);
+      exh[h] = (int32_t)(lv + 1);
+    }
+    ++cnt;
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ bool consumer_done(const ProdCtx &x) {
   int dn = (threadIdx.x & 31) == 0 ? x.hdr->done : 0;
   return __shfl_sync(FULL, dn, 0) != 0;
@@ -133,12 +167,18 @@ struct EvalLane {
   const uint8_t *qsm;   // the query's NCH chunks (shared)
   __device__ __forceinline__ uint32_t key(const uint8_t *sb, int pitch, int) const {
     const uint8_t *row = sb + (threadIdx.x & 31) * pitch;
-    if (M == M_U8) {
-      uint32_t acc = 0;
+    if (M == M_U8) {   // exact integer sum: four independent accumulators (short dependency chains)
+      uint32_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int c = 0; c < NCH; ++c)
-        chunk_acc<M_U8>(acc, *(const uint4 *)(qsm + 16 * c), *(const uint4 *)(row + 16 * c));
-      return acc;
+      for (int c = 0; c < NCH; ++c) {
+        const uint4 q = *(const uint4 *)(qsm + 16 * c), r = *(const uint4 *)(row + 16 * c);
+        uint32_t d;
+        d = __vabsdiffu4(q.x, r.x); acc[0] = __dp4a(d, d, acc[0]);
+        d = __vabsdiffu4(q.y, r.y); acc[1] = __dp4a(d, d, acc[1]);
+        d = __vabsdiffu4(q.z, r.z); acc[2] = __dp4a(d, d, acc[2]);
+        d = __vabsdiffu4(q.w, r.w); acc[3] = __dp4a(d, d, acc[3]);
+      }
+      return (acc[0] + acc[1]) + (acc[2] + acc[3]);
     } else {
       static_assert(NCH <= 32, "lane form: one chunk per partial");
       float p[32];
@@ -155,8 +195,10 @@ struct EvalLane {
 };
 
 // vectors: lane's copies within a stage are the 16-byte chunks e = lane + 32 j (j < nchunks) of the
-// 32 x nchunks stage, i.e. row e / nchunks, chunk e % nchunks (walked incrementally)
-template <int S, class EV>
+// 32 x nchunks stage, i.e. row e / nchunks, chunk e % nchunks (walked incrementally).
+// U chunks per iteration (their keys computed together for ILP) in two groups of U stages: group
+// g + 1's rows are in flight while group g is evaluated.
+template <int U, class EV>
 __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
   const int lane = threadIdx.x & 31;
   const int nck = EV::NCH > 0 ? EV::NCH : a.st.nchunks;
@@ -164,6 +206,7 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
   const size_t stride = a.st.stride;
   const int r0 = lane / nck, c0 = lane % nck, rs = 32 / nck, cs = 32 % nck;
   const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
+  const int64_t ng = (ni + U - 1) / U;
   const bool prof = a.prof != nullptr;
   long long p_wait = 0, p_work = 0;
   auto issue = [&](int st, int32_t node) {
@@ -179,48 +222,44 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
       if (cc >= nck) { cc -= nck; ++r; }
     }
   };
+  int32_t pn[U];
 #pragma unroll
-  for (int s = 0; s < S - 1; ++s) {
-    if (s < ni) issue(s, draw_node(x, s));
-    cp_async_commit();
-  }
-  int32_t pn = S - 1 < ni ? draw_node(x, S - 1) : 0;
-#ifdef KNNG_DEBUG_WAIT
-  if (lane == 0) { x.hdr->published = -1; x.hdr->pstate = 1000000 + (int)ni; }
-#endif
-  for (int64_t i = 0; i < ni; ++i) {
+  for (int u = 0; u < U; ++u)
+    if (u < ni) issue(u, draw_node(x, u));
+  cp_async_commit();
+#pragma unroll
+  for (int u = 0; u < U; ++u) pn[u] = U + u < ni ? draw_node(x, U + u) : 0;
+  for (int64_t g = 0; g < ng; ++g) {
     const long long t0 = prof ? clock64() : 0;
-#ifdef KNNG_DEBUG_WAIT
-    if (lane == 0) x.hdr->pstate = 1 + 10 * (int)i;
-#endif
     if (consumer_done(x)) break;
-    const int64_t ii = i + S - 1;
-    if (ii < ni) {
-      issue((int)(ii % S), pn);
-      if (ii + 1 < ni) pn = draw_node(x, ii + 1);   // (pool load) in flight during this compute
+    if (g + 1 < ng) {
+      const int h = (int)((g + 1) & 1) * U;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if ((g + 1) * U + u < ni) issue(h + u, pn[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)   // (pool loads) in flight during this group's evaluation
+        pn[u] = (g + 2) * U + u < ni ? draw_node(x, (g + 2) * U + u) : 0;
     }
     cp_async_commit();
-#ifdef KNNG_DEBUG_WAIT
-    if (lane == 0) x.hdr->pstate = 2 + 10 * (int)i;
-#endif
-    cp_async_wait<S - 1>();
+    cp_async_wait<1>();
     __syncwarp();
-#ifdef KNNG_DEBUG_WAIT
-    if (lane == 0) x.hdr->pstate = 3 + 10 * (int)i;
-#endif
-    const int st = (int)(i % S);
-    const uint32_t key = ev.key(x.stg + st * 32 * x.pitch, x.pitch, nck);
-    const int32_t node = x.meta[(st * 32 + lane) * 4];
+    const int h = (int)(g & 1) * U;
+    uint32_t key[U];
+    int32_t node[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      key[u] = ev.key(x.stg + (h + u) * 32 * x.pitch, x.pitch, nck);
+      node[u] = x.meta[((h + u) * 32 + lane) * 4];
+    }
     __syncwarp();
     if (prof) p_work += clock64() - t0;
-#ifdef KNNG_DEBUG_WAIT
-    if (lane == 0) x.hdr->pstate = 4 + 10 * (int)i;
-#endif
-    if (!publish(x, i, node, key, p_wait, prof)) break;
+    bool more = true;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (more && g * U + u < ni) more = publish(x, g * U + u, node[u], key[u], p_wait, prof);
+    if (!more) break;
   }
-#ifdef KNNG_DEBUG_WAIT
-  if (lane == 0) x.hdr->pstate = -x.hdr->pstate;
-#endif
   cp_async_wait<0>();
   __syncwarp();
   if (prof && lane == 0) {
@@ -231,8 +270,8 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
 
 template <class EV>
 __device__ __forceinline__ void produce_vec_s(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
-  if (a.stages <= 2) produce_vec<2>(a, ev, x);
-  else produce_vec<4>(a, ev, x);
+  if (a.stages <= 2) produce_vec<1>(a, ev, x);
+  else produce_vec<2>(a, ev, x);
 }
 
 // the producer's evaluator: lane form for the configured row widths, else the warp form
@@ -384,10 +423,12 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
   uint32_t *qscr = (uint32_t *)(lrowbuf2 + 32 * lk);                          // [2][QMAX] (sets)
   uint32_t *vbm = qscr + (M == M_JAC ? 2 * QMAX : 0);                        // [vwords] (sets)
   const int vwords = M == M_JAC ? a.st.vwords : 0;
-  uint32_t *sbits = vbm + vwords;
+  int32_t *exh = (int32_t *)(vbm + vwords);                                  // [EXCAP] expanded-set hash
+  uint32_t *sbits = (uint32_t *)(exh + EXCAP);                               // [bits_words / 2] (smem bits)
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
-  uint32_t *bits = a.smem_bits ? sbits : a.gbits + (int64_t)blockIdx.x * a.bits_words;
+  // per CTA slot in global memory: [evaluated words][expanded-overflow words]
+  uint32_t *gslot = a.gbits + (int64_t)blockIdx.x * a.bits_words;
   const float rk = 1.0f / (float)k;
   unsigned long long s_evals = 0, s_starts = 0, s_skip = 0, s_exp = 0;
   int prev_qn = 0;                              // sets: tokens of the previous query (scratch 0)
@@ -404,8 +445,12 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
     const int64_t m = a.P > 0 ? a.member_cnt[p] : a.n_t;
     const int32_t *pool = a.P > 0 ? a.members + (size_t)p * a.member_cap : nullptr;
     const int64_t words = (m + 31) >> 5;
-    uint32_t *ev = bits, *ex = bits + words;
-    for (int64_t w = threadIdx.x; w < 2 * words; w += blockDim.x) bits[w] = 0;
+    // evaluated set: bitmap over the pool (shared memory when it fits the plan, else L2/HBM);
+    // expanded set: shared hash, overflowing into a global bitmap (cleared when first used)
+    uint32_t *ev = a.smem_bits ? sbits : gslot;
+    uint32_t *gex = gslot + words;
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) ev[w] = 0;
+    for (int w = threadIdx.x; w < EXCAP; w += blockDim.x) exh[w] = 0;
     for (int w = threadIdx.x; w < a.ring * 32; w += blockDim.x)   // no stale tags from the last task
       ((uint4 *)ring)[w] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) { hdr->consumed = 0; hdr->done = 0; }
@@ -480,6 +525,8 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
 
     const long long tc0 = a.prof ? clock64() : 0;
     long long p_wait = 0, p_walk = 0, p_win = 0;
+    int ex_cnt = 0;
+    bool ex_ovf = false;
     while (c < budget) {
       // ------------------------------ restart ------------------------------
       if (wpos >= 32) {
@@ -672,7 +719,7 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
       if (!__shfl_sync(FULL, wpf, al)) pf2 = -1;
       bool stop = false;
       for (;;) {
-        if (lane == 0) bit_set(ex, curl);
+        ex_insert(exh, ex_cnt, ex_ovf, gex, words, curl);
         ++s_exp;
         int32_t v = -1, vl = -1;
         if (pf >= 0 || pf2 >= 0) {
@@ -701,7 +748,7 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
           }
         }
         const bool evb2 = inpool ? bit_get(ev, lv) : true;
-        const bool exb2 = inpool ? bit_get(ex, lv) : false;
+        const bool exb2 = inpool ? ex_has(exh, ex_ovf, gex, lv) : false;
         const uint32_t key = Q.eval(a.st, inpool ? v : -1, k);
         const bool imp = inpool && closer<M>(key, kcur);
         const unsigned im = __ballot_sync(FULL, imp);
@@ -778,8 +825,9 @@ __global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq,
 size_t search_smem_bytes(const SearchArgs &a, bool sets) {
   const int nprod = a.starts ? 0 : a.nprod;
   size_t smem = HDR_BYTES + (size_t)a.ring * 32 * 16 + (size_t)nprod * (a.stages * 32 * (a.pitch + 16) + 512) +
-                (size_t)(a.k * a.k + 32 * a.k) * 4 * (a.P > 0 ? 2 : 1) + (sets ? 2 * QMAX * 4 + (size_t)a.st.vwords * 4 : 0);
-  if (a.smem_bits) smem += (size_t)a.bits_words * 4;
+                (size_t)(a.k * a.k + 32 * a.k) * 4 * (a.P > 0 ? 2 : 1) + (sets ? 2 * QMAX * 4 + (size_t)a.st.vwords * 4 : 0) +
+                EXCAP * 4;
+  if (a.smem_bits) smem += (size_t)(a.bits_words / 2) * 4;   // the evaluated bitmap
   return smem;
 }
 
@@ -805,7 +853,7 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   int64_t blocks = T < (int64_t)per_sm * nsm ? T : (int64_t)per_sm * nsm;
-  if (!a.smem_bits && blocks > a.gslots) blocks = a.gslots;
+  if (blocks > a.gslots) blocks = a.gslots;
   cudaError_t me = cudaMemsetAsync(a.task_ctr, 0, sizeof(unsigned long long), s);
   if (me != cudaSuccess) return me;
   if (getenv("KNNG_PROFILE"))

@@ -1,7 +1,7 @@
 """Measurement helper: K1 (graph_search over one batch of stream points) under producer-shape
 knobs (KNNG_NPROD / KNNG_STAGES / KNNG_LANE_EVAL / KNNG_RING / KNNG_SMEM_BITS), one graph per config.
 Every setting must return the same ids/keys (the knobs change the schedule, not the result).
-usage: python scripts/sweep_search.py C2 [--n0 N] [--reps R] [--settings "plan RING=16 STAGES=4,NPROD=2"]"""
+usage: python scripts/sweep_search.py C2 [--n0 N] [--reps R] [--settings "plan/RING=16/STAGES=4,NPROD=2"] (settings separated by /)"""
 import argparse
 import os
 import sys
@@ -20,7 +20,7 @@ def main():
     ap.add_argument("--n0", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--kmedoids-iters", type=int, default=2)
-    ap.add_argument("--settings", default="plan RING=16 RING=32 SMEM_BITS=0 SMEM_BITS=1 STAGES=4 NPROD=2")
+    ap.add_argument("--settings", default="plan/RING=16/RING=32/SMEM_BITS=0/SMEM_BITS=1/STAGES=4/NPROD=2")
     args = ap.parse_args()
     import torch
     from paper_1602_06819_b200 import KnngGraph
@@ -38,7 +38,7 @@ def main():
         Q = torch.from_numpy(Q).cuda()
     ref = None
     knobs = ("KNNG_NPROD", "KNNG_STAGES", "KNNG_LANE_EVAL", "KNNG_RING", "KNNG_SMEM_BITS")
-    for s in args.settings.split():
+    for s in args.settings.split("/"):
         for kn in knobs:
             os.environ.pop(kn, None)
         if s != "plan":
