@@ -5,6 +5,8 @@
 // streams the whole store through shared memory in tiles of 64 vectors and evaluates every
 // (row, column) pair with the single-thread canonical distance (so the keys are bit-identical
 // to the search path's warp evaluator).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "knng_common.cuh"
@@ -116,6 +118,26 @@ cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0,
                              int64_t ncols, int k, const int32_t *seed_ids, const uint32_t *seed_keys, int32_t *out_ids,
                              uint32_t *out_keys, cudaStream_t s) {
   if (nrows <= 0) return cudaSuccess;
+  // u8 rows: the tcgen05 kind::i8 form (knng_tc.cu); two column halves per split, merged below
+  const char *tce = getenv("KNNG_TC");
+  if (g.metric == M_U8 && g.nchunks <= 16 && k <= 32 && !(tce && atoi(tce) == 0)) {
+    const int64_t bx = (nrows + 127) / 128;
+    int64_t ny = bx >= 148 ? 1 : std::min<int64_t>((148 + bx - 1) / bx, std::max<int64_t>(1, (ncols + 255) / 256));
+    const size_t need = (size_t)2 * ny * nrows * k * 8;
+    if (need > g_part_bytes) {
+      if (g_part_buf) cudaFree(g_part_buf);
+      cudaError_t e = cudaMalloc(&g_part_buf, need);
+      if (e != cudaSuccess) { g_part_buf = nullptr; g_part_bytes = 0; return e; }
+      g_part_bytes = need;
+    }
+    int32_t *pi = (int32_t *)g_part_buf;
+    uint32_t *pk = (uint32_t *)((char *)g_part_buf + (size_t)2 * ny * nrows * k * 4);
+    cudaError_t e = launch_tc_topk_u8(g, vec, row0, nrows, col0, ncols, k, ny, pi, pk, s);
+    if (e != cudaSuccess) return e;
+    k_merge_partials<M_U8><<<(unsigned)((nrows + 3) / 4), 128, 0, s>>>(nrows, k, (int)(2 * ny), seed_ids, seed_keys,
+                                                                        pi, pk, out_ids, out_keys);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)128 * (g.nchunks + 1) * 16;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   const int64_t bx = (nrows + 63) / 64;
