@@ -270,13 +270,30 @@ def run_ours(args, cfg):
     peak, peak_src = hbm_peak()
     achieved = bytes_search / (ms_search / 1000.0) / 1e9
     launches = sum(s["kernel_launches"] for s in stats)
-    traffic = None       # DRAM bytes per launch of k_search from the committed ncu --set full capture
+    # DRAM bytes per launch of k_search from the committed ncu --set full capture of this exact
+    # workload (profiles/k_search_ncu_<config>[_n<n0>].json), else null
+    traffic = None
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "k_search_ncu.json")))
-        if prof.get("config", "C1") == cfg.name and not args.n0:
-            traffic = prof["dram_bytes_per_launch"]
+        tag = cfg.name + ("_n%d" % cfg.n0 if args.n0 else "")
+        prof = json.load(open(os.path.join(ROOT, "profiles", "k_search_ncu_%s.json" % tag)))
+        traffic = prof["dram_bytes_per_launch"]
     except Exception:
         pass
+    # the dense step (A5 all-pairs, K3): tcgen05 kind::i8 for u8, SIMT otherwise; 2 * B^2 * d ops
+    ms_ap = sum(s["ms_allpairs"] for s in stats) / len(stats)
+    dense = None
+    if cfg.metric != D.JAC and ms_ap > 0:
+        ops = 2.0 * GB * GB * cfg.dim
+        try:
+            bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        except Exception:
+            bf16 = 1652.5
+        dpeak = 2 * bf16 if cfg.metric == D.U8 else bf16 / 2     # int8 = 2x bf16 (dense), tf32 = 1/2 bf16
+        dense = {"kernel": "k_tc_topk_u8 (tcgen05 kind::i8) + partial merge" if cfg.metric == D.U8 else
+                 "k_tile_topk (SIMT fp32, canonical order)", "achieved": ops / (ms_ap / 1000) / 1e12,
+                 "peak": dpeak, "unit": "TOP/s", "frac": ops / (ms_ap / 1000) / 1e12 / dpeak,
+                 "peak_source": "MEASURED_PEAKS.json bf16_tflops x nominal dtype ratio",
+                 "note": "B x B exact all-pairs of the batch with top-k epilogue; tiny per step, latency-bound"}
 
     # recall@k of the inserted points' rows vs the exact k-nn over the final point set (sampled, torch)
     rec = None
@@ -337,6 +354,7 @@ def run_ours(args, cfg):
                      "ms_per_launch": ms_search / len(stats),
                      "note": ("store + rows fit in L2 (126 MB): the HBM fraction is not the binding claim"
                               if cap * (V + 8 * cfg.k) < 100e6 else "HBM-resident store")},
+        "roofline_dense": dense,
         "phase_ms": {p: sum(s[p] for s in stats) / len(stats) for p in ("ms_search", "ms_allpairs",
                                                                        "ms_update", "ms_merge")},
         "e2e": {"value": args.steps * GB / t_e2e, "unit": "inserts/s", "h2d_bytes_per_step": GB * V,

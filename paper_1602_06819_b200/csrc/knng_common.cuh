@@ -167,6 +167,12 @@ struct WarpTopK {
   uint32_t key_at0;   // warp-uniform copy of the best key (valid when cnt > 0)
   __device__ __forceinline__ void init(int kr_) { key = 0; id = -1; cnt = 0; kr = kr_; key_at0 = 0; }
   __device__ __forceinline__ uint32_t best() const { return __shfl_sync(FULL, key, 0); }
+  // may an entry with key ck enter (some id)?  Lane-local view of the warp-uniform worst key: the
+  // worst entry's key is read by a shuffle, so every lane must call this together.
+  __device__ __forceinline__ bool could_take(uint32_t ck) const {
+    const uint32_t wk = __shfl_sync(FULL, key, (kr - 1) & 31);
+    return cnt < kr || !closer<M>(wk, ck);
+  }
   // insert every lane with flag set (distinct ids assumed)
   __device__ __forceinline__ void insert(bool flag, uint32_t ck, int32_t cid) {
     const int lane = threadIdx.x & 31;

@@ -54,10 +54,13 @@ struct ProdCtx {
   const int32_t *pool;
 };
 
-__device__ __forceinline__ int32_t draw_node(const ProdCtx &x, int64_t i) {
+// draw i of this lane: (node id, pool index).  The pool index is the node's partition-local index
+// (members_p is ascending in local index), which is what the ring carries: the consumer's visited
+// bitmap needs it, and the node id only when the draw may enter the top-k or start a walk.
+__device__ __forceinline__ int2 draw_node(const ProdCtx &x, int64_t i) {
   const int64_t c = x.pw + i * x.nprod;
   const uint64_t idx = rng_index(x.h3, (uint64_t)(c * 32 + (threadIdx.x & 31)), (uint64_t)x.m);
-  return x.pool ? x.pool[idx] : (int32_t)idx;
+  return make_int2(x.pool ? x.pool[idx] : (int32_t)idx, (int32_t)idx);
 }
 
 // publish chunk (local iteration i) to the ring; false when the consumer has finished
@@ -209,26 +212,26 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
   const int64_t ng = (ni + U - 1) / U;
   const bool prof = a.prof != nullptr;
   long long p_wait = 0, p_work = 0;
-  auto issue = [&](int st, int32_t node) {
-    x.meta[(st * 32 + lane) * 4] = node;
+  auto issue = [&](int st, int2 d) {
+    x.meta[(st * 32 + lane) * 4] = d.y;   // published: the pool index
     uint8_t *dst = x.stg + st * 32 * x.pitch;
     int r = r0, cc = c0;
 #pragma unroll 8
     for (int j = 0; j < nck; ++j) {
-      const int32_t id = __shfl_sync(FULL, node, r);
+      const int32_t id = __shfl_sync(FULL, d.x, r);
       cp_async16(dst + r * x.pitch + cc * 16, base + (size_t)id * stride + (size_t)cc * 16);
       cc += cs;
       r += rs;
       if (cc >= nck) { cc -= nck; ++r; }
     }
   };
-  int32_t pn[U];
+  int2 pn[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (u < ni) issue(u, draw_node(x, u));
   cp_async_commit();
 #pragma unroll
-  for (int u = 0; u < U; ++u) pn[u] = U + u < ni ? draw_node(x, U + u) : 0;
+  for (int u = 0; u < U; ++u) pn[u] = U + u < ni ? draw_node(x, U + u) : make_int2(0, 0);
   for (int64_t g = 0; g < ng; ++g) {
     const long long t0 = prof ? clock64() : 0;
     if (consumer_done(x)) break;
@@ -239,7 +242,7 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
         if ((g + 1) * U + u < ni) issue(h + u, pn[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u)   // (pool loads) in flight during this group's evaluation
-        pn[u] = (g + 2) * U + u < ni ? draw_node(x, (g + 2) * U + u) : 0;
+        pn[u] = (g + 2) * U + u < ni ? draw_node(x, (g + 2) * U + u) : make_int2(0, 0);
     }
     cp_async_commit();
     cp_async_wait<1>();
@@ -315,11 +318,11 @@ __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<
   const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
   const bool prof = a.prof != nullptr;
   long long p_wait = 0, p_work = 0;
-  auto issue = [&](int st, int32_t node, uint64_t b, uint64_t e) {
+  auto issue = [&](int st, int2 d, uint64_t b, uint64_t e) {
     const uint64_t a0 = b & ~3ull;
     const int rb = (int)(b - a0), re = (int)(e - a0);
     int4 *mt = (int4 *)(x.meta + (st * 32 + lane) * 4);
-    *mt = make_int4(node, rb, re, 0);
+    *mt = make_int4(d.x, rb, re, d.y);
     const int nch = (re + 3) >> 2;
     if (nch <= SLOTCH) {
       uint8_t *dst = x.stg + (st * 32 + lane) * x.pitch;
@@ -327,22 +330,22 @@ __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<
     }
   };
   // prologue
-  int32_t n1 = 0;
+  int2 n1 = make_int2(0, 0);
   uint64_t b1 = 0, e1 = 0;
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) {
     if (s < ni) {
-      const int32_t nd = draw_node(x, s);
-      issue(s, nd, off[nd], off[nd + 1]);
+      const int2 nd = draw_node(x, s);
+      issue(s, nd, off[nd.x], off[nd.x + 1]);
     }
     cp_async_commit();
   }
   if (S - 1 < ni) {
     n1 = draw_node(x, S - 1);
-    b1 = off[n1];
-    e1 = off[n1 + 1];
+    b1 = off[n1.x];
+    e1 = off[n1.x + 1];
   }
-  int32_t n2 = S < ni ? draw_node(x, S) : 0;
+  int2 n2 = S < ni ? draw_node(x, S) : make_int2(0, 0);
   for (int64_t i = 0; i < ni; ++i) {
     const long long t0 = prof ? clock64() : 0;
     if (consumer_done(x)) break;
@@ -351,8 +354,8 @@ __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<
       issue((int)(ii % S), n1, b1, e1);
       if (ii + 1 < ni) {
         n1 = n2;
-        b1 = off[n1];
-        e1 = off[n1 + 1];
+        b1 = off[n1.x];
+        e1 = off[n1.x + 1];
         if (ii + 2 < ni) n2 = draw_node(x, ii + 2);
       }
     }
@@ -370,7 +373,7 @@ __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<
     }
     __syncwarp();
     if (prof) p_work += clock64() - t0;
-    if (!publish(x, i, mt.x, key, p_wait, prof)) break;
+    if (!publish(x, i, mt.w, key, p_wait, prof)) break;
   }
   cp_async_wait<0>();
   __syncwarp();
@@ -517,6 +520,7 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
     int64_t c = 0, jbase = 0;
     int32_t wnode = -1;
     uint32_t wkey = 0, wl = 0;
+    bool wvalid = false;
     bool whave = false, wpf = false;
     SkipThr<M> thr;              // skip rule prepared against the current best key
     uint32_t thr_key = 0;
@@ -554,7 +558,7 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
             bool fr[FASTC];
 #pragma unroll
             for (int t = 0; t < FASTC; ++t) {
-              const uint32_t li = a.P > 0 ? (uint32_t)a.local_idx[fnode[t]] : (uint32_t)fnode[t];
+              const uint32_t li = (uint32_t)fnode[t];   // the ring carries the pool index
               const uint32_t bit = 1u << (li & 31);
               fr[t] = !(atomicOr(ev + (li >> 5), bit) & bit);
             }
@@ -562,7 +566,10 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
             int nf = 0;
 #pragma unroll
             for (int t = 0; t < FASTC; ++t) {
-              top.insert(fr[t], fkey[t], fnode[t]);     // Q5: skipped starts enter the top-k
+              int32_t nd = fnode[t];
+              const bool ct = top.could_take(fkey[t]);  // (warp-wide)
+              if (pool && fr[t] && ct) nd = pool[nd];   // node id only when it may enter the top-k
+              top.insert(fr[t], fkey[t], nd);           // Q5: skipped starts enter the top-k
               nf += __popc(__ballot_sync(FULL, fr[t]));
             }
             c += nf;
@@ -580,8 +587,12 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
         if (ch < nch && nprod > 0) {                 // produced ahead into the ring
           const long long tw = a.prof ? clock64() : 0;
           uint32_t kk;
-          ring_get(ring, a.ring, hdr, ch, wnode, kk);
+          int32_t pidx;
+          ring_get(ring, a.ring, hdr, ch, pidx, kk);
           wkey = kk;
+          wl = (uint32_t)pidx;
+          wnode = pool ? -2 : pidx;                   // -2: valid, node id not looked up yet
+          wvalid = true;
           if (a.prof) p_wait += clock64() - tw;
           ++p_win;
           whave = true;
@@ -590,25 +601,28 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
         } else {
           if (a.starts) {
             wnode = j < a.nstarts ? a.starts[j] : -1;
+            wl = wnode >= 0 ? (a.P > 0 ? (uint32_t)a.local_idx[wnode] : (uint32_t)wnode) : 0u;
           } else {
             const uint64_t idx = rng_index(h3, (uint64_t)j, (uint64_t)m);
             wnode = pool ? pool[idx] : (int32_t)idx;
+            wl = (uint32_t)idx;
           }
+          wvalid = wnode >= 0;
           whave = false;
         }
-        wl = wnode >= 0 ? (a.P > 0 ? (uint32_t)a.local_idx[wnode] : (uint32_t)wnode) : 0u;
         jbase += 32;
         wpos = 0;
         // prefetch the rows of the draws that could still be accepted: the skip threshold only
         // tightens as s_max improves, so "passes against the current best" is a superset
         wpf = false;
-        if (whave && wnode >= 0) {
+        if (whave && wvalid) {
           if (top.cnt > 0 && (!thr_ok || thr_key != top.key_at0)) {
             thr.set(top.key_at0, a.e_num, a.e_den);
             thr_key = top.key_at0;
             thr_ok = true;
           }
           wpf = top.cnt == 0 ? lane == 0 : !thr.skip(wkey);
+          if (wpf && wnode == -2) wnode = pool[wl];
           if (__ballot_sync(FULL, wpf)) {
             cp_async_wait_all();      // older copies into rowbuf2 must land first
             if (wpf)
@@ -620,9 +634,9 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
         }
       }
       const unsigned active = FULL << wpos;
-      const unsigned invm = __ballot_sync(FULL, wnode < 0) & active;
+      const unsigned invm = __ballot_sync(FULL, !wvalid) & active;
       const unsigned lim = invm ? ((1u << (__ffs(invm) - 1)) - 1u) : FULL;
-      const bool evb = wnode >= 0 ? bit_get(ev, wl) : true;
+      const bool evb = wvalid ? bit_get(ev, wl) : true;
       // Redraws of evaluated nodes are free (Q4).  A node drawn twice inside the window looks fresh
       // in both lanes: the later lane can never be accepted when the earlier one is skipped (same key,
       // tighter s_max), and the commit's atomicOr lets only the first evaluation count.
@@ -693,6 +707,9 @@ __global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
         const uint32_t bit = 1u << (wl & 31);
         newly = !(atomicOr(ev + (wl >> 5), bit) & bit);
       }
+      const bool ct = top.could_take(wkey);   // (warp-wide)
+      if (newly && wnode == -2 && ct) wnode = pool[wl];
+      if (am && lane == __ffs(am) - 1 && wnode == -2) wnode = pool[wl];   // the accepted start
       top.insert(newly, wkey, wnode);        // Q5: skipped starts enter the top-k too
       const int ncm = __popc(__ballot_sync(FULL, newly));
       c += ncm;

@@ -86,6 +86,14 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// one TMEM column of this thread's lane
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return v;
+}
+
 }  // namespace tc
 
 __global__ void k_norms_u8(const uint8_t *vec, size_t stride, int nchunks, int64_t row0, int64_t n, uint32_t *norms) {
@@ -215,37 +223,43 @@ __global__ void __launch_bounds__(256, 1)
     for (int q = 0; q < TN / 128; ++q) {
       uint32_t v[64];
       tmem_ld64(taddr + q * 64, v);
-      int kp[64];
-      bool any = false;
+      // screen: bit e of pm set when column e may enter the row's top-KM
       const int thr = wk[KM - 1] == 0xFFFFFFFFu ? 0x7FFFFFFF : (int)(wk[KM - 1] - ni);
+      uint32_t pm0 = 0, pm1 = 0;
 #pragma unroll
       for (int e4 = 0; e4 < 16; ++e4) {
         const int4 n4 = *(const int4 *)(nc + q * 64 + 4 * e4);
-        kp[4 * e4 + 0] = n4.x - 2 * (int)v[4 * e4 + 0];
-        kp[4 * e4 + 1] = n4.y - 2 * (int)v[4 * e4 + 1];
-        kp[4 * e4 + 2] = n4.z - 2 * (int)v[4 * e4 + 2];
-        kp[4 * e4 + 3] = n4.w - 2 * (int)v[4 * e4 + 3];
-        any |= (kp[4 * e4 + 0] < thr) | (kp[4 * e4 + 1] < thr) | (kp[4 * e4 + 2] < thr) | (kp[4 * e4 + 3] < thr);
+        const uint32_t b = ((n4.x - 2 * (int)v[4 * e4 + 0]) < thr ? 1u : 0u) |
+                           ((n4.y - 2 * (int)v[4 * e4 + 1]) < thr ? 2u : 0u) |
+                           ((n4.z - 2 * (int)v[4 * e4 + 2]) < thr ? 4u : 0u) |
+                           ((n4.w - 2 * (int)v[4 * e4 + 3]) < thr ? 8u : 0u);
+        if (e4 < 8) pm0 |= b << (4 * e4);
+        else pm1 |= b << (4 * (e4 - 8));
       }
-      if (any && myrow < nrows) {
+      if (myrow >= nrows) pm0 = pm1 = 0;
+      // insert the survivors: warp-uniform walk over the columns any lane kept; each step re-reads
+      // that column from TMEM (a warp-collective load) and inserts it in the lanes that kept it
+      uint32_t w0 = __reduce_or_sync(FULL, pm0), w1 = __reduce_or_sync(FULL, pm1);
+      while (w0 | w1) {
+        int e;
+        if (w0) { e = __ffs(w0) - 1; w0 &= w0 - 1; }
+        else { e = 32 + __ffs(w1) - 1; w1 &= w1 - 1; }
+        const uint32_t ve = tmem_ld1(taddr + q * 64 + e);
+        const bool mine = ((e < 32 ? pm0 >> e : pm1 >> (e - 32)) & 1u) != 0;
+        const int c = q * 64 + e;
+        const uint32_t key = (uint32_t)(nc[c] - 2 * (int)ve) + ni;
+        const bool ins = mine && key < wk[KM - 1] && c != selfc;
+        uint32_t ck = ins ? key : 0xFFFFFFFFu;
+        int32_t ci = ins ? (int32_t)(col0 + cbase + c) : 0x7FFFFFFF;
 #pragma unroll
-        for (int e = 0; e < 64; ++e) {
-          const int c = q * 64 + e;
-          const uint32_t key = (uint32_t)kp[e] + ni;
-          if (key < wk[KM - 1] && c != selfc) {
-            uint32_t ck = key;
-            int32_t ci = (int32_t)(col0 + cbase + c);
-#pragma unroll
-            for (int s2 = 0; s2 < KM; ++s2) {   // insertion by edge order (key, id)
-              const bool sw = ck < wk[s2] || (ck == wk[s2] && ci < wi[s2]);
-              const uint32_t tk = wk[s2];
-              const int32_t ti = wi[s2];
-              wk[s2] = sw ? ck : tk;
-              wi[s2] = sw ? ci : ti;
-              ck = sw ? tk : ck;
-              ci = sw ? ti : ci;
-            }
-          }
+        for (int s2 = 0; s2 < KM; ++s2) {   // insertion by edge order (key, id); a no-op when !ins
+          const bool sw = ck < wk[s2] || (ck == wk[s2] && ci < wi[s2]);
+          const uint32_t tk = wk[s2];
+          const int32_t ti = wi[s2];
+          wk[s2] = sw ? ck : tk;
+          wi[s2] = sw ? ci : ti;
+          ck = sw ? tk : ck;
+          ci = sw ? ti : ci;
         }
       }
     }

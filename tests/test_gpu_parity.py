@@ -70,6 +70,20 @@ def test_graph_init_ragged_dims_and_ties(metric, dim):
     _assert_rows_equal(metric, gi, gk, o.ids[:n], o.keys[:n], "init d=%d" % dim)
 
 
+@pytest.mark.parametrize("n,dim,k", [(129, 32, 1), (700, 128, 10), (555, 40, 16), (1300, 200, 32), (300, 256, 7),
+                                     (2049, 8, 10)])
+def test_graph_init_tcgen05_vs_oracle(n, dim, k):
+    """u8 rows go through the tcgen05 kind::i8 kernel (d <= 256): ragged row/column tiles, odd chunk
+    counts (padded K), top-k sizes 1..32 (KM = 10 / 16 / 32 instances), heavy ties."""
+    rng = np.random.default_rng(n + dim)
+    X = rng.integers(0, 6 if dim > 64 else 3, size=(n, dim)).astype(np.uint8)
+    g = _graph(X, k)
+    o = O.OracleGraph(O.U8, X, k)
+    o.init_exact()
+    gi, gk = g.rows()
+    _assert_rows_equal(O.U8, gi, gk, o.ids[:n], o.keys[:n], "tc init n=%d d=%d k=%d" % (n, dim, k))
+
+
 def test_graph_init_errors():
     from paper_1602_06819_b200 import KnngGraph, KnngError
     with pytest.raises(KnngError) as e:
