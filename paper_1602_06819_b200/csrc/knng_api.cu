@@ -313,10 +313,13 @@ static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
   a.stages = 2;
   if (const char *e = getenv("KNNG_STAGES")) a.stages = atoi(e) <= 2 ? 2 : 4;
   if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
-  const int need = (int)std::min<int64_t>(8, (tasks + nsm - 1) / nsm);
+  a.lean = 0;
+  if (const char *e = getenv("KNNG_LEAN")) a.lean = atoi(e) != 0;
+  const int cap = a.lean ? 12 : 8;                 // two-warp CTAs per SM the registers allow
+  const int need = (int)std::min<int64_t>(cap, (tasks + nsm - 1) / nsm);
   auto occ = [&](const SearchArgs &x) {
     const size_t sm = search_smem_bytes(x, sets) + 1024;
-    return (int)std::min<size_t>(8, (228 * 1024) / sm);
+    return (int)std::min<size_t>(cap, (228 * 1024) / sm);
   };
   // preference order: the evaluated bitmap in shared memory first (its test-and-set is on every
   // draw), then the deeper ring
@@ -336,7 +339,7 @@ static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
   if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
   if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 8 ? 8 : (atoi(e) <= 16 ? 16 : 32);
   if (const char *e = getenv("KNNG_SMEM_BITS")) a.smem_bits = atoi(e) != 0;
-  a.gslots = std::min<int64_t>(tasks, (int64_t)nsm * 8);
+  a.gslots = std::min<int64_t>(tasks, (int64_t)nsm * cap);
 }
 
 static int64_t max_pool(knng_graph *g) {

@@ -58,7 +58,8 @@ struct SearchArgs {
   int stages;                  // producer gather pipeline depth (2 or 4; sets: 4)
   int nprod;                   // producer warps per CTA (1..3)
   int lane_eval;               // producers evaluate one row per lane where the width allows
-  int ring;                    // ring chunks (16 or 32)
+  int ring;                    // ring chunks (8, 16 or 32)
+  int lean;                    // 1: the 80-register variant (12 two-warp CTAs per SM) where instantiated
 };
 size_t search_smem_bytes(const SearchArgs &a, bool sets);
 

@@ -405,8 +405,11 @@ __device__ __forceinline__ void produce_any(const SearchArgs &a, const SetQuery<
 
 // K1: one CTA per (query, partition) task: warp 0 runs the search in the paper's sequential
 // order, warps 1.. produce its random-start keys ahead of it.
-template <int M, int L, int CPL>
-__global__ void __launch_bounds__(128, 4) k_search(SearchArgs a) {
+// MB: launch-bound variant.  MB = 4 lets a CTA of up to 4 warps keep 128 registers per thread (8
+// two-warp CTAs per SM); MB = 12 caps a two-warp CTA at 80 registers (12 per SM, some spills) for
+// latency-bound task mixes that want more concurrent walks.
+template <int M, int L, int CPL, int MB>
+__global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nprod = (blockDim.x >> 5) - 1;
@@ -848,7 +851,7 @@ size_t search_smem_bytes(const SearchArgs &a, bool sets) {
   return smem;
 }
 
-template <int M, int L, int CPL>
+template <int M, int L, int CPL, int MB>
 static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
@@ -858,12 +861,12 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int warps = 1 + nprod;
   const size_t smem = search_smem_bytes(a, M == M_JAC);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   // persistent grid: the CTAs that fit at once (dynamic task scheduling balances the tail)
   int per_sm = 0;
-  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL>, warps * 32, smem);
+  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL, MB>, warps * 32, smem);
   if (oe != cudaSuccess) return oe;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int dev = 0, nsm = 148;
@@ -876,7 +879,7 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   if (getenv("KNNG_PROFILE"))
     fprintf(stderr, "KNNG_PROFILE k_search: %lld CTAs, %d per SM resident (%zu B smem each)\n", (long long)blocks,
             per_sm, smem);
-  k_search<M, L, CPL><<<(unsigned)blocks, warps * 32, smem, s>>>(a);
+  k_search<M, L, CPL, MB><<<(unsigned)blocks, warps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -887,10 +890,15 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   X(M_F32, 1, 1) X(M_F32, 1, 2) X(M_F32, 1, 3) X(M_F32, 1, 4) X(M_F32, 2, 3) X(M_F32, 2, 4) X(M_F32, 4, 3) \
   X(M_F32, 4, 4) X(M_F32, 8, 3) X(M_F32, 8, 4) X(M_F32, 32, 2) X(M_F32, 32, 4)
 
+// the lean (12 CTAs/SM) variant is instantiated for the u8 d=128 and Jaccard shapes (C1, C3, C4)
+#define LEAN_OK(MM, LL, CC) (((MM) == M_U8 && (LL) == 8 && (CC) == 1) || (MM) == M_JAC)
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch) {
   if (n_launch) ++*n_launch;
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC>(a, s);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) {                                        \
+    if (LEAN_OK(MM, LL, CC) && a.lean && !a.starts && a.nprod == 1) return run_search<MM, LL, CC, 12>(a, s); \
+    return run_search<MM, LL, CC, 4>(a, s);                                                 \
+  }
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
