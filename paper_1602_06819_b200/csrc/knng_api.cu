@@ -196,7 +196,7 @@ static void free_graph(knng_graph *g) {
     if (b) cudaFree(b);
   DBuf *ws[] = {&g->w_bits, &g->w_cand_i, &g->w_cand_k, &g->w_C_i, &g->w_C_k, &g->w_hash, &g->w_list, &g->w_props,
                 &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts,
-                &g->w_qoff, &g->w_qtok};
+                &g->w_qoff, &g->w_qtok, &g->w_tprof};
   for (DBuf *b : ws) b->release();
   for (auto &e : g->ev)
     if (e) cudaEventDestroy(e);
@@ -311,7 +311,7 @@ static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
   a.nprod = 1;
   a.lane_eval = 1;
   a.stages = 2;
-  if (const char *e = getenv("KNNG_STAGES")) a.stages = atoi(e) <= 2 ? 2 : 4;
+  if (const char *e = getenv("KNNG_STAGES")) a.stages = std::max(2, std::min(4, atoi(e)));
   if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
   a.lean = 0;
   if (const char *e = getenv("KNNG_LEAN")) a.lean = atoi(e) != 0;
@@ -390,6 +390,12 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.out_keys = out_k;
   a.stats = g->w_stats.as<unsigned long long>();
   a.prof = getenv("KNNG_PROFILE") ? a.stats + 8 : nullptr;   // cycle counters -> stats[8..13]
+  a.task_cycles = nullptr;
+  if (a.prof) {
+    CK(g->w_tprof.ensure((size_t)nq * pc * 8));
+    a.task_cycles = g->w_tprof.as<unsigned long long>();
+    g->tprof_n = nq * pc;
+  }
   a.task_ctr = a.stats + 14;
   a.pitch = g->metric == KNNG_JACCARD_U32SET ? 16 * 16 + 16 : (int)g->geom.stride + 16;
   plan_k1(a, g->metric == KNNG_JACCARD_U32SET, nq * pc, mmax);
@@ -561,9 +567,18 @@ static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t 
   CK(cudaMemcpyAsync(h, g->w_stats.p, 16 * 8, cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
   h[6] = (unsigned long long)(B * (B - 1));
-  if (getenv("KNNG_PROFILE") && B > 0)
+  if (getenv("KNNG_PROFILE") && B > 0) {
     fprintf(stderr, "KNNG_PROFILE cycles/task: consumer %.0f ring-wait %.0f walk %.0f | producer work %.0f wait %.0f | windows/task %.1f\n",
             (double)h[8] / B, (double)h[9] / B, (double)h[10] / B, (double)h[11] / B, (double)h[12] / B, (double)h[13] / B);
+    if (g->tprof_n > 0) {   // distribution of the per-task consumer time (the kernel ends with the longest)
+      std::vector<unsigned long long> tc((size_t)g->tprof_n);
+      CK(cudaMemcpy(tc.data(), g->w_tprof.p, tc.size() * 8, cudaMemcpyDeviceToHost));
+      std::sort(tc.begin(), tc.end());
+      auto q = [&](double f) { return (double)tc[std::min(tc.size() - 1, (size_t)(f * tc.size()))]; };
+      fprintf(stderr, "KNNG_PROFILE task cycles: p10 %.0f p50 %.0f p90 %.0f p99 %.0f max %.0f (%lld tasks)\n", q(0.1),
+              q(0.5), q(0.9), q(0.99), (double)tc.back(), (long long)g->tprof_n);
+    }
+  }
   fill_stats(g, st, h, nl, nev);
   return 0;
 }

@@ -57,7 +57,8 @@ struct knng_graph {
   uint32_t *tok = nullptr;                      // sets: tokens
   int64_t tok_cap = 0, tok_n = 0;               // token capacity / tokens in use (host mirror)
   int32_t *lrows = nullptr;                     // partitioned: [cap][k] partition-local row entries (-1 across)
-  uint32_t tok_max = 0;                         // largest stored token (valid when tok_n > 0)
+  uint32_t tok_max = 0;
+  int64_t tprof_n = 0;                          // KNNG_PROFILE: tasks of the last search                         // largest stored token (valid when tok_n > 0)
   int32_t *ids = nullptr;
   uint32_t *keys = nullptr;
   int32_t *ncnt = nullptr, *nfill = nullptr, *noff = nullptr, *scan_tmp = nullptr;
@@ -73,6 +74,7 @@ struct knng_graph {
   DBuf w_bits, w_cand_i, w_cand_k, w_C_i, w_C_k, w_hash, w_list, w_props, w_prop_cnt, w_sorted, w_stats,
       w_target, w_query, w_starts;
   DBuf w_qoff, w_qtok;
+  DBuf w_tprof;                                 // KNNG_PROFILE: per-task consumer cycles of the last search
   cudaEvent_t ev[6] = {};
 };
 

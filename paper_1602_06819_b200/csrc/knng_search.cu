@@ -21,7 +21,7 @@
 namespace knng {
 
 constexpr int RING_MAX = 32;      // smem ring of a.ring (16 or 32) chunks x 32 evaluated draws per CTA
-constexpr int FASTC = 4;          // chunks the consumer's skip-only fast path commits at once
+constexpr int FASTC = 4;          // chunks the consumer's skip-only fast path commits at once (<= ring)
 constexpr int HDR_BYTES = 128;
 
 struct RingHdr {
@@ -199,9 +199,8 @@ struct EvalLane {
 
 // vectors: lane's copies within a stage are the 16-byte chunks e = lane + 32 j (j < nchunks) of the
 // 32 x nchunks stage, i.e. row e / nchunks, chunk e % nchunks (walked incrementally).
-// U chunks per iteration (their keys computed together for ILP) in two groups of U stages: group
-// g + 1's rows are in flight while group g is evaluated.
-template <int U, class EV>
+// S single-chunk stages in a ring: chunks i+1 .. i+S-1 are in flight while chunk i is evaluated.
+template <int S, class EV>
 __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
   const int lane = threadIdx.x & 31;
   const int nck = EV::NCH > 0 ? EV::NCH : a.st.nchunks;
@@ -209,7 +208,6 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
   const size_t stride = a.st.stride;
   const int r0 = lane / nck, c0 = lane % nck, rs = 32 / nck, cs = 32 % nck;
   const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
-  const int64_t ng = (ni + U - 1) / U;
   const bool prof = a.prof != nullptr;
   long long p_wait = 0, p_work = 0;
   auto issue = [&](int st, int2 d) {
@@ -225,43 +223,29 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
       if (cc >= nck) { cc -= nck; ++r; }
     }
   };
-  int2 pn[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-    if (u < ni) issue(u, draw_node(x, u));
-  cp_async_commit();
-#pragma unroll
-  for (int u = 0; u < U; ++u) pn[u] = U + u < ni ? draw_node(x, U + u) : make_int2(0, 0);
-  for (int64_t g = 0; g < ng; ++g) {
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < ni) issue(s, draw_node(x, s));
+    cp_async_commit();
+  }
+  int2 pn = S - 1 < ni ? draw_node(x, S - 1) : make_int2(0, 0);
+  for (int64_t i = 0; i < ni; ++i) {
     const long long t0 = prof ? clock64() : 0;
     if (consumer_done(x)) break;
-    if (g + 1 < ng) {
-      const int h = (int)((g + 1) & 1) * U;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if ((g + 1) * U + u < ni) issue(h + u, pn[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u)   // (pool loads) in flight during this group's evaluation
-        pn[u] = (g + 2) * U + u < ni ? draw_node(x, (g + 2) * U + u) : make_int2(0, 0);
+    const int64_t ii = i + S - 1;
+    if (ii < ni) {
+      issue((int)(ii % S), pn);
+      if (ii + 1 < ni) pn = draw_node(x, ii + 1);   // (pool load) in flight during this evaluation
     }
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<S - 1>();
     __syncwarp();
-    const int h = (int)(g & 1) * U;
-    uint32_t key[U];
-    int32_t node[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      key[u] = ev.key(x.stg + (h + u) * 32 * x.pitch, x.pitch, nck);
-      node[u] = x.meta[((h + u) * 32 + lane) * 4];
-    }
+    const int st = (int)(i % S);
+    const uint32_t key = ev.key(x.stg + st * 32 * x.pitch, x.pitch, nck);
+    const int32_t node = x.meta[(st * 32 + lane) * 4];
     __syncwarp();
     if (prof) p_work += clock64() - t0;
-    bool more = true;
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (more && g * U + u < ni) more = publish(x, g * U + u, node[u], key[u], p_wait, prof);
-    if (!more) break;
+    if (!publish(x, i, node, key, p_wait, prof)) break;
   }
   cp_async_wait<0>();
   __syncwarp();
@@ -273,8 +257,9 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
 
 template <class EV>
 __device__ __forceinline__ void produce_vec_s(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
-  if (a.stages <= 2) produce_vec<1>(a, ev, x);
-  else produce_vec<2>(a, ev, x);
+  if (a.stages <= 2) produce_vec<2>(a, ev, x);
+  else if (a.stages == 3) produce_vec<3>(a, ev, x);
+  else produce_vec<4>(a, ev, x);
 }
 
 // the producer's evaluator: lane form for the configured row widths, else the warp form
@@ -400,6 +385,7 @@ template <int L>
 __device__ __forceinline__ void produce_any(const SearchArgs &a, const SetQuery<L> &Q, const ProdCtx &x, uint8_t *,
                                             int64_t) {
   if (a.stages <= 2) produce_set<2>(a, Q, x);
+  else if (a.stages == 3) produce_set<3>(a, Q, x);
   else produce_set<4>(a, Q, x);
 }
 
@@ -554,34 +540,41 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
             thr_key = top.key_at0;
             thr_ok = true;
           }
-          bool pass = false;
+          // the chunks before the first one holding a draw that passes the skip test go the fast way
+          unsigned pm = 0;
 #pragma unroll
-          for (int t = 0; t < FASTC; ++t) pass |= !thr.skip(fkey[t]);
-          if (!__any_sync(FULL, pass)) {
+          for (int t = 0; t < FASTC; ++t) pm |= __any_sync(FULL, !thr.skip(fkey[t])) ? (1u << t) : 0u;
+          const int tp = pm ? __ffs(pm) - 1 : FASTC;
+          if (tp > 0) {
             bool fr[FASTC];
 #pragma unroll
             for (int t = 0; t < FASTC; ++t) {
-              const uint32_t li = (uint32_t)fnode[t];   // the ring carries the pool index
-              const uint32_t bit = 1u << (li & 31);
-              fr[t] = !(atomicOr(ev + (li >> 5), bit) & bit);
+              fr[t] = false;
+              if (t < tp) {
+                const uint32_t li = (uint32_t)fnode[t];   // the ring carries the pool index
+                const uint32_t bit = 1u << (li & 31);
+                fr[t] = !(atomicOr(ev + (li >> 5), bit) & bit);
+              }
             }
             __syncwarp();
             int nf = 0;
 #pragma unroll
             for (int t = 0; t < FASTC; ++t) {
-              int32_t nd = fnode[t];
-              const bool ct = top.could_take(fkey[t]);  // (warp-wide)
-              if (pool && fr[t] && ct) nd = pool[nd];   // node id only when it may enter the top-k
-              top.insert(fr[t], fkey[t], nd);           // Q5: skipped starts enter the top-k
-              nf += __popc(__ballot_sync(FULL, fr[t]));
+              if (t < tp) {                             // (warp-uniform)
+                int32_t nd = fnode[t];
+                const bool ct = top.could_take(fkey[t]);
+                if (pool && fr[t] && ct) nd = pool[nd]; // node id only when it may enter the top-k
+                top.insert(fr[t], fkey[t], nd);         // Q5: skipped starts enter the top-k
+                nf += __popc(__ballot_sync(FULL, fr[t]));
+              }
             }
             c += nf;
             s_starts += nf;
             s_skip += nf;
-            p_win += FASTC;
+            p_win += tp;
             __syncwarp();
-            if (lane == 0) hdr->consumed = (int)(ch0 + FASTC);
-            jbase += 32 * FASTC;
+            if (lane == 0) hdr->consumed = (int)(ch0 + tp);
+            jbase += 32 * tp;
             continue;
           }
         }
@@ -795,6 +788,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
     }
     if (a.prof && lane == 0) {
       atomicAdd(a.prof + 0, (unsigned long long)(clock64() - tc0));
+      if (a.task_cycles) a.task_cycles[task] = (unsigned long long)(clock64() - tc0);
       atomicAdd(a.prof + 1, (unsigned long long)p_wait);
       atomicAdd(a.prof + 2, (unsigned long long)p_walk);
       atomicAdd(a.prof + 5, (unsigned long long)p_win);
