@@ -120,9 +120,11 @@ cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0,
   if (nrows <= 0) return cudaSuccess;
   // u8 rows: the tcgen05 kind::i8 form (knng_tc.cu); two column halves per split, merged below
   const char *tce = getenv("KNNG_TC");
-  if (g.metric == M_U8 && g.nchunks <= 16 && k <= 32 && !(tce && atoi(tce) == 0)) {
-    const int64_t bx = (nrows + 127) / 128;
-    int64_t ny = bx >= 148 ? 1 : std::min<int64_t>((148 + bx - 1) / bx, std::max<int64_t>(1, (ncols + 255) / 256));
+  const bool tc_u8 = g.metric == M_U8 && g.nchunks <= 16 && k <= 32;
+  const bool tc_f32 = g.metric == M_F32 && g.nchunks <= 24 && k <= 32;   // operands fit smem up to d = 96
+  if ((tc_u8 || tc_f32) && !(tce && atoi(tce) == 0)) {
+    const int64_t bx = (nrows + 127) / 128, tn = tc_u8 ? 256 : 64;
+    int64_t ny = bx >= 148 ? 1 : std::min<int64_t>((148 + bx - 1) / bx, std::max<int64_t>(1, (ncols + tn - 1) / tn));
     const size_t need = (size_t)2 * ny * nrows * k * 8;
     if (need > g_part_bytes) {
       if (g_part_buf) cudaFree(g_part_buf);
@@ -132,10 +134,15 @@ cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0,
     }
     int32_t *pi = (int32_t *)g_part_buf;
     uint32_t *pk = (uint32_t *)((char *)g_part_buf + (size_t)2 * ny * nrows * k * 4);
-    cudaError_t e = launch_tc_topk_u8(g, vec, row0, nrows, col0, ncols, k, ny, pi, pk, s);
+    cudaError_t e = tc_u8 ? launch_tc_topk_u8(g, vec, row0, nrows, col0, ncols, k, seed_ids, seed_keys, ny, pi, pk, s)
+                          : launch_tc_topk_f32(g, vec, row0, nrows, col0, ncols, k, seed_ids, seed_keys, ny, pi, pk, s);
     if (e != cudaSuccess) return e;
-    k_merge_partials<M_U8><<<(unsigned)((nrows + 3) / 4), 128, 0, s>>>(nrows, k, (int)(2 * ny), seed_ids, seed_keys,
-                                                                        pi, pk, out_ids, out_keys);
+    if (tc_u8)
+      k_merge_partials<M_U8><<<(unsigned)((nrows + 3) / 4), 128, 0, s>>>(nrows, k, (int)(2 * ny), seed_ids, seed_keys,
+                                                                          pi, pk, out_ids, out_keys);
+    else
+      k_merge_partials<M_F32><<<(unsigned)((nrows + 3) / 4), 128, 0, s>>>(nrows, k, (int)(2 * ny), seed_ids,
+                                                                           seed_keys, pi, pk, out_ids, out_keys);
     return cudaGetLastError();
   }
   const size_t smem = (size_t)128 * (g.nchunks + 1) * 16;

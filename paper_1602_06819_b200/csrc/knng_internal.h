@@ -102,7 +102,11 @@ cudaError_t launch_lrows(const int32_t *ids, int k, int64_t first, int64_t count
                          const int32_t *local_idx, int32_t *lrows, cudaStream_t s);
 cudaError_t exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t *tmp, int64_t n, cudaStream_t s);
 cudaError_t launch_tc_topk_u8(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
-                              int64_t ncols, int k, int64_t ny, int32_t *pi, uint32_t *pk, cudaStream_t s);
+                              int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
+                              uint32_t *pk, cudaStream_t s);
+cudaError_t launch_tc_topk_f32(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
+                               int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
+                               uint32_t *pk, cudaStream_t s);
 cudaError_t launch_exact_build(const VecGeom &g, const StoreView &st, int64_t n, int k, int32_t *ids,
                                uint32_t *keys, cudaStream_t s);
 cudaError_t launch_place(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int P,

@@ -120,7 +120,7 @@ template <int KM>
 __global__ void __launch_bounds__(256, 1)
     k_tc_topk_u8(const uint8_t *__restrict__ vec, size_t stride, int nchunks, int64_t row0, int64_t nrows, int64_t col0,
                  int64_t ncols, int k, const uint32_t *__restrict__ norms_r, const uint32_t *__restrict__ norms_c,
-                 int32_t *out_ids, uint32_t *out_keys) {
+                 const int32_t *seed_ids, const uint32_t *seed_keys, int32_t *out_ids, uint32_t *out_keys) {
   using namespace tc;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -179,6 +179,9 @@ __global__ void __launch_bounds__(256, 1)
   const int64_t myrow = r0 + quarter * 32 + lane;
   const uint32_t ni = myrow < nrows ? norms_r[myrow] : 0u;
   const int64_t mygid = row0 + myrow;             // global id of this row (self is excluded)
+  // seeded rows (A5: C_i): columns beyond the seeds' k-th key cannot reach the merged row
+  uint32_t seedk = 0xFFFFFFFFu;
+  if (seed_ids && myrow < nrows && seed_ids[(size_t)myrow * k + k - 1] >= 0) seedk = seed_keys[(size_t)myrow * k + k - 1];
 
   cp_async_wait<0>();
   fence_async_smem();
@@ -224,7 +227,8 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t v[64];
       tmem_ld64(taddr + q * 64, v);
       // screen: bit e of pm set when column e may enter the row's top-KM
-      const int thr = wk[KM - 1] == 0xFFFFFFFFu ? 0x7FFFFFFF : (int)(wk[KM - 1] - ni);
+      const uint32_t tk = min(wk[KM - 1], seedk);
+      const int thr = tk == 0xFFFFFFFFu ? 0x7FFFFFFF : (int)(tk - ni);
       uint32_t pm0 = 0, pm1 = 0;
 #pragma unroll
       for (int e4 = 0; e4 < 16; ++e4) {
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(256, 1)
         const bool mine = ((e < 32 ? pm0 >> e : pm1 >> (e - 32)) & 1u) != 0;
         const int c = q * 64 + e;
         const uint32_t key = (uint32_t)(nc[c] - 2 * (int)ve) + ni;
-        const bool ins = mine && key < wk[KM - 1] && c != selfc;
+        const bool ins = mine && key < wk[KM - 1] && key < seedk && c != selfc;
         uint32_t ck = ins ? key : 0xFFFFFFFFu;
         int32_t ci = ins ? (int32_t)(col0 + cbase + c) : 0x7FFFFFFF;
 #pragma unroll
@@ -284,8 +288,8 @@ __global__ void __launch_bounds__(256, 1)
 
 template <int KM>
 static cudaError_t run_tc(const uint8_t *vec, size_t stride, int nchunks, int64_t row0, int64_t nrows, int64_t col0,
-                          int64_t ncols, int k, const uint32_t *nr, const uint32_t *ncn, int64_t ny, int32_t *pi,
-                          uint32_t *pk, cudaStream_t s) {
+                          int64_t ncols, int k, const uint32_t *nr, const uint32_t *ncn, const int32_t *sid,
+                          const uint32_t *skey, int64_t ny, int32_t *pi, uint32_t *pk, cudaStream_t s) {
   const int NC = (nchunks + 1) & ~1;
   // operands + norms + barriers; >= 116 KB keeps one CTA per SM (its 512 TMEM columns)
   size_t smem = (size_t)tc::TM * NC * 16 + 2 * (size_t)tc::TN * NC * 16 + 3 * tc::TN * 4 + 64;
@@ -293,18 +297,302 @@ static cudaError_t run_tc(const uint8_t *vec, size_t stride, int nchunks, int64_
   cudaError_t e = cudaFuncSetAttribute(k_tc_topk_u8<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const dim3 grid((unsigned)((nrows + tc::TM - 1) / tc::TM), (unsigned)ny);
-  k_tc_topk_u8<KM><<<grid, 256, smem, s>>>(vec, stride, nchunks, row0, nrows, col0, ncols, k, nr, ncn, pi, pk);
+  k_tc_topk_u8<KM><<<grid, 256, smem, s>>>(vec, stride, nchunks, row0, nrows, col0, ncols, k, nr, ncn, sid, skey, pi, pk);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// fp32 rows (A0 / A5 for the F32 metric).  The exact key is the canonical fp32 sum of Q24, which a
+// tensor core cannot reproduce; the tensor core screens instead.  3xTF32: x = hi + lo with hi =
+// x with its 13 low mantissa bits cleared (exact in tf32) and lo = x - hi, and
+//   <a, b> ~ hi_a.hi_b + hi_a.lo_b + lo_a.hi_b          (kind::tf32 MMAs, fp32 accumulation)
+// whose error is below EPS * |a| |b| (dropped lo.lo term 2^-20, truncation of lo to tf32 2^-20 per
+// cross term, fp32 accumulation of 3 x 96 products; EPS = 6.1e-5 is 2x the sum of these bounds at
+// d <= 128).  A column survives the screen when its lower bound
+//   |a|^2 + |b|^2 - 2 <a,b>~ - 2 EPS |a||b| - GUARD (|a|^2 + |b|^2)
+// is below the row's exact k-th key; every survivor's key is then computed exactly in the canonical
+// order (thread_dist) and inserted.  A column that fails the screen cannot enter, so the rows are
+// bit-identical to the SIMT build's.
+// ---------------------------------------------------------------------------------------------
+namespace tc {
+constexpr int TNF = 64;    // columns per tile (MMA N) for fp32
+constexpr uint32_t IDESC_TF32 =
+    (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TNF >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+constexpr float EPS3 = 6.1e-5f, GUARD = 2.0e-5f;
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC_TF32), "r"(accum));
+}
+__device__ __forceinline__ void split_tf32(const uint4 &x, uint4 &hi, uint4 &lo) {
+  hi = make_uint4(x.x & 0xFFFFE000u, x.y & 0xFFFFE000u, x.z & 0xFFFFE000u, x.w & 0xFFFFE000u);
+  lo = make_uint4(__float_as_uint(__fsub_rn(__uint_as_float(x.x), __uint_as_float(hi.x))),
+                  __float_as_uint(__fsub_rn(__uint_as_float(x.y), __uint_as_float(hi.y))),
+                  __float_as_uint(__fsub_rn(__uint_as_float(x.z), __uint_as_float(hi.z))),
+                  __float_as_uint(__fsub_rn(__uint_as_float(x.w), __uint_as_float(hi.w))));
+}
+}  // namespace tc
+
+__global__ void k_norms_f32(const uint8_t *vec, size_t stride, int nchunks, int64_t row0, int64_t n, float *norms,
+                            float *roots) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 *r = (const uint4 *)(vec + (size_t)(row0 + i) * stride);
+  float acc = 0.0f;
+  for (int c = 0; c < nchunks; ++c) {
+    const uint4 v = ldg16(r + c);
+    acc = fmaf(__uint_as_float(v.x), __uint_as_float(v.x), acc);
+    acc = fmaf(__uint_as_float(v.y), __uint_as_float(v.y), acc);
+    acc = fmaf(__uint_as_float(v.z), __uint_as_float(v.z), acc);
+    acc = fmaf(__uint_as_float(v.w), __uint_as_float(v.w), acc);
+  }
+  norms[i] = acc;
+  roots[i] = sqrtf(acc);
+}
+
+// Same tiling and outputs as k_tc_topk_u8 with 64-column tiles: A (hi, lo) resident, B (hi, lo)
+// double-buffered through registers (the split needs the values), two 64-column TMEM accumulators.
+template <int KM>
+__global__ void __launch_bounds__(256, 1)
+    k_tc_topk_f32(const uint8_t *__restrict__ vec, size_t stride, int nchunks, int64_t row0, int64_t nrows,
+                  int64_t col0, int64_t ncols, int k, const float *__restrict__ norms_r, const float *__restrict__ roots_r,
+                  const float *__restrict__ norms_c, const float *__restrict__ roots_c, const int32_t *seed_ids,
+                  const uint32_t *seed_keys, int32_t *out_ids, uint32_t *out_keys) {
+  using namespace tc;
+  constexpr int TN = TNF;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NC = (nchunks + 1) & ~1;
+  const uint32_t sboA = NC * 128, sboB = NC * 128;
+  uint8_t *sAh = smem;                            // [TM/8][NC][8][16]
+  uint8_t *sAl = sAh + TM * NC * 16;
+  uint8_t *sB = sAl + TM * NC * 16;               // [2 buf][hi, lo][TN/8][NC][8][16]
+  const uint32_t bpart = TN * NC * 16;            // one B operand (hi or lo) of one buffer
+  float *sN = (float *)(sB + 4 * bpart);          // [3][TN] column norms (x (1 - GUARD)) and roots
+  float *sR = sN + 3 * TN;
+  uint64_t *bars = (uint64_t *)(sR + 3 * TN);
+  uint32_t *tslot = (uint32_t *)(bars + 2);
+
+  const int64_t per = ((ncols + gridDim.y - 1) / gridDim.y + TN - 1) / TN * TN;
+  const int64_t c_lo = (int64_t)blockIdx.y * per;
+  const int64_t c_hi = c_lo + per < ncols ? c_lo + per : ncols;
+  const int64_t ntile = c_hi > c_lo ? (c_hi - c_lo + TN - 1) / TN : 0;
+  const int64_t r0 = (int64_t)blockIdx.x * TM;
+
+  if (warp == 0) {   // TMEM: two 128 x 64 fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tslot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < TM * NC; i += 256) {      // A: rows split into hi / lo
+    const int r = i / NC, c = i % NC;
+    const uint32_t o = (r >> 3) * sboA + c * 128 + (r & 7) * 16;
+    uint4 x = make_uint4(0, 0, 0, 0), hi, lo;
+    if (r0 + r < nrows && c < nchunks) x = ldg16(vec + (size_t)(row0 + r0 + r) * stride + (size_t)c * 16);
+    split_tf32(x, hi, lo);
+    *(uint4 *)(sAh + o) = hi;
+    *(uint4 *)(sAl + o) = lo;
+  }
+  // B tile loads: TN x NC chunks, at most 8 per thread (NC <= 32), staged in registers
+  constexpr int BPT = (TN * 32 + 255) / 256;
+  uint4 breg[BPT];
+  auto load_regs = [&](int64_t t) {
+    const int64_t cb = c_lo + t * TN;
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const int i = tid + 256 * j;
+      const int r = i / NC, c = i % NC;
+      breg[j] = make_uint4(0, 0, 0, 0);
+      if (i < TN * NC && cb + r < c_hi && c < nchunks)
+        breg[j] = ldg16(vec + (size_t)(col0 + cb + r) * stride + (size_t)c * 16);
+    }
+  };
+  auto store_b = [&](int64_t t, int buf) {
+    const int64_t cb = c_lo + t * TN;
+    uint8_t *bh = sB + (size_t)(2 * buf) * bpart, *bl = bh + bpart;
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const int i = tid + 256 * j;
+      if (i < TN * NC) {
+        const int r = i / NC, c = i % NC;
+        const uint32_t o = (r >> 3) * sboB + c * 128 + (r & 7) * 16;
+        uint4 hi, lo;
+        split_tf32(breg[j], hi, lo);
+        *(uint4 *)(bh + o) = hi;
+        *(uint4 *)(bl + o) = lo;
+      }
+    }
+    for (int r = tid; r < TN; r += 256) {
+      const bool ok = cb + r < c_hi;
+      sN[(t % 3) * TN + r] = ok ? norms_c[cb + r] * (1.0f - GUARD) : __int_as_float(0x7F800000);
+      sR[(t % 3) * TN + r] = ok ? roots_c[cb + r] : 0.0f;
+    }
+  };
+
+  uint32_t wk[KM];   // exact keys (fp32 bits; non-negative, so integer order = float order)
+  int32_t wi[KM];
+#pragma unroll
+  for (int t = 0; t < KM; ++t) { wk[t] = 0x7F800000u; wi[t] = 0x7FFFFFFF; }
+  const int quarter = warp & 3, half = warp >> 2;
+  const int64_t myrow = r0 + quarter * 32 + lane;
+  const float nrow = myrow < nrows ? norms_r[myrow] : 0.0f;
+  const float arow = myrow < nrows ? 2.0f * EPS3 * roots_r[myrow] : 0.0f;
+  const int64_t mygid = row0 + myrow;
+  const uint8_t *rowp = vec + (size_t)(myrow < nrows ? row0 + myrow : row0) * stride;
+  // seeded rows (A5: C_i): no column beyond the seeds' k-th key can reach the merged row, and every
+  // column id exceeds every seed id, so equal keys lose too
+  uint32_t seedk = 0x7F800000u;
+  if (seed_ids && myrow < nrows && seed_ids[(size_t)myrow * k + k - 1] >= 0) seedk = seed_keys[(size_t)myrow * k + k - 1];
+
+  if (ntile > 0) { load_regs(0); store_b(0, 0); }
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t ah = smem_u32(sAh), al = smem_u32(sAl), b0 = smem_u32(sB);
+  auto issue_mma = [&](int64_t t) {
+    const int buf = (int)(t & 1);
+    const uint32_t td = tbase + (uint32_t)(buf * TN);
+    const uint32_t bh = b0 + 2 * buf * bpart, bl = bh + bpart;
+    for (int kk = 0; kk < NC / 2; ++kk) {
+      const uint64_t dah = smem_desc(ah + kk * 256, 128, sboA), dal = smem_desc(al + kk * 256, 128, sboA);
+      const uint64_t dbh = smem_desc(bh + kk * 256, 128, sboB), dbl = smem_desc(bl + kk * 256, 128, sboB);
+      mma_tf32(td, dah, dbh, kk > 0 ? 1u : 0u);
+      mma_tf32(td, dah, dbl, 1u);
+      mma_tf32(td, dal, dbh, 1u);
+    }
+    mma_commit(&bars[buf]);
+  };
+  if (ntile > 0 && tid == 0) issue_mma(0);
+  if (ntile > 1) load_regs(1);
+
+  for (int64_t t = 0; t < ntile; ++t) {
+    const int buf = (int)(t & 1);
+    mbar_wait(&bars[buf], (unsigned)((t >> 1) & 1));   // MMA t done: TMEM buf ready, B buf free
+    fence_after();
+    if (t + 1 < ntile) store_b(t + 1, buf ^ 1);         // B buf^1 was read by MMA t-1 (done)
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (t + 1 < ntile && tid == 0) issue_mma(t + 1);
+    if (t + 2 < ntile) load_regs(t + 2);                // in flight during the epilogue
+    // epilogue of tile t: this thread's row against its 32 columns
+    const int64_t cbase = c_lo + t * TN + half * (TN / 2);
+    const uint32_t taddr = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * TN + half * (TN / 2));
+    const float *nc = sN + (t % 3) * TN + half * (TN / 2);
+    const float *rc = sR + (t % 3) * TN + half * (TN / 2);
+    const int64_t selfc = mygid - (col0 + cbase);
+    uint32_t v[32];
+    tmem_ld32(taddr, v);
+    // screen: lower bound of the key below the exact k-th key (its fp32 value; +inf while empty)
+    const float rhs = __uint_as_float(min(wk[KM - 1], seedk)) - nrow * (1.0f - GUARD);
+    uint32_t pm = 0;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const float x = fmaf(-2.0f, __uint_as_float(v[e]), nc[e]);
+      const float lb = fmaf(-arow, rc[e], x);
+      pm |= (lb < rhs ? 1u : 0u) << e;
+    }
+    if (myrow >= nrows) pm = 0;
+    while (pm) {                                   // exact keys of this lane's survivors
+      const int e = __ffs(pm) - 1;
+      pm &= pm - 1;
+      if (e != selfc) {
+        const int64_t gc = col0 + cbase + e;
+        const uint32_t key = thread_dist<M_F32>((const uint4 *)rowp, (const uint4 *)(vec + (size_t)gc * stride), nchunks);
+        if (key < wk[KM - 1] && key < seedk) {
+          uint32_t ck = key;
+          int32_t ci = (int32_t)gc;
+#pragma unroll
+          for (int s2 = 0; s2 < KM; ++s2) {
+            const bool sw = ck < wk[s2] || (ck == wk[s2] && ci < wi[s2]);
+            const uint32_t tk = wk[s2];
+            const int32_t ti = wi[s2];
+            wk[s2] = sw ? ck : tk;
+            wi[s2] = sw ? ci : ti;
+            ck = sw ? tk : ck;
+            ci = sw ? ti : ci;
+          }
+        }
+      }
+    }
+    fence_before();
+  }
+  if (myrow < nrows) {
+    const size_t part = (size_t)blockIdx.y * 2 + half;
+    int32_t *oi = out_ids + (part * nrows + myrow) * k;
+    uint32_t *ok = out_keys + (part * nrows + myrow) * k;
+#pragma unroll
+    for (int s = 0; s < KM; ++s)
+      if (s < k) {
+        oi[s] = wi[s] == 0x7FFFFFFF ? -1 : wi[s];
+        ok[s] = wi[s] == 0x7FFFFFFF ? 0u : wk[s];
+      }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tbase) : "memory");
+}
+
+template <int KM>
+static cudaError_t run_tc_f32(const uint8_t *vec, size_t stride, int nchunks, int64_t row0, int64_t nrows,
+                              int64_t col0, int64_t ncols, int k, const float *nr, const float *rr, const float *ncn,
+                              const float *rcn, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
+                              uint32_t *pk, cudaStream_t s) {
+  const int NC = (nchunks + 1) & ~1;
+  size_t smem = 2 * (size_t)tc::TM * NC * 16 + 4 * (size_t)tc::TNF * NC * 16 + 6 * tc::TNF * 4 + 64;
+  if (smem < 116 * 1024) smem = 116 * 1024;   // one CTA per SM
+  cudaError_t e = cudaFuncSetAttribute(k_tc_topk_f32<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const dim3 grid((unsigned)((nrows + tc::TM - 1) / tc::TM), (unsigned)ny);
+  k_tc_topk_f32<KM><<<grid, 256, smem, s>>>(vec, stride, nchunks, row0, nrows, col0, ncols, k, nr, rr, ncn, rcn, sid,
+                                            skey, pi, pk);
   return cudaGetLastError();
 }
 
 static uint32_t *g_norm_buf = nullptr;
 static size_t g_norm_bytes = 0;
 
+static float *g_fnorm_buf = nullptr;
+static size_t g_fnorm_bytes = 0;
+
+// tcgen05 (3xTF32 screen + exact canonical rerank) form of launch_tile_topk for fp32 rows
+// (nchunks <= 24, k <= 32): partial rows per column split and half into pi/pk ([2 ny][nrows][k]).
+cudaError_t launch_tc_topk_f32(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
+                               int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
+                               uint32_t *pk, cudaStream_t s) {
+  if (g.metric != M_F32 || g.nchunks > 24 || k > 32) return cudaErrorNotSupported;
+  const size_t need = (size_t)(nrows + ncols) * 8;
+  if (need > g_fnorm_bytes) {
+    if (g_fnorm_buf) cudaFree(g_fnorm_buf);
+    cudaError_t e = cudaMalloc((void **)&g_fnorm_buf, need);
+    if (e != cudaSuccess) { g_fnorm_buf = nullptr; g_fnorm_bytes = 0; return e; }
+    g_fnorm_bytes = need;
+  }
+  float *nr = g_fnorm_buf, *rr = nr + nrows, *ncn = rr + nrows, *rcn = ncn + ncols;
+  k_norms_f32<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(vec, g.stride, g.nchunks, row0, nrows, nr, rr);
+  k_norms_f32<<<(unsigned)((ncols + 255) / 256), 256, 0, s>>>(vec, g.stride, g.nchunks, col0, ncols, ncn, rcn);
+  if (k <= 10)
+    return run_tc_f32<10>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, rr, ncn, rcn, sid, skey, ny, pi, pk, s);
+  if (k <= 20)
+    return run_tc_f32<20>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, rr, ncn, rcn, sid, skey, ny, pi, pk, s);
+  return run_tc_f32<32>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, rr, ncn, rcn, sid, skey, ny, pi, pk, s);
+}
+
 // tcgen05 form of launch_tile_topk for u8 rows (nchunks <= 16, k <= 32): partial rows per column
 // split and half into pi/pk ([2 ny][nrows][k]).  Returns cudaErrorNotSupported when the shape is
 // not covered.
 cudaError_t launch_tc_topk_u8(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
-                              int64_t ncols, int k, int64_t ny, int32_t *pi, uint32_t *pk, cudaStream_t s) {
+                              int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
+                              uint32_t *pk, cudaStream_t s) {
   if (g.metric != M_U8 || g.nchunks > 16 || k > 32) return cudaErrorNotSupported;
   const size_t need = (size_t)(nrows + ncols) * 4;
   if (need > g_norm_bytes) {
@@ -316,9 +604,9 @@ cudaError_t launch_tc_topk_u8(const VecGeom &g, const uint8_t *vec, int64_t row0
   uint32_t *nr = g_norm_buf, *ncn = g_norm_buf + nrows;
   k_norms_u8<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(vec, g.stride, g.nchunks, row0, nrows, nr);
   k_norms_u8<<<(unsigned)((ncols + 255) / 256), 256, 0, s>>>(vec, g.stride, g.nchunks, col0, ncols, ncn);
-  if (k <= 10) return run_tc<10>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, ncn, ny, pi, pk, s);
-  if (k <= 16) return run_tc<16>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, ncn, ny, pi, pk, s);
-  return run_tc<32>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, ncn, ny, pi, pk, s);
+  if (k <= 10) return run_tc<10>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, ncn, sid, skey, ny, pi, pk, s);
+  if (k <= 16) return run_tc<16>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, ncn, sid, skey, ny, pi, pk, s);
+  return run_tc<32>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, ncn, sid, skey, ny, pi, pk, s);
 }
 
 }  // namespace knng

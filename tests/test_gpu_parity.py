@@ -84,6 +84,22 @@ def test_graph_init_tcgen05_vs_oracle(n, dim, k):
     _assert_rows_equal(O.U8, gi, gk, o.ids[:n], o.keys[:n], "tc init n=%d d=%d k=%d" % (n, dim, k))
 
 
+@pytest.mark.parametrize("n,dim,k,scale", [(129, 4, 1, 1.0), (700, 96, 20, 1.0), (555, 33, 16, 100.0),
+                                           (1300, 96, 32, 0.01), (1300, 128, 32, 1.0), (300, 96, 7, 1.0)])
+def test_graph_init_tcgen05_f32_vs_oracle(n, dim, k, scale):
+    """fp32 rows go through the 3xTF32 tcgen05 screen + exact canonical rerank (d <= 128): the graph
+    must be bit-identical to the oracle's, including near-ties (duplicated points, tiny offsets)."""
+    rng = np.random.default_rng(n + dim)
+    X = (rng.standard_normal((n, dim)) * scale).astype(np.float32)
+    X[n // 2:n // 2 + 20] = X[:20]                                  # exact duplicates (key 0, ties by id)
+    X[n // 3:n // 3 + 20] = X[:20] + np.float32(1e-6 * scale)       # near-duplicates
+    g = _graph(X, k)
+    o = O.OracleGraph(O.F32, X, k)
+    o.init_exact()
+    gi, gk = g.rows()
+    _assert_rows_equal(O.F32, gi, gk, o.ids[:n], o.keys[:n], "tc f32 init n=%d d=%d k=%d" % (n, dim, k))
+
+
 def test_graph_init_errors():
     from paper_1602_06819_b200 import KnngGraph, KnngError
     with pytest.raises(KnngError) as e:
