@@ -389,7 +389,7 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.out_ids = out_i;
   a.out_keys = out_k;
   a.stats = g->w_stats.as<unsigned long long>();
-  a.prof = getenv("KNNG_PROFILE") ? a.stats + 8 : nullptr;   // cycle counters -> stats[8..13]
+  a.prof = getenv("KNNG_PROFILE") ? a.stats + 16 : nullptr;  // cycle counters -> stats[16..31]
   a.task_cycles = nullptr;
   if (a.prof) {
     CK(g->w_tprof.ensure((size_t)nq * pc * 8));
@@ -563,13 +563,15 @@ static int stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, c
 }
 
 static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t B) {
-  unsigned long long h[16];
-  CK(cudaMemcpyAsync(h, g->w_stats.p, 16 * 8, cudaMemcpyDeviceToHost, g->stream));
+  unsigned long long h[32];
+  CK(cudaMemcpyAsync(h, g->w_stats.p, 32 * 8, cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
   h[6] = (unsigned long long)(B * (B - 1));
   if (getenv("KNNG_PROFILE") && B > 0) {
     fprintf(stderr, "KNNG_PROFILE cycles/task: consumer %.0f ring-wait %.0f walk %.0f | producer work %.0f wait %.0f | windows/task %.1f\n",
-            (double)h[8] / B, (double)h[9] / B, (double)h[10] / B, (double)h[11] / B, (double)h[12] / B, (double)h[13] / B);
+            (double)h[16] / B, (double)h[17] / B, (double)h[18] / B, (double)h[19] / B, (double)h[20] / B, (double)h[21] / B);
+    fprintf(stderr, "KNNG_PROFILE walk step cycles/task: rows-wait %.0f issue+sets %.0f gather+eval %.0f commit %.0f\n",
+            (double)h[22] / B, (double)h[23] / B, (double)h[24] / B, (double)h[25] / B);
     if (g->tprof_n > 0) {   // distribution of the per-task consumer time (the kernel ends with the longest)
       std::vector<unsigned long long> tc((size_t)g->tprof_n);
       CK(cudaMemcpy(tc.data(), g->w_tprof.p, tc.size() * 8, cudaMemcpyDeviceToHost));
@@ -589,8 +591,8 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: null graph");
   if (first_id_out) *first_id_out = g->n;
   CK(cudaSetDevice(g->device));
-  CK(g->w_stats.ensure(16 * 8));
-  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  CK(g->w_stats.ensure(32 * 8));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   const int64_t B = pts ? pts->n : 0, k = g->k;
   const int Pn = g->P > 0 ? g->P : 1;
   CK(g->w_cand_i.ensure((size_t)std::max<int64_t>(B, 1) * Pn * k * 4));
@@ -629,8 +631,8 @@ int graph_insert_stage_search(knng_graph *g, const knng_points *pts, const knng_
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "stage_search: null graph");
   if (g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_search: a staged batch is pending");
   CK(cudaSetDevice(g->device));
-  CK(g->w_stats.ensure(16 * 8));
-  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  CK(g->w_stats.ensure(32 * 8));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   int nl = 0;
   CK(cudaEventRecord(g->ev[0], g->stream));
   if (int r = stage_search(g, pts, p, part_lo, part_hi, q_lo, q_hi, cand_ids, cand_keys, &nl)) {
@@ -648,7 +650,7 @@ int graph_insert_stage_update(knng_graph *g, const knng_params *p, int32_t world
   if (!g || !p) return fail(KNNG_ERR_INVALID_ARG, "stage_update: null argument");
   if (world < 1 || q_lo < 0 || q_hi < q_lo || q_hi > g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_update: bad range");
   CK(cudaSetDevice(g->device));
-  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   int nl = 0;
   CK(cudaEventRecord(g->ev[0], g->stream));
   if (int r = stage_update(g, p, world, cand_ids_all, cand_keys_all, q_lo, q_hi, (int2 *)props, prop_cnt, new_ids,
@@ -665,7 +667,7 @@ int graph_insert_stage_commit(knng_graph *g, const knng_params *p, int64_t nq_sl
   if (!g || !p) return fail(KNNG_ERR_INVALID_ARG, "stage_commit: null argument");
   if (nq_slots < g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "stage_commit: fewer query slots than the batch");
   CK(cudaSetDevice(g->device));
-  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   int nl = 0;
   CK(cudaEventRecord(g->ev[0], g->stream));
   if (int r = stage_commit(g, p, nq_slots, (const int2 *)props_all, prop_cnt_all, new_ids_all, new_keys_all, &nl))
@@ -684,14 +686,14 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
   if (kr < 1 || kr > 32) return fail(KNNG_ERR_INVALID_ARG, "graph_search: kr=%d outside 1..32", kr);
   if (q->n > 0 && (!ids_out || !keys_out)) return fail(KNNG_ERR_INVALID_ARG, "graph_search: null outputs");
   CK(cudaSetDevice(g->device));
-  CK(g->w_stats.ensure(16 * 8));
+  CK(g->w_stats.ensure(32 * 8));
   const int64_t nq = q->n;
   if (nq == 0) {
     fill_stats(g, st, (const unsigned long long[8]){0, 0, 0, 0, 0, 0, 0, 0}, 0, 0);
     return KNNG_OK;
   }
   int nl = 0;
-  CK(cudaMemsetAsync(g->w_stats.p, 0, 16 * 8, g->stream));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   StoreView qs = graph_store_view(g);
   if (g->metric == KNNG_JACCARD_U32SET) {
     CK(g->w_qoff.ensure((size_t)(nq + 1) * 8));
