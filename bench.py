@@ -295,19 +295,41 @@ def run_ours(args, cfg):
                  "peak_source": "MEASURED_PEAKS.json bf16_tflops x nominal dtype ratio",
                  "note": "B x B exact all-pairs of the batch with top-k epilogue; tiny per step, latency-bound"}
 
-    # recall@k of the inserted points' rows vs the exact k-nn over the final point set (sampled, torch)
-    rec = None
+    # graph quality on seeded samples (exact k-nn of the final point set: torch brute force for vectors,
+    # the library's own search in exact mode -- speedup 1, budget = pool, parity-tested equal to linear
+    # search -- for sets):  recall@k of the inserted points' rows, the fraction of correct edges over
+    # all nodes, and the paper's Q estimated from it
+    ntot = cfg.n0 + pos
+    rs = np.random.default_rng(4000 + int(cfg.name[1:]))
+    samp_new = cfg.n0 + np.sort(rs.choice(pos, min(pos, 256), replace=False)) if pos else np.zeros(0, np.int64)
+    samp_all = np.sort(rs.choice(ntot, min(ntot, 256), replace=False))
+    nodes = np.concatenate([samp_new, samp_all]).astype(np.int64)
     if cfg.metric != D.JAC:
-        ids, keys = g.rows(cfg.n0, pos)
-        samp = np.arange(0, pos, max(1, pos // 256))
         allp = torch.from_numpy(np.concatenate([X, S[:pos]])).to("cuda").float()
-        q = allp[cfg.n0 + samp]
-        d2 = torch.cat([torch.cdist(q, allp[i:i + (1 << 20)]).pow(2) for i in range(0, len(allp), 1 << 20)], 1)
-        d2[torch.arange(len(samp)), torch.from_numpy(cfg.n0 + samp).cuda()] = float("inf")
-        exact = torch.topk(d2, cfg.k, largest=False).indices.cpu().numpy()
-        rec = float(np.mean([len(set(ids[s].tolist()) & set(exact[i].tolist())) / cfg.k
-                             for i, s in enumerate(samp)]))
+        nq = torch.from_numpy(nodes).cuda()
+        q = allp[nq]
+        bd = torch.full((len(nodes), cfg.k), float("inf"), device="cuda")
+        bi = torch.zeros((len(nodes), cfg.k), dtype=torch.int64, device="cuda")
+        for i in range(0, len(allp), 1 << 20):      # running top-k over column chunks
+            d2 = torch.cdist(q, allp[i:i + (1 << 20)]).pow(2)
+            cols = torch.arange(i, i + d2.shape[1], device="cuda")
+            d2[nq[:, None] == cols[None, :]] = float("inf")
+            vd, vi = torch.topk(d2, min(cfg.k, d2.shape[1]), largest=False)
+            bd, sel = torch.topk(torch.cat([bd, vd], 1), cfg.k, largest=False)
+            bi = torch.gather(torch.cat([bi, vi + i], 1), 1, sel)
+        exact = bi.cpu().numpy()
         del allp, d2
+    else:
+        qs = [X[i] if i < cfg.n0 else S[i - cfg.n0] for i in nodes]
+        ex_ids, _, _ = g.search(qs, cfg.k + 1, 1.0, cfg.e_num, cfg.e_den, cfg.search_seed)
+        exact = np.stack([[x for x in r if x != nd][:cfg.k] for r, nd in zip(ex_ids, nodes)])
+    got = np.stack([g.rows(int(nd), 1)[0][0] for nd in nodes])
+    hit = np.array([len(set(a.tolist()) & set(b.tolist())) / cfg.k for a, b in zip(got, exact)])
+    rec = float(hit[:len(samp_new)].mean()) if len(samp_new) else None
+    cef = float(hit[len(samp_new):].mean())
+    e_m = pos * cfg.k + cfg.n0 * cfg.k * pos / (pos + cfg.n0) if pos else 0.0
+    e_u = ntot * cfg.k - e_m
+    Q = (cef * ntot * cfg.k - e_u) / e_m if e_m > 0 else None
     g.close()
 
     # ---------------- end to end through the C ABI with host buffers (e2e) ----------------
@@ -345,6 +367,9 @@ def run_ours(args, cfg):
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "similarities_per_s": evals / t_total,
         "recall_at_k": rec,
+        "quality": {"correct_edge_fraction": cef, "Q": Q, "n": cfg.n0, "n_a": pos,
+                    "samples": "%d inserted + %d uniform nodes (seeded), exact k-nn of the final point set" % (
+                        len(samp_new), len(samp_all))},
         "search_per_query": {f: sum(s_[f] for s_ in stats) / (len(stats) * B) for f in
                              ("search_evals", "search_starts", "search_skipped", "search_expansions", "ball_nodes",
                               "proposals")},
