@@ -21,13 +21,34 @@ def stale():
 
 
 def build(force=False, verbose=False):
+    """Compile every .cu to an object in parallel (one nvcc per file), then link the shared library."""
     if not force and not stale():
         return OUT
-    tmp = OUT + ".tmp%d" % os.getpid()
-    cmd = ["nvcc"] + NVCC_FLAGS + ["-o", tmp] + SRC
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    jobs = []
+    for src in SRC:
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".%d.o" % os.getpid())
+        jobs.append((["nvcc"] + cflags + ["-c", src, "-o", obj], obj))
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        for cmd, _ in jobs:
+            print(" ".join(cmd), file=sys.stderr)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        rcs = list(ex.map(lambda j: subprocess.run(j[0]).returncode, jobs))
+    if any(rcs):
+        for _, obj in jobs:
+            if os.path.exists(obj):
+                os.remove(obj)
+        raise subprocess.CalledProcessError(max(rcs), "nvcc")
+    tmp = OUT + ".tmp%d" % os.getpid()
+    link = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + [o for _, o in jobs]
+    if verbose:
+        print(" ".join(link), file=sys.stderr)
+    subprocess.check_call(link)
+    for _, obj in jobs:
+        os.remove(obj)
     os.replace(tmp, OUT)
     return OUT
 

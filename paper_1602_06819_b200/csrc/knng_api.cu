@@ -311,11 +311,10 @@ static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
   a.nprod = 1;
   a.lane_eval = 1;
   a.stages = 2;
-  if (const char *e = getenv("KNNG_STAGES")) a.stages = std::max(2, std::min(4, atoi(e)));
+  // (a.stages is fixed at 2: deeper producer pipelines measured slower everywhere)
   if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
-  a.lean = 0;
-  if (const char *e = getenv("KNNG_LEAN")) a.lean = atoi(e) != 0;
-  const int cap = a.lean ? 12 : 8;                 // two-warp CTAs per SM the registers allow
+  a.lean = 0;                                      // (the 80-register variant measured slower)
+  const int cap = 8;                               // two-warp CTAs per SM the registers allow
   const int need = (int)std::min<int64_t>(cap, (tasks + nsm - 1) / nsm);
   auto occ = [&](const SearchArgs &x) {
     const size_t sm = search_smem_bytes(x, sets) + 1024;

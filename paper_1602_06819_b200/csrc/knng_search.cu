@@ -20,7 +20,6 @@
 
 namespace knng {
 
-constexpr int RING_MAX = 32;      // smem ring of a.ring (16 or 32) chunks x 32 evaluated draws per CTA
 constexpr int FASTC = 4;          // chunks the consumer's skip-only fast path commits at once (<= ring)
 constexpr int HDR_BYTES = 128;
 
@@ -255,11 +254,10 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
   }
 }
 
+// two stages measured fastest on every config (deeper pipelines cost CTAs per SM): the only one built
 template <class EV>
 __device__ __forceinline__ void produce_vec_s(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
-  if (a.stages <= 2) produce_vec<2>(a, ev, x);
-  else if (a.stages == 3) produce_vec<3>(a, ev, x);
-  else produce_vec<4>(a, ev, x);
+  produce_vec<2>(a, ev, x);
 }
 
 // the producer's evaluator: lane form for the configured row widths, else the warp form
@@ -384,9 +382,7 @@ __device__ __forceinline__ void produce_any(const SearchArgs &a, const VecQuery<
 template <int L>
 __device__ __forceinline__ void produce_any(const SearchArgs &a, const SetQuery<L> &Q, const ProdCtx &x, uint8_t *,
                                             int64_t) {
-  if (a.stages <= 2) produce_set<2>(a, Q, x);
-  else if (a.stages == 3) produce_set<3>(a, Q, x);
-  else produce_set<4>(a, Q, x);
+  produce_set<2>(a, Q, x);
 }
 
 // K1: one CTA per (query, partition) task: warp 0 runs the search in the paper's sequential
@@ -415,6 +411,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
   uint32_t *qscr = (uint32_t *)(lrowbuf2 + 32 * lk);                          // [2][QMAX] (sets)
   uint32_t *vbm = qscr + (M == M_JAC ? 2 * QMAX : 0);                        // [vwords] (sets)
   const int vwords = M == M_JAC ? a.st.vwords : 0;
+  const uint32_t vw_lim = (uint32_t)a.st.vwords;   // (bounds for the Jaccard vocabulary bitmap)
   int32_t *exh = (int32_t *)(vbm + vwords);                                  // [EXCAP] expanded-set hash
   uint32_t *sbits = (uint32_t *)(exh + EXCAP);                               // [bits_words / 2] (smem bits)
   const int Pn = a.part_cnt;
@@ -449,7 +446,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
     if (M == M_JAC && vwords > 0 && warp == 0)   // clear the previous query's vocabulary bits
       for (int i = lane; i < prev_qn; i += 32) {
         const uint32_t t = qscr[i];
-        if ((t >> 5) < (uint32_t)vwords) vbm[t >> 5] = 0;
+        if ((t >> 5) < vw_lim) vbm[t >> 5] = 0;
       }
     __syncthreads();
     // dynamic task scheduling: the CTA's next task (read after the next top barrier)
@@ -473,7 +470,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
       if (warp == 0 && qn <= QMAX) {
         for (int i = lane; i < qn; i += 32) {
           const uint32_t t = qscr[i];
-          if ((t >> 5) < (uint32_t)vwords) atomicOr(vbm + (t >> 5), 1u << (t & 31));
+          if ((t >> 5) < vw_lim) atomicOr(vbm + (t >> 5), 1u << (t & 31));
         }
         prev_qn = qn;
       } else if (warp == 0) {
@@ -884,15 +881,10 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   X(M_F32, 1, 1) X(M_F32, 1, 2) X(M_F32, 1, 3) X(M_F32, 1, 4) X(M_F32, 2, 3) X(M_F32, 2, 4) X(M_F32, 4, 3) \
   X(M_F32, 4, 4) X(M_F32, 8, 3) X(M_F32, 8, 4) X(M_F32, 32, 2) X(M_F32, 32, 4)
 
-// the lean (12 CTAs/SM) variant is instantiated for the u8 d=128 and Jaccard shapes (C1, C3, C4)
-#define LEAN_OK(MM, LL, CC) (((MM) == M_U8 && (LL) == 8 && (CC) == 1) || (MM) == M_JAC)
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch) {
   if (n_launch) ++*n_launch;
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) {                                        \
-    if (LEAN_OK(MM, LL, CC) && a.lean && !a.starts && a.nprod == 1) return run_search<MM, LL, CC, 12>(a, s); \
-    return run_search<MM, LL, CC, 4>(a, s);                                                 \
-  }
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, 4>(a, s);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)

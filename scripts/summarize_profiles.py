@@ -18,7 +18,7 @@ tag = sys.argv[1] if len(sys.argv) > 1 else "round1"
 cfgtag = sys.argv[2] if len(sys.argv) > 2 else "C1"
 lpath = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "launches.csv")
 rep = sys.argv[4] if len(sys.argv) > 4 else os.path.join(ROOT, "gpurun_out", "prof_search.ncu-rep")
-out = os.path.join(ROOT, "profiles")
+out = os.environ.get("PROFILES_OUT") or os.path.join(ROOT, "profiles")
 os.makedirs(out, exist_ok=True)
 
 # ---- launch list ----
