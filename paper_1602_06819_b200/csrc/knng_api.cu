@@ -336,6 +336,8 @@ static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
   a.smem_bits = cand[best][0];
   a.ring = cand[best][1];
   if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
+  a.walk_prefetch = 0;   // measured faster on C1-C4: the k-row prefetch costs more issue than the round trip it saves
+  if (const char *e = getenv("KNNG_WALK_PREFETCH")) a.walk_prefetch = atoi(e) != 0;
   if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 8 ? 8 : (atoi(e) <= 16 ? 16 : 32);
   if (const char *e = getenv("KNNG_SMEM_BITS")) a.smem_bits = atoi(e) != 0;
   a.gslots = std::min<int64_t>(tasks, (int64_t)nsm * cap);

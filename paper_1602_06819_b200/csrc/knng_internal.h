@@ -61,6 +61,7 @@ struct SearchArgs {
   int ring;                    // ring chunks (8, 16 or 32)
   int lean;                    // 1: the 80-register variant (12 two-warp CTAs per SM) where instantiated
   unsigned long long *task_cycles;   // KNNG_PROFILE: consumer cycles per task [nq * part_cnt], else null
+  int walk_prefetch;           // 1: prefetch the rows of all k neighbours during a walk step
 };
 size_t search_smem_bytes(const SearchArgs &a, bool sets);
 

@@ -748,6 +748,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
         const uint32_t lv = inpool ? (a.P > 0 ? (uint32_t)vl : (uint32_t)v) : 0u;
         __syncwarp();
         // prefetch the rows of the in-pool neighbours: the next cur is one of them
+        if (a.walk_prefetch)
         for (int base = 0; base < k * k; base += 32) {
           const int idx = base + lane;
           const int t = __float2int_rz(__fmul_rn(__int2float_rn(idx) + 0.5f, rk));   // idx / k
@@ -777,7 +778,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
         cur = __shfl_sync(FULL, v, fi);
         kcur = __shfl_sync(FULL, key, fi);
         curl = __shfl_sync(FULL, lv, fi);
-        pf = fi;
+        pf = a.walk_prefetch ? fi : -1;
         if (__shfl_sync(FULL, exb2, fi)) break;   // Q9: moving onto an expanded node restarts
       }
       if (a.prof) p_walk += clock64() - tk0;
