@@ -338,6 +338,10 @@ static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
   if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
   a.walk_prefetch = 0;   // measured faster on C1-C4: the k-row prefetch costs more issue than the round trip it saves
   if (const char *e = getenv("KNNG_WALK_PREFETCH")) a.walk_prefetch = atoi(e) != 0;
+  a.ex_one = 1;   // measured faster (C1, C3): one hash lookup per step instead of k
+  a.win_prefetch = 1;
+  if (const char *e = getenv("KNNG_WIN_PREFETCH")) a.win_prefetch = atoi(e) != 0;
+  if (const char *e = getenv("KNNG_EX_ONE")) a.ex_one = atoi(e) != 0;
   if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 8 ? 8 : (atoi(e) <= 16 ? 16 : 32);
   if (const char *e = getenv("KNNG_SMEM_BITS")) a.smem_bits = atoi(e) != 0;
   a.gslots = std::min<int64_t>(tasks, (int64_t)nsm * cap);

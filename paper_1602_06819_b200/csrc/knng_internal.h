@@ -62,6 +62,8 @@ struct SearchArgs {
   int lean;                    // 1: the 80-register variant (12 two-warp CTAs per SM) where instantiated
   unsigned long long *task_cycles;   // KNNG_PROFILE: consumer cycles per task [nq * part_cnt], else null
   int walk_prefetch;           // 1: prefetch the rows of all k neighbours during a walk step
+  int ex_one;                  // 1: look up the expanded set for the chosen neighbour only
+  int win_prefetch;            // 1: prefetch the rows of a window's possible starts
 };
 size_t search_smem_bytes(const SearchArgs &a, bool sets);
 

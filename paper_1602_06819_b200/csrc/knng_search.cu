@@ -616,6 +616,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
           }
           wpf = top.cnt == 0 ? lane == 0 : !thr.skip(wkey);
           if (wpf && wnode == -2) wnode = pool[wl];
+          if (!a.win_prefetch) wpf = false;
           if (__ballot_sync(FULL, wpf)) {
             cp_async_wait_all();      // older copies into rowbuf2 must land first
             if (wpf)
@@ -759,7 +760,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
           }
         }
         const bool evb2 = inpool ? bit_get(ev, lv) : true;
-        const bool exb2 = inpool ? ex_has(exh, ex_ovf, gex, lv) : false;
+        const bool exb2 = (inpool && !a.ex_one) ? ex_has(exh, ex_ovf, gex, lv) : false;
         const uint32_t key = Q.eval(a.st, inpool ? v : -1, k);
         const bool imp = inpool && closer<M>(key, kcur);
         const unsigned im = __ballot_sync(FULL, imp);
@@ -779,7 +780,9 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
         kcur = __shfl_sync(FULL, key, fi);
         curl = __shfl_sync(FULL, lv, fi);
         pf = a.walk_prefetch ? fi : -1;
-        if (__shfl_sync(FULL, exb2, fi)) break;   // Q9: moving onto an expanded node restarts
+        bool exq = exb2;
+        if (a.ex_one) exq = lane == fi ? ex_has(exh, ex_ovf, gex, curl) : false;   // only the chosen neighbour
+        if (__shfl_sync(FULL, exq, fi)) break;   // Q9: moving onto an expanded node restarts
       }
       if (a.prof) p_walk += clock64() - tk0;
       if (stop) break;

@@ -37,7 +37,7 @@ def main():
     if cfg.metric != D.JAC:
         Q = torch.from_numpy(Q).cuda()
     ref = None
-    knobs = ("KNNG_NPROD", "KNNG_STAGES", "KNNG_LANE_EVAL", "KNNG_RING", "KNNG_SMEM_BITS", "KNNG_LEAN", "KNNG_WALK_PREFETCH")
+    knobs = ("KNNG_NPROD", "KNNG_STAGES", "KNNG_LANE_EVAL", "KNNG_RING", "KNNG_SMEM_BITS", "KNNG_LEAN", "KNNG_WALK_PREFETCH", "KNNG_EX_ONE", "KNNG_WIN_PREFETCH")
     for s in args.settings.split("/"):
         for kn in knobs:
             os.environ.pop(kn, None)
