@@ -165,23 +165,20 @@ struct WarpTopK {
   int32_t id;
   int cnt, kr;
   uint32_t key_at0;   // warp-uniform copy of the best key (valid when cnt > 0)
-  __device__ __forceinline__ void init(int kr_) { key = 0; id = -1; cnt = 0; kr = kr_; key_at0 = 0; }
-  __device__ __forceinline__ uint32_t best() const { return __shfl_sync(FULL, key, 0); }
-  // may an entry with key ck enter (some id)?  Lane-local view of the warp-uniform worst key: the
-  // worst entry's key is read by a shuffle, so every lane must call this together.
-  __device__ __forceinline__ bool could_take(uint32_t ck) const {
-    const uint32_t wk = __shfl_sync(FULL, key, (kr - 1) & 31);
-    return cnt < kr || !closer<M>(wk, ck);
+  uint32_t wk_u;      // warp-uniform copy of the worst entry (valid when cnt == kr)
+  int32_t wi_u;
+  __device__ __forceinline__ void init(int kr_) {
+    key = 0; id = -1; cnt = 0; kr = kr_; key_at0 = 0; wk_u = 0; wi_u = -1;
   }
+  __device__ __forceinline__ uint32_t best() const { return __shfl_sync(FULL, key, 0); }
+  // may an entry with key ck enter (some id)?  (lane-local; uses the cached worst entry)
+  __device__ __forceinline__ bool could_take(uint32_t ck) const { return cnt < kr || !closer<M>(wk_u, ck); }
   // insert every lane with flag set (distinct ids assumed)
   __device__ __forceinline__ void insert(bool flag, uint32_t ck, int32_t cid) {
     const int lane = threadIdx.x & 31;
-    if (cnt == kr) {   // pre-filter against the current worst entry (conservative)
-      const uint32_t wk = __shfl_sync(FULL, key, kr - 1);
-      const int32_t wi = __shfl_sync(FULL, id, kr - 1);
-      flag = flag && precedes<M>(ck, cid, wk, wi);
-    }
+    if (cnt == kr) flag = flag && precedes<M>(ck, cid, wk_u, wi_u);   // pre-filter against the worst entry
     unsigned m = __ballot_sync(FULL, flag);
+    if (!m) return;
     while (m) {
       const int src = __ffs(m) - 1;
       m &= m - 1;
@@ -196,6 +193,10 @@ struct WarpTopK {
       if (lane == pos) { key = k2; id = i2; }
       if (cnt < kr) ++cnt;
       if (pos == 0) key_at0 = k2;
+    }
+    if (cnt == kr) {
+      wk_u = __shfl_sync(FULL, key, (kr - 1) & 31);
+      wi_u = __shfl_sync(FULL, id, (kr - 1) & 31);
     }
   }
 };
