@@ -209,17 +209,34 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
   const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
   const bool prof = a.prof != nullptr;
   long long p_wait = 0, p_work = 0;
+  // compile-time widths: LR lanes per row, each copying chunks sl, sl + LR, ... of its row (immediate
+  // offsets), 32 / LR rows per pass -- one shuffle and NCH / LR copies per pass
+  constexpr int LR = EV::NCH >= 8 && EV::NCH % 8 == 0 ? 8 : (EV::NCH > 0 && EV::NCH <= 8 ? EV::NCH : 0);
   auto issue = [&](int st, int2 d) {
     x.meta[(st * 32 + lane) * 4] = d.y;   // published: the pool index
     uint8_t *dst = x.stg + st * 32 * x.pitch;
-    int r = r0, cc = c0;
+    if constexpr (LR > 0 && (32 % LR) == 0) {
+      constexpr int RPP = 32 / LR, CPR = EV::NCH / LR;
+      const int sl = lane % LR, rr = lane / LR;
+#pragma unroll
+      for (int p = 0; p < LR; ++p) {
+        const int r = p * RPP + rr;
+        const int32_t id = __shfl_sync(FULL, d.x, r);
+        const uint8_t *src = base + (size_t)id * stride + sl * 16;
+        uint8_t *drow = dst + r * x.pitch + sl * 16;
+#pragma unroll
+        for (int t = 0; t < CPR; ++t) cp_async16(drow + t * LR * 16, src + t * LR * 16);
+      }
+    } else {
+      int r = r0, cc = c0;
 #pragma unroll 8
-    for (int j = 0; j < nck; ++j) {
-      const int32_t id = __shfl_sync(FULL, d.x, r);
-      cp_async16(dst + r * x.pitch + cc * 16, base + (size_t)id * stride + (size_t)cc * 16);
-      cc += cs;
-      r += rs;
-      if (cc >= nck) { cc -= nck; ++r; }
+      for (int j = 0; j < nck; ++j) {
+        const int32_t id = __shfl_sync(FULL, d.x, r);
+        cp_async16(dst + r * x.pitch + cc * 16, base + (size_t)id * stride + (size_t)cc * 16);
+        cc += cs;
+        r += rs;
+        if (cc >= nck) { cc -= nck; ++r; }
+      }
     }
   };
 #pragma unroll
