@@ -92,6 +92,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def q_factor(n, n_a, k, correct_fraction):
+    """The paper's graph-quality factor: e_m = n_a k + n k n_a/(n_a+n),
+    e_u = (n+n_a) k - e_m, Q = (e_c - e_u)/e_m, with the correct-edge count e_c estimated as
+    correct_fraction x (n+n_a) k.  None without inserts."""
+    if not n_a:
+        return None
+    e_m = n_a * k + n * k * n_a / (n_a + n)
+    e_u = (n + n_a) * k - e_m
+    return (correct_fraction * (n + n_a) * k - e_u) / e_m
+
+
 def alg_bytes(st, V, k):
     """per committed search evaluation V + 4 B, per expanded node 4k B."""
     return st["search_evals"] * (V + 4) + st["search_expansions"] * 4 * k
@@ -327,9 +338,7 @@ def run_ours(args, cfg):
     hit = np.array([len(set(a.tolist()) & set(b.tolist())) / cfg.k for a, b in zip(got, exact)])
     rec = float(hit[:len(samp_new)].mean()) if len(samp_new) else None
     cef = float(hit[len(samp_new):].mean())
-    e_m = pos * cfg.k + cfg.n0 * cfg.k * pos / (pos + cfg.n0) if pos else 0.0
-    e_u = ntot * cfg.k - e_m
-    Q = (cef * ntot * cfg.k - e_u) / e_m if e_m > 0 else None
+    Q = q_factor(cfg.n0, pos, cfg.k, cef)
     g.close()
 
     # ---------------- end to end through the C ABI with host buffers (e2e) ----------------
