@@ -299,7 +299,7 @@ struct VecQuery {
   static constexpr int VPP = 32 / L;
   // passes whose loads are in flight together: up to 8 x 16 B per lane, 16 for wide vectors (one
   // vector per pass, L = 32) so that a 32-candidate chunk needs 2 round trips, not 4
-  static constexpr int LIM = (L == 32 && CPL == 1) ? 16 : 8;
+  static constexpr int LIM = (L == 32 && CPL == 1) ? 16 : (M == M_U8 && CPL == 1 ? 4 : 8);
   static constexpr int GRP = (L < (LIM / CPL) ? L : ((LIM / CPL) > 0 ? (LIM / CPL) : 1));
   uint4 q[CPL];
 
