@@ -466,7 +466,7 @@ struct VecQuery {
 constexpr int QMAX = 256;
 template <int L>
 struct SetQuery {
-  static constexpr int SU = 2;
+  static constexpr int SU = 1;
   const uint32_t *q;
   const uint32_t *bm;    // vocabulary bitmap of the query (shared) or null
   int qn;
