@@ -20,7 +20,7 @@
 
 namespace knng {
 
-constexpr int FASTC = 4;          // chunks the consumer's skip-only fast path commits at once (<= ring)
+constexpr int FASTC = 2;          // chunks the consumer's skip-only fast path commits at once (<= ring)
 constexpr int HDR_BYTES = 128;
 
 struct RingHdr {
