@@ -303,7 +303,7 @@ static int check_params(const knng_params *p) {
 // the register limit), then spends what shared memory is left on the visited bitmaps and a deeper
 // ring.  Knobs KNNG_STAGES / KNNG_NPROD / KNNG_LANE_EVAL / KNNG_RING / KNNG_SMEM_BITS override it
 // (measurement only).
-static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
+static void plan_k1(SearchArgs &a, bool sets, bool u8, int64_t tasks, int64_t mmax) {
   int nsm = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -313,8 +313,11 @@ static void plan_k1(SearchArgs &a, bool sets, int64_t tasks, int64_t mmax) {
   a.stages = 2;
   // (a.stages is fixed at 2: deeper producer pipelines measured slower everywhere)
   if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
-  a.lean = 0;                                      // (the 80-register variant measured slower)
-  const int cap = 8;                               // two-warp CTAs per SM the registers allow
+  // the 96-register variant (10 CTAs/SM) pays for many latency-bound u8 tasks (C3: +6%); with <= 8
+  // CTAs' worth of tasks (C1) or for sets (C4) the 128-register form is faster (measured)
+  a.lean = (u8 && tasks > (int64_t)nsm * 8) ? 1 : 0;
+  if (const char *e = getenv("KNNG_LEAN")) a.lean = atoi(e) != 0;
+  const int cap = a.lean ? 10 : 8;                 // two-warp CTAs per SM the registers allow
   const int need = (int)std::min<int64_t>(cap, (tasks + nsm - 1) / nsm);
   auto occ = [&](const SearchArgs &x) {
     const size_t sm = search_smem_bytes(x, sets) + 1024;
@@ -403,7 +406,7 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   }
   a.task_ctr = a.stats + 14;
   a.pitch = g->metric == KNNG_JACCARD_U32SET ? 16 * 16 + 16 : (int)g->geom.stride + 16;
-  plan_k1(a, g->metric == KNNG_JACCARD_U32SET, nq * pc, mmax);
+  plan_k1(a, g->metric == KNNG_JACCARD_U32SET, g->metric == KNNG_L2SQ_U8, nq * pc, mmax);
   CK(g->w_bits.ensure((size_t)a.gslots * a.bits_words * 4));
   a.gbits = g->w_bits.as<uint32_t>();
   cudaError_t e = launch_search(g->geom, a, g->stream, nl);

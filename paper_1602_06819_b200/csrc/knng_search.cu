@@ -408,7 +408,7 @@ __device__ __forceinline__ void produce_any(const SearchArgs &a, const SetQuery<
 // two-warp CTAs per SM); MB = 12 caps a two-warp CTA at 80 registers (12 per SM, some spills) for
 // latency-bound task mixes that want more concurrent walks.
 template <int M, int L, int CPL, int MB>
-__global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a) {
+__global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a) {   // MB 4: <= 128 regs; 10: <= 96
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nprod = (blockDim.x >> 5) - 1;
@@ -902,10 +902,15 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   X(M_F32, 1, 1) X(M_F32, 1, 2) X(M_F32, 1, 3) X(M_F32, 1, 4) X(M_F32, 2, 3) X(M_F32, 2, 4) X(M_F32, 4, 3) \
   X(M_F32, 4, 4) X(M_F32, 8, 3) X(M_F32, 8, 4) X(M_F32, 32, 2) X(M_F32, 32, 4)
 
+// the 96-register variant (10 two-warp CTAs per SM) for the u8 d=128 and Jaccard shapes (C1, C3, C4)
+#define LEAN_OK(MM, LL, CC) (((MM) == M_U8 && (LL) == 8 && (CC) == 1) || (MM) == M_JAC)
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch) {
   if (n_launch) ++*n_launch;
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, 4>(a, s);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) {                                         \
+    if (LEAN_OK(MM, LL, CC) && a.lean && !a.starts && a.nprod == 1) return run_search<MM, LL, CC, 10>(a, s); \
+    return run_search<MM, LL, CC, 4>(a, s);                                                  \
+  }
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
