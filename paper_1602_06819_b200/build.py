@@ -28,6 +28,8 @@ def build(force=False, verbose=False):
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    if os.environ.get("KNNG_BUILD_PROFILE"):   # K1 cycle counters (KNNG_PROFILE=1 at run time)
+        cflags.append("-DKNNG_PROFILE_COUNTERS")
     jobs = []
     for src in SRC:
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".%d.o" % os.getpid())

@@ -18,6 +18,14 @@
 #include "knng_common.cuh"
 #include "knng_internal.h"
 
+// Cycle counters of KNNG_PROFILE=1 exist only in builds with -DKNNG_PROFILE_COUNTERS (their state
+// costs the consumer registers): KP(p) is false at compile time otherwise.
+#ifdef KNNG_PROFILE_COUNTERS
+#define KP(p) ((p) != nullptr)
+#else
+#define KP(p) false
+#endif
+
 namespace knng {
 
 constexpr int FASTC = 2;          // chunks the consumer's skip-only fast path commits at once (<= ring)
@@ -207,7 +215,7 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
   const size_t stride = a.st.stride;
   const int r0 = lane / nck, c0 = lane % nck, rs = 32 / nck, cs = 32 % nck;
   const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
-  const bool prof = a.prof != nullptr;
+  const bool prof = KP(a.prof);
   long long p_wait = 0, p_work = 0;
   // compile-time widths: LR lanes per row, each copying chunks sl, sl + LR, ... of its row (immediate
   // offsets), 32 / LR rows per pass -- one shuffle and NCH / LR copies per pass
@@ -316,7 +324,7 @@ __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<
   const uint32_t *tok = a.st.tok;
   const uint64_t *off = a.st.off;
   const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
-  const bool prof = a.prof != nullptr;
+  const bool prof = KP(a.prof);
   long long p_wait = 0, p_work = 0;
   auto issue = [&](int st, int2 d, uint64_t b, uint64_t e) {
     const uint64_t a0 = b & ~3ull;
@@ -530,7 +538,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
     bool thr_ok = false;
     int wpos = 32;
 
-    const long long tc0 = a.prof ? clock64() : 0;
+    const long long tc0 = KP(a.prof) ? clock64() : 0;
     long long p_wait = 0, p_walk = 0, p_win = 0;
     int ex_cnt = 0;
     bool ex_ovf = false;
@@ -543,12 +551,12 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
         // skipped, exactly as the sequential loop would do draw by draw; the budget is not reached.
         const int64_t ch0 = jbase / 32;
         if (top.cnt > 0 && nprod > 0 && ch0 + FASTC <= nch && c + 32 * FASTC <= budget) {
-          const long long tw = a.prof ? clock64() : 0;
+          const long long tw = KP(a.prof) ? clock64() : 0;
           int32_t fnode[FASTC];
           uint32_t fkey[FASTC];
 #pragma unroll
           for (int t = 0; t < FASTC; ++t) ring_get(ring, a.ring, hdr, ch0 + t, fnode[t], fkey[t]);
-          if (a.prof) p_wait += clock64() - tw;
+          if (KP(a.prof)) p_wait += clock64() - tw;
           if (!thr_ok || thr_key != top.key_at0) {
             thr.set(top.key_at0, a.e_num, a.e_den);
             thr_key = top.key_at0;
@@ -595,7 +603,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
         const int64_t j = jbase + lane;
         const int64_t ch = jbase / 32;
         if (ch < nch && nprod > 0) {                 // produced ahead into the ring
-          const long long tw = a.prof ? clock64() : 0;
+          const long long tw = KP(a.prof) ? clock64() : 0;
           uint32_t kk;
           int32_t pidx;
           ring_get(ring, a.ring, hdr, ch, pidx, kk);
@@ -603,7 +611,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
           wl = (uint32_t)pidx;
           wnode = pool ? -2 : pidx;                   // -2: valid, node id not looked up yet
           wvalid = true;
-          if (a.prof) p_wait += clock64() - tw;
+          if (KP(a.prof)) p_wait += clock64() - tw;
           ++p_win;
           whave = true;
           __syncwarp();
@@ -738,7 +746,7 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
       wpos = al + 1;
 
       // ------------------- hill climbing, eager first improvement -------------------
-      const long long tk0 = a.prof ? clock64() : 0;
+      const long long tk0 = KP(a.prof) ? clock64() : 0;
       int32_t cur = __shfl_sync(FULL, wnode, al);
       uint32_t kcur = __shfl_sync(FULL, wkey, al);
       uint32_t curl = __shfl_sync(FULL, wl, al);
@@ -801,10 +809,10 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
         if (a.ex_one) exq = lane == fi ? ex_has(exh, ex_ovf, gex, curl) : false;   // only the chosen neighbour
         if (__shfl_sync(FULL, exq, fi)) break;   // Q9: moving onto an expanded node restarts
       }
-      if (a.prof) p_walk += clock64() - tk0;
+      if (KP(a.prof)) p_walk += clock64() - tk0;
       if (stop) break;
     }
-    if (a.prof && lane == 0) {
+    if (KP(a.prof) && lane == 0) {
       atomicAdd(a.prof + 0, (unsigned long long)(clock64() - tc0));
       if (a.task_cycles) a.task_cycles[task] = (unsigned long long)(clock64() - tc0);
       atomicAdd(a.prof + 1, (unsigned long long)p_wait);
@@ -908,7 +916,8 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
   if (n_launch) ++*n_launch;
 #define X(MM, LL, CC) \
   if (g.metric == MM && g.L == LL && g.CPL == CC) {                                         \
-    if (LEAN_OK(MM, LL, CC) && a.lean && !a.starts && a.nprod == 1) return run_search<MM, LL, CC, 10>(a, s); \
+    if constexpr (LEAN_OK(MM, LL, CC))                                                       \
+      if (a.lean && !a.starts && a.nprod == 1) return run_search<MM, LL, CC, 10>(a, s);      \
     return run_search<MM, LL, CC, 4>(a, s);                                                  \
   }
   KNNG_SHAPES(X, M_U8)
