@@ -527,6 +527,9 @@ static int stage_update(knng_graph *g, const knng_params *p, int world, const in
   ba.hcap = hcap;
   ba.list = g->w_list.as<int32_t>();
   ba.ballmax = (int)ballmax;
+  // small balls (depth 2, k <= 16: <= 4 KB of hash + list per warp) keep their sets in shared memory
+  ba.smem_ball = (size_t)4 * (hcap + ballmax) * 4 <= 24 * 1024 ? 1 : 0;
+  if (const char *e = getenv("KNNG_SMEM_BALL")) ba.smem_ball = atoi(e) != 0 && ba.smem_ball;
   ba.props = props;
   ba.prop_cnt = prop_cnt;
   ba.stats = g->w_stats.as<unsigned long long>();

@@ -82,6 +82,7 @@ struct BallArgs {
   int hcap;
   int32_t *list;               // per warp slot, ballmax entries
   int ballmax;
+  int smem_ball;               // 1: hash + list in shared memory (small balls), else the global slots
   int2 *props;                 // [B][ballmax] (node, key)
   int32_t *prop_cnt;           // [B]
   unsigned long long *stats;   // [4] ball nodes [5] proposals

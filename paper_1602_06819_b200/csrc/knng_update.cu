@@ -74,10 +74,11 @@ template <int M, int L, int CPL>
 __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
   __shared__ int s_n[4];
   __shared__ uint32_t qscr[M == M_JAC ? 4 * QMAX : 1];
+  extern __shared__ int32_t bsm[];   // small balls: [4][hcap] hash + [4][ballmax] list in shared memory
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * 4 + wib, nw = (int64_t)gridDim.x * 4;
-  int32_t *hash = a.hash + gw * a.hcap;
-  int32_t *list = a.list + gw * a.ballmax;
+  int32_t *hash = a.smem_ball ? bsm + wib * a.hcap : a.hash + gw * a.hcap;
+  int32_t *list = a.smem_ball ? bsm + 4 * a.hcap + wib * a.ballmax : a.list + gw * a.ballmax;
   const int k = a.k;
   unsigned long long s_ball = 0, s_prop = 0;
   for (int64_t bl = gw; bl < a.nqb; bl += nw) {
@@ -145,7 +146,8 @@ template <int M, int L, int CPL>
 static cudaError_t run_ball(const BallArgs &a, int64_t nslots, cudaStream_t s) {
   if (a.nqb == 0) return cudaSuccess;
   const int64_t blocks = nslots / 4;
-  k_ball<M, L, CPL><<<(unsigned)blocks, 128, 0, s>>>(a);
+  const size_t smem = a.smem_ball ? (size_t)4 * (a.hcap + a.ballmax) * 4 : 0;
+  k_ball<M, L, CPL><<<(unsigned)blocks, 128, smem, s>>>(a);
   return cudaGetLastError();
 }
 
