@@ -550,7 +550,7 @@ struct SetQuery {
   __device__ __forceinline__ uint32_t eval_slot(const uint8_t *slot, int rb, int re) const {
     const int nch = (re + 3) >> 2;
     int inter = 0;
-#pragma unroll 4
+#pragma unroll 1
     for (int i = 0; i < nch; ++i) {
       const uint4 t = *(const uint4 *)(slot + 16 * i);
       const int c0 = 4 * i;
