@@ -63,7 +63,8 @@ typedef enum {
 
 /* A set of points.  Vectors: data = u8[n*dim] or f32[n*dim], row-major.
  * Sets: data = uint32 tokens (each set sorted ascending, no duplicates), offsets = uint64[n+1]
- * (set i is data[offsets[i] .. offsets[i+1])), dim ignored; sets hold <= 65535 tokens.
+ * (set i is data[offsets[i] .. offsets[i+1])), dim ignored; sets hold <= 32767 tokens (the key packs
+ * the union |A u B| <= 65534 into 16 bits; longer sets fail with INVALID_ARG, host or device input).
  * data_on_device = 1: data (and offsets) are device pointers on the handle's GPU. */
 typedef struct {
   int32_t metric;

@@ -107,6 +107,17 @@ __global__ void k_token_max(const uint32_t *tok, int64_t n, unsigned *out) {
   if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
+// longest set of a device CSR batch (sets must hold <= KNNG_SET_MAX tokens: the key packs the union
+// |A u B| <= 2 * KNNG_SET_MAX into 16 bits)
+__global__ void k_max_set_len(const uint64_t *off, int64_t n, unsigned long long *out) {
+  unsigned long long m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)(off[i + 1] - off[i]));
+  for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+static constexpr uint64_t KNNG_SET_MAX = 32767;
+
 __global__ void k_rebase_offsets(const uint64_t *in, int64_t n, uint64_t base, uint64_t *out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i <= n) out[i] = base + (in[i] - in[0]);
@@ -118,14 +129,23 @@ static int append_sets(knng_graph *g, const knng_points *p, uint64_t **off_dst_b
                        int64_t *tok_cap, int64_t row0, int64_t tok0, int64_t *ntok_out, uint32_t *tok_max = nullptr) {
   uint64_t first = 0, last = 0;
   if (p->data_on_device) {
+    unsigned long long *dm = nullptr, mlen = 0;
+    CK(cudaMallocAsync((void **)&dm, 8, g->stream));
+    CK(cudaMemsetAsync(dm, 0, 8, g->stream));
+    if (p->n > 0) k_max_set_len<<<(unsigned)std::min<int64_t>((p->n + 255) / 256, 1024), 256, 0, g->stream>>>(p->offsets, p->n, dm);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&mlen, dm, 8, cudaMemcpyDeviceToHost, g->stream));
     CK(cudaMemcpyAsync(&first, p->offsets, 8, cudaMemcpyDeviceToHost, g->stream));
     CK(cudaMemcpyAsync(&last, p->offsets + p->n, 8, cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaFreeAsync(dm, g->stream));
     CK(cudaStreamSynchronize(g->stream));
+    if (mlen > KNNG_SET_MAX) return fail(KNNG_ERR_INVALID_ARG, "set longer than %llu tokens", (unsigned long long)KNNG_SET_MAX);
   } else {
     first = p->offsets[0];
     last = p->offsets[p->n];
     for (int64_t i = 0; i < p->n; ++i)
-      if (p->offsets[i + 1] - p->offsets[i] > 65535) return fail(KNNG_ERR_INVALID_ARG, "set longer than 65535");
+      if (p->offsets[i + 1] - p->offsets[i] > KNNG_SET_MAX)
+        return fail(KNNG_ERR_INVALID_ARG, "set longer than %llu tokens", (unsigned long long)KNNG_SET_MAX);
   }
   const int64_t nt = (int64_t)(last - first);
   if (tok0 + nt > *tok_cap) {
@@ -198,6 +218,8 @@ static void free_graph(knng_graph *g) {
                 &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts,
                 &g->w_qoff, &g->w_qtok, &g->w_tprof};
   for (DBuf *b : ws) b->release();
+  g->w_dense.part.release();
+  g->w_dense.norm.release();
   for (auto &e : g->ev)
     if (e) cudaEventDestroy(e);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
@@ -280,7 +302,7 @@ int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_g
       cudaMemsetAsync(g->nfill, 0, cap * 4, g->stream) != cudaSuccess)
     return bail(fail(KNNG_ERR_CUDA, "graph_init: memset failed"));
   if ((r = store_points(g, pts, 0))) return bail(r);
-  cudaError_t e = launch_exact_build(g->geom, graph_store_view(g), g->n, k, g->ids, g->keys, g->stream);
+  cudaError_t e = launch_exact_build(g->geom, graph_store_view(g), g->n, k, g->ids, g->keys, &g->w_dense, g->stream);
   if (e != cudaSuccess) return bail(fail(KNNG_ERR_CUDA, "exact build launch: %s", cudaGetErrorString(e)));
   e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return bail(fail(KNNG_ERR_CUDA, "exact build: %s", cudaGetErrorString(e)));
@@ -466,6 +488,7 @@ static int stage_search(knng_graph *g, const knng_points *pts, const knng_params
   if (q_lo < 0) q_hi = B, q_lo = 0;          // all queries
   if (q_hi > B || q_lo > q_hi) return fail(KNNG_ERR_INVALID_ARG, "bad query range");
   g->pend_B = B;
+  g->pend_parts = part_hi - part_lo;
   if (B == 0) return 0;
   // A1: batch ingest into the store tail (ids n_t .. n_t+B-1)
   if (int r = store_points(g, pts, n_t)) return r;
@@ -487,6 +510,9 @@ static int stage_update(knng_graph *g, const knng_params *p, int world, const in
   uint32_t *Ck = (uint32_t *)ck_all;
   if (g->P > 0) {
     if (g->P % world) return fail(KNNG_ERR_INVALID_ARG, "P=%d not divisible by world=%d", g->P, world);
+    if (g->pend_parts * world != g->P)   // the gathered candidates must cover every partition
+      return fail(KNNG_ERR_INVALID_ARG, "stage_update: %d ranks x %d searched partitions != P=%d", world, g->pend_parts,
+                  g->P);
     CK(g->w_C_i.ensure((size_t)B * k * 4));
     CK(g->w_C_k.ensure((size_t)B * k * 4));
     Ci = g->w_C_i.as<int32_t>();
@@ -500,7 +526,7 @@ static int stage_update(knng_graph *g, const knng_params *p, int world, const in
   int32_t *oi = new_ids ? new_ids : g->ids + (size_t)(n_t + q_lo) * k;
   uint32_t *ok = new_keys ? new_keys : g->keys + (size_t)(n_t + q_lo) * k;
   CK(launch_allpairs(g->geom, sv, n_t, B, q_lo, q_hi - q_lo, k, Ci + (size_t)q_lo * k, Ck + (size_t)q_lo * k, oi, ok,
-                     g->stream));
+                     &g->w_dense, g->stream));
   ++*nl;
   if (timed) CK(cudaEventRecord(g->ev[2], g->stream));
   // A6: update balls of queries [q_lo, q_hi) over the snapshot -> proposals
@@ -712,8 +738,7 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
     int64_t qcap = (int64_t)(g->w_qtok.bytes / 4), ntok = 0;
     uint64_t *qo = g->w_qoff.as<uint64_t>();
     if (int r = append_sets(g, q, &qo, &qt, &qcap, 0, 0, &ntok)) return r;
-    if (qt != g->w_qtok.p) {   // append_sets reallocated the token buffer
-      g->w_qtok.release();
+    if (qt != g->w_qtok.p) {   // append_sets reallocated the token buffer (and freed the old one)
       g->w_qtok.p = qt;
       g->w_qtok.bytes = (size_t)qcap * 4;
     }

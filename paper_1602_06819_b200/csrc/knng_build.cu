@@ -111,12 +111,9 @@ __global__ void k_merge_partials(int64_t nrows, int k, int ny, const int32_t *se
   }
 }
 
-static void *g_part_buf = nullptr;     // column-split partials (grown on demand, per process)
-static size_t g_part_bytes = 0;
-
 cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
                              int64_t ncols, int k, const int32_t *seed_ids, const uint32_t *seed_keys, int32_t *out_ids,
-                             uint32_t *out_keys, cudaStream_t s) {
+                             uint32_t *out_keys, DenseScratch *ws, cudaStream_t s) {
   if (nrows <= 0) return cudaSuccess;
   // u8 rows: the tcgen05 kind::i8 form (knng_tc.cu); two column halves per split, merged below
   const char *tce = getenv("KNNG_TC");
@@ -125,17 +122,12 @@ cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0,
   if ((tc_u8 || tc_f32) && !(tce && atoi(tce) == 0)) {
     const int64_t bx = (nrows + 127) / 128, tn = tc_u8 ? 256 : 64;
     int64_t ny = bx >= 148 ? 1 : std::min<int64_t>((148 + bx - 1) / bx, std::max<int64_t>(1, (ncols + tn - 1) / tn));
-    const size_t need = (size_t)2 * ny * nrows * k * 8;
-    if (need > g_part_bytes) {
-      if (g_part_buf) cudaFree(g_part_buf);
-      cudaError_t e = cudaMalloc(&g_part_buf, need);
-      if (e != cudaSuccess) { g_part_buf = nullptr; g_part_bytes = 0; return e; }
-      g_part_bytes = need;
-    }
-    int32_t *pi = (int32_t *)g_part_buf;
-    uint32_t *pk = (uint32_t *)((char *)g_part_buf + (size_t)2 * ny * nrows * k * 4);
-    cudaError_t e = tc_u8 ? launch_tc_topk_u8(g, vec, row0, nrows, col0, ncols, k, seed_ids, seed_keys, ny, pi, pk, s)
-                          : launch_tc_topk_f32(g, vec, row0, nrows, col0, ncols, k, seed_ids, seed_keys, ny, pi, pk, s);
+    if (cudaError_t e = ws->part.ensure((size_t)2 * ny * nrows * k * 8)) return e;
+    int32_t *pi = (int32_t *)ws->part.p;
+    uint32_t *pk = (uint32_t *)((char *)ws->part.p + (size_t)2 * ny * nrows * k * 4);
+    cudaError_t e =
+        tc_u8 ? launch_tc_topk_u8(g, vec, row0, nrows, col0, ncols, k, seed_ids, seed_keys, ny, pi, pk, &ws->norm, s)
+              : launch_tc_topk_f32(g, vec, row0, nrows, col0, ncols, k, seed_ids, seed_keys, ny, pi, pk, &ws->norm, s);
     if (e != cudaSuccess) return e;
     if (tc_u8)
       k_merge_partials<M_U8><<<(unsigned)((nrows + 3) / 4), 128, 0, s>>>(nrows, k, (int)(2 * ny), seed_ids, seed_keys,
@@ -155,15 +147,9 @@ cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0,
   int32_t *pi = out_ids;
   uint32_t *pk = out_keys;
   if (ny > 1) {
-    const size_t need = (size_t)ny * nrows * k * 8;
-    if (need > g_part_bytes) {
-      if (g_part_buf) cudaFree(g_part_buf);
-      cudaError_t e = cudaMalloc(&g_part_buf, need);
-      if (e != cudaSuccess) { g_part_buf = nullptr; g_part_bytes = 0; return e; }
-      g_part_bytes = need;
-    }
-    pi = (int32_t *)g_part_buf;
-    pk = (uint32_t *)((char *)g_part_buf + (size_t)ny * nrows * k * 4);
+    if (cudaError_t e = ws->part.ensure((size_t)ny * nrows * k * 8)) return e;
+    pi = (int32_t *)ws->part.p;
+    pk = (uint32_t *)((char *)ws->part.p + (size_t)ny * nrows * k * 4);
   }
   const dim3 grid((unsigned)bx, (unsigned)ny);
   cudaError_t e;
@@ -208,12 +194,12 @@ __global__ void __launch_bounds__(128) k_exact_build_sets(StoreView st, int64_t 
 }
 
 cudaError_t launch_exact_build(const VecGeom &g, const StoreView &st, int64_t n, int k, int32_t *ids, uint32_t *keys,
-                               cudaStream_t s) {
+                               DenseScratch *ws, cudaStream_t s) {
   if (g.metric == M_JAC) {
     k_exact_build_sets<<<(unsigned)((n + 3) / 4), 128, 0, s>>>(st, n, k, ids, keys);
     return cudaGetLastError();
   }
-  return launch_tile_topk(g, st.vec, 0, n, 0, n, k, nullptr, nullptr, ids, keys, s);
+  return launch_tile_topk(g, st.vec, 0, n, 0, n, k, nullptr, nullptr, ids, keys, ws, s);
 }
 
 }  // namespace knng

@@ -48,6 +48,7 @@ struct knng_graph {
   int metric = 0, dim = 0, k = 0;
   int64_t n = 0, cap = 0;
   int64_t pend_B = 0;                           // batch ingested by stage_search, not yet committed
+  int pend_parts = 0;                           // partitions stage_search searched for the pending batch
   knng::VecGeom geom{};
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -74,6 +75,7 @@ struct knng_graph {
   DBuf w_bits, w_cand_i, w_cand_k, w_C_i, w_C_k, w_hash, w_list, w_props, w_prop_cnt, w_sorted, w_stats,
       w_target, w_query, w_starts;
   DBuf w_qoff, w_qtok;
+  knng::DenseScratch w_dense;                    // A0 / A5 partial rows and norms
   DBuf w_tprof;                                 // KNNG_PROFILE: per-task consumer cycles of the last search
   cudaEvent_t ev[6] = {};
 };

@@ -8,6 +8,31 @@
 
 namespace knng {
 
+// Device scratch owned by a graph handle (never process-global: a handle is bound to one device and
+// one stream, and two handles may be used from two threads).  Grown on demand.
+struct Scratch {
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+// scratch of the dense exact steps (A0 build, A5 all-pairs): column-split partial rows and norms
+struct DenseScratch {
+  Scratch part, norm;
+};
+
 // Vector store geometry: rows of `stride` bytes (= nchunks * 16, zero padded).
 struct VecGeom {
   int metric;
@@ -94,7 +119,8 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
 cudaError_t launch_merge_parts(int metric, const int32_t *cand_ids, const uint32_t *cand_keys, int64_t nq,
                                int P, int world, int kr, int32_t *out_ids, uint32_t *out_keys, cudaStream_t s);
 cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int64_t q_lo, int64_t nq,
-                            int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi, uint32_t *ok, cudaStream_t s);
+                            int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi, uint32_t *ok, DenseScratch *ws,
+                            cudaStream_t s);
 cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cudaStream_t s);
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
@@ -107,12 +133,12 @@ cudaError_t launch_lrows(const int32_t *ids, int k, int64_t first, int64_t count
 cudaError_t exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t *tmp, int64_t n, cudaStream_t s);
 cudaError_t launch_tc_topk_u8(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
                               int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
-                              uint32_t *pk, cudaStream_t s);
+                              uint32_t *pk, Scratch *norm, cudaStream_t s);
 cudaError_t launch_tc_topk_f32(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
                                int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
-                               uint32_t *pk, cudaStream_t s);
+                               uint32_t *pk, Scratch *norm, cudaStream_t s);
 cudaError_t launch_exact_build(const VecGeom &g, const StoreView &st, int64_t n, int k, int32_t *ids,
-                               uint32_t *keys, cudaStream_t s);
+                               uint32_t *keys, DenseScratch *ws, cudaStream_t s);
 cudaError_t launch_place(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int P,
                          const int32_t *medoids, int32_t *members, int64_t member_cap, int64_t *member_cnt,
                          uint8_t *part_of, int32_t *local_idx, int32_t *target_tmp, cudaStream_t s);

@@ -137,6 +137,7 @@ __device__ __forceinline__ void ex_insert(int32_t *exh, int &cnt, bool &ovf, uin
   if (!ovf && cnt >= EXCAP * 3 / 4) {
     for (int64_t w = lane; w < words; w += 32) gex[w] = 0;
     __threadfence_block();
+    __syncwarp();      // every lane's zeroing lands before lane 0 sets the first bit
     ovf = true;
   }
   if (ovf) {

@@ -558,26 +558,14 @@ static cudaError_t run_tc_f32(const uint8_t *vec, size_t stride, int nchunks, in
   return cudaGetLastError();
 }
 
-static uint32_t *g_norm_buf = nullptr;
-static size_t g_norm_bytes = 0;
-
-static float *g_fnorm_buf = nullptr;
-static size_t g_fnorm_bytes = 0;
-
 // tcgen05 (3xTF32 screen + exact canonical rerank) form of launch_tile_topk for fp32 rows
 // (nchunks <= 24, k <= 32): partial rows per column split and half into pi/pk ([2 ny][nrows][k]).
 cudaError_t launch_tc_topk_f32(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
                                int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
-                               uint32_t *pk, cudaStream_t s) {
+                               uint32_t *pk, Scratch *norm, cudaStream_t s) {
   if (g.metric != M_F32 || g.nchunks > 24 || k > 32) return cudaErrorNotSupported;
-  const size_t need = (size_t)(nrows + ncols) * 8;
-  if (need > g_fnorm_bytes) {
-    if (g_fnorm_buf) cudaFree(g_fnorm_buf);
-    cudaError_t e = cudaMalloc((void **)&g_fnorm_buf, need);
-    if (e != cudaSuccess) { g_fnorm_buf = nullptr; g_fnorm_bytes = 0; return e; }
-    g_fnorm_bytes = need;
-  }
-  float *nr = g_fnorm_buf, *rr = nr + nrows, *ncn = rr + nrows, *rcn = ncn + ncols;
+  if (cudaError_t e = norm->ensure((size_t)(nrows + ncols) * 8)) return e;
+  float *nr = (float *)norm->p, *rr = nr + nrows, *ncn = rr + nrows, *rcn = ncn + ncols;
   k_norms_f32<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(vec, g.stride, g.nchunks, row0, nrows, nr, rr);
   k_norms_f32<<<(unsigned)((ncols + 255) / 256), 256, 0, s>>>(vec, g.stride, g.nchunks, col0, ncols, ncn, rcn);
   if (k <= 10)
@@ -592,16 +580,10 @@ cudaError_t launch_tc_topk_f32(const VecGeom &g, const uint8_t *vec, int64_t row
 // not covered.
 cudaError_t launch_tc_topk_u8(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
                               int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,
-                              uint32_t *pk, cudaStream_t s) {
+                              uint32_t *pk, Scratch *norm, cudaStream_t s) {
   if (g.metric != M_U8 || g.nchunks > 16 || k > 32) return cudaErrorNotSupported;
-  const size_t need = (size_t)(nrows + ncols) * 4;
-  if (need > g_norm_bytes) {
-    if (g_norm_buf) cudaFree(g_norm_buf);
-    cudaError_t e = cudaMalloc((void **)&g_norm_buf, need);
-    if (e != cudaSuccess) { g_norm_buf = nullptr; g_norm_bytes = 0; return e; }
-    g_norm_bytes = need;
-  }
-  uint32_t *nr = g_norm_buf, *ncn = g_norm_buf + nrows;
+  if (cudaError_t e = norm->ensure((size_t)(nrows + ncols) * 4)) return e;
+  uint32_t *nr = (uint32_t *)norm->p, *ncn = nr + nrows;
   k_norms_u8<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(vec, g.stride, g.nchunks, row0, nrows, nr);
   k_norms_u8<<<(unsigned)((ncols + 255) / 256), 256, 0, s>>>(vec, g.stride, g.nchunks, col0, ncols, ncn);
   if (k <= 10) return run_tc<10>(vec, g.stride, g.nchunks, row0, nrows, col0, ncols, k, nr, ncn, sid, skey, ny, pi, pk, s);

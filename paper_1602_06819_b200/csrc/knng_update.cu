@@ -41,15 +41,16 @@ __global__ void __launch_bounds__(128) k_allpairs(StoreView st, int64_t n_t, int
 
 cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
                              int64_t ncols, int k, const int32_t *seed_ids, const uint32_t *seed_keys, int32_t *out_ids,
-                             uint32_t *out_keys, cudaStream_t s);
+                             uint32_t *out_keys, DenseScratch *ws, cudaStream_t s);
 
 // A5: new rows of batch queries [q_lo, q_lo+nq): top-k(C_i u {(D(x_i, x_j), n_t+j) : j != i}).
 // Ci/Ck and the outputs are indexed by the local row (query - q_lo).
 cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int64_t q_lo, int64_t nq,
-                            int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi, uint32_t *ok, cudaStream_t s) {
+                            int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi, uint32_t *ok, DenseScratch *ws,
+                            cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   if (g.metric != M_JAC)   // vectors: the smem-tiled kernel of the exact build, seeded with C_i
-    return launch_tile_topk(g, st.vec, n_t + q_lo, nq, n_t, B, k, Ci, Ck, oi, ok, s);
+    return launch_tile_topk(g, st.vec, n_t + q_lo, nq, n_t, B, k, Ci, Ck, oi, ok, ws, s);
   k_allpairs<M_JAC><<<(unsigned)((nq + 3) / 4), 128, 0, s>>>(st, n_t, B, q_lo, nq, k, Ci, Ck, oi, ok);
   return cudaGetLastError();
 }

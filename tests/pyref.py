@@ -1,0 +1,242 @@
+"""Plain-Python re-derivations of the paper's procedures, used ONLY as pins of the C oracle.
+
+Nothing here imports oracle/ or the CUDA package: every function is written from the paper (and the
+readings of DESIGN.md) in exact arithmetic -- Python ints and Fractions, no floating point in any
+decision -- so that a dropped term, a wrong sign or a transposed operand in the oracle fails a test.
+
+  * mulhi RNG (reading Q4): the SplitMix64 finaliser chain, restated from Steele, Lea & Flood (2014).
+  * iGNNS (section 3) LITERALLY: no "restart when moving onto an expanded node" shortcut
+    (reading Q9) -- a walk that reaches an expanded node re-scans its row on cached keys.
+  * Alg. 4 with the sampled-candidate medoid update of reading Q22 and the
+    acceptance rule of Q23, every score compared as an exact fraction.
+"""
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+
+import numpy as np
+
+M64 = (1 << 64) - 1
+GOLDEN = 0x9E3779B97F4A7C15
+U8, F32, JAC = 0, 1, 2
+
+
+def mix64(z):
+    z &= M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def rng_hash(seed, pid, part, draw):
+    h = mix64((seed + GOLDEN) & M64)
+    h = mix64(h ^ ((pid + 2 * GOLDEN) & M64))
+    h = mix64(h ^ ((part + 3 * GOLDEN) & M64))
+    return mix64(h ^ ((draw + 4 * GOLDEN) & M64))
+
+
+def rng_draw(seed, pid, part, draw, m):
+    """index = floor(h * m / 2^64) (reading Q4)."""
+    return (rng_hash(seed, pid, part, draw) * m) >> 64
+
+
+# ---------------------------------------------------------------------------
+# Exact metric values.  L2: D as an exact integer / Fraction (inputs are integer-valued, so the
+# fp32 canonical sum of the oracle is exact too); Jaccard: (inter, union).
+# ---------------------------------------------------------------------------
+def metric_value(metric, a, b):
+    if metric == JAC:
+        sa, sb = set(int(x) for x in a), set(int(x) for x in b)
+        i = len(sa & sb)
+        return (i, len(sa) + len(sb) - i)
+    d = [Fraction(float(x)) - Fraction(float(y)) for x, y in zip(a, b)]
+    return sum(x * x for x in d)
+
+
+def similarity(metric, v):
+    """s = 1/(1+D) for L2 metrics (reading Q1), i/u for Jaccard."""
+    if metric == JAC:
+        i, u = v
+        return Fraction(i, u) if u else Fraction(0)
+    return Fraction(1) / (1 + v)
+
+
+def closer(metric, a, b):
+    """a strictly more similar than b (metric value only)."""
+    return similarity(metric, a) > similarity(metric, b)
+
+
+def sort_key(metric, v, node):
+    """Edge order: more similar first, equal similarity -> smaller id."""
+    return (-similarity(metric, v), node)
+
+
+def packed_key(metric, v):
+    """The library / oracle key format of a metric value."""
+    if metric == JAC:
+        return (v[0] << 16) | v[1]
+    if metric == U8:
+        return int(v)
+    return int(np.float32(float(v)).view(np.uint32))
+
+
+def skip(metric, v_r, v_best, e_num, e_den):
+    """discard a restart r when s_r < s_max / e (strict), e = num/den, den = 0 -> never."""
+    if e_den == 0:
+        return False
+    return similarity(metric, v_r) < similarity(metric, v_best) * Fraction(e_den, e_num)
+
+
+def budget(m, kr, speedup):
+    """P:89 + reading Q6: max(min(k, |pool|), floor(|pool| / speedup))."""
+    return max(min(kr, m), math.floor(m / speedup))
+
+
+# ---------------------------------------------------------------------------
+# iGNNS, literally
+# ---------------------------------------------------------------------------
+def ignns_literal(metric, point, rows, q, kr, speedup, e_num, e_den, seed, pid, pool=None, part=0, starts=None):
+    """Returns (ids, packed keys, stats) of the top-kr evaluated nodes.
+
+    point(i) -> the stored point i; rows[i] -> node i's neighbour ids (stored order, -1 padded);
+    pool = sorted node ids of the searched partition (None: all nodes 0..len(rows)-1)."""
+    pool = list(range(len(rows))) if pool is None else list(pool)
+    inpool = set(pool)
+    m = len(pool)
+    b = budget(m, kr, speedup)
+    val = {}                    # evaluated node -> metric value (the search cache)
+    c = 0                       # similarities computed
+    j = 0                       # draw counter
+    st = dict(evals=0, starts=0, skipped=0)
+    first = True
+
+    def best():
+        return min(val, key=lambda u: sort_key(metric, val[u], u))
+
+    while True:
+        if c == b or c == m:                       # budget; whole pool evaluated (Q7)
+            break
+        while True:                                # random restart; redraws are free (Q4)
+            if starts is not None:
+                if j >= len(starts):
+                    return _finish(metric, val, kr, st, c)
+                r = starts[j]
+            else:
+                r = pool[rng_draw(seed, pid, part, j, m)]
+            j += 1
+            if r not in val:
+                break
+        vb = val[best()] if val else None          # s_max before r
+        val[r] = metric_value(metric, q, point(r))
+        c += 1
+        st["starts"] += 1
+        if not first and vb is not None and skip(metric, val[r], vb, e_num, e_den):
+            st["skipped"] += 1                     # the skipped start stays in the result (Q5)
+            continue
+        first = False
+        cur = r
+        while True:                                # hill climbing, eager first improvement
+            moved = False
+            for v in rows[cur]:
+                v = int(v)
+                if v < 0 or v not in inpool:       # edges leaving the pool are skipped (Q10)
+                    continue
+                if v not in val:
+                    if c == b:                     # the over-budget evaluation is not performed
+                        return _finish(metric, val, kr, st, c)
+                    val[v] = metric_value(metric, q, point(v))
+                    c += 1
+                if closer(metric, val[v], val[cur]):
+                    cur = v
+                    moved = True
+                    break
+            if not moved:                          # local maximum -> restart
+                break
+    return _finish(metric, val, kr, st, c)
+
+
+def _finish(metric, val, kr, st, c):
+    st["evals"] = c
+    order = sorted(val, key=lambda u: sort_key(metric, val[u], u))[:kr]
+    return [int(u) for u in order], [packed_key(metric, val[u]) for u in order], st
+
+
+# ---------------------------------------------------------------------------
+# Alg. 4: balanced k-medoids, readings Q21-Q23
+# ---------------------------------------------------------------------------
+def _hop_sum(c, members, adj):
+    dist = {c: 0}
+    fr = [c]
+    while fr:
+        nf = []
+        for u in fr:
+            for w in adj[u]:
+                if w not in dist:
+                    dist[w] = dist[u] + 1
+                    nf.append(w)
+        fr = nf
+    return sum(dist.get(u, len(members)) for u in members)
+
+
+def kmedoids(metric, point, rows, P, imbalance, max_iter, seed, exact_limit=4096, ncand=64, init=None):
+    """Returns (part, medoids, costs of the kept iterations)."""
+    n = len(rows)
+    cap = math.ceil(n * imbalance / P)
+    if init is not None:
+        med = [int(x) for x in init]
+    else:
+        med, jd = [], 0
+        while len(med) < P:                        # P distinct seeded draws (Alg. 4 line 1)
+            cnd = rng_draw(seed, 0xFFFFFFFF, 0, jd, n)
+            jd += 1
+            if cnd not in med:
+                med.append(cnd)
+    part_out, costs, prev = None, [], None
+    for it in range(max_iter):
+        # assign: ascending id, eligible clusters only, score s(m, u) * (1 - |C|/cap)
+        size = [0] * P
+        part = [0] * n
+        for u in range(n):
+            best, bscore = None, None
+            for p in range(P):
+                if size[p] >= cap:
+                    continue
+                sc = similarity(metric, metric_value(metric, point(u), point(med[p]))) * Fraction(cap - size[p], cap)
+                if best is None or sc > bscore or (sc == bscore and (size[p], med[p]) < (size[best], med[best])):
+                    best, bscore = p, sc
+            part[u] = best
+            size[best] += 1
+        # update: member minimising the hop sum in the cluster-induced undirected view (Q29)
+        newmed, cost = [], 0
+        for p in range(P):
+            members = [u for u in range(n) if part[u] == p]
+            if not members:
+                newmed.append(med[p])
+                continue
+            ms = set(members)
+            adj = {u: set() for u in members}
+            for u in members:
+                for v in rows[u]:
+                    v = int(v)
+                    if v in ms:
+                        adj[u].add(v)
+                        adj[v].add(u)
+            if len(members) <= exact_limit:
+                cands = members
+            else:                                  # Q22: current medoid + ncand - 1 seeded draws
+                cands = ([med[p]] if med[p] in ms else []) + [
+                    members[rng_draw(seed, 0xFFFFFFFE, it * P + p, j, len(members))] for j in range(ncand - 1)]
+            bs, bc = min((_hop_sum(c, members, adj), c) for c in cands)   # ties -> smaller id
+            newmed.append(bc)
+            cost += bs
+        if it > 0 and cost > prev:                 # Q23: an iteration that raises the cost is not kept
+            break
+        part_out = part
+        costs.append(cost)
+        prev = cost
+        changed = newmed != med
+        med = newmed
+        if not changed:
+            break
+    return part_out, med, costs

@@ -1,0 +1,128 @@
+"""Pins of the oracle's remaining open branches (round 2), against tests/pyref.py.
+
+* iGNNS without the Q9 shortcut: the oracle restarts when a walk moves onto an already expanded
+  node (reading Q9, "result-equivalent").  tests/pyref.py walks literally (keep moving to
+  the first improving neighbour, re-scanning expanded rows on cached keys).  Results and the
+  evals / starts / skipped counters must agree on random u8, f32 and Jaccard graphs, partitioned and
+  not, for speedups 1.5..10 and e in {6/5, 1, 5, inf}.
+* Alg. 4 with the sampled-candidate medoid update (reading Q22) -- exact_limit lowered so every
+  cluster takes the sampled branch -- and with the exact branch, all three metrics, including the
+  fp32 assign comparator, against an exact-fraction re-derivation.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import pyref as R
+
+
+def _points(metric, rng, n, dim=4):
+    if metric == O.U8:
+        return rng.integers(0, 40, size=(n, dim)).astype(np.uint8)
+    if metric == O.F32:   # integer-valued fp32 (|x| <= 6): every canonical-order sum is exact
+        return rng.integers(-6, 7, size=(n, dim)).astype(np.float32)
+    out = []
+    for _ in range(n):
+        L = int(rng.integers(2, 8))
+        out.append(np.sort(rng.choice(25, size=L, replace=False)).astype(np.uint32))
+    return out
+
+
+def _graph(metric, n, k, seed):
+    rng = np.random.default_rng(seed)
+    X = _points(metric, rng, n)
+    g = O.OracleGraph(metric, X, k=k)
+    g.init_exact(2)
+    return g, rng
+
+
+@pytest.mark.parametrize("metric", [O.U8, O.F32, O.JAC])
+def test_ignns_equals_literal_walk_without_q9_shortcut(metric):
+    g, rng = _graph(metric, 260, 6, 1100 + metric)
+    rows = g.ids[:g.n]
+    moved_onto_expanded = 0
+    for qi in range(60):
+        q = _points(metric, rng, 1)[0]
+        sp = float(rng.choice([1.5, 2.0, 3.0, 5.0, 10.0]))
+        e_num, e_den = [(6, 5), (1, 1), (5, 1), (1, 0)][qi % 4]
+        ids, keys, st = g.ignns(q, 6, sp, e_num, e_den, seed=11, pid=qi)
+        rid, rkey, rst = R.ignns_literal(metric, g.point, rows, q, 6, sp, e_num, e_den, 11, qi)
+        assert ids.tolist() == rid and keys.tolist() == rkey, (qi, ids, rid)
+        assert (st["evals"], st["starts"], st["skipped"]) == (rst["evals"], rst["starts"], rst["skipped"])
+        # the literal walk expands at least as many rows (it re-scans expanded ones)
+        moved_onto_expanded += st["expansions"] < _literal_expansions(metric, g, rows, q, sp, e_num, e_den, qi)
+    assert moved_onto_expanded > 0   # the shortcut branch was really exercised
+
+
+def _literal_expansions(metric, g, rows, q, sp, e_num, e_den, qi):
+    """Count row scans of the literal walk (instrumented copy of the pyref walk's expansions)."""
+    count = [0]
+    orig = rows
+
+    class Rows:
+        def __len__(self):
+            return len(orig)
+
+        def __getitem__(self, i):
+            count[0] += 1
+            return orig[i]
+    R.ignns_literal(metric, g.point, Rows(), q, 6, sp, e_num, e_den, 11, qi)
+    return count[0]
+
+
+@pytest.mark.parametrize("metric", [O.U8, O.JAC])
+def test_partitioned_ignns_equals_literal_walk(metric):
+    g, rng = _graph(metric, 240, 5, 1200 + metric)
+    part, med, _ = g.partition_kmedoids(4, 1.05, 3, 2)
+    g.set_partition(part, med)
+    rows = g.ids[:g.n]
+    for qi in range(24):
+        q = _points(metric, rng, 1)[0]
+        p = qi % 4
+        pool = np.nonzero(part == p)[0].astype(np.int32)
+        ids, keys, st = g.ignns(q, 5, 2.5, 6, 5, seed=5, pid=qi, part=p, pool=pool)
+        rid, rkey, rst = R.ignns_literal(metric, g.point, rows, q, 5, 2.5, 6, 5, 5, qi, pool=pool.tolist(), part=p)
+        assert ids.tolist()[:len(rid)] == rid and keys.tolist()[:len(rkey)] == rkey
+        assert (st["evals"], st["starts"], st["skipped"]) == (rst["evals"], rst["starts"], rst["skipped"])
+
+
+def test_injected_starts_literal_walk():
+    """W3-style injected starts on a random graph (the start_override hook of graph_search)."""
+    g, rng = _graph(O.U8, 120, 4, 1300)
+    rows = g.ids[:g.n]
+    for qi in range(20):
+        q = _points(O.U8, rng, 1)[0]
+        starts = rng.integers(0, g.n, size=12).tolist()
+        ids, keys, st = g.ignns(q, 4, 3.0, 6, 5, seed=0, pid=0, starts=starts)
+        rid, rkey, rst = R.ignns_literal(O.U8, g.point, rows, q, 4, 3.0, 6, 5, 0, 0, starts=starts)
+        assert ids.tolist()[:len(rid)] == rid and keys.tolist()[:len(rkey)] == rkey
+        assert st["evals"] == rst["evals"] and st["skipped"] == rst["skipped"]
+
+
+@pytest.mark.parametrize("metric", [O.U8, O.F32, O.JAC])
+@pytest.mark.parametrize("exact_limit", [4096, 25])
+def test_kmedoids_equals_exact_fraction_rederivation(metric, exact_limit):
+    """exact_limit = 25 < every cluster: the Q22 sampled-candidate update on every cluster."""
+    g, _ = _graph(metric, 200, 4, 1400 + metric)
+    rows = g.ids[:g.n]
+    for P, imb, seed in ((2, 1.0, 3), (4, 1.1, 9), (5, 1.05, 21)):
+        part, med, cost = g.partition_kmedoids(P, imb, 6, seed, exact_limit=exact_limit, ncand=8)
+        rpart, rmed, rcost = R.kmedoids(metric, g.point, rows, P, imb, 6, seed, exact_limit=exact_limit, ncand=8)
+        assert part.tolist() == rpart
+        assert med.tolist() == rmed
+        assert cost.tolist() == rcost
+
+
+def test_kmedoids_f32_assign_uses_the_capacity_weight():
+    """fp32 assign: score = s(m,u) (1 - |C|/cap), s = 1/(1+D), compared exactly.
+    1-D points, medoids x=0 (A) and x=10 (B), cap = ceil(8 * 1.5 / 2) = 6.  Hand trace, ascending id:
+    x=0,1,2,-1,-2 -> A (A's sizes 0..4); x=10 -> B; x=4 (id 6): D_A = 16, D_B = 36, so the raw
+    similarity prefers A, but score_A = 1/17 * 1/6 = 0.0098 < score_B = 1/37 * 5/6 = 0.0225 -> B;
+    x=11 -> B.  A comparator with a dropped or transposed weight puts id 6 in A."""
+    X = np.array([[0], [1], [2], [-1], [-2], [10], [4], [11]], np.float32)
+    g = O.OracleGraph(O.F32, X, k=2)
+    g.init_exact(1)
+    part, med, cost = g.partition_kmedoids(2, 1.5, 1, 0, init_medoids=[0, 5])
+    assert part.tolist() == [0, 0, 0, 0, 0, 1, 1, 1]
+    rpart, rmed, rcost = R.kmedoids(O.F32, g.point, g.ids[:g.n], 2, 1.5, 1, 0, init=[0, 5])
+    assert rpart == part.tolist() and rmed == med.tolist() and rcost == cost.tolist()
