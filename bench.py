@@ -1,11 +1,16 @@
 #!/usr/bin/env python
-"""bench.py -- online inserts/s of the B200 path on BASELINE.json configs[1] (C1).
+"""bench.py -- online inserts/s of the B200 path on BASELINE.json configs[3] (C3) at G = 1.
 
-A step = one graph_insert_batch of B = 1024 points (search -> all-pairs -> update balls ->
-merge: every row of SURVEY.md 8(a) on the unpartitioned path) on the evolving graph, inputs
-already resident in HBM.  L2 is flushed (256 MiB write) between timed steps, outside the
-timed events.  Multi-GPU (torchrun): C1 is unpartitioned, so ranks run replicas (weak scaling,
-DESIGN.md "Multi-GPU").  --impl reference times the CPU oracle (the reference arm of this tier).
+C3 is the partitioned configuration the metric names ("... at 1/2/4/8 B200; gather GB/s vs HBM
+peak"): 8,000,000 uint8 d=128 points, exact initial graph (A0) and Alg. 4 partition into P = 8
+(A9) as untimed setup, then batches of 8,192 inserts from the configured 1M-insert stream.  A step
+= one graph_insert_batch (search over all 8 partitions -> merge -> all-pairs -> update balls ->
+ordered merge -> placement: every row of SURVEY.md 8(a)), inputs already resident in HBM.  L2 is
+flushed (256 MiB write) between timed steps, outside the timed events.  `e2e` continues the same
+stream through the C ABI from pinned host buffers.  Multi-GPU (torchrun): the P partition searches
+of each batch are sharded over the ranks (strong scaling).
+--impl reference times the CPU oracle (the reference arm of this tier).  --config C0..C4 gives the
+other configs' lines.
 """
 import argparse
 import json
@@ -22,7 +27,7 @@ sys.path.insert(0, ROOT)
 
 import datagen as D  # noqa: E402
 
-CFG_NAME = "C1"
+CFG_NAME = "C3"
 
 
 def baseline_metric():
@@ -108,37 +113,65 @@ def alg_bytes(st, V, k):
     return st["search_evals"] * (V + 4) + st["search_expansions"] * 4 * k
 
 
-def run_cpu_baseline(cfg, X, S, rows, budget_s=12.0, nthreads=None):
-    """The oracle as it stands, on host cores: insert whole batches of the same workload.
-    Its starting graph is the exact initial graph (rows copied in: building it on the CPU takes
-    minutes and is not the timed work)."""
+def cpu_model():
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_cpu_baseline(cfg, X, S, rows, part=None, budget_s=12.0, nthreads=None):
+    """The oracle as it stands, on host cores: whole batches of the same workload, starting from the
+    state the GPU's timed steps start from (the GPU-built exact initial graph -- sample-verified
+    against the oracle in tests/test_gpu_fullsize.py -- and, when partitioned, its Alg. 4 partition:
+    the oracle cannot build an 8M exact graph in bounded time).  At least one batch; then whole
+    batches while under budget_s."""
     from oracle import oracle as O
     nthreads = nthreads or os.cpu_count() or 1
     o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cfg.n0 + len(S) + 8)
     o.set_rows(*rows)
+    if part is not None:
+        o.set_partition(*part)
     done, t_tot = 0, 0.0
-    while t_tot < budget_s and done + cfg.batch <= len(S):
+    while (done == 0 or t_tot < budget_s) and done + cfg.batch <= len(S):
         t0 = time.perf_counter()
         o.insert_batch(S[done:done + cfg.batch], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed,
                        nthreads)
         t_tot += time.perf_counter() - t0
         done += cfg.batch
-    return {"value": done / t_tot, "unit": "inserts/s", "cores": nthreads, "kind": "oracle",
-            "sample": "%d inserts (%d batches of %d) of %s on the exact initial graph, %.1f s" % (
-                done, done // cfg.batch, cfg.batch, cfg.name, t_tot)}
+    return {"value": done / t_tot, "unit": "inserts/s", "cores": nthreads, "cpu_model": cpu_model(), "kind": "oracle",
+            "sample": "%d inserts (%d batches of %d) of %s: the first batches of the same stream from the same initial "
+                      "state (GPU-built exact graph%s), %.1f s" % (
+                          done, done // cfg.batch, cfg.batch, cfg.name,
+                          " + its Alg. 4 partition" if part is not None else "", t_tot)}
+
+
+REF_N0 = {"C3": 100_000, "C4": 60_000, "C2": 60_000}
 
 
 def run_reference(args, cfg):
+    """The reference arm of this tier: the CPU oracle, as it stands, on all host cores.  Its exact
+    initial graph is O(n^2) on the CPU (hours at C2/C3/C4's n0), so on those configs it runs the same
+    recipe at the n0 of REF_N0 (stated in config.workload); C0/C1 run at full size."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     from oracle import oracle as O
     nthreads = os.cpu_count() or 1
+    full_n0 = cfg.n0
+    if not args.n0 and cfg.name in REF_N0:
+        cfg = cfg.with_sizes(n0=REF_N0[cfg.name])
     X = D.initial_points(cfg)
     S = D.stream_points(cfg, 0, (args.warmup + args.steps) * cfg.batch)
     o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cfg.n0 + len(S) + 8)
     t0 = time.perf_counter()
     o.init_exact(nthreads)
+    if cfg.P:
+        part, med, _ = o.partition_kmedoids(cfg.P, cfg.imbalance, args.kmedoids_iters, cfg.part_seed)
+        o.set_partition(part, med)
     t_init = time.perf_counter() - t0
     pos = 0
     for _ in range(args.warmup):
@@ -150,13 +183,17 @@ def run_reference(args, cfg):
         pos += cfg.batch
     t = time.perf_counter() - t0
     val = args.steps * cfg.batch / t
+    note = "" if cfg.n0 == full_n0 else (
+        " (reduced from n0=%d: the oracle's exact initial graph is O(n^2) on the CPU)" % full_n0)
     line = {"impl": "reference", "metric": baseline_metric(), "value": val, "unit": "inserts/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_name(cfg), "data": "synthetic",
-            "config": {"workload": cfg_desc(cfg), "global_batch": cfg.batch},
-            "cpu_baseline": {"value": val, "unit": "inserts/s", "cores": nthreads, "kind": "oracle",
-                             "sample": "%d timed batches of %d inserts (oracle exact init %.0f s untimed)" % (
-                                 args.steps, cfg.batch, t_init)},
+            "config": {"workload": cfg_desc(cfg) + note, "global_batch": cfg.batch},
+            "cpu_baseline": {"value": val, "unit": "inserts/s", "cores": nthreads, "cpu_model": cpu_model(),
+                             "kind": "oracle",
+                             "sample": "%d timed batches of %d inserts after %d warm-up batches (oracle exact init%s "
+                                       "%.0f s, untimed)" % (args.steps, cfg.batch, args.warmup,
+                                                             " + Alg. 4" if cfg.P else "", t_init)},
             "e2e": {"value": val, "unit": "inserts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -198,14 +235,20 @@ def run_ours(args, cfg):
             dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
         else:
             dist.init_process_group(backend)
-    B = cfg.batch                      # per-rank batch; the global batch of a step is ws * B points
-    GB = ws * B
+    # Partitioned configs (C3, C4) shard the P partition searches of ONE batch over the ranks (Alg. 3):
+    # the global batch is the config's batch at every N (strong scaling).  Unpartitioned configs shard
+    # the queries of N batches (weak scaling).
+    GB = cfg.batch if cfg.P else ws * cfg.batch
     nsteps = args.warmup + args.steps
     X = D.initial_points(cfg)
-    S = D.stream_points(cfg, 0, max(cfg.n_insert, nsteps * GB))
+    n_stream = 2 * nsteps * GB                      # device-input steps, then the e2e steps
+    if n_stream > cfg.n_insert:
+        print("note: %d inserts requested, the %s stream has %d; the e2e steps continue past it" % (
+            n_stream, cfg.name, cfg.n_insert), file=sys.stderr)
+    S = D.stream_points(cfg, 0, n_stream)
     V = point_bytes(cfg, S)
     stream = torch.cuda.Stream()
-    cap = cfg.n0 + nsteps * GB + 8
+    cap = cfg.n0 + n_stream + 8
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     comm = None
     if ws > 1:
@@ -218,13 +261,13 @@ def run_ours(args, cfg):
             dist.barrier()
 
     def step(graph, pts):
-        """One global batch: 1 GPU -> graph_insert_batch; N GPUs -> the batch's queries sharded over the
-        ranks (replicated graph), stage_search / all-gather / stage_update / all-gather / stage_commit."""
+        """One global batch: 1 GPU -> graph_insert_batch; N GPUs -> stage_search / all-gather /
+        stage_update / all-gather / stage_commit (partitions or queries sharded over the ranks)."""
         if ws == 1:
             return graph.insert_batch(pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)[1]
         with torch.cuda.stream(stream):
             st = insert_batch_staged([graph], [rank], ws, pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth,
-                                     cfg.search_seed, 0, allgather=comm.allgather)[0]
+                                     cfg.search_seed, cfg.P, allgather=comm.allgather)[0]
         out = {f: st["search"][f] + st["update"][f] + st["commit"][f]
                for f in ("search_evals", "search_starts", "search_skipped", "search_expansions", "ball_nodes",
                          "proposals", "kernel_launches")}
@@ -234,17 +277,15 @@ def run_ours(args, cfg):
         out["ms_merge"] = st["commit"]["ms_total"]
         return out
 
-    # ---------------- device-resident inputs (value) ----------------
-    def new_graph():
-        gg = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
-        if cfg.P:     # Alg. 4 partitioning (setup, untimed)
-            gg.partition_kmedoids(cfg.P, cfg.imbalance, args.kmedoids_iters, cfg.part_seed)
-        return gg
-
+    # ---------------- setup (untimed): exact initial graph (A0) + Alg. 4 partition (A9) ----------------
     t_setup = time.perf_counter()
-    g = new_graph()
+    g = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
+    part0 = None
+    if cfg.P:
+        part0 = g.partition_kmedoids(cfg.P, cfg.imbalance, args.kmedoids_iters, cfg.part_seed)[:2]
     t_setup = time.perf_counter() - t_setup
-    rows0 = g.rows() if (rank == 0 and ws == 1 and not args.no_cpu_baseline and not cfg.P) else None
+    want_cpu = rank == 0 and ws == 1 and not args.no_cpu_baseline
+    rows0 = g.rows() if want_cpu else None          # the state the timed steps start from
     if cfg.metric == D.JAC:     # sets stay in host CSR: the library copies each batch in (H2D inside the step)
         S_dev = S[:nsteps * GB]
     else:
@@ -269,13 +310,14 @@ def run_ours(args, cfg):
             stats.append(st)
             pos += GB
     barrier()
+    del S_dev
     t_total = sum(ms_steps) / 1000.0
     if ws > 1:
         t = torch.tensor([t_total], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_total = float(t.item())
     value = args.steps * GB / t_total
-    evals = sum(s["search_evals"] + s["ball_nodes"] for s in stats) * ws
+    evals = sum(s["search_evals"] + s["ball_nodes"] for s in stats) * (1 if cfg.P else ws)
     ms_search = sum(s["ms_search"] for s in stats)
     bytes_search = sum(alg_bytes(s, V, cfg.k) for s in stats)
     peak, peak_src = hbm_peak()
@@ -301,35 +343,63 @@ def run_ours(args, cfg):
             bf16 = 1652.5
         dpeak = 2 * bf16 if cfg.metric == D.U8 else bf16 / 2     # int8 = 2x bf16 (dense), tf32 = 1/2 bf16
         dense = {"kernel": "k_tc_topk_u8 (tcgen05 kind::i8) + partial merge" if cfg.metric == D.U8 else
-                 "k_tile_topk (SIMT fp32, canonical order)", "achieved": ops / (ms_ap / 1000) / 1e12,
+                 "k_tc_topk_f32 (tcgen05 kind::tf32 screen + exact rerank)", "achieved": ops / (ms_ap / 1000) / 1e12,
                  "peak": dpeak, "unit": "TOP/s", "frac": ops / (ms_ap / 1000) / 1e12 / dpeak,
                  "peak_source": "MEASURED_PEAKS.json bf16_tflops x nominal dtype ratio",
                  "note": "B x B exact all-pairs of the batch with top-k epilogue; tiny per step, latency-bound"}
 
-    # graph quality on seeded samples (exact k-nn of the final point set: torch brute force for vectors,
-    # the library's own search in exact mode -- speedup 1, budget = pool, parity-tested equal to linear
-    # search -- for sets):  recall@k of the inserted points' rows, the fraction of correct edges over
-    # all nodes, and the paper's Q estimated from it
+    # ---------------- end to end through the C ABI with host buffers (e2e) ----------------
+    # the same graph continues the stream: each step copies its batch from pinned host memory (H2D)
+    # and reads the stats back (D2H) inside the timed region
+    if cfg.metric == D.JAC:
+        S_pin = S[pos:pos + nsteps * GB]
+    else:
+        S_pin = torch.from_numpy(S[pos:pos + nsteps * GB]).pin_memory().numpy()
+    p2 = 0
+    for _ in range(args.warmup):
+        step(g, S_pin[p2:p2 + GB])
+        p2 += GB
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(g, S_pin[p2:p2 + GB])
+        p2 += GB
+    barrier()
+    t_e2e = time.perf_counter() - t0
+    pos += p2
+    if ws > 1:
+        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+
+    # ---------------- graph quality on seeded samples ----------------
+    # exact k-nn of the final point set (torch brute force for vectors; the library's own search in exact
+    # mode -- speedup 1, budget = pool, parity-tested equal to linear search -- for sets): recall@k of the
+    # inserted points' rows, the fraction of correct edges over all nodes, and the paper's Q
     ntot = cfg.n0 + pos
     rs = np.random.default_rng(4000 + int(cfg.name[1:]))
     samp_new = cfg.n0 + np.sort(rs.choice(pos, min(pos, 256), replace=False)) if pos else np.zeros(0, np.int64)
     samp_all = np.sort(rs.choice(ntot, min(ntot, 256), replace=False))
     nodes = np.concatenate([samp_new, samp_all]).astype(np.int64)
     if cfg.metric != D.JAC:
-        allp = torch.from_numpy(np.concatenate([X, S[:pos]])).to("cuda").float()
         nq = torch.from_numpy(nodes).cuda()
-        q = allp[nq]
+        pts = [X, S[:pos]]
+        q = torch.from_numpy(np.concatenate(pts)[nodes]).cuda().float()
         bd = torch.full((len(nodes), cfg.k), float("inf"), device="cuda")
         bi = torch.zeros((len(nodes), cfg.k), dtype=torch.int64, device="cuda")
-        for i in range(0, len(allp), 1 << 20):      # running top-k over column chunks
-            d2 = torch.cdist(q, allp[i:i + (1 << 20)]).pow(2)
-            cols = torch.arange(i, i + d2.shape[1], device="cuda")
-            d2[nq[:, None] == cols[None, :]] = float("inf")
-            vd, vi = torch.topk(d2, min(cfg.k, d2.shape[1]), largest=False)
-            bd, sel = torch.topk(torch.cat([bd, vd], 1), cfg.k, largest=False)
-            bi = torch.gather(torch.cat([bi, vi + i], 1), 1, sel)
+        off = 0
+        for part_ in pts:
+            for i in range(0, len(part_), 1 << 20):      # running top-k over column chunks
+                blk = torch.from_numpy(part_[i:i + (1 << 20)]).cuda().float()
+                d2 = torch.cdist(q, blk).pow(2)
+                cols = torch.arange(off + i, off + i + d2.shape[1], device="cuda")
+                d2[nq[:, None] == cols[None, :]] = float("inf")
+                vd, vi = torch.topk(d2, min(cfg.k, d2.shape[1]), largest=False)
+                bd, sel = torch.topk(torch.cat([bd, vd], 1), cfg.k, largest=False)
+                bi = torch.gather(torch.cat([bi, vi + off + i], 1), 1, sel)
+            off += len(part_)
         exact = bi.cpu().numpy()
-        del allp, d2
+        del d2, blk
     else:
         qs = [X[i] if i < cfg.n0 else S[i - cfg.n0] for i in nodes]
         ex_ids, _, _ = g.search(qs, cfg.k + 1, 1.0, cfg.e_num, cfg.e_den, cfg.search_seed)
@@ -341,50 +411,31 @@ def run_ours(args, cfg):
     Q = q_factor(cfg.n0, pos, cfg.k, cef)
     g.close()
 
-    # ---------------- end to end through the C ABI with host buffers (e2e) ----------------
-    g2 = new_graph()
-    if cfg.metric == D.JAC:
-        S_pin = S[:nsteps * GB]
-    else:
-        S_pin_t = torch.from_numpy(S[:nsteps * GB]).pin_memory()
-        S_pin = S_pin_t.numpy()
-    pos2 = 0
-    for _ in range(args.warmup):
-        step(g2, S_pin[pos2:pos2 + GB])
-        pos2 += GB
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step(g2, S_pin[pos2:pos2 + GB])
-        pos2 += GB
-    barrier()
-    t_e2e = time.perf_counter() - t0
-    if ws > 1:
-        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_e2e = float(t.item())
-    g2.close()
-
     line = {
         "metric": baseline_metric(), "value": value, "unit": "inserts/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": dtype_name(cfg), "data": "synthetic",
+        "scaling": "strong" if cfg.P else "weak", "vs_baseline": None, "dtype": dtype_name(cfg), "data": "synthetic",
         "config": {"workload": cfg_desc(cfg), "global_batch": GB, "setup_s": t_setup,
-                   "parallelism": "1 GPU" if ws == 1 else
-                   "dp%d: replicated graph, the global batch's queries sharded over ranks, NCCL all-gathers of "
-                   "candidates and proposals" % ws,
+                   "timed_inserts": "%d..%d of the %d-insert stream" % (args.warmup * GB, nsteps * GB, cfg.n_insert),
+                   "parallelism": "1 GPU" if ws == 1 else (
+                       "%d ranks: replicated graph, the P=%d partition searches of each batch sharded over the ranks "
+                       "(Alg. 3), NCCL all-gathers of candidates and proposals" % (ws, cfg.P) if cfg.P else
+                       "dp%d: replicated graph, the global batch's queries sharded over ranks, NCCL all-gathers of "
+                       "candidates and proposals" % ws),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "similarities_per_s": evals / t_total,
         "recall_at_k": rec,
         "quality": {"correct_edge_fraction": cef, "Q": Q, "n": cfg.n0, "n_a": pos,
                     "samples": "%d inserted + %d uniform nodes (seeded), exact k-nn of the final point set" % (
                         len(samp_new), len(samp_all))},
-        "search_per_query": {f: sum(s_[f] for s_ in stats) / (len(stats) * B) for f in
+        "search_per_query": {f: sum(s_[f] for s_ in stats) / (len(stats) * GB) for f in
                              ("search_evals", "search_starts", "search_skipped", "search_expansions", "ball_nodes",
                               "proposals")},
         "roofline": {"bound": "hbm", "kernel": "k_search (K1 iGNNS)", "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": bytes_search / len(stats),
+                     "alg_bytes_model": "SURVEY 8(d): (V + 4) B per committed search evaluation + 4k B per expanded "
+                                        "node; V = %d" % V,
                      "ms_per_launch": ms_search / len(stats),
                      "note": ("store + rows fit in L2 (126 MB): the HBM fraction is not the binding claim"
                               if cap * (V + 8 * cfg.k) < 100e6 else "HBM-resident store")},
@@ -396,9 +447,9 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if rows0 is not None:
-        S_cpu = D.stream_points(cfg, 0, 48 * B)      # enough whole batches for ~10 s of oracle work
-        line["cpu_baseline"] = run_cpu_baseline(cfg, X, S_cpu, rows0)
+    if want_cpu:
+        S_cpu = D.stream_points(cfg, 0, max(8, 64 // max(1, cfg.batch // 1024)) * cfg.batch)
+        line["cpu_baseline"] = run_cpu_baseline(cfg, X, S_cpu, rows0, part0)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -414,7 +465,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default=CFG_NAME, choices=sorted(D.CONFIGS),
-                    help="BASELINE.json config (default C1 = configs[1], the metric's workload)")
+                    help="BASELINE.json config (default C3 = configs[3], the partitioned config the metric names, at G=1)")
     ap.add_argument("--n0", type=int, default=0, help="override the initial graph size (reduced runs)")
     ap.add_argument("--kmedoids-iters", type=int, default=10)
     args = ap.parse_args()

@@ -441,18 +441,23 @@ def test_multi_rank_stages_are_G_invariant(name):
 
 
 def test_query_sharded_unpartitioned_is_G_invariant():
-    """Unpartitioned graphs (C1 shape): the batch's queries are sharded over G ranks; the result
-    equals the single-GPU batch of the same points for every G."""
+    """Unpartitioned graphs (C1 shape): the batch's queries are sharded over G ranks;
+    every replica equals the ORACLE's batch of the same points (and the single-GPU graph) for every G."""
     from paper_1602_06819_b200.dist import insert_batch_staged
     cfg = _cfg_small("C1", n0=5000, n_insert=1500)
     X = D.initial_points(cfg)
     S = D.stream_points(cfg, 0, cfg.n_insert)
     cap = cfg.n0 + cfg.n_insert + 8
     ref = _graph(X, cfg.k, cap)
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cap)
+    o.init_exact()
     batches = [(0, 1024), (1024, 1025), (1025, 1500)]
     for lo, hi in batches:
         ref.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
-    ri, rk = ref.rows()
+        o.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+    ri, rk = o.rows()
+    gi, gk = ref.rows()
+    _assert_rows_equal(cfg.metric, gi, gk, ri, rk, "single-GPU vs oracle")
     for G in (2, 3, 8):
         reps = [_graph(X, cfg.k, cap) for _ in range(G)]
         for lo, hi in batches:
