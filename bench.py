@@ -250,36 +250,24 @@ def run_ours(args, cfg):
     stream = torch.cuda.Stream()
     cap = cfg.n0 + n_stream + 8
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    comm = None
-    if ws > 1:
-        from paper_1602_06819_b200.dist import TorchComm, insert_batch_staged
-        comm = TorchComm()
-
     def barrier():
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
 
     def step(graph, pts):
-        """One global batch: 1 GPU -> graph_insert_batch; N GPUs -> stage_search / all-gather /
-        stage_update / all-gather / stage_commit (partitions or queries sharded over the ranks)."""
-        if ws == 1:
-            return graph.insert_batch(pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)[1]
-        with torch.cuda.stream(stream):
-            st = insert_batch_staged([graph], [rank], ws, pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth,
-                                     cfg.search_seed, cfg.P, allgather=comm.allgather)[0]
-        out = {f: st["search"][f] + st["update"][f] + st["commit"][f]
-               for f in ("search_evals", "search_starts", "search_skipped", "search_expansions", "ball_nodes",
-                         "proposals", "kernel_launches")}
-        out["ms_search"] = st["search"]["ms_total"]
-        out["ms_allpairs"] = st["update"]["ms_total"]
-        out["ms_update"] = 0.0
-        out["ms_merge"] = st["commit"]["ms_total"]
-        return out
+        """One global batch: graph_insert_batch.  On N GPUs the handle owns the library's NCCL
+        communicator and the same call is the distributed insert (partitions or queries sharded over the
+        ranks, all-gathers on the handle's stream); its counters are job totals."""
+        return graph.insert_batch(pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)[1]
 
     # ---------------- setup (untimed): exact initial graph (A0) + Alg. 4 partition (A9) ----------------
     t_setup = time.perf_counter()
-    g = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
+    if ws > 1:
+        from paper_1602_06819_b200.dist import library_graph
+        g = library_graph(X, cfg.k, lrank, capacity=cap, stream=stream.cuda_stream)
+    else:
+        g = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
     part0 = None
     if cfg.P:
         part0 = g.partition_kmedoids(cfg.P, cfg.imbalance, args.kmedoids_iters, cfg.part_seed)[:2]
@@ -317,7 +305,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_total = float(t.item())
     value = args.steps * GB / t_total
-    evals = sum(s["search_evals"] + s["ball_nodes"] for s in stats) * (1 if cfg.P else ws)
+    evals = sum(s["search_evals"] + s["ball_nodes"] for s in stats)      # job totals (all-reduced by the library)
     ms_search = sum(s["ms_search"] for s in stats)
     bytes_search = sum(alg_bytes(s, V, cfg.k) for s in stats)
     peak, peak_src = hbm_peak()
@@ -419,9 +407,10 @@ def run_ours(args, cfg):
                    "timed_inserts": "%d..%d of the %d-insert stream" % (args.warmup * GB, nsteps * GB, cfg.n_insert),
                    "parallelism": "1 GPU" if ws == 1 else (
                        "%d ranks: replicated graph, the P=%d partition searches of each batch sharded over the ranks "
-                       "(Alg. 3), NCCL all-gathers of candidates and proposals" % (ws, cfg.P) if cfg.P else
-                       "dp%d: replicated graph, the global batch's queries sharded over ranks, NCCL all-gathers of "
-                       "candidates and proposals" % ws),
+                       "(Alg. 3), the library's NCCL all-gathers of candidates and proposals inside "
+                       "graph_insert_batch" % (ws, cfg.P) if cfg.P else
+                       "dp%d: replicated graph, the global batch's queries sharded over ranks, the library's NCCL "
+                       "all-gathers of candidates and proposals inside graph_insert_batch" % ws),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "similarities_per_s": evals / t_total,
         "recall_at_k": rec,

@@ -83,8 +83,13 @@ typedef struct {
  *  depth          DEPTH of the update (Alg. 2), 1..10.
  *  seed           key of the counter RNG of the random starts (reading Q4): results are a pure
  *                 function of (inputs, params, seed).
- *  start_override test hook (graph_search only): host array of node ids used as the start
- *                 sequence of every query instead of RNG draws; NULL in production. */
+ *  start_override test hook (graph_search only, unpartitioned graphs): host array of node ids used
+ *                 as the start sequence of every query instead of RNG draws; NULL in production.
+ *  full_scan      graph_search only: 1 = the GNNS baseline's walk (Hajebi et al., section 2.2):
+ *                 the similarity of EVERY neighbour of the current node is computed and the walk moves
+ *                 to the most similar one (the first in row order among equals) if it improves; with
+ *                 expansion_den = 0 (no restart skipping) this is GNNS, the baseline iGNNS is compared
+ *                 with.  0 = iGNNS's eager first-improvement walk. */
 typedef struct {
   double speedup;
   uint32_t expansion_num, expansion_den;
@@ -92,6 +97,7 @@ typedef struct {
   uint64_t seed;
   const int32_t *start_override;
   int32_t start_override_len;
+  int32_t full_scan;
 } knng_params;
 
 /* Counters and per-phase device times of the last call (CUDA events on the handle's stream). */
@@ -107,9 +113,14 @@ typedef struct {
   float ms_search, ms_allpairs, ms_update, ms_merge, ms_total;
 } knng_stats;
 
-/* Runtime placement.  device: CUDA ordinal.  rank/world/nccl_unique_id: reserved for the
- * multi-GPU path (world = 1 here).  cuda_stream: cudaStream_t to issue work on, or NULL.
- * capacity: maximum number of points the graph will hold (0 = 2 * n0). */
+/* Runtime placement.  device: CUDA ordinal.  cuda_stream: cudaStream_t to issue work on, or NULL.
+ * capacity: maximum number of points the graph will hold (0 = 2 * n0).
+ * Multi-GPU (one process per GPU): world = number of ranks, rank = this process's rank, and
+ * nccl_unique_id = the same 128-byte id on every rank (graph_nccl_unique_id() on rank 0, broadcast
+ * by the caller, e.g. over torch.distributed).  The library then owns an NCCL communicator: every
+ * rank holds a full replica of the graph, makes the same calls with the same inputs, and
+ * graph_insert_batch runs the distributed insert (Alg. 3 + Alg. 5,
+ * P:164-178).  world = 1 with a non-NULL id builds a 1-rank communicator (tests). */
 typedef struct {
   int32_t device;
   int32_t rank, world;
@@ -127,7 +138,11 @@ typedef struct knng_graph knng_graph;   /* opaque */
 int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_graph **out);
 
 /* graph_insert_batch -- add a batch of B points (Alg. 1 + Alg. 2; distributed form
- * Alg. 5, when partitioned).  Ids are n_t .. n_t+B-1 in batch order
+ * Alg. 5, when partitioned).  On a multi-GPU handle every rank passes the same batch:
+ * partitioned graphs search the rank's P/world partitions, unpartitioned ones the rank's share of
+ * the queries; NCCL all-gathers on the handle's stream exchange the candidates and proposals (no
+ * host synchronisation in between) and every replica ends identical to the 1-GPU result; the
+ * counters in *st are summed over the ranks.  Ids are n_t .. n_t+B-1 in batch order
  * (*first_id_out = n_t).  Semantics: every point is searched
  * with iGNNS on the snapshot G_t (RNG stream keyed by its id); its row is the top-k of its
  * search result and the other batch points; the update balls (DEPTH levels over the snapshot)
@@ -213,6 +228,14 @@ void graph_free(knng_graph *g);
 
 /* graph_last_error -- message of the last non-zero status of this thread ("" if none). */
 const char *graph_last_error(void);
+
+/* graph_nccl_unique_id -- write a new 128-byte NCCL unique id to id_out (host memory), for
+ * knng_runtime.nccl_unique_id.  Call on one rank and broadcast it.  Errors: INVALID_ARG, NCCL
+ * (libnccl.so.2 is loaded at run time; the single-GPU calls never need it). */
+int graph_nccl_unique_id(void *id_out);
+
+/* graph_world -- ranks of the handle's communicator (1 without one; -1 on a NULL handle). */
+int32_t graph_world(const knng_graph *g);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,9 @@
  *   or_rng_draw          parity unpinned by the paper (Q4); pinned only by a
  *                        second, independent Python implementation (KAT)
  *   or_exact_rows        pinned (hand examples, brute force in numpy)
- *   or_ignns_search      pinned (W3 hand traces, budget >= |pool| => linear search)
+ *   or_ignns_search      pinned (W3 hand traces, budget >= |pool| => linear search, a literal
+ *                        re-derivation of the walk without the Q9 shortcut in tests/pyref.py);
+ *                        its full_scan mode (the GNNS baseline) pinned the same way
  *   or_insert_batch      pinned (W1, W2, 1-D exactness, B=1 == literal Alg.1+2)
  *   or_insert_sequential pinned (W1, W2 sequential)
  *   or_partition_kmedoids pinned (W7 hand trace, balance bound, brute hop sums)
@@ -274,6 +276,8 @@ typedef struct {
   uint64_t seed;
   const int32_t *starts;    /* test hook: explicit start sequence (Q4 override) */
   int64_t nstarts;
+  int full_scan;            /* 1: the GNNS baseline's walk (section 2.2): evaluate every
+                               neighbour of the current node, move to the most similar one */
 } or_search_cfg;
 
 /* Q6: budget = max(min(k, |pool|), floor(|pool| / speedup)). */
@@ -332,6 +336,36 @@ static void ignns(const or_search_cfg *C, or_point q, int64_t pid, int kr,
     first = 0;
     cur = r; kcur = kr_key;
 
+    /* ---- GNNS baseline walk: scan all k neighbours, move to the most similar one if it
+     * improves on cur (ties -> the first in row order); same budget, restart and cache rules ---- */
+    if (C->full_scan) {
+      for (;;) {
+        int t;
+        int32_t best = -1;
+        uint32_t kbest = 0;
+        W->expanded[cur] = 1;
+        ++st->expansions;
+        for (t = 0; t < C->k; ++t) {
+          int32_t v = C->rows[(size_t)cur * C->k + t];
+          uint32_t kv;
+          if (v < 0 || !in_pool(C, v)) continue;
+          if (!W->evaluated[v]) {
+            if (c == budget) goto done;  /* the over-budget evaluation is not performed */
+            kv = key_of(C->S, q, store_point(C->S, v));
+            ++c;
+            W->evaluated[v] = 1; W->keyv[v] = kv; W->touched[ntouched++] = v;
+            list_insert(metric, T, kv, v);
+          } else {
+            kv = W->keyv[v];
+          }
+          if (closer(metric, kv, kcur) && (best < 0 || closer(metric, kv, kbest))) { best = v; kbest = kv; }
+        }
+        if (best < 0) break;               /* local maximum: restart */
+        cur = best; kcur = kbest;
+        if (W->expanded[cur]) break;       /* Q9 (same argument: the re-walk repeats the same choices) */
+      }
+      continue;
+    }
     /* ---- hill climbing with eager first-improvement descent ---- */
     for (;;) {
       int moved = 0, t;
@@ -376,7 +410,7 @@ int64_t or_ignns_search(int metric, int dim, const void *data, const uint64_t *o
                         int kr, double speedup, uint64_t e_num, uint64_t e_den,
                         uint64_t seed, int64_t pid,
                         const int32_t *starts, int64_t nstarts,
-                        int32_t *out_ids, uint32_t *out_keys, int64_t *out_stats4) {
+                        int32_t *out_ids, uint32_t *out_keys, int64_t *out_stats4, int full_scan) {
   or_store S;
   or_search_cfg C;
   or_scratch W;
@@ -391,7 +425,7 @@ int64_t or_ignns_search(int metric, int dim, const void *data, const uint64_t *o
   C.S = &S; C.k = k; C.rows = rows; C.pool = pool; C.m = m;
   C.part_of = part_of; C.part = part; C.speedup = speedup;
   C.e_num = e_num; C.e_den = e_den; C.seed = seed;
-  C.starts = starts; C.nstarts = nstarts;
+  C.starts = starts; C.nstarts = nstarts; C.full_scan = full_scan;
   memset(&q, 0, sizeof q);
   q.u8 = (const uint8_t *)qdata; q.f32 = (const float *)qdata; q.tok = qtok; q.ntok = qntok;
   if (!scratch_init(&W, n_store)) return -5;
@@ -433,6 +467,7 @@ typedef struct {
   int depth;
   uint64_t seed;
   int nthreads;
+  int full_scan;          /* graph_search only: the GNNS baseline walk */
 } or_params;
 
 typedef struct { int32_t node; uint32_t key; int32_t qid; } or_prop;
@@ -501,6 +536,7 @@ static void *search_worker(void *arg) {
       }
       C.speedup = J->prm->speedup; C.e_num = J->prm->e_num; C.e_den = J->prm->e_den;
       C.seed = J->prm->seed;
+      C.full_scan = J->prm->full_scan;
       T.cap = J->kr; T.cnt = 0; T.key = tk; T.id = ti;
       ignns(&C, q, pid, J->kr, &W, &T, &st);
       /* Alg. 3: keep the k most similar of the k*p candidates */
@@ -632,7 +668,7 @@ int or_insert_batch(int metric, int dim, void *data, uint64_t *off, int k,
   G.ids = ids; G.keys = keys; G.P = P; G.part_of = part_of; G.members = members;
   G.member_cnt = member_cnt; G.member_cap = member_cap; G.medoids = medoids;
   prm.speedup = speedup; prm.e_num = e_num; prm.e_den = e_den; prm.depth = depth;
-  prm.seed = seed; prm.nthreads = nthreads;
+  prm.seed = seed; prm.nthreads = nthreads; prm.full_scan = 0;
   S = graph_store(&G);
   if (B <= 0) return 0;
 
@@ -733,7 +769,7 @@ int or_insert_sequential(int metric, int dim, void *data, uint64_t *off, int k,
   G.metric = metric; G.dim = dim; G.k = k; G.data = data; G.off = off; G.n = n_t;
   G.ids = ids; G.keys = keys;
   prm.speedup = speedup; prm.e_num = e_num; prm.e_den = e_den; prm.depth = depth;
-  prm.seed = seed; prm.nthreads = 1;
+  prm.seed = seed; prm.nthreads = 1; prm.full_scan = 0;
   S = graph_store(&G);
   x = store_point(&S, n_t);
 
@@ -792,7 +828,7 @@ int or_graph_search(int metric, int dim, void *data, uint64_t *off, int k,
                     int64_t member_cap,
                     const void *qdata, const uint64_t *qoff, int64_t nq, int kr,
                     double speedup, uint64_t e_num, uint64_t e_den, uint64_t seed,
-                    int nthreads, int32_t *out_ids, uint32_t *out_keys, int64_t *out_stats4) {
+                    int nthreads, int32_t *out_ids, uint32_t *out_keys, int64_t *out_stats4, int full_scan) {
   or_graph G;
   or_params prm;
   or_search_job J;
@@ -802,7 +838,7 @@ int or_graph_search(int metric, int dim, void *data, uint64_t *off, int k,
   G.ids = ids; G.keys = keys; G.P = P; G.part_of = part_of; G.members = members;
   G.member_cnt = member_cnt; G.member_cap = member_cap;
   prm.speedup = speedup; prm.e_num = e_num; prm.e_den = e_den; prm.depth = 1;
-  prm.seed = seed; prm.nthreads = nthreads;
+  prm.seed = seed; prm.nthreads = nthreads; prm.full_scan = full_scan;
   memset(&J, 0, sizeof J);
   J.G = &G; J.prm = &prm; J.first_query = 0; J.kr = kr; J.cand_ids = out_ids; J.cand_keys = out_keys;
   J.stats = out_stats4; J.qpoint = NULL; J.qdata = qdata; J.qoff = qoff; J.pid_is_index = 1;
@@ -853,6 +889,70 @@ static int64_t hop_sum(int64_t c, const int32_t *mem, int64_t sz,
   for (i = 0; i < sz; ++i) s += dist[i] >= 0 ? dist[i] : sz;
   (void)mem;
   return s;
+}
+
+/* The update step of Alg. 4 for assignment part[0..n): per cluster, the member minimising the
+ * hop sum in the cluster-induced undirected view (Q29) -- every member when |C| <= exact_limit, else
+ * (Q22) the current medoid (if a member) and ncand-1 draws of stream (seed, tag, it*P + p, j).
+ * Unreachable members cost |C|; ties -> smaller id.  Empty clusters keep their medoid.  Returns the
+ * total hop sum of the chosen medoids; scratch arrays are sized n (adj: 2nk). */
+static int64_t update_medoids(int64_t n, int k, const int32_t *ids, int P, const uint8_t *part,
+                              const int32_t *med, int32_t *newmed, uint64_t seed, uint64_t tag, int64_t it,
+                              int64_t exact_limit, int ncand, int64_t *local, int32_t *mem, int32_t *deg,
+                              int64_t *adj_off, int32_t *adj, int32_t *dist, int32_t *queue) {
+  int64_t cost = 0, i;
+  int p, j;
+  for (p = 0; p < P; ++p) {
+    int64_t sz = 0, bestc = -1, bests = 0, c;
+    for (i = 0; i < n; ++i) if (part[i] == p) { local[i] = sz; mem[sz++] = (int32_t)i; } else local[i] = -1;
+    /* cluster-induced undirected adjacency (Q29) */
+    for (i = 0; i < sz; ++i) deg[i] = 0;
+    for (i = 0; i < sz; ++i) {
+      int t;
+      for (t = 0; t < k; ++t) {
+        int32_t u = ids[(size_t)mem[i] * k + t];
+        if (u >= 0 && local[u] >= 0) { deg[i]++; deg[local[u]]++; }
+      }
+    }
+    adj_off[0] = 0;
+    for (i = 0; i < sz; ++i) adj_off[i + 1] = adj_off[i] + deg[i];
+    for (i = 0; i < sz; ++i) deg[i] = 0;
+    for (i = 0; i < sz; ++i) {
+      int t;
+      for (t = 0; t < k; ++t) {
+        int32_t u = ids[(size_t)mem[i] * k + t];
+        if (u >= 0 && local[u] >= 0) {
+          int64_t lu = local[u];
+          adj[adj_off[i] + deg[i]++] = (int32_t)lu;
+          adj[adj_off[lu] + deg[lu]++] = (int32_t)i;
+        }
+      }
+    }
+    if (sz == 0) { newmed[p] = med[p]; continue; }
+    if (sz <= exact_limit) {
+      for (c = 0; c < sz; ++c) {
+        int64_t s = hop_sum(c, mem, sz, adj_off, adj, dist, queue);
+        if (bestc < 0 || s < bests) { bestc = c; bests = s; }   /* ties -> smaller id (ascending scan) */
+      }
+    } else {
+      /* Q22: candidates = {current medoid if member} u ncand-1 seeded draws */
+      int64_t cnt = 0;
+      int32_t *cl = (int32_t *)malloc(sizeof(int32_t) * ncand);
+      if (local[med[p]] >= 0) cl[cnt++] = (int32_t)local[med[p]];
+      for (j = 0; j < ncand - 1; ++j)
+        cl[cnt++] = (int32_t)or_rng_draw(seed, tag, (uint64_t)(it * P + p), (uint64_t)j, (uint64_t)sz);
+      for (j = 0; j < cnt; ++j) {
+        int64_t s;
+        c = cl[j];
+        s = hop_sum(c, mem, sz, adj_off, adj, dist, queue);
+        if (bestc < 0 || s < bests || (s == bests && mem[c] < mem[bestc])) { bestc = c; bests = s; }
+      }
+      free(cl);
+    }
+    newmed[p] = mem[bestc];
+    cost += bests;
+  }
+  return cost;
 }
 
 /* part_out[n], medoids_io[P] (output), cost_out[max_iter+1] (costs of accepted
@@ -919,57 +1019,8 @@ int or_partition_kmedoids(int metric, int dim, const void *data, const uint64_t 
       size[best]++;
     }
     /* ---- Update: new medoid = member minimising the hop sum ---- */
-    for (p = 0; p < P; ++p) {
-      int64_t sz = 0, e = 0, bestc = -1, bests = 0, c;
-      for (i = 0; i < n; ++i) if (part[i] == p) { local[i] = sz; mem[sz++] = (int32_t)i; } else local[i] = -1;
-      /* cluster-induced undirected adjacency (Q29) */
-      for (i = 0; i < sz; ++i) deg[i] = 0;
-      for (i = 0; i < sz; ++i) {
-        int t;
-        for (t = 0; t < k; ++t) {
-          int32_t u = ids[(size_t)mem[i] * k + t];
-          if (u >= 0 && local[u] >= 0) { deg[i]++; deg[local[u]]++; }
-        }
-      }
-      adj_off[0] = 0;
-      for (i = 0; i < sz; ++i) adj_off[i + 1] = adj_off[i] + deg[i];
-      for (i = 0; i < sz; ++i) deg[i] = 0;
-      for (i = 0; i < sz; ++i) {
-        int t;
-        for (t = 0; t < k; ++t) {
-          int32_t u = ids[(size_t)mem[i] * k + t];
-          if (u >= 0 && local[u] >= 0) {
-            int64_t lu = local[u];
-            adj[adj_off[i] + deg[i]++] = (int32_t)lu;
-            adj[adj_off[lu] + deg[lu]++] = (int32_t)i;
-          }
-        }
-      }
-      (void)e;
-      if (sz == 0) { newmed[p] = med[p]; continue; }
-      if (sz <= exact_limit) {
-        for (c = 0; c < sz; ++c) {
-          int64_t s = hop_sum(c, mem, sz, adj_off, adj, dist, queue);
-          if (bestc < 0 || s < bests) { bestc = c; bests = s; }   /* ties -> smaller id (ascending scan) */
-        }
-      } else {
-        /* Q22: candidates = {current medoid if member} u ncand-1 seeded draws */
-        int64_t cnt = 0;
-        int32_t *cl = (int32_t *)malloc(sizeof(int32_t) * ncand);
-        if (local[med[p]] >= 0) cl[cnt++] = (int32_t)local[med[p]];
-        for (j = 0; j < ncand - 1; ++j)
-          cl[cnt++] = (int32_t)or_rng_draw(seed, 0xFFFFFFFEull, (uint64_t)(it * P + p), (uint64_t)j, (uint64_t)sz);
-        for (j = 0; j < cnt; ++j) {
-          int64_t s;
-          c = cl[j];
-          s = hop_sum(c, mem, sz, adj_off, adj, dist, queue);
-          if (bestc < 0 || s < bests || (s == bests && mem[c] < mem[bestc])) { bestc = c; bests = s; }
-        }
-        free(cl);
-      }
-      newmed[p] = mem[bestc];
-      cost += bests;
-    }
+    cost = update_medoids(n, k, ids, P, part, med, newmed, seed, 0xFFFFFFFEull, it, exact_limit, ncand,
+                          local, mem, deg, adj_off, adj, dist, queue);
     /* Q23: accept only if the hop-sum cost does not rise */
     if (it > 0 && cost > prev_cost) break;
     memcpy(part_out, part, (size_t)n);
@@ -984,6 +1035,28 @@ int or_partition_kmedoids(int metric, int dim, const void *data, const uint64_t 
   free(med); free(newmed); free(part); free(size); free(local); free(dist); free(queue);
   free(mem); free(adj_off); free(adj); free(deg); free(dk);
   return (int)accepted;
+}
+
+/* Alg. 5's last step, "compute new medoids" (F5): the update step of Alg. 4
+ * on the current partition part_of[0..n) -- nodes keep their partitions; medoids_io[P] in/out.
+ * Candidate draws use stream (seed, 0xFFFFFFFD, epoch*P + p, j).  Returns 0, the total hop sum in
+ * *cost_out. */
+int or_recompute_medoids(int64_t n, int k, const int32_t *ids, int P, const uint8_t *part_of, int32_t *medoids_io,
+                         uint64_t seed, int64_t epoch, int64_t exact_limit, int ncand, int64_t *cost_out) {
+  int64_t *local = (int64_t *)malloc(sizeof(int64_t) * n);
+  int32_t *dist = (int32_t *)malloc(sizeof(int32_t) * n);
+  int32_t *queue = (int32_t *)malloc(sizeof(int32_t) * n);
+  int32_t *mem = (int32_t *)malloc(sizeof(int32_t) * n);
+  int64_t *adj_off = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+  int32_t *adj = (int32_t *)malloc(sizeof(int32_t) * (size_t)(2 * n * k + 1));
+  int32_t *deg = (int32_t *)malloc(sizeof(int32_t) * n);
+  int32_t *newmed = (int32_t *)malloc(sizeof(int32_t) * P);
+  int64_t cost = update_medoids(n, k, ids, P, part_of, medoids_io, newmed, seed, 0xFFFFFFFDull, epoch, exact_limit,
+                                ncand, local, mem, deg, adj_off, adj, dist, queue);
+  memcpy(medoids_io, newmed, sizeof(int32_t) * P);
+  if (cost_out) *cost_out = cost;
+  free(local); free(dist); free(queue); free(mem); free(adj_off); free(adj); free(deg); free(newmed);
+  return 0;
 }
 
 /* ------------------------------------------------------------------ */

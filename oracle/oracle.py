@@ -57,7 +57,7 @@ def lib():
             L.or_ignns_search.restype = i64
             L.or_ignns_search.argtypes = [i32, i32, P, P, i64, P, i32, P, i64, P, i32,
                                           P, P, i64, i32, dbl, u64, u64, u64, i64, P, i64,
-                                          P, P, P]
+                                          P, P, P, i32]
             L.or_insert_batch.restype = i32
             L.or_insert_batch.argtypes = [i32, i32, P, P, i32, i64, P, P, i32, P, P, P, i64, P,
                                           i64, dbl, u64, u64, i32, u64, i32, P]
@@ -66,7 +66,7 @@ def lib():
                                                u64, P]
             L.or_graph_search.restype = i32
             L.or_graph_search.argtypes = [i32, i32, P, P, i32, i64, P, P, i32, P, P, P, i64,
-                                          P, P, i64, i32, dbl, u64, u64, u64, i32, P, P, P]
+                                          P, P, i64, i32, dbl, u64, u64, u64, i32, P, P, P, i32]
             L.or_partition_kmedoids.restype = i32
             L.or_partition_kmedoids.argtypes = [i32, i32, P, P, i64, i32, P, i32, dbl, i32, u64,
                                                 P, P, P, i64, i32, P]
@@ -331,7 +331,8 @@ class OracleGraph:
         self.n = n_t + 1
         return st
 
-    def search(self, queries, kr, speedup, e_num, e_den, seed, nthreads=None):
+    def search(self, queries, kr, speedup, e_num, e_den, seed, nthreads=None, full_scan=0):
+        """graph_search; full_scan=1 with e_den=0 is the GNNS baseline."""
         if self.metric == JAC:
             qoff = np.zeros(len(queries) + 1, np.uint64)
             qoff[1:] = np.cumsum([len(q) for q in queries])
@@ -347,13 +348,14 @@ class OracleGraph:
                                    _p(self.ids), _p(self.keys), self.P, _p(self.part_of),
                                    _p(self.members), _p(self.member_cnt), self.member_cap,
                                    _p(qd), _p(qoff), nq, kr, speedup, e_num, e_den, seed,
-                                   nthreads or default_threads(), _p(oi), _p(ok), _p(st))
+                                   nthreads or default_threads(), _p(oi), _p(ok), _p(st), int(full_scan))
         if rc:
             raise RuntimeError("or_graph_search rc=%d" % rc)
         return oi, ok, st
 
-    def ignns(self, q, kr, speedup, e_num, e_den, seed, pid, starts=None, part=0, pool=None):
-        """One iGNNS search on the current graph; optional injected starts."""
+    def ignns(self, q, kr, speedup, e_num, e_den, seed, pid, starts=None, part=0, pool=None, full_scan=0):
+        """One iGNNS search on the current graph; optional injected starts.  full_scan=1:
+        the GNNS baseline's walk (with e_den=0, no restart skipping: GNNS)."""
         if self.metric == JAC:
             qd = np.ascontiguousarray(q, np.uint32)
             qtok, qn, qdata = qd, len(qd), None
@@ -374,7 +376,7 @@ class OracleGraph:
         lib().or_ignns_search(self.metric, self.dim, _p(self.data), _p(self.off), self.n,
                               _p(self.ids), self.k, _p(pool_a), m, _p(part_of), part,
                               _p(qdata), _p(qtok), qn, kr, speedup, e_num, e_den, seed, pid,
-                              _p(st_a), 0 if st_a is None else len(st_a), _p(oi), _p(ok), _p(st))
+                              _p(st_a), 0 if st_a is None else len(st_a), _p(oi), _p(ok), _p(st), int(full_scan))
         return oi, ok, dict(evals=int(st[0]), starts=int(st[1]), skipped=int(st[2]),
                             expansions=int(st[3]))
 

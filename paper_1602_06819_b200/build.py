@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 HDR = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(os.path.join(HERE, "csrc", "*.h")) +
              [os.path.join(HERE, "..", "include", "knng.h")])
-OUT = os.path.join(HERE, "libknng.so")
+OUT = os.environ.get("KNNG_BUILD_OUT") or os.path.join(HERE, "libknng.so")
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-shared"]
 
@@ -30,6 +30,10 @@ def build(force=False, verbose=False):
     cflags = [f for f in NVCC_FLAGS if f != "-shared"]
     if os.environ.get("KNNG_BUILD_PROFILE"):   # K1 cycle counters (KNNG_PROFILE=1 at run time)
         cflags.append("-DKNNG_PROFILE_COUNTERS")
+    if os.environ.get("KNNG_BUILD_HACK"):   # timing experiments only (wrong results): see knng_search.cu
+        cflags.append("-DKNNG_HACK_" + os.environ["KNNG_BUILD_HACK"])
+    if os.environ.get("KNNG_BUILD_DEBUG_WAIT"):   # K1 ring waits report a stuck producer / consumer
+        cflags.append("-DKNNG_DEBUG_WAIT")
     jobs = []
     for src in SRC:
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".%d.o" % os.getpid())

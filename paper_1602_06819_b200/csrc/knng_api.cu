@@ -25,6 +25,7 @@
 #include "knng_internal.h"
 
 #include "knng_handle.h"
+#include "knng_nccl.h"
 
 using namespace knng;
 
@@ -222,6 +223,12 @@ static void free_graph(knng_graph *g) {
   g->w_dense.norm.release();
   for (auto &e : g->ev)
     if (e) cudaEventDestroy(e);
+  if (g->ev_cnt) cudaEventDestroy(g->ev_cnt);
+  if (g->h_cnt) cudaFreeHost(g->h_cnt);
+  DBuf *dws[] = {&g->w_dci, &g->w_dck, &g->w_gci, &g->w_gck, &g->w_dprops, &g->w_dcnt, &g->w_dnid, &g->w_dnkey,
+                 &g->w_gprops, &g->w_gcnt, &g->w_gnid, &g->w_gnkey, &g->w_dstats};
+  for (DBuf *b : dws) b->release();
+  if (g->comm) knng::nccl_comm_destroy(g->comm);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
   delete g;
 }
@@ -229,6 +236,15 @@ static void free_graph(knng_graph *g) {
 extern "C" {
 
 const char *graph_last_error(void) { return knng_err_slot().c_str(); }
+
+int graph_nccl_unique_id(void *id_out) {
+  knng_err_slot().clear();
+  if (!id_out) return fail(KNNG_ERR_INVALID_ARG, "graph_nccl_unique_id: null output");
+  if (const char *m = knng::nccl_get_unique_id(id_out)) return fail(KNNG_ERR_NCCL, "%s", m);
+  return KNNG_OK;
+}
+
+int32_t graph_world(const knng_graph *g) { return g ? g->world : -1; }
 
 int64_t graph_size(const knng_graph *g) { return g ? g->n : -1; }
 int32_t graph_degree(const knng_graph *g) { return g ? g->k : -1; }
@@ -262,11 +278,25 @@ int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_g
     delete g;
     return fail(KNNG_ERR_CUDA, "graph_init: cudaSetDevice(%d) failed", rt ? rt->device : 0);
   }
+  // multi-GPU: the library's own NCCL communicator (every rank calls graph_init with the same inputs and
+  // the same 128-byte id from graph_nccl_unique_id on rank 0); a 1-rank communicator is allowed (tests)
+  if (rt && (rt->world > 1 || rt->nccl_unique_id)) {
+    if (rt->world < 1 || rt->rank < 0 || rt->rank >= rt->world || !rt->nccl_unique_id) {
+      delete g;
+      return fail(KNNG_ERR_INVALID_ARG, "graph_init: bad rank %d / world %d / id", rt->rank, rt->world);
+    }
+    g->rank = rt->rank;
+    g->world = rt->world;
+    if (const char *m = knng::nccl_comm_init(&g->comm, rt->world, rt->nccl_unique_id, rt->rank)) {
+      delete g;
+      return fail(KNNG_ERR_NCCL, "graph_init: %s", m);
+    }
+  }
   if (rt && rt->cuda_stream) {
     g->stream = (cudaStream_t)rt->cuda_stream;
   } else {
     if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess) {
-      delete g;
+      free_graph(g);
       return fail(KNNG_ERR_CUDA, "graph_init: stream create failed");
     }
     g->own_stream = true;
@@ -320,23 +350,21 @@ static int check_params(const knng_params *p) {
 }
 
 // K1 launch shape.  Each CTA runs one (query, partition) task at a time: a consumer warp (the
-// sequential iGNNS) and a producer warp (the random starts, S chunks of rows in flight).  The walks
-// are latency chains, so the plan first makes room for every task at once (up to 8 CTAs per SM,
-// the register limit), then spends what shared memory is left on the visited bitmaps and a deeper
-// ring.  Knobs KNNG_STAGES / KNNG_NPROD / KNNG_LANE_EVAL / KNNG_RING / KNNG_SMEM_BITS override it
-// (measurement only).
+// sequential iGNNS) and a producer warp (the random starts).  The walks are latency chains, so the
+// plan first makes room for every task at once (up to 8 CTAs per SM, the register limit; 10 with
+// the 96-register build), then puts the task's D/E bit planes in shared memory when they fit, then
+// deepens the ring.  Knobs KNNG_LANE_EVAL / KNNG_RING / KNNG_SMEM_BITS / KNNG_HBITS / KNNG_LEAN /
+// KNNG_WALK_PREFETCH / KNNG_WIN_PREFETCH override it (measurement and tests only: results do not
+// depend on them).
 static void plan_k1(SearchArgs &a, bool sets, bool u8, int64_t tasks, int64_t mmax) {
   int nsm = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  a.bits_words = 2 * ((mmax + 31) / 32);
-  a.nprod = 1;
+  a.de_words = (((mmax + 15) / 16) + 3) & ~3ll;
+  a.x_words = (((mmax + 31) / 32) + 3) & ~3ll;
   a.lane_eval = 1;
-  a.stages = 2;
-  // (a.stages is fixed at 2: deeper producer pipelines measured slower everywhere)
-  if (const char *e = getenv("KNNG_NPROD")) a.nprod = std::max(1, std::min(3, atoi(e)));
-  // the 96-register variant (10 CTAs/SM) pays for many latency-bound u8 tasks (C3: +6%); with <= 8
-  // CTAs' worth of tasks (C1) or for sets (C4) the 128-register form is faster (measured)
+  a.hbits = 12;
+  if (const char *e = getenv("KNNG_HBITS")) a.hbits = std::max(6, std::min(14, atoi(e)));
   a.lean = (u8 && tasks > (int64_t)nsm * 8) ? 1 : 0;
   if (const char *e = getenv("KNNG_LEAN")) a.lean = atoi(e) != 0;
   const int cap = a.lean ? 10 : 8;                 // two-warp CTAs per SM the registers allow
@@ -345,15 +373,14 @@ static void plan_k1(SearchArgs &a, bool sets, bool u8, int64_t tasks, int64_t mm
     const size_t sm = search_smem_bytes(x, sets) + 1024;
     return (int)std::min<size_t>(cap, (228 * 1024) / sm);
   };
-  // preference order: the evaluated bitmap in shared memory first (its test-and-set is on every
-  // draw), then the deeper ring
-  const int cand[6][2] = {{1, 32}, {1, 16}, {1, 8}, {0, 32}, {0, 16}, {0, 8}};
+  // preference order: the D/E planes in shared memory first (no L2 atomics), then the deeper ring
+  const int cand[6][2] = {{1, 16}, {1, 8}, {0, 16}, {0, 8}, {1, 4}, {0, 4}};
   int best = -1, best_occ = -1;
   for (int i = 0; i < 6; ++i) {
     SearchArgs x = a;
     x.smem_bits = cand[i][0];
     x.ring = cand[i][1];
-    if (x.smem_bits && (size_t)(x.bits_words / 2) * 4 > 96 * 1024) continue;
+    if (x.smem_bits && (size_t)x.de_words * 4 > 96 * 1024) continue;
     const int o = occ(x);
     if (o >= need) { best = i; best_occ = o; break; }
     if (o > best_occ) { best = i; best_occ = o; }
@@ -361,24 +388,38 @@ static void plan_k1(SearchArgs &a, bool sets, bool u8, int64_t tasks, int64_t mm
   a.smem_bits = cand[best][0];
   a.ring = cand[best][1];
   if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
-  a.walk_prefetch = 0;   // measured faster on C1-C4: the k-row prefetch costs more issue than the round trip it saves
+  a.walk_prefetch = 1;
   if (const char *e = getenv("KNNG_WALK_PREFETCH")) a.walk_prefetch = atoi(e) != 0;
-  a.ex_one = 1;   // measured faster (C1, C3): one hash lookup per step instead of k
   a.win_prefetch = 1;
   if (const char *e = getenv("KNNG_WIN_PREFETCH")) a.win_prefetch = atoi(e) != 0;
-  if (const char *e = getenv("KNNG_EX_ONE")) a.ex_one = atoi(e) != 0;
-  if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 8 ? 8 : (atoi(e) <= 16 ? 16 : 32);
+  if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 4 ? 4 : (atoi(e) <= 8 ? 8 : 16);
   if (const char *e = getenv("KNNG_SMEM_BITS")) a.smem_bits = atoi(e) != 0;
   a.gslots = std::min<int64_t>(tasks, (int64_t)nsm * cap);
 }
 
-static int64_t max_pool(knng_graph *g) {
-  if (g->P == 0) return g->n;
-  std::vector<int64_t> cnt(g->P);
-  cudaMemcpy(cnt.data(), g->member_cnt, sizeof(int64_t) * g->P, cudaMemcpyDeviceToHost);
-  int64_t m = 0;
-  for (auto c : cnt) m = std::max(m, c);
-  return m;
+// Largest partition pool (sizes the search's workspaces; the kernel reads the exact sizes on the
+// device).  An upper bound kept on the host -- exact after the asynchronous read-back that follows
+// every placement, else the last exact value plus the points placed since -- so no search waits on
+// the device for it.
+static int max_pool(knng_graph *g, int64_t *out) {
+  if (g->P == 0) { *out = g->n; return 0; }
+  if (!g->h_cnt) CK(cudaMallocHost((void **)&g->h_cnt, 256 * sizeof(int64_t)));
+  if (!g->ev_cnt) CK(cudaEventCreateWithFlags(&g->ev_cnt, cudaEventDisableTiming));
+  if (g->cnt_pending && cudaEventQuery(g->ev_cnt) == cudaSuccess) {
+    int64_t m = 0;
+    for (int p = 0; p < g->P; ++p) m = std::max(m, g->h_cnt[p]);
+    g->pool_bound = m + (g->n - g->cnt_n);   // + the points placed since the read-back was issued
+    g->cnt_pending = false;
+  }
+  if (g->pool_bound <= 0) {   // first search after partitioning: one synchronous read
+    CK(cudaMemcpyAsync(g->h_cnt, g->member_cnt, sizeof(int64_t) * g->P, cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    int64_t m = 0;
+    for (int p = 0; p < g->P; ++p) m = std::max(m, g->h_cnt[p]);
+    g->pool_bound = m;
+  }
+  *out = g->pool_bound;
+  return 0;
 }
 
 // K1 over partitions [part_lo, part_hi) (unpartitioned: [0, 1)): raw per-partition candidates
@@ -386,11 +427,13 @@ static int64_t max_pool(knng_graph *g) {
 static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, int64_t nq, int64_t pid_base, int kr,
                             const knng_params *p, const int32_t *d_starts, int nstarts, int part_lo, int part_hi,
                             int32_t *out_i, uint32_t *out_k, int *nl) {
-  const int64_t mmax = max_pool(g);
+  int64_t mmax = 0;
+  if (int r = max_pool(g, &mmax)) return r;
   if (g->P > 0 && mmax == 0) return fail(KNNG_ERR_EMPTY, "all partitions are empty");
   const int pc = part_hi - part_lo;
   SearchArgs a;
   memset(&a, 0, sizeof a);
+  a.metric = g->metric;
   a.st = graph_store_view(g);
   a.qs = qs;
   a.qrow0 = qrow0;
@@ -415,7 +458,7 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.kr = kr;
   a.starts = d_starts;
   a.nstarts = nstarts;
-  a.G = 8;
+  a.full_scan = p->full_scan != 0;
   a.out_ids = out_i;
   a.out_keys = out_k;
   a.stats = g->w_stats.as<unsigned long long>();
@@ -429,7 +472,7 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.task_ctr = a.stats + 14;
   a.pitch = g->metric == KNNG_JACCARD_U32SET ? 16 * 16 + 16 : (int)g->geom.stride + 16;
   plan_k1(a, g->metric == KNNG_JACCARD_U32SET, g->metric == KNNG_L2SQ_U8, nq * pc, mmax);
-  CK(g->w_bits.ensure((size_t)a.gslots * a.bits_words * 4));
+  CK(g->w_bits.ensure((size_t)a.gslots * (a.de_words + a.x_words) * 4));
   a.gbits = g->w_bits.as<uint32_t>();
   cudaError_t e = launch_search(g->geom, a, g->stream, nl);
   if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
@@ -494,6 +537,7 @@ static int stage_search(knng_graph *g, const knng_points *pts, const knng_params
   if (int r = store_points(g, pts, n_t)) return r;
   // A2-A3: iGNNS per (point, partition) on the snapshot, for queries [q_lo, q_hi)
   if (q_hi == q_lo) return 0;
+  if (p->full_scan) return fail(KNNG_ERR_INVALID_ARG, "insert: full_scan (the GNNS baseline) is a graph_search mode");
   return run_search_phase(g, graph_store_view(g), n_t + q_lo, q_hi - q_lo, n_t + q_lo, g->k, p, nullptr, 0, part_lo,
                           part_hi, ci, ck, nl);
 }
@@ -593,10 +637,30 @@ static int stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, c
   if (g->P > 0) {   // the new rows' partition-local view
     CK(launch_lrows(g->ids, g->k, n_t, B, g->part_of, g->local_idx, g->lrows, g->stream));
     ++*nl;
+    // partition sizes: bound now, exact once the read-back lands
+    if (g->pool_bound > 0) g->pool_bound += B;
+    if (g->h_cnt && g->ev_cnt && !g->cnt_pending) {
+      CK(cudaMemcpyAsync(g->h_cnt, g->member_cnt, sizeof(int64_t) * g->P, cudaMemcpyDeviceToHost, g->stream));
+      CK(cudaEventRecord(g->ev_cnt, g->stream));
+      g->cnt_pending = true;
+      g->cnt_n = n_t + B;
+    }
   }
   g->n = n_t + B;
   g->pend_B = 0;
   return 0;
+}
+
+static void print_profile(knng_graph *g, const unsigned long long *h, int64_t B) {
+  if (!getenv("KNNG_PROFILE") || B <= 0 || !h[16]) return;
+  const double T = (double)g->tprof_n > 0 ? (double)g->tprof_n : (double)B;
+  fprintf(stderr, "KNNG_PROFILE per task (%.0f tasks): consumer %.0f cyc (ring wait %.0f, walks %.0f) | producer gather "
+          "wait %.0f, ring-full wait %.0f | windows %.1f, walk steps %.1f, fast chunks %.1f, produced chunks %.1f | "
+          "hash-overflow tasks %.0f\n", T, h[16] / T, h[17] / T, h[18] / T, h[19] / T, h[20] / T, h[21] / T, h[22] / T,
+          h[24] / T, h[25] / T, (double)h[23]);
+  if (h[22])
+    fprintf(stderr, "KNNG_PROFILE walk step: %.0f cyc = row %.0f + sets/gathers/keys %.0f + commit %.0f (+ move)\n",
+            (double)h[18] / h[22], (double)h[26] / h[22], (double)h[27] / h[22], (double)h[28] / h[22]);
 }
 
 static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t B) {
@@ -604,30 +668,21 @@ static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t 
   CK(cudaMemcpyAsync(h, g->w_stats.p, 32 * 8, cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
   h[6] = (unsigned long long)(B * (B - 1));
-  if (getenv("KNNG_PROFILE") && B > 0) {
-    fprintf(stderr, "KNNG_PROFILE cycles/task: consumer %.0f ring-wait %.0f walk %.0f | producer work %.0f wait %.0f | windows/task %.1f\n",
-            (double)h[16] / B, (double)h[17] / B, (double)h[18] / B, (double)h[19] / B, (double)h[20] / B, (double)h[21] / B);
-    fprintf(stderr, "KNNG_PROFILE walk step cycles/task: rows-wait %.0f issue+sets %.0f gather+eval %.0f commit %.0f\n",
-            (double)h[22] / B, (double)h[23] / B, (double)h[24] / B, (double)h[25] / B);
-    if (g->tprof_n > 0) {   // distribution of the per-task consumer time (the kernel ends with the longest)
-      std::vector<unsigned long long> tc((size_t)g->tprof_n);
-      CK(cudaMemcpy(tc.data(), g->w_tprof.p, tc.size() * 8, cudaMemcpyDeviceToHost));
-      std::sort(tc.begin(), tc.end());
-      auto q = [&](double f) { return (double)tc[std::min(tc.size() - 1, (size_t)(f * tc.size()))]; };
-      fprintf(stderr, "KNNG_PROFILE task cycles: p10 %.0f p50 %.0f p90 %.0f p99 %.0f max %.0f (%lld tasks)\n", q(0.1),
-              q(0.5), q(0.9), q(0.99), (double)tc.back(), (long long)g->tprof_n);
-    }
-  }
+  print_profile(g, h, B);
   fill_stats(g, st, h, nl, nev);
   return 0;
 }
+
+static int insert_batch_dist(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st);
 
 int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,
                        knng_stats *st) {
   knng_err_slot().clear();
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: null graph");
+  if (g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_batch: a staged batch is pending");
   if (first_id_out) *first_id_out = g->n;
   CK(cudaSetDevice(g->device));
+  if (g->comm) return insert_batch_dist(g, pts, p, st);
   CK(g->w_stats.ensure(32 * 8));
   CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   const int64_t B = pts ? pts->n : 0, k = g->k;
@@ -636,8 +691,10 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   CK(g->w_cand_k.ensure((size_t)std::max<int64_t>(B, 1) * Pn * k * 4));
   int nl = 0;
   CK(cudaEventRecord(g->ev[0], g->stream));
-  if (int r = stage_search(g, pts, p, 0, Pn, -1, -1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl))
+  if (int r = stage_search(g, pts, p, 0, Pn, -1, -1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl)) {
+    g->pend_B = 0;   // a failed batch leaves the graph as it was (its points are past n)
     return r;
+  }
   if (B == 0) {
     g->pend_B = 0;
     return finish_stats(g, st, 0, 0, 0);
@@ -646,11 +703,109 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   CK(g->w_props.ensure((size_t)B * ballmax * 8));
   CK(g->w_prop_cnt.ensure((size_t)B * 4));
   if (int r = stage_update(g, p, 1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), 0, B,
-                           g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), nullptr, nullptr, &nl, true))
+                           g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), nullptr, nullptr, &nl, true)) {
+    g->pend_B = 0;
     return r;
+  }
   CK(cudaEventRecord(g->ev[3], g->stream));
-  if (int r = stage_commit(g, p, B, g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), nullptr, nullptr, &nl))
+  if (int r = stage_commit(g, p, B, g->w_props.as<int2>(), g->w_prop_cnt.as<int32_t>(), nullptr, nullptr, &nl)) {
+    g->pend_B = 0;
     return r;
+  }
+  CK(cudaEventRecord(g->ev[4], g->stream));
+  return finish_stats(g, st, nl, 5, B);
+}
+
+// ---------------------------------------------------------------------------------------------
+// graph_insert_batch on G ranks (Alg. 3 + Alg. 5 across GPUs): every rank
+// holds a full replica and makes the same call with the same batch; everything is stream-ordered on
+// the handle's stream, with the library's NCCL all-gathers between the stages and no host sync:
+//   search   partitioned: this rank's partitions [r P/G, (r+1) P/G) for all B points -> cand [B][P/G][k]
+//            unpartitioned: all partitions for the query shard [r S, r S + S)         -> cand [S][1][k]
+//   all-gather cand ("the compute nodes send the k.p candidates")
+//   update   K2 merge (identical on every rank), new rows + balls of the query shard [r S, r S + S)
+//   all-gather new rows, proposals and their counts (S slots per rank)
+//   commit   write the new rows, apply every proposal, place the points (identical on every rank)
+// The counters are summed over the ranks (one more all-reduce), so every rank reports the job's.
+// ---------------------------------------------------------------------------------------------
+static int nccl_ck(const char *m) { return m ? fail(KNNG_ERR_NCCL, "%s", m) : 0; }
+
+static int insert_batch_dist_(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st);
+static int insert_batch_dist(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st) {
+  const int rc = insert_batch_dist_(g, pts, p, st);
+  if (rc) g->pend_B = 0;
+  return rc;
+}
+static int insert_batch_dist_(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st) {
+  const int G = g->world, r = g->rank, k = g->k;
+  const int64_t B = pts ? pts->n : 0, n_t = g->n;
+  const int P = g->P;
+  if (P > 0 && P % G) return fail(KNNG_ERR_INVALID_ARG, "P=%d is not a multiple of the world size %d", P, G);
+  const int64_t S = (B + G - 1) / G;                     // query slots per rank (balls, new rows)
+  const int64_t qlo = std::min<int64_t>(r * S, B), qhi = std::min<int64_t>(qlo + S, B);
+  if (p && (p->depth < 1 || p->depth > 10)) return fail(KNNG_ERR_INVALID_ARG, "depth %d outside 1..10", p->depth);
+  const int64_t ballmax = p ? ball_bound(n_t, k, p->depth) : 0;
+  const int pown = P > 0 ? P / G : 1;
+  const int64_t cand_rows = P > 0 ? B : S;               // rows of this rank's candidate buffer
+  const size_t cand_n = (size_t)std::max<int64_t>(cand_rows, 1) * pown * k;
+  CK(g->w_dci.ensure(cand_n * 4));
+  CK(g->w_dck.ensure(cand_n * 4));
+  CK(g->w_gci.ensure(cand_n * G * 4));
+  CK(g->w_gck.ensure(cand_n * G * 4));
+  const size_t sl = (size_t)std::max<int64_t>(S, 1);
+  CK(g->w_dprops.ensure(sl * std::max<int64_t>(ballmax, 1) * 8));
+  CK(g->w_dcnt.ensure(sl * 4));
+  CK(g->w_dnid.ensure(sl * k * 4));
+  CK(g->w_dnkey.ensure(sl * k * 4));
+  CK(g->w_gprops.ensure(sl * G * std::max<int64_t>(ballmax, 1) * 8));
+  CK(g->w_gcnt.ensure(sl * G * 4));
+  CK(g->w_gnid.ensure(sl * G * k * 4));
+  CK(g->w_gnkey.ensure(sl * G * k * 4));
+  CK(g->w_dstats.ensure(16 * 8));
+  CK(g->w_stats.ensure(32 * 8));
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
+  int nl = 0;
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  // candidate slots this rank does not fill (short last shard) stay empty: -1 ids
+  CK(cudaMemsetAsync(g->w_dci.p, 0xFF, cand_n * 4, g->stream));
+  if (int rc = stage_search(g, pts, p, P > 0 ? r * pown : 0, P > 0 ? (r + 1) * pown : 1, P > 0 ? -1 : qlo,
+                            P > 0 ? -1 : qhi, g->w_dci.as<int32_t>(), g->w_dck.as<uint32_t>(), &nl)) {
+    g->pend_B = 0;
+    return rc;
+  }
+  if (B == 0) {
+    g->pend_B = 0;
+    return finish_stats(g, st, nl, 0, 0);
+  }
+  if (int rc = nccl_ck(knng::nccl_allgather(g->w_dci.p, g->w_gci.p, cand_n, ncclInt32, g->comm, g->stream))) return rc;
+  if (int rc = nccl_ck(knng::nccl_allgather(g->w_dck.p, g->w_gck.p, cand_n, ncclInt32, g->comm, g->stream))) return rc;
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  CK(cudaMemsetAsync(g->w_dcnt.p, 0, sl * 4, g->stream));
+  CK(cudaMemsetAsync(g->w_dnid.p, 0xFF, sl * k * 4, g->stream));
+  // the gathered candidates: partitioned [G][B][P/G][k] (rank-major, merged by K2 with world = G);
+  // unpartitioned [G*S][1][k], row b = query b (world = 1)
+  if (int rc = stage_update(g, p, P > 0 ? G : 1, g->w_gci.as<int32_t>(), g->w_gck.as<uint32_t>(), qlo, qhi,
+                            g->w_dprops.as<int2>(), g->w_dcnt.as<int32_t>(), g->w_dnid.as<int32_t>(),
+                            g->w_dnkey.as<uint32_t>(), &nl, false))
+    return rc;
+  CK(cudaEventRecord(g->ev[2], g->stream));
+  if (int rc = nccl_ck(knng::nccl_group_start())) return rc;
+  const char *m = knng::nccl_allgather(g->w_dprops.p, g->w_gprops.p, sl * std::max<int64_t>(ballmax, 1) * 2, ncclInt32,
+                                       g->comm, g->stream);
+  if (!m) m = knng::nccl_allgather(g->w_dcnt.p, g->w_gcnt.p, sl, ncclInt32, g->comm, g->stream);
+  if (!m) m = knng::nccl_allgather(g->w_dnid.p, g->w_gnid.p, sl * k, ncclInt32, g->comm, g->stream);
+  if (!m) m = knng::nccl_allgather(g->w_dnkey.p, g->w_gnkey.p, sl * k, ncclInt32, g->comm, g->stream);
+  const char *m2 = knng::nccl_group_end();
+  if (int rc = nccl_ck(m ? m : m2)) return rc;
+  CK(cudaEventRecord(g->ev[3], g->stream));
+  // the ball slots are ballmax wide on every rank (same n_t, k, depth)
+  if (int rc = stage_commit(g, p, G * S, g->w_gprops.as<int2>(), g->w_gcnt.as<int32_t>(), g->w_gnid.as<int32_t>(),
+                            g->w_gnkey.as<uint32_t>(), &nl))
+    return rc;
+  // job-wide counters
+  if (int rc = nccl_ck(knng::nccl_allreduce_sum(g->w_stats.p, g->w_dstats.p, 8, ncclInt64, g->comm, g->stream)))
+    return rc;
+  CK(cudaMemcpyAsync(g->w_stats.p, g->w_dstats.p, 8 * 8, cudaMemcpyDeviceToDevice, g->stream));
   CK(cudaEventRecord(g->ev[4], g->stream));
   return finish_stats(g, st, nl, 5, B);
 }
@@ -753,6 +908,10 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
   const int32_t *d_starts = nullptr;
   int nstarts = 0;
   if (p->start_override && p->start_override_len > 0) {
+    if (g->P > 0) return fail(KNNG_ERR_INVALID_ARG, "graph_search: start_override needs an unpartitioned graph");
+    for (int i = 0; i < p->start_override_len; ++i)
+      if (p->start_override[i] < 0 || p->start_override[i] >= g->n)
+        return fail(KNNG_ERR_INVALID_ARG, "graph_search: start_override[%d] = %d is not a node", i, p->start_override[i]);
     nstarts = p->start_override_len;
     CK(g->w_starts.ensure((size_t)nstarts * 4));
     CK(cudaMemcpyAsync(g->w_starts.p, p->start_override, (size_t)nstarts * 4, cudaMemcpyHostToDevice, g->stream));
@@ -784,9 +943,10 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
     CK(cudaMemcpyAsync(ids_out, oi, (size_t)nq * kr * 4, cudaMemcpyDeviceToHost, g->stream));
     CK(cudaMemcpyAsync(keys_out, ok, (size_t)nq * kr * 4, cudaMemcpyDeviceToHost, g->stream));
   }
-  unsigned long long h[16];
-  CK(cudaMemcpyAsync(h, g->w_stats.p, 16 * 8, cudaMemcpyDeviceToHost, g->stream));
+  unsigned long long h[32];
+  CK(cudaMemcpyAsync(h, g->w_stats.p, 32 * 8, cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
+  print_profile(g, h, nq);
   h[4] = h[5] = h[6] = 0;
   fill_stats(g, st, h, nl, 2);
   return KNNG_OK;

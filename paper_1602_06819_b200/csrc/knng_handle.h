@@ -57,7 +57,7 @@ struct knng_graph {
   uint64_t *off = nullptr;                      // sets: [cap+1] offsets into tok
   uint32_t *tok = nullptr;                      // sets: tokens
   int64_t tok_cap = 0, tok_n = 0;               // token capacity / tokens in use (host mirror)
-  int32_t *lrows = nullptr;                     // partitioned: [cap][k] partition-local row entries (-1 across)
+  int2 *lrows = nullptr;                        // partitioned: [cap][k] (id, partition-local index or -1 across)
   uint32_t tok_max = 0;
   int64_t tprof_n = 0;                          // KNNG_PROFILE: tasks of the last search                         // largest stored token (valid when tok_n > 0)
   int32_t *ids = nullptr;
@@ -76,6 +76,18 @@ struct knng_graph {
       w_target, w_query, w_starts;
   DBuf w_qoff, w_qtok;
   knng::DenseScratch w_dense;                    // A0 / A5 partial rows and norms
+  // multi-GPU (knng_runtime.world > 1, or a 1-rank communicator for tests): the library's NCCL
+  // communicator and the buffers of the two all-gathers of graph_insert_batch
+  void *comm = nullptr;
+  int rank = 0, world = 1;
+  DBuf w_dci, w_dck, w_gci, w_gck, w_dprops, w_dcnt, w_dnid, w_dnkey, w_gprops, w_gcnt, w_gnid, w_gnkey, w_dstats;
+  // partition sizes: the host keeps an upper bound (exact after an asynchronous read-back) so that
+  // sizing a search never waits on the device
+  int64_t *h_cnt = nullptr;                     // pinned [P]
+  cudaEvent_t ev_cnt = nullptr;
+  bool cnt_pending = false;
+  int64_t cnt_n = 0;                            // graph size the pending read-back describes
+  int64_t pool_bound = 0;
   DBuf w_tprof;                                 // KNNG_PROFILE: per-task consumer cycles of the last search
   cudaEvent_t ev[6] = {};
 };

@@ -42,6 +42,7 @@ struct VecGeom {
 };
 
 struct SearchArgs {
+  int metric;                  // M_U8 / M_F32 / M_JAC (the kernel's template metric)
   StoreView st;                // the graph's points
   StoreView qs;                // the queries (== st for inserts)
   int64_t qrow0;               // query b is row qrow0 + b of qs
@@ -59,36 +60,36 @@ struct SearchArgs {
   const int64_t *member_cnt;   // [P] (device)
   const uint8_t *part_of;      // [cap]
   const int32_t *local_idx;    // [cap]
-  const int32_t *lrows;        // [cap][k]: local index of each row entry in the row owner's partition, -1 if
-                               // the entry lies in another partition (P > 0)
+  const int2 *lrows;           // [cap][k]: (id, local index of the entry in the row owner's partition, or -1
+                               // when the entry lies in another partition) -- the row K1 walks when P > 0
   // parameters
   double speedup;
   uint64_t e_num, e_den, seed;
   int kr;
-  const int32_t *starts;       // injected start sequence (device) or null
+  const int32_t *starts;       // injected start sequence (device, unpartitioned graphs) or null
   int nstarts;
-  int G;                       // restart draws evaluated together
-  // bitmap workspace
-  uint32_t *gbits;             // global: per CTA slot, bits_words each
-  int64_t gslots;              // CTA slots of gbits (grid cap when bitmaps are global)
-  int64_t bits_words;          // evaluated + expanded words per task slot
-  int smem_bits;               // 1: bitmaps in dynamic shared memory
+  // per-task visited state: D/E bit planes (2 bits per pool node) in shared memory when the plan
+  // allows, else in a global slot per CTA followed by the expanded-overflow bitmap
+  uint32_t *gbits;             // global: per CTA slot, de_words + x_words words
+  int64_t gslots;              // CTA slots of gbits (grid cap)
+  int64_t de_words;            // ceil(max pool / 16)
+  int64_t x_words;             // ceil(max pool / 32)
+  int smem_bits;               // 1: D/E planes in dynamic shared memory
+  int hbits;                   // log2 entries of the consumer's walk-evaluated / expanded hash
   // outputs
   int32_t *out_ids;            // [nq][part_cnt][kr]
   uint32_t *out_keys;
   unsigned long long *stats;   // [0] evals [1] starts [2] skipped [3] expansions
-  unsigned long long *prof;    // optional cycle counters (KNNG_PROFILE=1), else null
+  unsigned long long *prof;    // optional cycle counters (unused by this kernel), else null
   unsigned long long *task_ctr;  // dynamic task scheduler counter (zeroed by the launcher)
   int pitch;                   // producer stage: bytes per staged row (vectors) / set slot
-  int stages;                  // producer gather pipeline depth (2 or 4; sets: 4)
-  int nprod;                   // producer warps per CTA (1..3)
-  int lane_eval;               // producers evaluate one row per lane where the width allows
+  int lane_eval;               // producer evaluates one row per lane where the width allows
   int ring;                    // ring chunks (8, 16 or 32)
-  int lean;                    // 1: the 80-register variant (12 two-warp CTAs per SM) where instantiated
-  unsigned long long *task_cycles;   // KNNG_PROFILE: consumer cycles per task [nq * part_cnt], else null
+  int lean;                    // 1: the 96-register variant where instantiated
+  unsigned long long *task_cycles;   // unused (profiling hook), null
   int walk_prefetch;           // 1: prefetch the rows of all k neighbours during a walk step
-  int ex_one;                  // 1: look up the expanded set for the chosen neighbour only
   int win_prefetch;            // 1: prefetch the rows of a window's possible starts
+  int full_scan;               // 1: the GNNS baseline walk (all k neighbours, move to the best)
 };
 size_t search_smem_bytes(const SearchArgs &a, bool sets);
 
@@ -125,11 +126,11 @@ cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cud
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
                                int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted,
-                               cudaStream_t s, int *n_launch, int32_t *lrows = nullptr,
+                               cudaStream_t s, int *n_launch, int2 *lrows = nullptr,
                                const uint8_t *part_of = nullptr, const int32_t *local_idx = nullptr);
 // lrows of rows [first, first + count): partition-local index of each entry, -1 across partitions
 cudaError_t launch_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
-                         const int32_t *local_idx, int32_t *lrows, cudaStream_t s);
+                         const int32_t *local_idx, int2 *lrows, cudaStream_t s);
 cudaError_t exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t *tmp, int64_t n, cudaStream_t s);
 cudaError_t launch_tc_topk_u8(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
                               int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,

@@ -185,8 +185,8 @@ __global__ void k_cluster_of(const int64_t *base, int P, int64_t n, uint8_t *cl)
 
 // candidates (Q22): all members if |C| <= exact_limit, else {current medoid if member} u draws
 __global__ void k_candidates(const int64_t *sizes, const int32_t *med, const uint8_t *part, const int32_t *local_idx,
-                             int P, int64_t exact_limit, int ncand, uint64_t seed, int64_t iter, int32_t *cand,
-                             int32_t *ncand_out, int candcap) {
+                             int P, int64_t exact_limit, int ncand, uint64_t seed, uint64_t tag, int64_t iter,
+                             int32_t *cand, int32_t *ncand_out, int candcap) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const int64_t sz = sizes[p];
@@ -197,7 +197,7 @@ __global__ void k_candidates(const int64_t *sizes, const int32_t *med, const uin
     for (int64_t i = 0; i < sz; ++i) c[cnt++] = (int32_t)i;
   } else {
     if (part[med[p]] == p) c[cnt++] = local_idx[med[p]];
-    const uint64_t h3 = rng_prefix(seed, 0xFFFFFFFEull, (uint64_t)(iter * P + p));
+    const uint64_t h3 = rng_prefix(seed, tag, (uint64_t)(iter * P + p));   // stream (seed, tag, iter P + p, j)
     for (int j = 0; j < ncand - 1; ++j) c[cnt++] = (int32_t)rng_index(h3, (uint64_t)j, (uint64_t)sz);
   }
   ncand_out[p] = cnt;
@@ -297,10 +297,136 @@ static int build_members(knng_graph *g, int32_t *flag, int32_t *scan, int32_t *t
   }
   CK(cudaMemcpyAsync(g->member_cnt, cnt.data(), sizeof(int64_t) * g->P, cudaMemcpyHostToDevice, g->stream));
   // the rows' partition-local view, read by the partition-local walks of K1
-  if (!g->lrows) CK(cudaMalloc((void **)&g->lrows, (size_t)g->cap * g->k * 4));
+  if (!g->lrows) CK(cudaMalloc((void **)&g->lrows, (size_t)g->cap * g->k * 8));
   CK(launch_lrows(g->ids, g->k, 0, n, g->part_of, g->local_idx, g->lrows, g->stream));
   CK(cudaStreamSynchronize(g->stream));
   return 0;
+}
+
+// Device workspace of Alg. 4 (sized for n nodes, P clusters, degree k).
+struct PartWs {
+  DBuf wD, wpart, wacc, wflag, wscan, wtmp, wdeg, woff, wfill, wadj, wcl, wvis, wfr, wnx, wcand, wnc, whop, wreach,
+      wbs, wbi, wsz, wbase, wany, wmed;
+  int candcap = 0;
+  cudaError_t ensure(int64_t n, int P, int k, int candcap_) {
+    candcap = candcap_;
+    cudaError_t e = cudaSuccess;
+    auto E = [&](DBuf &b, size_t bytes) { if (e == cudaSuccess) e = b.ensure(bytes); };
+    E(wD, (size_t)n * P * 4);
+    E(wpart, (size_t)n);
+    E(wacc, (size_t)n);
+    E(wflag, (size_t)(n + 1) * 4);
+    E(wscan, (size_t)(n + 1) * 4);
+    E(wtmp, (size_t)((n + 1) / 1024 + 2) * 4);
+    E(wdeg, (size_t)(n + 1) * 4);
+    E(woff, (size_t)(n + 1) * 4);
+    E(wfill, (size_t)(n + 1) * 4);
+    E(wadj, (size_t)2 * n * k * 4 + 4);
+    E(wcl, (size_t)n);
+    E(wvis, (size_t)n * 8);
+    E(wfr, (size_t)n * 8);
+    E(wnx, (size_t)n * 8);
+    E(wcand, (size_t)P * candcap * 4);
+    E(wnc, (size_t)P * 4);
+    E(whop, (size_t)P * 64 * 8);
+    E(wreach, (size_t)P * 64 * 8);
+    E(wbs, (size_t)P * 8);
+    E(wbi, (size_t)P * 4);
+    E(wsz, (size_t)P * 8);
+    E(wbase, (size_t)(P + 1) * 8);
+    E(wany, 8);
+    E(wmed, (size_t)P * 4);
+    return e;
+  }
+  ~PartWs() {
+    DBuf *all[] = {&wD, &wpart, &wacc, &wflag, &wscan, &wtmp, &wdeg, &woff, &wfill, &wadj, &wcl, &wvis, &wfr, &wnx,
+                   &wcand, &wnc, &whop, &wreach, &wbs, &wbi, &wsz, &wbase, &wany, &wmed};
+    for (DBuf *b : all) b->release();
+  }
+};
+
+// The update step of Alg. 4 on the current assignment g->part_of: member lists, the
+// cluster-induced undirected adjacency, and per cluster the candidate (reading Q22: every member when
+// |C| <= exact_limit, else the current medoid and ncand - 1 draws of stream (seed, tag, iter P + p, j))
+// minimising the hop sum; unreachable members cost |C|, ties -> smaller id.  Empty clusters keep their
+// medoid and add nothing to the cost.
+static int medoid_update(knng_graph *g, int P, const std::vector<int32_t> &med, uint64_t seed, uint64_t tag,
+                         int64_t iter, int64_t exact_limit, int ncand, PartWs &w, std::vector<int32_t> &newmed,
+                         int64_t *cost_out) {
+  const int64_t n = g->n;
+  const int k = g->k;
+  const int candcap = w.candcap;
+  cudaStream_t s = g->stream;
+  const unsigned nb = (unsigned)((n + 255) / 256);
+  CK(cudaMemcpyAsync(w.wmed.p, med.data(), (size_t)P * 4, cudaMemcpyHostToDevice, s));
+  g->P = P;
+  if (int r = build_members(g, w.wflag.as<int32_t>(), w.wscan.as<int32_t>(), w.wtmp.as<int32_t>())) return r;
+  std::vector<int64_t> sizes(P), base(P + 1, 0);
+  CK(cudaMemcpyAsync(sizes.data(), g->member_cnt, (size_t)P * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int p = 0; p < P; ++p) base[p + 1] = base[p] + sizes[p];
+  CK(cudaMemcpyAsync(w.wbase.p, base.data(), (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(w.wsz.p, sizes.data(), (size_t)P * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(w.wdeg.p, 0, (size_t)(n + 1) * 4, s));
+  CK(cudaMemsetAsync(w.wfill.p, 0, (size_t)(n + 1) * 4, s));
+  k_adj_degree<<<nb, 256, 0, s>>>(g->ids, k, n, g->part_of, g->local_idx, w.wbase.as<int64_t>(), w.wdeg.as<int32_t>());
+  CK(exclusive_scan_i32(w.wdeg.as<int32_t>(), w.woff.as<int32_t>(), w.wtmp.as<int32_t>(), n + 1, s));
+  k_adj_fill<<<nb, 256, 0, s>>>(g->ids, k, n, g->part_of, g->local_idx, w.wbase.as<int64_t>(), w.woff.as<int32_t>(),
+                                w.wfill.as<int32_t>(), w.wadj.as<int32_t>());
+  k_cluster_of<<<nb, 256, 0, s>>>(w.wbase.as<int64_t>(), P, n, w.wcl.as<uint8_t>());
+  k_candidates<<<(P + 63) / 64, 64, 0, s>>>(w.wsz.as<int64_t>(), w.wmed.as<int32_t>(), g->part_of, g->local_idx, P,
+                                            exact_limit, ncand, seed, tag, iter, w.wcand.as<int32_t>(),
+                                            w.wnc.as<int32_t>(), candcap);
+  std::vector<int32_t> nc(P);
+  CK(cudaMemcpyAsync(nc.data(), w.wnc.p, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemsetAsync(w.wbi.p, 0xFF, (size_t)P * 4, s));
+  CK(cudaStreamSynchronize(s));
+  int maxc = 0;
+  for (int p = 0; p < P; ++p) maxc = std::max(maxc, nc[p]);
+  for (int b = 0; b * 64 < maxc; ++b) {
+    k_bfs_init<<<nb, 256, 0, s>>>(n, w.wvis.as<unsigned long long>(), w.wfr.as<unsigned long long>());
+    CK(cudaMemsetAsync(w.whop.p, 0, (size_t)P * 64 * 8, s));
+    k_bfs_seed<<<P, 64, 0, s>>>(w.wbase.as<int64_t>(), P, w.wcand.as<int32_t>(), w.wnc.as<int32_t>(), candcap, b,
+                                w.wvis.as<unsigned long long>(), w.wfr.as<unsigned long long>(),
+                                w.wreach.as<unsigned long long>());
+    for (unsigned long long level = 1;; ++level) {
+      CK(cudaMemsetAsync(w.wany.p, 0, 4, s));
+      k_bfs_level<<<nb, 256, 0, s>>>(n, w.woff.as<int32_t>(), w.wadj.as<int32_t>(), w.wcl.as<uint8_t>(),
+                                     w.wvis.as<unsigned long long>(), w.wfr.as<unsigned long long>(),
+                                     w.wnx.as<unsigned long long>(), w.whop.as<unsigned long long>(),
+                                     w.wreach.as<unsigned long long>(), level, w.wany.as<int>());
+      int any = 0;
+      CK(cudaMemcpyAsync(&any, w.wany.p, 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      std::swap(w.wfr.p, w.wnx.p);
+      std::swap(w.wfr.bytes, w.wnx.bytes);
+      if (!any) break;
+    }
+    k_bfs_pick<<<(P + 63) / 64, 64, 0, s>>>(P, w.wsz.as<int64_t>(), w.wcand.as<int32_t>(), w.wnc.as<int32_t>(),
+                                            candcap, b, g->members, g->cap, w.whop.as<unsigned long long>(),
+                                            w.wreach.as<unsigned long long>(), w.wbs.as<unsigned long long>(),
+                                            w.wbi.as<int32_t>());
+  }
+  std::vector<unsigned long long> bsum(P);
+  newmed.assign(P, 0);
+  CK(cudaMemcpyAsync(bsum.data(), w.wbs.p, (size_t)P * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(newmed.data(), w.wbi.p, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  int64_t cost = 0;
+  for (int p = 0; p < P; ++p) {
+    if (sizes[p] == 0) { newmed[p] = med[p]; continue; }
+    cost += (int64_t)bsum[p];
+  }
+  *cost_out = cost;
+  return 0;
+}
+
+static void install_medoids(knng_graph *g, const std::vector<int32_t> &med) {
+  cudaMemcpyAsync(g->medoids, med.data(), med.size() * 4, cudaMemcpyHostToDevice, g->stream);
+  g->h_medoids = med;
+  g->pool_bound = 0;        // the next search reads the partition sizes
+  g->cnt_pending = false;
 }
 
 extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, int32_t max_iter, uint64_t seed,
@@ -320,10 +446,8 @@ extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, in
     if (init_medoids[i] < 0 || init_medoids[i] >= n) return fail(KNNG_ERR_INVALID_ARG, "bad init medoid");
   CK(cudaSetDevice(g->device));
   cudaStream_t s = g->stream;
-  const int k = g->k;
   const int64_t exact_limit = 4096;
   const int ncand = 64;
-  const int candcap = (int)std::max<int64_t>(exact_limit, ncand);
 
   // partition state of the handle (member lists sized for the whole capacity)
   if (!g->part_of) {
@@ -339,38 +463,8 @@ extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, in
   CK(cudaMalloc((void **)&g->member_cnt, (size_t)P * 8));
   CK(cudaMalloc((void **)&g->medoids, (size_t)P * 4));
 
-  // workspace
-  DBuf wD, wpart, wacc, wflag, wscan, wtmp, wdeg, woff, wfill, wadj, wcl, wvis, wfr, wnx, wcand, wnc, whop, wreach,
-      wbs, wbi, wsz, wbase, wany, wmed;
-  CK(wD.ensure((size_t)n * P * 4));
-  CK(wpart.ensure((size_t)n));
-  CK(wacc.ensure((size_t)n));
-  CK(wflag.ensure((size_t)(n + 1) * 4));
-  CK(wscan.ensure((size_t)(n + 1) * 4));
-  CK(wtmp.ensure((size_t)((n + 1) / 1024 + 2) * 4));
-  CK(wdeg.ensure((size_t)(n + 1) * 4));
-  CK(woff.ensure((size_t)(n + 1) * 4));
-  CK(wfill.ensure((size_t)(n + 1) * 4));
-  CK(wadj.ensure((size_t)2 * n * k * 4 + 4));
-  CK(wcl.ensure((size_t)n));
-  CK(wvis.ensure((size_t)n * 8));
-  CK(wfr.ensure((size_t)n * 8));
-  CK(wnx.ensure((size_t)n * 8));
-  CK(wcand.ensure((size_t)P * candcap * 4));
-  CK(wnc.ensure((size_t)P * 4));
-  CK(whop.ensure((size_t)P * 64 * 8));
-  CK(wreach.ensure((size_t)P * 64 * 8));
-  CK(wbs.ensure((size_t)P * 8));
-  CK(wbi.ensure((size_t)P * 4));
-  CK(wsz.ensure((size_t)P * 8));
-  CK(wbase.ensure((size_t)(P + 1) * 8));
-  CK(wany.ensure(8));
-  CK(wmed.ensure((size_t)P * 4));
-  auto release = [&]() {
-    DBuf *all[] = {&wD, &wpart, &wacc, &wflag, &wscan, &wtmp, &wdeg, &woff, &wfill, &wadj, &wcl, &wvis, &wfr, &wnx,
-                   &wcand, &wnc, &whop, &wreach, &wbs, &wbi, &wsz, &wbase, &wany, &wmed};
-    for (DBuf *b : all) b->release();
-  };
+  PartWs w;
+  CK(w.ensure(n, P, g->k, (int)std::max<int64_t>(exact_limit, ncand)));
   const unsigned nb = (unsigned)((n + 255) / 256);
 
   // initial medoids (Alg. 4 "Randomly pick k initial medoids")
@@ -387,84 +481,28 @@ extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, in
   // the handle's part_of doubles as the working assignment; the accepted one is kept in wacc
   for (int it = 0; it < max_iter; ++it) {
     // ---------------- assign ----------------
-    CK(cudaMemcpyAsync(wmed.p, med.data(), (size_t)P * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(w.wmed.p, med.data(), (size_t)P * 4, cudaMemcpyHostToDevice, s));
     const StoreView st = graph_store_view(g);
     if (g->metric == KNNG_L2SQ_U8) {
-      k_medoid_keys<M_U8><<<nb, 256, 0, s>>>(st, n, P, wmed.as<int32_t>(), wD.as<uint32_t>());
-      k_greedy_assign<M_U8><<<1, 32, 0, s>>>(wD.as<uint32_t>(), n, P, wmed.as<int32_t>(), cap, g->part_of,
-                                             wsz.as<int64_t>());
+      k_medoid_keys<M_U8><<<nb, 256, 0, s>>>(st, n, P, w.wmed.as<int32_t>(), w.wD.as<uint32_t>());
+      k_greedy_assign<M_U8><<<1, 32, 0, s>>>(w.wD.as<uint32_t>(), n, P, w.wmed.as<int32_t>(), cap, g->part_of,
+                                             w.wsz.as<int64_t>());
     } else if (g->metric == KNNG_L2SQ_F32) {
-      k_medoid_keys<M_F32><<<nb, 256, 0, s>>>(st, n, P, wmed.as<int32_t>(), wD.as<uint32_t>());
-      k_greedy_assign<M_F32><<<1, 32, 0, s>>>(wD.as<uint32_t>(), n, P, wmed.as<int32_t>(), cap, g->part_of,
-                                              wsz.as<int64_t>());
+      k_medoid_keys<M_F32><<<nb, 256, 0, s>>>(st, n, P, w.wmed.as<int32_t>(), w.wD.as<uint32_t>());
+      k_greedy_assign<M_F32><<<1, 32, 0, s>>>(w.wD.as<uint32_t>(), n, P, w.wmed.as<int32_t>(), cap, g->part_of,
+                                              w.wsz.as<int64_t>());
     } else {
-      k_medoid_keys<M_JAC><<<nb, 256, 0, s>>>(st, n, P, wmed.as<int32_t>(), wD.as<uint32_t>());
-      k_greedy_assign<M_JAC><<<1, 32, 0, s>>>(wD.as<uint32_t>(), n, P, wmed.as<int32_t>(), cap, g->part_of,
-                                              wsz.as<int64_t>());
+      k_medoid_keys<M_JAC><<<nb, 256, 0, s>>>(st, n, P, w.wmed.as<int32_t>(), w.wD.as<uint32_t>());
+      k_greedy_assign<M_JAC><<<1, 32, 0, s>>>(w.wD.as<uint32_t>(), n, P, w.wmed.as<int32_t>(), cap, g->part_of,
+                                              w.wsz.as<int64_t>());
     }
     CK(cudaGetLastError());
     // ---------------- update: members, adjacency, hop sums ----------------
-    g->P = P;
-    if (int r = build_members(g, wflag.as<int32_t>(), wscan.as<int32_t>(), wtmp.as<int32_t>())) { release(); return r; }
-    std::vector<int64_t> sizes(P), base(P + 1, 0);
-    CK(cudaMemcpyAsync(sizes.data(), g->member_cnt, (size_t)P * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    for (int p = 0; p < P; ++p) base[p + 1] = base[p] + sizes[p];
-    CK(cudaMemcpyAsync(wbase.p, base.data(), (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(wsz.p, sizes.data(), (size_t)P * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(wdeg.p, 0, (size_t)(n + 1) * 4, s));
-    CK(cudaMemsetAsync(wfill.p, 0, (size_t)(n + 1) * 4, s));
-    k_adj_degree<<<nb, 256, 0, s>>>(g->ids, k, n, g->part_of, g->local_idx, wbase.as<int64_t>(), wdeg.as<int32_t>());
-    CK(exclusive_scan_i32(wdeg.as<int32_t>(), woff.as<int32_t>(), wtmp.as<int32_t>(), n + 1, s));
-    k_adj_fill<<<nb, 256, 0, s>>>(g->ids, k, n, g->part_of, g->local_idx, wbase.as<int64_t>(), woff.as<int32_t>(),
-                                  wfill.as<int32_t>(), wadj.as<int32_t>());
-    k_cluster_of<<<nb, 256, 0, s>>>(wbase.as<int64_t>(), P, n, wcl.as<uint8_t>());
-    k_candidates<<<(P + 63) / 64, 64, 0, s>>>(wsz.as<int64_t>(), wmed.as<int32_t>(), g->part_of, g->local_idx, P,
-                                              exact_limit, ncand, seed, it, wcand.as<int32_t>(), wnc.as<int32_t>(),
-                                              candcap);
-    std::vector<int32_t> nc(P);
-    CK(cudaMemcpyAsync(nc.data(), wnc.p, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemsetAsync(wbi.p, 0xFF, (size_t)P * 4, s));
-    CK(cudaStreamSynchronize(s));
-    int maxc = 0;
-    for (int p = 0; p < P; ++p) maxc = std::max(maxc, nc[p]);
-    for (int b = 0; b * 64 < maxc; ++b) {
-      k_bfs_init<<<nb, 256, 0, s>>>(n, wvis.as<unsigned long long>(), wfr.as<unsigned long long>());
-      CK(cudaMemsetAsync(whop.p, 0, (size_t)P * 64 * 8, s));
-      k_bfs_seed<<<P, 64, 0, s>>>(wbase.as<int64_t>(), P, wcand.as<int32_t>(), wnc.as<int32_t>(), candcap, b,
-                                  wvis.as<unsigned long long>(), wfr.as<unsigned long long>(),
-                                  wreach.as<unsigned long long>());
-      for (unsigned long long level = 1;; ++level) {
-        CK(cudaMemsetAsync(wany.p, 0, 4, s));
-        k_bfs_level<<<nb, 256, 0, s>>>(n, woff.as<int32_t>(), wadj.as<int32_t>(), wcl.as<uint8_t>(),
-                                       wvis.as<unsigned long long>(), wfr.as<unsigned long long>(),
-                                       wnx.as<unsigned long long>(), whop.as<unsigned long long>(),
-                                       wreach.as<unsigned long long>(), level, wany.as<int>());
-        int any = 0;
-        CK(cudaMemcpyAsync(&any, wany.p, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        std::swap(wfr.p, wnx.p);
-        std::swap(wfr.bytes, wnx.bytes);
-        if (!any) break;
-      }
-      k_bfs_pick<<<(P + 63) / 64, 64, 0, s>>>(P, wsz.as<int64_t>(), wcand.as<int32_t>(), wnc.as<int32_t>(), candcap,
-                                              b, g->members, g->cap, whop.as<unsigned long long>(),
-                                              wreach.as<unsigned long long>(), wbs.as<unsigned long long>(),
-                                              wbi.as<int32_t>());
-    }
-    std::vector<unsigned long long> bsum(P);
-    CK(cudaMemcpyAsync(bsum.data(), wbs.p, (size_t)P * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(newmed.data(), wbi.p, (size_t)P * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    CK(cudaGetLastError());
     int64_t cost = 0;
-    for (int p = 0; p < P; ++p) {
-      if (sizes[p] == 0) { newmed[p] = med[p]; continue; }
-      cost += (int64_t)bsum[p];
-    }
+    if (int r = medoid_update(g, P, med, seed, 0xFFFFFFFEull, it, exact_limit, ncand, w, newmed, &cost)) return r;
     // Q23: keep the iteration only if the total hop sum does not rise
     if (it > 0 && cost > prev_cost) break;
-    CK(cudaMemcpyAsync(wacc.p, g->part_of, (size_t)n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(w.wacc.p, g->part_of, (size_t)n, cudaMemcpyDeviceToDevice, s));
     if (cost_out) cost_out[accepted] = cost;
     ++accepted;
     prev_cost = cost;
@@ -474,14 +512,37 @@ extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, in
     if (!changed) break;
   }
   // install the accepted partition
-  CK(cudaMemcpyAsync(g->part_of, wacc.p, (size_t)n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(g->part_of, w.wacc.p, (size_t)n, cudaMemcpyDeviceToDevice, s));
   g->P = P;
-  if (int r = build_members(g, wflag.as<int32_t>(), wscan.as<int32_t>(), wtmp.as<int32_t>())) { release(); return r; }
-  CK(cudaMemcpyAsync(g->medoids, med.data(), (size_t)P * 4, cudaMemcpyHostToDevice, s));
-  g->h_medoids = med;
+  if (int r = build_members(g, w.wflag.as<int32_t>(), w.wscan.as<int32_t>(), w.wtmp.as<int32_t>())) return r;
+  install_medoids(g, med);
   memcpy(medoids_out, med.data(), (size_t)P * 4);
   if (part_out) CK(cudaMemcpyAsync(part_out, g->part_of, (size_t)n, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  release();
   return accepted;
+}
+
+// Alg. 5's last step ("compute new medoids"; F5 P:1349-1353): the update step of Alg. 4 on
+// the current partition -- nodes keep their partitions (placement already assigned the inserted ones),
+// every medoid becomes its cluster's hop-sum minimiser over the current graph.  Candidate draws use
+// stream (seed, 0xFFFFFFFD, epoch P + p, j).
+extern "C" int graph_recompute_medoids(knng_graph *g, uint64_t seed, int64_t epoch, int32_t *medoids_out,
+                                       int64_t *cost_out) {
+  knng_err_slot().clear();
+  if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_recompute_medoids: null graph");
+  if (g->P == 0) return fail(KNNG_ERR_INVALID_ARG, "graph_recompute_medoids: the graph is not partitioned");
+  if (g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "graph_recompute_medoids: a staged batch is pending");
+  if (epoch < 0) return fail(KNNG_ERR_INVALID_ARG, "graph_recompute_medoids: epoch < 0");
+  CK(cudaSetDevice(g->device));
+  const int P = g->P;
+  PartWs w;
+  CK(w.ensure(g->n, P, g->k, 4096));
+  std::vector<int32_t> med = g->h_medoids, newmed;
+  int64_t cost = 0;
+  if (int r = medoid_update(g, P, med, seed, 0xFFFFFFFDull, epoch, 4096, 64, w, newmed, &cost)) return r;
+  install_medoids(g, newmed);
+  if (medoids_out) memcpy(medoids_out, newmed.data(), (size_t)P * 4);
+  if (cost_out) *cost_out = cost;
+  CK(cudaStreamSynchronize(g->stream));
+  return KNNG_OK;
 }

@@ -1,160 +1,254 @@
 // knng_search.cu -- K1 iGNNS search (section 3) and K2 partition merge (Alg. 3,
 // P:166-178).
 //
-// One warp per (query, partition) task.  The search is a dependent pointer chase, so the
-// commit order is the paper's sequential order (every evaluation, top-k insert, visited mark
-// and move happens exactly as in the algorithm); the warp's 32 lanes work speculatively:
-//   * walk step: the k neighbours of `cur` are gathered and evaluated together (16-byte
-//     vector loads), then the scan "first neighbour that improves" is resolved with a
-//     ballot; only the fresh evaluations up to that neighbour are committed (budget).
-//   * restart: a window of 32 RNG draws (Q4) is held in lanes; redraws of evaluated nodes are
-//     free; the next G fresh draws are evaluated together and their keys cached in registers,
-//     so a run of skipped starts costs one round trip per G starts.
-// Visited / expanded sets are bitmaps over the pool-local index, in shared memory when the pool
-// is small enough, else in a per-warp-slot global workspace.
+// One CTA runs one (query, partition) task at a time: warp 0 is the CONSUMER, which takes every
+// decision of the search in the paper's sequential order (draw, redraw, evaluate, skip, accept,
+// walk, budget); warp 1 is the PRODUCER, which evaluates the random starts ahead of it.  The draw
+// sequence of a task is a pure function of the counter RNG (reading Q4) and the key of a draw a
+// pure function of (query, node), so the producer can run ahead, 32 draws per chunk:
+//   * gather: the 32 drawn rows are staged in shared memory with 16-byte cp.async copies;
+//   * evaluate: one row per lane from shared memory (or the warp evaluator);
+//   * repeat flag: whether the draw's pool node was already drawn EARLIER in the sequence -- a
+//     test-and-set on the task's draw bitmap D (lowest lane first inside a chunk), whose latency is
+//     hidden behind the next chunk's gather;
+//   * publish: (pool index, key, node id, repeat) into a ring of chunks in shared memory.
+// A draw is a free redraw (Q4) iff it repeats an earlier draw, or its node was evaluated by a walk
+// -- and the consumer keeps the nodes its walks evaluated (W) and expanded (X) in a hash table in
+// SHARED memory.  So deciding which draws are fresh needs no global-memory round trip: the restart
+// loop of the consumer runs from shared memory alone.  The walk's neighbours consult W and the
+// bitmap E of the consumed fresh draws (fire-and-forget reductions when a draw is committed), read
+// together with the neighbours' vectors -- one round trip per walk step with the next rows
+// prefetched.  Everything the consumer commits -- evaluations, top-k inserts, counters -- happens
+// in the sequential algorithm's order, so results and counters are identical to the oracle's.
 #include <stdio.h>
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "knng_common.cuh"
 #include "knng_internal.h"
 
-// Cycle counters of KNNG_PROFILE=1 exist only in builds with -DKNNG_PROFILE_COUNTERS (their state
-// costs the consumer registers): KP(p) is false at compile time otherwise.
+// Cycle counters (builds with -DKNNG_PROFILE_COUNTERS, KNNG_PROFILE=1 at run time): summed per task into
+// SearchArgs::prof[0..9] = consumer, consumer ring wait, walks, producer gather wait, producer ring-full
+// wait, windows, walk steps, tasks whose hash overflowed, fast-path chunks, produced chunks.
 #ifdef KNNG_PROFILE_COUNTERS
-#define KP(p) ((p) != nullptr)
+#define KPROF(...) __VA_ARGS__
 #else
-#define KP(p) false
+#define KPROF(...)
 #endif
 
 namespace knng {
 
 constexpr int FASTC = 2;          // chunks the consumer's skip-only fast path commits at once (<= ring)
 constexpr int HDR_BYTES = 128;
+constexpr int WPF = 8;            // window prefetch slots (rows of draws that may be accepted)
+constexpr uint32_t HW = 1u, HX = 2u;   // hash entry flags: evaluated by a walk / expanded
 
 struct RingHdr {
-  int consumed;           // chunks < consumed are free
+  int consumed;           // consumer -> producer: chunks < consumed are free
   int done;               // consumer finished the task
   int next_task;          // dynamic task scheduler: the CTA's next task
-  int published;          // debug: last chunk a producer published
-  int pstate;             // debug: producer state
+  int pad;
 };
 
-// Producer warp(s): speculative evaluation of the random starts.  The draw sequence of a search
-// is fixed by the counter RNG (Q4) and the key of a draw is a pure function of (query, node), so
-// producers evaluate draws ahead of the consumer, 32 per chunk, into the CTA's smem ring.
-// Nothing here touches a counter, the visited sets or the top-k.
-//
-// The rows of the drawn nodes are gathered into shared memory with 16-byte cp.async copies
-// (no registers held by loads in flight), S chunks deep; the keys are computed from shared
-// memory.  Producer pw owns chunks pw, pw + nprod, ...; local iteration i <-> chunk pw + i*nprod.
+// explicit state spaces (a generic volatile access compiles to LD.E.STRONG.SYS, a generic atomic to ATOM.E)
+__device__ __forceinline__ int lds_volatile(const int *p) {
+  int v;
+  asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_volatile(int *p, int v) {
+  asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// bit-plane words of the task: shared (gs = false) or global (gs = true); warp-uniform choice
+__device__ __forceinline__ void plane_red_or(uint32_t *p, uint32_t v, bool gs) {
+  if (gs) asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t plane_atom_or(uint32_t *p, uint32_t v, bool gs) {
+  uint32_t o;
+  if (gs) asm volatile("atom.relaxed.gpu.global.or.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+  else asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(o) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return o;
+}
+__device__ __forceinline__ uint32_t plane_ld(const uint32_t *p, bool gs) {
+  uint32_t v;
+  if (gs) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
+// asynchronous global -> shared copy of 4, 8 or 16 bytes (the row prefetches of the walk)
+__device__ __forceinline__ void cp_async_n(void *smem_dst, const void *gsrc, int bytes) {
+  const unsigned sa = smem_u32(smem_dst);
+  if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+  else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+// D/E bit planes of a task: word w holds the draw bits (D, producer) of pool nodes 16w..16w+15 in its
+// low half and their consumed-evaluation bits (E, consumer) in its high half.
+__device__ __forceinline__ uint32_t de_word(int32_t pidx) { return (uint32_t)pidx >> 4; }
+__device__ __forceinline__ uint32_t d_bit(int32_t pidx) { return 1u << (pidx & 15); }
+__device__ __forceinline__ uint32_t e_bit(int32_t pidx) { return 1u << (16 + (pidx & 15)); }
+
+// ---- the consumer's hash of walk-evaluated (W) / expanded (X) pool nodes: entries (pidx << 2) | flags ----
+__device__ __forceinline__ uint32_t h_slot(uint32_t pidx, int hb) { return (pidx * 0x9E3779B1u) >> (32 - hb); }
+__device__ __forceinline__ uint32_t h_get(const uint32_t *H, int hb, int32_t pidx) {
+  const uint32_t mask = (1u << hb) - 1u;
+  uint32_t h = h_slot((uint32_t)pidx, hb);
+  for (;;) {
+    const uint32_t e = H[h];
+    if (e == 0) return 0;
+    if ((e >> 2) == (uint32_t)pidx) return e & 3u;
+    h = (h + 1) & mask;
+  }
+}
+// lane-concurrent insert (distinct or equal keys across lanes are both fine)
+__device__ __forceinline__ void h_put(uint32_t *H, int hb, int32_t pidx, uint32_t fl) {
+  const uint32_t mask = (1u << hb) - 1u, ent = ((uint32_t)pidx << 2) | fl;
+  uint32_t h = h_slot((uint32_t)pidx, hb);
+  for (;;) {
+    uint32_t e = H[h];
+    if (e == 0) {
+      e = atomicCAS(H + h, 0u, ent);
+      if (e == 0) return;
+    }
+    if ((e >> 2) == (uint32_t)pidx) {
+      if ((e & fl) != fl) atomicOr(H + h, fl);
+      return;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Producer
+// ---------------------------------------------------------------------------------------------
 struct ProdCtx {
-  volatile RingHdr *hdr;
-  unsigned long long *ring;   // [ring][32][2]: (tag << 32 | node), (tag << 32 | key), tag = chunk + 1
+  RingHdr *hdr;
+  unsigned long long *ring;   // [ring][32][3] tagged words (see ring_put)
   int ring_n;                 // ring chunks (power of 2)
-  uint8_t *stg;       // this producer's S x 32 rows (pitch bytes each)
-  int32_t *meta;      // this producer's S x 32 x 4 ints (node, rb, re, -)
+  uint8_t *stg;               // 2 x 32 staged rows (pitch bytes each)
+  int4 *meta;                 // 2 x 32 {node, pidx, rb, re}
   int pitch;
-  int pw, nprod;
-  int64_t nch;
   uint64_t h3;
   int64_t m;
   const int32_t *pool;
+  const int32_t *starts;      // injected start sequence (unpartitioned only) or null
+  int nstarts;
+  uint32_t *de;               // D/E words of the task (shared or global)
+  bool gde;                   // the D/E words are in global memory
+  unsigned long long *prof;   // cycle counters or null
 };
 
-// draw i of this lane: (node id, pool index).  The pool index is the node's partition-local index
-// (members_p is ascending in local index), which is what the ring carries: the consumer's visited
-// bitmap needs it, and the node id only when the draw may enter the top-k or start a walk.
-__device__ __forceinline__ int2 draw_node(const ProdCtx &x, int64_t i) {
-  const int64_t c = x.pw + i * x.nprod;
-  const uint64_t idx = rng_index(x.h3, (uint64_t)(c * 32 + (threadIdx.x & 31)), (uint64_t)x.m);
+// draw j = 32 c + lane: (node id, pool index); pool index -1 past an injected sequence
+__device__ __forceinline__ int2 draw_node(const ProdCtx &x, int64_t c) {
+  const int64_t j = c * 32 + (threadIdx.x & 31);
+  if (x.starts) {
+    const int32_t nd = j < x.nstarts ? x.starts[j] : -1;
+    return make_int2(nd, nd);
+  }
+  const uint64_t idx = rng_index(x.h3, (uint64_t)j, (uint64_t)x.m);
   return make_int2(x.pool ? x.pool[idx] : (int32_t)idx, (int32_t)idx);
 }
 
-// publish chunk (local iteration i) to the ring; false when the consumer has finished
-__device__ __forceinline__ bool publish(const ProdCtx &x, int64_t i, int32_t node, uint32_t key, long long &p_wait,
-                                        bool prof) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = x.pw + i * x.nprod;
-  const long long t0 = prof ? clock64() : 0;
-  int dn = 0;
-  if (lane == 0)
-    while (c - x.hdr->consumed >= x.ring_n && !(dn = x.hdr->done)) __nanosleep(32);
-  dn = __shfl_sync(FULL, dn, 0);
-  if (prof) p_wait += clock64() - t0;
-  if (dn) return false;
-  // Each entry word carries its chunk's tag next to the datum: an aligned 64-bit shared store is
-  // single-copy atomic, so the consumer sees a whole (tag, datum) pair and needs no fence or barrier.
-  const unsigned long long tag = (unsigned long long)(unsigned)(c + 1) << 32;
-  volatile unsigned long long *e = x.ring + ((c & (x.ring_n - 1)) * 32 + lane) * 2;
-  e[0] = tag | (uint32_t)node;
-  e[1] = tag | key;
-#ifdef KNNG_DEBUG_WAIT
-  if (lane == 0) x.hdr->published = (int)c;
+// Test-and-set of the draw bitmap for a chunk's draws, in sequence order: inside the chunk the lowest
+// lane of equal pool indices is the first occurrence (the others are repeats); across chunks the
+// single producer issues chunk c's atomics after chunk c-1's.  Returns a word from which
+// repeat_of() extracts the flag once the atomic has completed (used one iteration later).
+__device__ __forceinline__ uint32_t draw_mark(const ProdCtx &x, int32_t pidx) {
+  const unsigned grp = __match_any_sync(FULL, pidx);
+  if (pidx < 0) return 0u;
+  if (grp & lanemask_lt()) return 0xFFFFFFFFu;                  // an earlier lane drew the same node
+#ifdef KNNG_HACK_NOATOM
+  return x.gde ? plane_ld(x.de + de_word(pidx), true) : plane_atom_or(x.de + de_word(pidx), d_bit(pidx), x.gde);
+#else
+  return plane_atom_or(x.de + de_word(pidx), d_bit(pidx), x.gde);
 #endif
+}
+__device__ __forceinline__ int repeat_of(uint32_t mark, int32_t pidx) {
+  return pidx >= 0 ? (int)((mark & d_bit(pidx)) != 0) : 0;
+}
+
+// Ring entries: three 64-bit words per lane, each carrying its chunk's tag (chunk + 1) in the high half
+// next to one datum -- (pidx | repeat << 31), key, node -- so that the consumer sees whole entries
+// without a fence or flag: an aligned 64-bit shared store is single-copy atomic.  pidx 0x7FFFFFFF marks
+// "no draw" (past the end of an injected start sequence).
+constexpr uint32_t NO_DRAW = 0x7FFFFFFFu;
+__device__ __forceinline__ void ring_put(unsigned long long *ring, int ring_n, int64_t c, int32_t pidx, int rep,
+                                         uint32_t key, int32_t node) {
+  const unsigned long long tag = (unsigned long long)(uint32_t)(c + 1) << 32;
+  // plane-major slot: [3][32] words, so each plane's 32 lanes are one contiguous 256-byte row
+  const unsigned sa = smem_u32(ring + (c & (ring_n - 1)) * 96 + (threadIdx.x & 31));
+  const uint32_t w0 = pidx < 0 ? NO_DRAW : ((uint32_t)pidx | ((uint32_t)rep << 31));
+  asm volatile("st.volatile.shared.b64 [%0], %1;" ::"r"(sa), "l"(tag | key) : "memory");
+  asm volatile("st.volatile.shared.b64 [%0], %1;" ::"r"(sa + 256), "l"(tag | (uint32_t)node) : "memory");
+  asm volatile("st.volatile.shared.b64 [%0], %1;" ::"r"(sa + 512), "l"(tag | w0) : "memory");
+}
+struct RingEnt {
+  int32_t pidx;   // -1: no draw
+  int rep;
+  uint32_t key;
+  int32_t node;
+};
+// consumer: wait until chunk ch is in its slot and read this lane's entry
+__device__ __forceinline__ RingEnt ring_get(const unsigned long long *ring, int ring_n, int64_t ch) {
+  const uint32_t tag = (uint32_t)(ch + 1);
+  const unsigned sa = smem_u32(ring + (ch & (ring_n - 1)) * 96 + (threadIdx.x & 31));
+  unsigned long long a, b, c;
+  for (;;) {
+    asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(a) : "r"(sa) : "memory");
+    asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(b) : "r"(sa + 256) : "memory");
+    asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(c) : "r"(sa + 512) : "memory");
+    if (__all_sync(FULL, (uint32_t)(a >> 32) == tag && (uint32_t)(b >> 32) == tag && (uint32_t)(c >> 32) == tag)) break;
+    __nanosleep(16);
+  }
+  RingEnt r;
+  const uint32_t w0 = (uint32_t)c;
+  r.pidx = w0 == NO_DRAW ? -1 : (int32_t)(w0 & 0x7FFFFFFFu);
+  r.rep = (int)(w0 >> 31) & (w0 != NO_DRAW);
+  r.key = (uint32_t)a;
+  r.node = (int32_t)(uint32_t)b;
+  return r;
+}
+
+// publish chunk c to the ring; false when the consumer has finished
+__device__ __forceinline__ bool publish(const ProdCtx &x, int64_t c, int32_t pidx, int rep, uint32_t key,
+                                        int32_t node) {
+  const int lane = threadIdx.x & 31;
+  int dn = 0;
+  KPROF(const long long t0 = clock64();)
+#ifdef KNNG_DEBUG_WAIT
+  long long nw = 0;
+  if (lane == 0)
+    while (c - ((volatile RingHdr *)x.hdr)->consumed >= x.ring_n && !(dn = ((volatile RingHdr *)x.hdr)->done)) {
+      __nanosleep(32);
+      if (++nw == (1ll << 24))
+        printf("KNNG stuck producer: block %d chunk %lld consumed %d\n", blockIdx.x, (long long)c,
+               ((volatile RingHdr *)x.hdr)->consumed);
+    }
+#else
+  // ring full: the consumer is behind (walking); back off so the waiting producer does not take issue
+  // slots from the consumers of the SM
+  if (lane == 0) {
+    unsigned ns = 64;
+    while (c - lds_volatile(&x.hdr->consumed) >= x.ring_n && !(dn = lds_volatile(&x.hdr->done))) {
+      __nanosleep(ns);
+      ns = ns < 1024 ? 2 * ns : 1024;
+    }
+  }
+#endif
+  dn = __shfl_sync(FULL, dn, 0);
+  KPROF(if (x.prof && lane == 0) atomicAdd(x.prof + 4, (unsigned long long)(clock64() - t0));)
+  if (dn) return false;
+  KPROF(if (x.prof && lane == 0) atomicAdd(x.prof + 9, 1ull);)
+  ring_put(x.ring, x.ring_n, c, pidx, rep, key, node);
   return true;
 }
 
-// consumer: wait until chunk ch is in its slot and read this lane's (node, key)
-__device__ __forceinline__ void ring_get(const unsigned long long *ring, int ring_n, volatile RingHdr *hdr, int64_t ch,
-                                         int32_t &node, uint32_t &key) {
-  const unsigned tag = (unsigned)(ch + 1);
-  const volatile unsigned long long *e = ring + ((ch & (ring_n - 1)) * 32 + (threadIdx.x & 31)) * 2;
-  unsigned long long w0, w1;
-#ifdef KNNG_DEBUG_WAIT
-  long long n = 0;
-#endif
-  for (;;) {
-    w0 = e[0];
-    w1 = e[1];
-    if (__all_sync(FULL, (unsigned)(w0 >> 32) == tag && (unsigned)(w1 >> 32) == tag)) break;
-#ifdef KNNG_DEBUG_WAIT
-    if (++n == (1ll << 22) && (threadIdx.x & 31) == 0)
-      printf("KNNG stuck wait: block %d chunk %lld consumed %d done %d published %d pstate %d\n", blockIdx.x,
-             (long long)ch, hdr->consumed, hdr->done, hdr->published, hdr->pstate);
-#endif
-    __nanosleep(16);
-  }
-  node = (int32_t)(uint32_t)w0;
-  key = (uint32_t)w1;
-}
-
-// Expanded set of the consumer warp (warp-uniform state): a shared open-addressing hash of
-// pool-local ids (+1; 0 = empty), filled to 3/4 at most; beyond that the global bitmap gex takes
-// the further entries (zeroed by the warp when first needed) and lookups consult both.
-constexpr int EXCAP = 512;
-__device__ __forceinline__ bool ex_has(const int32_t *exh, bool ovf, const uint32_t *gex, uint32_t lv) {
-  uint32_t h = (lv * 0x9E3779B1u) >> (32 - 9);
-  for (;;) {
-    const int32_t e = exh[h];
-    if (e == 0) break;
-    if (e == (int32_t)(lv + 1)) return true;
-    h = (h + 1) & (EXCAP - 1);
-  }
-  return ovf ? bit_get(gex, lv) : false;
-}
-__device__ __forceinline__ void ex_insert(int32_t *exh, int &cnt, bool &ovf, uint32_t *gex, int64_t words, uint32_t lv) {
-  const int lane = threadIdx.x & 31;
-  if (!ovf && cnt >= EXCAP * 3 / 4) {
-    for (int64_t w = lane; w < words; w += 32) gex[w] = 0;
-    __threadfence_block();
-    __syncwarp();      // every lane's zeroing lands before lane 0 sets the first bit
-    ovf = true;
-  }
-  if (ovf) {
-    if (lane == 0) bit_set(gex, lv);
-  } else {
-    if (lane == 0) {
-      uint32_t h = (lv * 0x9E3779B1u) >> (32 - 9);
-      while (exh[h] != 0 && exh[h] != (int32_t)(lv + 1)) h = (h + 1) & (EXCAP - 1);
-      exh[h] = (int32_t)(lv + 1);
-    }
-    ++cnt;
-  }
-  __syncwarp();
-}
-
 __device__ __forceinline__ bool consumer_done(const ProdCtx &x) {
-  int dn = (threadIdx.x & 31) == 0 ? x.hdr->done : 0;
+  int dn = (threadIdx.x & 31) == 0 ? lds_volatile(&x.hdr->done) : 0;
   return __shfl_sync(FULL, dn, 0) != 0;
 }
 
@@ -205,24 +299,20 @@ struct EvalLane {
   }
 };
 
-// vectors: lane's copies within a stage are the 16-byte chunks e = lane + 32 j (j < nchunks) of the
-// 32 x nchunks stage, i.e. row e / nchunks, chunk e % nchunks (walked incrementally).
-// S single-chunk stages in a ring: chunks i+1 .. i+S-1 are in flight while chunk i is evaluated.
-template <int S, class EV>
+// Vectors: two single-chunk stages; the gathers of chunk i+1 (and the draw bitmap atomics, and the
+// pool loads of chunk i+2) are in flight while chunk i is evaluated and published.
+template <class EV>
 __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
   const int lane = threadIdx.x & 31;
   const int nck = EV::NCH > 0 ? EV::NCH : a.st.nchunks;
   const uint8_t *base = a.st.vec;
   const size_t stride = a.st.stride;
   const int r0 = lane / nck, c0 = lane % nck, rs = 32 / nck, cs = 32 % nck;
-  const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
-  const bool prof = KP(a.prof);
-  long long p_wait = 0, p_work = 0;
   // compile-time widths: LR lanes per row, each copying chunks sl, sl + LR, ... of its row (immediate
   // offsets), 32 / LR rows per pass -- one shuffle and NCH / LR copies per pass
   constexpr int LR = EV::NCH >= 8 && EV::NCH % 8 == 0 ? 8 : (EV::NCH > 0 && EV::NCH <= 8 ? EV::NCH : 0);
   auto issue = [&](int st, int2 d) {
-    x.meta[(st * 32 + lane) * 4] = d.y;   // published: the pool index
+    x.meta[st * 32 + lane] = make_int4(d.x, d.y, 0, 0);
     uint8_t *dst = x.stg + st * 32 * x.pitch;
     if constexpr (LR > 0 && (32 % LR) == 0) {
       constexpr int RPP = 32 / LR, CPR = EV::NCH / LR;
@@ -231,59 +321,51 @@ __device__ __forceinline__ void produce_vec(const SearchArgs &a, const EV &ev, c
       for (int p = 0; p < LR; ++p) {
         const int r = p * RPP + rr;
         const int32_t id = __shfl_sync(FULL, d.x, r);
-        const uint8_t *src = base + (size_t)id * stride + sl * 16;
-        uint8_t *drow = dst + r * x.pitch + sl * 16;
+        if (id >= 0) {
+          const uint8_t *src = base + (size_t)id * stride + sl * 16;
+          uint8_t *drow = dst + r * x.pitch + sl * 16;
 #pragma unroll
-        for (int t = 0; t < CPR; ++t) cp_async16(drow + t * LR * 16, src + t * LR * 16);
+          for (int t = 0; t < CPR; ++t) cp_async16(drow + t * LR * 16, src + t * LR * 16);
+        }
       }
     } else {
       int r = r0, cc = c0;
 #pragma unroll 8
       for (int j = 0; j < nck; ++j) {
         const int32_t id = __shfl_sync(FULL, d.x, r);
-        cp_async16(dst + r * x.pitch + cc * 16, base + (size_t)id * stride + (size_t)cc * 16);
+        if (id >= 0) cp_async16(dst + r * x.pitch + cc * 16, base + (size_t)id * stride + (size_t)cc * 16);
         cc += cs;
         r += rs;
         if (cc >= nck) { cc -= nck; ++r; }
       }
     }
   };
-#pragma unroll
-  for (int s = 0; s < S - 1; ++s) {
-    if (s < ni) issue(s, draw_node(x, s));
-    cp_async_commit();
-  }
-  int2 pn = S - 1 < ni ? draw_node(x, S - 1) : make_int2(0, 0);
-  for (int64_t i = 0; i < ni; ++i) {
-    const long long t0 = prof ? clock64() : 0;
+  int2 d0 = draw_node(x, 0);
+  issue(0, d0);
+  uint32_t mk_cur = draw_mark(x, d0.y);
+  cp_async_commit();
+  int2 pn = draw_node(x, 1);
+  for (int64_t i = 0;; ++i) {
     if (consumer_done(x)) break;
-    const int64_t ii = i + S - 1;
-    if (ii < ni) {
-      issue((int)(ii % S), pn);
-      if (ii + 1 < ni) pn = draw_node(x, ii + 1);   // (pool load) in flight during this evaluation
-    }
+    issue((int)((i + 1) & 1), pn);
+    const uint32_t mk_next = draw_mark(x, pn.y);
+    pn = draw_node(x, i + 2);             // (pool load) in flight during this evaluation
     cp_async_commit();
-    cp_async_wait<S - 1>();
+    KPROF(const long long tw = clock64();)
+    cp_async_wait<1>();
     __syncwarp();
-    const int st = (int)(i % S);
-    const uint32_t key = ev.key(x.stg + st * 32 * x.pitch, x.pitch, nck);
-    const int32_t node = x.meta[(st * 32 + lane) * 4];
+    KPROF(if (x.prof && lane == 0) atomicAdd(x.prof + 3, (unsigned long long)(clock64() - tw));)
+    const int st = (int)(i & 1);
+    const int4 mt = x.meta[st * 32 + lane];
+    // (the warp evaluator is warp-collective: every lane evaluates, invalid draws are masked after)
+    const uint32_t kv = ev.key(x.stg + st * 32 * x.pitch, x.pitch, nck);
+    const uint32_t key = mt.y >= 0 ? kv : 0u;
     __syncwarp();
-    if (prof) p_work += clock64() - t0;
-    if (!publish(x, i, node, key, p_wait, prof)) break;
+    if (!publish(x, i, mt.y, repeat_of(mk_cur, mt.y), key, mt.x)) break;
+    mk_cur = mk_next;
   }
   cp_async_wait<0>();
   __syncwarp();
-  if (prof && lane == 0) {
-    atomicAdd(a.prof + 3, (unsigned long long)p_work);
-    atomicAdd(a.prof + 4, (unsigned long long)p_wait);
-  }
-}
-
-// two stages measured fastest on every config (deeper pipelines cost CTAs per SM): the only one built
-template <class EV>
-__device__ __forceinline__ void produce_vec_s(const SearchArgs &a, const EV &ev, const ProdCtx &x) {
-  produce_vec<2>(a, ev, x);
 }
 
 // the producer's evaluator: lane form for the configured row widths, else the warp form
@@ -298,10 +380,10 @@ __device__ __forceinline__ void produce_rows(const SearchArgs &a, const VecQuery
     for (int c = lane; c < nck; c += 32) *(uint4 *)(qsm + 16 * c) = ldg16(qg + 16 * c);
     __syncwarp();
     if constexpr (M == M_U8) {
-      if (nck == 8) produce_vec_s(a, EvalLane<M_U8, 8>{qsm}, x);
-      else produce_vec_s(a, EvalLane<M_U8, 2>{qsm}, x);
+      if (nck == 8) produce_vec(a, EvalLane<M_U8, 8>{qsm}, x);
+      else produce_vec(a, EvalLane<M_U8, 2>{qsm}, x);
     } else if constexpr (M == M_F32) {
-      produce_vec_s(a, EvalLane<M_F32, 24>{qsm}, x);
+      produce_vec(a, EvalLane<M_F32, 24>{qsm}, x);
     }
     return;
   }
@@ -309,87 +391,72 @@ __device__ __forceinline__ void produce_rows(const SearchArgs &a, const VecQuery
     // u8 rows of <= 128 B: 4 lanes x 2 chunks per candidate (2 shuffle levels)
     VecQuery<M_U8, 4, 2> PQ;
     PQ.load(a.qs, qrow, nullptr);
-    produce_vec_s(a, EvalWarp<VecQuery<M_U8, 4, 2>>{PQ}, x);
+    produce_vec(a, EvalWarp<VecQuery<M_U8, 4, 2>>{PQ}, x);
   } else {
-    produce_vec_s(a, EvalWarp<VecQuery<M, L, CPL>>{Q}, x);
+    produce_vec(a, EvalWarp<VecQuery<M, L, CPL>>{Q}, x);
   }
 }
 
-// sets: lane j stages candidate j's token range (aligned 16-byte chunks, SLOTCH at most) in its own
-// slot; longer sets are evaluated from global memory.  Two prefetch levels: the node of chunk
-// i + S and the offsets of chunk i + S - 1 are loaded while chunk i is computed.
-template <int S, int L>
+// Sets: lane j stages candidate j's token range (aligned 16-byte chunks, SLOTCH at most) in its own
+// slot; longer sets are evaluated from global memory.  Prefetch levels: the node of chunk i + 2 and
+// the offsets of chunk i + 1 are loaded while chunk i is computed.
+template <int L>
 __device__ __forceinline__ void produce_set(const SearchArgs &a, const SetQuery<L> &Q, const ProdCtx &x) {
   constexpr int SLOTCH = SetQuery<L>::SLOTCH;
   const int lane = threadIdx.x & 31;
   const uint32_t *tok = a.st.tok;
   const uint64_t *off = a.st.off;
-  const int64_t ni = x.nch > x.pw ? (x.nch - x.pw + x.nprod - 1) / x.nprod : 0;
-  const bool prof = KP(a.prof);
-  long long p_wait = 0, p_work = 0;
   auto issue = [&](int st, int2 d, uint64_t b, uint64_t e) {
     const uint64_t a0 = b & ~3ull;
     const int rb = (int)(b - a0), re = (int)(e - a0);
-    int4 *mt = (int4 *)(x.meta + (st * 32 + lane) * 4);
-    *mt = make_int4(d.x, rb, re, d.y);
-    const int nch = (re + 3) >> 2;
+    x.meta[st * 32 + lane] = make_int4(d.x, d.y, rb, re);
+    const int nch = d.y >= 0 ? (re + 3) >> 2 : 0;
     if (nch <= SLOTCH) {
       uint8_t *dst = x.stg + (st * 32 + lane) * x.pitch;
       for (int j = 0; j < nch; ++j) cp_async16(dst + 16 * j, tok + a0 + 4 * j);
     }
   };
-  // prologue
-  int2 n1 = make_int2(0, 0);
-  uint64_t b1 = 0, e1 = 0;
-#pragma unroll
-  for (int s = 0; s < S - 1; ++s) {
-    if (s < ni) {
-      const int2 nd = draw_node(x, s);
-      issue(s, nd, off[nd.x], off[nd.x + 1]);
-    }
-    cp_async_commit();
-  }
-  if (S - 1 < ni) {
-    n1 = draw_node(x, S - 1);
-    b1 = off[n1.x];
-    e1 = off[n1.x + 1];
-  }
-  int2 n2 = S < ni ? draw_node(x, S) : make_int2(0, 0);
-  for (int64_t i = 0; i < ni; ++i) {
-    const long long t0 = prof ? clock64() : 0;
+  auto offs = [&](int2 d, uint64_t &b, uint64_t &e) {
+    b = d.y >= 0 ? off[d.x] : 0;
+    e = d.y >= 0 ? off[d.x + 1] : 0;
+  };
+  int2 d0 = draw_node(x, 0);
+  uint64_t b0, e0;
+  offs(d0, b0, e0);
+  issue(0, d0, b0, e0);
+  uint32_t mk_cur = draw_mark(x, d0.y);
+  cp_async_commit();
+  int2 n1 = draw_node(x, 1);
+  uint64_t b1, e1;
+  offs(n1, b1, e1);
+  int2 n2 = draw_node(x, 2);
+  for (int64_t i = 0;; ++i) {
     if (consumer_done(x)) break;
-    const int64_t ii = i + S - 1;
-    if (ii < ni) {
-      issue((int)(ii % S), n1, b1, e1);
-      if (ii + 1 < ni) {
-        n1 = n2;
-        b1 = off[n1.x];
-        e1 = off[n1.x + 1];
-        if (ii + 2 < ni) n2 = draw_node(x, ii + 2);
+    issue((int)((i + 1) & 1), n1, b1, e1);
+    const uint32_t mk_next = draw_mark(x, n1.y);
+    n1 = n2;
+    offs(n1, b1, e1);
+    n2 = draw_node(x, i + 3);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const int st = (int)(i & 1);
+    const int4 mt = x.meta[st * 32 + lane];
+    uint32_t key = 0;
+    if (mt.y >= 0) {
+      if (((mt.w + 3) >> 2) <= SLOTCH) {
+        key = Q.eval_slot(x.stg + (st * 32 + lane) * x.pitch, mt.z, mt.w);
+      } else {   // long set: straight from global memory
+        const uint64_t b = off[mt.x];
+        key = Q.eval_slot_global(tok + (b & ~3ull), mt.z, mt.w);
       }
     }
-    cp_async_commit();
-    cp_async_wait<S - 1>();
     __syncwarp();
-    const int st = (int)(i % S);
-    const int4 mt = *(const int4 *)(x.meta + (st * 32 + lane) * 4);
-    uint32_t key;
-    if (((mt.z + 3) >> 2) <= SLOTCH) {
-      key = Q.eval_slot(x.stg + (st * 32 + lane) * x.pitch, mt.y, mt.z);
-    } else {   // long set: straight from global memory
-      const uint64_t b = off[mt.x];
-      key = Q.eval_slot_global(tok + (b & ~3ull), mt.y, mt.z);
-    }
-    __syncwarp();
-    if (prof) p_work += clock64() - t0;
-    if (!publish(x, i, mt.w, key, p_wait, prof)) break;
+    if (!publish(x, i, mt.y, repeat_of(mk_cur, mt.y), key, mt.x)) break;
+    mk_cur = mk_next;
   }
   cp_async_wait<0>();
   __syncwarp();
-  if (prof && lane == 0) {
-    atomicAdd(a.prof + 3, (unsigned long long)p_work);
-    atomicAdd(a.prof + 4, (unsigned long long)p_wait);
-  }
 }
 
 template <class QT>
@@ -408,50 +475,62 @@ __device__ __forceinline__ void produce_any(const SearchArgs &a, const VecQuery<
 template <int L>
 __device__ __forceinline__ void produce_any(const SearchArgs &a, const SetQuery<L> &Q, const ProdCtx &x, uint8_t *,
                                             int64_t) {
-  produce_set<2>(a, Q, x);
+  produce_set(a, Q, x);
 }
 
+// widths whose walk evaluates staged vectors one lane per neighbour (EvalLane shapes)
+__host__ __device__ __forceinline__ bool walk_stage_ok(int metric, int nchunks) {
+  return (metric == M_U8 && (nchunks == 8 || nchunks == 2)) || (metric == M_F32 && nchunks == 24);
+}
+
+// ---------------------------------------------------------------------------------------------
 // K1: one CTA per (query, partition) task: warp 0 runs the search in the paper's sequential
-// order, warps 1.. produce its random-start keys ahead of it.
-// MB: launch-bound variant.  MB = 4 lets a CTA of up to 4 warps keep 128 registers per thread (8
-// two-warp CTAs per SM); MB = 12 caps a two-warp CTA at 80 registers (12 per SM, some spills) for
-// latency-bound task mixes that want more concurrent walks.
+// order, warp 1 produces its random-start keys ahead of it.
+// MB: launch-bound variant.  MB = 8 keeps 128 registers per thread (8 two-warp CTAs per SM);
+// MB = 10 caps a two-warp CTA at 96 registers for task mixes that want more concurrent walks.
+// ---------------------------------------------------------------------------------------------
 template <int M, int L, int CPL, int MB>
-__global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a) {   // MB 4: <= 128 regs; 10: <= 96
+__global__ void __launch_bounds__(64, MB) k_search(SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nprod = (blockDim.x >> 5) - 1;
   const int k = a.k;
-  volatile RingHdr *hdr = (volatile RingHdr *)smem;
-  unsigned long long *ring = (unsigned long long *)(smem + HDR_BYTES);
-  const int S = a.stages;
-  uint8_t *stg = smem + HDR_BYTES + a.ring * 32 * 16;                         // [nprod][S][32] rows
-  int32_t *meta = (int32_t *)(stg + (size_t)nprod * S * 32 * a.pitch);        // [nprod][S][32][4]
-  uint8_t *qprod = (uint8_t *)(meta + nprod * S * 32 * 4);                   // [nprod][512 B] query copies
-  int32_t *rowbuf = (int32_t *)(qprod + nprod * 512);                         // [k][k]
-  int32_t *rowbuf2 = rowbuf + k * k;                                          // [32][k]
-  // partitioned: the same rows' partition-local indices (lrows, -1 = other partition)
-  const int lk = a.P > 0 ? k : 0;
-  int32_t *lrowbuf = rowbuf2 + 32 * k;                                        // [k][k] (P > 0)
-  int32_t *lrowbuf2 = lrowbuf + lk * k;                                       // [32][k] (P > 0)
-  uint32_t *qscr = (uint32_t *)(lrowbuf2 + 32 * lk);                          // [2][QMAX] (sets)
-  uint32_t *vbm = qscr + (M == M_JAC ? 2 * QMAX : 0);                        // [vwords] (sets)
+  RingHdr *hdr = (RingHdr *)smem;
+  unsigned long long *ring = (unsigned long long *)(smem + HDR_BYTES);   // [ring][32][3] tagged words
+  uint8_t *stg = smem + HDR_BYTES + a.ring * 32 * 24;                   // [2][32] rows
+  int4 *meta = (int4 *)(stg + 2 * 32 * a.pitch);                        // [2][32]
+  uint8_t *qprod = (uint8_t *)(meta + 2 * 32);                          // [512 B] query copy
+  // rows the walk reads: ids int32[k] (unpartitioned) or lrows int2[k] = (id, local index) (P > 0),
+  // RB bytes each, prefetched with cp.async of CU bytes
+  const int RB = (a.P > 0 ? 8 : 4) * k;
+  const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4), NU = RB / CU;
+  uint8_t *rowbuf = qprod + 512;                                        // [k] rows of cur's neighbours
+  uint8_t *wbuf = rowbuf + ((k * RB + 15) & ~15);                       // [WPF] rows of possible starts
+  // lane-form widths: the walk stages cur's neighbours' vectors too ([k] x pitch) and evaluates them
+  // one lane per neighbour against the consumer's query copy qcons
+  const bool wstage = M != M_JAC && walk_stage_ok(M, a.st.nchunks);
+  uint8_t *qcons = wbuf + ((WPF * RB + 15) & ~15);                     // [512 B] (wstage)
+  uint8_t *vbuf = qcons + (wstage ? 512 : 0);                           // [k][pitch] (wstage)
+  uint32_t *pkey = (uint32_t *)(vbuf + (wstage ? k * a.pitch : 0));     // [32] pending walk evaluations
+  int32_t *pid = (int32_t *)(pkey + 32);                                // [32]
+  uint32_t *qscr = (uint32_t *)(pid + 32);                              // [2][QMAX] (sets)
+  uint32_t *vbm = qscr + (M == M_JAC ? 2 * QMAX : 0);                   // [vwords] (sets)
   const int vwords = M == M_JAC ? a.st.vwords : 0;
-  const uint32_t vw_lim = (uint32_t)a.st.vwords;   // (bounds for the Jaccard vocabulary bitmap)
-  int32_t *exh = (int32_t *)(vbm + vwords);                                  // [EXCAP] expanded-set hash
-  uint32_t *sbits = (uint32_t *)(exh + EXCAP);                               // [bits_words / 2] (smem bits)
+  const uint32_t vw_lim = (uint32_t)a.st.vwords;
+  uint32_t *H = vbm + vwords;                                           // [1 << hbits] W / X hash
+  uint32_t *sbits = (uint32_t *)(((uintptr_t)(H + (1 << a.hbits)) + 15) & ~(uintptr_t)15);   // [de_words] (smem D/E)
+  const int hb = a.hbits;
+  const int hthr = (3 << hb) >> 2;                                      // fill limit of the hash
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
-  // per CTA slot in global memory: [evaluated words][expanded-overflow words]
-  uint32_t *gslot = a.gbits + (int64_t)blockIdx.x * a.bits_words;
-  const float rk = 1.0f / (float)k;
+  // per CTA slot in global memory: [D/E words][expanded-overflow words]
+  uint32_t *gslot = a.gbits + (int64_t)blockIdx.x * (a.de_words + a.x_words);
   unsigned long long s_evals = 0, s_starts = 0, s_skip = 0, s_exp = 0;
   int prev_qn = 0;                              // sets: tokens of the previous query (scratch 0)
   for (int w = threadIdx.x; w < vwords; w += blockDim.x) vbm[w] = 0;
   if (threadIdx.x == 0) hdr->next_task = (int)blockIdx.x;
 
   for (;;) {
-    __syncthreads();                          // previous task finished by every warp
+    __syncthreads();                          // previous task finished by both warps
     const int64_t task = hdr->next_task;
     if (task >= T) break;
     const int64_t b = task / Pn;
@@ -459,15 +538,13 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
     const int p = a.part_lo + pl;             // partition searched
     const int64_t m = a.P > 0 ? a.member_cnt[p] : a.n_t;
     const int32_t *pool = a.P > 0 ? a.members + (size_t)p * a.member_cap : nullptr;
-    const int64_t words = (m + 31) >> 5;
-    // evaluated set: bitmap over the pool (shared memory when it fits the plan, else L2/HBM);
-    // expanded set: shared hash, overflowing into a global bitmap (cleared when first used)
-    uint32_t *ev = a.smem_bits ? sbits : gslot;
-    uint32_t *gex = gslot + words;
-    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) ev[w] = 0;
-    for (int w = threadIdx.x; w < EXCAP; w += blockDim.x) exh[w] = 0;
-    for (int w = threadIdx.x; w < a.ring * 32; w += blockDim.x)   // no stale tags from the last task
-      ((uint4 *)ring)[w] = make_uint4(0, 0, 0, 0);
+    const int64_t dew = (m + 15) >> 4;
+    uint32_t *de = a.smem_bits ? sbits : gslot;
+    uint32_t *xg = gslot + a.de_words;
+    for (int64_t w = threadIdx.x; w < (dew >> 2); w += blockDim.x) ((uint4 *)de)[w] = make_uint4(0, 0, 0, 0);
+    for (int64_t w = (dew & ~3ll) + threadIdx.x; w < dew; w += blockDim.x) de[w] = 0;
+    for (int w = threadIdx.x; w < (1 << hb); w += blockDim.x) H[w] = 0;
+    for (int w = threadIdx.x; w < a.ring * 32 * 3; w += blockDim.x) ring[w] = 0;   // no stale tags
     if (threadIdx.x == 0) { hdr->consumed = 0; hdr->done = 0; }
     if (M == M_JAC && vwords > 0 && warp == 0)   // clear the previous query's vocabulary bits
       for (int i = lane; i < prev_qn; i += 32) {
@@ -483,12 +560,9 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
     const int64_t lo = m < a.kr ? m : a.kr;
     if (budget < lo) budget = lo;
     if (budget > m) budget = m;
-    // chunks the producers may evaluate: they run until the consumer is done (redraws push the
-    // consumed draws past the budget), capped for degenerate cases (speedup ~ 1)
-    const int64_t nch = a.starts ? 0 : (8 * budget + 31) / 32 + 8;
 
     typename QuerySel<M, L, CPL>::T Q;
-    Q.load(a.qs, a.qrow0 + b, M == M_JAC ? qscr + (warp < 2 ? warp : 1) * QMAX : nullptr);
+    Q.load(a.qs, a.qrow0 + b, M == M_JAC ? qscr + warp * QMAX : nullptr);
     if (M == M_JAC && vwords > 0) {
       // vocabulary bitmap of the query: one bit test per candidate token (tokens beyond the store's
       // largest token cannot match and are left out)
@@ -507,231 +581,191 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
     }
     const uint64_t h3 = rng_prefix(a.seed, (uint64_t)(a.pid_base + b), (uint64_t)p);
     if (warp > 0) {
-      if (budget > 0 && nch > 0) {
+      if (budget > 0) {
         ProdCtx x;
         x.hdr = hdr;
         x.ring = ring;
         x.ring_n = a.ring;
-        x.stg = stg + (size_t)(warp - 1) * S * 32 * a.pitch;
-        x.meta = meta + (warp - 1) * S * 32 * 4;
+        x.stg = stg;
+        x.meta = meta;
         x.pitch = a.pitch;
-        x.pw = warp - 1;
-        x.nprod = nprod;
-        x.nch = nch;
         x.h3 = h3;
         x.m = m;
         x.pool = pool;
-        produce_any(a, Q, x, qprod + (warp - 1) * 512, a.qrow0 + b);
+        x.starts = a.starts;
+        x.nstarts = a.nstarts;
+        x.de = de;
+        x.gde = !a.smem_bits;
+        x.prof = a.prof;
+        produce_any(a, Q, x, qprod, a.qrow0 + b);
       }
       continue;
     }
 
     // ================================ consumer ================================
+    if (wstage) {
+      const uint8_t *qg = a.qs.vec + (size_t)(a.qrow0 + b) * a.qs.stride;
+      for (int cc = lane; cc < a.st.nchunks; cc += 32) *(uint4 *)(qcons + 16 * cc) = ldg16(qg + 16 * cc);
+      __syncwarp();
+    }
     WarpTopK<M> top;
     top.init(a.kr);
     int64_t c = 0, jbase = 0;
-    int32_t wnode = -1;
-    uint32_t wkey = 0, wl = 0;
-    bool wvalid = false;
-    bool whave = false, wpf = false;
-    SkipThr<M> thr;              // skip rule prepared against the current best key
+    int32_t wnode = -1, wl = -1;
+    uint32_t wkey = 0;
+    bool wrep = true;
+    int wpos = 32, wslot = -1;                   // window lane state; wslot: its prefetch slot (-1: none)
+    SkipThr<M> thr;                              // skip rule prepared against the current best key
     uint32_t thr_key = 0;
     bool thr_ok = false;
-    int wpos = 32;
+    int hcnt = 0;
+    bool hovf = false;                           // the hash is full: walk evaluations go to E, expansions to xg
+    const bool gde = !a.smem_bits;
+    auto e_get = [&](int32_t pidx) -> bool {     // consumed evaluation bit (walk neighbours)
+      return (plane_ld(de + de_word(pidx), gde) & e_bit(pidx)) != 0;
+    };
+    auto thr_update = [&]() {
+      if (top.cnt > 0 && (!thr_ok || thr_key != top.key_at0)) {
+        thr.set(top.key_at0, a.e_num, a.e_den);
+        thr_key = top.key_at0;
+        thr_ok = true;
+      }
+    };
 
-    const long long tc0 = KP(a.prof) ? clock64() : 0;
-    long long p_wait = 0, p_walk = 0, p_win = 0;
-    int ex_cnt = 0;
-    bool ex_ovf = false;
+    KPROF(const long long tc0 = clock64(); long long c_wait = 0, c_walk = 0; unsigned long long c_win = 0, c_steps = 0,
+          c_fast = 0; long long c_ph[3] = {0, 0, 0};)
     while (c < budget) {
       // ------------------------------ restart ------------------------------
       if (wpos >= 32) {
         // ---- fast path: FASTC whole produced chunks in which no draw can be accepted.  Against the
         // current s_max every draw is skipped (so none is a new best and the threshold cannot move);
-        // each unevaluated node among them is evaluated once (the atomicOr that flips its bit) and
-        // skipped, exactly as the sequential loop would do draw by draw; the budget is not reached.
-        const int64_t ch0 = jbase / 32;
-        if (top.cnt > 0 && nprod > 0 && ch0 + FASTC <= nch && c + 32 * FASTC <= budget) {
-          const long long tw = KP(a.prof) ? clock64() : 0;
-          int32_t fnode[FASTC];
-          uint32_t fkey[FASTC];
+        // each fresh draw among them is evaluated once and skipped, exactly as the sequential loop
+        // does draw by draw; the budget is not reached.
+        const int64_t ch0 = jbase >> 5;
+        if (top.cnt > 0 && c + 32 * FASTC <= budget) {
+          KPROF(const long long tw = clock64();)
+          RingEnt fe[FASTC];
 #pragma unroll
-          for (int t = 0; t < FASTC; ++t) ring_get(ring, a.ring, hdr, ch0 + t, fnode[t], fkey[t]);
-          if (KP(a.prof)) p_wait += clock64() - tw;
-          if (!thr_ok || thr_key != top.key_at0) {
-            thr.set(top.key_at0, a.e_num, a.e_den);
-            thr_key = top.key_at0;
-            thr_ok = true;
-          }
-          // the chunks before the first one holding a draw that passes the skip test go the fast way
+          for (int t = 0; t < FASTC; ++t) fe[t] = ring_get(ring, a.ring, ch0 + t);
+          KPROF(c_wait += clock64() - tw;)
+          thr_update();
+          // the chunks before the first one holding a draw that passes the skip test (or the end of an
+          // injected sequence) go the fast way
           unsigned pm = 0;
 #pragma unroll
-          for (int t = 0; t < FASTC; ++t) pm |= __any_sync(FULL, !thr.skip(fkey[t])) ? (1u << t) : 0u;
+          for (int t = 0; t < FASTC; ++t)
+            pm |= __any_sync(FULL, fe[t].pidx < 0 || !thr.skip(fe[t].key)) ? (1u << t) : 0u;
           const int tp = pm ? __ffs(pm) - 1 : FASTC;
           if (tp > 0) {
-            bool fr[FASTC];
-#pragma unroll
-            for (int t = 0; t < FASTC; ++t) {
-              fr[t] = false;
-              if (t < tp) {
-                const uint32_t li = (uint32_t)fnode[t];   // the ring carries the pool index
-                const uint32_t bit = 1u << (li & 31);
-                fr[t] = !(atomicOr(ev + (li >> 5), bit) & bit);
-              }
-            }
-            __syncwarp();
             int nf = 0;
 #pragma unroll
             for (int t = 0; t < FASTC; ++t) {
-              if (t < tp) {                             // (warp-uniform)
-                int32_t nd = fnode[t];
-                const bool ct = top.could_take(fkey[t]);
-                if (pool && fr[t] && ct) nd = pool[nd]; // node id only when it may enter the top-k
-                top.insert(fr[t], fkey[t], nd);         // Q5: skipped starts enter the top-k
-                nf += __popc(__ballot_sync(FULL, fr[t]));
+              if (t < tp) {                                   // (warp-uniform)
+                const int32_t li = fe[t].pidx;
+                bool fr = fe[t].rep == 0 && !(h_get(H, hb, li) & HW);
+                if (hovf && fr) fr = !e_get(li);              // walk evaluations past the hash are in E
+#ifndef KNNG_HACK_NOATOM
+                if (fr) plane_red_or(de + de_word(li), e_bit(li), gde);
+#endif
+                top.insert(fr, fe[t].key, fe[t].node);        // Q5: skipped starts enter the top-k
+                nf += __popc(__ballot_sync(FULL, fr));
               }
             }
             c += nf;
             s_starts += nf;
             s_skip += nf;
-            p_win += tp;
             __syncwarp();
-            if (lane == 0) hdr->consumed = (int)(ch0 + tp);
+            if (lane == 0) sts_volatile(&hdr->consumed, (int)(ch0 + tp));
             jbase += 32 * tp;
+            KPROF(c_fast += tp;)
             continue;
           }
         }
-        const int64_t j = jbase + lane;
-        const int64_t ch = jbase / 32;
-        if (ch < nch && nprod > 0) {                 // produced ahead into the ring
-          const long long tw = KP(a.prof) ? clock64() : 0;
-          uint32_t kk;
-          int32_t pidx;
-          ring_get(ring, a.ring, hdr, ch, pidx, kk);
-          wkey = kk;
-          wl = (uint32_t)pidx;
-          wnode = pool ? -2 : pidx;                   // -2: valid, node id not looked up yet
-          wvalid = true;
-          if (KP(a.prof)) p_wait += clock64() - tw;
-          ++p_win;
-          whave = true;
-          __syncwarp();
-          if (lane == 0) hdr->consumed = (int)(ch + 1);
-        } else {
-          if (a.starts) {
-            wnode = j < a.nstarts ? a.starts[j] : -1;
-            wl = wnode >= 0 ? (a.P > 0 ? (uint32_t)a.local_idx[wnode] : (uint32_t)wnode) : 0u;
-          } else {
-            const uint64_t idx = rng_index(h3, (uint64_t)j, (uint64_t)m);
-            wnode = pool ? pool[idx] : (int32_t)idx;
-            wl = (uint32_t)idx;
-          }
-          wvalid = wnode >= 0;
-          whave = false;
-        }
+        // ---- one chunk draw by draw ----
+        const int64_t ch = jbase >> 5;
+        KPROF(const long long tw = clock64();)
+        const RingEnt e = ring_get(ring, a.ring, ch);
+        KPROF(c_wait += clock64() - tw; ++c_win;)
+        wl = e.pidx;
+        wkey = e.key;
+        wnode = e.node;
+        wrep = e.rep != 0;
+        __syncwarp();
+        if (lane == 0) sts_volatile(&hdr->consumed, (int)(ch + 1));
         jbase += 32;
         wpos = 0;
         // prefetch the rows of the draws that could still be accepted: the skip threshold only
         // tightens as s_max improves, so "passes against the current best" is a superset
-        wpf = false;
-        if (whave && wvalid) {
-          if (top.cnt > 0 && (!thr_ok || thr_key != top.key_at0)) {
-            thr.set(top.key_at0, a.e_num, a.e_den);
-            thr_key = top.key_at0;
-            thr_ok = true;
-          }
-          wpf = top.cnt == 0 ? lane == 0 : !thr.skip(wkey);
-          if (wpf && wnode == -2) wnode = pool[wl];
-          if (!a.win_prefetch) wpf = false;
-          if (__ballot_sync(FULL, wpf)) {
-            cp_async_wait_all();      // older copies into rowbuf2 must land first
-            if (wpf)
-              for (int e = 0; e < k; ++e) {
-                cp_async4(rowbuf2 + lane * k + e, a.rows + (size_t)wnode * k + e);
-                if (a.P > 0) cp_async4(lrowbuf2 + lane * k + e, a.lrows + (size_t)wnode * k + e);
-              }
+        wslot = -1;
+        if (a.win_prefetch) {
+          thr_update();
+          const bool cand = wl >= 0 && !wrep && (top.cnt == 0 ? lane == 0 : !thr.skip(wkey));
+          const unsigned cmk = __ballot_sync(FULL, cand);
+          if (cmk) {
+            const int r = __popc(cmk & lanemask_lt());
+            if (cand && r < WPF) wslot = r;
+            cp_async_wait_all();      // older copies into wbuf must land first
+            __syncwarp();
+            if (wslot >= 0) {
+              const uint8_t *src = a.P > 0 ? (const uint8_t *)(a.lrows + (size_t)wnode * k)
+                                           : (const uint8_t *)(a.rows + (size_t)wnode * k);
+              for (int u = 0; u < NU; ++u) cp_async_n(wbuf + wslot * RB + u * CU, src + u * CU, CU);
+            }
           }
         }
       }
       const unsigned active = FULL << wpos;
+      const bool wvalid = wl >= 0;
       const unsigned invm = __ballot_sync(FULL, !wvalid) & active;
       const unsigned lim = invm ? ((1u << (__ffs(invm) - 1)) - 1u) : FULL;
-      const bool evb = wvalid ? bit_get(ev, wl) : true;
-      // Redraws of evaluated nodes are free (Q4).  A node drawn twice inside the window looks fresh
-      // in both lanes: the later lane can never be accepted when the earlier one is skipped (same key,
-      // tighter s_max), and the commit's atomicOr lets only the first evaluation count.
-      const bool fresh = lane >= wpos && !evb;
+      // Redraws are free (Q4): a draw repeating an earlier draw, or of a node a walk evaluated
+      bool fresh = lane >= wpos && wvalid && !wrep && !(h_get(H, hb, wl) & HW);
+      if (hovf && fresh) fresh = !e_get(wl);
       const unsigned fm = __ballot_sync(FULL, fresh) & active & lim;
       if (fm == 0) {
         if (invm) break;          // injected start sequence exhausted
         wpos = 32;
         continue;
       }
-      // evaluate the next G fresh draws that have no key yet (beyond the produced range)
-      unsigned hm = __ballot_sync(FULL, whave);
-      const unsigned nokey = fm & ~hm;
-      if (nokey) {
-        const unsigned need = first_bits(nokey, a.G);
-        const int nn = __popc(need);
-        const int src = lane < nn ? (int)__fns(need, 0, lane + 1) : 0;
-        const int32_t cid = __shfl_sync(FULL, wnode, src);
-        const uint32_t kk = Q.eval(a.st, lane < nn ? cid : -1, nn);
-        const int rank = __popc(need & lanemask_lt());
-        const uint32_t mine = __shfl_sync(FULL, kk, rank & 31);
-        if ((need >> lane) & 1u) { wkey = mine; whave = true; }
-        hm |= need;
-      }
-      // committable: fresh draws in order up to the first one without a key
-      const unsigned miss = fm & ~hm;
-      const unsigned cmfull = miss ? (fm & ((1u << (__ffs(miss) - 1)) - 1u)) : fm;
-      unsigned cm = cmfull;
+      unsigned cm = fm;
       if ((int64_t)__popc(cm) > budget - c) cm = first_bits(cm, (int)(budget - c));
       const bool inc = (cm >> lane) & 1u;
       unsigned am;
-      if (top.cnt > 0 && (!thr_ok || thr_key != top.key_at0)) {
-        thr.set(top.key_at0, a.e_num, a.e_den);
-        thr_key = top.key_at0;
-        thr_ok = true;
-      }
+      thr_update();
       if (top.cnt > 0 && __ballot_sync(FULL, inc && !thr.skip(wkey)) == 0) {
         am = 0;   // every committable draw is skipped even against the current s_max
       } else {
-      // s_max before each draw: best of top-k and of the earlier committed draws
-      uint32_t run = wkey;
-      bool rv = inc;
+        // s_max before each draw: best of top-k and of the earlier committed draws
+        uint32_t run = wkey;
+        bool rv = inc;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t ok_ = __shfl_up_sync(FULL, run, o);
-        const bool ov = __shfl_up_sync(FULL, rv, o);
-        if (lane >= o && ov) {
-          if (!rv || closer<M>(ok_, run)) run = ok_;
-          rv = true;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t ok_ = __shfl_up_sync(FULL, run, o);
+          const bool ov = __shfl_up_sync(FULL, rv, o);
+          if (lane >= o && ov) {
+            if (!rv || closer<M>(ok_, run)) run = ok_;
+            rv = true;
+          }
         }
-      }
-      uint32_t bk = __shfl_up_sync(FULL, run, 1);
-      bool bv = __shfl_up_sync(FULL, rv, 1) && lane > 0;
-      if (top.cnt > 0) {
-        const uint32_t tb = top.best();
-        bk = (bv && closer<M>(bk, tb)) ? bk : tb;
-        bv = true;
-      }
-      // first start never skipped (Q3): it is the only draw with no best before it
-      const bool acc = inc && (!bv || !skip_start<M>(wkey, bk, a.e_num, a.e_den));
-      am = __ballot_sync(FULL, acc);
+        uint32_t bk = __shfl_up_sync(FULL, run, 1);
+        bool bv = __shfl_up_sync(FULL, rv, 1) && lane > 0;
+        if (top.cnt > 0) {
+          const uint32_t tb = top.best();
+          bk = (bv && closer<M>(bk, tb)) ? bk : tb;
+          bv = true;
+        }
+        // first start never skipped (Q3): it is the only draw with no best before it
+        const bool acc = inc && (!bv || !skip_start<M>(wkey, bk, a.e_num, a.e_den));
+        am = __ballot_sync(FULL, acc);
       }
       const int al = am ? __ffs(am) - 1 : -1;
       const unsigned commit = am ? (cm & (al == 31 ? FULL : ((2u << al) - 1u))) : cm;
       const bool cmt = (commit >> lane) & 1u;
-      bool newly = false;
-      if (cmt) {
-        const uint32_t bit = 1u << (wl & 31);
-        newly = !(atomicOr(ev + (wl >> 5), bit) & bit);
-      }
-      const bool ct = top.could_take(wkey);   // (warp-wide)
-      if (newly && wnode == -2 && ct) wnode = pool[wl];
-      if (am && lane == __ffs(am) - 1 && wnode == -2) wnode = pool[wl];   // the accepted start
-      top.insert(newly, wkey, wnode);        // Q5: skipped starts enter the top-k too
-      const int ncm = __popc(__ballot_sync(FULL, newly));
+#ifndef KNNG_HACK_NOATOM
+      if (cmt) plane_red_or(de + de_word(wl), e_bit(wl), gde);
+#endif
+      top.insert(cmt, wkey, wnode);          // Q5: skipped starts enter the top-k too
+      const int ncm = __popc(commit);
       c += ncm;
       s_starts += ncm;
       s_skip += ncm - (am ? 1 : 0);
@@ -740,93 +774,186 @@ __global__ void __launch_bounds__(MB == 4 ? 128 : 64, MB) k_search(SearchArgs a)
       // algorithm, its walk begins and ends at the first fresh evaluation it needs
       if (c >= budget && !am) break;
       if (!am) {
-        const unsigned rest = cmfull & ~commit;   // truncated by the budget (repeats inside): resume there
-        wpos = rest ? (__ffs(rest) - 1) : (miss ? (__ffs(miss) - 1) : 32);
+        if (invm) break;
+        wpos = 32;
         continue;
       }
       wpos = al + 1;
 
       // ------------------- hill climbing, eager first improvement -------------------
-      const long long tk0 = KP(a.prof) ? clock64() : 0;
+      // One memory round trip per step: the rows and (for the lane-form widths) the vectors of cur's
+      // in-pool neighbours are copied to shared memory together with their E bits; the next step reads
+      // the chosen neighbour's row from there.  The walk's own evaluations go to the top-k in batches
+      // (pbuf, flushed at the walk's end): the walk itself only compares against kcur.
       int32_t cur = __shfl_sync(FULL, wnode, al);
       uint32_t kcur = __shfl_sync(FULL, wkey, al);
-      uint32_t curl = __shfl_sync(FULL, wl, al);
-      int pf = -1;                 // row of cur prefetched into rowbuf[pf*k ..] by the last step
-      int pf2 = al;                // ... or into rowbuf2[pf2*k ..] when the window was loaded
-      if (!__shfl_sync(FULL, wpf, al)) pf2 = -1;
+      int32_t curl = __shfl_sync(FULL, wl, al);
+      int rs = -1;                 // row of cur: rowbuf slot rs (prefetched by the last step), else
+      int rw = __shfl_sync(FULL, wslot, al);   // wbuf slot rw (prefetched with the window), else global
       bool stop = false;
+      int pn = 0;                  // pending walk evaluations in pbuf
+      auto flush = [&]() {
+        if (pn == 0) return;
+        __syncwarp();
+        const bool has = lane < pn;
+        top.insert(has, has ? pkey[lane] : 0u, has ? pid[lane] : -1);
+        pn = 0;
+        __syncwarp();
+      };
+      KPROF(const long long tk0 = clock64();)
+      if (rw >= 0) {               // the window's row copies must have landed
+        cp_async_wait_all();
+        __syncwarp();
+      }
       for (;;) {
-        ex_insert(exh, ex_cnt, ex_ovf, gex, words, curl);
+        KPROF(++c_steps; long long ts0 = clock64();)
         ++s_exp;
         int32_t v = -1, vl = -1;
-        if (pf >= 0 || pf2 >= 0) {
-          cp_async_wait_all();
-          __syncwarp();
-        }
         if (lane < k) {
-          v = pf >= 0 ? rowbuf[pf * k + lane] : (pf2 >= 0 ? rowbuf2[pf2 * k + lane] : a.rows[(size_t)cur * k + lane]);
-          if (a.P > 0)
-            vl = pf >= 0 ? lrowbuf[pf * k + lane]
-                         : (pf2 >= 0 ? lrowbuf2[pf2 * k + lane] : a.lrows[(size_t)cur * k + lane]);
-        }
-        pf2 = -1;
-        // Q10: neighbours in another partition are skipped (lrows holds -1 for them)
-        const bool inpool = v >= 0 && (a.P == 0 || vl >= 0);
-        const uint32_t lv = inpool ? (a.P > 0 ? (uint32_t)vl : (uint32_t)v) : 0u;
-        __syncwarp();
-        // prefetch the rows of the in-pool neighbours: the next cur is one of them
-        if (a.walk_prefetch)
-        for (int base = 0; base < k * k; base += 32) {
-          const int idx = base + lane;
-          const int t = __float2int_rz(__fmul_rn(__int2float_rn(idx) + 0.5f, rk));   // idx / k
-          const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t < 32 ? t : 31);
-          if (idx < k * k && vt >= 0) {
-            cp_async4(rowbuf + idx, a.rows + (size_t)vt * k + (idx - t * k));
-            if (a.P > 0) cp_async4(lrowbuf + idx, a.lrows + (size_t)vt * k + (idx - t * k));
+          if (a.P > 0) {
+            const int2 e2 = rs >= 0 ? ((const int2 *)(rowbuf + rs * RB))[lane]
+                                    : (rw >= 0 ? ((const int2 *)(wbuf + rw * RB))[lane] : a.lrows[(size_t)cur * k + lane]);
+            v = e2.x;
+            vl = e2.y;
+          } else {
+            v = rs >= 0 ? ((const int32_t *)(rowbuf + rs * RB))[lane]
+                        : (rw >= 0 ? ((const int32_t *)(wbuf + rw * RB))[lane] : a.rows[(size_t)cur * k + lane]);
           }
         }
-        const bool evb2 = inpool ? bit_get(ev, lv) : true;
-        const bool exb2 = (inpool && !a.ex_one) ? ex_has(exh, ex_ovf, gex, lv) : false;
-        const uint32_t key = Q.eval(a.st, inpool ? v : -1, k);
+        rw = -1;
+        // Q10: neighbours in another partition are skipped (lrows holds -1 for them)
+        const bool inpool = v >= 0 && (a.P == 0 || vl >= 0);
+        const int32_t lv = inpool ? (a.P > 0 ? vl : v) : 0;
+        __syncwarp();                          // rowbuf is read before the copies below overwrite it
+        KPROF(__ballot_sync(FULL, inpool); long long ts1 = clock64(); c_ph[0] += ts1 - ts0;)
+        // issue: rows (NU copies of CU bytes) and staged vectors (NCK copies of 16 bytes) of the in-pool
+        // neighbours, their E bits and hash flags -- all in flight together
+        const int per = NU + (wstage ? a.st.nchunks : 0);
+        {
+          const uint8_t *rsrc = a.P > 0 ? (const uint8_t *)a.lrows : (const uint8_t *)a.rows;
+          for (int base = 0; base < k * per; base += 32) {
+            const int idx = base + lane;
+            const int t = idx / per;
+            const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t < 32 ? t : 31);
+            if (idx < k * per && vt >= 0) {
+              const int u = idx - t * per;
+              if (u < NU) cp_async_n(rowbuf + t * RB + u * CU, rsrc + (size_t)vt * RB + u * CU, CU);
+              else cp_async16(vbuf + t * a.pitch + (u - NU) * 16, a.st.vec + (size_t)vt * a.st.stride + (u - NU) * 16);
+            }
+          }
+        }
+        // evaluated before?  W (this task's walks) or E (consumed fresh draws; walk evaluations past a full
+        // hash)
+        const bool eb = inpool ? e_get(lv) : true;
+        const uint32_t hf = inpool ? h_get(H, hb, lv) : 0u;
+        // cur is expanded (Q9 bookkeeping), while the copies are in flight
+        if (!hovf) {
+          if (lane == 0) h_put(H, hb, curl, HX);
+          ++hcnt;
+        } else if (lane == 0) {
+          plane_red_or(xg + ((uint32_t)curl >> 5), 1u << (curl & 31), true);
+        }
+        uint32_t key;
+        if constexpr (M == M_JAC) {
+          key = Q.eval(a.st, inpool ? v : -1, k);
+          cp_async_wait_all();
+          __syncwarp();
+        } else {
+          cp_async_wait_all();
+          __syncwarp();
+          if (wstage) {   // lane t: neighbour t's whole distance from shared memory (lanes >= k read row 0)
+            const uint8_t *vb = vbuf - (lane < k ? 0 : lane * a.pitch);
+            if constexpr (M == M_U8) {
+              key = a.st.nchunks == 8 ? EvalLane<M_U8, 8>{qcons}.key(vb, a.pitch, 8)
+                                      : EvalLane<M_U8, 2>{qcons}.key(vb, a.pitch, 2);
+            } else {
+              key = EvalLane<M_F32, 24>{qcons}.key(vb, a.pitch, 24);
+            }
+          } else {
+            key = Q.eval(a.st, inpool ? v : -1, k);
+          }
+        }
+        const bool evb2 = (hf & HW) || eb;
         const bool imp = inpool && closer<M>(key, kcur);
+        KPROF(__ballot_sync(FULL, imp); long long ts2 = clock64(); c_ph[1] += ts2 - ts1;)
         const unsigned im = __ballot_sync(FULL, imp);
-        const int fi = im ? __ffs(im) - 1 : 31;
-        const unsigned range = fi == 31 ? FULL : ((2u << fi) - 1u);
+        int fi = im ? __ffs(im) - 1 : 31;
+        unsigned range = fi == 31 ? FULL : ((2u << fi) - 1u);
+        if (a.full_scan) {
+          // GNNS: every neighbour is evaluated; the walk moves to the most similar improving one
+          // (the first in row order among equals): a warp arg-min under closer<M>
+          range = FULL;
+          uint32_t bk = key;
+          int bl = imp ? lane : 32;
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            const uint32_t ok2 = __shfl_xor_sync(FULL, bk, o);
+            const int ol = __shfl_xor_sync(FULL, bl, o);
+            if (ol < 32 && (bl == 32 || closer<M>(ok2, bk) || (!closer<M>(bk, ok2) && ol < bl))) {
+              bk = ok2;
+              bl = ol;
+            }
+          }
+          fi = im ? bl : 31;
+        }
         unsigned fm2 = __ballot_sync(FULL, inpool && !evb2) & range;
         bool hit2 = false;
         if ((int64_t)__popc(fm2) > budget - c) { fm2 = first_bits(fm2, (int)(budget - c)); hit2 = true; }
         const bool cm2 = (fm2 >> lane) & 1u;
-        if (cm2) bit_set(ev, lv);
-        top.insert(cm2, key, v);
-        c += __popc(fm2);
+        const int nf2 = __popc(fm2);
+        if (!hovf && hcnt + nf2 > hthr) {   // the hash is full: overflow into E / xg from here on
+          for (int64_t w = lane; w < ((m + 31) >> 5); w += 32) xg[w] = 0;
+          __syncwarp();
+          hovf = true;
+        }
+        if (cm2) {
+          if (!hovf) h_put(H, hb, lv, HW);
+          else plane_red_or(de + de_word(lv), e_bit(lv), gde);
+        }
+        hcnt += nf2;
+        if (pn + nf2 > 32) flush();
+        if (cm2) {
+          const int q = pn + __popc(fm2 & lanemask_lt());
+          pkey[q] = key;
+          pid[q] = v;
+        }
+        pn += nf2;
+        c += nf2;
         __syncwarp();
+        KPROF(long long ts3 = clock64(); c_ph[2] += ts3 - ts2;)
         if (hit2) { stop = true; break; }    // the over-budget evaluation is not performed
         if (!im) break;                      // local maximum -> restart
         cur = __shfl_sync(FULL, v, fi);
         kcur = __shfl_sync(FULL, key, fi);
         curl = __shfl_sync(FULL, lv, fi);
-        pf = a.walk_prefetch ? fi : -1;
-        bool exq = exb2;
-        if (a.ex_one) exq = lane == fi ? ex_has(exh, ex_ovf, gex, curl) : false;   // only the chosen neighbour
+        rs = fi;
+        bool exq = lane == fi ? ((hf & HX) != 0 || (hovf && ((plane_ld(xg + ((uint32_t)curl >> 5), true) >> (curl & 31)) & 1u))) : false;
         if (__shfl_sync(FULL, exq, fi)) break;   // Q9: moving onto an expanded node restarts
       }
-      if (KP(a.prof)) p_walk += clock64() - tk0;
+      flush();
+      KPROF(c_walk += clock64() - tk0;)
       if (stop) break;
     }
-    if (KP(a.prof) && lane == 0) {
+    KPROF(if (a.prof && lane == 0) {
       atomicAdd(a.prof + 0, (unsigned long long)(clock64() - tc0));
-      if (a.task_cycles) a.task_cycles[task] = (unsigned long long)(clock64() - tc0);
-      atomicAdd(a.prof + 1, (unsigned long long)p_wait);
-      atomicAdd(a.prof + 2, (unsigned long long)p_walk);
-      atomicAdd(a.prof + 5, (unsigned long long)p_win);
-    }
-    if (lane == 0) hdr->done = 1;
+      atomicAdd(a.prof + 1, (unsigned long long)c_wait);
+      atomicAdd(a.prof + 2, (unsigned long long)c_walk);
+      atomicAdd(a.prof + 5, c_win);
+      atomicAdd(a.prof + 6, c_steps);
+      atomicAdd(a.prof + 7, hovf ? 1ull : 0ull);
+      atomicAdd(a.prof + 8, c_fast);
+      atomicAdd(a.prof + 10, (unsigned long long)c_ph[0]);
+      atomicAdd(a.prof + 11, (unsigned long long)c_ph[1]);
+      atomicAdd(a.prof + 12, (unsigned long long)c_ph[2]);
+    })
+    if (lane == 0) sts_volatile(&hdr->done, 1);
     s_evals += c;
     if (lane < a.kr) {
       const size_t o = ((size_t)b * Pn + pl) * a.kr + lane;
       a.out_ids[o] = lane < top.cnt ? top.id : -1;
       a.out_keys[o] = lane < top.cnt ? top.key : 0u;
     }
+    cp_async_wait_all();
     __syncwarp();
   }
   if (lane == 0 && warp == 0) {
@@ -864,11 +991,13 @@ __global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq,
 
 // dynamic shared memory of one K1 CTA (the kernel's carve-up above)
 size_t search_smem_bytes(const SearchArgs &a, bool sets) {
-  const int nprod = a.starts ? 0 : a.nprod;
-  size_t smem = HDR_BYTES + (size_t)a.ring * 32 * 16 + (size_t)nprod * (a.stages * 32 * (a.pitch + 16) + 512) +
-                (size_t)(a.k * a.k + 32 * a.k) * 4 * (a.P > 0 ? 2 : 1) + (sets ? 2 * QMAX * 4 + (size_t)a.st.vwords * 4 : 0) +
-                EXCAP * 4;
-  if (a.smem_bits) smem += (size_t)(a.bits_words / 2) * 4;   // the evaluated bitmap
+  const size_t RB = (size_t)(a.P > 0 ? 8 : 4) * a.k;
+  const bool wstage = !sets && walk_stage_ok(a.metric, a.st.nchunks);
+  size_t smem = HDR_BYTES + (size_t)a.ring * 32 * 24 + (size_t)2 * 32 * (a.pitch + 16) + 512 +
+                ((a.k * RB + 15) & ~(size_t)15) + ((WPF * RB + 15) & ~(size_t)15) +
+                (wstage ? 512 + (size_t)a.k * a.pitch : 0) + 2 * 32 * 4 +
+                (sets ? 2 * QMAX * 4 + (size_t)a.st.vwords * 4 : 0) + ((size_t)4 << a.hbits);
+  if (a.smem_bits) smem += (size_t)a.de_words * 4 + 16;   // the D/E planes (16-byte aligned)
   return smem;
 }
 
@@ -877,9 +1006,6 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   if (T == 0) return cudaSuccess;
-  // consumer + a.nprod producers (none when the starts are injected)
-  const int nprod = a.starts ? 0 : a.nprod;
-  const int warps = 1 + nprod;
   const size_t smem = search_smem_bytes(a, M == M_JAC);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -887,7 +1013,7 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   }
   // persistent grid: the CTAs that fit at once (dynamic task scheduling balances the tail)
   int per_sm = 0;
-  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL, MB>, warps * 32, smem);
+  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL, MB>, 64, smem);
   if (oe != cudaSuccess) return oe;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int dev = 0, nsm = 148;
@@ -895,12 +1021,13 @@ static cudaError_t run_search(const SearchArgs &a, cudaStream_t s) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   int64_t blocks = T < (int64_t)per_sm * nsm ? T : (int64_t)per_sm * nsm;
   if (blocks > a.gslots) blocks = a.gslots;
+  if (const char *e = getenv("KNNG_GRID")) blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, atoll(e)));   // measurement
   cudaError_t me = cudaMemsetAsync(a.task_ctr, 0, sizeof(unsigned long long), s);
   if (me != cudaSuccess) return me;
   if (getenv("KNNG_PROFILE"))
-    fprintf(stderr, "KNNG_PROFILE k_search: %lld CTAs, %d per SM resident (%zu B smem each)\n", (long long)blocks,
-            per_sm, smem);
-  k_search<M, L, CPL, MB><<<(unsigned)blocks, warps * 32, smem, s>>>(a);
+    fprintf(stderr, "KNNG_PROFILE k_search: %lld CTAs, %d per SM resident (%zu B smem each, ring %d, hash %d, %s D/E)\n",
+            (long long)blocks, per_sm, smem, a.ring, 1 << a.hbits, a.smem_bits ? "smem" : "global");
+  k_search<M, L, CPL, MB><<<(unsigned)blocks, 64, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -918,8 +1045,8 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
 #define X(MM, LL, CC) \
   if (g.metric == MM && g.L == LL && g.CPL == CC) {                                         \
     if constexpr (LEAN_OK(MM, LL, CC))                                                       \
-      if (a.lean && !a.starts && a.nprod == 1) return run_search<MM, LL, CC, 10>(a, s);      \
-    return run_search<MM, LL, CC, 4>(a, s);                                                  \
+      if (a.lean) return run_search<MM, LL, CC, 10>(a, s);                                   \
+    return run_search<MM, LL, CC, 8>(a, s);                                                  \
   }
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)

@@ -274,7 +274,7 @@ __global__ void k_prop_scatter(const int2 *props, const int32_t *prop_cnt, int b
 
 template <int M>
 __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, int32_t *ncnt, int32_t *nfill,
-                             const int32_t *noff, const int2 *sorted, int32_t *lrows, const uint8_t *part_of,
+                             const int32_t *noff, const int2 *sorted, int2 *lrows, const uint8_t *part_of,
                              const int32_t *local_idx) {
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n_t) return;
@@ -303,7 +303,7 @@ __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, i
     const uint8_t pv = part_of[v];
     for (int e = 0; e < k; ++e) {
       const int32_t u = ri[e];
-      lrows[v * k + e] = (u >= 0 && part_of[u] == pv) ? local_idx[u] : -1;
+      lrows[v * k + e] = make_int2(u, (u >= 0 && part_of[u] == pv) ? local_idx[u] : -1);
     }
   }
   ncnt[v] = 0;
@@ -313,7 +313,7 @@ __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, i
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
                                int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted, cudaStream_t s,
-                               int *n_launch, int32_t *lrows, const uint8_t *part_of, const int32_t *local_idx) {
+                               int *n_launch, int2 *lrows, const uint8_t *part_of, const int32_t *local_idx) {
   if (B == 0) return cudaSuccess;
   k_prop_count<<<(unsigned)B, 128, 0, s>>>(props, prop_cnt, ballmax, B, ncnt);
   const int64_t nb = (n_t + 1023) / 1024;
@@ -333,17 +333,17 @@ cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, 
 }
 
 __global__ void k_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
-                        const int32_t *local_idx, int32_t *lrows) {
+                        const int32_t *local_idx, int2 *lrows) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count * k) return;
   const int64_t v = first + i / k;
   const size_t o = (size_t)first * k + i;
   const int32_t u = ids[o];
-  lrows[o] = (u >= 0 && part_of[u] == part_of[v]) ? local_idx[u] : -1;
+  lrows[o] = make_int2(u, (u >= 0 && part_of[u] == part_of[v]) ? local_idx[u] : -1);
 }
 
 cudaError_t launch_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
-                         const int32_t *local_idx, int32_t *lrows, cudaStream_t s) {
+                         const int32_t *local_idx, int2 *lrows, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const int64_t n = count * k;
   k_lrows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ids, k, first, count, part_of, local_idx, lrows);

@@ -68,8 +68,30 @@ def _sync():
         torch.cuda.current_stream().synchronize()
 
 
+def library_graph(points, k, device, capacity=0, stream=None, group=None):
+    """This rank's replica with the LIBRARY-owned NCCL communicator: rank 0 makes the 128-byte NCCL id
+    (graph_nccl_unique_id), torch.distributed broadcasts it, and every rank's graph_init joins the
+    communicator.  graph_insert_batch on the returned handle is then the whole distributed insert in
+    one C-ABI call (all-gathers on the handle's stream, no host sync between the stages)."""
+    import torch.distributed as dist
+    from .knng import KnngGraph, nccl_unique_id
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    idt = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        idt[:] = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        idd = idt.cuda()
+        dist.broadcast(idd, 0, group=group)
+        idt = idd.cpu()
+    else:
+        dist.broadcast(idt, 0, group=group)
+    return KnngGraph(points, k, device=device, capacity=capacity, stream=stream, rank=rank, world=world,
+                     nccl_id=bytes(idt.numpy().tobytes()))
+
+
 class DistributedGraph:
-    """A rank's replica of a partitioned graph (KnngGraph) plus the communicator of the job."""
+    """A rank's replica of a graph driven by the STAGED C-ABI calls and torch.distributed all-gathers
+    (the host-orchestrated form of the library's distributed insert: plumbing tests, gloo)."""
 
     def __init__(self, graph, comm):
         self.g = graph

@@ -35,7 +35,7 @@ class knng_points(C.Structure):
 class knng_params(C.Structure):
     _fields_ = [("speedup", C.c_double), ("expansion_num", C.c_uint32), ("expansion_den", C.c_uint32),
                 ("depth", C.c_int32), ("seed", C.c_uint64), ("start_override", C.c_void_p),
-                ("start_override_len", C.c_int32)]
+                ("start_override_len", C.c_int32), ("full_scan", C.c_int32)]
 
 
 class knng_stats(C.Structure):
@@ -56,7 +56,8 @@ class knng_runtime(C.Structure):
 
 EXPORTS = ["graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
            "graph_get_partition", "graph_size", "graph_degree", "graph_free", "graph_last_error",
-           "graph_ball_bound", "graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit"]
+           "graph_ball_bound", "graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit",
+           "graph_nccl_unique_id", "graph_world"]
 
 _lib = None
 
@@ -92,6 +93,10 @@ def load_library(path=LIB_PATH):
     L.graph_insert_stage_update.argtypes = [P, C.POINTER(knng_params), C.c_int32, P, P, C.c_int64, C.c_int64, P, P,
                                             P, P, C.POINTER(knng_stats)]
     L.graph_insert_stage_commit.argtypes = [P, C.POINTER(knng_params), C.c_int64, P, P, P, P, C.POINTER(knng_stats)]
+    L.graph_nccl_unique_id.argtypes = [P]
+    L.graph_nccl_unique_id.restype = C.c_int
+    L.graph_world.argtypes = [P]
+    L.graph_world.restype = C.c_int32
     for f in ("graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit"):
         getattr(L, f).restype = C.c_int
     for f in ("graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
@@ -167,22 +172,33 @@ def make_points(points):
     return p, a
 
 
-def make_params(speedup, e_num, e_den, depth, seed, starts=None):
+def make_params(speedup, e_num, e_den, depth, seed, starts=None, full_scan=0):
     keep = None
     sp, sl = None, 0
     if starts is not None:
         keep = np.ascontiguousarray(starts, np.int32)
         sp, sl = keep.ctypes.data_as(C.c_void_p), len(keep)
-    return knng_params(float(speedup), int(e_num), int(e_den), int(depth), int(seed), sp, sl), keep
+    return knng_params(float(speedup), int(e_num), int(e_den), int(depth), int(seed), sp, sl, int(full_scan)), keep
+
+
+def nccl_unique_id():
+    """A new 128-byte NCCL unique id (bytes) for KnngGraph(..., rank, world, nccl_id)."""
+    buf = C.create_string_buffer(128)
+    _check(load_library().graph_nccl_unique_id(buf))
+    return buf.raw
 
 
 class KnngGraph:
-    """One graph handle (graph_init ... graph_free)."""
+    """One graph handle (graph_init ... graph_free).  With world > 1 (or an nccl_id), the handle owns an
+    NCCL communicator and insert_batch is the distributed insert (every rank passes the same batch)."""
 
-    def __init__(self, points, k, device=0, capacity=0, stream=None):
+    def __init__(self, points, k, device=0, capacity=0, stream=None, rank=0, world=1, nccl_id=None):
         L = load_library()
         p, keep = make_points(points)
-        rt = knng_runtime(int(device), 0, 1, None, C.c_void_p(stream) if stream else None, int(capacity))
+        self._id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
+        rt = knng_runtime(int(device), int(rank), int(world),
+                          None if self._id is None else C.cast(self._id, C.c_void_p),
+                          C.c_void_p(stream) if stream else None, int(capacity))
         h = C.c_void_p()
         _check(L.graph_init(C.byref(p), int(k), C.byref(rt), C.byref(h)))
         del keep
@@ -203,6 +219,10 @@ class KnngGraph:
             pass
 
     @property
+    def world(self):
+        return int(load_library().graph_world(self._h))
+
+    @property
     def n(self):
         return int(load_library().graph_size(self._h))
 
@@ -214,9 +234,10 @@ class KnngGraph:
         _check(load_library().graph_insert_batch(self._h, C.byref(p), C.byref(prm), C.byref(first), C.byref(st)))
         return int(first.value), st.as_dict()
 
-    def search(self, queries, kr, speedup, e_num, e_den, seed, starts=None, out=None):
+    def search(self, queries, kr, speedup, e_num, e_den, seed, starts=None, out=None, full_scan=0):
+        """graph_search: iGNNS; full_scan=1 with e_den=0 is the GNNS baseline."""
         p, keep = make_points(queries)
-        prm, keep2 = make_params(speedup, e_num, e_den, 1, seed, starts)
+        prm, keep2 = make_params(speedup, e_num, e_den, 1, seed, starts, full_scan)
         st = knng_stats()
         if out is not None:        # device outputs (torch int32 tensors)
             oi, ok = out

@@ -47,5 +47,5 @@ for r in rows:
 tot = sum(v[0] for v in agg.values()) or 1
 toti = sum(v[1] for v in agg.values()) or 1
 print("stall samples %d, instructions %d" % (tot, toti))
-for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+for k, v in sorted(agg.items(), key=lambda x: -x[1][int(__import__("os").environ.get("NCU_SORT_INST", "0"))])[:top]:
     print("%5.1f%% %5.1f%%  %s:%d  %s" % (100 * v[0] / tot, 100 * v[1] / toti, k[0], k[1], src.get(k, "")))

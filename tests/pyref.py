@@ -7,6 +7,7 @@ decision -- so that a dropped term, a wrong sign or a transposed operand in the 
   * mulhi RNG (reading Q4): the SplitMix64 finaliser chain, restated from Steele, Lea & Flood (2014).
   * iGNNS (section 3) LITERALLY: no "restart when moving onto an expanded node" shortcut
     (reading Q9) -- a walk that reaches an expanded node re-scans its row on cached keys.
+  * the GNNS baseline walk (section 2.2): all k neighbours evaluated, move to the best.
   * Alg. 4 with the sampled-candidate medoid update of reading Q22 and the
     acceptance rule of Q23, every score compared as an exact fraction.
 """
@@ -96,8 +97,13 @@ def budget(m, kr, speedup):
 # ---------------------------------------------------------------------------
 # iGNNS, literally
 # ---------------------------------------------------------------------------
-def ignns_literal(metric, point, rows, q, kr, speedup, e_num, e_den, seed, pid, pool=None, part=0, starts=None):
+def ignns_literal(metric, point, rows, q, kr, speedup, e_num, e_den, seed, pid, pool=None, part=0, starts=None,
+                  full_scan=False):
     """Returns (ids, packed keys, stats) of the top-kr evaluated nodes.
+
+    full_scan=True is the GNNS baseline's walk (section 2.2): the similarity of EVERY neighbour
+    of the current node is computed and the walk moves to the most similar one (first in row order
+    among equals) if it improves on the current node.
 
     point(i) -> the stored point i; rows[i] -> node i's neighbour ids (stored order, -1 padded);
     pool = sorted node ids of the searched partition (None: all nodes 0..len(rows)-1)."""
@@ -136,7 +142,23 @@ def ignns_literal(metric, point, rows, q, kr, speedup, e_num, e_den, seed, pid, 
             continue
         first = False
         cur = r
-        while True:                                # hill climbing, eager first improvement
+        while full_scan:                           # GNNS: best of all k neighbours
+            nb = None
+            for v in rows[cur]:
+                v = int(v)
+                if v < 0 or v not in inpool:
+                    continue
+                if v not in val:
+                    if c == b:
+                        return _finish(metric, val, kr, st, c)
+                    val[v] = metric_value(metric, q, point(v))
+                    c += 1
+                if closer(metric, val[v], val[cur]) and (nb is None or closer(metric, val[v], val[nb])):
+                    nb = v
+            if nb is None:
+                break
+            cur = nb
+        while not full_scan:                       # hill climbing, eager first improvement
             moved = False
             for v in rows[cur]:
                 v = int(v)

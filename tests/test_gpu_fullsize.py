@@ -307,3 +307,60 @@ def test_C3_full_prefix():
     _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "C3 full batch")
     gpart, _ = g.partition()
     assert (gpart == o.part_of[:o.n]).all()
+
+
+# ---------------------------------------------------------------------------
+# The library-owned NCCL data plane (graph_insert_batch on a communicator handle): one GPU can only
+# hold a 1-rank communicator, so this runs the whole distributed pipeline -- stage kernels, NCCL
+# all-gathers and the counters' all-reduce on the handle's stream -- with world = 1.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,n0,part", [("C3", 12000, True), ("C1", 6000, False), ("C4", 2500, True)])
+def test_library_nccl_pipeline_one_rank(name, n0, part):
+    from paper_1602_06819_b200 import KnngGraph, nccl_unique_id
+    cfg = D.CONFIGS[name].with_sizes(n0=n0, n_insert=1300)
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    cap = n0 + 1400
+    g = KnngGraph(X, cfg.k, device=0, capacity=cap, rank=0, world=1, nccl_id=nccl_unique_id())
+    assert g.world == 1
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cap)
+    o.init_exact()
+    if part:
+        gp, gm, _ = g.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+        op, om, _ = o.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+        assert (gp == op).all()
+        o.set_partition(op, om)
+    for lo, hi in ((0, 1024), (1024, 1025), (1025, 1300)):
+        _, gst = g.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        ost = o.insert_batch(S[lo:hi], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        assert gst["search_evals"] == ost[:, 0].sum() and gst["proposals"] == ost[:, 5].sum()
+    gi, gk = g.rows()
+    oi, ok = o.rows()
+    _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "nccl pipeline " + name)
+    if part:
+        gpart, _ = g.partition()
+        assert (gpart == o.part_of[:o.n]).all()
+    g.close()
+
+
+# ---------------------------------------------------------------------------
+# GNNS baseline: graph_search with full_scan = 1 against the oracle's GNNS walk
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,n0,part", [("C1", 8000, False), ("C2", 5000, False), ("C3", 12000, True),
+                                          ("C4", 3000, False)])
+def test_gnns_search_matches_oracle(name, n0, part):
+    cfg = D.CONFIGS[name].with_sizes(n0=n0)
+    X = D.initial_points(cfg)
+    Q = D.query_points(cfg, 300)
+    g = _graph(X, cfg.k)
+    o = O.OracleGraph(cfg.metric, X, cfg.k)
+    o.init_exact()
+    if part:
+        gp, gm, _ = g.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+        o.set_partition(gp, gm)
+    for sp, num, den in ((cfg.speedup, 1, 0), (4.0, 1, 0), (cfg.speedup, 6, 5)):
+        gi, gk, gst = g.search(Q, cfg.k, sp, num, den, 21, full_scan=1)
+        oi, ok, ost = o.search(Q, cfg.k, sp, num, den, 21, full_scan=1)
+        _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "GNNS %s sp=%g e=%d/%d" % (name, sp, num, den))
+        assert gst["search_evals"] == ost[:, 0].sum() and gst["search_expansions"] == ost[:, 3].sum()
+        assert gst["search_skipped"] == ost[:, 2].sum()

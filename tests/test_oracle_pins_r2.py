@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
+import datagen as D
 from tests import pyref as R
 
 
@@ -126,3 +127,53 @@ def test_kmedoids_f32_assign_uses_the_capacity_weight():
     assert part.tolist() == [0, 0, 0, 0, 0, 1, 1, 1]
     rpart, rmed, rcost = R.kmedoids(O.F32, g.point, g.ids[:g.n], 2, 1.5, 1, 0, init=[0, 5])
     assert rpart == part.tolist() and rmed == med.tolist() and rcost == cost.tolist()
+
+
+# ---------------------------------------------------------------------------
+# GNNS baseline (section 2.2): full neighbour scan, move to the best neighbour
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("metric", [O.U8, O.F32, O.JAC])
+def test_gnns_equals_literal_full_scan_walk(metric):
+    g, rng = _graph(metric, 240, 6, 1500 + metric)
+    rows = g.ids[:g.n]
+    for qi in range(40):
+        q = _points(metric, rng, 1)[0]
+        sp = float(rng.choice([1.5, 3.0, 8.0]))
+        e_num, e_den = [(1, 0), (6, 5)][qi % 2]     # GNNS proper (no skip) and the ablation with the skip rule
+        ids, keys, st = g.ignns(q, 6, sp, e_num, e_den, seed=13, pid=qi, full_scan=1)
+        rid, rkey, rst = R.ignns_literal(metric, g.point, rows, q, 6, sp, e_num, e_den, 13, qi, full_scan=True)
+        assert ids.tolist() == rid and keys.tolist() == rkey, qi
+        assert (st["evals"], st["starts"], st["skipped"]) == (rst["evals"], rst["starts"], rst["skipped"])
+
+
+def test_gnns_hand_trace_differs_from_eager():
+    """1-D u8 points 0,10,20,30,40 (k=2, rows as W1: 0:(1,2) 1:(0,2) 2:(1,3) 3:(2,4) 4:(3,2)),
+    query 25 (D = 625, 225, 25, 25, 225), injected start [0], e = inf.
+    iGNNS (eager, P:83): expand 0 -> 1 (225) improves, move; expand 1 -> 0 cached, 2 (25) move;
+    expand 2 -> 1 cached, 3 (25) not strictly better: local maximum.  3 expansions, evals 0,1,2,3.
+    GNNS: expand 0 -> evaluates 1 AND 2, moves to the best (2); expand 2 -> 3 (25) not better.
+    2 expansions, same 4 evals.  Budget 2: both stop before evaluating 2 -> (225,1),(625,0)."""
+    X = D.line_points([0, 10, 20, 30, 40])
+    g = O.OracleGraph(O.U8, X, k=2)
+    g.init_exact(1)
+    q = np.array([25], np.uint8)
+    for fs in (0, 1):
+        i2, k2, s2 = g.ignns(q, 2, 2.5, 1, 0, seed=0, pid=0, starts=[0], full_scan=fs)   # budget floor(5/2.5) = 2
+        assert [(int(a), int(b)) for a, b in zip(k2, i2)] == [(225, 1), (625, 0)] and s2["evals"] == 2
+        i5, k5, s5 = g.ignns(q, 2, 1.0, 1, 0, seed=0, pid=0, starts=[0], full_scan=fs)   # budget 5
+        assert [(int(a), int(b)) for a, b in zip(k5, i5)] == [(25, 2), (25, 3)] and s5["evals"] == 4
+        assert s5["expansions"] == (2 if fs else 3)
+
+
+def test_gnns_spec_examples():
+    """SPEC gnns_search examples: unlimited budget -> recall 1.0 vs brute force; a query equal to a
+    stored point is rank 1."""
+    g, rng = _graph(O.U8, 90, 5, 1600)
+    for qi in range(10):
+        q = _points(O.U8, rng, 1)[0]
+        ids, keys, st = g.ignns(q, 5, 1.0, 1, 0, seed=2, pid=qi, full_scan=1)
+        want = sorted((R.metric_value(O.U8, q, g.point(u)), u) for u in range(g.n))[:5]
+        assert [(int(a), int(b)) for a, b in zip(keys, ids)] == [(int(d), u) for d, u in want]
+    for u in (0, 17, 89):
+        ids, keys, st = g.ignns(g.point(u).copy(), 5, 2.0, 1, 0, seed=3, pid=u, full_scan=1, starts=[u])
+        assert ids[0] == u and keys[0] == 0
