@@ -349,52 +349,28 @@ static int check_params(const knng_params *p) {
   return 0;
 }
 
-// K1 launch shape.  Each CTA runs one (query, partition) task at a time: a consumer warp (the
-// sequential iGNNS) and a producer warp (the random starts).  The walks are latency chains, so the
-// plan first makes room for every task at once (up to 8 CTAs per SM, the register limit; 10 with
-// the 96-register build), then puts the task's D/E bit planes in shared memory when they fit, then
-// deepens the ring.  Knobs KNNG_LANE_EVAL / KNNG_RING / KNNG_SMEM_BITS / KNNG_HBITS / KNNG_LEAN /
-// KNNG_WALK_PREFETCH / KNNG_WIN_PREFETCH override it (measurement and tests only: results do not
-// depend on them).
-static void plan_k1(SearchArgs &a, bool sets, bool u8, int64_t tasks, int64_t mmax) {
-  int nsm = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+// K1 launch shape: one warp per (query, partition) task, WPC warps per CTA, as many CTAs as fit;
+// each resident warp owns a slot of E / X bit planes sized for the largest pool.  Knobs
+// KNNG_LANE_EVAL / KNNG_WIN_PREFETCH override it (measurement and tests only: results do not depend
+// on them).
+static int plan_k1(knng_graph *g, SearchArgs &a, int64_t tasks, int64_t mmax) {
   a.de_words = (((mmax + 15) / 16) + 3) & ~3ll;
-  a.x_words = (((mmax + 31) / 32) + 3) & ~3ll;
   a.lane_eval = 1;
-  a.hbits = 12;
-  if (const char *e = getenv("KNNG_HBITS")) a.hbits = std::max(6, std::min(14, atoi(e)));
-  a.lean = (u8 && tasks > (int64_t)nsm * 8) ? 1 : 0;
-  if (const char *e = getenv("KNNG_LEAN")) a.lean = atoi(e) != 0;
-  const int cap = a.lean ? 10 : 8;                 // two-warp CTAs per SM the registers allow
-  const int need = (int)std::min<int64_t>(cap, (tasks + nsm - 1) / nsm);
-  auto occ = [&](const SearchArgs &x) {
-    const size_t sm = search_smem_bytes(x, sets) + 1024;
-    return (int)std::min<size_t>(cap, (228 * 1024) / sm);
-  };
-  // preference order: the D/E planes in shared memory first (no L2 atomics), then the deeper ring
-  const int cand[6][2] = {{1, 16}, {1, 8}, {0, 16}, {0, 8}, {1, 4}, {0, 4}};
-  int best = -1, best_occ = -1;
-  for (int i = 0; i < 6; ++i) {
-    SearchArgs x = a;
-    x.smem_bits = cand[i][0];
-    x.ring = cand[i][1];
-    if (x.smem_bits && (size_t)x.de_words * 4 > 96 * 1024) continue;
-    const int o = occ(x);
-    if (o >= need) { best = i; best_occ = o; break; }
-    if (o > best_occ) { best = i; best_occ = o; }
-  }
-  a.smem_bits = cand[best][0];
-  a.ring = cand[best][1];
   if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
-  a.walk_prefetch = 1;
-  if (const char *e = getenv("KNNG_WALK_PREFETCH")) a.walk_prefetch = atoi(e) != 0;
+  // staged rows: the lane-form widths with nchunks % 8 == 0 are stored swizzled (no bank-conflict pad)
+  const bool sets = g->metric == KNNG_JACCARD_U32SET;
+  const bool lform = !sets && a.lane_eval &&
+                     ((g->metric == KNNG_L2SQ_U8 && (g->geom.nchunks == 8 || g->geom.nchunks == 2)) ||
+                      (g->metric == KNNG_L2SQ_F32 && g->geom.nchunks == 24));
+  a.swz = lform && g->geom.nchunks % 8 == 0;
+  a.pitch = sets ? 16 * 16 + 16 : (int)g->geom.stride + (a.swz ? 0 : 16);
+
   a.win_prefetch = 1;
   if (const char *e = getenv("KNNG_WIN_PREFETCH")) a.win_prefetch = atoi(e) != 0;
-  if (const char *e = getenv("KNNG_RING")) a.ring = atoi(e) <= 4 ? 4 : (atoi(e) <= 8 ? 8 : 16);
-  if (const char *e = getenv("KNNG_SMEM_BITS")) a.smem_bits = atoi(e) != 0;
-  a.gslots = std::min<int64_t>(tasks, (int64_t)nsm * cap);
+  int64_t warps = 0;
+  CK(search_resident_warps(g->geom, a, &warps));
+  a.gslots = std::min<int64_t>(warps, (tasks + 3) / 4 * 4);
+  return 0;
 }
 
 // Largest partition pool (sizes the search's workspaces; the kernel reads the exact sizes on the
@@ -463,16 +439,10 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.out_keys = out_k;
   a.stats = g->w_stats.as<unsigned long long>();
   a.prof = getenv("KNNG_PROFILE") ? a.stats + 16 : nullptr;  // cycle counters -> stats[16..31]
-  a.task_cycles = nullptr;
-  if (a.prof) {
-    CK(g->w_tprof.ensure((size_t)nq * pc * 8));
-    a.task_cycles = g->w_tprof.as<unsigned long long>();
-    g->tprof_n = nq * pc;
-  }
+  if (a.prof) g->tprof_n = nq * pc;
   a.task_ctr = a.stats + 14;
-  a.pitch = g->metric == KNNG_JACCARD_U32SET ? 16 * 16 + 16 : (int)g->geom.stride + 16;
-  plan_k1(a, g->metric == KNNG_JACCARD_U32SET, g->metric == KNNG_L2SQ_U8, nq * pc, mmax);
-  CK(g->w_bits.ensure((size_t)a.gslots * (a.de_words + a.x_words) * 4));
+  if (int r = plan_k1(g, a, nq * pc, mmax)) return r;
+  CK(g->w_bits.ensure((size_t)a.gslots * a.de_words * 4));
   a.gbits = g->w_bits.as<uint32_t>();
   cudaError_t e = launch_search(g->geom, a, g->stream, nl);
   if (e != cudaSuccess) return fail(KNNG_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
@@ -654,12 +624,10 @@ static int stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, c
 static void print_profile(knng_graph *g, const unsigned long long *h, int64_t B) {
   if (!getenv("KNNG_PROFILE") || B <= 0 || !h[16]) return;
   const double T = (double)g->tprof_n > 0 ? (double)g->tprof_n : (double)B;
-  fprintf(stderr, "KNNG_PROFILE per task (%.0f tasks): consumer %.0f cyc (ring wait %.0f, walks %.0f) | producer gather "
-          "wait %.0f, ring-full wait %.0f | windows %.1f, walk steps %.1f, fast chunks %.1f, produced chunks %.1f | "
-          "hash-overflow tasks %.0f\n", T, h[16] / T, h[17] / T, h[18] / T, h[19] / T, h[20] / T, h[21] / T, h[22] / T,
-          h[24] / T, h[25] / T, (double)h[23]);
+  fprintf(stderr, "KNNG_PROFILE per task (%.0f tasks): %.0f cyc, walks %.0f | chunks %.1f (fast %.1f, windows %.1f) | "
+          "walk steps %.1f\n", T, h[16] / T, h[18] / T, h[25] / T, h[24] / T, h[21] / T, h[22] / T);
   if (h[22])
-    fprintf(stderr, "KNNG_PROFILE walk step: %.0f cyc = row %.0f + sets/gathers/keys %.0f + commit %.0f (+ move)\n",
+    fprintf(stderr, "KNNG_PROFILE walk step: %.0f cyc = row %.0f + copies/keys %.0f + commit %.0f (+ move)\n",
             (double)h[18] / h[22], (double)h[26] / h[22], (double)h[27] / h[22], (double)h[28] / h[22]);
 }
 

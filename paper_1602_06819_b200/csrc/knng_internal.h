@@ -68,30 +68,26 @@ struct SearchArgs {
   int kr;
   const int32_t *starts;       // injected start sequence (device, unpartitioned graphs) or null
   int nstarts;
-  // per-task visited state: D/E bit planes (2 bits per pool node) in shared memory when the plan
-  // allows, else in a global slot per CTA followed by the expanded-overflow bitmap
-  uint32_t *gbits;             // global: per CTA slot, de_words + x_words words
-  int64_t gslots;              // CTA slots of gbits (grid cap)
-  int64_t de_words;            // ceil(max pool / 16)
-  int64_t x_words;             // ceil(max pool / 32)
-  int smem_bits;               // 1: D/E planes in dynamic shared memory
-  int hbits;                   // log2 entries of the consumer's walk-evaluated / expanded hash
+  // per-task visited state: the E (evaluated) / X (expanded) bit planes of every warp slot
+  uint32_t *gbits;             // [gslots][de_words]
+  int64_t gslots;              // warp slots of gbits (resident warps of the launch)
+  int64_t de_words;            // ceil(max pool / 16), rounded up to a multiple of 4
   // outputs
   int32_t *out_ids;            // [nq][part_cnt][kr]
   uint32_t *out_keys;
   unsigned long long *stats;   // [0] evals [1] starts [2] skipped [3] expansions
-  unsigned long long *prof;    // optional cycle counters (unused by this kernel), else null
+  unsigned long long *prof;    // cycle counters (profile builds, KNNG_PROFILE=1), else null
   unsigned long long *task_ctr;  // dynamic task scheduler counter (zeroed by the launcher)
-  int pitch;                   // producer stage: bytes per staged row (vectors) / set slot
-  int lane_eval;               // producer evaluates one row per lane where the width allows
-  int ring;                    // ring chunks (8, 16 or 32)
-  int lean;                    // 1: the 96-register variant where instantiated
-  unsigned long long *task_cycles;   // unused (profiling hook), null
-  int walk_prefetch;           // 1: prefetch the rows of all k neighbours during a walk step
+  int pitch;                   // bytes per staged row (vectors: stride + 16) / set slot
+  int wbytes;                  // shared memory of one warp (set by the launcher)
+  int swz;                     // 1: staged rows are swizzled 16-byte chunks (lane-form widths, nchunks % 8 == 0)
+  int lane_eval;               // 1: one lane per staged row where the width allows
   int win_prefetch;            // 1: prefetch the rows of a window's possible starts
   int full_scan;               // 1: the GNNS baseline walk (all k neighbours, move to the best)
 };
 size_t search_smem_bytes(const SearchArgs &a, bool sets);
+// warps of one K1 launch that can be resident at once (sizes the per-warp E / X planes)
+cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t *warps);
 
 struct BallArgs {
   StoreView st;

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python scripts/k1_ab.py --config C3 --n0 2000000 --reps 2 - KNNG_GRID=444 KNNG_GRID=740 > gpurun_out/ab4_C3.log 2>&1
-KNNG_LIB=$PWD/paper_1602_06819_b200/libknng_hack.so timeout 600 python scripts/k1_ab.py --config C3 --n0 2000000 --reps 2 - KNNG_GRID=444 > gpurun_out/ab4_C3_hack.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_search -c 1 -f -o gpurun_out/k1v3_C3 python scripts/k1_ab.py --config C3 --n0 2000000 --reps 1 > gpurun_out/ncuv3.log 2>&1
+echo "rc=$?" >> gpurun_out/ncuv3.log
