@@ -30,6 +30,8 @@ def build(force=False, verbose=False):
     cflags = [f for f in NVCC_FLAGS if f != "-shared"]
     if os.environ.get("KNNG_BUILD_PROFILE"):   # K1 cycle counters (KNNG_PROFILE=1 at run time)
         cflags.append("-DKNNG_PROFILE_COUNTERS")
+    if os.environ.get("KNNG_BUILD_FLAGS"):   # extra nvcc flags (measurement variants, e.g. -DKNNG_K1_MB=8)
+        cflags += os.environ["KNNG_BUILD_FLAGS"].split()
     if os.environ.get("KNNG_BUILD_HACK"):   # timing experiments only (wrong results): see knng_search.cu
         cflags.append("-DKNNG_HACK_" + os.environ["KNNG_BUILD_HACK"])
     if os.environ.get("KNNG_BUILD_DEBUG_WAIT"):   # K1 ring waits report a stuck producer / consumer

@@ -41,6 +41,9 @@
 namespace knng {
 
 constexpr int WPC = 4;            // warps (independent tasks) per CTA
+#ifndef KNNG_K1_MB
+#define KNNG_K1_MB 6              // launch bound: >= 6 CTAs (24 warps) per SM -> <= 80 registers (measured best: 5 -> 96 and 8 -> 64 are slower)
+#endif
 constexpr int WPF = 4;            // window row prefetch slots (draws that may be accepted)
 
 // explicit state spaces for the task's bit planes (global, gpu-scope: one warp reads and writes them)
@@ -259,12 +262,13 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       tb = te = 0;
       if (M == M_JAC && d.x >= 0) { tb = a.st.off[d.y]; te = a.st.off[d.y + 1]; }
     };
-    // next chunk's draws dnx (pool loaded; sets: offsets bnx / enx in flight); sets: dnx2 one level deeper
+    // next chunk's draws dnx (pool loaded; sets: offsets bnx / enx in flight) and dnx2 (pool loads in flight)
     int2 dnx = make_int2(-1, -1), dnx2 = make_int2(-1, -1);
     uint64_t bnx = 0, enx = 0;
     if (budget > 0) {
       dnx = draw(0);
-      if (M == M_JAC) { offs(dnx, bnx, enx); dnx2 = draw(1); }
+      if (M == M_JAC) offs(dnx, bnx, enx);
+      dnx2 = draw(1);
     }
     // the window: the current chunk, lanes >= wpos not yet processed
     int32_t wl = -1, wnode = -1;
@@ -281,13 +285,11 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         wnode = dnx.y;
         const uint64_t cb = bnx, ce = enx;
         const uint32_t ew = issue(dnx, cb, ce);
-        if (M == M_JAC) {
-          dnx = dnx2;
-          offs(dnx, bnx, enx);
-          dnx2 = draw(ch + 2);
-        } else {
-          dnx = draw(ch + 1);
-        }
+        // the next chunk's pool loads were issued a chunk ago (sets: its offsets now); the one after
+        // next starts its pool loads
+        dnx = dnx2;
+        if (M == M_JAC) offs(dnx, bnx, enx);
+        dnx2 = draw(ch + 2);
         cp_async_wait_all();
         __syncwarp();
         const bool ok = wl >= 0;
@@ -642,7 +644,7 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch) {
   if (n_launch) ++*n_launch;
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, 5>(a, s);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, KNNG_K1_MB>(a, s);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
@@ -669,7 +671,7 @@ static cudaError_t resident(SearchArgs a, int64_t *warps) {
 
 cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t *warps) {
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, 5>(a, warps);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, KNNG_K1_MB>(a, warps);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
