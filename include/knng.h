@@ -89,7 +89,11 @@ typedef struct {
  *                 the similarity of EVERY neighbour of the current node is computed and the walk moves
  *                 to the most similar one (the first in row order among equals) if it improves; with
  *                 expansion_den = 0 (no restart skipping) this is GNNS, the baseline iGNNS is compared
- *                 with.  0 = iGNNS's eager first-improvement walk. */
+ *                 with.  0 = iGNNS's eager first-improvement walk.
+ *  route          partitioned graphs: 1 = search only the partition of the query's nearest medoid
+ *                 (ties -> lowest p, as placement) -- the "queries sent to partitions by medoid
+ *                 distance" variant of reading Q18; 0 = every partition (Alg. 3).  Single-GPU
+ *                 handles only (INVALID_ARG on a multi-GPU handle). */
 typedef struct {
   double speedup;
   uint32_t expansion_num, expansion_den;
@@ -98,6 +102,7 @@ typedef struct {
   const int32_t *start_override;
   int32_t start_override_len;
   int32_t full_scan;
+  int32_t route;
 } knng_params;
 
 /* Counters and per-phase device times of the last call (CUDA events on the handle's stream). */
@@ -175,6 +180,15 @@ int graph_search(knng_graph *g, const knng_points *queries, int32_t kr, const kn
 int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, int32_t max_iter,
                        uint64_t seed, uint8_t *part_out, int32_t *medoids_out, int64_t *cost_out,
                        const int32_t *init_medoids);
+
+/* graph_recompute_medoids -- the last step of Alg. 5 ("compute new medoids"; F5):
+ * the update step of Alg. 4 on the CURRENT partition (nodes keep their partitions; the inserted ones
+ * were placed at their nearest medoid): every medoid becomes the member minimising the hop sum in its
+ * cluster-induced undirected subgraph -- exact when |C| <= 4096, else over {current medoid} + 63
+ * draws of stream (seed, 0xFFFFFFFD, epoch * P + p, j) (reading Q22).  Later inserts are placed by
+ * the new medoids.  medoids_out: int32[P] or NULL; cost_out: total hop sum or NULL (host pointers).
+ * Errors: INVALID_ARG (not partitioned, epoch < 0, a staged batch pending), OOM, CUDA. */
+int graph_recompute_medoids(knng_graph *g, uint64_t seed, int64_t epoch, int32_t *medoids_out, int64_t *cost_out);
 
 /* ---- Staged insert: the multi-GPU building blocks (all buffers are DEVICE pointers) ----
  * graph_insert_batch == stage_search(all partitions) + stage_update(world 1, all queries) +

@@ -468,6 +468,7 @@ typedef struct {
   uint64_t seed;
   int nthreads;
   int full_scan;          /* graph_search only: the GNNS baseline walk */
+  int route;              /* 1: search only the partition of the nearest medoid (reading Q18's variant) */
 } or_params;
 
 typedef struct { int32_t node; uint32_t key; int32_t qid; } or_prop;
@@ -498,6 +499,8 @@ typedef struct {
   int rc;
 } or_search_job;
 
+static int nearest_medoid(const or_graph *G, or_point x);
+
 static void *search_worker(void *arg) {
   or_search_job *J = (or_search_job *)arg;
   const or_graph *G = J->G;
@@ -521,7 +524,12 @@ static void *search_worker(void *arg) {
     }
     Cq.cap = J->kr; Cq.cnt = 0; Cq.key = J->cand_keys + b * J->kr; Cq.id = J->cand_ids + b * J->kr;
     for (t = 0; t < 4; ++t) J->stats[b * 4 + t] = 0;
-    for (p = 0; p < nparts; ++p) {
+    {
+      int p0 = 0, p1 = nparts;
+      /* routing variant (Q18: "queries sent to partitions by medoid distance"): only the partition of
+       * the nearest medoid (ties -> lowest p, as placement) is searched */
+      if (J->prm->route && G->P > 0) { p0 = nearest_medoid(G, q); p1 = p0 + 1; }
+    for (p = p0; p < p1; ++p) {
       or_search_cfg C;
       or_list T;
       or_search_stats st;
@@ -543,6 +551,7 @@ static void *search_worker(void *arg) {
       for (t = 0; t < T.cnt; ++t) list_insert(G->metric, &Cq, T.key[t], T.id[t]);
       J->stats[b * 4 + 0] += st.evals; J->stats[b * 4 + 1] += st.starts;
       J->stats[b * 4 + 2] += st.skipped; J->stats[b * 4 + 3] += st.expansions;
+    }
     }
     for (t = Cq.cnt; t < J->kr; ++t) { Cq.id[t] = -1; Cq.key[t] = 0; }
   }
@@ -650,7 +659,7 @@ int or_insert_batch(int metric, int dim, void *data, uint64_t *off, int k,
                     int P, uint8_t *part_of, int32_t *members, int64_t *member_cnt,
                     int64_t member_cap, const int32_t *medoids,
                     int64_t B, double speedup, uint64_t e_num, uint64_t e_den, int depth,
-                    uint64_t seed, int nthreads, int64_t *out_stats) {
+                    uint64_t seed, int nthreads, int64_t *out_stats, int route) {
   or_graph G;
   or_params prm;
   or_search_job J;
@@ -668,7 +677,7 @@ int or_insert_batch(int metric, int dim, void *data, uint64_t *off, int k,
   G.ids = ids; G.keys = keys; G.P = P; G.part_of = part_of; G.members = members;
   G.member_cnt = member_cnt; G.member_cap = member_cap; G.medoids = medoids;
   prm.speedup = speedup; prm.e_num = e_num; prm.e_den = e_den; prm.depth = depth;
-  prm.seed = seed; prm.nthreads = nthreads; prm.full_scan = 0;
+  prm.seed = seed; prm.nthreads = nthreads; prm.full_scan = 0; prm.route = route;
   S = graph_store(&G);
   if (B <= 0) return 0;
 
@@ -769,7 +778,7 @@ int or_insert_sequential(int metric, int dim, void *data, uint64_t *off, int k,
   G.metric = metric; G.dim = dim; G.k = k; G.data = data; G.off = off; G.n = n_t;
   G.ids = ids; G.keys = keys;
   prm.speedup = speedup; prm.e_num = e_num; prm.e_den = e_den; prm.depth = depth;
-  prm.seed = seed; prm.nthreads = 1; prm.full_scan = 0;
+  prm.seed = seed; prm.nthreads = 1; prm.full_scan = 0; prm.route = 0;
   S = graph_store(&G);
   x = store_point(&S, n_t);
 
@@ -828,7 +837,8 @@ int or_graph_search(int metric, int dim, void *data, uint64_t *off, int k,
                     int64_t member_cap,
                     const void *qdata, const uint64_t *qoff, int64_t nq, int kr,
                     double speedup, uint64_t e_num, uint64_t e_den, uint64_t seed,
-                    int nthreads, int32_t *out_ids, uint32_t *out_keys, int64_t *out_stats4, int full_scan) {
+                    int nthreads, int32_t *out_ids, uint32_t *out_keys, int64_t *out_stats4, int full_scan,
+                    const int32_t *medoids, int route) {
   or_graph G;
   or_params prm;
   or_search_job J;
@@ -838,7 +848,8 @@ int or_graph_search(int metric, int dim, void *data, uint64_t *off, int k,
   G.ids = ids; G.keys = keys; G.P = P; G.part_of = part_of; G.members = members;
   G.member_cnt = member_cnt; G.member_cap = member_cap;
   prm.speedup = speedup; prm.e_num = e_num; prm.e_den = e_den; prm.depth = 1;
-  prm.seed = seed; prm.nthreads = nthreads; prm.full_scan = full_scan;
+  prm.seed = seed; prm.nthreads = nthreads; prm.full_scan = full_scan; prm.route = route;
+  G.medoids = medoids;
   memset(&J, 0, sizeof J);
   J.G = &G; J.prm = &prm; J.first_query = 0; J.kr = kr; J.cand_ids = out_ids; J.cand_keys = out_keys;
   J.stats = out_stats4; J.qpoint = NULL; J.qdata = qdata; J.qoff = qoff; J.pid_is_index = 1;

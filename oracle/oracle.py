@@ -60,13 +60,13 @@ def lib():
                                           P, P, P, i32]
             L.or_insert_batch.restype = i32
             L.or_insert_batch.argtypes = [i32, i32, P, P, i32, i64, P, P, i32, P, P, P, i64, P,
-                                          i64, dbl, u64, u64, i32, u64, i32, P]
+                                          i64, dbl, u64, u64, i32, u64, i32, P, i32]
             L.or_insert_sequential.restype = i32
             L.or_insert_sequential.argtypes = [i32, i32, P, P, i32, i64, P, P, dbl, u64, u64, i32,
                                                u64, P]
             L.or_graph_search.restype = i32
             L.or_graph_search.argtypes = [i32, i32, P, P, i32, i64, P, P, i32, P, P, P, i64,
-                                          P, P, i64, i32, dbl, u64, u64, u64, i32, P, P, P, i32]
+                                          P, P, i64, i32, dbl, u64, u64, u64, i32, P, P, P, i32, P, i32]
             L.or_partition_kmedoids.restype = i32
             L.or_partition_kmedoids.argtypes = [i32, i32, P, P, i64, i32, P, i32, dbl, i32, u64,
                                                 P, P, P, i64, i32, P]
@@ -303,7 +303,8 @@ class OracleGraph:
         return part, med, cost[:rc]
 
     # -- A1..A8: one batch -------------------------------------------------------
-    def insert_batch(self, pts, speedup, e_num, e_den, depth, seed, nthreads=None):
+    def insert_batch(self, pts, speedup, e_num, e_den, depth, seed, nthreads=None, route=0):
+        """route=1: search only the nearest medoid's partition (reading Q18's routing variant)."""
         B = len(pts)
         n_t = self.n
         self._append_points(pts)
@@ -312,7 +313,7 @@ class OracleGraph:
                                    _p(self.ids), _p(self.keys), self.P, _p(self.part_of),
                                    _p(self.members), _p(self.member_cnt), self.member_cap,
                                    _p(self.medoids), B, speedup, e_num, e_den, depth, seed,
-                                   nthreads or default_threads(), _p(st))
+                                   nthreads or default_threads(), _p(st), int(route))
         if rc:
             raise RuntimeError("or_insert_batch rc=%d" % rc)
         self.n = n_t + B
@@ -331,8 +332,9 @@ class OracleGraph:
         self.n = n_t + 1
         return st
 
-    def search(self, queries, kr, speedup, e_num, e_den, seed, nthreads=None, full_scan=0):
-        """graph_search; full_scan=1 with e_den=0 is the GNNS baseline."""
+    def search(self, queries, kr, speedup, e_num, e_den, seed, nthreads=None, full_scan=0, route=0):
+        """graph_search; full_scan=1 with e_den=0 is the GNNS baseline; route=1 searches only the
+        nearest medoid's partition (reading Q18's routing variant)."""
         if self.metric == JAC:
             qoff = np.zeros(len(queries) + 1, np.uint64)
             qoff[1:] = np.cumsum([len(q) for q in queries])
@@ -348,7 +350,8 @@ class OracleGraph:
                                    _p(self.ids), _p(self.keys), self.P, _p(self.part_of),
                                    _p(self.members), _p(self.member_cnt), self.member_cap,
                                    _p(qd), _p(qoff), nq, kr, speedup, e_num, e_den, seed,
-                                   nthreads or default_threads(), _p(oi), _p(ok), _p(st), int(full_scan))
+                                   nthreads or default_threads(), _p(oi), _p(ok), _p(st), int(full_scan),
+                                   _p(self.medoids), int(route))
         if rc:
             raise RuntimeError("or_graph_search rc=%d" % rc)
         return oi, ok, st
@@ -379,6 +382,21 @@ class OracleGraph:
                               _p(st_a), 0 if st_a is None else len(st_a), _p(oi), _p(ok), _p(st), int(full_scan))
         return oi, ok, dict(evals=int(st[0]), starts=int(st[1]), skipped=int(st[2]),
                             expansions=int(st[3]))
+
+    def recompute_medoids(self, seed, epoch, exact_limit=4096, ncand=64):
+        """Alg. 5's last step: the Alg. 4 update step on the current partition."""
+        L = lib()
+        if not hasattr(L, "_rm"):
+            L.or_recompute_medoids.restype = C.c_int
+            L.or_recompute_medoids.argtypes = [C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                               C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+            L._rm = True
+        med = np.ascontiguousarray(self.medoids, np.int32).copy()
+        cost = np.zeros(1, np.int64)
+        L.or_recompute_medoids(self.n, self.k, _p(self.ids), self.P, _p(self.part_of), _p(med), seed, epoch,
+                               exact_limit, ncand, _p(cost))
+        self.medoids = med
+        return med, int(cost[0])
 
     def nearest_medoid(self, x):
         if self.metric == JAC:

@@ -216,7 +216,7 @@ static void free_graph(knng_graph *g) {
   for (void *b : bufs)
     if (b) cudaFree(b);
   DBuf *ws[] = {&g->w_bits, &g->w_cand_i, &g->w_cand_k, &g->w_C_i, &g->w_C_k, &g->w_hash, &g->w_list, &g->w_props,
-                &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts,
+                &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts, &g->w_route,
                 &g->w_qoff, &g->w_qtok, &g->w_tprof};
   for (DBuf *b : ws) b->release();
   g->w_dense.part.release();
@@ -406,6 +406,16 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   int64_t mmax = 0;
   if (int r = max_pool(g, &mmax)) return r;
   if (g->P > 0 && mmax == 0) return fail(KNNG_ERR_EMPTY, "all partitions are empty");
+  // routing variant (reading Q18): one task per query, on the partition of its nearest medoid
+  const bool routed = p->route && g->P > 0;
+  if (routed) {
+    CK(g->w_route.ensure((size_t)std::max<int64_t>(nq, 1) * 4));
+    CK(launch_route_target(g->geom, qs, qrow0, nq, graph_store_view(g), g->P, g->medoids, g->w_route.as<int32_t>(),
+                           g->stream));
+    ++*nl;
+    part_lo = 0;
+    part_hi = 1;
+  }
   const int pc = part_hi - part_lo;
   SearchArgs a;
   memset(&a, 0, sizeof a);
@@ -435,6 +445,7 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.starts = d_starts;
   a.nstarts = nstarts;
   a.full_scan = p->full_scan != 0;
+  a.route = routed ? g->w_route.as<int32_t>() : nullptr;
   a.out_ids = out_i;
   a.out_keys = out_k;
   a.stats = g->w_stats.as<unsigned long long>();
@@ -502,6 +513,7 @@ static int stage_search(knng_graph *g, const knng_points *pts, const knng_params
   if (q_hi > B || q_lo > q_hi) return fail(KNNG_ERR_INVALID_ARG, "bad query range");
   g->pend_B = B;
   g->pend_parts = part_hi - part_lo;
+  g->pend_route = p->route && g->P > 0;
   if (B == 0) return 0;
   // A1: batch ingest into the store tail (ids n_t .. n_t+B-1)
   if (int r = store_points(g, pts, n_t)) return r;
@@ -522,7 +534,7 @@ static int stage_update(knng_graph *g, const knng_params *p, int world, const in
   // A4: keep the k best of the P*k per-partition candidates (all-gathered, rank-major)
   int32_t *Ci = (int32_t *)ci_all;
   uint32_t *Ck = (uint32_t *)ck_all;
-  if (g->P > 0) {
+  if (g->P > 0 && !g->pend_route) {
     if (g->P % world) return fail(KNNG_ERR_INVALID_ARG, "P=%d not divisible by world=%d", g->P, world);
     if (g->pend_parts * world != g->P)   // the gathered candidates must cover every partition
       return fail(KNNG_ERR_INVALID_ARG, "stage_update: %d ranks x %d searched partitions != P=%d", world, g->pend_parts,
@@ -643,6 +655,43 @@ static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t 
 
 static int insert_batch_dist(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st);
 
+// B = 1 on an unpartitioned single-GPU graph -- the paper's sequential algorithm (Alg. 1 + Alg. 2,
+// P:109-151): ingest, K1 on one task, and the fused one-warp update (new row = C, ball, proposals
+// applied in place); three launches and one synchronisation per insert.
+static int insert_one(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st) {
+  int nl = 0;
+  CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  if (int r = stage_search(g, pts, p, 0, 1, -1, -1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl)) {
+    g->pend_B = 0;
+    return r;
+  }
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  const int64_t n_t = g->n;
+  const int64_t ballmax = ball_bound(n_t, g->k, p->depth);
+  int hcap = 64;
+  while (hcap < 2 * ballmax) hcap <<= 1;
+  BallArgs ba;
+  memset(&ba, 0, sizeof ba);
+  ba.st = graph_store_view(g);
+  ba.ids = g->ids;
+  ba.keys = g->keys;
+  ba.k = g->k;
+  ba.n_t = n_t;
+  ba.B = 1;
+  ba.depth = p->depth;
+  ba.C = g->w_cand_i.as<int32_t>();
+  ba.hcap = hcap;
+  ba.ballmax = (int)ballmax;
+  ba.stats = g->w_stats.as<unsigned long long>();
+  CK(launch_update_one(g->geom, ba, g->w_cand_k.as<uint32_t>(), g->stream));
+  ++nl;
+  CK(cudaEventRecord(g->ev[2], g->stream));
+  g->n = n_t + 1;
+  g->pend_B = 0;
+  return finish_stats(g, st, nl, 3, 1);
+}
+
 int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,
                        knng_stats *st) {
   knng_err_slot().clear();
@@ -651,6 +700,14 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   if (first_id_out) *first_id_out = g->n;
   CK(cudaSetDevice(g->device));
   if (g->comm) return insert_batch_dist(g, pts, p, st);
+  // the sequential algorithm's fast path (the ball of a B = 1 insert fits one warp's shared memory)
+  if (pts && pts->n == 1 && g->P == 0 && p && p->depth >= 1 && p->depth <= 10 && !getenv("KNNG_NO_B1") &&
+      ball_bound(g->n, g->k, p->depth) <= 4096) {
+    CK(g->w_stats.ensure(32 * 8));
+    CK(g->w_cand_i.ensure((size_t)g->k * 4));
+    CK(g->w_cand_k.ensure((size_t)g->k * 4));
+    return insert_one(g, pts, p, st);
+  }
   CK(g->w_stats.ensure(32 * 8));
   CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   const int64_t B = pts ? pts->n : 0, k = g->k;
@@ -709,6 +766,7 @@ static int insert_batch_dist_(knng_graph *g, const knng_points *pts, const knng_
   const int64_t B = pts ? pts->n : 0, n_t = g->n;
   const int P = g->P;
   if (P > 0 && P % G) return fail(KNNG_ERR_INVALID_ARG, "P=%d is not a multiple of the world size %d", P, G);
+  if (p && p->route) return fail(KNNG_ERR_INVALID_ARG, "route: single-GPU handles only");
   const int64_t S = (B + G - 1) / G;                     // query slots per rank (balls, new rows)
   const int64_t qlo = std::min<int64_t>(r * S, B), qhi = std::min<int64_t>(qlo + S, B);
   if (p && (p->depth < 1 || p->depth > 10)) return fail(KNNG_ERR_INVALID_ARG, "depth %d outside 1..10", p->depth);
@@ -894,7 +952,7 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
     ok = g->w_C_k.as<uint32_t>();
   }
   CK(cudaEventRecord(g->ev[0], g->stream));
-  if (g->P > 0) {
+  if (g->P > 0 && !p->route) {
     CK(g->w_cand_i.ensure((size_t)nq * g->P * kr * 4));
     CK(g->w_cand_k.ensure((size_t)nq * g->P * kr * 4));
     if (int r = run_search_phase(g, qs, 0, nq, 0, kr, p, d_starts, nstarts, 0, g->P, g->w_cand_i.as<int32_t>(),

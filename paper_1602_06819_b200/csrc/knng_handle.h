@@ -49,6 +49,8 @@ struct knng_graph {
   int64_t n = 0, cap = 0;
   int64_t pend_B = 0;                           // batch ingested by stage_search, not yet committed
   int pend_parts = 0;                           // partitions stage_search searched for the pending batch
+  int pend_route = 0;                           // ... or 1: the batch was searched on its routed partitions
+  DBuf w_route;                                 // routing targets of a search
   knng::VecGeom geom{};
   int device = 0;
   cudaStream_t stream = nullptr;

@@ -84,6 +84,7 @@ struct SearchArgs {
   int lane_eval;               // 1: one lane per staged row where the width allows
   int win_prefetch;            // 1: prefetch the rows of a window's possible starts
   int full_scan;               // 1: the GNNS baseline walk (all k neighbours, move to the best)
+  const int32_t *route;        // routed search (reading Q18's variant): partition of query b, else null
 };
 size_t search_smem_bytes(const SearchArgs &a, bool sets);
 // warps of one K1 launch that can be resident at once (sizes the per-warp E / X planes)
@@ -119,6 +120,8 @@ cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, 
                             int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi, uint32_t *ok, DenseScratch *ws,
                             cudaStream_t s);
 cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cudaStream_t s);
+// B = 1: new row, ball, proposals and their application for one insert (one warp, one launch)
+cudaError_t launch_update_one(const VecGeom &g, const BallArgs &a, const uint32_t *Ckeys, cudaStream_t s);
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
                                int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted,
@@ -136,6 +139,9 @@ cudaError_t launch_tc_topk_f32(const VecGeom &g, const uint8_t *vec, int64_t row
                                uint32_t *pk, Scratch *norm, cudaStream_t s);
 cudaError_t launch_exact_build(const VecGeom &g, const StoreView &st, int64_t n, int k, int32_t *ids,
                                uint32_t *keys, DenseScratch *ws, cudaStream_t s);
+// nearest medoid of queries [qrow0, qrow0 + nq) of qs (ties -> lowest p): the routing target
+cudaError_t launch_route_target(const VecGeom &g, const StoreView &qs, int64_t qrow0, int64_t nq, const StoreView &st,
+                                int P, const int32_t *medoids, int32_t *target, cudaStream_t s);
 cudaError_t launch_place(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int P,
                          const int32_t *medoids, int32_t *members, int64_t member_cap, int64_t *member_cnt,
                          uint8_t *part_of, int32_t *local_idx, int32_t *target_tmp, cudaStream_t s);

@@ -25,6 +25,8 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "knng_common.cuh"
 #include "knng_internal.h"
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   uint32_t *pkey = (uint32_t *)(qsm + 512);                                // [32] pending walk evaluations
   int32_t *pid = (int32_t *)(pkey + 32);                                   // [32]
   uint32_t *qscr = (uint32_t *)(pid + 32);                                 // [QMAX] query tokens (sets)
-  int *sched = (int *)(smem + (size_t)WPC * a.wbytes);                     // [WPC] next task per warp
+  long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
   const int nck = M == M_JAC ? 0 : a.st.nchunks;
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
@@ -167,11 +169,11 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   while (task < T) {
     const int64_t b = task / Pn;
     const int pl = (int)(task % Pn);          // output slot
-    const int p = a.part_lo + pl;             // partition searched
+    const int p = a.route ? a.route[b] : a.part_lo + pl;   // partition searched
     const int64_t m = a.P > 0 ? a.member_cnt[p] : a.n_t;
     const int32_t *pool = a.P > 0 ? a.members + (size_t)p * a.member_cap : nullptr;
     // next task (dynamic scheduling), read back at the end of this one
-    if (lane == 0) sched[warp] = (int)(gridDim.x * WPC + atomicAdd(a.task_ctr, 1ull));
+    if (lane == 0) sched[warp] = (long long)(gridDim.x * WPC + atomicAdd(a.task_ctr, 1ull));
     KPROF(const long long tc0 = clock64(); long long c_walk = 0; unsigned long long c_win = 0, c_steps = 0,
           c_fast = 0, c_chunks = 0; long long c_ph[3] = {0, 0, 0};)
     // clear the task's E / X planes
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     }
     cp_async_wait_all();
     __syncwarp();
-    task = *(volatile int *)(sched + warp);
+    task = *(volatile long long *)(sched + warp);
     __syncwarp();
   }
   if (lane == 0) {
@@ -601,7 +603,34 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   size_t b = (size_t)32 * a.pitch + ((a.k * RB + 15) & ~(size_t)15) + ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QMAX * 4 : 0);
   return (b + 15) & ~(size_t)15;
 }
-size_t search_smem_bytes(const SearchArgs &a, bool sets) { return WPC * search_warp_bytes(a, sets) + 16 * WPC; }
+size_t search_smem_bytes(const SearchArgs &a, bool sets) { return WPC * search_warp_bytes(a, sets) + 8 * WPC; }
+
+// occupancy of a K1 instantiation at a shared-memory size on the current device, cached (a B = 1 insert
+// launches K1 once per point: the attribute / occupancy queries would otherwise dominate its host time)
+template <int M, int L, int CPL, int MB>
+static cudaError_t k1_occupancy(size_t smem, int *per_sm, int *nsm) {
+  static std::mutex mu;
+  static std::map<std::pair<int, size_t>, std::pair<int, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, smem});
+  if (it != cache.end()) {
+    *per_sm = it->second.first;
+    *nsm = it->second.second;
+    return cudaSuccess;
+  }
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_search<M, L, CPL, MB>, 32 * WPC, smem);
+  if (e != cudaSuccess) return e;
+  *nsm = 148;
+  cudaDeviceGetAttribute(nsm, cudaDevAttrMultiProcessorCount, dev);
+  cache[{dev, smem}] = {*per_sm, *nsm};
+  return cudaSuccess;
+}
 
 template <int M, int L, int CPL, int MB>
 static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
@@ -610,23 +639,17 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   a.wbytes = (int)search_warp_bytes(a, M == M_JAC);
   const size_t smem = search_smem_bytes(a, M == M_JAC);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
   // persistent grid: the CTAs that fit at once (dynamic task scheduling balances the tail)
-  int per_sm = 0;
-  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL, MB>, 32 * WPC, smem);
-  if (oe != cudaSuccess) return oe;
+  int per_sm = 0, nsm = 148;
+  if (cudaError_t oe = k1_occupancy<M, L, CPL, MB>(smem, &per_sm, &nsm)) return oe;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   int64_t blocks = std::min<int64_t>((T + WPC - 1) / WPC, (int64_t)per_sm * nsm);
   blocks = std::min<int64_t>(blocks, a.gslots / WPC);
   if (const char *e = getenv("KNNG_GRID")) blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, atoll(e)));   // measurement
-  cudaError_t me = cudaMemsetAsync(a.task_ctr, 0, sizeof(unsigned long long), s);
-  if (me != cudaSuccess) return me;
+  if (T > blocks * WPC) {   // the dynamic task counter is only read when there are more tasks than warps
+    cudaError_t me = cudaMemsetAsync(a.task_ctr, 0, sizeof(unsigned long long), s);
+    if (me != cudaSuccess) return me;
+  }
   if (getenv("KNNG_PROFILE"))
     fprintf(stderr, "KNNG_PROFILE k_search: %lld CTAs x %d warps, %d CTAs per SM resident (%zu B smem each)\n",
             (long long)blocks, WPC, per_sm, smem);
@@ -654,17 +677,9 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
 
 template <int M, int L, int CPL, int MB>
 static cudaError_t resident(SearchArgs a, int64_t *warps) {
-  a.wbytes = (int)search_warp_bytes(a, M == M_JAC);
   const size_t smem = search_smem_bytes(a, M == M_JAC);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  int per_sm = 0, dev = 0, nsm = 148;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<M, L, CPL, MB>, 32 * WPC, smem);
-  if (e != cudaSuccess) return e;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 0, nsm = 148;
+  if (cudaError_t e = k1_occupancy<M, L, CPL, MB>(smem, &per_sm, &nsm)) return e;
   *warps = (int64_t)per_sm * nsm * WPC;
   return cudaSuccess;
 }

@@ -143,6 +143,102 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// B = 1 (the paper's sequential algorithm, Alg. 1 + Alg. 2): the whole update of one insert in one warp.
+// The new row is the search result C (no batch peers); the ball is collected over the snapshot rows
+// first (levels with dedup, Q12-Q13), its nodes are evaluated, and then every proposal is applied in
+// place -- each ball node's row has exactly one writer (the ball is a set), so no bucketing is needed.
+// Shared memory: hash [hcap] + list [ballmax] + proposals [ballmax] (node, key).
+// ---------------------------------------------------------------------------
+template <int M, int L, int CPL>
+__global__ void __launch_bounds__(32) k_update_one(BallArgs a, const uint32_t *Ckeys) {
+  extern __shared__ int32_t usm[];
+  __shared__ uint32_t qscr[M == M_JAC ? QMAX : 1];
+  __shared__ int s_n;
+  const int lane = threadIdx.x;
+  const int k = a.k;
+  int32_t *hash = usm;
+  int32_t *list = hash + a.hcap;
+  int2 *props = (int2 *)(list + a.ballmax + (a.ballmax & 1));
+  const int32_t idx = (int32_t)a.n_t;            // the new point's id
+  // new row n_t = C (the top-k of the search; B = 1 has no batch peers)
+  if (lane < k) {
+    a.ids[(size_t)idx * k + lane] = a.C[lane];
+    a.keys[(size_t)idx * k + lane] = Ckeys[lane];
+  }
+  for (int i = lane; i < a.hcap; i += 32) hash[i] = -1;
+  if (lane == 0) s_n = 0;
+  __syncwarp();
+  typename QuerySel<M, L, CPL>::T Q;
+  Q.load(a.st, a.n_t, M == M_JAC ? qscr : nullptr);
+  {
+    const int32_t v = lane < k ? a.C[lane] : -1;
+    const bool ins = v >= 0 && hash_insert(hash, a.hcap, v);
+    const unsigned m = __ballot_sync(FULL, ins);
+    if (ins) list[__popc(m & lanemask_lt())] = v;
+    if (lane == 0) s_n = __popc(m);
+    __syncwarp();
+  }
+  // levels 1..DEPTH over the snapshot rows: collect the ball, evaluate, propose
+  int lo = 0, hi = s_n, np = 0;
+  for (int d = 1; d <= a.depth; ++d) {
+    for (int base = lo; base < hi; base += 32) {
+      const int t = base + lane;
+      const int32_t v = t < hi ? list[t] : -1;
+      if (d < a.depth && v >= 0) {
+        for (int e = 0; e < k; ++e) {
+          const int32_t u = a.ids[(size_t)v * k + e];
+          if (u >= 0 && u != idx && hash_insert(hash, a.hcap, u)) {
+            const int pos = atomicAdd(&s_n, 1);
+            if (pos < a.ballmax) list[pos] = u;
+          }
+        }
+      }
+      const int cnt = hi - base < 32 ? hi - base : 32;
+      const uint32_t key = Q.eval(a.st, v, cnt);
+      bool prop = false;
+      if (v >= 0) prop = precedes<M>(key, idx, a.keys[(size_t)v * k + k - 1], a.ids[(size_t)v * k + k - 1]);
+      const unsigned pm = __ballot_sync(FULL, prop);
+      if (prop) props[np + __popc(pm & lanemask_lt())] = make_int2(v, (int)key);
+      np += __popc(pm);
+    }
+    __syncwarp();
+    lo = hi;
+    hi = s_n < a.ballmax ? s_n : a.ballmax;
+    __syncwarp();
+  }
+  // apply (Q14): row_v = top-k(row_v u {(D, idx)}); one lane per proposal, distinct rows
+  for (int j = lane; j < np; j += 32) {
+    const int32_t v = props[j].x;
+    const uint32_t key = (uint32_t)props[j].y;
+    int32_t *ri = a.ids + (size_t)v * k;
+    uint32_t *rk = a.keys + (size_t)v * k;
+    int pos = k - 1;
+    while (pos > 0 && precedes<M>(key, idx, rk[pos - 1], ri[pos - 1])) {
+      rk[pos] = rk[pos - 1];
+      ri[pos] = ri[pos - 1];
+      --pos;
+    }
+    rk[pos] = key;
+    ri[pos] = idx;
+  }
+  if (lane == 0) {
+    atomicAdd(a.stats + 4, (unsigned long long)lo);
+    atomicAdd(a.stats + 5, (unsigned long long)np);
+  }
+}
+
+template <int M, int L, int CPL>
+static cudaError_t run_update_one(const BallArgs &a, const uint32_t *Ckeys, cudaStream_t s) {
+  const size_t smem = (size_t)(a.hcap + a.ballmax + 1) * 4 + (size_t)a.ballmax * 8;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_update_one<M, L, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_update_one<M, L, CPL><<<1, 32, smem, s>>>(a, Ckeys);
+  return cudaGetLastError();
+}
+
 template <int M, int L, int CPL>
 static cudaError_t run_ball(const BallArgs &a, int64_t nslots, cudaStream_t s) {
   if (a.nqb == 0) return cudaSuccess;
@@ -158,6 +254,16 @@ static cudaError_t run_ball(const BallArgs &a, int64_t nslots, cudaStream_t s) {
 #define KNNG_SHAPES_F32(X) \
   X(M_F32, 1, 1) X(M_F32, 1, 2) X(M_F32, 1, 3) X(M_F32, 1, 4) X(M_F32, 2, 3) X(M_F32, 2, 4) X(M_F32, 4, 3) \
   X(M_F32, 4, 4) X(M_F32, 8, 3) X(M_F32, 8, 4) X(M_F32, 32, 2) X(M_F32, 32, 4)
+
+cudaError_t launch_update_one(const VecGeom &g, const BallArgs &a, const uint32_t *Ckeys, cudaStream_t s) {
+#define X(MM, LL, CC) \
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_update_one<MM, LL, CC>(a, Ckeys, s);
+  KNNG_SHAPES(X, M_U8)
+  KNNG_SHAPES_F32(X)
+  X(M_JAC, 8, 1)
+#undef X
+  return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cudaStream_t s) {
 #define X(MM, LL, CC) \
@@ -396,6 +502,39 @@ __global__ void k_place_append(int64_t n_t, int64_t B, int P, const int32_t *tar
     __syncthreads();
   }
   for (int p = threadIdx.x; p < P; p += blockDim.x) member_cnt[p] = base[p];
+}
+
+// key of query row i of qs against graph row j of st (two stores)
+template <int M>
+__device__ __forceinline__ uint32_t cross_key(const StoreView &qs, int64_t i, const StoreView &st, int64_t j) {
+  if (M == M_JAC) {
+    const uint64_t ai = qs.off[i], bj = st.off[j];
+    return set_key(qs.tok + ai, (int)(qs.off[i + 1] - ai), st.tok + bj, (int)(st.off[j + 1] - bj));
+  }
+  return thread_dist<M>((const uint4 *)(qs.vec + (size_t)i * qs.stride), (const uint4 *)(st.vec + (size_t)j * st.stride),
+                        st.nchunks);
+}
+template <int M>
+__global__ void k_route_target(StoreView qs, int64_t qrow0, int64_t nq, StoreView st, int P, const int32_t *medoids,
+                               int32_t *target) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq) return;
+  int best = 0;
+  uint32_t bk = 0;
+  for (int p = 0; p < P; ++p) {
+    const uint32_t kp = cross_key<M>(qs, qrow0 + i, st, medoids[p]);
+    if (p == 0 || closer<M>(kp, bk)) { best = p; bk = kp; }
+  }
+  target[i] = best;
+}
+cudaError_t launch_route_target(const VecGeom &g, const StoreView &qs, int64_t qrow0, int64_t nq, const StoreView &st,
+                                int P, const int32_t *medoids, int32_t *target, cudaStream_t s) {
+  if (nq == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((nq + 127) / 128);
+  if (g.metric == M_U8) k_route_target<M_U8><<<blocks, 128, 0, s>>>(qs, qrow0, nq, st, P, medoids, target);
+  else if (g.metric == M_F32) k_route_target<M_F32><<<blocks, 128, 0, s>>>(qs, qrow0, nq, st, P, medoids, target);
+  else k_route_target<M_JAC><<<blocks, 128, 0, s>>>(qs, qrow0, nq, st, P, medoids, target);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_place(const VecGeom &g, const StoreView &st, int64_t n_t, int64_t B, int P, const int32_t *medoids,

@@ -35,7 +35,7 @@ class knng_points(C.Structure):
 class knng_params(C.Structure):
     _fields_ = [("speedup", C.c_double), ("expansion_num", C.c_uint32), ("expansion_den", C.c_uint32),
                 ("depth", C.c_int32), ("seed", C.c_uint64), ("start_override", C.c_void_p),
-                ("start_override_len", C.c_int32), ("full_scan", C.c_int32)]
+                ("start_override_len", C.c_int32), ("full_scan", C.c_int32), ("route", C.c_int32)]
 
 
 class knng_stats(C.Structure):
@@ -57,7 +57,7 @@ class knng_runtime(C.Structure):
 EXPORTS = ["graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
            "graph_get_partition", "graph_size", "graph_degree", "graph_free", "graph_last_error",
            "graph_ball_bound", "graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit",
-           "graph_nccl_unique_id", "graph_world"]
+           "graph_nccl_unique_id", "graph_world", "graph_recompute_medoids"]
 
 _lib = None
 
@@ -95,6 +95,8 @@ def load_library(path=LIB_PATH):
     L.graph_insert_stage_commit.argtypes = [P, C.POINTER(knng_params), C.c_int64, P, P, P, P, C.POINTER(knng_stats)]
     L.graph_nccl_unique_id.argtypes = [P]
     L.graph_nccl_unique_id.restype = C.c_int
+    L.graph_recompute_medoids.argtypes = [P, C.c_uint64, C.c_int64, P, C.POINTER(C.c_int64)]
+    L.graph_recompute_medoids.restype = C.c_int
     L.graph_world.argtypes = [P]
     L.graph_world.restype = C.c_int32
     for f in ("graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit"):
@@ -172,13 +174,14 @@ def make_points(points):
     return p, a
 
 
-def make_params(speedup, e_num, e_den, depth, seed, starts=None, full_scan=0):
+def make_params(speedup, e_num, e_den, depth, seed, starts=None, full_scan=0, route=0):
     keep = None
     sp, sl = None, 0
     if starts is not None:
         keep = np.ascontiguousarray(starts, np.int32)
         sp, sl = keep.ctypes.data_as(C.c_void_p), len(keep)
-    return knng_params(float(speedup), int(e_num), int(e_den), int(depth), int(seed), sp, sl, int(full_scan)), keep
+    return knng_params(float(speedup), int(e_num), int(e_den), int(depth), int(seed), sp, sl, int(full_scan),
+                       int(route)), keep
 
 
 def nccl_unique_id():
@@ -226,18 +229,19 @@ class KnngGraph:
     def n(self):
         return int(load_library().graph_size(self._h))
 
-    def insert_batch(self, points, speedup, e_num, e_den, depth, seed):
+    def insert_batch(self, points, speedup, e_num, e_den, depth, seed, route=0):
         p, keep = make_points(points)
-        prm, _ = make_params(speedup, e_num, e_den, depth, seed)
+        prm, _ = make_params(speedup, e_num, e_den, depth, seed, route=route)
         first = C.c_int64()
         st = knng_stats()
         _check(load_library().graph_insert_batch(self._h, C.byref(p), C.byref(prm), C.byref(first), C.byref(st)))
         return int(first.value), st.as_dict()
 
-    def search(self, queries, kr, speedup, e_num, e_den, seed, starts=None, out=None, full_scan=0):
-        """graph_search: iGNNS; full_scan=1 with e_den=0 is the GNNS baseline."""
+    def search(self, queries, kr, speedup, e_num, e_den, seed, starts=None, out=None, full_scan=0, route=0):
+        """graph_search: iGNNS; full_scan=1 with e_den=0 is the GNNS baseline; route=1 searches only
+        the nearest medoid's partition (reading Q18's variant)."""
         p, keep = make_points(queries)
-        prm, keep2 = make_params(speedup, e_num, e_den, 1, seed, starts, full_scan)
+        prm, keep2 = make_params(speedup, e_num, e_den, 1, seed, starts, full_scan, route)
         st = knng_stats()
         if out is not None:        # device outputs (torch int32 tensors)
             oi, ok = out
@@ -305,6 +309,16 @@ class KnngGraph:
         _check(load_library().graph_get_rows(self._h, int(first), int(count), ids.ctypes.data_as(C.c_void_p),
                                              keys.ctypes.data_as(C.c_void_p)))
         return ids, keys
+
+    def recompute_medoids(self, seed, epoch):
+        """graph_recompute_medoids (Alg. 5's last step): returns (medoids, total hop-sum cost)."""
+        L = load_library()
+        med = np.zeros(256, np.int32)
+        cost = C.c_int64()
+        _check(L.graph_recompute_medoids(self._h, int(seed), int(epoch), med.ctypes.data_as(C.c_void_p),
+                                         C.byref(cost)))
+        _, m = self.partition()
+        return m, int(cost.value)
 
     def partition(self):
         P = C.c_int32()

@@ -114,6 +114,51 @@ def main():
                              update_sims_per_insert=ball / 8192))
             g.close()
         print("%s done (init %.1f s)" % (tag, t_init), file=sys.stderr, flush=True)
+    # F4 partition count, routing variant (Q18), F5 medoid recomputation interval: the C3 recipe (u8 d=128)
+    cfg = D.CONFIGS["C3"].with_sizes(n0=min(args.n0, 100_000))
+    X = D.initial_points(cfg)
+    Q = D.query_points(cfg, args.nq, seed_offset=7)
+    tag = "C3 recipe n0=%d" % cfg.n0
+    g0 = KnngGraph(X, cfg.k)
+    ex = exact_knn(cfg, X, Q, cfg.k)
+    ids, _, st = g0.search(Q, cfg.k, cfg.speedup, cfg.e_num, cfg.e_den, 5)
+    rows.append(dict(study="F4 partition count", workload=tag, P=0, speedup=cfg.speedup, recall=recall(ids, ex),
+                     routed_recall=None, sims_per_query=st["search_evals"] / len(Q)))
+    g0.close()
+    for P in (1, 2, 4, 8, 16):
+        g = KnngGraph(X, cfg.k)
+        g.partition_kmedoids(P, cfg.imbalance, 10, cfg.part_seed)
+        ids, _, st = g.search(Q, cfg.k, cfg.speedup, cfg.e_num, cfg.e_den, 5)
+        rid, _, rst = g.search(Q, cfg.k, cfg.speedup, cfg.e_num, cfg.e_den, 5, route=1)
+        rows.append(dict(study="F4 partition count", workload=tag, P=P, speedup=cfg.speedup, recall=recall(ids, ex),
+                         routed_recall=recall(rid, ex), sims_per_query=st["search_evals"] / len(Q),
+                         routed_sims_per_query=rst["search_evals"] / len(Q)))
+        g.close()
+    # F5: a stream of as many inserts as the initial graph, medoids recomputed every 10% of the graph size
+    n_ins = cfg.n0
+    S = D.stream_points(cfg, 0, n_ins)
+    allp = np.concatenate([X, S])
+    for interval in (0.1, None):
+        g = KnngGraph(X, cfg.k, capacity=cfg.n0 + n_ins + 8)
+        g.partition_kmedoids(cfg.P, cfg.imbalance, 10, cfg.part_seed)
+        pos, nxt, epoch, nrec = 0, (int(cfg.n0 * interval) if interval else None), 0, 0
+        while pos < n_ins:
+            B = min(cfg.batch, n_ins - pos)
+            g.insert_batch(S[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+            pos += B
+            if nxt is not None and pos >= nxt:
+                g.recompute_medoids(cfg.part_seed, epoch)
+                epoch += 1
+                nrec += 1
+                nxt = pos + int((cfg.n0 + pos) * interval)
+        rs = np.random.default_rng(11)
+        nodes = np.sort(rs.choice(cfg.n0 + n_ins, 1000, replace=False))
+        exr = exact_knn(cfg, allp, allp[nodes], cfg.k, exclude=nodes)
+        got, _ = g.rows()
+        rows.append(dict(study="F5 medoid recomputation", workload=tag + " + %d inserts, P=%d" % (n_ins, cfg.P),
+                         interval="every 10%" if interval else "never", recomputations=nrec,
+                         correct_edges=recall(got[nodes], exr)))
+        g.close()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(rows, open(args.out + ".json", "w"), indent=1)
     with open(args.out + ".md", "w") as f:
@@ -122,7 +167,8 @@ def main():
         for study in sorted({r["study"] for r in rows}):
             rr = [r for r in rows if r["study"] == study]
             keys = [k for k in rr[0] if k != "study"]
-            f.write("## %s\n\n| %s |\n|%s|\n" % (study, " | ".join(keys), "---|" * len(keys)))
+            keys = list(dict.fromkeys(k for r in rr for k in r if k != "study"))
+            f.write("## %s\n\n| %s |\n|%s\n" % (study, " | ".join(keys), "---|" * len(keys)))
             for r in rr:
                 f.write("| %s |\n" % " | ".join(("%.4f" % r[k]) if isinstance(r.get(k), float) else str(r.get(k))
                                               for k in keys))

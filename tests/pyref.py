@@ -201,6 +201,56 @@ def _hop_sum(c, members, adj):
     return sum(dist.get(u, len(members)) for u in members)
 
 
+def _best_medoid(members, adj, cur, seed, tag, stream, exact_limit, ncand):
+    """(hop sum, id) of the candidate minimising the hop sum; candidates: every member when
+    |C| <= exact_limit, else (Q22) the current medoid and ncand - 1 draws of stream (seed, tag, stream, j)."""
+    if len(members) <= exact_limit:
+        cands = members
+    else:
+        cands = ([cur] if cur in set(members) else []) + [
+            members[rng_draw(seed, tag, stream, j, len(members))] for j in range(ncand - 1)]
+    return min((_hop_sum(c, members, adj), c) for c in cands)   # ties -> smaller id
+
+
+def _cluster_adj(members, rows):
+    ms = set(members)
+    adj = {u: set() for u in members}
+    for u in members:
+        for v in rows[u]:
+            v = int(v)
+            if v in ms:
+                adj[u].add(v)
+                adj[v].add(u)
+    return adj
+
+
+def recompute_medoids(rows, part, med, seed, epoch, exact_limit=4096, ncand=64):
+    """Alg. 5's last step: every medoid becomes its cluster's hop-sum minimiser on the current
+    graph and partition (stream tag 0xFFFFFFFD, stream epoch * P + p).  Returns (medoids, total cost)."""
+    P = len(med)
+    out, cost = [], 0
+    for p in range(P):
+        members = [u for u in range(len(part)) if part[u] == p]
+        if not members:
+            out.append(int(med[p]))
+            continue
+        bs, bc = _best_medoid(members, _cluster_adj(members, rows), int(med[p]), seed, 0xFFFFFFFD, epoch * P + p,
+                              exact_limit, ncand)
+        out.append(bc)
+        cost += bs
+    return out, cost
+
+
+def nearest_medoid(metric, point, q, med):
+    """Placement / routing target: argmin_p D(q, medoid_p), ties -> lowest p."""
+    best = None
+    for p, m in enumerate(med):
+        v = metric_value(metric, q, point(int(m)))
+        if best is None or closer(metric, v, best[0]):
+            best = (v, p)
+    return best[1]
+
+
 def kmedoids(metric, point, rows, P, imbalance, max_iter, seed, exact_limit=4096, ncand=64, init=None):
     """Returns (part, medoids, costs of the kept iterations)."""
     n = len(rows)
@@ -236,20 +286,8 @@ def kmedoids(metric, point, rows, P, imbalance, max_iter, seed, exact_limit=4096
             if not members:
                 newmed.append(med[p])
                 continue
-            ms = set(members)
-            adj = {u: set() for u in members}
-            for u in members:
-                for v in rows[u]:
-                    v = int(v)
-                    if v in ms:
-                        adj[u].add(v)
-                        adj[v].add(u)
-            if len(members) <= exact_limit:
-                cands = members
-            else:                                  # Q22: current medoid + ncand - 1 seeded draws
-                cands = ([med[p]] if med[p] in ms else []) + [
-                    members[rng_draw(seed, 0xFFFFFFFE, it * P + p, j, len(members))] for j in range(ncand - 1)]
-            bs, bc = min((_hop_sum(c, members, adj), c) for c in cands)   # ties -> smaller id
+            adj = _cluster_adj(members, rows)
+            bs, bc = _best_medoid(members, adj, med[p], seed, 0xFFFFFFFE, it * P + p, exact_limit, ncand)
             newmed.append(bc)
             cost += bs
         if it > 0 and cost > prev:                 # Q23: an iteration that raises the cost is not kept

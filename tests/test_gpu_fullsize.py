@@ -364,3 +364,42 @@ def test_gnns_search_matches_oracle(name, n0, part):
         _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "GNNS %s sp=%g e=%d/%d" % (name, sp, num, den))
         assert gst["search_evals"] == ost[:, 0].sum() and gst["search_expansions"] == ost[:, 3].sum()
         assert gst["search_skipped"] == ost[:, 2].sum()
+
+
+# ---------------------------------------------------------------------------
+# Alg. 5's medoid recomputation (graph_recompute_medoids) and the routing variant (knng_params.route)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,n0", [("C3", 9000), ("C4", 2500)])
+def test_recompute_medoids_and_routing_match_oracle(name, n0):
+    cfg = D.CONFIGS[name].with_sizes(n0=n0, n_insert=1500)
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    Q = D.query_points(cfg, 200)
+    cap = n0 + 1600
+    g = _graph(X, cfg.k, cap)
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cap)
+    o.init_exact()
+    gp, gm, _ = g.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+    op, om, _ = o.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+    assert (gp == op).all() and gm.tolist() == om.tolist()
+    o.set_partition(op, om)
+    # routed search (every query on its nearest medoid's partition)
+    gi, gk, gst = g.search(Q, cfg.k, cfg.speedup, cfg.e_num, cfg.e_den, 5, route=1)
+    oi, ok, ost = o.search(Q, cfg.k, cfg.speedup, cfg.e_num, cfg.e_den, 5, route=1)
+    _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "routed search")
+    assert gst["search_evals"] == ost[:, 0].sum()
+    # a stream with routed inserts, the medoids recomputed after 10% and 20% more (F5)
+    pos, epoch = 0, 0
+    for B in (700, 300, 500):
+        g.insert_batch(S[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed, route=1)
+        o.insert_batch(S[pos:pos + B], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed, route=1)
+        pos += B
+        gmed, gcost = g.recompute_medoids(31, epoch)
+        omed, ocost = o.recompute_medoids(31, epoch)
+        assert gmed.tolist() == omed.tolist() and gcost == ocost
+        epoch += 1
+    gi, gk = g.rows()
+    oi, ok = o.rows()
+    _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "routed stream with medoid recomputation")
+    gpart, _ = g.partition()
+    assert (gpart == o.part_of[:o.n]).all()

@@ -177,3 +177,49 @@ def test_gnns_spec_examples():
     for u in (0, 17, 89):
         ids, keys, st = g.ignns(g.point(u).copy(), 5, 2.0, 1, 0, seed=3, pid=u, full_scan=1, starts=[u])
         assert ids[0] == u and keys[0] == 0
+
+
+# ---------------------------------------------------------------------------
+# Alg. 5's medoid recomputation and the nearest-medoid routing variant (reading Q18)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("metric", [O.U8, O.JAC])
+@pytest.mark.parametrize("exact_limit", [4096, 20])
+def test_recompute_medoids_equals_rederivation(metric, exact_limit):
+    g, rng = _graph(metric, 220, 4, 1700 + metric)
+    g.cap = 400
+    part, med, _ = g.partition_kmedoids(4, 1.05, 3, 2)
+    g.set_partition(part, med)
+    pts = _points(metric, rng, 60)
+    g.insert_batch(pts if metric == O.JAC else np.stack(pts), 3.0, 6, 5, 2, 8)
+    rows = g.ids[:g.n]
+    for epoch in (0, 3):
+        want, wcost = R.recompute_medoids(rows, g.part_of[:g.n], g.medoids, 17, epoch, exact_limit, 8)
+        got, cost = g.recompute_medoids(17, epoch, exact_limit, 8)
+        assert got.tolist() == want and cost == wcost
+
+
+@pytest.mark.parametrize("metric", [O.U8, O.JAC])
+def test_routed_search_equals_literal_walk_on_nearest_partition(metric):
+    g, rng = _graph(metric, 240, 5, 1800 + metric)
+    part, med, _ = g.partition_kmedoids(4, 1.05, 3, 2)
+    g.set_partition(part, med)
+    rows = g.ids[:g.n]
+    qs = [_points(metric, rng, 1)[0] for _ in range(20)]
+    qa = qs if metric == O.JAC else np.stack(qs)
+    ids, keys, st = g.search(qa, 5, 2.5, 6, 5, 3, route=1)
+    for i, q in enumerate(qs):
+        p = R.nearest_medoid(metric, g.point, q, g.medoids)
+        pool = np.nonzero(part == p)[0].tolist()
+        rid, rkey, rst = R.ignns_literal(metric, g.point, rows, q, 5, 2.5, 6, 5, 3, i, pool=pool, part=p)
+        assert ids[i].tolist()[:len(rid)] == rid and keys[i].tolist()[:len(rkey)] == rkey
+        assert st[i, 0] == rst["evals"]
+
+
+def test_routing_with_one_partition_is_unpartitioned():
+    g, rng = _graph(O.U8, 150, 5, 1900)
+    h, _ = _graph(O.U8, 150, 5, 1900)
+    h.set_partition(np.zeros(150, np.uint8), np.array([0], np.int32))
+    Q = np.stack(_points(O.U8, rng, 12))
+    a = g.search(Q, 5, 4.0, 6, 5, 7)
+    b = h.search(Q, 5, 4.0, 6, 5, 7, route=1)
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all() and (a[2] == b[2]).all()
