@@ -19,8 +19,13 @@ for name, n0, B in (("C0", 700, 64), ("C2", 600, 64), ("C4", 400, 48)):
     g = KnngGraph(X, cfg.k, capacity=n0 + 4 * B)
     g.search(Q, cfg.k, 3.0, cfg.e_num, cfg.e_den, 1)
     g.insert_batch(S[:B], 3.0, cfg.e_num, cfg.e_den, cfg.depth, 1)
+    for i in range(3):                          # B = 1 fast path (fused one-warp update)
+        g.insert_batch(S[B + i:B + i + 1], 3.0, cfg.e_num, cfg.e_den, cfg.depth, 1)
+    g.search(Q, cfg.k, 3.0, 1, 0, 1, full_scan=1)   # GNNS walk
     g.partition_kmedoids(4, 1.05, 2, 3)
-    g.insert_batch(S[B:2 * B], 3.0, cfg.e_num, cfg.e_den, cfg.depth, 1)
+    g.insert_batch(S[B + 3:2 * B], 3.0, cfg.e_num, cfg.e_den, cfg.depth, 1)
+    g.search(Q, cfg.k, 3.0, cfg.e_num, cfg.e_den, 1, route=1)   # routing variant
+    g.recompute_medoids(3, 0)
     reps = [KnngGraph(X, cfg.k, capacity=n0 + 4 * B) for _ in range(2)]
     for r in reps:
         r.partition_kmedoids(4, 1.05, 2, 3)

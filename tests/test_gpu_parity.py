@@ -195,6 +195,37 @@ def test_insert_C0_sequential_batches_of_one():
     _run_stream(cfg, [1] * 60)
 
 
+@pytest.mark.parametrize("name,n0,depth,k", [("C2", 3000, 3, 20), ("C4", 1500, 2, 10), ("C1", 2500, 1, 1),
+                                              ("C0", 400, 4, 32)])
+def test_insert_batches_of_one_fast_path(name, n0, depth, k, monkeypatch):
+    """B = 1 takes the fused one-warp update (insert_one); every metric, depths 1-4, k = 1..32: equal to
+    the oracle after every insert, and the batched path (KNNG_NO_B1) reaches the same graph."""
+    cfg = _cfg_small(name, n0=n0, n_insert=40)
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    cap = cfg.n0 + cfg.n_insert + 8
+    g = _graph(X, k, cap)
+    o = O.OracleGraph(cfg.metric, X, k, capacity=cap)
+    o.init_exact()
+    for i in range(cfg.n_insert):
+        first, gst = g.insert_batch(S[i:i + 1], cfg.speedup, cfg.e_num, cfg.e_den, depth, cfg.search_seed)
+        ost = o.insert_batch(S[i:i + 1], cfg.speedup, cfg.e_num, cfg.e_den, depth, cfg.search_seed)
+        assert first == cfg.n0 + i and gst["kernel_launches"] <= 3
+        assert gst["search_evals"] == ost[:, 0].sum() and gst["ball_nodes"] == ost[:, 4].sum()
+        assert gst["proposals"] == ost[:, 5].sum()
+        if i % 8 == 7 or i == cfg.n_insert - 1:
+            gi, gk = g.rows()
+            oi, ok = o.rows()
+            _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "%s B=1 after %d" % (name, i + 1))
+    monkeypatch.setenv("KNNG_NO_B1", "1")
+    h = _graph(X, k, cap)
+    for i in range(cfg.n_insert):
+        h.insert_batch(S[i:i + 1], cfg.speedup, cfg.e_num, cfg.e_den, depth, cfg.search_seed)
+    hi, hk = h.rows()
+    gi, gk = g.rows()
+    assert (hi == gi).all() and (hk == gk).all()
+
+
 def test_insert_C1_shape():
     cfg = _cfg_small("C1", n0=20000, n_insert=2100)
     _run_stream(cfg, [1024, 1024, 52])
