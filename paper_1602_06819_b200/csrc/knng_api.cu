@@ -359,15 +359,49 @@ static int plan_k1(knng_graph *g, SearchArgs &a, int64_t tasks, int64_t mmax) {
   if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
   // staged rows: the lane-form widths with nchunks % 8 == 0 are stored swizzled (no bank-conflict pad)
   const bool sets = g->metric == KNNG_JACCARD_U32SET;
-  const bool lform = !sets && a.lane_eval &&
-                     ((g->metric == KNNG_L2SQ_U8 && (g->geom.nchunks == 8 || g->geom.nchunks == 2)) ||
-                      (g->metric == KNNG_L2SQ_F32 && g->geom.nchunks == 24));
+  const bool lform = search_lane_form(g->geom, a.lane_eval);
   a.swz = lform && g->geom.nchunks % 8 == 0;
   a.pitch = sets ? 16 * 16 + 16 : (int)g->geom.stride + (a.swz ? 0 : 16);
 
+  // walk steps copy the rows of all of cur's neighbours with their vectors when the vectors dominate the
+  // step's bytes anyway (measured: C2's 384-byte rows gain 6%, the 128-byte rows of C1/C3/C4 lose 12-17%)
+  a.row_pf = !sets && g->geom.stride >= 256;
+  if (const char *e = getenv("KNNG_ROW_PF")) a.row_pf = atoi(e) != 0;
   a.win_prefetch = 1;
   if (const char *e = getenv("KNNG_WIN_PREFETCH")) a.win_prefetch = atoi(e) != 0;
+  // latency-bound launches (every task resident at once): the E bitmap (and, if it fits too, the X
+  // bitmap) in shared memory and two chunk stages, if that plan still holds every task; else the E / X
+  // bits in the per-slot global words and one stage
   int64_t warps = 0;
+  a.e_smem = 0;
+  a.x_smem = 0;
+  a.ns2 = 0;
+  a.e_bytes = 0;
+  const int64_t eb = (((mmax + 31) / 32) * 4 + 15) & ~15ll;   // one bitmap
+  int es_mode = -1;   // -1: automatic
+  if (const char *e = getenv("KNNG_ESMEM")) es_mode = atoi(e);
+  if (a.kt) {   // the key table's launch: E and X in shared memory, no chunk stages in flight
+    a.e_smem = 1;
+    a.x_smem = 1;
+    a.e_bytes = (int)eb;
+  } else if (!sets && es_mode != 0 && eb <= 64 * 1024) {
+    for (int xs = 1; xs >= 0 && !a.e_smem; --xs) {
+      SearchArgs t = a;
+      t.e_smem = 1;
+      t.x_smem = xs;
+      t.ns2 = 1;
+      t.e_bytes = (int)eb;
+      if (const char *e = getenv("KNNG_NS2")) t.ns2 = atoi(e) != 0;
+      if (const char *e = getenv("KNNG_XSMEM")) t.x_smem = atoi(e) != 0;
+      int64_t w2 = 0;
+      if (search_resident_warps(g->geom, t, &w2) == cudaSuccess && w2 > 0 && (es_mode == 1 || w2 >= tasks)) {
+        a.e_smem = 1;
+        a.x_smem = t.x_smem;
+        a.ns2 = t.ns2;
+        a.e_bytes = t.e_bytes;
+      }
+    }
+  }
   CK(search_resident_warps(g->geom, a, &warps));
   a.gslots = std::min<int64_t>(warps, (tasks + 3) / 4 * 4);
   return 0;
@@ -452,6 +486,12 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.prof = getenv("KNNG_PROFILE") ? a.stats + 16 : nullptr;  // cycle counters -> stats[16..31]
   if (a.prof) g->tprof_n = nq * pc;
   a.task_ctr = a.stats + 14;
+  if (g->fuse_b1) {
+    a.fuse = 1;
+    a.ub = *g->fuse_b1;
+    // small graphs: one key table for the search and the update (<= 32 KB of shared memory)
+    a.kt = g->n <= 8192 && !getenv("KNNG_NO_KT");
+  }
   if (int r = plan_k1(g, a, nq * pc, mmax)) return r;
   CK(g->w_bits.ensure((size_t)a.gslots * a.de_words * 4));
   a.gbits = g->w_bits.as<uint32_t>();
@@ -641,6 +681,9 @@ static void print_profile(knng_graph *g, const unsigned long long *h, int64_t B)
   if (h[22])
     fprintf(stderr, "KNNG_PROFILE walk step: %.0f cyc = row %.0f + copies/keys %.0f + commit %.0f (+ move)\n",
             (double)h[18] / h[22], (double)h[26] / h[22], (double)h[27] / h[22], (double)h[28] / h[22]);
+  if (h[25])
+    fprintf(stderr, "KNNG_PROFILE chunk: draw+gather+keys %.0f cyc; fast chunks: decision %.0f + commit %.0f cyc\n",
+            (double)h[29] / h[25], h[24] ? (double)h[30] / h[24] : 0.0, h[24] ? (double)h[31] / h[24] : 0.0);
 }
 
 static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t B) {
@@ -656,17 +699,10 @@ static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t 
 static int insert_batch_dist(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st);
 
 // B = 1 on an unpartitioned single-GPU graph -- the paper's sequential algorithm (Alg. 1 + Alg. 2,
-// P:109-151): ingest, K1 on one task, and the fused one-warp update (new row = C, ball, proposals
-// applied in place); three launches and one synchronisation per insert.
+// P:109-151): ingest, then ONE launch in which a warp searches (K1, one task) and runs the insert's
+// update (new row = C, ball, proposals applied in place), and one synchronisation for the stats.
 static int insert_one(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st) {
   int nl = 0;
-  CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
-  CK(cudaEventRecord(g->ev[0], g->stream));
-  if (int r = stage_search(g, pts, p, 0, 1, -1, -1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl)) {
-    g->pend_B = 0;
-    return r;
-  }
-  CK(cudaEventRecord(g->ev[1], g->stream));
   const int64_t n_t = g->n;
   const int64_t ballmax = ball_bound(n_t, g->k, p->depth);
   int hcap = 64;
@@ -684,12 +720,18 @@ static int insert_one(knng_graph *g, const knng_points *pts, const knng_params *
   ba.hcap = hcap;
   ba.ballmax = (int)ballmax;
   ba.stats = g->w_stats.as<unsigned long long>();
-  CK(launch_update_one(g->geom, ba, g->w_cand_k.as<uint32_t>(), g->stream));
-  ++nl;
-  CK(cudaEventRecord(g->ev[2], g->stream));
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  g->fuse_b1 = &ba;
+  const int r = stage_search(g, pts, p, 0, 1, -1, -1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl);
+  g->fuse_b1 = nullptr;
+  if (r) {
+    g->pend_B = 0;
+    return r;
+  }
+  CK(cudaEventRecord(g->ev[1], g->stream));
   g->n = n_t + 1;
   g->pend_B = 0;
-  return finish_stats(g, st, nl, 3, 1);
+  return finish_stats(g, st, nl, 2, 1);
 }
 
 int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,

@@ -41,6 +41,27 @@ struct VecGeom {
   int L, CPL;   // lanes per vector and chunks per lane of the warp evaluator
 };
 
+struct BallArgs {
+  StoreView st;
+  int32_t *ids;                // rows (snapshot until the merge)
+  uint32_t *keys;
+  int k;
+  int64_t n_t;
+  int64_t B;
+  int depth;
+  const int32_t *C;            // search results [B][k] (all B queries of the batch)
+  int64_t q0;                  // this launch handles queries q0 .. q0+nqb-1 (props index is local)
+  int64_t nqb;
+  int32_t *hash;               // per warp slot, hcap entries
+  int hcap;
+  int32_t *list;               // per warp slot, ballmax entries
+  int ballmax;
+  int smem_ball;               // 1: hash + list in shared memory (small balls), else the global slots
+  int2 *props;                 // [B][ballmax] (node, key)
+  int32_t *prop_cnt;           // [B]
+  unsigned long long *stats;   // [4] ball nodes [5] proposals
+};
+
 struct SearchArgs {
   int metric;                  // M_U8 / M_F32 / M_JAC (the kernel's template metric)
   StoreView st;                // the graph's points
@@ -83,33 +104,27 @@ struct SearchArgs {
   int swz;                     // 1: staged rows are swizzled 16-byte chunks (lane-form widths, nchunks % 8 == 0)
   int lane_eval;               // 1: one lane per staged row where the width allows
   int win_prefetch;            // 1: prefetch the rows of a window's possible starts
+  int e_smem;                  // 1: the E bitmap of a task lives in the warp's shared memory (e_bytes, 1 bit per
+                               // pool node; X stays in the global words) -- the latency-bound plans
+  int e_bytes;                 // bytes of one bitmap (16-byte multiple)
+  int x_smem;                  // (e_smem) 1: the X bitmap too (after E); KT launches always
+  int ns2;                     // 1 (with e_smem): two chunk stages, chunk c + 1's rows in flight while c is processed
+  int row_pf;                  // 1: a walk step copies the rows of all of cur's neighbours with their vectors
+                               // (0: the chosen neighbour's row is loaded once the move is known)
   int full_scan;               // 1: the GNNS baseline walk (all k neighbours, move to the best)
   const int32_t *route;        // routed search (reading Q18's variant): partition of query b, else null
+  // B = 1 fused launch (one task): after the search, the same warp runs the update of the insert
+  // (update_one_warp with ub, C = out_ids / out_keys) and writes stats[0..5] itself
+  int fuse;
+  BallArgs ub;
+  int kt;                      // (fuse) 1: the keys against all n_t pool nodes precomputed into shared memory
 };
 size_t search_smem_bytes(const SearchArgs &a, bool sets);
 // warps of one K1 launch that can be resident at once (sizes the per-warp E / X planes)
 cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t *warps);
+// K1 computes keys one lane per staged row for this width (the compile-time lane-form kernels)
+bool search_lane_form(const VecGeom &g, int lane_eval);
 
-struct BallArgs {
-  StoreView st;
-  int32_t *ids;                // rows (snapshot until the merge)
-  uint32_t *keys;
-  int k;
-  int64_t n_t;
-  int64_t B;
-  int depth;
-  const int32_t *C;            // search results [B][k] (all B queries of the batch)
-  int64_t q0;                  // this launch handles queries q0 .. q0+nqb-1 (props index is local)
-  int64_t nqb;
-  int32_t *hash;               // per warp slot, hcap entries
-  int hcap;
-  int32_t *list;               // per warp slot, ballmax entries
-  int ballmax;
-  int smem_ball;               // 1: hash + list in shared memory (small balls), else the global slots
-  int2 *props;                 // [B][ballmax] (node, key)
-  int32_t *prop_cnt;           // [B]
-  unsigned long long *stats;   // [4] ball nodes [5] proposals
-};
 
 // Launchers (return cudaError_t of the launch)
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch);

@@ -30,6 +30,7 @@
 
 #include "knng_common.cuh"
 #include "knng_internal.h"
+#include "knng_update_one.cuh"
 
 // Cycle counters (builds with -DKNNG_PROFILE_COUNTERS, KNNG_PROFILE=1 at run time): summed per task into
 // SearchArgs::prof[0..12] = task, -, walks, -, -, windows, walk steps, -, fast chunks, chunks, walk
@@ -134,50 +135,104 @@ __device__ __forceinline__ uint32_t staged_keys(const typename QuerySel<M, L, CP
   }
 }
 
+// shared memory of the fused B = 1 update (after the warps' regions): s_n, hash / list / props, query tokens
+__host__ __device__ __forceinline__ size_t fuse_bytes(const SearchArgs &a, bool sets) {
+  return a.fuse ? ((16 + update_one_smem(a.ub.hcap, a.ub.ballmax) + (sets ? QMAX * 4 : 0) + 15) & ~(size_t)15) : 0;
+}
+
+// Rows of a lane-form width (NCK 16-byte chunks, compile time) gathered into stage slots: lane r
+// holds the node id of slot r (-1: none), rows r < nrows.  LPR lanes share a row so that every copy
+// instruction reads whole 128-byte segments; rows with NCK % 8 == 0 are stored swizzled (swz_pos).
+template <int NCK>
+__device__ __forceinline__ void gather_lf(unsigned sb, int pitch, const uint8_t *base, int32_t myid, int nrows) {
+  constexpr int LPR = NCK < 8 ? NCK : 8;   // lanes per row
+  constexpr int RPI = 32 / LPR;            // rows per pass
+  constexpr int CPR = NCK / LPR;           // copies per lane and row
+  constexpr bool SWZ = NCK % 8 == 0;
+  const int lane = threadIdx.x & 31, sl = lane % LPR, rr = lane / LPR;
+#pragma unroll
+  for (int pp = 0; pp < 32 / RPI; ++pp) {
+    if (pp * RPI >= nrows) break;   // warp-uniform
+    const int r = pp * RPI + rr;
+    const int32_t id = __shfl_sync(FULL, myid, r);
+    if (r < nrows && id >= 0) {
+      const uint8_t *src = base + (size_t)(uint32_t)id * (NCK * 16) + 16 * sl;
+      const unsigned dst = sb + r * pitch;
+#pragma unroll
+      for (int j = 0; j < CPR; ++j) {
+        const int t = sl + LPR * j;
+        cpa16(dst + 16 * (SWZ ? ((t & ~7) | ((t ^ r) & 7)) : t), src + 16 * LPR * j);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
-// K1: MB = minimum CTAs per SM of the launch bounds (WPC warps each): 5 -> <= 96 registers.
+// K1: MB = minimum CTAs per SM of the launch bounds (WPC warps each).  NCK > 0: a lane-form width
+// (u8 d = 32 / 128, f32 d = 96) with its geometry known at compile time; PART = 1 / 0: partitioned /
+// unpartitioned graph (-1: read from the arguments).
 // ---------------------------------------------------------------------------------------------
-template <int M, int L, int CPL, int MB>
+template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
 __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k = a.k;
-  // ---- this warp's shared memory (a.wbytes each) ----
+  constexpr bool LF = NCK > 0;                                             // one lane per staged row
+  constexpr bool SWZ = LF && NCK % 8 == 0;
+  const bool part = PART < 0 ? a.P > 0 : PART == 1;
+  const int nck = M == M_JAC ? 0 : (LF ? NCK : a.st.nchunks);
+  const int pitch = LF ? (SWZ ? NCK * 16 : NCK * 16 + 16) : a.pitch;
+  const int EB = part ? 8 : 4;                                             // bytes of a walked row entry
+  const int RB = EB * k;                                                   // bytes of a walked row
+  const bool row_pf = KT == 0 && a.row_pf != 0;                           // (KT: rows are loaded, keys looked up)
+  const bool es = KT || a.e_smem != 0;                                     // E bitmap in shared memory
+  const bool ns2 = !KT && M != M_JAC && es && a.ns2 != 0;                  // two chunk stages (needs es)
+  const bool xs = es && (KT || a.x_smem != 0);                             // X bitmap in shared memory too
+  // ---- this warp's shared memory (a.wbytes each; search_warp_bytes) ----
   uint8_t *wsm = smem + (size_t)warp * a.wbytes;
   uint8_t *stage = wsm;                                                   // [32][pitch] draw rows / set slots
-  const int RB = (a.P > 0 ? 8 : 4) * k;                                   // bytes of a walked row
-  const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4), NU = RB / CU;
-  const bool lform = M != M_JAC && lane_eval_ok(M, a.st.nchunks) && a.lane_eval;
-  const bool swz = a.swz != 0;                                             // staged rows swizzled (lform, nck % 8 == 0)
   uint8_t *wvec = stage;                                                   // [k][pitch] the walk's neighbour vectors
-  uint8_t *rowbuf = stage + 32 * a.pitch;                                  // [k] rows of cur's neighbours
-  uint8_t *wrow = rowbuf + ((k * RB + 15) & ~15);                          // [WPF] rows of possible starts
+  uint8_t *rowbuf = stage + (ns2 ? 64 : 32) * pitch;                       // [k] rows of cur's neighbours (row_pf)
+  uint8_t *wrow = rowbuf + (row_pf ? ((k * RB + 15) & ~15) : 0);           // [WPF] rows of possible starts
   uint8_t *qsm = wrow + ((WPF * RB + 15) & ~15);                           // [512 B] query (vectors)
   uint32_t *pkey = (uint32_t *)(qsm + 512);                                // [32] pending walk evaluations
   int32_t *pid = (int32_t *)(pkey + 32);                                   // [32]
   uint32_t *qscr = (uint32_t *)(pid + 32);                                 // [QMAX] query tokens (sets)
+  uint32_t *ebits = qscr + (M == M_JAC ? QMAX : 0);                        // [e_bytes / 4] E bitmap (es)
   long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
-  const int nck = M == M_JAC ? 0 : a.st.nchunks;
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   const int64_t gw = (int64_t)blockIdx.x * WPC + warp;                      // warp slot
   uint32_t *planes = a.gbits + gw * a.de_words;                            // E / X words of the task
   unsigned long long s_evals = 0, s_starts = 0, s_skip = 0, s_exp = 0;
-  const uint8_t *rsrc = a.P > 0 ? (const uint8_t *)a.lrows : (const uint8_t *)a.rows;
   int64_t task = gw;
+  // KT (the fused B = 1 launch on a small graph): the keys of the query against every pool node are
+  // computed up front by the whole CTA into a shared table; the search and the update then read keys
+  // from it instead of gathering rows (same keys, same decisions, same counters).
+  uint32_t *kt = nullptr;
+  if constexpr (KT != 0) {
+    kt = (uint32_t *)(smem + (size_t)WPC * a.wbytes + 8 * WPC + fuse_bytes(a, M == M_JAC));
+    const int64_t m0 = a.n_t;
+    for (int64_t v = threadIdx.x; v < m0; v += blockDim.x) kt[v] = pair_key<M>(a.qs, a.qrow0, v);
+    __syncthreads();
+  }
 
   while (task < T) {
     const int64_t b = task / Pn;
     const int pl = (int)(task % Pn);          // output slot
     const int p = a.route ? a.route[b] : a.part_lo + pl;   // partition searched
-    const int64_t m = a.P > 0 ? a.member_cnt[p] : a.n_t;
-    const int32_t *pool = a.P > 0 ? a.members + (size_t)p * a.member_cap : nullptr;
+    const int64_t m = part ? a.member_cnt[p] : a.n_t;
+    const int32_t *pool = part ? a.members + (size_t)p * a.member_cap : nullptr;
     // next task (dynamic scheduling), read back at the end of this one
     if (lane == 0) sched[warp] = (long long)(gridDim.x * WPC + atomicAdd(a.task_ctr, 1ull));
     KPROF(const long long tc0 = clock64(); long long c_walk = 0; unsigned long long c_win = 0, c_steps = 0,
-          c_fast = 0, c_chunks = 0; long long c_ph[3] = {0, 0, 0};)
+          c_fast = 0, c_chunks = 0; long long c_ph[6] = {0, 0, 0, 0, 0, 0};)
     // clear the task's E / X planes
-    {
+    if (es) {   // E (and X) bitmaps in shared memory
+      uint4 *e4 = (uint4 *)ebits;
+      for (int w = lane; w < (a.e_bytes >> (xs ? 3 : 4)); w += 32) e4[w] = make_uint4(0, 0, 0, 0);
+    }
+    if (!xs) {
       const int64_t nw = (m + 15) >> 4;
       uint4 *p4 = (uint4 *)planes;
       for (int64_t w = lane; w < (nw >> 2); w += 32) p4[w] = make_uint4(0, 0, 0, 0);
@@ -190,8 +245,8 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     if (budget > m) budget = m;
 
     typename QuerySel<M, L, CPL>::T Q;
-    Q.load(a.qs, a.qrow0 + b, M == M_JAC ? qscr : nullptr);
-    if (lform) {
+    if (!LF) Q.load(a.qs, a.qrow0 + b, M == M_JAC ? qscr : nullptr);
+    if (LF) {
       const uint8_t *qg = a.qs.vec + (size_t)(a.qrow0 + b) * a.qs.stride;
       for (int cc = lane; cc < nck; cc += 32) *(uint4 *)(qsm + 16 * cc) = ldg16(qg + 16 * cc);
     }
@@ -219,58 +274,83 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         return make_int2(nd, nd);
       }
       const uint64_t idx = rng_index(h3, (uint64_t)j, (uint64_t)m);
-      return make_int2((int32_t)idx, pool ? pool[idx] : (int32_t)idx);
+      return make_int2((int32_t)idx, pool ? __ldg(pool + idx) : (int32_t)idx);
     };
     // ---- the draw of a chunk: issue(d) copies the drawn rows into the stage (sets: each lane its token
-    // range) and returns the E word of each draw, read in the same round trip; the next chunk's pool
-    // loads (sets: their offsets, one chunk later) ride along.
+    // range) and returns the E word of each draw, read in the same round trip.
     const unsigned sb0 = smem_u32(stage);
     auto issue = [&](int2 d, uint64_t tb, uint64_t te) -> uint32_t {
-      if constexpr (M == M_JAC) {
+      if constexpr (KT != 0) {
+        return 0u;
+      } else if constexpr (M == M_JAC) {
         const uint64_t a0 = tb & ~3ull;
         const int nch = d.x >= 0 ? ((int)(te - a0) + 3) >> 2 : 0;
         if (nch <= SetQuery<L>::SLOTCH)
-          for (int jj = 0; jj < nch; ++jj) cpa16(sb0 + lane * a.pitch + 16 * jj, a.st.tok + a0 + 4 * jj);
+          for (int jj = 0; jj < nch; ++jj) cpa16(sb0 + lane * pitch + 16 * jj, a.st.tok + a0 + 4 * jj);
+      } else if constexpr (LF) {
+        gather_lf<NCK>(sb0, pitch, a.st.vec, d.y, 32);
       } else {
-        // 8 lanes per 128-byte row segment (coalesced): lane l copies chunks (l % 8) + 8 t of rows l / 8 + 4 p;
-        // the 8 row ids are fetched first, then the copies go out back to back
         const uint8_t *base = a.st.vec;
         const size_t stride = a.st.stride;
-        if (nck % 8 == 0) {
-          const int sl = lane & 7, rr = lane >> 3;
-          int32_t ids[8];
-#pragma unroll
-          for (int pp = 0; pp < 8; ++pp) ids[pp] = __shfl_sync(FULL, d.y, pp * 4 + rr);
-#pragma unroll
-          for (int pp = 0; pp < 8; ++pp) {
-            const int r = pp * 4 + rr;
-            if (ids[pp] >= 0) {
-              const uint8_t *src = base + (size_t)ids[pp] * stride + 16 * sl;
-              const unsigned dst = sb0 + r * a.pitch;
-              for (int t = sl; t < nck; t += 8) cpa16(dst + 16 * swz_pos(t, r, swz), src + 16 * (t - sl));
-            }
-          }
+        for (int e = lane; e < 32 * nck; e += 32) {
+          const int r = e / nck, t = e - r * nck;
+          const int32_t id = __shfl_sync(FULL, d.y, r);
+          if (id >= 0) cpa16(sb0 + r * pitch + 16 * t, base + (size_t)id * stride + 16 * t);
+        }
+      }
+      return (!es && d.x >= 0) ? g_ld(planes + pw(d.x)) : 0u;
+    };
+    // the E bit of pool node i: set / test (shared bitmap, or the low halves of the global words)
+    auto e_set = [&](int32_t i) {
+      if (es) atomicOr(ebits + (i >> 5), 1u << (i & 31));
+      else g_red_or(planes + pw(i), e_bit(i));
+    };
+    auto e_smem_test = [&](int32_t i) -> bool { return ((ebits[i >> 5] >> (i & 31)) & 1u) != 0; };
+    uint32_t *xbits = ebits + (a.e_bytes >> 2);  // xs: the X bitmap follows the E bitmap
+    auto issue_to = [&](uint8_t *dst, int2 d) {
+      if constexpr (M != M_JAC && KT == 0) {
+        if constexpr (LF) {
+          gather_lf<NCK>(smem_u32(dst), pitch, a.st.vec, d.y, 32);
         } else {
+          const unsigned sb = smem_u32(dst);
           for (int e = lane; e < 32 * nck; e += 32) {
             const int r = e / nck, t = e - r * nck;
             const int32_t id = __shfl_sync(FULL, d.y, r);
-            if (id >= 0) cpa16(sb0 + r * a.pitch + 16 * t, base + (size_t)id * stride + 16 * t);
+            if (id >= 0) cpa16(sb + r * pitch + 16 * t, a.st.vec + (size_t)id * a.st.stride + 16 * t);
           }
         }
       }
-      return d.x >= 0 ? g_ld(planes + pw(d.x)) : 0u;
     };
     auto offs = [&](int2 d, uint64_t &tb, uint64_t &te) {
       tb = te = 0;
       if (M == M_JAC && d.x >= 0) { tb = a.st.off[d.y]; te = a.st.off[d.y + 1]; }
     };
+    // keys of staged rows (lane r: slot r; lanes >= nrows read slot 0 and are masked by the callers)
+    auto keys_of = [&](const uint8_t *stg, int nrows) -> uint32_t {
+      if constexpr (M == M_JAC) {
+        return 0u;
+      } else if constexpr (LF) {
+        const int r = lane < nrows ? lane : 0;
+        return lane_key<M, NCK>(qsm, stg + r * pitch, r, SWZ);
+      } else {
+        return Q.eval_smem(stg, pitch, nck);
+      }
+    };
     // next chunk's draws dnx (pool loaded; sets: offsets bnx / enx in flight) and dnx2 (pool loads in flight)
     int2 dnx = make_int2(-1, -1), dnx2 = make_int2(-1, -1);
     uint64_t bnx = 0, enx = 0;
+    int2 infl = make_int2(-1, -1);               // ns2: the chunk whose rows are in flight
     if (budget > 0) {
       dnx = draw(0);
       if (M == M_JAC) offs(dnx, bnx, enx);
       dnx2 = draw(1);
+      if (ns2) {   // prologue: chunk 0 goes out now, chunk 1 at the start of chunk 0
+        issue(dnx, 0, 0);
+        cp_async_commit();
+        infl = dnx;
+        dnx = dnx2;
+        dnx2 = draw(2);
+      }
     }
     // the window: the current chunk, lanes >= wpos not yet processed
     int32_t wl = -1, wnode = -1;
@@ -283,34 +363,53 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     while (!stop && c < budget) {
       // ------------------------------ restart ------------------------------
       if (wpos >= 32) {
-        wl = dnx.x;
-        wnode = dnx.y;
+        KPROF(const long long tq0 = clock64();)
         const uint64_t cb = bnx, ce = enx;
-        const uint32_t ew = issue(dnx, cb, ce);
-        // the next chunk's pool loads were issued a chunk ago (sets: its offsets now); the one after
-        // next starts its pool loads
-        dnx = dnx2;
-        if (M == M_JAC) offs(dnx, bnx, enx);
-        dnx2 = draw(ch + 2);
-        cp_async_wait_all();
+        uint32_t ew = 0;
+        const uint8_t *cst = stage;              // this chunk's staged rows
+        if (ns2) {
+          // chunk ch's rows were issued a chunk ago into stage (ch & 1); chunk ch + 1 goes out now
+          wl = infl.x;
+          wnode = infl.y;
+          cst = stage + (ch & 1) * 32 * pitch;
+          issue_to(stage + ((ch + 1) & 1) * 32 * pitch, dnx);
+          cp_async_commit();
+          infl = dnx;
+          dnx = dnx2;
+          dnx2 = draw(ch + 3);
+          cp_async_wait<1>();
+        } else {
+          wl = dnx.x;
+          wnode = dnx.y;
+          ew = issue(dnx, cb, ce);
+          // the next chunk's pool loads were issued a chunk ago (sets: its offsets now); the one after
+          // next starts its pool loads
+          dnx = dnx2;
+          if (M == M_JAC) offs(dnx, bnx, enx);
+          dnx2 = draw(ch + 2);
+          cp_async_wait_all();
+        }
         __syncwarp();
+        wvec = (uint8_t *)cst;
         const bool ok = wl >= 0;
-        if constexpr (M == M_JAC) {
+        if constexpr (KT != 0) {
+          wkey = ok ? kt[wl] : 0u;
+        } else if constexpr (M == M_JAC) {
           wkey = 0;
           if (ok) {
             const uint64_t a0 = cb & ~3ull;
             const int rb = (int)(cb - a0), re = (int)(ce - a0);
-            if (((re + 3) >> 2) <= SetQuery<L>::SLOTCH) wkey = Q.eval_slot(stage + lane * a.pitch, rb, re);
+            if (((re + 3) >> 2) <= SetQuery<L>::SLOTCH) wkey = Q.eval_slot(stage + lane * pitch, rb, re);
             else wkey = Q.eval_slot_global(a.st.tok + a0, rb, re);
           }
         } else {
-          wkey = staged_keys<M, L, CPL>(Q, qsm, stage, a.pitch, nck, 32, lform, swz);
+          wkey = keys_of(cst, 32);
         }
-        KPROF(++c_chunks;)
+        KPROF(++c_chunks; const long long tq1 = clock64(); c_ph[3] += tq1 - tq0;)
         ++ch;
         const unsigned grp = __match_any_sync(FULL, wl);
         wfr0 = ok && !(grp & lanemask_lt());
-        wev = (ew & e_bit(wl)) != 0;
+        wev = es ? (ok && e_smem_test(wl)) : (ew & e_bit(wl)) != 0;
         wpos = 0;
         wslot = -1;
         // ---- fast path: no fresh draw of the chunk can be accepted against the current s_max: every
@@ -321,7 +420,8 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         const unsigned inv = __ballot_sync(FULL, !ok);
         thr_update();
         if (top.cnt > 0 && inv == 0 && c + __popc(fm) <= budget && !__any_sync(FULL, fr && !thr.skip(wkey))) {
-          if (fr) g_red_or(planes + pw(wl), e_bit(wl));
+          KPROF(const long long tq2 = clock64(); c_ph[4] += tq2 - tq1;)
+          if (fr) e_set(wl);
           top.insert(fr, wkey, wnode);             // Q5: skipped starts enter the top-k
           const int nf = __popc(fm);
           c += nf;
@@ -330,6 +430,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           wpos = 32;
           KPROF(++c_fast;)
           __syncwarp();
+          KPROF(c_ph[5] += clock64() - tq2;)
           continue;
         }
         KPROF(++c_win;)
@@ -341,8 +442,9 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           const int r = __popc(cmk & lanemask_lt());
           if (cand && r < WPF) {
             wslot = r;
-            const uint8_t *src = rsrc + (size_t)wnode * RB;
-            for (int u = 0; u < NU; ++u) cpa_n(smem_u32(wrow) + r * RB + u * CU, src + u * CU, CU);
+            const uint8_t *src = (part ? (const uint8_t *)a.lrows : (const uint8_t *)a.rows) + (size_t)wnode * RB;
+            const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4);
+            for (int u = 0; u < RB; u += CU) cpa_n(smem_u32(wrow) + r * RB + u, src + u, CU);
           }
         }
       }
@@ -392,7 +494,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       const int al = am ? __ffs(am) - 1 : -1;
       const unsigned commit = am ? (cm & (al == 31 ? FULL : ((2u << al) - 1u))) : cm;
       const bool cmt = (commit >> lane) & 1u;
-      if (cmt) g_red_or(planes + pw(wl), e_bit(wl));
+      if (cmt) e_set(wl);
       top.insert(cmt, wkey, wnode);          // Q5: skipped starts enter the top-k too
       const int ncm = __popc(commit);
       c += ncm;
@@ -410,14 +512,17 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       wpos = al + 1;
 
       // ------------------- hill climbing, eager first improvement -------------------
-      // One memory round trip per step: the rows, vectors (lane-form widths) and E / X words of cur's
-      // in-pool neighbours are copied together; the next step reads the chosen neighbour's row from
-      // rowbuf.  The walk's evaluations reach the top-k in batches (pbuf, flushed at the walk's end).
+      // One memory round trip per step: the vectors (lane-form widths) and E / X words of cur's in-pool
+      // neighbours are copied together (row_pf: with their rows, so the next step's row is in shared
+      // memory; else the chosen neighbour's row is loaded into registers as soon as the move is known).
+      // The walk's evaluations reach the top-k in batches (pbuf, flushed at the walk's end).
       int32_t cur = __shfl_sync(FULL, wnode, al);
       uint32_t kcur = __shfl_sync(FULL, wkey, al);
       int32_t curl = __shfl_sync(FULL, wl, al);
-      int rs = -1;                               // cur's row in rowbuf slot rs, or wrow slot rw, or global
-      int rw = __shfl_sync(FULL, wslot, al);
+      int rs = -1;                               // cur's row in rowbuf slot rs (row_pf)
+      int rw = __shfl_sync(FULL, wslot, al);     // ... or in window slot rw
+      bool have_nr = false;                      // ... or in nr (loaded after the move)
+      int2 nr = make_int2(-1, -1);
       int pn = 0;
       auto flush = [&]() {
         if (pn == 0) return;
@@ -435,56 +540,71 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       for (;;) {
         KPROF(++c_steps; long long ts0 = clock64();)
         ++s_exp;
-        if (lane == 0) g_red_or(planes + pw(curl), x_bit(curl));   // cur is expanded (Q9 bookkeeping)
+        if (lane == 0) {                         // cur is expanded (Q9 bookkeeping)
+          if (xs) atomicOr(xbits + (curl >> 5), 1u << (curl & 31));
+          else g_red_or(planes + pw(curl), x_bit(curl));
+        }
         int32_t v = -1, vl = -1;
         if (lane < k) {
-          if (a.P > 0) {
-            const int2 e2 = rs >= 0 ? ((const int2 *)(rowbuf + rs * RB))[lane]
-                                    : (rw >= 0 ? ((const int2 *)(wrow + rw * RB))[lane] : a.lrows[(size_t)cur * k + lane]);
-            v = e2.x;
-            vl = e2.y;
+          int2 e2;
+          if (rw >= 0) {
+            e2 = part ? ((const int2 *)(wrow + rw * RB))[lane] : make_int2(((const int32_t *)(wrow + rw * RB))[lane], 0);
+          } else if (rs >= 0) {
+            e2 = part ? ((const int2 *)(rowbuf + rs * RB))[lane] : make_int2(((const int32_t *)(rowbuf + rs * RB))[lane], 0);
+          } else if (have_nr) {
+            e2 = nr;
           } else {
-            v = rs >= 0 ? ((const int32_t *)(rowbuf + rs * RB))[lane]
-                        : (rw >= 0 ? ((const int32_t *)(wrow + rw * RB))[lane] : a.rows[(size_t)cur * k + lane]);
+            e2 = part ? __ldg(a.lrows + (size_t)cur * k + lane) : make_int2(__ldg(a.rows + (size_t)cur * k + lane), 0);
           }
+          v = e2.x;
+          vl = part ? e2.y : e2.x;
         }
         rw = -1;
         // Q10: neighbours in another partition are skipped (lrows holds -1 for them)
-        const bool inpool = v >= 0 && (a.P == 0 || vl >= 0);
-        const int32_t lv = inpool ? (a.P > 0 ? vl : v) : 0;
+        const bool inpool = v >= 0 && vl >= 0;
+        const int32_t lv = inpool ? vl : 0;
         __syncwarp();                            // rowbuf read before the copies below overwrite it
         KPROF(long long ts1 = clock64(); c_ph[0] += ts1 - ts0;)
-        // issue: rows (NU copies of CU bytes) and, for the lane-form widths, vectors (nck x 16 bytes) of
-        // the in-pool neighbours, and their E / X words
-        // lane l serves neighbour t = l % 16 (t + 16 for k > 16), copying its units l / 16, l / 16 + 2, ...
-        {
-          const int per = NU + (lform ? nck : 0);
-          const unsigned rb0 = smem_u32(rowbuf), wv0 = smem_u32(wvec);
+        // issue: the vectors (lane-form widths), rows (row_pf) and E / X words of the in-pool neighbours
+        if constexpr (KT != 0) {
+          // keys from the table
+        } else if constexpr (LF) {
+          gather_lf<NCK>(smem_u32(wvec), pitch, a.st.vec, inpool ? v : -1, k);
+          if (row_pf) {
+            const unsigned rb0 = smem_u32(rowbuf);
+            const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4), NU = RB / CU;
+            const uint8_t *rsrc = part ? (const uint8_t *)a.lrows : (const uint8_t *)a.rows;
+            for (int e0 = 0; e0 < k * NU; e0 += 32) {
+              const int e = e0 + lane, t = e / NU, u = e - t * NU;
+              const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t & 31);
+              if (e < k * NU && vt >= 0) cpa_n(rb0 + t * RB + u * CU, rsrc + (size_t)vt * RB + u * CU, CU);
+            }
+          }
+        } else if (row_pf) {
+          const unsigned rb0 = smem_u32(rowbuf);
+          const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4), NU = RB / CU;
+          const uint8_t *rsrc = part ? (const uint8_t *)a.lrows : (const uint8_t *)a.rows;
           for (int t0 = 0; t0 < k; t0 += 16) {
             const int t = t0 + (lane & 15);
             const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t & 31);
-            if (t < k && vt >= 0) {
-              const uint8_t *rsv = rsrc + (size_t)vt * RB;
-              const uint8_t *vsv = a.st.vec + (size_t)vt * a.st.stride;
-              for (int u = lane >> 4; u < per; u += 2) {
-                if (u < NU) cpa_n(rb0 + t * RB + u * CU, rsv + u * CU, CU);
-                else cpa16(wv0 + t * a.pitch + 16 * swz_pos(u - NU, t, swz), vsv + (u - NU) * 16);
-              }
-            }
+            if (t < k && vt >= 0)
+              for (int u = lane >> 4; u < NU; u += 2) cpa_n(rb0 + t * RB + u * CU, rsrc + (size_t)vt * RB + u * CU, CU);
           }
         }
-        const uint32_t xw = inpool ? g_ld(planes + pw(lv)) : 0u;
+        const uint32_t xw = (inpool && !xs) ? g_ld(planes + pw(lv)) : 0u;
         uint32_t key;
-        if (lform) {
+        if constexpr (KT != 0) {
+          key = inpool ? kt[lv] : 0u;
+        } else if constexpr (LF) {
           cp_async_wait_all();
           __syncwarp();
-          key = staged_keys<M, L, CPL>(Q, qsm, wvec, a.pitch, nck, k, true, swz);
+          key = keys_of(wvec, k);
         } else {
           key = Q.eval(a.st, inpool ? v : -1, k);
           cp_async_wait_all();
           __syncwarp();
         }
-        const bool evb2 = !inpool || (xw & e_bit(lv));
+        const bool evb2 = !inpool || (es ? e_smem_test(lv) : (xw & e_bit(lv)) != 0);
         const bool imp = inpool && closer<M>(key, kcur);
         KPROF(long long ts2 = clock64(); c_ph[1] += ts2 - ts1;)
         const unsigned im = __ballot_sync(FULL, imp);
@@ -507,12 +627,17 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           }
           fi = im ? bl : 31;
         }
+        const bool mv_x = __shfl_sync(FULL, xs ? (inpool && ((xbits[lv >> 5] >> (lv & 31)) & 1u)) : (xw & x_bit(lv)) != 0, fi);
+        // the move (if any) is known: its row is loaded now, under the bookkeeping below
+        const int32_t ncur = __shfl_sync(FULL, v, fi);
+        if (!row_pf && im && !mv_x && lane < k)
+          nr = part ? __ldg(a.lrows + (size_t)ncur * k + lane) : make_int2(__ldg(a.rows + (size_t)ncur * k + lane), 0);
         unsigned fm2 = __ballot_sync(FULL, !evb2) & range;
         bool hit2 = false;
         if ((int64_t)__popc(fm2) > budget - c) { fm2 = first_bits(fm2, (int)(budget - c)); hit2 = true; }
         const bool cm2 = (fm2 >> lane) & 1u;
         const int nf2 = __popc(fm2);
-        if (cm2) g_red_or(planes + pw(lv), e_bit(lv));
+        if (cm2) e_set(lv);
         if (pn + nf2 > 32) flush();
         if (cm2) {
           const int q = pn + __popc(fm2 & lanemask_lt());
@@ -525,11 +650,12 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         KPROF(long long ts3 = clock64(); c_ph[2] += ts3 - ts2;)
         if (hit2) { stop = true; break; }    // the over-budget evaluation is not performed
         if (!im) break;                      // local maximum -> restart
-        cur = __shfl_sync(FULL, v, fi);
+        if (mv_x) break;                     // Q9: moving onto an expanded node restarts
+        cur = ncur;
         kcur = __shfl_sync(FULL, key, fi);
         curl = __shfl_sync(FULL, lv, fi);
-        rs = fi;
-        if (__shfl_sync(FULL, (xw & x_bit(lv)) != 0, fi)) break;   // Q9: moving onto an expanded node restarts
+        if (row_pf) rs = fi;
+        else have_nr = true;
       }
       flush();
       KPROF(c_walk += clock64() - tk0;)
@@ -537,21 +663,25 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       if (!stop && wpos < 32) {
         const bool need = lane >= wpos && wfr0 && !wev;
         if (__any_sync(FULL, need)) {
-          const uint32_t ew = need ? g_ld(planes + pw(wl)) : 0u;
-          if (need) wev = (ew & e_bit(wl)) != 0;
+          if (es) {
+            if (need) wev = e_smem_test(wl);
+          } else {
+            const uint32_t ew = need ? g_ld(planes + pw(wl)) : 0u;
+            if (need) wev = (ew & e_bit(wl)) != 0;
+          }
         }
       }
     }
     KPROF(if (a.prof && lane == 0) {
-      atomicAdd(a.prof + 0, (unsigned long long)(clock64() - tc0));
-      atomicAdd(a.prof + 2, (unsigned long long)c_walk);
-      atomicAdd(a.prof + 5, c_win);
-      atomicAdd(a.prof + 6, c_steps);
-      atomicAdd(a.prof + 8, c_fast);
-      atomicAdd(a.prof + 9, c_chunks);
-      atomicAdd(a.prof + 10, (unsigned long long)c_ph[0]);
-      atomicAdd(a.prof + 11, (unsigned long long)c_ph[1]);
-      atomicAdd(a.prof + 12, (unsigned long long)c_ph[2]);
+      // (the fused B = 1 launch owns the counters: stores, so that no memset precedes it)
+      auto put = [&](int i, unsigned long long v) { if (a.fuse) a.prof[i] = v; else atomicAdd(a.prof + i, v); };
+      put(0, (unsigned long long)(clock64() - tc0));
+      put(2, (unsigned long long)c_walk);
+      put(5, c_win);
+      put(6, c_steps);
+      put(8, c_fast);
+      put(9, c_chunks);
+      for (int i = 0; i < 6; ++i) put(10 + i, (unsigned long long)c_ph[i]);
     })
     s_evals += c;
     if (lane < a.kr) {
@@ -563,6 +693,21 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     __syncwarp();
     task = *(volatile long long *)(sched + warp);
     __syncwarp();
+  }
+  if (a.fuse) {   // B = 1: one CTA, warp 0 ran the only task; it owns the stats and runs the update
+    if (gw == 0) {
+      if (lane == 0) {
+        a.stats[0] = s_evals;
+        a.stats[1] = s_starts;
+        a.stats[2] = s_skip;
+        a.stats[3] = s_exp;
+      }
+      uint8_t *us = smem + (size_t)WPC * a.wbytes + 8 * WPC;
+      int32_t *usm = (int32_t *)(us + 16);
+      uint32_t *uq = (uint32_t *)(us + 16 + update_one_smem(a.ub.hcap, a.ub.ballmax));
+      update_one_warp<M, L, CPL>(a.ub, a.out_ids, a.out_keys, usm, (int *)us, M == M_JAC ? uq : nullptr, true, kt);
+    }
+    return;
   }
   if (lane == 0) {
     atomicAdd(a.stats + 0, s_evals);
@@ -600,39 +745,62 @@ __global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq,
 // shared memory of one warp of K1 (the kernel's carve-up above)
 size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   const size_t RB = (size_t)(a.P > 0 ? 8 : 4) * a.k;
-  size_t b = (size_t)32 * a.pitch + ((a.k * RB + 15) & ~(size_t)15) + ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QMAX * 4 : 0);
+  const bool ns2 = !sets && a.e_smem && a.ns2;
+  size_t b = (size_t)(ns2 ? 64 : 32) * a.pitch + (a.row_pf ? ((a.k * RB + 15) & ~(size_t)15) : 0) +
+             ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QMAX * 4 : 0) +
+             (a.e_smem ? (size_t)a.e_bytes * ((a.x_smem || a.kt) ? 2 : 1) : 0);
   return (b + 15) & ~(size_t)15;
 }
-size_t search_smem_bytes(const SearchArgs &a, bool sets) { return WPC * search_warp_bytes(a, sets) + 8 * WPC; }
+size_t search_smem_bytes(const SearchArgs &a, bool sets) {
+  return WPC * search_warp_bytes(a, sets) + 8 * WPC + fuse_bytes(a, sets) + (a.kt ? ((a.n_t * 4 + 15) & ~15ll) : 0);
+}
 
 // occupancy of a K1 instantiation at a shared-memory size on the current device, cached (a B = 1 insert
 // launches K1 once per point: the attribute / occupancy queries would otherwise dominate its host time)
-template <int M, int L, int CPL, int MB>
+template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
 static cudaError_t k1_occupancy(size_t smem, int *per_sm, int *nsm) {
   static std::mutex mu;
   static std::map<std::pair<int, size_t>, std::pair<int, int>> cache;
+  static std::map<int, size_t> attr;   // per device: the opt-in shared memory size set so far (only grows, so
+                                       // that every cached size stays launchable)
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
+  static std::map<int, int> optin;
+  if (!optin.count(dev)) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    optin[dev] = v;
+  }
+  // a plan that does not fit is refused here, without an API error (cudaGetLastError would report a
+  // failed attribute call at the next launch)
+  if (smem > (size_t)optin[dev]) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024 && smem > attr[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB, NCK, PART, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return e;
+    }
+    attr[dev] = smem;
+  }
   auto it = cache.find({dev, smem});
   if (it != cache.end()) {
     *per_sm = it->second.first;
     *nsm = it->second.second;
     return cudaSuccess;
   }
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_search<M, L, CPL, MB, NCK, PART, KT>, 32 * WPC, smem);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
   }
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_search<M, L, CPL, MB>, 32 * WPC, smem);
-  if (e != cudaSuccess) return e;
   *nsm = 148;
   cudaDeviceGetAttribute(nsm, cudaDevAttrMultiProcessorCount, dev);
   cache[{dev, smem}] = {*per_sm, *nsm};
   return cudaSuccess;
 }
 
-template <int M, int L, int CPL, int MB>
+template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
 static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
@@ -641,7 +809,7 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   const size_t smem = search_smem_bytes(a, M == M_JAC);
   // persistent grid: the CTAs that fit at once (dynamic task scheduling balances the tail)
   int per_sm = 0, nsm = 148;
-  if (cudaError_t oe = k1_occupancy<M, L, CPL, MB>(smem, &per_sm, &nsm)) return oe;
+  if (cudaError_t oe = k1_occupancy<M, L, CPL, MB, NCK, PART, KT>(smem, &per_sm, &nsm)) return oe;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t blocks = std::min<int64_t>((T + WPC - 1) / WPC, (int64_t)per_sm * nsm);
   blocks = std::min<int64_t>(blocks, a.gslots / WPC);
@@ -653,7 +821,7 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   if (getenv("KNNG_PROFILE"))
     fprintf(stderr, "KNNG_PROFILE k_search: %lld CTAs x %d warps, %d CTAs per SM resident (%zu B smem each)\n",
             (long long)blocks, WPC, per_sm, smem);
-  k_search<M, L, CPL, MB><<<(unsigned)blocks, 32 * WPC, smem, s>>>(a);
+  k_search<M, L, CPL, MB, NCK, PART, KT><<<(unsigned)blocks, 32 * WPC, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -664,10 +832,33 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   X(M_F32, 1, 1) X(M_F32, 1, 2) X(M_F32, 1, 3) X(M_F32, 1, 4) X(M_F32, 2, 3) X(M_F32, 2, 4) X(M_F32, 4, 3) \
   X(M_F32, 4, 4) X(M_F32, 8, 3) X(M_F32, 8, 4) X(M_F32, 32, 2) X(M_F32, 32, 4)
 
+// the lane-form widths with their geometry at compile time (search_lane_form)
+#define KNNG_LF_SHAPES(X) X(M_U8, 8, 1, 8) X(M_U8, 2, 1, 2) X(M_F32, 8, 3, 24)
+
+bool search_lane_form(const VecGeom &g, int lane_eval) {
+  return lane_eval && g.metric != M_JAC && lane_eval_ok(g.metric, g.nchunks);
+}
+
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch) {
   if (n_launch) ++*n_launch;
+  if (a.kt) {
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, KNNG_K1_MB>(a, s);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, KNNG_K1_MB, 0, 0, 1>(a, s);
+    KNNG_SHAPES(X, M_U8)
+    KNNG_SHAPES_F32(X)
+    X(M_JAC, 8, 1)
+#undef X
+    return cudaErrorInvalidValue;
+  }
+  if (search_lane_form(g, a.lane_eval)) {
+#define X(MM, LL, CC, NN) \
+  if (g.metric == MM && g.nchunks == NN) \
+    return a.P > 0 ? run_search<MM, LL, CC, KNNG_K1_MB, NN, 1, 0>(a, s) : run_search<MM, LL, CC, KNNG_K1_MB, NN, 0, 0>(a, s);
+    KNNG_LF_SHAPES(X)
+#undef X
+  }
+#define X(MM, LL, CC) \
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, KNNG_K1_MB, 0, -1, 0>(a, s);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
@@ -675,18 +866,34 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
   return cudaErrorInvalidValue;
 }
 
-template <int M, int L, int CPL, int MB>
+template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
 static cudaError_t resident(SearchArgs a, int64_t *warps) {
   const size_t smem = search_smem_bytes(a, M == M_JAC);
   int per_sm = 0, nsm = 148;
-  if (cudaError_t e = k1_occupancy<M, L, CPL, MB>(smem, &per_sm, &nsm)) return e;
+  if (cudaError_t e = k1_occupancy<M, L, CPL, MB, NCK, PART, KT>(smem, &per_sm, &nsm)) return e;
   *warps = (int64_t)per_sm * nsm * WPC;
   return cudaSuccess;
 }
 
 cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t *warps) {
+  if (a.kt) {
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, KNNG_K1_MB>(a, warps);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, KNNG_K1_MB, 0, 0, 1>(a, warps);
+    KNNG_SHAPES(X, M_U8)
+    KNNG_SHAPES_F32(X)
+    X(M_JAC, 8, 1)
+#undef X
+    return cudaErrorInvalidValue;
+  }
+  if (search_lane_form(g, a.lane_eval)) {
+#define X(MM, LL, CC, NN) \
+  if (g.metric == MM && g.nchunks == NN) \
+    return a.P > 0 ? resident<MM, LL, CC, KNNG_K1_MB, NN, 1, 0>(a, warps) : resident<MM, LL, CC, KNNG_K1_MB, NN, 0, 0>(a, warps);
+    KNNG_LF_SHAPES(X)
+#undef X
+  }
+#define X(MM, LL, CC) \
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, KNNG_K1_MB, 0, -1, 0>(a, warps);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)

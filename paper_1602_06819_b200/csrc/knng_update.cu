@@ -5,6 +5,7 @@
 //   K6 placement at the nearest medoid      (Alg. 5)
 #include "knng_common.cuh"
 #include "knng_internal.h"
+#include "knng_update_one.cuh"
 
 namespace knng {
 
@@ -60,16 +61,6 @@ cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, 
 // each level's nodes are evaluated 32 at a time with the warp evaluator; a node v proposes the
 // new point when (D, id_x) precedes row_v[k-1] (Q14).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool hash_insert(int32_t *h, int hcap, int32_t u) {
-  uint32_t x = (uint32_t)u * 0x9E3779B1u;
-  int pos = (int)(x >> 7) & (hcap - 1);
-  for (;;) {
-    const int32_t old = atomicCAS(h + pos, -1, u);
-    if (old == -1) return true;
-    if (old == u) return false;
-    pos = (pos + 1) & (hcap - 1);
-  }
-}
 
 template <int M, int L, int CPL>
 __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
@@ -155,82 +146,12 @@ __global__ void __launch_bounds__(32) k_update_one(BallArgs a, const uint32_t *C
   extern __shared__ int32_t usm[];
   __shared__ uint32_t qscr[M == M_JAC ? QMAX : 1];
   __shared__ int s_n;
-  const int lane = threadIdx.x;
-  const int k = a.k;
-  int32_t *hash = usm;
-  int32_t *list = hash + a.hcap;
-  int2 *props = (int2 *)(list + a.ballmax + (a.ballmax & 1));
-  const int32_t idx = (int32_t)a.n_t;            // the new point's id
-  // new row n_t = C (the top-k of the search; B = 1 has no batch peers)
-  if (lane < k) {
-    a.ids[(size_t)idx * k + lane] = a.C[lane];
-    a.keys[(size_t)idx * k + lane] = Ckeys[lane];
-  }
-  for (int i = lane; i < a.hcap; i += 32) hash[i] = -1;
-  if (lane == 0) s_n = 0;
-  __syncwarp();
-  typename QuerySel<M, L, CPL>::T Q;
-  Q.load(a.st, a.n_t, M == M_JAC ? qscr : nullptr);
-  {
-    const int32_t v = lane < k ? a.C[lane] : -1;
-    const bool ins = v >= 0 && hash_insert(hash, a.hcap, v);
-    const unsigned m = __ballot_sync(FULL, ins);
-    if (ins) list[__popc(m & lanemask_lt())] = v;
-    if (lane == 0) s_n = __popc(m);
-    __syncwarp();
-  }
-  // levels 1..DEPTH over the snapshot rows: collect the ball, evaluate, propose
-  int lo = 0, hi = s_n, np = 0;
-  for (int d = 1; d <= a.depth; ++d) {
-    for (int base = lo; base < hi; base += 32) {
-      const int t = base + lane;
-      const int32_t v = t < hi ? list[t] : -1;
-      if (d < a.depth && v >= 0) {
-        for (int e = 0; e < k; ++e) {
-          const int32_t u = a.ids[(size_t)v * k + e];
-          if (u >= 0 && u != idx && hash_insert(hash, a.hcap, u)) {
-            const int pos = atomicAdd(&s_n, 1);
-            if (pos < a.ballmax) list[pos] = u;
-          }
-        }
-      }
-      const int cnt = hi - base < 32 ? hi - base : 32;
-      const uint32_t key = Q.eval(a.st, v, cnt);
-      bool prop = false;
-      if (v >= 0) prop = precedes<M>(key, idx, a.keys[(size_t)v * k + k - 1], a.ids[(size_t)v * k + k - 1]);
-      const unsigned pm = __ballot_sync(FULL, prop);
-      if (prop) props[np + __popc(pm & lanemask_lt())] = make_int2(v, (int)key);
-      np += __popc(pm);
-    }
-    __syncwarp();
-    lo = hi;
-    hi = s_n < a.ballmax ? s_n : a.ballmax;
-    __syncwarp();
-  }
-  // apply (Q14): row_v = top-k(row_v u {(D, idx)}); one lane per proposal, distinct rows
-  for (int j = lane; j < np; j += 32) {
-    const int32_t v = props[j].x;
-    const uint32_t key = (uint32_t)props[j].y;
-    int32_t *ri = a.ids + (size_t)v * k;
-    uint32_t *rk = a.keys + (size_t)v * k;
-    int pos = k - 1;
-    while (pos > 0 && precedes<M>(key, idx, rk[pos - 1], ri[pos - 1])) {
-      rk[pos] = rk[pos - 1];
-      ri[pos] = ri[pos - 1];
-      --pos;
-    }
-    rk[pos] = key;
-    ri[pos] = idx;
-  }
-  if (lane == 0) {
-    atomicAdd(a.stats + 4, (unsigned long long)lo);
-    atomicAdd(a.stats + 5, (unsigned long long)np);
-  }
+  update_one_warp<M, L, CPL>(a, a.C, Ckeys, usm, &s_n, M == M_JAC ? qscr : nullptr, false);
 }
 
 template <int M, int L, int CPL>
 static cudaError_t run_update_one(const BallArgs &a, const uint32_t *Ckeys, cudaStream_t s) {
-  const size_t smem = (size_t)(a.hcap + a.ballmax + 1) * 4 + (size_t)a.ballmax * 8;
+  const size_t smem = update_one_smem(a.hcap, a.ballmax);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_update_one<M, L, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

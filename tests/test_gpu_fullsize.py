@@ -84,16 +84,36 @@ def _stream_vs_oracle(cfg, X, S, batches, part=False, what=""):
 # ---------------------------------------------------------------------------
 # Forced K1 paths
 # ---------------------------------------------------------------------------
+_K1_PATHS = {
+    # E bits in the per-slot global words, one chunk stage: the plan of C2/C3/C4 at full size
+    "global-E": {"KNNG_ESMEM": 0},
+    # E bitmap in shared memory + two chunk stages: the latency-bound plan (C0, C1, small batches)
+    "smem-E+2stages": {"KNNG_ESMEM": 1},
+    "smem-E+1stage": {"KNNG_ESMEM": 1, "KNNG_NS2": 0},
+    # walk steps that copy the rows of all neighbours with their vectors
+    "row-prefetch": {"KNNG_ROW_PF": 1, "KNNG_ESMEM": 0},
+    "row-prefetch+smem-E": {"KNNG_ROW_PF": 1, "KNNG_ESMEM": 1},
+    # the warp-form evaluator (generic widths) instead of one lane per row
+    "warp-form": {"KNNG_LANE_EVAL": 0},
+    "warp-form+smem-E": {"KNNG_LANE_EVAL": 0, "KNNG_ESMEM": 1},
+}
+
+
+@pytest.mark.parametrize("path", sorted(_K1_PATHS))
 @pytest.mark.parametrize("name,n0,part", [("C1", 12000, False), ("C2", 6000, False), ("C3", 16000, True),
-                                          ("C4", 3000, True), ("C4", 2500, False)])
-def test_global_evaluated_set_matches_oracle(env, name, n0, part):
-    """KNNG_SMEM_BITS=0: the evaluated set of every task in the per-slot global workspace -- the path
-    the plan takes for C2/C3/C4 at full size (pools of ~1M nodes)."""
-    env("KNNG_SMEM_BITS", 0)
+                                          ("C4", 2500, True)])
+def test_forced_k1_paths_match_oracle(env, path, name, n0, part):
+    """Every K1 launch-plan path on every metric, forced by its knobs (the plan picks one per launch
+    from the task count and pool size), equal to the oracle with all counters: B = 1,024 + a ragged
+    376-point tail."""
+    if name == "C4" and ("warp" in path or "2stages" in path):
+        pytest.skip("sets: one evaluator, one stage")
+    for k_, v in _K1_PATHS[path].items():
+        env(k_, v)
     cfg = D.CONFIGS[name].with_sizes(n0=n0, n_insert=1400)
     X = D.initial_points(cfg)
     S = D.stream_points(cfg, 0, cfg.n_insert)
-    _stream_vs_oracle(cfg, X, S, [1024, 376], part=part, what="global bitmap")
+    _stream_vs_oracle(cfg, X, S, [1024, 376], part=part, what=path)
 
 
 def _path_points(n, dim=8):
@@ -109,10 +129,12 @@ def _path_points(n, dim=8):
     return X
 
 
+@pytest.mark.parametrize("esmem", ["0", "1"])
 @pytest.mark.parametrize("k", [2, 4])
-def test_long_walk_expands_past_the_shared_hash(k):
-    """A walk of ~n expansions (the shared expanded-set hash holds 384 before it spills to global
-    memory): injected start at the far end, budget = pool (speedup 1)."""
+def test_long_walks_match_oracle(env, k, esmem):
+    """A walk of ~n expansions (one step per node along the path): injected start at the far end,
+    budget = pool (speedup 1); under every E-bit placement."""
+    env("KNNG_ESMEM", esmem)
     X = _path_points(1500)
     g = _graph(X, k, 1600)
     o = O.OracleGraph(O.U8, X, k, capacity=1600)
@@ -403,3 +425,18 @@ def test_recompute_medoids_and_routing_match_oracle(name, n0):
     _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "routed stream with medoid recomputation")
     gpart, _ = g.partition()
     assert (gpart == o.part_of[:o.n]).all()
+
+
+@pytest.mark.parametrize("nq", [64, 3000])
+def test_launch_plan_fallbacks_on_a_large_pool(nq):
+    """A 250k-node unpartitioned pool: the plan tries E + X bitmaps in shared memory (does not fit one
+    CTA), then E alone (fits for 64 tasks, not for 3,000), else the global words -- every attempt that is
+    refused must leave no error behind, and the search must equal the oracle's."""
+    cfg = D.CONFIGS["C1"].with_sizes(n0=250_000)
+    X = D.initial_points(cfg)
+    g, o = _gpu_init_checked(cfg, X, cfg.n0, 64)
+    Q = D.query_points(cfg, nq, seed_offset=3)
+    gi, gk, gst = g.search(Q, cfg.k, 64.0, cfg.e_num, cfg.e_den, 9)
+    oi, ok, ost = o.search(Q, cfg.k, 64.0, cfg.e_num, cfg.e_den, 9)
+    _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "plan fallback nq=%d" % nq)
+    assert gst["search_evals"] == ost[:, 0].sum() and gst["search_expansions"] == ost[:, 3].sum()

@@ -195,11 +195,15 @@ def test_insert_C0_sequential_batches_of_one():
     _run_stream(cfg, [1] * 60)
 
 
+@pytest.mark.parametrize("keytable", [True, False])
 @pytest.mark.parametrize("name,n0,depth,k", [("C2", 3000, 3, 20), ("C4", 1500, 2, 10), ("C1", 2500, 1, 1),
                                               ("C0", 400, 4, 32)])
-def test_insert_batches_of_one_fast_path(name, n0, depth, k, monkeypatch):
-    """B = 1 takes the fused one-warp update (insert_one); every metric, depths 1-4, k = 1..32: equal to
-    the oracle after every insert, and the batched path (KNNG_NO_B1) reaches the same graph."""
+def test_insert_batches_of_one_fast_path(name, n0, depth, k, keytable, monkeypatch):
+    """B = 1 takes the fused launch (search + the insert's update by one warp; on small graphs with the
+    key table); every metric, depths 1-4, k = 1..32: equal to the oracle after every insert, and the
+    batched path (KNNG_NO_B1) reaches the same graph."""
+    if not keytable:
+        monkeypatch.setenv("KNNG_NO_KT", "1")
     cfg = _cfg_small(name, n0=n0, n_insert=40)
     X = D.initial_points(cfg)
     S = D.stream_points(cfg, 0, cfg.n_insert)
