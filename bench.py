@@ -239,6 +239,11 @@ def run_ours(args, cfg):
     # the global batch is the config's batch at every N (strong scaling).  Unpartitioned configs shard
     # the queries of N batches (weak scaling).
     GB = cfg.batch if cfg.P else ws * cfg.batch
+    # B = 1 configs (the paper's sequential algorithm, C0): a step inserts SEQ points one after another
+    # (each a batch of one) through graph_insert_sequential -- one launch, no host round trip per point
+    SEQ = 32 if cfg.batch == 1 and ws == 1 and not cfg.P else 0
+    if SEQ:
+        GB = SEQ
     nsteps = args.warmup + args.steps
     X = D.initial_points(cfg)
     n_stream = 2 * nsteps * GB                      # device-input steps, then the e2e steps
@@ -259,6 +264,8 @@ def run_ours(args, cfg):
         """One global batch: graph_insert_batch.  On N GPUs the handle owns the library's NCCL
         communicator and the same call is the distributed insert (partitions or queries sharded over the
         ranks, all-gathers on the handle's stream); its counters are job totals."""
+        if SEQ:
+            return graph.insert_sequential(pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)[1]
         return graph.insert_batch(pts, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)[1]
 
     # ---------------- setup (untimed): exact initial graph (A0) + Alg. 4 partition (A9) ----------------
@@ -403,7 +410,10 @@ def run_ours(args, cfg):
         "metric": baseline_metric(), "value": value, "unit": "inserts/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * t_total / args.steps, "higher_is_better": True,
         "scaling": "strong" if cfg.P else "weak", "vs_baseline": None, "dtype": dtype_name(cfg), "data": "synthetic",
-        "config": {"workload": cfg_desc(cfg), "global_batch": GB, "setup_s": t_setup,
+        "config": {"workload": cfg_desc(cfg), "global_batch": cfg.batch if SEQ else GB, "setup_s": t_setup,
+                   "step": ("graph_insert_sequential of %d points: each a batch of one on the graph the previous "
+                            "one left (B = 1, the paper's sequential algorithm), all in one launch" % SEQ
+                            if SEQ else "graph_insert_batch of the global batch"),
                    "timed_inserts": "%d..%d of the %d-insert stream" % (args.warmup * GB, nsteps * GB, cfg.n_insert),
                    "parallelism": "1 GPU" if ws == 1 else (
                        "%d ranks: replicated graph, the P=%d partition searches of each batch sharded over the ranks "

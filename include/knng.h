@@ -158,6 +158,16 @@ int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_g
 int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p,
                        int64_t *first_id_out, knng_stats *st);
 
+/* graph_insert_sequential -- add n points ONE AFTER ANOTHER: point i is inserted as a batch of one
+ * on the graph that point i-1 left (the paper's sequential Alg. 1 + Alg. 2 per point, P:109-151,
+ * i.e. the online stream of Section 4), so the result equals n calls of graph_insert_batch with
+ * B = 1.  On an unpartitioned single-GPU handle the whole sequence runs in ONE launch (one warp
+ * searches and updates point after point; the graph stays on the device, no host round trip between
+ * points); otherwise the library loops over the points.  Ids n_t .. n_t+n-1 (*first_id_out = n_t);
+ * *st sums the counters of the n inserts.  Arguments, layout and errors as graph_insert_batch. */
+int graph_insert_sequential(knng_graph *g, const knng_points *pts, const knng_params *p,
+                            int64_t *first_id_out, knng_stats *st);
+
 /* graph_search -- iGNNS k_r-nn search of nq queries on the current graph (read-only; P:73-89,
  * Alg. 3 P:166-178 when partitioned).  Query i uses RNG stream (seed, i, partition).
  * ids_out int32[nq*kr], keys_out uint32[nq*kr], sorted by edge order; -1 / 0 pad when the pool

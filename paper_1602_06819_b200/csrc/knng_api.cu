@@ -217,7 +217,7 @@ static void free_graph(knng_graph *g) {
     if (b) cudaFree(b);
   DBuf *ws[] = {&g->w_bits, &g->w_cand_i, &g->w_cand_k, &g->w_C_i, &g->w_C_k, &g->w_hash, &g->w_list, &g->w_props,
                 &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts, &g->w_route,
-                &g->w_qoff, &g->w_qtok, &g->w_tprof};
+                &g->w_qoff, &g->w_qtok, &g->w_tprof, &g->w_ktm};
   for (DBuf *b : ws) b->release();
   g->w_dense.part.release();
   g->w_dense.norm.release();
@@ -488,9 +488,19 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.task_ctr = a.stats + 14;
   if (g->fuse_b1) {
     a.fuse = 1;
+    a.nseq = (int)g->fuse_nseq;
     a.ub = *g->fuse_b1;
-    // small graphs: one key table for the search and the update (<= 32 KB of shared memory)
-    a.kt = g->n <= 8192 && !getenv("KNNG_NO_KT");
+    mmax = g->n + g->fuse_nseq;   // the pool of the last insert of the sequence
+    // small graphs: the sequence's keys against the whole pool, computed densely by one launch and
+    // staged per insert in shared memory (<= 32 KB) for the search and the update
+    a.kt = mmax <= 8192 && !getenv("KNNG_NO_KT");
+    if (a.kt) {
+      a.ktm_ld = (mmax + 3) & ~3ll;
+      CK(g->w_ktm.ensure((size_t)g->fuse_nseq * a.ktm_ld * 4));
+      a.ktm = g->w_ktm.as<uint32_t>();
+      CK(launch_keymat(g->metric, qs, qrow0, g->n, g->fuse_nseq, a.ktm_ld, g->w_ktm.as<uint32_t>(), g->stream));
+      ++*nl;
+    }
   }
   if (int r = plan_k1(g, a, nq * pc, mmax)) return r;
   CK(g->w_bits.ensure((size_t)a.gslots * a.de_words * 4));
@@ -698,15 +708,20 @@ static int finish_stats(knng_graph *g, knng_stats *st, int nl, int nev, int64_t 
 
 static int insert_batch_dist(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st);
 
-// B = 1 on an unpartitioned single-GPU graph -- the paper's sequential algorithm (Alg. 1 + Alg. 2,
-// P:109-151): ingest, then ONE launch in which a warp searches (K1, one task) and runs the insert's
-// update (new row = C, ball, proposals applied in place), and one synchronisation for the stats.
-static int insert_one(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st) {
+// Sequential inserts on an unpartitioned single-GPU graph -- the paper's sequential algorithm (Alg. 1 +
+// Alg. 2 per point): ingest all n points (rows n_t.., invisible to the searches until their
+// turn), then ONE launch in which a warp searches (K1, one task) and runs the update (new row = C,
+// ball, proposals applied in place) point after point, and one synchronisation for the stats.
+static int insert_seq(knng_graph *g, const knng_points *pts, const knng_params *p, knng_stats *st) {
   int nl = 0;
-  const int64_t n_t = g->n;
-  const int64_t ballmax = ball_bound(n_t, g->k, p->depth);
+  const int64_t n_t = g->n, B = pts->n;
+  const int64_t ballmax = ball_bound(n_t + B - 1, g->k, p->depth);
   int hcap = 64;
   while (hcap < 2 * ballmax) hcap <<= 1;
+  CK(g->w_stats.ensure(32 * 8));
+  CK(g->w_cand_i.ensure((size_t)g->k * 4));
+  CK(g->w_cand_k.ensure((size_t)g->k * 4));
+  if (getenv("KNNG_PROFILE")) CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));   // cycle counters add up
   BallArgs ba;
   memset(&ba, 0, sizeof ba);
   ba.st = graph_store_view(g);
@@ -722,16 +737,27 @@ static int insert_one(knng_graph *g, const knng_points *pts, const knng_params *
   ba.stats = g->w_stats.as<unsigned long long>();
   CK(cudaEventRecord(g->ev[0], g->stream));
   g->fuse_b1 = &ba;
-  const int r = stage_search(g, pts, p, 0, 1, -1, -1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl);
+  g->fuse_nseq = B;
+  const int r = stage_search(g, pts, p, 0, 1, 0, 1, g->w_cand_i.as<int32_t>(), g->w_cand_k.as<uint32_t>(), &nl);
   g->fuse_b1 = nullptr;
+  g->fuse_nseq = 0;
   if (r) {
     g->pend_B = 0;
     return r;
   }
   CK(cudaEventRecord(g->ev[1], g->stream));
-  g->n = n_t + 1;
+  g->n = n_t + B;
   g->pend_B = 0;
-  return finish_stats(g, st, nl, 2, 1);
+  g->tprof_n = B;
+  const int rc = finish_stats(g, st, nl, 2, 1);
+  g->tprof_n = 0;
+  if (st) st->allpair_pairs = 0;
+  return rc;
+}
+
+static bool seq_fusable(const knng_graph *g, const knng_points *pts, const knng_params *p) {
+  return pts && pts->n >= 1 && g->P == 0 && !g->comm && p && p->depth >= 1 && p->depth <= 10 &&
+         !getenv("KNNG_NO_B1") && g->n + pts->n <= g->cap && ball_bound(g->n + pts->n - 1, g->k, p->depth) <= 4096;
 }
 
 int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,
@@ -743,13 +769,7 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   CK(cudaSetDevice(g->device));
   if (g->comm) return insert_batch_dist(g, pts, p, st);
   // the sequential algorithm's fast path (the ball of a B = 1 insert fits one warp's shared memory)
-  if (pts && pts->n == 1 && g->P == 0 && p && p->depth >= 1 && p->depth <= 10 && !getenv("KNNG_NO_B1") &&
-      ball_bound(g->n, g->k, p->depth) <= 4096) {
-    CK(g->w_stats.ensure(32 * 8));
-    CK(g->w_cand_i.ensure((size_t)g->k * 4));
-    CK(g->w_cand_k.ensure((size_t)g->k * 4));
-    return insert_one(g, pts, p, st);
-  }
+  if (pts && pts->n == 1 && seq_fusable(g, pts, p)) return insert_seq(g, pts, p, st);
   CK(g->w_stats.ensure(32 * 8));
   CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   const int64_t B = pts ? pts->n : 0, k = g->k;
@@ -781,6 +801,70 @@ int graph_insert_batch(knng_graph *g, const knng_points *pts, const knng_params 
   }
   CK(cudaEventRecord(g->ev[4], g->stream));
   return finish_stats(g, st, nl, 5, B);
+}
+
+int graph_insert_sequential(knng_graph *g, const knng_points *pts, const knng_params *p, int64_t *first_id_out,
+                            knng_stats *st) {
+  knng_err_slot().clear();
+  if (!g) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_sequential: null graph");
+  if (g->pend_B) return fail(KNNG_ERR_INVALID_ARG, "graph_insert_sequential: a staged batch is pending");
+  if (first_id_out) *first_id_out = g->n;
+  if (int r = check_points(pts, "insert")) return r;
+  if (st) memset(st, 0, sizeof *st);
+  if (pts->n == 0) return 0;
+  CK(cudaSetDevice(g->device));
+  if (seq_fusable(g, pts, p)) return insert_seq(g, pts, p, st);
+  // otherwise one graph_insert_batch of one point after another (views into the caller's points)
+  std::vector<uint64_t> hoff;
+  if (pts->metric == KNNG_JACCARD_U32SET) {
+    hoff.resize((size_t)pts->n + 1);
+    if (pts->data_on_device)
+      CK(cudaMemcpy(hoff.data(), pts->offsets, hoff.size() * 8, cudaMemcpyDeviceToHost));
+    else
+      memcpy(hoff.data(), pts->offsets, hoff.size() * 8);
+  }
+  uint64_t *doff = nullptr;   // 2-entry offsets of a one-set view, in the caller's memory space
+  if (pts->metric == KNNG_JACCARD_U32SET && pts->data_on_device) CK(cudaMalloc(&doff, 16));
+  knng_stats acc;
+  memset(&acc, 0, sizeof acc);
+  int rc = 0;
+  for (int64_t i = 0; i < pts->n && rc == 0; ++i) {
+    knng_points one = *pts;
+    one.n = 1;
+    uint64_t ho[2];
+    if (pts->metric == KNNG_JACCARD_U32SET) {
+      ho[0] = 0;
+      ho[1] = hoff[i + 1] - hoff[i];
+      one.data = (const uint32_t *)pts->data + hoff[i];
+      if (doff) {
+        if (cudaMemcpy(doff, ho, 16, cudaMemcpyHostToDevice) != cudaSuccess) { rc = fail(KNNG_ERR_CUDA, "offsets"); break; }
+        one.offsets = doff;
+      } else {
+        one.offsets = ho;
+      }
+    } else {
+      one.data = (const uint8_t *)pts->data + (size_t)i * pts->dim * (pts->metric == KNNG_L2SQ_U8 ? 1 : 4);
+    }
+    knng_stats s1;
+    rc = graph_insert_batch(g, &one, p, nullptr, &s1);
+    if (rc == 0) {
+      acc.search_evals += s1.search_evals;
+      acc.search_starts += s1.search_starts;
+      acc.search_skipped += s1.search_skipped;
+      acc.search_expansions += s1.search_expansions;
+      acc.ball_nodes += s1.ball_nodes;
+      acc.proposals += s1.proposals;
+      acc.kernel_launches += s1.kernel_launches;
+      acc.ms_search += s1.ms_search;
+      acc.ms_allpairs += s1.ms_allpairs;
+      acc.ms_update += s1.ms_update;
+      acc.ms_merge += s1.ms_merge;
+      acc.ms_total += s1.ms_total;
+    }
+  }
+  if (doff) cudaFree(doff);
+  if (st) *st = acc;
+  return rc;
 }
 
 // ---------------------------------------------------------------------------------------------

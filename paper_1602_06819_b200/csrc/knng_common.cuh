@@ -63,9 +63,10 @@ __device__ __forceinline__ bool skip_start(uint32_t kr, uint32_t kb, uint64_t nu
          den * (uint64_t)(kb >> 16) * (uint64_t)(kr & 0xFFFFu);
 }
 
-// The same rule against a fixed s_max, its best-key side prepared once per change of the best key
-// (no division: a u8 test is den(1+D_r) > num(1+D_b) in 64-bit integers); the f32 and Jaccard forms
-// keep exactly the operations of skip_start.
+// The same rule against a fixed s_max, prepared once per change of the best key: a u8 test becomes
+// one compare (den(1+D_r) > num(1+D_b)  <=>  D_r >= floor(num(1+D_b)/den); the floor is one fp64
+// division rounded toward zero, exact while num(1+D_b) < 2^53, else an integer division); the f32 and
+// Jaccard forms keep exactly the operations of skip_start.
 template <int M>
 struct SkipThr {
   uint64_t t, A, Bv;
@@ -74,13 +75,16 @@ struct SkipThr {
   __device__ __forceinline__ void set(uint32_t kb, uint64_t num, uint64_t den_) {
     den = den_;
     if (den == 0) return;
-    if (M == M_U8) t = num * (1ull + kb);
+    if (M == M_U8) {
+      const uint64_t x = num * (1ull + kb);
+      t = x < (1ull << 53) ? (uint64_t)__ddiv_rz((double)x, (double)den) : x / den;
+    }
     if (M == M_F32) rhs = __dmul_rn((double)num, __dadd_rn(1.0, (double)__uint_as_float(kb)));
     if (M == M_JAC) { A = num * (uint64_t)(kb & 0xFFFFu); Bv = den * (uint64_t)(kb >> 16); }
   }
   __device__ __forceinline__ bool skip(uint32_t kr) const {
     if (den == 0) return false;
-    if (M == M_U8) return den * (1ull + kr) > t;
+    if (M == M_U8) return (uint64_t)kr >= t;
     if (M == M_F32) return __dmul_rn((double)den, __dadd_rn(1.0, (double)__uint_as_float(kr))) > rhs;
     return A * (uint64_t)(kr >> 16) < Bv * (uint64_t)(kr & 0xFFFFu);
   }

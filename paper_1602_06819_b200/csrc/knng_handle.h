@@ -50,7 +50,9 @@ struct knng_graph {
   int64_t pend_B = 0;                           // batch ingested by stage_search, not yet committed
   int pend_parts = 0;                           // partitions stage_search searched for the pending batch
   int pend_route = 0;                           // ... or 1: the batch was searched on its routed partitions
-  const knng::BallArgs *fuse_b1 = nullptr;   // set by insert_one around its search launch (B = 1 fused)
+  const knng::BallArgs *fuse_b1 = nullptr;   // set by insert_seq around its search launch (B = 1 fused)
+  int64_t fuse_nseq = 0;
+  DBuf w_ktm;                                // [nseq][ld] key matrix of a sequence on a small graph (KT)                     // ... and the number of sequential inserts of that launch
   DBuf w_route;                                 // routing targets of a search
   knng::VecGeom geom{};
   int device = 0;

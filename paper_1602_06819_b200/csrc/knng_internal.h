@@ -116,12 +116,18 @@ struct SearchArgs {
   // B = 1 fused launch (one task): after the search, the same warp runs the update of the insert
   // (update_one_warp with ub, C = out_ids / out_keys) and writes stats[0..5] itself
   int fuse;
+  int nseq;                    // (fuse) sequential inserts: rows n_t .. n_t + nseq - 1 (ingested), one after another
   BallArgs ub;
-  int kt;                      // (fuse) 1: the keys against all n_t pool nodes precomputed into shared memory
+  int kt;                      // (fuse) 1: the keys against all n_t pool nodes precomputed (ktm) and staged in smem
+  const uint32_t *ktm;         // (kt) [nseq][ktm_ld] key matrix of the sequence (launch_keymat)
+  int64_t ktm_ld;
 };
 size_t search_smem_bytes(const SearchArgs &a, bool sets);
 // warps of one K1 launch that can be resident at once (sizes the per-warp E / X planes)
 cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t *warps);
+// keys of points qrow0 + i (i < B) against nodes 0 .. n0 + i - 1 into out [B][ld] (the KT launches)
+cudaError_t launch_keymat(int metric, const StoreView &st, int64_t qrow0, int64_t n0, int64_t B, int64_t ld,
+                          uint32_t *out, cudaStream_t s);
 // K1 computes keys one lane per staged row for this width (the compile-time lane-form kernels)
 bool search_lane_form(const VecGeom &g, int lane_eval);
 

@@ -140,6 +140,27 @@ __host__ __device__ __forceinline__ size_t fuse_bytes(const SearchArgs &a, bool 
   return a.fuse ? ((16 + update_one_smem(a.ub.hcap, a.ub.ballmax) + (sets ? QMAX * 4 : 0) + 15) & ~(size_t)15) : 0;
 }
 
+// Key matrix of a sequence of B inserts on a small graph (the KT launches): row i = the keys of point
+// qrow0 + i against nodes 0 .. n0 + i - 1 (the pool its search and update will see); ld = n0 + B rounded
+// to 4.  Thread per (i, v); exact keys (pair_key: the canonical forms of every metric).
+template <int M>
+__global__ void k_keymat(StoreView st, int64_t qrow0, int64_t n0, int64_t B, int64_t ld, uint32_t *out) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (i >= B || v >= n0 + i) return;
+  out[(size_t)i * ld + v] = pair_key<M>(st, qrow0 + i, v);
+}
+
+cudaError_t launch_keymat(int metric, const StoreView &st, int64_t qrow0, int64_t n0, int64_t B, int64_t ld,
+                          uint32_t *out, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)((n0 + B + 127) / 128), (unsigned)B);
+  if (metric == M_U8) k_keymat<M_U8><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
+  else if (metric == M_F32) k_keymat<M_F32><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
+  else k_keymat<M_JAC><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
+  return cudaGetLastError();
+}
+
 // Rows of a lane-form width (NCK 16-byte chunks, compile time) gathered into stage slots: lane r
 // holds the node id of slot r (-1: none), rows r < nrows.  LPR lanes share a row so that every copy
 // instruction reads whole 128-byte segments; rows with NCK % 8 == 0 are stored swizzled (swz_pos).
@@ -205,15 +226,24 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   const int64_t gw = (int64_t)blockIdx.x * WPC + warp;                      // warp slot
   uint32_t *planes = a.gbits + gw * a.de_words;                            // E / X words of the task
   unsigned long long s_evals = 0, s_starts = 0, s_skip = 0, s_exp = 0;
+  unsigned long long s_ball = 0, s_prop = 0;
+  // fused launch: nseq sequential inserts (each a batch of one against the graph the previous one left:
+  // the paper's Alg. 1 + 2 point after point); else one pass over the launch's tasks
+  const int nseq = a.fuse ? a.nseq : 1;
+  for (int it = 0; it < nseq; ++it) {
+  const int64_t n_t = a.n_t + it, qrow0 = a.qrow0 + it, pid_base = a.pid_base + it;
   int64_t task = gw;
   // KT (the fused B = 1 launch on a small graph): the keys of the query against every pool node are
   // computed up front by the whole CTA into a shared table; the search and the update then read keys
   // from it instead of gathering rows (same keys, same decisions, same counters).
   uint32_t *kt = nullptr;
-  if constexpr (KT != 0) {
+  if constexpr (KT != 0) {   // row `it` of the sequence's key matrix (k_keymat) into shared memory
     kt = (uint32_t *)(smem + (size_t)WPC * a.wbytes + 8 * WPC + fuse_bytes(a, M == M_JAC));
-    const int64_t m0 = a.n_t;
-    for (int64_t v = threadIdx.x; v < m0; v += blockDim.x) kt[v] = pair_key<M>(a.qs, a.qrow0, v);
+    const uint32_t *src = a.ktm + (size_t)it * a.ktm_ld;
+    const int64_t n4 = n_t >> 2;
+#pragma unroll 4
+    for (int64_t v = threadIdx.x; v < n4; v += blockDim.x) ((uint4 *)kt)[v] = ((const uint4 *)src)[v];
+    for (int64_t v = (n4 << 2) + threadIdx.x; v < n_t; v += blockDim.x) kt[v] = src[v];
     __syncthreads();
   }
 
@@ -221,7 +251,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     const int64_t b = task / Pn;
     const int pl = (int)(task % Pn);          // output slot
     const int p = a.route ? a.route[b] : a.part_lo + pl;   // partition searched
-    const int64_t m = part ? a.member_cnt[p] : a.n_t;
+    const int64_t m = part ? a.member_cnt[p] : n_t;
     const int32_t *pool = part ? a.members + (size_t)p * a.member_cap : nullptr;
     // next task (dynamic scheduling), read back at the end of this one
     if (lane == 0) sched[warp] = (long long)(gridDim.x * WPC + atomicAdd(a.task_ctr, 1ull));
@@ -245,12 +275,12 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     if (budget > m) budget = m;
 
     typename QuerySel<M, L, CPL>::T Q;
-    if (!LF) Q.load(a.qs, a.qrow0 + b, M == M_JAC ? qscr : nullptr);
+    if (!LF && KT == 0) Q.load(a.qs, qrow0 + b, M == M_JAC ? qscr : nullptr);
     if (LF) {
-      const uint8_t *qg = a.qs.vec + (size_t)(a.qrow0 + b) * a.qs.stride;
+      const uint8_t *qg = a.qs.vec + (size_t)(qrow0 + b) * a.qs.stride;
       for (int cc = lane; cc < nck; cc += 32) *(uint4 *)(qsm + 16 * cc) = ldg16(qg + 16 * cc);
     }
-    const uint64_t h3 = rng_prefix(a.seed, (uint64_t)(a.pid_base + b), (uint64_t)p);
+    const uint64_t h3 = rng_prefix(a.seed, (uint64_t)(pid_base + b), (uint64_t)p);
     __syncwarp();
 
     WarpTopK<M> top;
@@ -673,8 +703,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       }
     }
     KPROF(if (a.prof && lane == 0) {
-      // (the fused B = 1 launch owns the counters: stores, so that no memset precedes it)
-      auto put = [&](int i, unsigned long long v) { if (a.fuse) a.prof[i] = v; else atomicAdd(a.prof + i, v); };
+      auto put = [&](int i, unsigned long long v) { atomicAdd(a.prof + i, v); };
       put(0, (unsigned long long)(clock64() - tc0));
       put(2, (unsigned long long)c_walk);
       put(5, c_win);
@@ -694,18 +723,29 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     task = *(volatile long long *)(sched + warp);
     __syncwarp();
   }
-  if (a.fuse) {   // B = 1: one CTA, warp 0 ran the only task; it owns the stats and runs the update
+  if (a.fuse) {   // B = 1: one CTA, warp 0 ran the only task; it runs the insert's update
     if (gw == 0) {
-      if (lane == 0) {
-        a.stats[0] = s_evals;
-        a.stats[1] = s_starts;
-        a.stats[2] = s_skip;
-        a.stats[3] = s_exp;
-      }
       uint8_t *us = smem + (size_t)WPC * a.wbytes + 8 * WPC;
       int32_t *usm = (int32_t *)(us + 16);
       uint32_t *uq = (uint32_t *)(us + 16 + update_one_smem(a.ub.hcap, a.ub.ballmax));
-      update_one_warp<M, L, CPL>(a.ub, a.out_ids, a.out_keys, usm, (int *)us, M == M_JAC ? uq : nullptr, true, kt);
+      BallArgs ub = a.ub;
+      ub.n_t = n_t;
+      int nb = 0, np = 0;
+      update_one_warp<M, L, CPL>(ub, a.out_ids, a.out_keys, usm, (int *)us, M == M_JAC ? uq : nullptr, &nb, &np, kt);
+      s_ball += (unsigned)nb;
+      s_prop += (unsigned)np;
+    }
+    __syncthreads();   // the insert's rows (global) before the next insert's search and key table
+  }
+  }   // sequential inserts
+  if (a.fuse) {   // the fused launch owns the stats (no memset before it)
+    if (gw == 0 && lane == 0) {
+      a.stats[0] = s_evals;
+      a.stats[1] = s_starts;
+      a.stats[2] = s_skip;
+      a.stats[3] = s_exp;
+      a.stats[4] = s_ball;
+      a.stats[5] = s_prop;
     }
     return;
   }
@@ -752,7 +792,8 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   return (b + 15) & ~(size_t)15;
 }
 size_t search_smem_bytes(const SearchArgs &a, bool sets) {
-  return WPC * search_warp_bytes(a, sets) + 8 * WPC + fuse_bytes(a, sets) + (a.kt ? ((a.n_t * 4 + 15) & ~15ll) : 0);
+  return WPC * search_warp_bytes(a, sets) + 8 * WPC + fuse_bytes(a, sets) +
+         (a.kt ? (((a.n_t + (a.fuse ? a.nseq : 0)) * 4 + 15) & ~15ll) : 0);
 }
 
 // occupancy of a K1 instantiation at a shared-memory size on the current device, cached (a B = 1 insert

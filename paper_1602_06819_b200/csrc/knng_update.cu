@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(32) k_update_one(BallArgs a, const uint32_t *C
   extern __shared__ int32_t usm[];
   __shared__ uint32_t qscr[M == M_JAC ? QMAX : 1];
   __shared__ int s_n;
-  update_one_warp<M, L, CPL>(a, a.C, Ckeys, usm, &s_n, M == M_JAC ? qscr : nullptr, false);
+  update_one_warp<M, L, CPL>(a, a.C, Ckeys, usm, &s_n, M == M_JAC ? qscr : nullptr, nullptr, nullptr);
 }
 
 template <int M, int L, int CPL>

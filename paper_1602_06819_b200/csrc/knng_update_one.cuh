@@ -25,12 +25,12 @@ __host__ __device__ __forceinline__ size_t update_one_smem(int hcap, int ballmax
   return (size_t)(hcap + ballmax + (ballmax & 1)) * 4 + (size_t)ballmax * 8;
 }
 
-// C / Ckeys: the new point's search result (k entries, -1 padded).  plain: write stats[4], [5] with
-// stores (the fused launch owns the stats), else add to them.  kt: keys of the new point against
-// nodes 0..n_t-1 (the fused launch's table), else evaluated here.
+// C / Ckeys: the new point's search result (k entries, -1 padded).  nb / np: the ball and proposal
+// counts are returned there (the fused launch sums them), else added to stats[4], [5].  kt: keys of
+// the new point against nodes 0..n_t-1 (the fused launch's table), else evaluated here.
 template <int M, int L, int CPL>
 __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t *C, const uint32_t *Ckeys,
-                                                int32_t *usm, int *s_n, uint32_t *qscr, bool plain,
+                                                int32_t *usm, int *s_n, uint32_t *qscr, int *nb, int *npr,
                                                 const uint32_t *kt = nullptr) {
   const int lane = threadIdx.x & 31;
   const int k = a.k;
@@ -56,21 +56,32 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
     if (lane == 0) *s_n = __popc(m);
     __syncwarp();
   }
-  // levels 1..DEPTH over the snapshot rows: collect the ball, evaluate, propose
+  // levels 1..DEPTH over the snapshot rows: collect the ball, evaluate, propose.  A level's rows are
+  // read G = 32 / k at a time (lane = node g, entry e), four groups in flight before the inserts.
+  const int G = 32 / k;
+  const int gl = lane / k, ge = lane - gl * k;
   int lo = 0, hi = *(volatile int *)s_n, np = 0;
   for (int d = 1; d <= a.depth; ++d) {
-    for (int base = lo; base < hi; base += 32) {
-      const int t = base + lane;
-      const int32_t v = t < hi ? list[t] : -1;
-      if (d < a.depth && v >= 0) {
-        for (int e = 0; e < k; ++e) {
-          const int32_t u = a.ids[(size_t)v * k + e];
-          if (u >= 0 && u != idx && hash_insert(hash, a.hcap, u)) {
+    if (d < a.depth) {
+      for (int gb = lo; gb < hi; gb += 4 * G) {
+        int32_t u[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int t = gb + r * G + gl;
+          u[r] = (gl < G && t < hi) ? a.ids[(size_t)list[t] * k + ge] : -1;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (u[r] >= 0 && u[r] != idx && hash_insert(hash, a.hcap, u[r])) {
             const int pos = atomicAdd(s_n, 1);
-            if (pos < a.ballmax) list[pos] = u;
+            if (pos < a.ballmax) list[pos] = u[r];
           }
         }
       }
+    }
+    for (int base = lo; base < hi; base += 32) {
+      const int t = base + lane;
+      const int32_t v = t < hi ? list[t] : -1;
       const int cnt = hi - base < 32 ? hi - base : 32;
       const uint32_t key = kt ? (v >= 0 ? kt[v] : 0u) : Q.eval(a.st, v, cnt);   // kt: the fused launch's key table
       bool prop = false;
@@ -85,29 +96,35 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
     hi = sn < a.ballmax ? sn : a.ballmax;
     __syncwarp();
   }
-  // apply (Q14): row_v = top-k(row_v u {(D, idx)}); one lane per proposal, distinct rows
-  for (int j = lane; j < np; j += 32) {
-    const int32_t v = props[j].x;
-    const uint32_t key = (uint32_t)props[j].y;
-    int32_t *ri = a.ids + (size_t)v * k;
-    uint32_t *rk = a.keys + (size_t)v * k;
-    int pos = k - 1;
-    while (pos > 0 && precedes<M>(key, idx, rk[pos - 1], ri[pos - 1])) {
-      rk[pos] = rk[pos - 1];
-      ri[pos] = ri[pos - 1];
-      --pos;
+  // apply (Q14): row_v = top-k(row_v u {(D, idx)}); G proposals at a time, k lanes each (distinct rows):
+  // the row is read at once, the entry's position is a ballot, the tail shifts by one lane
+  for (int j0 = 0; j0 < np; j0 += G) {
+    const int j = j0 + gl;
+    const bool act = gl < G && j < np;
+    int32_t v = -1, ri = -1;
+    uint32_t key = 0, rk = 0;
+    if (act) {
+      v = props[j].x;
+      key = (uint32_t)props[j].y;
+      ri = a.ids[(size_t)v * k + ge];
+      rk = a.keys[(size_t)v * k + ge];
     }
-    rk[pos] = key;
-    ri[pos] = idx;
+    const bool before = act && precedes<M>(rk, ri, key, idx);   // entry e stays ahead of the new one
+    const unsigned grp = (k == 32 ? FULL : ((1u << k) - 1u)) << (gl * k);
+    const int pos = __popc(__ballot_sync(FULL, before) & grp);
+    const uint32_t uk = __shfl_up_sync(FULL, rk, 1);
+    const int32_t ui = __shfl_up_sync(FULL, ri, 1);
+    if (act && ge >= pos) {
+      a.keys[(size_t)v * k + ge] = ge == pos ? key : uk;
+      a.ids[(size_t)v * k + ge] = ge == pos ? idx : ui;
+    }
   }
-  if (lane == 0) {
-    if (plain) {
-      a.stats[4] = (unsigned long long)lo;
-      a.stats[5] = (unsigned long long)np;
-    } else {
-      atomicAdd(a.stats + 4, (unsigned long long)lo);
-      atomicAdd(a.stats + 5, (unsigned long long)np);
-    }
+  if (nb) {
+    *nb = lo;
+    *npr = np;
+  } else if (lane == 0) {
+    atomicAdd(a.stats + 4, (unsigned long long)lo);
+    atomicAdd(a.stats + 5, (unsigned long long)np);
   }
 }
 

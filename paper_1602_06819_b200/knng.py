@@ -57,7 +57,7 @@ class knng_runtime(C.Structure):
 EXPORTS = ["graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
            "graph_get_partition", "graph_size", "graph_degree", "graph_free", "graph_last_error",
            "graph_ball_bound", "graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit",
-           "graph_nccl_unique_id", "graph_world", "graph_recompute_medoids"]
+           "graph_nccl_unique_id", "graph_world", "graph_recompute_medoids", "graph_insert_sequential"]
 
 _lib = None
 
@@ -74,6 +74,8 @@ def load_library(path=LIB_PATH):
     L.graph_init.argtypes = [C.POINTER(knng_points), C.c_int32, C.POINTER(knng_runtime), C.POINTER(C.c_void_p)]
     L.graph_insert_batch.argtypes = [P, C.POINTER(knng_points), C.POINTER(knng_params), C.POINTER(C.c_int64),
                                      C.POINTER(knng_stats)]
+    L.graph_insert_sequential.argtypes = [P, C.POINTER(knng_points), C.POINTER(knng_params), C.POINTER(C.c_int64),
+                                          C.POINTER(knng_stats)]
     L.graph_search.argtypes = [P, C.POINTER(knng_points), C.c_int32, C.POINTER(knng_params), P, P, C.c_int32,
                                C.POINTER(knng_stats)]
     L.partition_kmedoids.argtypes = [P, C.c_int32, C.c_double, C.c_int32, C.c_uint64, P, P, P, P]
@@ -101,8 +103,8 @@ def load_library(path=LIB_PATH):
     L.graph_world.restype = C.c_int32
     for f in ("graph_insert_stage_search", "graph_insert_stage_update", "graph_insert_stage_commit"):
         getattr(L, f).restype = C.c_int
-    for f in ("graph_init", "graph_insert_batch", "graph_search", "partition_kmedoids", "graph_get_rows",
-              "graph_get_partition"):
+    for f in ("graph_init", "graph_insert_batch", "graph_insert_sequential", "graph_search", "partition_kmedoids",
+              "graph_get_rows", "graph_get_partition"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -235,6 +237,17 @@ class KnngGraph:
         first = C.c_int64()
         st = knng_stats()
         _check(load_library().graph_insert_batch(self._h, C.byref(p), C.byref(prm), C.byref(first), C.byref(st)))
+        return int(first.value), st.as_dict()
+
+    def insert_sequential(self, points, speedup, e_num, e_den, depth, seed):
+        """graph_insert_sequential: the points one after another, each a batch of one (the paper's
+        sequential algorithm); one launch on an unpartitioned single-GPU graph."""
+        p, keep = make_points(points)
+        prm, _ = make_params(speedup, e_num, e_den, depth, seed)
+        first = C.c_int64()
+        st = knng_stats()
+        _check(load_library().graph_insert_sequential(self._h, C.byref(p), C.byref(prm), C.byref(first),
+                                                      C.byref(st)))
         return int(first.value), st.as_dict()
 
     def search(self, queries, kr, speedup, e_num, e_den, seed, starts=None, out=None, full_scan=0, route=0):

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 -k "sequential or fast_path" > gpurun_out/r2o_pytest0.log 2>&1; echo "rc=$?" >> gpurun_out/r2o_pytest0.log
+timeout 300 python bench.py --config C0 --steps 20 --warmup 3 > gpurun_out/r2o_bench_C0.json 2> gpurun_out/r2o_bench_C0.err
+KNNG_LIB=$PWD/paper_1602_06819_b200/libknng_prof.so KNNG_PROFILE=1 timeout 300 python bench.py --config C0 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r2o_bench_C0_prof.json 2> gpurun_out/r2o_bench_C0_prof.err
+timeout 600 python scripts/k1_ab.py --config C3 --n0 2000000 --reps 3 - > gpurun_out/r2o_C3.log 2>&1
+timeout 300 python scripts/k1_ab.py --config C1 --n0 100000 --reps 3 - > gpurun_out/r2o_C1.log 2>&1

@@ -230,6 +230,43 @@ def test_insert_batches_of_one_fast_path(name, n0, depth, k, keytable, monkeypat
     assert (hi == gi).all() and (hk == gk).all()
 
 
+@pytest.mark.parametrize("name,n0,part,env", [("C0", 2000, False, None), ("C1", 12000, False, None),
+                                              ("C2", 3000, False, None), ("C4", 1500, False, None),
+                                              ("C0", 2000, False, "KNNG_NO_KT"), ("C2", 3000, False, "KNNG_ESMEM"),
+                                              ("C3", 6000, True, None), ("C4", 1500, True, None)])
+def test_insert_sequential_matches_oracle(name, n0, part, env, monkeypatch):
+    """graph_insert_sequential: n points one after another (one launch when unpartitioned: key table /
+    gathers / global E words; a loop of B = 1 inserts when partitioned) == the oracle's n B = 1 inserts,
+    rows and summed counters."""
+    if env:
+        monkeypatch.setenv(env, "1" if env != "KNNG_ESMEM" else "0")
+    cfg = _cfg_small(name, n0=n0, n_insert=70)
+    X = D.initial_points(cfg)
+    S = D.stream_points(cfg, 0, cfg.n_insert)
+    cap = cfg.n0 + cfg.n_insert + 8
+    g = _graph(X, cfg.k, cap)
+    o = O.OracleGraph(cfg.metric, X, cfg.k, capacity=cap)
+    o.init_exact()
+    if part:
+        gp, gm, _ = g.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+        op, om, _ = o.partition_kmedoids(cfg.P, cfg.imbalance, 3, cfg.part_seed)
+        assert (gp == op).all()
+        o.set_partition(op, om)
+    pos = 0
+    for n in (1, 45, 24):
+        first, gst = g.insert_sequential(S[pos:pos + n], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)
+        tot = np.zeros(6, np.int64)
+        for i in range(pos, pos + n):
+            tot += o.insert_batch(S[i:i + 1], cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, cfg.search_seed)[0, :6]
+        assert first == cfg.n0 + pos
+        assert (gst["search_evals"], gst["search_starts"], gst["search_skipped"], gst["search_expansions"],
+                gst["ball_nodes"], gst["proposals"]) == tuple(int(x) for x in tot), (name, n, gst, tot)
+        pos += n
+        gi, gk = g.rows()
+        oi, ok = o.rows()
+        _assert_rows_equal(cfg.metric, gi, gk, oi, ok, "%s sequential after %d" % (name, pos))
+
+
 def test_insert_C1_shape():
     cfg = _cfg_small("C1", n0=20000, n_insert=2100)
     _run_stream(cfg, [1024, 1024, 52])
