@@ -468,6 +468,8 @@ struct VecQuery {
 // the range hold valid tokens), and a 4-bit mask per chunk keeps only the candidate's own tokens.
 // Up to SU chunks per lane and set are in flight together.
 constexpr int QMAX = 256;
+constexpr int SET_HT = 256;              // open-addressing table of the query's tokens (membership in ~1 probe)
+constexpr int QSCR = QMAX + SET_HT;      // words of a set query's shared scratch: tokens, then the table
 template <int L>
 struct SetQuery {
   static constexpr int SU = 1;
@@ -475,21 +477,48 @@ struct SetQuery {
   const uint32_t *bm;    // vocabulary bitmap of the query (shared) or null
   int qn;
 
+  const uint32_t *ht;    // hash table of the query's tokens (shared; token + 1, 0 = empty) or null
+  static __device__ __forceinline__ int hslot(uint32_t t) { return (int)((t * 0x9E3779B1u) >> 24); }
+
+  // scratch: QSCR words of shared memory (tokens, then the table), or null
   __device__ __forceinline__ void load(const StoreView &s, int64_t r, uint32_t *scratch) {
     const int lane = threadIdx.x & 31;
     const uint64_t b = s.off[r];
     qn = (int)(s.off[r + 1] - b);
     bm = nullptr;
+    ht = nullptr;
     if (qn <= QMAX && scratch) {
-      for (int i = lane; i < qn; i += 32) scratch[i] = s.tok[b + i];
-      __syncwarp();
+      bool big = false;
+      for (int i = lane; i < qn; i += 32) {
+        scratch[i] = s.tok[b + i];
+        big |= scratch[i] == 0xFFFFFFFFu;
+      }
       q = scratch;
+      if (qn <= SET_HT / 2 && !__any_sync(FULL, big)) {   // load factor <= 1/2
+        uint32_t *t = scratch + QMAX;
+        for (int i = lane; i < SET_HT; i += 32) t[i] = 0u;
+        __syncwarp();
+        for (int i = lane; i < qn; i += 32) {
+          const uint32_t v = scratch[i] + 1u;
+          int h = hslot(scratch[i]);
+          while (atomicCAS(t + h, 0u, v) != 0u) h = (h + 1) & (SET_HT - 1);
+        }
+        ht = t;
+      }
+      __syncwarp();
     } else {
       q = s.tok + b;
     }
   }
 
   __device__ __forceinline__ int has(uint32_t t) const {
+    if (ht) {
+      for (int h = hslot(t);; h = (h + 1) & (SET_HT - 1)) {
+        const uint32_t e = ht[h];
+        if (e == t + 1u) return 1;
+        if (e == 0u) return 0;
+      }
+    }
     if (bm) return (bm[t >> 5] >> (t & 31)) & 1u;
     int lo = 0, hi = qn;
     while (lo < hi) {

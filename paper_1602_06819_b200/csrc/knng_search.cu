@@ -137,7 +137,7 @@ __device__ __forceinline__ uint32_t staged_keys(const typename QuerySel<M, L, CP
 
 // shared memory of the fused B = 1 update (after the warps' regions): s_n, hash / list / props, query tokens
 __host__ __device__ __forceinline__ size_t fuse_bytes(const SearchArgs &a, bool sets) {
-  return a.fuse ? ((16 + update_one_smem(a.ub.hcap, a.ub.ballmax) + (sets ? QMAX * 4 : 0) + 15) & ~(size_t)15) : 0;
+  return a.fuse ? ((16 + update_one_smem(a.ub.hcap, a.ub.ballmax) + (sets ? QSCR * 4 : 0) + 15) & ~(size_t)15) : 0;
 }
 
 // Key matrix of a sequence of B inserts on a small graph (the KT launches): row i = the keys of point
@@ -218,8 +218,8 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   uint8_t *qsm = wrow + ((WPF * RB + 15) & ~15);                           // [512 B] query (vectors)
   uint32_t *pkey = (uint32_t *)(qsm + 512);                                // [32] pending walk evaluations
   int32_t *pid = (int32_t *)(pkey + 32);                                   // [32]
-  uint32_t *qscr = (uint32_t *)(pid + 32);                                 // [QMAX] query tokens (sets)
-  uint32_t *ebits = qscr + (M == M_JAC ? QMAX : 0);                        // [e_bytes / 4] E bitmap (es)
+  uint32_t *qscr = (uint32_t *)(pid + 32);                                 // [QSCR] query tokens + table (sets)
+  uint32_t *ebits = qscr + (M == M_JAC ? QSCR : 0);                        // [e_bytes / 4] E bitmap (es)
   long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
@@ -787,7 +787,7 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   const size_t RB = (size_t)(a.P > 0 ? 8 : 4) * a.k;
   const bool ns2 = !sets && a.e_smem && a.ns2;
   size_t b = (size_t)(ns2 ? 64 : 32) * a.pitch + (a.row_pf ? ((a.k * RB + 15) & ~(size_t)15) : 0) +
-             ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QMAX * 4 : 0) +
+             ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QSCR * 4 : 0) +
              (a.e_smem ? (size_t)a.e_bytes * ((a.x_smem || a.kt) ? 2 : 1) : 0);
   return (b + 15) & ~(size_t)15;
 }

@@ -65,7 +65,7 @@ cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, 
 template <int M, int L, int CPL>
 __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
   __shared__ int s_n[4];
-  __shared__ uint32_t qscr[M == M_JAC ? 4 * QMAX : 1];
+  __shared__ uint32_t qscr[M == M_JAC ? 4 * QSCR : 1];
   extern __shared__ int32_t bsm[];   // small balls: [4][hcap] hash + [4][ballmax] list in shared memory
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * 4 + wib, nw = (int64_t)gridDim.x * 4;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
     if (lane == 0) s_n[wib] = 0;
     __syncwarp();
     typename QuerySel<M, L, CPL>::T Q;
-    Q.load(a.st, a.n_t + b, M == M_JAC ? qscr + wib * QMAX : nullptr);
+    Q.load(a.st, a.n_t + b, M == M_JAC ? qscr + wib * QSCR : nullptr);
     const int32_t idx = (int32_t)(a.n_t + b);
     // L1 = the search result C(x)
     {
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
 template <int M, int L, int CPL>
 __global__ void __launch_bounds__(32) k_update_one(BallArgs a, const uint32_t *Ckeys) {
   extern __shared__ int32_t usm[];
-  __shared__ uint32_t qscr[M == M_JAC ? QMAX : 1];
+  __shared__ uint32_t qscr[M == M_JAC ? QSCR : 1];
   __shared__ int s_n;
   update_one_warp<M, L, CPL>(a, a.C, Ckeys, usm, &s_n, M == M_JAC ? qscr : nullptr, nullptr, nullptr);
 }
