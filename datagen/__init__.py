@@ -18,7 +18,8 @@ import numpy as np
 
 CHUNK = 4096
 
-U8, F32, JAC = 0, 1, 2
+U8, F32, JAC, JW, COS = 0, 1, 2, 3, 4
+CSR = (JAC, JW, COS)   # points as lists of uint32 arrays (token sets; strings of characters)
 
 
 @dataclasses.dataclass(frozen=True)
@@ -73,6 +74,14 @@ CONFIGS = {
                n_insert=200_000, batch=4096, speedup=16.0, e_num=6, e_den=5, depth=2,
                P=8, imbalance=1.05),
 }
+
+# the paper's string workloads (P:289 SPAM subjects under Jaro-Winkler, P:292 Wikipedia
+# pages under the 2-gram cosine) on synthetic strings (their corpora are absent): `clusters` templates,
+# each point a template with random edits (STR_RECIPE).  Not BASELINE.json configs: parity / bench cases.
+CONFIGS["S1"] = _cfg(5, name="S1", metric=JW, n0=100_000, dim=0, clusters=2000, sigma=0.0, k=10,
+                     n_insert=10_000, batch=1024, speedup=8.0, e_num=6, e_den=5, depth=2)
+CONFIGS["S2"] = _cfg(6, name="S2", metric=COS, n0=100_000, dim=0, clusters=2000, sigma=0.0, k=10,
+                     n_insert=10_000, batch=1024, speedup=8.0, e_num=6, e_den=5, depth=2)
 
 
 def _rng(seed, purpose, chunk=0):
@@ -135,6 +144,48 @@ def _token_sets(r, n):
     return sets
 
 
+# ---------------------------------------------------------------------------
+# Synthetic strings (8(f)#4): alphabet a-z and space (code points); template t of a config has length
+# U{10..60} (JW, subject-like) or U{40..120} (COS, text-like) drawn from the alphabet; a point is a
+# uniformly chosen template with each character substituted (p 0.08), deleted (p 0.04) or followed by an
+# inserted character (p 0.04); lengths are clipped to 1..127 (the metrics' bound).
+# ---------------------------------------------------------------------------
+ALPHABET = np.array([ord(c) for c in "abcdefghijklmnopqrstuvwxyz "], dtype=np.uint32)
+STR_RECIPE = dict(p_sub=0.08, p_del=0.04, p_ins=0.04, max_len=127)
+
+
+def _templates(cfg: Config):
+    r = _rng(cfg.data_seed, 0)
+    lo, hi = (10, 61) if cfg.metric == JW else (40, 121)
+    lens = r.integers(lo, hi, size=cfg.clusters)
+    return [ALPHABET[r.integers(0, len(ALPHABET), size=int(L))] for L in lens]
+
+
+def _strings(cfg: Config, tmpl, r, n):
+    out = []
+    lab = r.integers(0, len(tmpl), size=n)
+    for t in lab:
+        base = tmpl[int(t)]
+        u = r.random((len(base), 3))
+        subs = ALPHABET[r.integers(0, len(ALPHABET), size=len(base))]
+        ins = ALPHABET[r.integers(0, len(ALPHABET), size=len(base))]
+        s = []
+        for i, ch in enumerate(base):
+            if u[i, 1] < STR_RECIPE["p_del"]:
+                continue
+            s.append(int(subs[i]) if u[i, 0] < STR_RECIPE["p_sub"] else int(ch))
+            if u[i, 2] < STR_RECIPE["p_ins"]:
+                s.append(int(ins[i]))
+        if not s:
+            s = [int(base[0])]
+        out.append(np.asarray(s[:STR_RECIPE["max_len"]], dtype=np.uint32))
+    return out
+
+
+def _csr_points(cfg: Config, r, n):
+    return _token_sets(r, n) if cfg.metric == JAC else _strings(cfg, _templates(cfg), r, n)
+
+
 def sets_to_csr(sets):
     off = np.zeros(len(sets) + 1, dtype=np.uint64)
     off[1:] = np.cumsum([len(s) for s in sets])
@@ -148,26 +199,26 @@ def sets_to_csr(sets):
 def initial_points(cfg: Config):
     """u8/f32: array [n0, dim]; JAC: list of sorted uint32 arrays."""
     r = _rng(cfg.data_seed, 1)
-    if cfg.metric == JAC:
-        return _token_sets(r, cfg.n0)
+    if cfg.metric in CSR:
+        return _csr_points(cfg, r, cfg.n0)
     return _mixture(cfg, _means(cfg), r, cfg.n0)
 
 
 def stream_points(cfg: Config, start: int, count: int):
     """Points start .. start+count-1 of the insert stream (prefix-stable)."""
     if count <= 0:
-        if cfg.metric == JAC:
+        if cfg.metric in CSR:
             return []
         dt = np.uint8 if cfg.metric == U8 else np.float32
         return np.zeros((0, cfg.dim), dt)
     c0, c1 = start // CHUNK, (start + count - 1) // CHUNK
-    means = None if cfg.metric == JAC else _means(cfg)
+    means = None if cfg.metric in CSR else _means(cfg)
     parts = []
     for c in range(c0, c1 + 1):
         r = _rng(cfg.data_seed, 2, c)
-        parts.append(_token_sets(r, CHUNK) if cfg.metric == JAC else _mixture(cfg, means, r, CHUNK))
+        parts.append(_csr_points(cfg, r, CHUNK) if cfg.metric in CSR else _mixture(cfg, means, r, CHUNK))
     lo = start - c0 * CHUNK
-    if cfg.metric == JAC:
+    if cfg.metric in CSR:
         allp = [s for p in parts for s in p]
         return allp[lo:lo + count]
     return np.concatenate(parts)[lo:lo + count]
@@ -175,8 +226,8 @@ def stream_points(cfg: Config, start: int, count: int):
 
 def query_points(cfg: Config, count: int, seed_offset: int = 0):
     r = _rng(cfg.data_seed, 3, seed_offset)
-    if cfg.metric == JAC:
-        return _token_sets(r, count)
+    if cfg.metric in CSR:
+        return _csr_points(cfg, r, count)
     return _mixture(cfg, _means(cfg), r, count)
 
 

@@ -53,18 +53,35 @@ extern "C" {
  * KNNG_JACCARD_U32SET sorted, duplicate-free uint32 token sets (set-similarity stand-in for
  *                     P:292); key = (|A n B| << 16) | |A u B|, similarity = inter/union,
  *                     compared exactly by cross-multiplication.
+ * KNNG_JARO_WINKLER   strings (section 7.1.2: the SPAM subjects' measure):
+ *                     Jaro similarity with the Winkler prefix boost (common prefix l <= 4, scaling
+ *                     0.1), matching window max(|a|,|b|)/2 - 1, T = matched characters out of order
+ *                     (t = T/2 transpositions).  key = m | T << 7 | l << 14 | |a| << 17 | |b| << 24;
+ *                     jw = ((10-l)(2m^2|b| + 2m^2|a| + (2m-T)|a||b|) + 6 l |a||b| m) / (60 |a||b| m),
+ *                     compared exactly as fractions.
+ * KNNG_COSINE_2GRAM   strings (section 7.1.3: the Wikipedia pages' measure):
+ *                     cosine of the count vectors of the 2-grams (contiguous character pairs); a string
+ *                     shorter than 2 is the zero vector (cosine 0).  The key of b in a's row (or in
+ *                     query a's result) = (dot << 16) | max(|b|^2, 1): a's norm is common to every key
+ *                     a row or a search compares, so cos_1 > cos_2 <=> dot_1^2 |b_2|^2 > dot_2^2 |b_1|^2.
+ *                     Keys are therefore directed (a row holds its owner's keys); JW keys are symmetric.
+ *                     Strings: unpartitioned graphs only (partition_kmedoids returns INVALID_ARG).
  * Edge order (all metrics): more similar key first, equal similarity -> smaller id.
  * Every neighbour row is sorted by edge order. */
 typedef enum {
   KNNG_L2SQ_U8 = 0,
   KNNG_L2SQ_F32 = 1,
-  KNNG_JACCARD_U32SET = 2
+  KNNG_JACCARD_U32SET = 2,
+  KNNG_JARO_WINKLER = 3,
+  KNNG_COSINE_2GRAM = 4
 } knng_metric;
 
 /* A set of points.  Vectors: data = u8[n*dim] or f32[n*dim], row-major.
  * Sets: data = uint32 tokens (each set sorted ascending, no duplicates), offsets = uint64[n+1]
  * (set i is data[offsets[i] .. offsets[i+1])), dim ignored; sets hold <= 32767 tokens (the key packs
  * the union |A u B| <= 65534 into 16 bits; longer sets fail with INVALID_ARG, host or device input).
+ * Strings (KNNG_JARO_WINKLER, KNNG_COSINE_2GRAM): the same CSR form, one uint32 character (code unit)
+ * per element in string order, 0..127 characters per string (the keys pack lengths in 7 bits).
  * data_on_device = 1: data (and offsets) are device pointers on the handle's GPU. */
 typedef struct {
   int32_t metric;

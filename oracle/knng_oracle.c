@@ -42,8 +42,14 @@
 /*   OR_U8  : D = sum_j (a_j-b_j)^2, exact integer (Q25: squared L2)    */
 /*   OR_F32 : D = fp32 squared L2 in the canonical order (Q24), as bits */
 /*   OR_JAC : (inter << 16) | union of two token sets                   */
+/*   OR_JW  : Jaro-Winkler of two strings (section 7.1.2):        */
+/*            m | T << 7 | l << 14 | |a| << 17 | |b| << 24               */
+/*   OR_COS : cosine of the 2-gram count vectors (section 7.1.3): */
+/*            (dot << 16) | max(|b|^2, 1), b = the row's other end       */
+/* Strings are sequences of uint32 characters (<= 127) held like sets    */
+/* (tok / off), in their original order.                                 */
 /* ------------------------------------------------------------------ */
-enum { OR_U8 = 0, OR_F32 = 1, OR_JAC = 2 };
+enum { OR_U8 = 0, OR_F32 = 1, OR_JAC = 2, OR_JW = 3, OR_COS = 4 };
 
 typedef struct {
   int metric;
@@ -100,6 +106,68 @@ static float f32_canonical_l2sq(const float *a, const float *b, int dim) {
   return acc[0];
 }
 
+/* Jaro-Winkler (Jaro similarity with the Winkler prefix boost, prefix <= 4,
+ * scaling 0.1), the textbook definition step by step:
+ *   window w = max(|a|, |b|) / 2 - 1 (floor, at least 0);
+ *   a character a[i] matches the first not yet matched b[j] with b[j] == a[i] and |i - j| <= w,
+ *   taking i in order;  m = the number of matches;
+ *   T = the number of positions at which the matched characters of a and of b, each read in
+ *   order, differ (t = T / 2 transpositions);
+ *   jaro = (m/|a| + m/|b| + (m - t)/m) / 3  (0 when m = 0);
+ *   l = the common prefix length, at most 4;  jw = jaro + l * 0.1 * (1 - jaro).
+ * The key keeps (m, T, l, |a|, |b|): jw is recovered exactly as a fraction (or_jw_fraction). */
+static uint32_t jw_key(const uint32_t *a, int64_t la, const uint32_t *b, int64_t lb) {
+  unsigned char amatch[128], bmatch[128];
+  int64_t w = (la > lb ? la : lb) / 2 - 1, i, j, m = 0, T = 0, l = 0;
+  if (w < 0) w = 0;
+  memset(amatch, 0, sizeof amatch);
+  memset(bmatch, 0, sizeof bmatch);
+  for (i = 0; i < la; ++i) {
+    int64_t lo = i - w > 0 ? i - w : 0, hi = i + w < lb - 1 ? i + w : lb - 1;
+    for (j = lo; j <= hi; ++j) {
+      if (!bmatch[j] && b[j] == a[i]) { bmatch[j] = 1; amatch[i] = 1; ++m; break; }
+    }
+  }
+  j = 0;
+  for (i = 0; i < la; ++i) {
+    if (!amatch[i]) continue;
+    while (!bmatch[j]) ++j;
+    if (a[i] != b[j]) ++T;
+    ++j;
+  }
+  while (l < 4 && l < la && l < lb && a[l] == b[l]) ++l;
+  return (uint32_t)(m | (T << 7) | (l << 14) | (la << 17) | (lb << 24));
+}
+
+/* jw = N / D exactly: jaro = (2 m^2 |b| + 2 m^2 |a| + (2m - T) |a| |b|) / (6 |a| |b| m) and
+ * jw = ((10 - l) jaro + l) / 10.  m = 0: 0 / 1. */
+void or_jw_fraction(uint32_t key, uint64_t *num, uint64_t *den) {
+  uint64_t m = key & 127, T = (key >> 7) & 127, l = (key >> 14) & 7, la = (key >> 17) & 127, lb = (key >> 24) & 127;
+  uint64_t n0, d0;
+  if (m == 0) { *num = 0; *den = 1; return; }
+  n0 = 2 * m * m * lb + 2 * m * m * la + (2 * m - T) * la * lb;
+  d0 = 6 * la * lb * m;
+  *num = (10 - l) * n0 + l * d0;
+  *den = 10 * d0;
+}
+
+/* Cosine of the 2-gram count vectors: a string's 2-grams are its contiguous
+ * pairs (s[i], s[i+1]); dot = sum over 2-grams g of c_a(g) c_b(g) = the number of position pairs
+ * (i, j) with equal 2-grams; |b|^2 = sum_g c_b(g)^2 likewise.  cos = dot / (|a| |b|), 0 when either
+ * string is shorter than 2 (zero vector).  The key keeps dot and |b|^2 (1 for a zero vector): within
+ * one row or one query |a| is common, so cos_1 > cos_2 <=> dot_1^2 |b_2|^2 > dot_2^2 |b_1|^2. */
+static uint32_t cos2_key(const uint32_t *a, int64_t la, const uint32_t *b, int64_t lb) {
+  int64_t i, j, dot = 0, nb = 0;
+  for (i = 0; i + 1 < la; ++i)
+    for (j = 0; j + 1 < lb; ++j)
+      if (a[i] == b[j] && a[i + 1] == b[j + 1]) ++dot;
+  for (i = 0; i + 1 < lb; ++i)
+    for (j = 0; j + 1 < lb; ++j)
+      if (b[i] == b[j] && b[i + 1] == b[j + 1]) ++nb;
+  if (nb == 0) nb = 1;
+  return (uint32_t)((dot << 16) | nb);
+}
+
 static uint32_t key_of(const or_store *S, or_point a, or_point b) {
   if (S->metric == OR_U8) {
     int32_t D = 0;
@@ -111,6 +179,10 @@ static uint32_t key_of(const or_store *S, or_point a, or_point b) {
     return (uint32_t)D;
   } else if (S->metric == OR_F32) {
     return float_bits(f32_canonical_l2sq(a.f32, b.f32, S->dim));
+  } else if (S->metric == OR_JW) {
+    return jw_key(a.tok, a.ntok, b.tok, b.ntok);
+  } else if (S->metric == OR_COS) {
+    return cos2_key(a.tok, a.ntok, b.tok, b.ntok);
   } else {
     /* |A n B| by merging two sorted lists; |A u B| = |A| + |B| - |A n B| */
     int64_t i = 0, j = 0, inter = 0;
@@ -127,6 +199,16 @@ static uint32_t key_of(const or_store *S, or_point a, or_point b) {
 static int closer(int metric, uint32_t a, uint32_t b) {
   if (metric == OR_U8) return a < b;
   if (metric == OR_F32) return bits_float(a) < bits_float(b);
+  if (metric == OR_JW) {          /* jw_a > jw_b as fractions */
+    uint64_t na, da, nb, db;
+    or_jw_fraction(a, &na, &da);
+    or_jw_fraction(b, &nb, &db);
+    return (unsigned __int128)na * db > (unsigned __int128)nb * da;
+  }
+  if (metric == OR_COS) {         /* dot_a / |x_a| > dot_b / |x_b|, squared */
+    uint64_t da = a >> 16, na = a & 0xFFFF, db = b >> 16, nb = b & 0xFFFF;
+    return (unsigned __int128)da * da * nb > (unsigned __int128)db * db * na;
+  }
   {
     int64_t ia = a >> 16, ua = a & 0xFFFF, ib = b >> 16, ub = b & 0xFFFF;
     return ia * ub > ib * ua;      /* i_a/u_a > i_b/u_b, exact (C.1) */
@@ -153,6 +235,14 @@ static int skip_start(int metric, uint32_t kr, uint32_t kbest, uint64_t num, uin
     volatile double lhs = (double)den * (1.0 + (double)bits_float(kr));
     volatile double rhs = (double)num * (1.0 + (double)bits_float(kbest));
     return lhs > rhs;
+  } else if (metric == OR_JW) {   /* s = jw: num * jw_r < den * jw_best, as fractions */
+    uint64_t nr, dr, nbst, dbst;
+    or_jw_fraction(kr, &nr, &dr);
+    or_jw_fraction(kbest, &nbst, &dbst);
+    return (unsigned __int128)num * nr * dbst < (unsigned __int128)den * nbst * dr;
+  } else if (metric == OR_COS) {  /* s = cos (|a| common): num dot_r / |x_r| < den dot_b / |x_b|, squared */
+    unsigned __int128 dr = kr >> 16, nr = kr & 0xFFFF, db = kbest >> 16, nbst = kbest & 0xFFFF;
+    return (unsigned __int128)num * num * dr * dr * nbst < (unsigned __int128)den * den * db * db * nr;
   } else {
     uint64_t ir = kr >> 16, ur = kr & 0xFFFF, ib = kbest >> 16, ub = kbest & 0xFFFF;
     return num * ir * ub < den * ib * ur;
@@ -614,7 +704,7 @@ static int64_t update_ball(const or_graph *G, or_point x, int32_t idx, const int
           seen[u] = 1; buf[nhi++] = u;
         }
       }
-      D = key_of(&S, x, store_point(&S, v));
+      D = key_of(&S, store_point(&S, v), x);   /* v's similarity to x, as v's row holds it */
       ++nball;
       if (precedes(G->metric, D, idx, G->keys[(size_t)v * k + k - 1], G->ids[(size_t)v * k + k - 1])) {
         props[*nprops].node = v; props[*nprops].key = D; props[*nprops].qid = qid;
@@ -816,7 +906,7 @@ int or_insert_sequential(int metric, int dim, void *data, uint64_t *off, int k,
         if (u < 0 || u == newid) continue;
         Qn[nn++] = u;
       }
-      D = key_of(&S, x, store_point(&S, node)); /* compute similarity(new, node) */
+      D = key_of(&S, store_point(&S, node), x); /* compute similarity(new, node), as node's row holds it */
       if (out_stats) out_stats[4] += 1;
       L.cap = k; L.cnt = k; L.key = keys + (size_t)node * k; L.id = ids + (size_t)node * k;
       if (list_insert(metric, &L, D, newid) && out_stats) out_stats[5] += 1;  /* if needed, add new */

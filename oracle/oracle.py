@@ -17,7 +17,8 @@ import threading
 
 import numpy as np
 
-U8, F32, JAC = 0, 1, 2
+U8, F32, JAC, JW, COS = 0, 1, 2, 3, 4
+CSR = (JAC, JW, COS)   # points held as uint32 sequences in CSR form (sets; strings of characters)
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "knng_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
@@ -50,6 +51,8 @@ def lib():
             L.or_key.restype = C.c_uint32
             L.or_key.argtypes = [i32, i32, P, i64, P, i64]
             L.or_closer.argtypes = [i32, C.c_uint32, C.c_uint32]
+            L.or_jw_fraction.argtypes = [C.c_uint32, C.POINTER(u64), C.POINTER(u64)]
+            L.or_jw_fraction.restype = None
             L.or_precedes.argtypes = [i32, C.c_uint32, i64, C.c_uint32, i64]
             L.or_skip.argtypes = [i32, C.c_uint32, C.c_uint32, u64, u64]
             L.or_exact_rows.restype = None
@@ -96,7 +99,7 @@ def default_threads():
 # JAC: (inter << 16) | union.
 # ---------------------------------------------------------------------------
 def key(metric, a, b):
-    if metric == JAC:
+    if metric in CSR:
         a = np.ascontiguousarray(a, np.uint32)
         b = np.ascontiguousarray(b, np.uint32)
         return int(lib().or_key(metric, 0, _p(a), len(a), _p(b), len(b)))
@@ -107,13 +110,27 @@ def key(metric, a, b):
 
 
 def key_value(metric, k):
-    """Numeric view of a key: D for L2 metrics, similarity i/u for Jaccard."""
+    """Numeric view of a key: D for L2 metrics, similarity i/u for Jaccard, jw for Jaro-Winkler, cos^2 * |a|^2
+    (dot^2 / |b|^2, the row-relative value) for the 2-gram cosine."""
     if metric == F32:
         return float(np.uint32(k).view(np.float32))
+    if metric == JW:
+        n, d = jw_fraction(k)
+        return n / d
+    if metric == COS:
+        return (k >> 16) ** 2 / (k & 0xFFFF)
     if metric == JAC:
         i, u = k >> 16, k & 0xFFFF
         return i / u if u else 0.0
     return int(k)
+
+
+def jw_fraction(key):
+    """Jaro-Winkler value of a key as an exact fraction (numerator, denominator) (or_jw_fraction)."""
+    L = lib()
+    num, den = C.c_uint64(), C.c_uint64()
+    L.or_jw_fraction(C.c_uint32(int(key)), C.byref(num), C.byref(den))
+    return int(num.value), int(den.value)
 
 
 def closer(metric, a, b):
@@ -179,7 +196,7 @@ class OracleGraph:
     def __init__(self, metric, points, k, capacity=None, dim=None):
         self.metric = metric
         self.k = int(k)
-        if metric == JAC:
+        if metric in CSR:
             sets = list(points)
             n = len(sets)
             self.n = n
@@ -218,7 +235,7 @@ class OracleGraph:
         B = len(pts)
         if self.n + B > self.cap:
             raise RuntimeError("capacity exceeded")
-        if self.metric == JAC:
+        if self.metric in CSR:
             pos = int(self.off[self.n])
             need = pos + sum(len(s) for s in pts)
             if need > len(self.tok):
@@ -232,7 +249,7 @@ class OracleGraph:
             self.data[self.n:self.n + B] = np.asarray(pts)
 
     def point(self, i):
-        if self.metric == JAC:
+        if self.metric in CSR:
             return self.tok[int(self.off[i]):int(self.off[i + 1])]
         return self.data[i]
 
@@ -322,7 +339,7 @@ class OracleGraph:
     def insert_sequential(self, pt, speedup, e_num, e_den, depth, seed):
         """Literal Alg. 1 + Alg. 2 for one point."""
         n_t = self.n
-        self._append_points([pt] if self.metric == JAC else np.asarray(pt)[None])
+        self._append_points([pt] if self.metric in CSR else np.asarray(pt)[None])
         st = np.zeros(6, np.int64)
         rc = lib().or_insert_sequential(self.metric, self.dim, _p(self.data), _p(self.off), self.k,
                                         n_t, _p(self.ids), _p(self.keys), speedup, e_num, e_den,
@@ -335,7 +352,7 @@ class OracleGraph:
     def search(self, queries, kr, speedup, e_num, e_den, seed, nthreads=None, full_scan=0, route=0):
         """graph_search; full_scan=1 with e_den=0 is the GNNS baseline; route=1 searches only the
         nearest medoid's partition (reading Q18's routing variant)."""
-        if self.metric == JAC:
+        if self.metric in CSR:
             qoff = np.zeros(len(queries) + 1, np.uint64)
             qoff[1:] = np.cumsum([len(q) for q in queries])
             qd = np.concatenate(queries).astype(np.uint32) if len(queries) else np.zeros(1, np.uint32)
@@ -359,7 +376,7 @@ class OracleGraph:
     def ignns(self, q, kr, speedup, e_num, e_den, seed, pid, starts=None, part=0, pool=None, full_scan=0):
         """One iGNNS search on the current graph; optional injected starts.  full_scan=1:
         the GNNS baseline's walk (with e_den=0, no restart skipping: GNNS)."""
-        if self.metric == JAC:
+        if self.metric in CSR:
             qd = np.ascontiguousarray(q, np.uint32)
             qtok, qn, qdata = qd, len(qd), None
         else:
@@ -399,7 +416,7 @@ class OracleGraph:
         return med, int(cost[0])
 
     def nearest_medoid(self, x):
-        if self.metric == JAC:
+        if self.metric in CSR:
             xa = np.ascontiguousarray(x, np.uint32)
             nx = len(xa)
         else:

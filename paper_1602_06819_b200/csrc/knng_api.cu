@@ -45,9 +45,14 @@ int knng_fail(int code, const char *fmt, ...) {
 }
 
 static int elem_bytes(int metric) { return metric == KNNG_L2SQ_U8 ? 1 : 4; }
+// points held as uint32 sequences in CSR form: token sets, strings of characters
+static bool csr_points(int metric) {
+  return metric == KNNG_JACCARD_U32SET || metric == KNNG_JARO_WINKLER || metric == KNNG_COSINE_2GRAM;
+}
+static bool str_points(int metric) { return metric == KNNG_JARO_WINKLER || metric == KNNG_COSINE_2GRAM; }
 
 static int geom_for(int metric, int dim, VecGeom *g) {
-  if (metric == KNNG_JACCARD_U32SET) {   // sets: L = 8 lanes per candidate in the warp evaluator
+  if (csr_points(metric)) {   // sets / strings: one lane per candidate (L = 8: the set evaluator's instantiation)
     g->metric = metric;
     g->nchunks = 0;
     g->stride = 0;
@@ -82,12 +87,12 @@ static int geom_for(int metric, int dim, VecGeom *g) {
 
 static int check_points(const knng_points *p, const char *what) {
   if (!p) return fail(KNNG_ERR_INVALID_ARG, "%s: null points", what);
-  if (p->metric != KNNG_L2SQ_U8 && p->metric != KNNG_L2SQ_F32 && p->metric != KNNG_JACCARD_U32SET)
+  if (p->metric != KNNG_L2SQ_U8 && p->metric != KNNG_L2SQ_F32 && !csr_points(p->metric))
     return fail(KNNG_ERR_INVALID_ARG, "%s: bad metric %d", what, p->metric);
-  if (p->metric != KNNG_JACCARD_U32SET && p->dim < 1) return fail(KNNG_ERR_INVALID_ARG, "%s: dim < 1", what);
+  if (!csr_points(p->metric) && p->dim < 1) return fail(KNNG_ERR_INVALID_ARG, "%s: dim < 1", what);
   if (p->n < 0) return fail(KNNG_ERR_INVALID_ARG, "%s: n < 0", what);
   if (p->n > 0 && !p->data) return fail(KNNG_ERR_INVALID_ARG, "%s: null data", what);
-  if (p->metric == KNNG_JACCARD_U32SET && !p->offsets) return fail(KNNG_ERR_INVALID_ARG, "%s: null offsets", what);
+  if (csr_points(p->metric) && !p->offsets) return fail(KNNG_ERR_INVALID_ARG, "%s: null offsets", what);
   return 0;
 }
 
@@ -118,6 +123,21 @@ __global__ void k_max_set_len(const uint64_t *off, int64_t n, unsigned long long
   if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 static constexpr uint64_t KNNG_SET_MAX = 32767;
+static uint64_t csr_max_len(int metric) { return str_points(metric) ? (uint64_t)STR_MAX : KNNG_SET_MAX; }
+
+// 2-gram cosine strings: |x|^2 = sum_g c_x(g)^2 = the number of position pairs with equal 2-grams, for
+// strings [first, first + count) of a store (thread per string; 1 for strings shorter than 2, whose
+// count vector is zero -- their cosine with anything is 0 whatever the norm)
+__global__ void k_str_norms(const uint64_t *off, const uint32_t *tok, int64_t first, int64_t count, uint32_t *n2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint32_t *x = tok + off[first + i];
+  const int L = (int)(off[first + i + 1] - off[first + i]);
+  uint32_t c = 0;
+  for (int a = 0; a + 1 < L; ++a)
+    for (int b = 0; b + 1 < L; ++b) c += (x[a] == x[b]) & (x[a + 1] == x[b + 1]);
+  n2[first + i] = c > 0 ? c : 1u;
+}
 
 __global__ void k_rebase_offsets(const uint64_t *in, int64_t n, uint64_t base, uint64_t *out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -140,13 +160,14 @@ static int append_sets(knng_graph *g, const knng_points *p, uint64_t **off_dst_b
     CK(cudaMemcpyAsync(&last, p->offsets + p->n, 8, cudaMemcpyDeviceToHost, g->stream));
     CK(cudaFreeAsync(dm, g->stream));
     CK(cudaStreamSynchronize(g->stream));
-    if (mlen > KNNG_SET_MAX) return fail(KNNG_ERR_INVALID_ARG, "set longer than %llu tokens", (unsigned long long)KNNG_SET_MAX);
+    if (mlen > csr_max_len(p->metric))
+      return fail(KNNG_ERR_INVALID_ARG, "set / string longer than %llu", (unsigned long long)csr_max_len(p->metric));
   } else {
     first = p->offsets[0];
     last = p->offsets[p->n];
     for (int64_t i = 0; i < p->n; ++i)
-      if (p->offsets[i + 1] - p->offsets[i] > KNNG_SET_MAX)
-        return fail(KNNG_ERR_INVALID_ARG, "set longer than %llu tokens", (unsigned long long)KNNG_SET_MAX);
+      if (p->offsets[i + 1] - p->offsets[i] > csr_max_len(p->metric))
+        return fail(KNNG_ERR_INVALID_ARG, "set / string longer than %llu", (unsigned long long)csr_max_len(p->metric));
   }
   const int64_t nt = (int64_t)(last - first);
   if (tok0 + nt > *tok_cap) {
@@ -198,10 +219,14 @@ static int append_sets(knng_graph *g, const knng_points *p, uint64_t **off_dst_b
 
 // store the batch's points at rows [row0, row0+n) of the graph's store
 static int store_points(knng_graph *g, const knng_points *p, int64_t row0) {
-  if (g->metric == KNNG_JACCARD_U32SET) {
+  if (csr_points(g->metric)) {
     int64_t nt = 0;
     if (int r = append_sets(g, p, &g->off, &g->tok, &g->tok_cap, row0, g->tok_n, &nt, &g->tok_max)) return r;
     g->tok_n += nt;
+    if (g->metric == KNNG_COSINE_2GRAM && p->n > 0) {
+      k_str_norms<<<(unsigned)((p->n + 127) / 128), 128, 0, g->stream>>>(g->off, g->tok, row0, p->n, g->sn2);
+      CK(cudaGetLastError());
+    }
     return 0;
   }
   return copy_rows(g, g->vec + (size_t)row0 * g->geom.stride, p);
@@ -211,13 +236,13 @@ static void free_graph(knng_graph *g) {
   if (!g) return;
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
-  void *bufs[] = {g->vec, g->ids, g->keys, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->part_of, g->local_idx, g->lrows,
-                  g->members, g->member_cnt, g->medoids, g->off, g->tok};
+  void *bufs[] = {g->vec, g->ids, g->keys, g->ncnt, g->nfill, g->noff, g->scan_tmp, g->part_of, g->local_idx, g->prow,
+                  g->pvec, g->pset, g->members, g->member_cnt, g->medoids, g->off, g->tok, g->sn2};
   for (void *b : bufs)
     if (b) cudaFree(b);
   DBuf *ws[] = {&g->w_bits, &g->w_cand_i, &g->w_cand_k, &g->w_C_i, &g->w_C_k, &g->w_hash, &g->w_list, &g->w_props,
                 &g->w_prop_cnt, &g->w_sorted, &g->w_stats, &g->w_target, &g->w_query, &g->w_starts, &g->w_route,
-                &g->w_qoff, &g->w_qtok, &g->w_tprof, &g->w_ktm};
+                &g->w_qoff, &g->w_qtok, &g->w_tprof, &g->w_ktm, &g->w_qn2};
   for (DBuf *b : ws) b->release();
   g->w_dense.part.release();
   g->w_dense.norm.release();
@@ -313,8 +338,9 @@ int graph_init(const knng_points *pts, int32_t k, const knng_runtime *rt, knng_g
       return bail(KNNG_ERR_OOM);                                  \
     }                                                             \
   } while (0)
-  if (g->metric == KNNG_JACCARD_U32SET) {
+  if (csr_points(g->metric)) {
     A(g->off, (cap + 1) * 8);
+    if (g->metric == KNNG_COSINE_2GRAM) A(g->sn2, cap * 4);
   } else {
     A(g->vec, cap * g->geom.stride);
   }
@@ -358,7 +384,7 @@ static int plan_k1(knng_graph *g, SearchArgs &a, int64_t tasks, int64_t mmax) {
   a.lane_eval = 1;
   if (const char *e = getenv("KNNG_LANE_EVAL")) a.lane_eval = atoi(e);
   // staged rows: the lane-form widths with nchunks % 8 == 0 are stored swizzled (no bank-conflict pad)
-  const bool sets = g->metric == KNNG_JACCARD_U32SET;
+  const bool sets = csr_points(g->metric);
   const bool lform = search_lane_form(g->geom, a.lane_eval);
   a.swz = lform && g->geom.nchunks % 8 == 0;
   a.pitch = sets ? 16 * 16 + 16 : (int)g->geom.stride + (a.swz ? 0 : 16);
@@ -470,7 +496,9 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
   a.member_cnt = g->member_cnt;
   a.part_of = g->part_of;
   a.local_idx = g->local_idx;
-  a.lrows = g->lrows;
+  a.prow = g->prow;
+  a.pvec = g->pvec;
+  a.pset = g->pset;
   a.speedup = p->speedup;
   a.e_num = p->expansion_num;
   a.e_den = p->expansion_den;
@@ -550,7 +578,7 @@ static int stage_search(knng_graph *g, const knng_points *pts, const knng_params
                         int64_t q_lo, int64_t q_hi, int32_t *ci, uint32_t *ck, int *nl) {
   if (int r = check_points(pts, "insert")) return r;
   if (int r = check_params(p)) return r;
-  if (pts->metric != g->metric || (g->metric != KNNG_JACCARD_U32SET && pts->dim != g->dim))
+  if (pts->metric != g->metric || (!csr_points(g->metric) && pts->dim != g->dim))
     return fail(KNNG_ERR_INVALID_ARG, "insert: metric/dim mismatch");
   if (p->depth < 1 || p->depth > 10) return fail(KNNG_ERR_INVALID_ARG, "depth %d outside 1..10", p->depth);
   const int Pn = g->P > 0 ? g->P : 1;
@@ -655,7 +683,7 @@ static int stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, c
   CK(g->w_sorted.ensure((size_t)nq_slots * ballmax * 8));
   // A8: placement at the nearest medoid.  It reads only the new points and the medoids, and the
   // search of this batch is complete, so it runs before the merge: the merged rows' partition-local
-  // view (lrows) then sees the new ids' partitions.
+  // copies (prow) then see the new ids' partitions.
   if (g->P > 0) {
     CK(g->w_target.ensure((size_t)B * 4));
     CK(launch_place(g->geom, graph_store_view(g), n_t, B, g->P, g->medoids, g->members, g->cap, g->member_cnt,
@@ -665,10 +693,11 @@ static int stage_commit(knng_graph *g, const knng_params *p, int64_t nq_slots, c
   // A7: row_v = top-k(row_v u proposals), proposal (slot b) carries the new id n_t + b
   CK(launch_merge_props(g->metric, g->ids, g->keys, g->k, n_t, nq_slots, props_all, prop_cnt_all, (int)ballmax,
                         g->ncnt, g->nfill, g->noff, g->scan_tmp, g->w_sorted.as<int2>(), g->stream, nl,
-                        g->P > 0 ? g->lrows : nullptr, g->part_of, g->local_idx));
-  if (g->P > 0) {   // the new rows' partition-local view
-    CK(launch_lrows(g->ids, g->k, n_t, B, g->part_of, g->local_idx, g->lrows, g->stream));
-    ++*nl;
+                        g->P > 0 ? g->prow : nullptr, g->cap, g->part_of, g->local_idx));
+  if (g->P > 0) {   // the new nodes' partition-local store (rows, vectors / token ranges)
+    CK(launch_local_store(graph_store_view(g), g->ids, g->k, n_t, B, g->part_of, g->local_idx, graph_local_store(g),
+                          g->stream));
+    *nl += 2;
     // partition sizes: bound now, exact once the read-back lands
     if (g->pool_bound > 0) g->pool_bound += B;
     if (g->h_cnt && g->ev_cnt && !g->cnt_pending) {
@@ -816,7 +845,7 @@ int graph_insert_sequential(knng_graph *g, const knng_points *pts, const knng_pa
   if (seq_fusable(g, pts, p)) return insert_seq(g, pts, p, st);
   // otherwise one graph_insert_batch of one point after another (views into the caller's points)
   std::vector<uint64_t> hoff;
-  if (pts->metric == KNNG_JACCARD_U32SET) {
+  if (csr_points(pts->metric)) {
     hoff.resize((size_t)pts->n + 1);
     if (pts->data_on_device)
       CK(cudaMemcpy(hoff.data(), pts->offsets, hoff.size() * 8, cudaMemcpyDeviceToHost));
@@ -824,7 +853,7 @@ int graph_insert_sequential(knng_graph *g, const knng_points *pts, const knng_pa
       memcpy(hoff.data(), pts->offsets, hoff.size() * 8);
   }
   uint64_t *doff = nullptr;   // 2-entry offsets of a one-set view, in the caller's memory space
-  if (pts->metric == KNNG_JACCARD_U32SET && pts->data_on_device) CK(cudaMalloc(&doff, 16));
+  if (csr_points(pts->metric) && pts->data_on_device) CK(cudaMalloc(&doff, 16));
   knng_stats acc;
   memset(&acc, 0, sizeof acc);
   int rc = 0;
@@ -832,7 +861,7 @@ int graph_insert_sequential(knng_graph *g, const knng_points *pts, const knng_pa
     knng_points one = *pts;
     one.n = 1;
     uint64_t ho[2];
-    if (pts->metric == KNNG_JACCARD_U32SET) {
+    if (csr_points(pts->metric)) {
       ho[0] = 0;
       ho[1] = hoff[i + 1] - hoff[i];
       one.data = (const uint32_t *)pts->data + hoff[i];
@@ -1039,7 +1068,7 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
   int nl = 0;
   CK(cudaMemsetAsync(g->w_stats.p, 0, 32 * 8, g->stream));
   StoreView qs = graph_store_view(g);
-  if (g->metric == KNNG_JACCARD_U32SET) {
+  if (csr_points(g->metric)) {
     CK(g->w_qoff.ensure((size_t)(nq + 1) * 8));
     uint32_t *qt = g->w_qtok.as<uint32_t>();
     int64_t qcap = (int64_t)(g->w_qtok.bytes / 4), ntok = 0;
@@ -1051,6 +1080,13 @@ int graph_search(knng_graph *g, const knng_points *q, int32_t kr, const knng_par
     }
     qs.off = g->w_qoff.as<uint64_t>();
     qs.tok = g->w_qtok.as<uint32_t>();
+    if (g->metric == KNNG_COSINE_2GRAM) {   // the queries' own |q|^2 (a query is never another row's entry, but
+                                           // the evaluator's layout is the store's)
+      CK(g->w_qn2.ensure((size_t)nq * 4));
+      k_str_norms<<<(unsigned)((nq + 127) / 128), 128, 0, g->stream>>>(qs.off, qs.tok, 0, nq, g->w_qn2.as<uint32_t>());
+      CK(cudaGetLastError());
+      qs.n2 = g->w_qn2.as<uint32_t>();
+    }
   } else {
     CK(g->w_query.ensure((size_t)nq * g->geom.stride));
     CK(cudaMemsetAsync(g->w_query.p, 0, (size_t)nq * g->geom.stride, g->stream));

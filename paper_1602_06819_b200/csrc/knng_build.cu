@@ -174,17 +174,19 @@ cudaError_t launch_tile_topk(const VecGeom &g, const uint8_t *vec, int64_t row0,
   return cudaGetLastError();
 }
 
-// Jaccard sets: warp per row, lanes over all columns (single-thread sorted-list intersection).
-__global__ void __launch_bounds__(128) k_exact_build_sets(StoreView st, int64_t n, int k, int32_t *ids, uint32_t *keys) {
+// Jaccard sets and strings: warp per row, lanes over all columns (single-thread pair keys: sorted-list
+// intersection / str_key with the row as owner).
+template <int M>
+__global__ void __launch_bounds__(128) k_exact_build_csr(StoreView st, int64_t n, int k, int32_t *ids, uint32_t *keys) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (row >= n) return;
-  WarpTopK<M_JAC> top;
+  WarpTopK<M> top;
   top.init(k);
   for (int64_t c0 = 0; c0 < n; c0 += 32) {
     const int64_t col = c0 + lane;
     const bool valid = col < n && col != row;
-    const uint32_t key = valid ? pair_key<M_JAC>(st, row, col) : 0u;
+    const uint32_t key = valid ? pair_key<M>(st, row, col) : 0u;
     top.insert(valid, key, (int32_t)col);
   }
   if (lane < k) {
@@ -195,8 +197,11 @@ __global__ void __launch_bounds__(128) k_exact_build_sets(StoreView st, int64_t 
 
 cudaError_t launch_exact_build(const VecGeom &g, const StoreView &st, int64_t n, int k, int32_t *ids, uint32_t *keys,
                                DenseScratch *ws, cudaStream_t s) {
-  if (g.metric == M_JAC) {
-    k_exact_build_sets<<<(unsigned)((n + 3) / 4), 128, 0, s>>>(st, n, k, ids, keys);
+  if (csr_metric(g.metric)) {
+    const unsigned nb = (unsigned)((n + 3) / 4);
+    if (g.metric == M_JAC) k_exact_build_csr<M_JAC><<<nb, 128, 0, s>>>(st, n, k, ids, keys);
+    else if (g.metric == M_JW) k_exact_build_csr<M_JW><<<nb, 128, 0, s>>>(st, n, k, ids, keys);
+    else k_exact_build_csr<M_COS><<<nb, 128, 0, s>>>(st, n, k, ids, keys);
     return cudaGetLastError();
   }
   return launch_tile_topk(g, st.vec, 0, n, 0, n, k, nullptr, nullptr, ids, keys, ws, s);

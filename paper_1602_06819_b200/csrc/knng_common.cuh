@@ -9,7 +9,23 @@
 namespace knng {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
-enum { M_U8 = 0, M_F32 = 1, M_JAC = 2 };
+enum { M_U8 = 0, M_F32 = 1, M_JAC = 2, M_JW = 3, M_COS = 4 };
+// points held as uint32 sequences in CSR form (token sets; strings of characters)
+__host__ __device__ constexpr bool csr_metric(int m) { return m >= M_JAC; }
+// strings: Jaro-Winkler, cosine of 2-gram count vectors
+__host__ __device__ constexpr bool str_metric(int m) { return m == M_JW || m == M_COS; }
+constexpr int STR_MAX = 127;   // characters per string (the keys pack lengths / counts in 7 / 16 bits)
+
+// Jaro-Winkler key m | T << 7 | l << 14 | |a| << 17 | |b| << 24 as the exact fraction num / den:
+// jaro = (2m^2|b| + 2m^2|a| + (2m - T)|a||b|) / (6|a||b|m), jw = ((10 - l) jaro + l) / 10 (0 when m = 0).
+__host__ __device__ __forceinline__ void jw_frac(uint32_t key, uint64_t &num, uint64_t &den) {
+  const uint64_t m = key & 127u, T = (key >> 7) & 127u, l = (key >> 14) & 7u, la = (key >> 17) & 127u,
+                 lb = (key >> 24) & 127u;
+  if (m == 0) { num = 0; den = 1; return; }
+  const uint64_t d0 = 6 * la * lb * m;
+  num = (10 - l) * (2 * m * m * (la + lb) + (2 * m - T) * la * lb) + l * d0;
+  den = 10 * d0;
+}
 
 // ---------------------------------------------------------------------------
 // Counter RNG of the random starts (Q4): SplitMix64 finaliser chain keyed by
@@ -40,6 +56,16 @@ template <int M>
 __device__ __forceinline__ bool closer(uint32_t a, uint32_t b) {
   if (M == M_U8) return a < b;
   if (M == M_F32) return __uint_as_float(a) < __uint_as_float(b);
+  if (M == M_JW) {   // jw_a > jw_b (num, den < 2^31: products < 2^62)
+    uint64_t na, da, nb, db;
+    jw_frac(a, na, da);
+    jw_frac(b, nb, db);
+    return na * db > nb * da;
+  }
+  if (M == M_COS) {  // dot_a / |x_a| > dot_b / |x_b| (the row owner's norm is common), squared
+    const uint64_t xa = a >> 16, xb = b >> 16;
+    return xa * xa * (b & 0xFFFFu) > xb * xb * (a & 0xFFFFu);
+  }
   return (uint64_t)(a >> 16) * (b & 0xFFFFu) > (uint64_t)(b >> 16) * (a & 0xFFFFu);
 }
 template <int M>
@@ -59,6 +85,17 @@ __device__ __forceinline__ bool skip_start(uint32_t kr, uint32_t kb, uint64_t nu
     const double r = __dmul_rn((double)num, __dadd_rn(1.0, (double)__uint_as_float(kb)));
     return l > r;
   }
+  if (M == M_JW) {   // num jw_r < den jw_best, as fractions (128-bit products)
+    uint64_t nr, dr, nb, db;
+    jw_frac(kr, nr, dr);
+    jw_frac(kb, nb, db);
+    return (unsigned __int128)(num * nr) * db < (unsigned __int128)(den * nb) * dr;
+  }
+  if (M == M_COS) {  // num cos_r < den cos_best  <=>  num^2 dot_r^2 |x_b|^2 < den^2 dot_b^2 |x_r|^2
+    const uint64_t dr = kr >> 16, db = kb >> 16;
+    return (unsigned __int128)(num * num) * (dr * dr * (kb & 0xFFFFu)) <
+           (unsigned __int128)(den * den) * (db * db * (kr & 0xFFFFu));
+  }
   return num * (uint64_t)(kr >> 16) * (uint64_t)(kb & 0xFFFFu) <
          den * (uint64_t)(kb >> 16) * (uint64_t)(kr & 0xFFFFu);
 }
@@ -71,9 +108,13 @@ template <int M>
 struct SkipThr {
   uint64_t t, A, Bv;
   double rhs;
-  uint64_t den;
-  __device__ __forceinline__ void set(uint32_t kb, uint64_t num, uint64_t den_) {
+  uint64_t den, num;
+  uint32_t kb_;
+  __device__ __forceinline__ void set(uint32_t kb, uint64_t num_, uint64_t den_) {
     den = den_;
+    num = num_;
+    kb_ = kb;
+    const uint64_t num = num_;
     if (den == 0) return;
     if (M == M_U8) {
       const uint64_t x = num * (1ull + kb);
@@ -86,6 +127,7 @@ struct SkipThr {
     if (den == 0) return false;
     if (M == M_U8) return (uint64_t)kr >= t;
     if (M == M_F32) return __dmul_rn((double)den, __dadd_rn(1.0, (double)__uint_as_float(kr))) > rhs;
+    if (str_metric(M)) return skip_start<M>(kr, kb_, num, den);
     return A * (uint64_t)(kr >> 16) < Bv * (uint64_t)(kr & 0xFFFFu);
   }
 };
@@ -268,6 +310,11 @@ struct StoreView {
   const uint64_t *off;   // sets: [n+1]
   const uint32_t *tok;   // sets: sorted, unique tokens (16-byte aligned buffer, zeroed slack)
   int vwords;            // sets: words of a vocabulary bitmap covering every stored token (0: none)
+  // sets, partition-local view (K1 on a partitioned graph): [begin, end) token range of local index i at
+  // rng[i] (ids are then partition-local indices; off is not used), else null
+  const ulonglong2 *rng = nullptr;
+  // 2-gram cosine strings: |x|^2 = sum_g c_x(g)^2 of every stored string (>= 1), else null
+  const uint32_t *n2 = nullptr;
 };
 constexpr int VOCAB_SMEM_WORDS = 8192;   // vocabulary bitmaps up to 2^18 token ids live in smem
 
@@ -283,9 +330,65 @@ __device__ __forceinline__ uint32_t set_key(const uint32_t *a, int la, const uin
   return ((uint32_t)inter << 16) | (uint32_t)(la + lb - inter);
 }
 
-// Key of rows i and j of a store (single thread).
+// Key of string b as an entry of string a's row (single thread; a: the row owner / query).
+//  JW: matches in a's order, each a[i] taking the first free b[j] with |i - j| <= max(|a|,|b|)/2 - 1
+//      (free positions of b as a 128-bit mask); T = positions where the matched characters of a and
+//      of b, each in order, differ; l = common prefix (<= 4).  Key m | T<<7 | l<<14 | |a|<<17 | |b|<<24.
+//  COS: dot = pairs of equal 2-grams (a[i], a[i+1]) == (b[j], b[j+1]); key (dot << 16) | n2b, n2b =
+//      |b|^2 of the count vector (>= 1).
+template <int M>
+__device__ __forceinline__ uint32_t str_key(const uint32_t *a, int la, const uint32_t *b, int lb, uint32_t n2b) {
+  if (M == M_COS) {
+    uint32_t dot = 0;
+    for (int i = 0; i + 1 < la; ++i) {
+      const uint32_t a0 = a[i], a1 = a[i + 1];
+      uint32_t b0 = lb > 0 ? b[0] : 0u;
+      for (int j = 0; j + 1 < lb; ++j) {
+        const uint32_t b1 = b[j + 1];
+        dot += (a0 == b0) & (a1 == b1);
+        b0 = b1;
+      }
+    }
+    return (dot << 16) | n2b;
+  } else {
+    int w = (la > lb ? la : lb) / 2 - 1;
+    if (w < 0) w = 0;
+    uint32_t bfree[4] = {~0u, ~0u, ~0u, ~0u};   // b positions not yet matched
+    uint32_t amat[4] = {0u, 0u, 0u, 0u};         // a positions matched
+    int m = 0;
+    for (int i = 0; i < la; ++i) {
+      const uint32_t c = a[i];
+      const int lo = i - w > 0 ? i - w : 0, hi = i + w < lb - 1 ? i + w : lb - 1;
+      for (int j = lo; j <= hi; ++j) {
+        if (((bfree[j >> 5] >> (j & 31)) & 1u) && b[j] == c) {
+          bfree[j >> 5] &= ~(1u << (j & 31));
+          amat[i >> 5] |= 1u << (i & 31);
+          ++m;
+          break;
+        }
+      }
+    }
+    int T = 0, j = 0;
+    for (int i = 0; i < la; ++i) {
+      if (!((amat[i >> 5] >> (i & 31)) & 1u)) continue;
+      while ((bfree[j >> 5] >> (j & 31)) & 1u) ++j;   // next matched position of b
+      T += a[i] != b[j];
+      ++j;
+    }
+    int l = 0;
+    while (l < 4 && l < la && l < lb && a[l] == b[l]) ++l;
+    return (uint32_t)m | ((uint32_t)T << 7) | ((uint32_t)l << 14) | ((uint32_t)la << 17) | ((uint32_t)lb << 24);
+  }
+}
+
+// Key of rows i and j of a store (single thread; i owns the row).
 template <int M>
 __device__ __forceinline__ uint32_t pair_key(const StoreView &s, int64_t i, int64_t j) {
+  if (str_metric(M)) {
+    const uint64_t ai = s.off[i], bj = s.off[j];
+    return str_key<M>(s.tok + ai, (int)(s.off[i + 1] - ai), s.tok + bj, (int)(s.off[j + 1] - bj),
+                      M == M_COS ? s.n2[j] : 0u);
+  }
   if (M == M_JAC) {
     const uint64_t ai = s.off[i], bi = s.off[j];
     return set_key(s.tok + ai, (int)(s.off[i + 1] - ai), s.tok + bi, (int)(s.off[j + 1] - bi));
@@ -539,8 +642,14 @@ struct SetQuery {
     for (int j = 0; j < NS; ++j) {
       uint64_t b = 0, e = 0;
       if (cand[j] >= 0) {
-        b = s.off[cand[j]];
-        e = s.off[cand[j] + 1];
+        if (s.rng) {
+          const ulonglong2 r = s.rng[cand[j]];
+          b = r.x;
+          e = r.y;
+        } else {
+          b = s.off[cand[j]];
+          e = s.off[cand[j] + 1];
+        }
       }
       a0[j] = b & ~3ull;
       rb[j] = (int)(b - a0[j]);
@@ -630,9 +739,63 @@ struct SetQuery {
   }
 };
 
+// Strings (M_JW / M_COS): the query's characters in shared scratch (QSCR words >= STR_MAX), one lane per
+// candidate, its characters read from global memory (str_key).  n2 of a candidate from StoreView::n2.
+template <int M>
+struct StrQuery {
+  const uint32_t *q;
+  int qn;
+  uint32_t qn2;   // COS: the query's own |q|^2 (a key of the query as another row's entry)
+  __device__ __forceinline__ void load(const StoreView &s, int64_t r, uint32_t *scratch) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t b = s.off[r];
+    qn = (int)(s.off[r + 1] - b);
+    qn2 = (M == M_COS && s.n2) ? s.n2[r] : 0u;
+    if (scratch) {
+      for (int i = lane; i < qn; i += 32) scratch[i] = s.tok[b + i];
+      __syncwarp();
+      q = scratch;
+    } else {
+      q = s.tok + b;
+    }
+  }
+  // key of candidate cand (lane-local; cand < 0: 0)
+  __device__ __forceinline__ uint32_t key(const StoreView &s, int32_t cand) const {
+    if (cand < 0) return 0u;
+    uint64_t b, e;
+    if (s.rng) {
+      const ulonglong2 r = s.rng[cand];
+      b = r.x;
+      e = r.y;
+    } else {
+      b = s.off[cand];
+      e = s.off[cand + 1];
+    }
+    return str_key<M>(q, qn, s.tok + b, (int)(e - b), M == M_COS ? s.n2[cand] : 0u);
+  }
+  __device__ __forceinline__ uint32_t eval(const StoreView &s, int32_t cand, int n) const {
+    return key(s, (threadIdx.x & 31) < n ? cand : -1);
+  }
+  // the query as an entry of node v's row (the update's proposals): v owns the key
+  __device__ __forceinline__ uint32_t rkey(const StoreView &s, int32_t v) const {
+    if (v < 0) return 0u;
+    const uint64_t b = s.off[v];
+    return str_key<M>(s.tok + b, (int)(s.off[v + 1] - b), q, qn, qn2);
+  }
+  __device__ __forceinline__ void eval2(const StoreView &s, int32_t ca, int32_t cb, uint32_t &oa, uint32_t &ob) const {
+    oa = key(s, ca);
+    ob = key(s, cb);
+  }
+  __device__ __forceinline__ uint32_t eval_smem(const uint8_t *, int, int) const { return 0u; }
+};
+
 template <int M, int L, int CPL>
 struct QuerySel { typedef VecQuery<M, L, CPL> T; };
 template <int L, int CPL>
 struct QuerySel<M_JAC, L, CPL> { typedef SetQuery<L> T; };
+template <int L, int CPL>
+struct QuerySel<M_JW, L, CPL> { typedef StrQuery<M_JW> T; };
+template <int L, int CPL>
+struct QuerySel<M_COS, L, CPL> { typedef StrQuery<M_COS> T; };
 
 }  // namespace knng

@@ -60,9 +60,16 @@ struct knng_graph {
   bool own_stream = false;
   uint8_t *vec = nullptr;                       // vectors (u8 / f32 rows)
   uint64_t *off = nullptr;                      // sets: [cap+1] offsets into tok
-  uint32_t *tok = nullptr;                      // sets: tokens
+  uint32_t *tok = nullptr;                      // sets: tokens (strings: characters)
+  uint32_t *sn2 = nullptr;                      // 2-gram cosine strings: |x|^2 of every stored string [cap]
   int64_t tok_cap = 0, tok_n = 0;               // token capacity / tokens in use (host mirror)
-  int2 *lrows = nullptr;                        // partitioned: [cap][k] (id, partition-local index or -1 across)
+  // partitioned graphs: the partition-local store K1 reads (index = (p, local index), member_cap = cap rows per
+  // partition): prow [P][cap][k] local index of each row entry in the row owner's partition (-1 across),
+  // pvec [P][cap][stride] the vectors (vector metrics), pset [P][cap] the [begin, end) token ranges (sets)
+  int32_t *prow = nullptr;
+  uint8_t *pvec = nullptr;
+  ulonglong2 *pset = nullptr;
+  int local_P = 0;                              // partitions the local store is allocated for
   uint32_t tok_max = 0;
   int64_t tprof_n = 0;                          // KNNG_PROFILE: tasks of the last search                         // largest stored token (valid when tok_n > 0)
   int32_t *ids = nullptr;
@@ -79,7 +86,7 @@ struct knng_graph {
   // workspaces
   DBuf w_bits, w_cand_i, w_cand_k, w_C_i, w_C_k, w_hash, w_list, w_props, w_prop_cnt, w_sorted, w_stats,
       w_target, w_query, w_starts;
-  DBuf w_qoff, w_qtok;
+  DBuf w_qoff, w_qtok, w_qn2;
   knng::DenseScratch w_dense;                    // A0 / A5 partial rows and norms
   // multi-GPU (knng_runtime.world > 1, or a 1-rank communicator for tests): the library's NCCL
   // communicator and the buffers of the two all-gathers of graph_insert_batch
@@ -104,7 +111,17 @@ inline knng::StoreView graph_store_view(const knng_graph *g) {
   v.nchunks = g->geom.nchunks;
   v.off = g->off;
   v.tok = g->tok;
+  v.n2 = g->sn2;
   const int64_t vw = g->tok_n > 0 ? ((int64_t)g->tok_max + 32) / 32 : 0;
   v.vwords = (g->metric == KNNG_JACCARD_U32SET && vw > 0 && vw <= knng::VOCAB_SMEM_WORDS) ? (int)vw : 0;
   return v;
+}
+
+inline knng::LocalStore graph_local_store(const knng_graph *g) {
+  knng::LocalStore ls;
+  ls.prow = g->prow;
+  ls.pvec = g->pvec;
+  ls.pset = g->pset;
+  ls.cap = g->cap;
+  return ls;
 }

@@ -81,8 +81,11 @@ struct SearchArgs {
   const int64_t *member_cnt;   // [P] (device)
   const uint8_t *part_of;      // [cap]
   const int32_t *local_idx;    // [cap]
-  const int2 *lrows;           // [cap][k]: (id, local index of the entry in the row owner's partition, or -1
-                               // when the entry lies in another partition) -- the row K1 walks when P > 0
+  // the partition-local store (P > 0): K1 draws, walks and ranks partition-local indices and converts its
+  // top-k to ids through members at the end (members[p] is ascending, so ties by local index are ties by id)
+  const int32_t *prow;         // [P][member_cap][k]: local index of each entry in the row owner's partition, -1 across
+  const uint8_t *pvec;         // [P][member_cap][stride] (vector metrics)
+  const ulonglong2 *pset;      // [P][member_cap] token ranges (sets)
   // parameters
   double speedup;
   uint64_t e_num, e_den, seed;
@@ -146,11 +149,17 @@ cudaError_t launch_update_one(const VecGeom &g, const BallArgs &a, const uint32_
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
                                int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted,
-                               cudaStream_t s, int *n_launch, int2 *lrows = nullptr,
+                               cudaStream_t s, int *n_launch, int32_t *prow = nullptr, int64_t member_cap = 0,
                                const uint8_t *part_of = nullptr, const int32_t *local_idx = nullptr);
-// lrows of rows [first, first + count): partition-local index of each entry, -1 across partitions
-cudaError_t launch_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
-                         const int32_t *local_idx, int2 *lrows, cudaStream_t s);
+// the partition-local store of nodes [first, first + count) (rows, and vectors or token ranges)
+struct LocalStore {
+  int32_t *prow;
+  uint8_t *pvec;
+  ulonglong2 *pset;
+  int64_t cap;
+};
+cudaError_t launch_local_store(const StoreView &st, const int32_t *ids, int k, int64_t first, int64_t count,
+                               const uint8_t *part_of, const int32_t *local_idx, const LocalStore &ls, cudaStream_t s);
 cudaError_t exclusive_scan_i32(const int32_t *in, int32_t *out, int32_t *tmp, int64_t n, cudaStream_t s);
 cudaError_t launch_tc_topk_u8(const VecGeom &g, const uint8_t *vec, int64_t row0, int64_t nrows, int64_t col0,
                               int64_t ncols, int k, const int32_t *sid, const uint32_t *skey, int64_t ny, int32_t *pi,

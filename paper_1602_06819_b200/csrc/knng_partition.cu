@@ -296,9 +296,27 @@ static int build_members(knng_graph *g, int32_t *flag, int32_t *scan, int32_t *t
     cnt[p] = (int64_t)last[0] + last[1];
   }
   CK(cudaMemcpyAsync(g->member_cnt, cnt.data(), sizeof(int64_t) * g->P, cudaMemcpyHostToDevice, g->stream));
-  // the rows' partition-local view, read by the partition-local walks of K1
-  if (!g->lrows) CK(cudaMalloc((void **)&g->lrows, (size_t)g->cap * g->k * 8));
-  CK(launch_lrows(g->ids, g->k, 0, n, g->part_of, g->local_idx, g->lrows, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  return 0;
+}
+
+// the partition-local store K1 reads (rows, and vectors or token ranges, at (p, local index)), for the
+// installed partition of nodes 0..n-1
+static int build_local_store(knng_graph *g) {
+  if (g->local_P != g->P) {
+    if (g->prow) cudaFree(g->prow);
+    if (g->pvec) cudaFree(g->pvec);
+    if (g->pset) cudaFree(g->pset);
+    g->prow = nullptr; g->pvec = nullptr; g->pset = nullptr;
+    g->local_P = 0;
+    const size_t rows = (size_t)g->P * g->cap;
+    CK(cudaMalloc((void **)&g->prow, rows * g->k * 4));
+    if (g->metric == KNNG_JACCARD_U32SET) CK(cudaMalloc((void **)&g->pset, rows * sizeof(ulonglong2)));
+    else CK(cudaMalloc((void **)&g->pvec, rows * g->geom.stride));
+    g->local_P = g->P;
+  }
+  CK(launch_local_store(graph_store_view(g), g->ids, g->k, 0, g->n, g->part_of, g->local_idx, graph_local_store(g),
+                        g->stream));
   CK(cudaStreamSynchronize(g->stream));
   return 0;
 }
@@ -434,6 +452,8 @@ extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, in
                                   const int32_t *init_medoids) {
   knng_err_slot().clear();
   if (!g) return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: null graph");
+  if (g->metric == KNNG_JARO_WINKLER || g->metric == KNNG_COSINE_2GRAM)
+    return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: string metrics run on unpartitioned graphs");
   if (P < 1 || P > 255) return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: P=%d outside 1..255", P);
   if (!(imbalance >= 1.0)) return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: imbalance < 1");
   if (max_iter < 1) return fail(KNNG_ERR_INVALID_ARG, "partition_kmedoids: max_iter < 1");
@@ -515,6 +535,7 @@ extern "C" int partition_kmedoids(knng_graph *g, int32_t P, double imbalance, in
   CK(cudaMemcpyAsync(g->part_of, w.wacc.p, (size_t)n, cudaMemcpyDeviceToDevice, s));
   g->P = P;
   if (int r = build_members(g, w.wflag.as<int32_t>(), w.wscan.as<int32_t>(), w.wtmp.as<int32_t>())) return r;
+  if (int r = build_local_store(g)) return r;
   install_medoids(g, med);
   memcpy(medoids_out, med.data(), (size_t)P * 4);
   if (part_out) CK(cudaMemcpyAsync(part_out, g->part_of, (size_t)n, cudaMemcpyDeviceToHost, s));

@@ -122,8 +122,8 @@ __device__ __forceinline__ uint32_t staged_keys(const typename QuerySel<M, L, CP
                                                 const uint8_t *stage, int pitch, int nck, int nrows, bool lane_form,
                                                 bool swz) {
   const int lane = threadIdx.x & 31;
-  if constexpr (M == M_JAC) {
-    return 0u;   // (sets are evaluated per lane by the callers)
+  if constexpr (csr_metric(M)) {
+    return 0u;   // (sets and strings are evaluated per lane by the callers)
   } else {
     if (lane_form) {
       const int r = lane < nrows ? lane : 0;
@@ -157,7 +157,9 @@ cudaError_t launch_keymat(int metric, const StoreView &st, int64_t qrow0, int64_
   const dim3 grid((unsigned)((n0 + B + 127) / 128), (unsigned)B);
   if (metric == M_U8) k_keymat<M_U8><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
   else if (metric == M_F32) k_keymat<M_F32><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
-  else k_keymat<M_JAC><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
+  else if (metric == M_JAC) k_keymat<M_JAC><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
+  else if (metric == M_JW) k_keymat<M_JW><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
+  else k_keymat<M_COS><<<grid, 128, 0, s>>>(st, qrow0, n0, B, ld, out);
   return cudaGetLastError();
 }
 
@@ -201,13 +203,12 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   constexpr bool LF = NCK > 0;                                             // one lane per staged row
   constexpr bool SWZ = LF && NCK % 8 == 0;
   const bool part = PART < 0 ? a.P > 0 : PART == 1;
-  const int nck = M == M_JAC ? 0 : (LF ? NCK : a.st.nchunks);
+  const int nck = csr_metric(M) ? 0 : (LF ? NCK : a.st.nchunks);
   const int pitch = LF ? (SWZ ? NCK * 16 : NCK * 16 + 16) : a.pitch;
-  const int EB = part ? 8 : 4;                                             // bytes of a walked row entry
-  const int RB = EB * k;                                                   // bytes of a walked row
+  const int RB = 4 * k;                                                    // bytes of a walked row (local indices)
   const bool row_pf = KT == 0 && a.row_pf != 0;                           // (KT: rows are loaded, keys looked up)
   const bool es = KT || a.e_smem != 0;                                     // E bitmap in shared memory
-  const bool ns2 = !KT && M != M_JAC && es && a.ns2 != 0;                  // two chunk stages (needs es)
+  const bool ns2 = !KT && !csr_metric(M) && es && a.ns2 != 0;                  // two chunk stages (needs es)
   const bool xs = es && (KT || a.x_smem != 0);                             // X bitmap in shared memory too
   // ---- this warp's shared memory (a.wbytes each; search_warp_bytes) ----
   uint8_t *wsm = smem + (size_t)warp * a.wbytes;
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   uint32_t *pkey = (uint32_t *)(qsm + 512);                                // [32] pending walk evaluations
   int32_t *pid = (int32_t *)(pkey + 32);                                   // [32]
   uint32_t *qscr = (uint32_t *)(pid + 32);                                 // [QSCR] query tokens + table (sets)
-  uint32_t *ebits = qscr + (M == M_JAC ? QSCR : 0);                        // [e_bytes / 4] E bitmap (es)
+  uint32_t *ebits = qscr + (csr_metric(M) ? QSCR : 0);                       // [e_bytes / 4] E bitmap (es)
   long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   // from it instead of gathering rows (same keys, same decisions, same counters).
   uint32_t *kt = nullptr;
   if constexpr (KT != 0) {   // row `it` of the sequence's key matrix (k_keymat) into shared memory
-    kt = (uint32_t *)(smem + (size_t)WPC * a.wbytes + 8 * WPC + fuse_bytes(a, M == M_JAC));
+    kt = (uint32_t *)(smem + (size_t)WPC * a.wbytes + 8 * WPC + fuse_bytes(a, csr_metric(M)));
     const uint32_t *src = a.ktm + (size_t)it * a.ktm_ld;
     const int64_t n4 = n_t >> 2;
 #pragma unroll 4
@@ -252,7 +253,14 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     const int pl = (int)(task % Pn);          // output slot
     const int p = a.route ? a.route[b] : a.part_lo + pl;   // partition searched
     const int64_t m = part ? a.member_cnt[p] : n_t;
-    const int32_t *pool = part ? a.members + (size_t)p * a.member_cap : nullptr;
+    // the pool's store: on a partitioned graph the partition-local copy (index = local index, the pool
+    // index of the draws); ids are converted through members when the task writes its top-k
+    const size_t pbase = part ? (size_t)p * a.member_cap : 0;
+    const uint8_t *vbase = (part && !csr_metric(M)) ? a.pvec + pbase * a.st.stride : a.st.vec;
+    const int32_t *rbase = part ? a.prow + pbase * k : a.rows;
+    StoreView sv = a.st;
+    sv.vec = vbase;
+    if (csr_metric(M) && part) sv.rng = a.pset + pbase;
     // next task (dynamic scheduling), read back at the end of this one
     if (lane == 0) sched[warp] = (long long)(gridDim.x * WPC + atomicAdd(a.task_ctr, 1ull));
     KPROF(const long long tc0 = clock64(); long long c_walk = 0; unsigned long long c_win = 0, c_steps = 0,
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     if (budget > m) budget = m;
 
     typename QuerySel<M, L, CPL>::T Q;
-    if (!LF && KT == 0) Q.load(a.qs, qrow0 + b, M == M_JAC ? qscr : nullptr);
+    if (!LF && KT == 0) Q.load(a.qs, qrow0 + b, csr_metric(M) ? qscr : nullptr);
     if (LF) {
       const uint8_t *qg = a.qs.vec + (size_t)(qrow0 + b) * a.qs.stride;
       for (int cc = lane; cc < nck; cc += 32) *(uint4 *)(qsm + 16 * cc) = ldg16(qg + 16 * cc);
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         return make_int2(nd, nd);
       }
       const uint64_t idx = rng_index(h3, (uint64_t)j, (uint64_t)m);
-      return make_int2((int32_t)idx, pool ? __ldg(pool + idx) : (int32_t)idx);
+      return make_int2((int32_t)idx, (int32_t)idx);
     };
     // ---- the draw of a chunk: issue(d) copies the drawn rows into the stage (sets: each lane its token
     // range) and returns the E word of each draw, read in the same round trip.
@@ -312,15 +320,17 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     auto issue = [&](int2 d, uint64_t tb, uint64_t te) -> uint32_t {
       if constexpr (KT != 0) {
         return 0u;
+      } else if constexpr (str_metric(M)) {
+        // strings: keys are computed per lane from global memory (StrQuery)
       } else if constexpr (M == M_JAC) {
         const uint64_t a0 = tb & ~3ull;
         const int nch = d.x >= 0 ? ((int)(te - a0) + 3) >> 2 : 0;
         if (nch <= SetQuery<L>::SLOTCH)
           for (int jj = 0; jj < nch; ++jj) cpa16(sb0 + lane * pitch + 16 * jj, a.st.tok + a0 + 4 * jj);
       } else if constexpr (LF) {
-        gather_lf<NCK>(sb0, pitch, a.st.vec, d.y, 32);
+        gather_lf<NCK>(sb0, pitch, vbase, d.y, 32);
       } else {
-        const uint8_t *base = a.st.vec;
+        const uint8_t *base = vbase;
         const size_t stride = a.st.stride;
         for (int e = lane; e < 32 * nck; e += 32) {
           const int r = e / nck, t = e - r * nck;
@@ -338,26 +348,35 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     auto e_smem_test = [&](int32_t i) -> bool { return ((ebits[i >> 5] >> (i & 31)) & 1u) != 0; };
     uint32_t *xbits = ebits + (a.e_bytes >> 2);  // xs: the X bitmap follows the E bitmap
     auto issue_to = [&](uint8_t *dst, int2 d) {
-      if constexpr (M != M_JAC && KT == 0) {
+      if constexpr (!csr_metric(M) && KT == 0) {
         if constexpr (LF) {
-          gather_lf<NCK>(smem_u32(dst), pitch, a.st.vec, d.y, 32);
+          gather_lf<NCK>(smem_u32(dst), pitch, vbase, d.y, 32);
         } else {
           const unsigned sb = smem_u32(dst);
           for (int e = lane; e < 32 * nck; e += 32) {
             const int r = e / nck, t = e - r * nck;
             const int32_t id = __shfl_sync(FULL, d.y, r);
-            if (id >= 0) cpa16(sb + r * pitch + 16 * t, a.st.vec + (size_t)id * a.st.stride + 16 * t);
+            if (id >= 0) cpa16(sb + r * pitch + 16 * t, vbase + (size_t)id * a.st.stride + 16 * t);
           }
         }
       }
     };
     auto offs = [&](int2 d, uint64_t &tb, uint64_t &te) {
       tb = te = 0;
-      if (M == M_JAC && d.x >= 0) { tb = a.st.off[d.y]; te = a.st.off[d.y + 1]; }
+      if (M == M_JAC && d.x >= 0) {
+        if (part) {
+          const ulonglong2 r = sv.rng[d.y];
+          tb = r.x;
+          te = r.y;
+        } else {
+          tb = a.st.off[d.y];
+          te = a.st.off[d.y + 1];
+        }
+      }
     };
     // keys of staged rows (lane r: slot r; lanes >= nrows read slot 0 and are masked by the callers)
     auto keys_of = [&](const uint8_t *stg, int nrows) -> uint32_t {
-      if constexpr (M == M_JAC) {
+      if constexpr (csr_metric(M)) {
         return 0u;
       } else if constexpr (LF) {
         const int r = lane < nrows ? lane : 0;
@@ -424,6 +443,8 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         const bool ok = wl >= 0;
         if constexpr (KT != 0) {
           wkey = ok ? kt[wl] : 0u;
+        } else if constexpr (str_metric(M)) {
+          wkey = ok ? Q.key(sv, wnode) : 0u;
         } else if constexpr (M == M_JAC) {
           wkey = 0;
           if (ok) {
@@ -472,7 +493,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           const int r = __popc(cmk & lanemask_lt());
           if (cand && r < WPF) {
             wslot = r;
-            const uint8_t *src = (part ? (const uint8_t *)a.lrows : (const uint8_t *)a.rows) + (size_t)wnode * RB;
+            const uint8_t *src = (const uint8_t *)rbase + (size_t)wnode * RB;
             const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4);
             for (int u = 0; u < RB; u += CU) cpa_n(smem_u32(wrow) + r * RB + u, src + u, CU);
           }
@@ -552,7 +573,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       int rs = -1;                               // cur's row in rowbuf slot rs (row_pf)
       int rw = __shfl_sync(FULL, wslot, al);     // ... or in window slot rw
       bool have_nr = false;                      // ... or in nr (loaded after the move)
-      int2 nr = make_int2(-1, -1);
+      int32_t nr = -1;
       int pn = 0;
       auto flush = [&]() {
         if (pn == 0) return;
@@ -576,21 +597,16 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         }
         int32_t v = -1, vl = -1;
         if (lane < k) {
-          int2 e2;
-          if (rw >= 0) {
-            e2 = part ? ((const int2 *)(wrow + rw * RB))[lane] : make_int2(((const int32_t *)(wrow + rw * RB))[lane], 0);
-          } else if (rs >= 0) {
-            e2 = part ? ((const int2 *)(rowbuf + rs * RB))[lane] : make_int2(((const int32_t *)(rowbuf + rs * RB))[lane], 0);
-          } else if (have_nr) {
-            e2 = nr;
-          } else {
-            e2 = part ? __ldg(a.lrows + (size_t)cur * k + lane) : make_int2(__ldg(a.rows + (size_t)cur * k + lane), 0);
-          }
-          v = e2.x;
-          vl = part ? e2.y : e2.x;
+          int32_t e2;
+          if (rw >= 0) e2 = ((const int32_t *)(wrow + rw * RB))[lane];
+          else if (rs >= 0) e2 = ((const int32_t *)(rowbuf + rs * RB))[lane];
+          else if (have_nr) e2 = nr;
+          else e2 = __ldg(rbase + (size_t)cur * k + lane);
+          v = e2;
+          vl = e2;
         }
         rw = -1;
-        // Q10: neighbours in another partition are skipped (lrows holds -1 for them)
+        // Q10: neighbours in another partition are skipped (prow holds -1 for them)
         const bool inpool = v >= 0 && vl >= 0;
         const int32_t lv = inpool ? vl : 0;
         __syncwarp();                            // rowbuf read before the copies below overwrite it
@@ -599,11 +615,11 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         if constexpr (KT != 0) {
           // keys from the table
         } else if constexpr (LF) {
-          gather_lf<NCK>(smem_u32(wvec), pitch, a.st.vec, inpool ? v : -1, k);
+          gather_lf<NCK>(smem_u32(wvec), pitch, vbase, inpool ? v : -1, k);
           if (row_pf) {
             const unsigned rb0 = smem_u32(rowbuf);
             const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4), NU = RB / CU;
-            const uint8_t *rsrc = part ? (const uint8_t *)a.lrows : (const uint8_t *)a.rows;
+            const uint8_t *rsrc = (const uint8_t *)rbase;
             for (int e0 = 0; e0 < k * NU; e0 += 32) {
               const int e = e0 + lane, t = e / NU, u = e - t * NU;
               const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t & 31);
@@ -613,7 +629,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         } else if (row_pf) {
           const unsigned rb0 = smem_u32(rowbuf);
           const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4), NU = RB / CU;
-          const uint8_t *rsrc = part ? (const uint8_t *)a.lrows : (const uint8_t *)a.rows;
+          const uint8_t *rsrc = (const uint8_t *)rbase;
           for (int t0 = 0; t0 < k; t0 += 16) {
             const int t = t0 + (lane & 15);
             const int32_t vt = __shfl_sync(FULL, inpool ? v : -1, t & 31);
@@ -630,7 +646,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           __syncwarp();
           key = keys_of(wvec, k);
         } else {
-          key = Q.eval(a.st, inpool ? v : -1, k);
+          key = Q.eval(sv, inpool ? v : -1, k);
           cp_async_wait_all();
           __syncwarp();
         }
@@ -661,7 +677,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         // the move (if any) is known: its row is loaded now, under the bookkeeping below
         const int32_t ncur = __shfl_sync(FULL, v, fi);
         if (!row_pf && im && !mv_x && lane < k)
-          nr = part ? __ldg(a.lrows + (size_t)ncur * k + lane) : make_int2(__ldg(a.rows + (size_t)ncur * k + lane), 0);
+          nr = __ldg(rbase + (size_t)ncur * k + lane);
         unsigned fm2 = __ballot_sync(FULL, !evb2) & range;
         bool hit2 = false;
         if ((int64_t)__popc(fm2) > budget - c) { fm2 = first_bits(fm2, (int)(budget - c)); hit2 = true; }
@@ -715,7 +731,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     s_evals += c;
     if (lane < a.kr) {
       const size_t o = ((size_t)b * Pn + pl) * a.kr + lane;
-      a.out_ids[o] = lane < top.cnt ? top.id : -1;
+      a.out_ids[o] = lane < top.cnt ? (part ? a.members[pbase + top.id] : top.id) : -1;
       a.out_keys[o] = lane < top.cnt ? top.key : 0u;
     }
     cp_async_wait_all();
@@ -731,7 +747,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       BallArgs ub = a.ub;
       ub.n_t = n_t;
       int nb = 0, np = 0;
-      update_one_warp<M, L, CPL>(ub, a.out_ids, a.out_keys, usm, (int *)us, M == M_JAC ? uq : nullptr, &nb, &np, kt);
+      update_one_warp<M, L, CPL>(ub, a.out_ids, a.out_keys, usm, (int *)us, csr_metric(M) ? uq : nullptr, &nb, &np, kt);
       s_ball += (unsigned)nb;
       s_prop += (unsigned)np;
     }
@@ -784,7 +800,7 @@ __global__ void k_merge_parts(const int32_t *ci, const uint32_t *ck, int64_t nq,
 
 // shared memory of one warp of K1 (the kernel's carve-up above)
 size_t search_warp_bytes(const SearchArgs &a, bool sets) {
-  const size_t RB = (size_t)(a.P > 0 ? 8 : 4) * a.k;
+  const size_t RB = (size_t)4 * a.k;
   const bool ns2 = !sets && a.e_smem && a.ns2;
   size_t b = (size_t)(ns2 ? 64 : 32) * a.pitch + (a.row_pf ? ((a.k * RB + 15) & ~(size_t)15) : 0) +
              ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QSCR * 4 : 0) +
@@ -846,8 +862,8 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   if (T == 0) return cudaSuccess;
-  a.wbytes = (int)search_warp_bytes(a, M == M_JAC);
-  const size_t smem = search_smem_bytes(a, M == M_JAC);
+  a.wbytes = (int)search_warp_bytes(a, csr_metric(M));
+  const size_t smem = search_smem_bytes(a, csr_metric(M));
   // persistent grid: the CTAs that fit at once (dynamic task scheduling balances the tail)
   int per_sm = 0, nsm = 148;
   if (cudaError_t oe = k1_occupancy<M, L, CPL, MB, NCK, PART, KT>(smem, &per_sm, &nsm)) return oe;
@@ -877,7 +893,7 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
 #define KNNG_LF_SHAPES(X) X(M_U8, 8, 1, 8) X(M_U8, 2, 1, 2) X(M_F32, 8, 3, 24)
 
 bool search_lane_form(const VecGeom &g, int lane_eval) {
-  return lane_eval && g.metric != M_JAC && lane_eval_ok(g.metric, g.nchunks);
+  return lane_eval && !csr_metric(g.metric) && lane_eval_ok(g.metric, g.nchunks);
 }
 
 cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s, int *n_launch) {
@@ -888,6 +904,8 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
     KNNG_SHAPES(X, M_U8)
     KNNG_SHAPES_F32(X)
     X(M_JAC, 8, 1)
+    X(M_JW, 8, 1)
+    X(M_COS, 8, 1)
 #undef X
     return cudaErrorInvalidValue;
   }
@@ -903,13 +921,15 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
+  X(M_JW, 8, 1)
+  X(M_COS, 8, 1)
 #undef X
   return cudaErrorInvalidValue;
 }
 
 template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
 static cudaError_t resident(SearchArgs a, int64_t *warps) {
-  const size_t smem = search_smem_bytes(a, M == M_JAC);
+  const size_t smem = search_smem_bytes(a, csr_metric(M));
   int per_sm = 0, nsm = 148;
   if (cudaError_t e = k1_occupancy<M, L, CPL, MB, NCK, PART, KT>(smem, &per_sm, &nsm)) return e;
   *warps = (int64_t)per_sm * nsm * WPC;
@@ -923,6 +943,8 @@ cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t
     KNNG_SHAPES(X, M_U8)
     KNNG_SHAPES_F32(X)
     X(M_JAC, 8, 1)
+    X(M_JW, 8, 1)
+    X(M_COS, 8, 1)
 #undef X
     return cudaErrorInvalidValue;
   }
@@ -938,6 +960,8 @@ cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
+  X(M_JW, 8, 1)
+  X(M_COS, 8, 1)
 #undef X
   return cudaErrorInvalidValue;
 }
@@ -948,7 +972,9 @@ cudaError_t launch_merge_parts(int metric, const int32_t *ci, const uint32_t *ck
   const unsigned blocks = (unsigned)((nq + 3) / 4);
   if (metric == M_U8) k_merge_parts<M_U8><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
   else if (metric == M_F32) k_merge_parts<M_F32><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
-  else k_merge_parts<M_JAC><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
+  else if (metric == M_JAC) k_merge_parts<M_JAC><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
+  else if (metric == M_JW) k_merge_parts<M_JW><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
+  else k_merge_parts<M_COS><<<blocks, 128, 0, s>>>(ci, ck, nq, P, world, kr, oi, ok);
   return cudaGetLastError();
 }
 

@@ -50,9 +50,12 @@ cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, 
                             int k, const int32_t *Ci, const uint32_t *Ck, int32_t *oi, uint32_t *ok, DenseScratch *ws,
                             cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  if (g.metric != M_JAC)   // vectors: the smem-tiled kernel of the exact build, seeded with C_i
+  if (!csr_metric(g.metric))   // vectors: the smem-tiled kernel of the exact build, seeded with C_i
     return launch_tile_topk(g, st.vec, n_t + q_lo, nq, n_t, B, k, Ci, Ck, oi, ok, ws, s);
-  k_allpairs<M_JAC><<<(unsigned)((nq + 3) / 4), 128, 0, s>>>(st, n_t, B, q_lo, nq, k, Ci, Ck, oi, ok);
+  const unsigned nb = (unsigned)((nq + 3) / 4);
+  if (g.metric == M_JAC) k_allpairs<M_JAC><<<nb, 128, 0, s>>>(st, n_t, B, q_lo, nq, k, Ci, Ck, oi, ok);
+  else if (g.metric == M_JW) k_allpairs<M_JW><<<nb, 128, 0, s>>>(st, n_t, B, q_lo, nq, k, Ci, Ck, oi, ok);
+  else k_allpairs<M_COS><<<nb, 128, 0, s>>>(st, n_t, B, q_lo, nq, k, Ci, Ck, oi, ok);
   return cudaGetLastError();
 }
 
@@ -65,7 +68,7 @@ cudaError_t launch_allpairs(const VecGeom &g, const StoreView &st, int64_t n_t, 
 template <int M, int L, int CPL>
 __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
   __shared__ int s_n[4];
-  __shared__ uint32_t qscr[M == M_JAC ? 4 * QSCR : 1];
+  __shared__ uint32_t qscr[csr_metric(M) ? 4 * QSCR : 1];
   extern __shared__ int32_t bsm[];   // small balls: [4][hcap] hash + [4][ballmax] list in shared memory
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * 4 + wib, nw = (int64_t)gridDim.x * 4;
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
     if (lane == 0) s_n[wib] = 0;
     __syncwarp();
     typename QuerySel<M, L, CPL>::T Q;
-    Q.load(a.st, a.n_t + b, M == M_JAC ? qscr + wib * QSCR : nullptr);
+    Q.load(a.st, a.n_t + b, csr_metric(M) ? qscr + wib * QSCR : nullptr);
     const int32_t idx = (int32_t)(a.n_t + b);
     // L1 = the search result C(x)
     {
@@ -107,7 +110,9 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
           }
         }
         const int cnt = hi - base < 32 ? hi - base : 32;
-        const uint32_t key = Q.eval(a.st, v, cnt);
+        uint32_t key;
+        if constexpr (str_metric(M)) key = Q.rkey(a.st, v);   // strings: v's own key of the new point (v's row)
+        else key = Q.eval(a.st, v, cnt);
         bool prop = false;
         if (v >= 0) {
           const uint32_t kk = a.keys[(size_t)v * k + k - 1];
@@ -144,9 +149,9 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
 template <int M, int L, int CPL>
 __global__ void __launch_bounds__(32) k_update_one(BallArgs a, const uint32_t *Ckeys) {
   extern __shared__ int32_t usm[];
-  __shared__ uint32_t qscr[M == M_JAC ? QSCR : 1];
+  __shared__ uint32_t qscr[csr_metric(M) ? QSCR : 1];
   __shared__ int s_n;
-  update_one_warp<M, L, CPL>(a, a.C, Ckeys, usm, &s_n, M == M_JAC ? qscr : nullptr, nullptr, nullptr);
+  update_one_warp<M, L, CPL>(a, a.C, Ckeys, usm, &s_n, csr_metric(M) ? qscr : nullptr, nullptr, nullptr);
 }
 
 template <int M, int L, int CPL>
@@ -182,6 +187,8 @@ cudaError_t launch_update_one(const VecGeom &g, const BallArgs &a, const uint32_
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
+  X(M_JW, 8, 1)
+  X(M_COS, 8, 1)
 #undef X
   return cudaErrorInvalidValue;
 }
@@ -192,6 +199,8 @@ cudaError_t launch_ball(const VecGeom &g, const BallArgs &a, int64_t nslots, cud
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
+  X(M_JW, 8, 1)
+  X(M_COS, 8, 1)
 #undef X
   return cudaErrorInvalidValue;
 }
@@ -301,8 +310,8 @@ __global__ void k_prop_scatter(const int2 *props, const int32_t *prop_cnt, int b
 
 template <int M>
 __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, int32_t *ncnt, int32_t *nfill,
-                             const int32_t *noff, const int2 *sorted, int2 *lrows, const uint8_t *part_of,
-                             const int32_t *local_idx) {
+                             const int32_t *noff, const int2 *sorted, int32_t *prow, int64_t member_cap,
+                             const uint8_t *part_of, const int32_t *local_idx) {
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n_t) return;
   const int c = ncnt[v];
@@ -326,11 +335,12 @@ __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, i
     ri[pos] = id;
   }
   for (int e = 0; e < k; ++e) { ids[v * k + e] = ri[e]; keys[v * k + e] = rk[e]; }
-  if (lrows) {   // partitioned: keep the row's partition-local view current (new ids are placed already)
+  if (prow) {   // partitioned: keep the row's partition-local copy current (new ids are placed already)
     const uint8_t pv = part_of[v];
+    int32_t *lr = prow + ((size_t)pv * member_cap + local_idx[v]) * k;
     for (int e = 0; e < k; ++e) {
       const int32_t u = ri[e];
-      lrows[v * k + e] = make_int2(u, (u >= 0 && part_of[u] == pv) ? local_idx[u] : -1);
+      lr[e] = (u >= 0 && part_of[u] == pv) ? local_idx[u] : -1;
     }
   }
   ncnt[v] = 0;
@@ -340,7 +350,8 @@ __global__ void k_node_merge(int32_t *ids, uint32_t *keys, int k, int64_t n_t, i
 cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, int64_t n_t, int64_t B,
                                const int2 *props, const int32_t *prop_cnt, int ballmax, int32_t *ncnt,
                                int32_t *nfill, int32_t *noff, int32_t *scan_tmp, int2 *sorted, cudaStream_t s,
-                               int *n_launch, int2 *lrows, const uint8_t *part_of, const int32_t *local_idx) {
+                               int *n_launch, int32_t *prow, int64_t member_cap, const uint8_t *part_of,
+                               const int32_t *local_idx) {
   if (B == 0) return cudaSuccess;
   k_prop_count<<<(unsigned)B, 128, 0, s>>>(props, prop_cnt, ballmax, B, ncnt);
   const int64_t nb = (n_t + 1023) / 1024;
@@ -349,31 +360,63 @@ cudaError_t launch_merge_props(int metric, int32_t *ids, uint32_t *keys, int k, 
   k_scan_add<<<(unsigned)nb, 1024, 0, s>>>(noff, scan_tmp, n_t);
   k_prop_scatter<<<(unsigned)B, 128, 0, s>>>(props, prop_cnt, ballmax, B, n_t, noff, nfill, sorted);
   const unsigned mb = (unsigned)((n_t + 255) / 256);
-  if (metric == M_U8) k_node_merge<M_U8><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, lrows, part_of,
+  if (metric == M_U8) k_node_merge<M_U8><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, prow, member_cap, part_of,
                                                           local_idx);
-  else if (metric == M_F32) k_node_merge<M_F32><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, lrows, part_of,
+  else if (metric == M_F32) k_node_merge<M_F32><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, prow, member_cap, part_of,
                                                           local_idx);
-  else k_node_merge<M_JAC><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, lrows, part_of,
+  else if (metric == M_JW) k_node_merge<M_JW><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, prow, member_cap, part_of,
+                                                          local_idx);
+  else if (metric == M_COS) k_node_merge<M_COS><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, prow, member_cap, part_of,
+                                                          local_idx);
+  else k_node_merge<M_JAC><<<mb, 256, 0, s>>>(ids, keys, k, n_t, ncnt, nfill, noff, sorted, prow, member_cap, part_of,
                                                           local_idx);
   if (n_launch) *n_launch += 6;
   return cudaGetLastError();
 }
 
-__global__ void k_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
-                        const int32_t *local_idx, int2 *lrows) {
+// The partition-local store of nodes [first, first + count) (read by K1 on partitioned graphs): row v of
+// partition p = part_of[v] at local index l = local_idx[v] holds the local index of each entry in p (-1
+// across partitions, Q10); vector rows / token ranges are copied to the same (p, l) slot.
+__global__ void k_local_rows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
+                             const int32_t *local_idx, int32_t *prow, int64_t cap) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count * k) return;
   const int64_t v = first + i / k;
-  const size_t o = (size_t)first * k + i;
-  const int32_t u = ids[o];
-  lrows[o] = make_int2(u, (u >= 0 && part_of[u] == part_of[v]) ? local_idx[u] : -1);
+  const int e = (int)(i % k);
+  const int32_t u = ids[v * k + e];
+  const uint8_t pv = part_of[v];
+  prow[((size_t)pv * cap + local_idx[v]) * k + e] = (u >= 0 && part_of[u] == pv) ? local_idx[u] : -1;
+}
+__global__ void k_local_vecs(const uint8_t *vec, int nchunks, size_t stride, int64_t first, int64_t count,
+                             const uint8_t *part_of, const int32_t *local_idx, uint8_t *pvec, int64_t cap) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count * nchunks) return;
+  const int64_t v = first + i / nchunks;
+  const int c = (int)(i % nchunks);
+  const uint4 x = *(const uint4 *)(vec + (size_t)v * stride + 16 * c);
+  *(uint4 *)(pvec + ((size_t)part_of[v] * cap + local_idx[v]) * stride + 16 * c) = x;
+}
+__global__ void k_local_sets(const uint64_t *off, int64_t first, int64_t count, const uint8_t *part_of,
+                             const int32_t *local_idx, ulonglong2 *pset, int64_t cap) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int64_t v = first + i;
+  pset[(size_t)part_of[v] * cap + local_idx[v]] = make_ulonglong2(off[v], off[v + 1]);
 }
 
-cudaError_t launch_lrows(const int32_t *ids, int k, int64_t first, int64_t count, const uint8_t *part_of,
-                         const int32_t *local_idx, int2 *lrows, cudaStream_t s) {
+cudaError_t launch_local_store(const StoreView &st, const int32_t *ids, int k, int64_t first, int64_t count,
+                               const uint8_t *part_of, const int32_t *local_idx, const LocalStore &ls, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  const int64_t n = count * k;
-  k_lrows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ids, k, first, count, part_of, local_idx, lrows);
+  const int64_t nr = count * k;
+  k_local_rows<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(ids, k, first, count, part_of, local_idx, ls.prow, ls.cap);
+  if (ls.pvec) {
+    const int64_t nv = count * st.nchunks;
+    k_local_vecs<<<(unsigned)((nv + 255) / 256), 256, 0, s>>>(st.vec, st.nchunks, st.stride, first, count, part_of,
+                                                              local_idx, ls.pvec, ls.cap);
+  }
+  if (ls.pset)
+    k_local_sets<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(st.off, first, count, part_of, local_idx, ls.pset,
+                                                                 ls.cap);
   return cudaGetLastError();
 }
 

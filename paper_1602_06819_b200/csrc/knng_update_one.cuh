@@ -47,7 +47,7 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
   if (lane == 0) *s_n = 0;
   __syncwarp();
   typename QuerySel<M, L, CPL>::T Q;
-  if (!kt) Q.load(a.st, a.n_t, qscr);
+  if (!kt || str_metric(M)) Q.load(a.st, a.n_t, qscr);
   {
     const int32_t v = lane < k ? C[lane] : -1;
     const bool ins = v >= 0 && hash_insert(hash, a.hcap, v);
@@ -83,7 +83,9 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
       const int t = base + lane;
       const int32_t v = t < hi ? list[t] : -1;
       const int cnt = hi - base < 32 ? hi - base : 32;
-      const uint32_t key = kt ? (v >= 0 ? kt[v] : 0u) : Q.eval(a.st, v, cnt);   // kt: the fused launch's key table
+      uint32_t key;
+      if constexpr (str_metric(M)) key = Q.rkey(a.st, v);   // strings: v's own key of the new point (v's row)
+      else key = kt ? (v >= 0 ? kt[v] : 0u) : Q.eval(a.st, v, cnt);   // kt: the fused launch's key table
       bool prop = false;
       if (v >= 0) prop = precedes<M>(key, idx, a.keys[(size_t)v * k + k - 1], a.ids[(size_t)v * k + k - 1]);
       const unsigned pm = __ballot_sync(FULL, prop);
