@@ -202,7 +202,10 @@ def run_reference(args, cfg):
 def cfg_desc(cfg):
     pts = {D.U8: "uint8 d=%d (%d-cluster mixture), squared-L2 int32" % (cfg.dim, cfg.clusters),
            D.F32: "fp32 d=%d (%d-cluster mixture), squared-L2 fp32" % (cfg.dim, cfg.clusters),
-           D.JAC: "Zipf(1.1) token sets, Jaccard (exact cross-multiplied)"}[cfg.metric]
+           D.JAC: "Zipf(1.1) token sets, Jaccard (exact cross-multiplied)",
+           D.JW: "synthetic strings (%d templates with edits), Jaro-Winkler (exact fractions)" % cfg.clusters,
+           D.COS: "synthetic strings (%d templates with edits), 2-gram cosine (exact cross-multiplied)" % cfg.clusters
+           }[cfg.metric]
     part = ", P=%d partitions (imbalance %g)" % (cfg.P, cfg.imbalance) if cfg.P else ""
     return ("%s: n0=%d %s, k=%d, batches of %d, speedup=%g, expansion %d/%d, depth %d%s" % (
         cfg.name, cfg.n0, pts, cfg.k, cfg.batch, cfg.speedup, cfg.e_num, cfg.e_den, cfg.depth, part))
@@ -218,7 +221,7 @@ def point_bytes(cfg, S=None):
 
 
 def dtype_name(cfg):
-    return {D.U8: "u8", D.F32: "f32", D.JAC: "u32 sets"}[cfg.metric]
+    return {D.U8: "u8", D.F32: "f32", D.JAC: "u32 sets", D.JW: "u32 strings", D.COS: "u32 strings"}[cfg.metric]
 
 
 def run_ours(args, cfg):
@@ -272,16 +275,16 @@ def run_ours(args, cfg):
     t_setup = time.perf_counter()
     if ws > 1:
         from paper_1602_06819_b200.dist import library_graph
-        g = library_graph(X, cfg.k, lrank, capacity=cap, stream=stream.cuda_stream)
+        g = library_graph(X, cfg.k, lrank, capacity=cap, stream=stream.cuda_stream, metric=cfg.metric)
     else:
-        g = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream)
+        g = KnngGraph(X, cfg.k, device=lrank, capacity=cap, stream=stream.cuda_stream, metric=cfg.metric)
     part0 = None
     if cfg.P:
         part0 = g.partition_kmedoids(cfg.P, cfg.imbalance, args.kmedoids_iters, cfg.part_seed)[:2]
     t_setup = time.perf_counter() - t_setup
     want_cpu = rank == 0 and ws == 1 and not args.no_cpu_baseline
     rows0 = g.rows() if want_cpu else None          # the state the timed steps start from
-    if cfg.metric == D.JAC:     # sets stay in host CSR: the library copies each batch in (H2D inside the step)
+    if cfg.metric in D.CSR:     # sets stay in host CSR: the library copies each batch in (H2D inside the step)
         S_dev = S[:nsteps * GB]
     else:
         S_dev = torch.from_numpy(S[:nsteps * GB]).to("cuda")
@@ -330,7 +333,7 @@ def run_ours(args, cfg):
     # the dense step (A5 all-pairs, K3): tcgen05 kind::i8 for u8, SIMT otherwise; 2 * B^2 * d ops
     ms_ap = sum(s["ms_allpairs"] for s in stats) / len(stats)
     dense = None
-    if cfg.metric != D.JAC and ms_ap > 0:
+    if cfg.metric not in D.CSR and ms_ap > 0:
         ops = 2.0 * GB * GB * cfg.dim
         try:
             bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
@@ -346,7 +349,7 @@ def run_ours(args, cfg):
     # ---------------- end to end through the C ABI with host buffers (e2e) ----------------
     # the same graph continues the stream: each step copies its batch from pinned host memory (H2D)
     # and reads the stats back (D2H) inside the timed region
-    if cfg.metric == D.JAC:
+    if cfg.metric in D.CSR:
         S_pin = S[pos:pos + nsteps * GB]
     else:
         S_pin = torch.from_numpy(S[pos:pos + nsteps * GB]).pin_memory().numpy()
@@ -376,7 +379,7 @@ def run_ours(args, cfg):
     samp_new = cfg.n0 + np.sort(rs.choice(pos, min(pos, 256), replace=False)) if pos else np.zeros(0, np.int64)
     samp_all = np.sort(rs.choice(ntot, min(ntot, 256), replace=False))
     nodes = np.concatenate([samp_new, samp_all]).astype(np.int64)
-    if cfg.metric != D.JAC:
+    if cfg.metric not in D.CSR:
         nq = torch.from_numpy(nodes).cuda()
         pts = [X, S[:pos]]
         q = torch.from_numpy(np.concatenate(pts)[nodes]).cuda().float()

@@ -518,6 +518,7 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
     a.fuse = 1;
     a.nseq = (int)g->fuse_nseq;
     a.ub = *g->fuse_b1;
+    a.ub.st = graph_store_view(g);   // after the ingest: a set / string store may have grown (moved) since
     mmax = g->n + g->fuse_nseq;   // the pool of the last insert of the sequence
     // small graphs: the sequence's keys against the whole pool, computed densely by one launch and
     // staged per insert in shared memory (<= 32 KB) for the search and the update

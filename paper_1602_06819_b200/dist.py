@@ -68,7 +68,7 @@ def _sync():
         torch.cuda.current_stream().synchronize()
 
 
-def library_graph(points, k, device, capacity=0, stream=None, group=None):
+def library_graph(points, k, device, capacity=0, stream=None, group=None, metric=None):
     """This rank's replica with the LIBRARY-owned NCCL communicator: rank 0 makes the 128-byte NCCL id
     (graph_nccl_unique_id), torch.distributed broadcasts it, and every rank's graph_init joins the
     communicator.  graph_insert_batch on the returned handle is then the whole distributed insert in
@@ -85,7 +85,7 @@ def library_graph(points, k, device, capacity=0, stream=None, group=None):
         idt = idd.cpu()
     else:
         dist.broadcast(idt, 0, group=group)
-    return KnngGraph(points, k, device=device, capacity=capacity, stream=stream, rank=rank, world=world,
+    return KnngGraph(points, k, device=device, capacity=capacity, stream=stream, rank=rank, world=world, metric=metric,
                      nccl_id=bytes(idt.numpy().tobytes()))
 
 

@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KNNG_LIB") or os.path.join(_HERE, "libknng.so")
 
-KNNG_L2SQ_U8, KNNG_L2SQ_F32, KNNG_JACCARD_U32SET = 0, 1, 2
+KNNG_L2SQ_U8, KNNG_L2SQ_F32, KNNG_JACCARD_U32SET, KNNG_JARO_WINKLER, KNNG_COSINE_2GRAM = 0, 1, 2, 3, 4
 ERRORS = {
     -1: "INVALID_ARG", -2: "INSUFFICIENT", -3: "EMPTY", -4: "CAPACITY_INFEAS", -5: "OOM",
     -6: "CUDA", -7: "NCCL", -8: "CAPACITY_EXCEEDED",
@@ -128,39 +128,59 @@ def _metric_of(arr):
 class TokenSets:
     """Jaccard sets in CSR form: offsets uint64[n+1], tokens uint32 (each set sorted, unique).
     Both host numpy arrays, or both CUDA torch tensors (int64 / int32 views are accepted)."""
+    metric = KNNG_JACCARD_U32SET
 
     def __init__(self, offsets, tokens):
         self.offsets = offsets
         self.tokens = tokens
 
-    @staticmethod
-    def from_list(sets):
+    @classmethod
+    def from_list(cls, sets, **kw):
         off = np.zeros(len(sets) + 1, np.uint64)
         off[1:] = np.cumsum([len(x) for x in sets])
         tok = (np.concatenate([np.asarray(x, np.uint32) for x in sets]) if len(sets) else np.zeros(0, np.uint32))
-        return TokenSets(off, np.ascontiguousarray(tok, np.uint32))
+        return cls(off, np.ascontiguousarray(tok, np.uint32), **kw)
+
+
+class Strings(TokenSets):
+    """Strings for KNNG_JARO_WINKLER / KNNG_COSINE_2GRAM in the same CSR form: one uint32 character per
+    element, in string order (<= 127 per string).  from_list accepts python str or arrays of code units."""
+
+    def __init__(self, offsets, chars, metric):
+        super().__init__(offsets, chars)
+        if metric not in (KNNG_JARO_WINKLER, KNNG_COSINE_2GRAM):
+            raise ValueError("Strings: metric must be KNNG_JARO_WINKLER or KNNG_COSINE_2GRAM")
+        self.metric = metric
+
+    @classmethod
+    def from_list(cls, strs, metric):
+        arrs = [np.frombuffer(x.encode("utf-32-le"), np.uint32) if isinstance(x, str) else np.asarray(x, np.uint32)
+                for x in strs]
+        return super().from_list(arrs, metric=metric)
 
     def __len__(self):
         return len(self.offsets) - 1
 
 
-def make_points(points):
-    """Marshal host numpy [n, dim] / CUDA torch [n, dim] vectors, or Jaccard sets (a list of sorted
-    uint32 arrays or a TokenSets), into knng_points.  Returns (struct, keepalive)."""
+def make_points(points, metric=None):
+    """Marshal host numpy [n, dim] / CUDA torch [n, dim] vectors, Jaccard sets (a list of sorted uint32
+    arrays or a TokenSets) or strings (a Strings, or a list with metric = a string metric) into
+    knng_points.  Returns (struct, keepalive)."""
     if isinstance(points, list):
-        points = TokenSets.from_list(points)
+        points = (Strings.from_list(points, metric) if metric in (KNNG_JARO_WINKLER, KNNG_COSINE_2GRAM)
+                  else TokenSets.from_list(points))
     if isinstance(points, TokenSets):
         o, t = points.offsets, points.tokens
         if hasattr(o, "is_cuda") and o.is_cuda:
             o, t = o.contiguous(), t.contiguous()
-            p = knng_points(KNNG_JACCARD_U32SET, 0, len(o) - 1, C.c_void_p(t.data_ptr() if t.numel() else 0),
+            p = knng_points(points.metric, 0, len(o) - 1, C.c_void_p(t.data_ptr() if t.numel() else 0),
                             C.c_void_p(o.data_ptr()), 1)
             return p, (o, t)
         o = np.ascontiguousarray(o, np.uint64)
         t = np.ascontiguousarray(t, np.uint32)
         if len(t) == 0:
             t = np.zeros(1, np.uint32)
-        p = knng_points(KNNG_JACCARD_U32SET, 0, len(o) - 1, t.ctypes.data_as(C.c_void_p),
+        p = knng_points(points.metric, 0, len(o) - 1, t.ctypes.data_as(C.c_void_p),
                         o.ctypes.data_as(C.c_void_p), 0)
         return p, (o, t)
     if hasattr(points, "is_cuda") and points.is_cuda:
@@ -197,9 +217,9 @@ class KnngGraph:
     """One graph handle (graph_init ... graph_free).  With world > 1 (or an nccl_id), the handle owns an
     NCCL communicator and insert_batch is the distributed insert (every rank passes the same batch)."""
 
-    def __init__(self, points, k, device=0, capacity=0, stream=None, rank=0, world=1, nccl_id=None):
+    def __init__(self, points, k, device=0, capacity=0, stream=None, rank=0, world=1, nccl_id=None, metric=None):
         L = load_library()
-        p, keep = make_points(points)
+        p, keep = make_points(points, metric)
         self._id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
         rt = knng_runtime(int(device), int(rank), int(world),
                           None if self._id is None else C.cast(self._id, C.c_void_p),
@@ -232,7 +252,7 @@ class KnngGraph:
         return int(load_library().graph_size(self._h))
 
     def insert_batch(self, points, speedup, e_num, e_den, depth, seed, route=0):
-        p, keep = make_points(points)
+        p, keep = make_points(points, self.metric)
         prm, _ = make_params(speedup, e_num, e_den, depth, seed, route=route)
         first = C.c_int64()
         st = knng_stats()
@@ -242,7 +262,7 @@ class KnngGraph:
     def insert_sequential(self, points, speedup, e_num, e_den, depth, seed):
         """graph_insert_sequential: the points one after another, each a batch of one (the paper's
         sequential algorithm); one launch on an unpartitioned single-GPU graph."""
-        p, keep = make_points(points)
+        p, keep = make_points(points, self.metric)
         prm, _ = make_params(speedup, e_num, e_den, depth, seed)
         first = C.c_int64()
         st = knng_stats()
@@ -253,7 +273,7 @@ class KnngGraph:
     def search(self, queries, kr, speedup, e_num, e_den, seed, starts=None, out=None, full_scan=0, route=0):
         """graph_search: iGNNS; full_scan=1 with e_den=0 is the GNNS baseline; route=1 searches only
         the nearest medoid's partition (reading Q18's variant)."""
-        p, keep = make_points(queries)
+        p, keep = make_points(queries, self.metric)
         prm, keep2 = make_params(speedup, e_num, e_den, 1, seed, starts, full_scan, route)
         st = knng_stats()
         if out is not None:        # device outputs (torch int32 tensors)
@@ -275,7 +295,7 @@ class KnngGraph:
 
     def stage_search(self, points, speedup, e_num, e_den, depth, seed, part_lo, part_hi, cand_ids, cand_keys,
                      q_lo=-1, q_hi=-1):
-        p, keep = make_points(points)
+        p, keep = make_points(points, self.metric)
         prm, _ = make_params(speedup, e_num, e_den, depth, seed)
         st = knng_stats()
         _check(load_library().graph_insert_stage_search(self._h, C.byref(p), C.byref(prm), int(part_lo), int(part_hi),

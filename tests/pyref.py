@@ -10,6 +10,8 @@ decision -- so that a dropped term, a wrong sign or a transposed operand in the 
   * the GNNS baseline walk (section 2.2): all k neighbours evaluated, move to the best.
   * Alg. 4 with the sampled-candidate medoid update of reading Q22 and the
     acceptance rule of Q23, every score compared as an exact fraction.
+  * the string measures of SURVEY 8(f)#4 (P:289 Jaro-Winkler, P:292 cosine of 2-gram count vectors) as
+    exact fractions (the cosine as its square, which orders the same way).
 """
 from __future__ import annotations
 
@@ -300,3 +302,51 @@ def kmedoids(metric, point, rows, P, imbalance, max_iter, seed, exact_limit=4096
         if not changed:
             break
     return part_out, med, costs
+
+
+# ---------------------------------------------------------------------------
+# String measures, exact
+# ---------------------------------------------------------------------------
+def jaro_winkler(a, b):
+    """Textbook Jaro-Winkler as a Fraction: Jaro (matching window max(|a|,|b|)//2 - 1, characters of a
+    matched in order to the first unused equal character of b inside the window, t = half the matched
+    characters out of order) plus the Winkler boost l/10 (1 - jaro), l = common prefix <= 4."""
+    a, b = list(a), list(b)
+    if not a or not b:
+        return Fraction(0)
+    w = max(max(len(a), len(b)) // 2 - 1, 0)
+    used = [False] * len(b)
+    a_seq = []
+    for i, c in enumerate(a):
+        for j in range(max(0, i - w), min(len(b), i + w + 1)):
+            if not used[j] and b[j] == c:
+                used[j] = True
+                a_seq.append(c)
+                break
+    b_seq = [c for c, u in zip(b, used) if u]
+    m = len(a_seq)
+    if m == 0:
+        return Fraction(0)
+    t = Fraction(sum(x != y for x, y in zip(a_seq, b_seq)), 2)
+    jaro = (Fraction(m, len(a)) + Fraction(m, len(b)) + (m - t) / m) / 3
+    ell = 0
+    while ell < min(4, len(a), len(b)) and a[ell] == b[ell]:
+        ell += 1
+    return jaro + Fraction(ell, 10) * (1 - jaro)
+
+
+def bigram_counts(s):
+    from collections import Counter
+    s = list(s)
+    return Counter(zip(s, s[1:]))
+
+
+def cosine_2gram_sq(a, b):
+    """cos^2 of the 2-gram count vectors as a Fraction (0 when either vector is zero)."""
+    ca, cb = bigram_counts(a), bigram_counts(b)
+    dot = sum(v * cb[g] for g, v in ca.items())
+    na, nb = sum(v * v for v in ca.values()), sum(v * v for v in cb.values())
+    if na == 0 or nb == 0:
+        return Fraction(0)
+    return Fraction(dot * dot, na * nb)
+
