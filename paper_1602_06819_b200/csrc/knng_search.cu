@@ -48,7 +48,6 @@ constexpr int WPC = 4;            // warps (independent tasks) per CTA
 #define KNNG_K1_MB 6              // launch bound: >= 6 CTAs (24 warps) per SM -> <= 80 registers (measured best: 5 -> 96 and 8 -> 64 are slower)
 #endif
 constexpr int WPF = 4;            // window row prefetch slots (draws that may be accepted)
-constexpr int WLCAP = 64;         // pool indices a walk evaluates, kept to refresh the window's E bits
 
 // explicit state spaces for the task's bit planes (global, gpu-scope: one warp reads and writes them)
 __device__ __forceinline__ void g_red_or(uint32_t *p, uint32_t v) {
@@ -220,8 +219,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   uint8_t *qsm = wrow + ((WPF * RB + 15) & ~15);                           // [512 B] query (vectors)
   uint32_t *pkey = (uint32_t *)(qsm + 512);                                // [32] pending walk evaluations
   int32_t *pid = (int32_t *)(pkey + 32);                                   // [32]
-  int32_t *wlst = pid + 32;                                                // [WLCAP] the walk's fresh evaluations
-  uint32_t *qscr = (uint32_t *)(wlst + WLCAP);                                // [QSCR] query tokens + table (sets)
+  uint32_t *qscr = (uint32_t *)(pid + 32);                                // [QSCR] query tokens + table (sets)
   uint32_t *ebits = qscr + (csr_metric(M) ? QSCR : 0);                       // [e_bytes / 4] E bitmap (es)
   long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
   const int Pn = a.part_cnt;
@@ -577,7 +575,6 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       bool have_nr = false;                      // ... or in nr (loaded after the move)
       int32_t nr = -1;
       int pn = 0;
-      int wn = 0;                                // the walk's fresh evaluations (wlst, global-E plans)
       auto flush = [&]() {
         if (pn == 0) return;
         __syncwarp();
@@ -687,13 +684,6 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         const bool cm2 = (fm2 >> lane) & 1u;
         const int nf2 = __popc(fm2);
         if (cm2) e_set(lv);
-        if (!es) {   // kept so that the window's E bits can be refreshed without a global round trip
-          if (cm2) {
-            const int q2 = wn + __popc(fm2 & lanemask_lt());
-            if (q2 < WLCAP) wlst[q2] = lv;
-          }
-          wn += nf2;
-        }
         if (pn + nf2 > 32) flush();
         if (cm2) {
           const int q = pn + __popc(fm2 & lanemask_lt());
@@ -715,18 +705,12 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       }
       flush();
       KPROF(c_walk += clock64() - tk0;)
-      // the walk may have evaluated nodes the rest of the window drew: refresh their E bits (from the walk's
-      // list of fresh evaluations when it fits, else re-read the global words)
+      // the walk may have evaluated nodes the rest of the window drew: re-read their E bits
       if (!stop && wpos < 32) {
         const bool need = lane >= wpos && wfr0 && !wev;
         if (__any_sync(FULL, need)) {
           if (es) {
             if (need) wev = e_smem_test(wl);
-          } else if (wn <= WLCAP) {
-            __syncwarp();
-            bool hit = false;
-            for (int i = 0; i < wn; ++i) hit |= wlst[i] == wl;
-            if (need) wev = hit;
           } else {
             const uint32_t ew = need ? g_ld(planes + pw(wl)) : 0u;
             if (need) wev = (ew & e_bit(wl)) != 0;
@@ -819,7 +803,7 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   const size_t RB = (size_t)4 * a.k;
   const bool ns2 = !sets && a.e_smem && a.ns2;
   size_t b = (size_t)(ns2 ? 64 : 32) * a.pitch + (a.row_pf ? ((a.k * RB + 15) & ~(size_t)15) : 0) +
-             ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + WLCAP * 4 + (sets ? QSCR * 4 : 0) +
+             ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QSCR * 4 : 0) +
              (a.e_smem ? (size_t)a.e_bytes * ((a.x_smem || a.kt) ? 2 : 1) : 0);
   return (b + 15) & ~(size_t)15;
 }
