@@ -428,6 +428,16 @@ static int plan_k1(knng_graph *g, SearchArgs &a, int64_t tasks, int64_t mmax) {
       }
     }
   }
+  // one-stage plans of the lane-form widths: the rows may be gathered by the TMA engine (one bulk copy per
+  // row on the warp's mbarrier instead of 16-byte cp.async per lane); KNNG_BULK=0/1 (measurement)
+  a.bulk = 0;
+  if (lform && !a.ns2 && !a.kt) {
+    if (const char *e = getenv("KNNG_BULK")) a.bulk = atoi(e) != 0;
+  }
+  if (a.bulk) {
+    a.swz = 0;
+    a.pitch = (int)g->geom.stride + 16;
+  }
   CK(search_resident_warps(g->geom, a, &warps));
   a.gslots = std::min<int64_t>(warps, (tasks + 3) / 4 * 4);
   return 0;

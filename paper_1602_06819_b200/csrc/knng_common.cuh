@@ -182,6 +182,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// mbarrier arrival that also expects tx bytes of asynchronous (bulk) copies in the current phase
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(tx)
+               : "memory");
+}
+// one bulk copy global -> shared (the TMA engine; UBLKCP), completing `bytes` on the mbarrier at bar
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -332,8 +343,9 @@ __device__ __forceinline__ uint32_t set_key(const uint32_t *a, int la, const uin
 
 // Key of string b as an entry of string a's row (single thread; a: the row owner / query).
 //  JW: matches in a's order, each a[i] taking the first free b[j] with |i - j| <= max(|a|,|b|)/2 - 1
-//      (free positions of b as a 128-bit mask); T = positions where the matched characters of a and
-//      of b, each in order, differ; l = common prefix (<= 4).  Key m | T<<7 | l<<14 | |a|<<17 | |b|<<24.
+//      (matched positions of a and b as pairs of 64-bit register masks); T = positions where the matched
+//      characters of a and of b, each in order, differ (walked by find-first-set over the masks); l =
+//      common prefix (<= 4).  Key m | T<<7 | l<<14 | |a|<<17 | |b|<<24.
 //  COS: dot = pairs of equal 2-grams (a[i], a[i+1]) == (b[j], b[j+1]); key (dot << 16) | n2b, n2b =
 //      |b|^2 of the count vector (>= 1).
 template <int M>
@@ -353,27 +365,34 @@ __device__ __forceinline__ uint32_t str_key(const uint32_t *a, int la, const uin
   } else {
     int w = (la > lb ? la : lb) / 2 - 1;
     if (w < 0) w = 0;
-    uint32_t bfree[4] = {~0u, ~0u, ~0u, ~0u};   // b positions not yet matched
-    uint32_t amat[4] = {0u, 0u, 0u, 0u};         // a positions matched
+    // matched positions as two 64-bit register masks each (strings <= 127 characters): no local memory
+    uint64_t bm0 = 0, bm1 = 0;   // b positions matched
+    uint64_t am0 = 0, am1 = 0;   // a positions matched
     int m = 0;
     for (int i = 0; i < la; ++i) {
       const uint32_t c = a[i];
       const int lo = i - w > 0 ? i - w : 0, hi = i + w < lb - 1 ? i + w : lb - 1;
       for (int j = lo; j <= hi; ++j) {
-        if (((bfree[j >> 5] >> (j & 31)) & 1u) && b[j] == c) {
-          bfree[j >> 5] &= ~(1u << (j & 31));
-          amat[i >> 5] |= 1u << (i & 31);
+        const uint64_t bw = j < 64 ? bm0 : bm1;
+        if (!((bw >> (j & 63)) & 1ull) && b[j] == c) {
+          if (j < 64) bm0 |= 1ull << j;
+          else bm1 |= 1ull << (j - 64);
+          if (i < 64) am0 |= 1ull << i;
+          else am1 |= 1ull << (i - 64);
           ++m;
           break;
         }
       }
     }
-    int T = 0, j = 0;
-    for (int i = 0; i < la; ++i) {
-      if (!((amat[i >> 5] >> (i & 31)) & 1u)) continue;
-      while ((bfree[j >> 5] >> (j & 31)) & 1u) ++j;   // next matched position of b
+    // T: the r-th matched character of a against the r-th matched character of b
+    int T = 0;
+    uint64_t ra0 = am0, ra1 = am1, rb0 = bm0, rb1 = bm1;
+    for (int r = 0; r < m; ++r) {
+      const int i = ra0 ? __ffsll((long long)ra0) - 1 : 64 + __ffsll((long long)ra1) - 1;
+      const int j = rb0 ? __ffsll((long long)rb0) - 1 : 64 + __ffsll((long long)rb1) - 1;
+      if (ra0) ra0 &= ra0 - 1; else ra1 &= ra1 - 1;
+      if (rb0) rb0 &= rb0 - 1; else rb1 &= rb1 - 1;
       T += a[i] != b[j];
-      ++j;
     }
     int l = 0;
     while (l < 4 && l < la && l < lb && a[l] == b[l]) ++l;
@@ -572,7 +591,7 @@ struct VecQuery {
 // Up to SU chunks per lane and set are in flight together.
 constexpr int QMAX = 256;
 constexpr int SET_HT = 256;              // open-addressing table of the query's tokens (membership in ~1 probe)
-constexpr int QSCR = QMAX + SET_HT;      // words of a set query's shared scratch: tokens, then the table
+constexpr int QSCR = QMAX + SET_HT;      // words of a set / string query's shared scratch: tokens, then the table
 template <int L>
 struct SetQuery {
   static constexpr int SU = 1;
@@ -741,23 +760,70 @@ struct SetQuery {
 
 // Strings (M_JW / M_COS): the query's characters in shared scratch (QSCR words >= STR_MAX), one lane per
 // candidate, its characters read from global memory (str_key).  n2 of a candidate from StoreView::n2.
+// COS with scratch: the query's 2-grams also go into a 256-slot open-addressing table (word (i + 1) |
+// count << 16, i = the 2-gram's first position in the query), so that dot(q, x) = sum over x's 2-gram
+// positions of the query's count of that 2-gram -- one probe per position of x instead of |q| compares.
+constexpr int STR_HT = 256;
+__device__ __forceinline__ int bigram_slot(uint32_t c0, uint32_t c1) {
+  return (int)(((c0 * 0x9E3779B1u) ^ (c1 * 0x85EBCA77u)) >> 24);
+}
 template <int M>
 struct StrQuery {
   const uint32_t *q;
   int qn;
-  uint32_t qn2;   // COS: the query's own |q|^2 (a key of the query as another row's entry)
+  uint32_t qn2;           // COS: the query's own |q|^2 (a key of the query as another row's entry)
+  const uint32_t *ht;     // COS: the query's 2-gram table (shared scratch), else null
   __device__ __forceinline__ void load(const StoreView &s, int64_t r, uint32_t *scratch) {
     const int lane = threadIdx.x & 31;
     const uint64_t b = s.off[r];
     qn = (int)(s.off[r + 1] - b);
     qn2 = (M == M_COS && s.n2) ? s.n2[r] : 0u;
+    ht = nullptr;
     if (scratch) {
       for (int i = lane; i < qn; i += 32) scratch[i] = s.tok[b + i];
-      __syncwarp();
       q = scratch;
+      if (M == M_COS) {   // the 2-gram table after the characters (STR_MAX + 1 + STR_HT <= QSCR words)
+        uint32_t *t = scratch + STR_MAX + 1;
+        for (int i = lane; i < STR_HT; i += 32) t[i] = 0u;
+        __syncwarp();
+        for (int i = lane; i + 1 < qn; i += 32) {
+          const uint32_t c0 = scratch[i], c1 = scratch[i + 1];
+          for (int h = bigram_slot(c0, c1);; h = (h + 1) & (STR_HT - 1)) {
+            const uint32_t old = atomicCAS(t + h, 0u, (uint32_t)(i + 1) | (1u << 16));
+            if (old == 0u) break;
+            const int j = (int)(old & 0xFFFFu) - 1;
+            if (scratch[j] == c0 && scratch[j + 1] == c1) {
+              atomicAdd(t + h, 1u << 16);
+              break;
+            }
+          }
+        }
+        ht = t;
+      }
+      __syncwarp();
     } else {
       q = s.tok + b;
     }
+  }
+  // the query's count of 2-gram (c0, c1) (COS with the table)
+  __device__ __forceinline__ uint32_t qcount(uint32_t c0, uint32_t c1) const {
+    for (int h = bigram_slot(c0, c1);; h = (h + 1) & (STR_HT - 1)) {
+      const uint32_t e = ht[h];
+      if (e == 0u) return 0u;
+      const int j = (int)(e & 0xFFFFu) - 1;
+      if (q[j] == c0 && q[j + 1] == c1) return e >> 16;
+    }
+  }
+  // dot(q, x) over x's 2-gram positions (COS with the table)
+  __device__ __forceinline__ uint32_t qdot(const uint32_t *x, int lx) const {
+    uint32_t dot = 0;
+    uint32_t c0 = lx > 0 ? x[0] : 0u;
+    for (int j = 0; j + 1 < lx; ++j) {
+      const uint32_t c1 = x[j + 1];
+      dot += qcount(c0, c1);
+      c0 = c1;
+    }
+    return dot;
   }
   // key of candidate cand (lane-local; cand < 0: 0)
   __device__ __forceinline__ uint32_t key(const StoreView &s, int32_t cand) const {
@@ -771,6 +837,7 @@ struct StrQuery {
       b = s.off[cand];
       e = s.off[cand + 1];
     }
+    if (M == M_COS && ht) return (qdot(s.tok + b, (int)(e - b)) << 16) | s.n2[cand];
     return str_key<M>(q, qn, s.tok + b, (int)(e - b), M == M_COS ? s.n2[cand] : 0u);
   }
   __device__ __forceinline__ uint32_t eval(const StoreView &s, int32_t cand, int n) const {
@@ -780,6 +847,7 @@ struct StrQuery {
   __device__ __forceinline__ uint32_t rkey(const StoreView &s, int32_t v) const {
     if (v < 0) return 0u;
     const uint64_t b = s.off[v];
+    if (M == M_COS && ht) return (qdot(s.tok + b, (int)(s.off[v + 1] - b)) << 16) | qn2;   // dot is symmetric
     return str_key<M>(s.tok + b, (int)(s.off[v + 1] - b), q, qn, qn2);
   }
   __device__ __forceinline__ void eval2(const StoreView &s, int32_t ca, int32_t cb, uint32_t &oa, uint32_t &ob) const {

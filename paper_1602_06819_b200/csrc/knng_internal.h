@@ -115,6 +115,7 @@ struct SearchArgs {
   int row_pf;                  // 1: a walk step copies the rows of all of cur's neighbours with their vectors
                                // (0: the chosen neighbour's row is loaded once the move is known)
   int full_scan;               // 1: the GNNS baseline walk (all k neighbours, move to the best)
+  int bulk;                    // 1 (lane-form widths, one chunk stage): rows gathered by TMA bulk copies
   const int32_t *route;        // routed search (reading Q18's variant): partition of query b, else null
   // B = 1 fused launch (one task): after the search, the same warp runs the update of the insert
   // (update_one_warp with ub, C = out_ids / out_keys) and writes stats[0..5] itself

@@ -190,18 +190,38 @@ __device__ __forceinline__ void gather_lf(unsigned sb, int pitch, const uint8_t 
   }
 }
 
+// The same rows gathered by the TMA engine: lane r issues ONE bulk copy of row r (cp.async.bulk, NCK * 16
+// bytes, unswizzled at pitch NCK * 16 + 16: the pad keeps the lane-per-row key loads conflict-free) that
+// completes on the warp's mbarrier; lane 0 arrives with the phase's byte count first.  The caller waits
+// for the phase (bulk_wait) before reading the stage.
+template <int NCK>
+__device__ __forceinline__ void gather_bulk(unsigned sb, int pitch, const uint8_t *base, int32_t myid, int nrows,
+                                            uint64_t *bar) {
+  const int lane = threadIdx.x & 31;
+  const bool v = lane < nrows && myid >= 0;
+  const unsigned m = __ballot_sync(FULL, v);
+  if (lane == 0) mbar_arrive_expect_tx(bar, (unsigned)__popc(m) * (NCK * 16));
+  __syncwarp();
+  if (v) bulk_g2s(sb + lane * pitch, base + (size_t)(uint32_t)myid * (NCK * 16), NCK * 16, smem_u32(bar));
+}
+__device__ __forceinline__ void bulk_wait(uint64_t *bar, uint32_t &phase) {
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+}
+
 // ---------------------------------------------------------------------------------------------
 // K1: MB = minimum CTAs per SM of the launch bounds (WPC warps each).  NCK > 0: a lane-form width
 // (u8 d = 32 / 128, f32 d = 96) with its geometry known at compile time; PART = 1 / 0: partitioned /
-// unpartitioned graph (-1: read from the arguments).
+// unpartitioned graph (-1: read from the arguments); BK = 1: lane-form rows gathered by bulk copies
+// (one-stage plans).
 // ---------------------------------------------------------------------------------------------
-template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
+template <int M, int L, int CPL, int MB, int NCK, int PART, int KT, int BK>
 __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k = a.k;
   constexpr bool LF = NCK > 0;                                             // one lane per staged row
-  constexpr bool SWZ = LF && NCK % 8 == 0;
+  constexpr bool SWZ = LF && !BK && NCK % 8 == 0;
   const bool part = PART < 0 ? a.P > 0 : PART == 1;
   const int nck = csr_metric(M) ? 0 : (LF ? NCK : a.st.nchunks);
   const int pitch = LF ? (SWZ ? NCK * 16 : NCK * 16 + 16) : a.pitch;
@@ -222,6 +242,15 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   uint32_t *qscr = (uint32_t *)(pid + 32);                                // [QSCR] query tokens + table (sets)
   uint32_t *ebits = qscr + (csr_metric(M) ? QSCR : 0);                       // [e_bytes / 4] E bitmap (es)
   long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
+  uint64_t *mbar = (uint64_t *)(sched + WPC) + warp;                       // (BK) the warp's bulk-copy barrier
+  uint32_t bph = 0;                                                        // (BK) its phase
+  if constexpr (BK != 0) {
+    if (lane == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
   const int64_t gw = (int64_t)blockIdx.x * WPC + warp;                      // warp slot
@@ -239,7 +268,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   // from it instead of gathering rows (same keys, same decisions, same counters).
   uint32_t *kt = nullptr;
   if constexpr (KT != 0) {   // row `it` of the sequence's key matrix (k_keymat) into shared memory
-    kt = (uint32_t *)(smem + (size_t)WPC * a.wbytes + 8 * WPC + fuse_bytes(a, csr_metric(M)));
+    kt = (uint32_t *)(smem + (size_t)WPC * a.wbytes + 16 * WPC + fuse_bytes(a, csr_metric(M)));
     const uint32_t *src = a.ktm + (size_t)it * a.ktm_ld;
     const int64_t n4 = n_t >> 2;
 #pragma unroll 4
@@ -328,7 +357,8 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         if (nch <= SetQuery<L>::SLOTCH)
           for (int jj = 0; jj < nch; ++jj) cpa16(sb0 + lane * pitch + 16 * jj, a.st.tok + a0 + 4 * jj);
       } else if constexpr (LF) {
-        gather_lf<NCK>(sb0, pitch, vbase, d.y, 32);
+        if constexpr (BK != 0) gather_bulk<NCK>(sb0, pitch, vbase, d.y, 32, mbar);
+        else gather_lf<NCK>(sb0, pitch, vbase, d.y, 32);
       } else {
         const uint8_t *base = vbase;
         const size_t stride = a.st.stride;
@@ -436,6 +466,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           dnx = dnx2;
           if (M == M_JAC) offs(dnx, bnx, enx);
           dnx2 = draw(ch + 2);
+          if constexpr (BK != 0) bulk_wait(mbar, bph);
           cp_async_wait_all();
         }
         __syncwarp();
@@ -615,7 +646,8 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         if constexpr (KT != 0) {
           // keys from the table
         } else if constexpr (LF) {
-          gather_lf<NCK>(smem_u32(wvec), pitch, vbase, inpool ? v : -1, k);
+          if constexpr (BK != 0) gather_bulk<NCK>(smem_u32(wvec), pitch, vbase, inpool ? v : -1, k, mbar);
+          else gather_lf<NCK>(smem_u32(wvec), pitch, vbase, inpool ? v : -1, k);
           if (row_pf) {
             const unsigned rb0 = smem_u32(rowbuf);
             const int CU = (RB % 16 == 0) ? 16 : ((RB % 8 == 0) ? 8 : 4), NU = RB / CU;
@@ -642,6 +674,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         if constexpr (KT != 0) {
           key = inpool ? kt[lv] : 0u;
         } else if constexpr (LF) {
+          if constexpr (BK != 0) bulk_wait(mbar, bph);
           cp_async_wait_all();
           __syncwarp();
           key = keys_of(wvec, k);
@@ -741,7 +774,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   }
   if (a.fuse) {   // B = 1: one CTA, warp 0 ran the only task; it runs the insert's update
     if (gw == 0) {
-      uint8_t *us = smem + (size_t)WPC * a.wbytes + 8 * WPC;
+      uint8_t *us = smem + (size_t)WPC * a.wbytes + 16 * WPC;
       int32_t *usm = (int32_t *)(us + 16);
       uint32_t *uq = (uint32_t *)(us + 16 + update_one_smem(a.ub.hcap, a.ub.ballmax));
       BallArgs ub = a.ub;
@@ -808,13 +841,13 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   return (b + 15) & ~(size_t)15;
 }
 size_t search_smem_bytes(const SearchArgs &a, bool sets) {
-  return WPC * search_warp_bytes(a, sets) + 8 * WPC + fuse_bytes(a, sets) +
+  return WPC * search_warp_bytes(a, sets) + 16 * WPC + fuse_bytes(a, sets) +
          (a.kt ? (((a.n_t + (a.fuse ? a.nseq : 0)) * 4 + 15) & ~15ll) : 0);
 }
 
 // occupancy of a K1 instantiation at a shared-memory size on the current device, cached (a B = 1 insert
 // launches K1 once per point: the attribute / occupancy queries would otherwise dominate its host time)
-template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
+template <int M, int L, int CPL, int MB, int NCK, int PART, int KT, int BK>
 static cudaError_t k1_occupancy(size_t smem, int *per_sm, int *nsm) {
   static std::mutex mu;
   static std::map<std::pair<int, size_t>, std::pair<int, int>> cache;
@@ -833,7 +866,7 @@ static cudaError_t k1_occupancy(size_t smem, int *per_sm, int *nsm) {
   // failed attribute call at the next launch)
   if (smem > (size_t)optin[dev]) return cudaErrorInvalidValue;
   if (smem > 48 * 1024 && smem > attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB, NCK, PART, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_search<M, L, CPL, MB, NCK, PART, KT, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return e;
@@ -846,7 +879,7 @@ static cudaError_t k1_occupancy(size_t smem, int *per_sm, int *nsm) {
     *nsm = it->second.second;
     return cudaSuccess;
   }
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_search<M, L, CPL, MB, NCK, PART, KT>, 32 * WPC, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_search<M, L, CPL, MB, NCK, PART, KT, BK>, 32 * WPC, smem);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return e;
@@ -857,7 +890,7 @@ static cudaError_t k1_occupancy(size_t smem, int *per_sm, int *nsm) {
   return cudaSuccess;
 }
 
-template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
+template <int M, int L, int CPL, int MB, int NCK, int PART, int KT, int BK>
 static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   const int Pn = a.part_cnt;
   const int64_t T = a.nq * Pn;
@@ -866,7 +899,7 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   const size_t smem = search_smem_bytes(a, csr_metric(M));
   // persistent grid: the CTAs that fit at once (dynamic task scheduling balances the tail)
   int per_sm = 0, nsm = 148;
-  if (cudaError_t oe = k1_occupancy<M, L, CPL, MB, NCK, PART, KT>(smem, &per_sm, &nsm)) return oe;
+  if (cudaError_t oe = k1_occupancy<M, L, CPL, MB, NCK, PART, KT, BK>(smem, &per_sm, &nsm)) return oe;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t blocks = std::min<int64_t>((T + WPC - 1) / WPC, (int64_t)per_sm * nsm);
   blocks = std::min<int64_t>(blocks, a.gslots / WPC);
@@ -878,7 +911,7 @@ static cudaError_t run_search(SearchArgs a, cudaStream_t s) {
   if (getenv("KNNG_PROFILE"))
     fprintf(stderr, "KNNG_PROFILE k_search: %lld CTAs x %d warps, %d CTAs per SM resident (%zu B smem each)\n",
             (long long)blocks, WPC, per_sm, smem);
-  k_search<M, L, CPL, MB, NCK, PART, KT><<<(unsigned)blocks, 32 * WPC, smem, s>>>(a);
+  k_search<M, L, CPL, MB, NCK, PART, KT, BK><<<(unsigned)blocks, 32 * WPC, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -900,7 +933,7 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
   if (n_launch) ++*n_launch;
   if (a.kt) {
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, KNNG_K1_MB, 0, 0, 1>(a, s);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, KNNG_K1_MB, 0, 0, 1, 0>(a, s);
     KNNG_SHAPES(X, M_U8)
     KNNG_SHAPES_F32(X)
     X(M_JAC, 8, 1)
@@ -912,12 +945,15 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
   if (search_lane_form(g, a.lane_eval)) {
 #define X(MM, LL, CC, NN) \
   if (g.metric == MM && g.nchunks == NN) \
-    return a.P > 0 ? run_search<MM, LL, CC, KNNG_K1_MB, NN, 1, 0>(a, s) : run_search<MM, LL, CC, KNNG_K1_MB, NN, 0, 0>(a, s);
+    return a.bulk ? (a.P > 0 ? run_search<MM, LL, CC, KNNG_K1_MB, NN, 1, 0, 1>(a, s) \
+                             : run_search<MM, LL, CC, KNNG_K1_MB, NN, 0, 0, 1>(a, s)) \
+                  : (a.P > 0 ? run_search<MM, LL, CC, KNNG_K1_MB, NN, 1, 0, 0>(a, s) \
+                             : run_search<MM, LL, CC, KNNG_K1_MB, NN, 0, 0, 0>(a, s));
     KNNG_LF_SHAPES(X)
 #undef X
   }
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, KNNG_K1_MB, 0, -1, 0>(a, s);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return run_search<MM, LL, CC, KNNG_K1_MB, 0, -1, 0, 0>(a, s);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)
@@ -927,11 +963,11 @@ cudaError_t launch_search(const VecGeom &g, const SearchArgs &a, cudaStream_t s,
   return cudaErrorInvalidValue;
 }
 
-template <int M, int L, int CPL, int MB, int NCK, int PART, int KT>
+template <int M, int L, int CPL, int MB, int NCK, int PART, int KT, int BK>
 static cudaError_t resident(SearchArgs a, int64_t *warps) {
   const size_t smem = search_smem_bytes(a, csr_metric(M));
   int per_sm = 0, nsm = 148;
-  if (cudaError_t e = k1_occupancy<M, L, CPL, MB, NCK, PART, KT>(smem, &per_sm, &nsm)) return e;
+  if (cudaError_t e = k1_occupancy<M, L, CPL, MB, NCK, PART, KT, BK>(smem, &per_sm, &nsm)) return e;
   *warps = (int64_t)per_sm * nsm * WPC;
   return cudaSuccess;
 }
@@ -939,7 +975,7 @@ static cudaError_t resident(SearchArgs a, int64_t *warps) {
 cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t *warps) {
   if (a.kt) {
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, KNNG_K1_MB, 0, 0, 1>(a, warps);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, KNNG_K1_MB, 0, 0, 1, 0>(a, warps);
     KNNG_SHAPES(X, M_U8)
     KNNG_SHAPES_F32(X)
     X(M_JAC, 8, 1)
@@ -951,12 +987,15 @@ cudaError_t search_resident_warps(const VecGeom &g, const SearchArgs &a, int64_t
   if (search_lane_form(g, a.lane_eval)) {
 #define X(MM, LL, CC, NN) \
   if (g.metric == MM && g.nchunks == NN) \
-    return a.P > 0 ? resident<MM, LL, CC, KNNG_K1_MB, NN, 1, 0>(a, warps) : resident<MM, LL, CC, KNNG_K1_MB, NN, 0, 0>(a, warps);
+    return a.bulk ? (a.P > 0 ? resident<MM, LL, CC, KNNG_K1_MB, NN, 1, 0, 1>(a, warps) \
+                             : resident<MM, LL, CC, KNNG_K1_MB, NN, 0, 0, 1>(a, warps)) \
+                  : (a.P > 0 ? resident<MM, LL, CC, KNNG_K1_MB, NN, 1, 0, 0>(a, warps) \
+                             : resident<MM, LL, CC, KNNG_K1_MB, NN, 0, 0, 0>(a, warps));
     KNNG_LF_SHAPES(X)
 #undef X
   }
 #define X(MM, LL, CC) \
-  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, KNNG_K1_MB, 0, -1, 0>(a, warps);
+  if (g.metric == MM && g.L == LL && g.CPL == CC) return resident<MM, LL, CC, KNNG_K1_MB, 0, -1, 0, 0>(a, warps);
   KNNG_SHAPES(X, M_U8)
   KNNG_SHAPES_F32(X)
   X(M_JAC, 8, 1)

@@ -93,6 +93,10 @@ _K1_PATHS = {
     # walk steps that copy the rows of all neighbours with their vectors
     "row-prefetch": {"KNNG_ROW_PF": 1, "KNNG_ESMEM": 0},
     "row-prefetch+smem-E": {"KNNG_ROW_PF": 1, "KNNG_ESMEM": 1},
+    # lane-form rows gathered by TMA bulk copies on the warp's mbarrier (one-stage plans)
+    "bulk": {"KNNG_BULK": 1, "KNNG_ESMEM": 0},
+    "bulk+smem-E+1stage": {"KNNG_BULK": 1, "KNNG_ESMEM": 1, "KNNG_NS2": 0},
+    "bulk+row-prefetch": {"KNNG_BULK": 1, "KNNG_ESMEM": 0, "KNNG_ROW_PF": 1},
     # the warp-form evaluator (generic widths) instead of one lane per row
     "warp-form": {"KNNG_LANE_EVAL": 0},
     "warp-form+smem-E": {"KNNG_LANE_EVAL": 0, "KNNG_ESMEM": 1},
@@ -129,19 +133,21 @@ def _path_points(n, dim=8):
     return X
 
 
+@pytest.mark.parametrize("bulk", ["0", "1"])
 @pytest.mark.parametrize("esmem", ["0", "1"])
 @pytest.mark.parametrize("k", [2, 4])
-def test_long_walks_match_oracle(env, k, esmem):
+def test_long_walks_match_oracle(env, k, esmem, bulk):
     """A walk of ~n expansions (one step per node along the path): injected start at the far end,
-    budget = pool (speedup 1); under every E-bit placement."""
+    budget = pool (speedup 1); under every E-bit placement, with cp.async or bulk-copy gathers."""
     env("KNNG_ESMEM", esmem)
-    X = _path_points(1500)
+    env("KNNG_BULK", bulk)
+    X = _path_points(1500, 32)             # d = 32: a lane-form width (the bulk-copy gathers apply)
     g = _graph(X, k, 1600)
     o = O.OracleGraph(O.U8, X, k, capacity=1600)
     o.init_exact()
     gi, gk = g.rows()
     _assert_rows_equal(O.U8, gi, gk, o.ids[:1500], o.keys[:1500], "path init")
-    q = np.zeros((3, 8), np.uint8)
+    q = np.zeros((3, 32), np.uint8)
     q[1, 0] = 3
     q[2, :2] = (255, 9)
     for starts in ([1499], [1499, 700, 3], [1200, 1499]):
