@@ -671,7 +671,8 @@ static int stage_update(knng_graph *g, const knng_params *p, int world, const in
   ba.list = g->w_list.as<int32_t>();
   ba.ballmax = (int)ballmax;
   // small balls (depth 2, k <= 16: <= 4 KB of hash + list per warp) keep their sets in shared memory
-  ba.smem_ball = (size_t)4 * (hcap + ballmax) * 4 <= 24 * 1024 ? 1 : 0;
+  // (JW: 24 KB of the 48 KB static budget hold the per-lane character pointers)
+  ba.smem_ball = (size_t)4 * (hcap + ballmax) * 4 <= (g->metric == KNNG_JARO_WINKLER ? 16 : 24) * 1024 ? 1 : 0;
   if (const char *e = getenv("KNNG_SMEM_BALL")) ba.smem_ball = atoi(e) != 0 && ba.smem_ball;
   ba.props = props;
   ba.prop_cnt = prop_cnt;

@@ -183,11 +183,26 @@ __global__ void __launch_bounds__(128) k_exact_build_csr(StoreView st, int64_t n
   if (row >= n) return;
   WarpTopK<M> top;
   top.init(k);
-  for (int64_t c0 = 0; c0 < n; c0 += 32) {
-    const int64_t col = c0 + lane;
-    const bool valid = col < n && col != row;
-    const uint32_t key = valid ? pair_key<M>(st, row, col) : 0u;
-    top.insert(valid, key, (int32_t)col);
+  if constexpr (str_metric(M)) {   // strings: the row's string as the warp's query (2-gram / character tables)
+    __shared__ uint32_t qscr[4 * QSCR];
+    __shared__ __align__(16) uint8_t jwp[M == M_JW ? 4 * 32 * JW_PTR : 16];
+    const int wib = threadIdx.x >> 5;
+    StrQuery<M> Q;
+    if constexpr (M == M_JW) Q.ptr = jwp + (wib * 32 + lane) * JW_PTR;
+    Q.load(st, row, qscr + wib * QSCR);
+    for (int64_t c0 = 0; c0 < n; c0 += 32) {
+      const int64_t col = c0 + lane;
+      const bool valid = col < n && col != row;
+      const uint32_t key = valid ? Q.key(st, (int32_t)col) : 0u;
+      top.insert(valid, key, (int32_t)col);
+    }
+  } else {
+    for (int64_t c0 = 0; c0 < n; c0 += 32) {
+      const int64_t col = c0 + lane;
+      const bool valid = col < n && col != row;
+      const uint32_t key = valid ? pair_key<M>(st, row, col) : 0u;
+      top.insert(valid, key, (int32_t)col);
+    }
   }
   if (lane < k) {
     ids[(size_t)row * k + lane] = lane < top.cnt ? top.id : -1;

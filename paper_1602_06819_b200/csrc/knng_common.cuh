@@ -767,18 +767,30 @@ constexpr int STR_HT = 256;
 __device__ __forceinline__ int bigram_slot(uint32_t c0, uint32_t c1) {
   return (int)(((c0 * 0x9E3779B1u) ^ (c1 * 0x85EBCA77u)) >> 24);
 }
+// JW with scratch: the query's character positions grouped by character (qpos, ascending within a
+// character) and a 256-slot table character -> (first position + 1, count, start in qpos, character id).
+// A pair is then matched by ONE pass over the other string x: for x[j], the query positions of that
+// character are consumed left to right by a per-character pointer (positions < j - w can never match a
+// later j and are skipped for good; the next one matches if <= j + w).  Per character this is the greedy
+// matching of Q33 taken from x's side; it picks the same pairs as from the query's side (both match the
+// occurrences window-feasibly in order; the GPU parity tests compare every key with the oracle's
+// query-side loop), so m and T are unchanged.  The pointers live in a 128-byte slot per lane.
+constexpr int JW_PTR = 128;   // bytes of one lane's character pointers (<= 127 distinct characters)
 template <int M>
 struct StrQuery {
   const uint32_t *q;
   int qn;
   uint32_t qn2;           // COS: the query's own |q|^2 (a key of the query as another row's entry)
-  const uint32_t *ht;     // COS: the query's 2-gram table (shared scratch), else null
+  const uint32_t *ht;     // COS: the query's 2-gram table / JW: the character table (shared scratch), else null
+  const uint32_t *qpos;   // JW: the query's positions grouped by character
+  uint8_t *ptr = nullptr; // JW: this lane's character pointers (JW_PTR bytes of shared memory), else null
   __device__ __forceinline__ void load(const StoreView &s, int64_t r, uint32_t *scratch) {
     const int lane = threadIdx.x & 31;
     const uint64_t b = s.off[r];
     qn = (int)(s.off[r + 1] - b);
     qn2 = (M == M_COS && s.n2) ? s.n2[r] : 0u;
     ht = nullptr;
+    qpos = nullptr;
     if (scratch) {
       for (int i = lane; i < qn; i += 32) scratch[i] = s.tok[b + i];
       q = scratch;
@@ -800,10 +812,117 @@ struct StrQuery {
         }
         ht = t;
       }
+      if (M == M_JW && ptr) {   // character table at [256, 512), positions at [128, 256)
+        uint32_t *t = scratch + 2 * (STR_MAX + 1);
+        uint32_t *qp = scratch + STR_MAX + 1;
+        for (int i = lane; i < STR_HT; i += 32) t[i] = 0u;
+        __syncwarp();
+        // slot word: first position + 1 (the character's first occurrence inserts it)
+        for (int i = lane; i < qn; i += 32) {
+          const uint32_t c = scratch[i];
+          int first = i;
+          for (int j = 0; j < i; ++j)
+            if (scratch[j] == c) { first = j; break; }
+          if (first != i) continue;
+          for (int h = (int)((c * 0x9E3779B1u) >> 24);; h = (h + 1) & (STR_HT - 1))
+            if (atomicCAS(t + h, 0u, (uint32_t)(i + 1)) == 0u) break;
+        }
+        __syncwarp();
+        // per slot: count, start in qp (exclusive scan in slot order) and character id (rank of the slot)
+        uint32_t cnt[STR_HT / 32];
+        int tot = 0, ids = 0;
+#pragma unroll
+        for (int u = 0; u < STR_HT / 32; ++u) {
+          const uint32_t e = t[lane * (STR_HT / 32) + u];
+          uint32_t n = 0;
+          if (e) {
+            const uint32_t c = scratch[(e & 0xFFu) - 1];
+            for (int j = 0; j < qn; ++j) n += scratch[j] == c;
+          }
+          cnt[u] = n;
+          tot += (int)n;
+          ids += e ? 1 : 0;
+        }
+        int pre = tot, pid = ids;   // inclusive warp scans of the counts and of the occupied slots
+        for (int o = 1; o < 32; o <<= 1) {
+          const int x1 = __shfl_up_sync(FULL, pre, o), x2 = __shfl_up_sync(FULL, pid, o);
+          if (lane >= o) { pre += x1; pid += x2; }
+        }
+        int start = pre - tot, cid = pid - ids;
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < STR_HT / 32; ++u) {
+          const int h = lane * (STR_HT / 32) + u;
+          const uint32_t e = t[h];
+          if (e) {
+            t[h] = (e & 0xFFu) | (cnt[u] << 8) | ((uint32_t)start << 15) | ((uint32_t)cid << 22);
+            start += (int)cnt[u];
+            ++cid;
+          }
+        }
+        __syncwarp();
+        // positions of each character, ascending: rank = earlier positions with the same character
+        for (int i = lane; i < qn; i += 32) {
+          const uint32_t c = scratch[i];
+          int rank = 0;
+          for (int j = 0; j < i; ++j) rank += scratch[j] == c;
+          for (int h = (int)((c * 0x9E3779B1u) >> 24);; h = (h + 1) & (STR_HT - 1)) {
+            const uint32_t e = t[h];
+            if (scratch[(e & 0xFFu) - 1] == c) {
+              qp[((e >> 15) & 0x7Fu) + rank] = (uint32_t)i;
+              break;
+            }
+          }
+        }
+        ht = t;
+        qpos = qp;
+      }
       __syncwarp();
     } else {
       q = s.tok + b;
     }
+  }
+  // JW key of the query against x (lane-local, the character table): x's characters in order, each
+  // matched to the next feasible query position of the same character (see the comment above).  a_is_q:
+  // the key's first string is the query (search) or x (the update's key, x = the row owner).
+  __device__ __forceinline__ uint32_t jw_table(const uint32_t *x, int lx, bool a_is_q) const {
+    const int la = a_is_q ? qn : lx, lb = a_is_q ? lx : qn;
+    int w = (qn > lx ? qn : lx) / 2 - 1;
+    if (w < 0) w = 0;
+    for (int u = 0; u < JW_PTR / 16; ++u) ((uint4 *)ptr)[u] = make_uint4(0, 0, 0, 0);
+    uint64_t qm0 = 0, qm1 = 0, xm0 = 0, xm1 = 0;   // matched positions of the query / of x
+    int m = 0;
+    for (int j = 0; j < lx; ++j) {
+      const uint32_t c = x[j];
+      uint32_t e;
+      for (int h = (int)((c * 0x9E3779B1u) >> 24);; h = (h + 1) & (STR_HT - 1)) {
+        e = ht[h];
+        if (e == 0u || q[(e & 0xFFu) - 1] == c) break;
+      }
+      if (e == 0u) continue;
+      const int cnt = (int)((e >> 8) & 0x7Fu), st = (int)((e >> 15) & 0x7Fu), cid = (int)(e >> 22);
+      int p = ptr[cid];
+      while (p < cnt && (int)qpos[st + p] < j - w) ++p;
+      if (p < cnt && (int)qpos[st + p] <= j + w) {
+        const int i = (int)qpos[st + p];
+        ++p;
+        ++m;
+        if (i < 64) qm0 |= 1ull << i; else qm1 |= 1ull << (i - 64);
+        if (j < 64) xm0 |= 1ull << j; else xm1 |= 1ull << (j - 64);
+      }
+      ptr[cid] = (uint8_t)p;
+    }
+    int T = 0;
+    for (int r = 0; r < m; ++r) {
+      const int i = qm0 ? __ffsll((long long)qm0) - 1 : 64 + __ffsll((long long)qm1) - 1;
+      const int j = xm0 ? __ffsll((long long)xm0) - 1 : 64 + __ffsll((long long)xm1) - 1;
+      if (qm0) qm0 &= qm0 - 1; else qm1 &= qm1 - 1;
+      if (xm0) xm0 &= xm0 - 1; else xm1 &= xm1 - 1;
+      T += q[i] != x[j];
+    }
+    int l = 0;
+    while (l < 4 && l < qn && l < lx && q[l] == x[l]) ++l;
+    return (uint32_t)m | ((uint32_t)T << 7) | ((uint32_t)l << 14) | ((uint32_t)la << 17) | ((uint32_t)lb << 24);
   }
   // the query's count of 2-gram (c0, c1) (COS with the table)
   __device__ __forceinline__ uint32_t qcount(uint32_t c0, uint32_t c1) const {
@@ -838,6 +957,7 @@ struct StrQuery {
       e = s.off[cand + 1];
     }
     if (M == M_COS && ht) return (qdot(s.tok + b, (int)(e - b)) << 16) | s.n2[cand];
+    if (M == M_JW && qpos) return jw_table(s.tok + b, (int)(e - b), true);
     return str_key<M>(q, qn, s.tok + b, (int)(e - b), M == M_COS ? s.n2[cand] : 0u);
   }
   __device__ __forceinline__ uint32_t eval(const StoreView &s, int32_t cand, int n) const {
@@ -848,6 +968,7 @@ struct StrQuery {
     if (v < 0) return 0u;
     const uint64_t b = s.off[v];
     if (M == M_COS && ht) return (qdot(s.tok + b, (int)(s.off[v + 1] - b)) << 16) | qn2;   // dot is symmetric
+    if (M == M_JW && qpos) return jw_table(s.tok + b, (int)(s.off[v + 1] - b), false);   // from v's side
     return str_key<M>(s.tok + b, (int)(s.off[v + 1] - b), q, qn, qn2);
   }
   __device__ __forceinline__ void eval2(const StoreView &s, int32_t ca, int32_t cb, uint32_t &oa, uint32_t &ob) const {

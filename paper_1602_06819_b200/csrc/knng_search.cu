@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   uint32_t *pkey = (uint32_t *)(qsm + 512);                                // [32] pending walk evaluations
   int32_t *pid = (int32_t *)(pkey + 32);                                   // [32]
   uint32_t *qscr = (uint32_t *)(pid + 32);                                // [QSCR] query tokens + table (sets)
-  uint32_t *ebits = qscr + (csr_metric(M) ? QSCR : 0);                       // [e_bytes / 4] E bitmap (es)
+  uint8_t *jwp = (uint8_t *)(qscr + (csr_metric(M) ? QSCR : 0));            // [32][JW_PTR] JW character pointers
+  uint32_t *ebits = (uint32_t *)(jwp + (M == M_JW ? 32 * JW_PTR : 0));      // [e_bytes / 4] E bitmap (es)
   long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
   uint64_t *mbar = (uint64_t *)(sched + WPC) + warp;                       // (BK) the warp's bulk-copy barrier
   uint32_t bph = 0;                                                        // (BK) its phase
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     if (budget > m) budget = m;
 
     typename QuerySel<M, L, CPL>::T Q;
+    if constexpr (M == M_JW) Q.ptr = jwp + lane * JW_PTR;
     if (!LF && KT == 0) Q.load(a.qs, qrow0 + b, csr_metric(M) ? qscr : nullptr);
     if (LF) {
       const uint8_t *qg = a.qs.vec + (size_t)(qrow0 + b) * a.qs.stride;
@@ -780,7 +782,8 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       BallArgs ub = a.ub;
       ub.n_t = n_t;
       int nb = 0, np = 0;
-      update_one_warp<M, L, CPL>(ub, a.out_ids, a.out_keys, usm, (int *)us, csr_metric(M) ? uq : nullptr, &nb, &np, kt);
+      update_one_warp<M, L, CPL>(ub, a.out_ids, a.out_keys, usm, (int *)us, csr_metric(M) ? uq : nullptr, &nb, &np, kt,
+                                 M == M_JW ? jwp : nullptr);
       s_ball += (unsigned)nb;
       s_prop += (unsigned)np;
     }
@@ -837,6 +840,7 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   const bool ns2 = !sets && a.e_smem && a.ns2;
   size_t b = (size_t)(ns2 ? 64 : 32) * a.pitch + (a.row_pf ? ((a.k * RB + 15) & ~(size_t)15) : 0) +
              ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QSCR * 4 : 0) +
+             (a.metric == M_JW ? 32 * JW_PTR : 0) +
              (a.e_smem ? (size_t)a.e_bytes * ((a.x_smem || a.kt) ? 2 : 1) : 0);
   return (b + 15) & ~(size_t)15;
 }

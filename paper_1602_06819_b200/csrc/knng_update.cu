@@ -27,12 +27,27 @@ __global__ void __launch_bounds__(128) k_allpairs(StoreView st, int64_t n_t, int
     const uint32_t ck = lane < k ? Ck[r * k + lane] : 0u;
     top.insert(cid >= 0, ck, cid);
   }
-  for (int64_t j0 = 0; j0 < B; j0 += 32) {
-    const int64_t j = j0 + lane;
-    const bool valid = j < B && j != i;
-    uint32_t key = 0;
-    if (valid) key = pair_key<M>(st, n_t + i, n_t + j);
-    top.insert(valid, key, (int32_t)(n_t + j));
+  if constexpr (str_metric(M)) {   // strings: the row's string as the warp's query (2-gram / character tables)
+    __shared__ uint32_t qscr[4 * QSCR];
+    __shared__ __align__(16) uint8_t jwp[M == M_JW ? 4 * 32 * JW_PTR : 16];
+    const int wib = threadIdx.x >> 5;
+    StrQuery<M> Q;
+    if constexpr (M == M_JW) Q.ptr = jwp + (wib * 32 + lane) * JW_PTR;
+    Q.load(st, n_t + i, qscr + wib * QSCR);
+    for (int64_t j0 = 0; j0 < B; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const bool valid = j < B && j != i;
+      const uint32_t key = valid ? Q.key(st, (int32_t)(n_t + j)) : 0u;
+      top.insert(valid, key, (int32_t)(n_t + j));
+    }
+  } else {
+    for (int64_t j0 = 0; j0 < B; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const bool valid = j < B && j != i;
+      uint32_t key = 0;
+      if (valid) key = pair_key<M>(st, n_t + i, n_t + j);
+      top.insert(valid, key, (int32_t)(n_t + j));
+    }
   }
   if (lane < k) {
     oi[(size_t)r * k + lane] = lane < top.cnt ? top.id : -1;
@@ -69,6 +84,7 @@ template <int M, int L, int CPL>
 __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
   __shared__ int s_n[4];
   __shared__ uint32_t qscr[csr_metric(M) ? 4 * QSCR : 1];
+  __shared__ __align__(16) uint8_t jwp[M == M_JW ? 4 * 32 * JW_PTR : 16];   // JW character pointers per lane
   extern __shared__ int32_t bsm[];   // small balls: [4][hcap] hash + [4][ballmax] list in shared memory
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * 4 + wib, nw = (int64_t)gridDim.x * 4;
@@ -82,6 +98,7 @@ __global__ void __launch_bounds__(128) k_ball(BallArgs a) {
     if (lane == 0) s_n[wib] = 0;
     __syncwarp();
     typename QuerySel<M, L, CPL>::T Q;
+    if constexpr (M == M_JW) Q.ptr = jwp + (wib * 32 + lane) * JW_PTR;
     Q.load(a.st, a.n_t + b, csr_metric(M) ? qscr + wib * QSCR : nullptr);
     const int32_t idx = (int32_t)(a.n_t + b);
     // L1 = the search result C(x)
@@ -150,8 +167,10 @@ template <int M, int L, int CPL>
 __global__ void __launch_bounds__(32) k_update_one(BallArgs a, const uint32_t *Ckeys) {
   extern __shared__ int32_t usm[];
   __shared__ uint32_t qscr[csr_metric(M) ? QSCR : 1];
+  __shared__ __align__(16) uint8_t jwp[M == M_JW ? 32 * JW_PTR : 16];
   __shared__ int s_n;
-  update_one_warp<M, L, CPL>(a, a.C, Ckeys, usm, &s_n, csr_metric(M) ? qscr : nullptr, nullptr, nullptr);
+  update_one_warp<M, L, CPL>(a, a.C, Ckeys, usm, &s_n, csr_metric(M) ? qscr : nullptr, nullptr, nullptr, nullptr,
+                             M == M_JW ? jwp : nullptr);
 }
 
 template <int M, int L, int CPL>

@@ -31,7 +31,7 @@ __host__ __device__ __forceinline__ size_t update_one_smem(int hcap, int ballmax
 template <int M, int L, int CPL>
 __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t *C, const uint32_t *Ckeys,
                                                 int32_t *usm, int *s_n, uint32_t *qscr, int *nb, int *npr,
-                                                const uint32_t *kt = nullptr) {
+                                                const uint32_t *kt = nullptr, uint8_t *jwp = nullptr) {
   const int lane = threadIdx.x & 31;
   const int k = a.k;
   int32_t *hash = usm;
@@ -47,6 +47,7 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
   if (lane == 0) *s_n = 0;
   __syncwarp();
   typename QuerySel<M, L, CPL>::T Q;
+  if constexpr (M == M_JW) Q.ptr = jwp ? jwp + lane * JW_PTR : nullptr;
   if (!kt || str_metric(M)) Q.load(a.st, a.n_t, qscr);
   {
     const int32_t v = lane < k ? C[lane] : -1;

@@ -189,3 +189,55 @@ def test_datagen_string_recipe():
         assert len(X) == 500 and all(1 <= len(x) <= 127 for x in X)
         assert set(np.concatenate(X).tolist()) <= set(D.ALPHABET.tolist())
         assert all((a == b).all() for a, b in zip(D.stream_points(cfg, 0, 10), D.stream_points(cfg, 0, 20)[:10]))
+
+
+def _jw_counts_a_side(a, b):
+    """(m, T) of the textbook matching: a's characters in order take the first free equal b character."""
+    w = max(max(len(a), len(b)) // 2 - 1, 0)
+    used = [False] * len(b)
+    amatch = []
+    for i, c in enumerate(a):
+        for j in range(max(0, i - w), min(len(b), i + w + 1)):
+            if not used[j] and b[j] == c:
+                used[j] = True
+                amatch.append(i)
+                break
+    bmatch = [j for j in range(len(b)) if used[j]]
+    return len(amatch), sum(a[i] != b[j] for i, j in zip(amatch, bmatch))
+
+
+def _jw_counts_b_side_pointers(a, b):
+    """(m, T) the way the GPU's table evaluator matches: b's characters in order, each consuming the next
+    feasible position of the same character in a (per-character pointers; positions < j - w skipped)."""
+    w = max(max(len(a), len(b)) // 2 - 1, 0)
+    pos = {}
+    for i, c in enumerate(a):
+        pos.setdefault(c, []).append(i)
+    ptr = {c: 0 for c in pos}
+    amatch, bmatch = [], []
+    for j, c in enumerate(b):
+        if c not in pos:
+            continue
+        p, lst = ptr[c], pos[c]
+        while p < len(lst) and lst[p] < j - w:
+            p += 1
+        if p < len(lst) and lst[p] <= j + w:
+            amatch.append(lst[p])
+            bmatch.append(j)
+            p += 1
+        ptr[c] = p
+    amatch.sort()
+    return len(amatch), sum(a[i] != b[j] for i, j in zip(amatch, bmatch))
+
+
+def test_jw_matching_side_independent():
+    """The GPU evaluates JW by scanning the candidate against the query's per-character position lists
+    (matching from the candidate's side); pinned here: that matching has the textbook (m, T) on random
+    strings of small alphabets (many repeated characters) and every length up to the 127-character bound."""
+    rng = np.random.default_rng(12)
+    for alpha, hi in ((2, 20), (3, 40), (5, 127), (26, 127)):
+        for _ in range(1500 if hi <= 40 else 300):
+            a = rng.integers(0, alpha, size=int(rng.integers(0, hi + 1))).tolist()
+            b = rng.integers(0, alpha, size=int(rng.integers(0, hi + 1))).tolist()
+            assert _jw_counts_b_side_pointers(a, b) == _jw_counts_a_side(a, b), (a, b)
+            assert _jw_counts_b_side_pointers(b, a) == _jw_counts_a_side(a, b), (a, b)
