@@ -387,7 +387,11 @@ static int plan_k1(knng_graph *g, SearchArgs &a, int64_t tasks, int64_t mmax) {
   const bool sets = csr_points(g->metric);
   const bool lform = search_lane_form(g->geom, a.lane_eval);
   a.swz = lform && g->geom.nchunks % 8 == 0;
-  a.pitch = sets ? 16 * 16 + 16 : (int)g->geom.stride + (a.swz ? 0 : 16);
+  // sets: a lane's slot holds SETCH aligned 16-byte token chunks (longer sets are read from global memory);
+  // KNNG_SET_SLOTCH overrides (measurement)
+  int setch = 16;
+  if (const char *e = getenv("KNNG_SET_SLOTCH")) setch = std::max(1, std::min(64, atoi(e)));
+  a.pitch = sets ? setch * 16 + 16 : (int)g->geom.stride + (a.swz ? 0 : 16);
 
   // walk steps copy the rows of all of cur's neighbours with their vectors when the vectors dominate the
   // step's bytes anyway (measured: C2's 384-byte rows gain 6%, the 128-byte rows of C1/C3/C4 lose 12-17%)

@@ -705,9 +705,8 @@ struct SetQuery {
       out[j] = cand[j] >= 0 ? (((uint32_t)inter[j] << 16) | (uint32_t)(qn + (re[j] - rb[j]) - inter[j])) : 0u;
   }
 
-  // Key of the candidate whose aligned token chunks are staged at slot (16 B each, SLOTCH at
+  // Key of the candidate whose aligned token chunks are staged at slot (16 B each, the launch's slot size at
   // most; rb/re = first/end token relative to the first chunk).  Lane-local.
-  static constexpr int SLOTCH = 16;
   __device__ __forceinline__ uint32_t eval_slot(const uint8_t *slot, int rb, int re) const {
     const int nch = (re + 3) >> 2;
     int inter = 0;

@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   const int nck = csr_metric(M) ? 0 : (LF ? NCK : a.st.nchunks);
   const int pitch = LF ? (SWZ ? NCK * 16 : NCK * 16 + 16) : a.pitch;
   const int RB = 4 * k;                                                    // bytes of a walked row (local indices)
+  const int slotch = (pitch - 16) >> 4;                                    // sets: 16-byte chunks of a lane's slot
   const bool row_pf = KT == 0 && a.row_pf != 0;                           // (KT: rows are loaded, keys looked up)
   const bool es = KT || a.e_smem != 0;                                     // E bitmap in shared memory
   const bool ns2 = !KT && !csr_metric(M) && es && a.ns2 != 0;                  // two chunk stages (needs es)
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       } else if constexpr (M == M_JAC) {
         const uint64_t a0 = tb & ~3ull;
         const int nch = d.x >= 0 ? ((int)(te - a0) + 3) >> 2 : 0;
-        if (nch <= SetQuery<L>::SLOTCH)
+        if (nch <= slotch)
           for (int jj = 0; jj < nch; ++jj) cpa16(sb0 + lane * pitch + 16 * jj, a.st.tok + a0 + 4 * jj);
       } else if constexpr (LF) {
         if constexpr (BK != 0) gather_bulk<NCK>(sb0, pitch, vbase, d.y, 32, mbar);
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           if (ok) {
             const uint64_t a0 = cb & ~3ull;
             const int rb = (int)(cb - a0), re = (int)(ce - a0);
-            if (((re + 3) >> 2) <= SetQuery<L>::SLOTCH) wkey = Q.eval_slot(stage + lane * pitch, rb, re);
+            if (((re + 3) >> 2) <= slotch) wkey = Q.eval_slot(stage + lane * pitch, rb, re);
             else wkey = Q.eval_slot_global(a.st.tok + a0, rb, re);
           }
         } else {

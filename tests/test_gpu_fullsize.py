@@ -97,6 +97,8 @@ _K1_PATHS = {
     "bulk": {"KNNG_BULK": 1, "KNNG_ESMEM": 0},
     "bulk+smem-E+1stage": {"KNNG_BULK": 1, "KNNG_ESMEM": 1, "KNNG_NS2": 0},
     "bulk+row-prefetch": {"KNNG_BULK": 1, "KNNG_ESMEM": 0, "KNNG_ROW_PF": 1},
+    # sets: 4-chunk lane slots (most sets evaluated from global memory instead of the staged slot)
+    "set-slots-4": {"KNNG_SET_SLOTCH": 4},
     # the warp-form evaluator (generic widths) instead of one lane per row
     "warp-form": {"KNNG_LANE_EVAL": 0},
     "warp-form+smem-E": {"KNNG_LANE_EVAL": 0, "KNNG_ESMEM": 1},
