@@ -399,6 +399,7 @@ static int plan_k1(knng_graph *g, SearchArgs &a, int64_t tasks, int64_t mmax) {
   if (const char *e = getenv("KNNG_ROW_PF")) a.row_pf = atoi(e) != 0;
   a.win_prefetch = 1;
   if (const char *e = getenv("KNNG_WIN_PREFETCH")) a.win_prefetch = atoi(e) != 0;
+  if (a.srows) a.win_prefetch = 0;   // rows already in shared memory (the prefetch copies from global)
   // latency-bound launches (every task resident at once): the E bitmap (and, if it fits too, the X
   // bitmap) in shared memory and two chunk stages, if that plan still holds every task; else the E / X
   // bits in the per-slot global words and one stage
@@ -539,6 +540,8 @@ static int run_search_phase(knng_graph *g, const StoreView &qs, int64_t qrow0, i
     // small graphs: the sequence's keys against the whole pool, computed densely by one launch and
     // staged per insert in shared memory (<= 32 KB) for the search and the update
     a.kt = mmax <= 8192 && !getenv("KNNG_NO_KT");
+    // the rows too when they fit (<= 160 KB): the walks' and the update's row reads become shared-memory reads
+    a.srows = a.kt && mmax * g->k * 4 <= 160 * 1024 && !getenv("KNNG_NO_SROWS");
     if (a.kt) {
       a.ktm_ld = (mmax + 3) & ~3ll;
       CK(g->w_ktm.ensure((size_t)g->fuse_nseq * a.ktm_ld * 4));

@@ -123,6 +123,7 @@ struct SearchArgs {
   int nseq;                    // (fuse) sequential inserts: rows n_t .. n_t + nseq - 1 (ingested), one after another
   BallArgs ub;
   int kt;                      // (fuse) 1: the keys against all n_t pool nodes precomputed (ktm) and staged in smem
+  int srows;                   // (kt) 1: the rows (ids) of nodes 0 .. n_t + nseq - 1 kept in shared memory too
   const uint32_t *ktm;         // (kt) [nseq][ktm_ld] key matrix of the sequence (launch_keymat)
   int64_t ktm_ld;
 };

@@ -262,6 +262,19 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   // fused launch: nseq sequential inserts (each a batch of one against the graph the previous one left:
   // the paper's Alg. 1 + 2 point after point); else one pass over the launch's tasks
   const int nseq = a.fuse ? a.nseq : 1;
+  // KT launches with srows: the rows of every node the sequence can reach, in shared memory after the key
+  // table (the walks and the update read them there; the update writes both copies)
+  int32_t *srw = nullptr;
+  if constexpr (KT != 0) {
+    if (a.srows) {
+      srw = (int32_t *)(smem + (size_t)WPC * a.wbytes + 16 * WPC + fuse_bytes(a, csr_metric(M)) +
+                        (((a.n_t + nseq) * 4 + 15) & ~15ll));
+      const int64_t nr4 = ((a.n_t + nseq) * k) >> 2;
+      for (int64_t v = threadIdx.x; v < nr4; v += blockDim.x) ((int4 *)srw)[v] = ((const int4 *)a.rows)[v];
+      for (int64_t v = (nr4 << 2) + threadIdx.x; v < (a.n_t + nseq) * k; v += blockDim.x) srw[v] = a.rows[v];
+      __syncthreads();
+    }
+  }
   for (int it = 0; it < nseq; ++it) {
   const int64_t n_t = a.n_t + it, qrow0 = a.qrow0 + it, pid_base = a.pid_base + it;
   int64_t task = gw;
@@ -288,7 +301,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     // index of the draws); ids are converted through members when the task writes its top-k
     const size_t pbase = part ? (size_t)p * a.member_cap : 0;
     const uint8_t *vbase = (part && !csr_metric(M)) ? a.pvec + pbase * a.st.stride : a.st.vec;
-    const int32_t *rbase = part ? a.prow + pbase * k : a.rows;
+    const int32_t *rbase = part ? a.prow + pbase * k : (srw ? srw : a.rows);
     StoreView sv = a.st;
     sv.vec = vbase;
     if (csr_metric(M) && part) sv.rng = a.pset + pbase;
@@ -635,7 +648,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           if (rw >= 0) e2 = ((const int32_t *)(wrow + rw * RB))[lane];
           else if (rs >= 0) e2 = ((const int32_t *)(rowbuf + rs * RB))[lane];
           else if (have_nr) e2 = nr;
-          else e2 = __ldg(rbase + (size_t)cur * k + lane);
+          else e2 = KT ? rbase[(size_t)cur * k + lane] : __ldg(rbase + (size_t)cur * k + lane);
           v = e2;
           vl = e2;
         }
@@ -713,7 +726,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         // the move (if any) is known: its row is loaded now, under the bookkeeping below
         const int32_t ncur = __shfl_sync(FULL, v, fi);
         if (!row_pf && im && !mv_x && lane < k)
-          nr = __ldg(rbase + (size_t)ncur * k + lane);
+          nr = KT ? rbase[(size_t)ncur * k + lane] : __ldg(rbase + (size_t)ncur * k + lane);
         unsigned fm2 = __ballot_sync(FULL, !evb2) & range;
         bool hit2 = false;
         if ((int64_t)__popc(fm2) > budget - c) { fm2 = first_bits(fm2, (int)(budget - c)); hit2 = true; }
@@ -784,7 +797,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       ub.n_t = n_t;
       int nb = 0, np = 0;
       update_one_warp<M, L, CPL>(ub, a.out_ids, a.out_keys, usm, (int *)us, csr_metric(M) ? uq : nullptr, &nb, &np, kt,
-                                 M == M_JW ? jwp : nullptr);
+                                 M == M_JW ? jwp : nullptr, srw);
       s_ball += (unsigned)nb;
       s_prop += (unsigned)np;
     }
@@ -847,7 +860,8 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
 }
 size_t search_smem_bytes(const SearchArgs &a, bool sets) {
   return WPC * search_warp_bytes(a, sets) + 16 * WPC + fuse_bytes(a, sets) +
-         (a.kt ? (((a.n_t + (a.fuse ? a.nseq : 0)) * 4 + 15) & ~15ll) : 0);
+         (a.kt ? (((a.n_t + (a.fuse ? a.nseq : 0)) * 4 + 15) & ~15ll) : 0) +
+         (a.kt && a.srows ? (((a.n_t + (a.fuse ? a.nseq : 0)) * a.k * 4 + 15) & ~15ll) : 0);
 }
 
 // occupancy of a K1 instantiation at a shared-memory size on the current device, cached (a B = 1 insert

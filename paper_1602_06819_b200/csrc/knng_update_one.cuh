@@ -31,9 +31,11 @@ __host__ __device__ __forceinline__ size_t update_one_smem(int hcap, int ballmax
 template <int M, int L, int CPL>
 __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t *C, const uint32_t *Ckeys,
                                                 int32_t *usm, int *s_n, uint32_t *qscr, int *nb, int *npr,
-                                                const uint32_t *kt = nullptr, uint8_t *jwp = nullptr) {
+                                                const uint32_t *kt = nullptr, uint8_t *jwp = nullptr,
+                                                int32_t *sids = nullptr) {
   const int lane = threadIdx.x & 31;
   const int k = a.k;
+  const int32_t *rows = sids ? sids : a.ids;   // the rows the update reads (the fused launch's shared copy)
   int32_t *hash = usm;
   int32_t *list = hash + a.hcap;
   int2 *props = (int2 *)(list + a.ballmax + (a.ballmax & 1));
@@ -41,6 +43,7 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
   // new row n_t = C (the top-k of the search; B = 1 has no batch peers)
   if (lane < k) {
     a.ids[(size_t)idx * k + lane] = C[lane];
+    if (sids) sids[(size_t)idx * k + lane] = C[lane];
     a.keys[(size_t)idx * k + lane] = Ckeys[lane];
   }
   for (int i = lane; i < a.hcap; i += 32) hash[i] = -1;
@@ -69,7 +72,7 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int t = gb + r * G + gl;
-          u[r] = (gl < G && t < hi) ? a.ids[(size_t)list[t] * k + ge] : -1;
+          u[r] = (gl < G && t < hi) ? rows[(size_t)list[t] * k + ge] : -1;
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -88,7 +91,7 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
       if constexpr (str_metric(M)) key = Q.rkey(a.st, v);   // strings: v's own key of the new point (v's row)
       else key = kt ? (v >= 0 ? kt[v] : 0u) : Q.eval(a.st, v, cnt);   // kt: the fused launch's key table
       bool prop = false;
-      if (v >= 0) prop = precedes<M>(key, idx, a.keys[(size_t)v * k + k - 1], a.ids[(size_t)v * k + k - 1]);
+      if (v >= 0) prop = precedes<M>(key, idx, a.keys[(size_t)v * k + k - 1], rows[(size_t)v * k + k - 1]);
       const unsigned pm = __ballot_sync(FULL, prop);
       if (prop) props[np + __popc(pm & lanemask_lt())] = make_int2(v, (int)key);
       np += __popc(pm);
@@ -109,7 +112,7 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
     if (act) {
       v = props[j].x;
       key = (uint32_t)props[j].y;
-      ri = a.ids[(size_t)v * k + ge];
+      ri = rows[(size_t)v * k + ge];
       rk = a.keys[(size_t)v * k + ge];
     }
     const bool before = act && precedes<M>(rk, ri, key, idx);   // entry e stays ahead of the new one
@@ -120,6 +123,7 @@ __device__ __forceinline__ void update_one_warp(const BallArgs &a, const int32_t
     if (act && ge >= pos) {
       a.keys[(size_t)v * k + ge] = ge == pos ? key : uk;
       a.ids[(size_t)v * k + ge] = ge == pos ? idx : ui;
+      if (sids) sids[(size_t)v * k + ge] = ge == pos ? idx : ui;
     }
   }
   if (nb) {
