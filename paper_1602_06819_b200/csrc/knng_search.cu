@@ -265,15 +265,30 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   // KT launches with srows: the rows of every node the sequence can reach, in shared memory after the key
   // table (the walks and the update read them there; the update writes both copies)
   int32_t *srw = nullptr;
+  // KT: two key-table buffers -- insert it reads buffer it & 1 while warps 1.. (idle: the launch has one
+  // task) stage row it + 1 of the key matrix into the other
+  uint8_t *ktbase = smem + (size_t)WPC * a.wbytes + 16 * WPC + fuse_bytes(a, csr_metric(M));
+  const size_t ktb = (size_t)(((a.n_t + nseq) * 4 + 15) & ~15ll);
+  auto stage_kt = [&](int r, int t0, int nth) {
+    uint32_t *dst = (uint32_t *)(ktbase + (r & 1) * ktb);
+    const uint32_t *src = a.ktm + (size_t)r * a.ktm_ld;
+    const int64_t nn = a.n_t + r, n4 = nn >> 2;
+#pragma unroll 4
+    for (int64_t v = (int)threadIdx.x - t0; v < n4; v += nth) ((uint4 *)dst)[v] = ((const uint4 *)src)[v];
+    for (int64_t v = (n4 << 2) + (int)threadIdx.x - t0; v < nn; v += nth) dst[v] = src[v];
+  };
   if constexpr (KT != 0) {
     if (a.srows) {
-      srw = (int32_t *)(smem + (size_t)WPC * a.wbytes + 16 * WPC + fuse_bytes(a, csr_metric(M)) +
-                        (((a.n_t + nseq) * 4 + 15) & ~15ll));
+      srw = (int32_t *)(ktbase + 2 * ktb);
       const int64_t nr4 = ((a.n_t + nseq) * k) >> 2;
       for (int64_t v = threadIdx.x; v < nr4; v += blockDim.x) ((int4 *)srw)[v] = ((const int4 *)a.rows)[v];
       for (int64_t v = (nr4 << 2) + threadIdx.x; v < (a.n_t + nseq) * k; v += blockDim.x) srw[v] = a.rows[v];
       __syncthreads();
     }
+  }
+  if constexpr (KT != 0) {
+    stage_kt(0, 0, blockDim.x);
+    __syncthreads();
   }
   for (int it = 0; it < nseq; ++it) {
   const int64_t n_t = a.n_t + it, qrow0 = a.qrow0 + it, pid_base = a.pid_base + it;
@@ -282,15 +297,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   // computed up front by the whole CTA into a shared table; the search and the update then read keys
   // from it instead of gathering rows (same keys, same decisions, same counters).
   uint32_t *kt = nullptr;
-  if constexpr (KT != 0) {   // row `it` of the sequence's key matrix (k_keymat) into shared memory
-    kt = (uint32_t *)(smem + (size_t)WPC * a.wbytes + 16 * WPC + fuse_bytes(a, csr_metric(M)));
-    const uint32_t *src = a.ktm + (size_t)it * a.ktm_ld;
-    const int64_t n4 = n_t >> 2;
-#pragma unroll 4
-    for (int64_t v = threadIdx.x; v < n4; v += blockDim.x) ((uint4 *)kt)[v] = ((const uint4 *)src)[v];
-    for (int64_t v = (n4 << 2) + threadIdx.x; v < n_t; v += blockDim.x) kt[v] = src[v];
-    __syncthreads();
-  }
+  if constexpr (KT != 0) kt = (uint32_t *)(ktbase + (it & 1) * ktb);   // row `it` of the key matrix (staged)
 
   while (task < T) {
     const int64_t b = task / Pn;
@@ -801,6 +808,9 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       s_ball += (unsigned)nb;
       s_prop += (unsigned)np;
     }
+    if constexpr (KT != 0) {   // the other warps stage the next insert's key-table row meanwhile
+      if (threadIdx.x >= 32 && it + 1 < nseq) stage_kt(it + 1, 32, (int)blockDim.x - 32);
+    }
     __syncthreads();   // the insert's rows (global) before the next insert's search and key table
   }
   }   // sequential inserts
@@ -860,7 +870,7 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
 }
 size_t search_smem_bytes(const SearchArgs &a, bool sets) {
   return WPC * search_warp_bytes(a, sets) + 16 * WPC + fuse_bytes(a, sets) +
-         (a.kt ? (((a.n_t + (a.fuse ? a.nseq : 0)) * 4 + 15) & ~15ll) : 0) +
+         (a.kt ? 2 * (((a.n_t + (a.fuse ? a.nseq : 0)) * 4 + 15) & ~15ll) : 0) +
          (a.kt && a.srows ? (((a.n_t + (a.fuse ? a.nseq : 0)) * a.k * 4 + 15) & ~15ll) : 0);
 }
 
