@@ -439,6 +439,11 @@ def run_ours(args, cfg):
                      "alg_bytes_model": "SURVEY 8(d): (V + 4) B per committed search evaluation + 4k B per expanded "
                                         "node; V = %d" % V,
                      "ms_per_launch": ms_search / len(stats),
+                     # the DRAM traffic ncu counts for one launch of this workload over this run's launch time:
+                     # what the memory system actually moves (algorithmic bytes + visited-set and re-gather
+                     # overhead), against the same peak
+                     "dram_gbs": (traffic / (ms_search / len(stats) / 1000.0) / 1e9) if traffic else None,
+                     "dram_frac": (traffic / (ms_search / len(stats) / 1000.0) / 1e9 / peak) if traffic else None,
                      "note": ("store + rows fit in L2 (126 MB): the HBM fraction is not the binding claim"
                               if cap * (V + 8 * cfg.k) < 100e6 else "HBM-resident store")},
         "roofline_dense": dense,
