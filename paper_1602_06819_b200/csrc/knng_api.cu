@@ -436,13 +436,10 @@ static int plan_k1(knng_graph *g, SearchArgs &a, int64_t tasks, int64_t mmax) {
   // one-stage plans of the lane-form widths: the rows are gathered by the TMA engine (one bulk copy per row
   // on the warp's mbarrier instead of 16-byte cp.async per lane; measured C2 -3%, C3 at 2M -4.5%, C3 at 8M
   // equal: profiles/round2/k1_ab_bulk.txt); KNNG_BULK=0 restores the cp.async gathers (measurement, tests)
-  // Two-stage plans (C1) use them only with KNNG_BULK2=1 (measurement): one barrier per stage.
   a.bulk = 0;
   if (lform && !a.ns2 && !a.kt) {
     a.bulk = 1;
     if (const char *e = getenv("KNNG_BULK")) a.bulk = atoi(e) != 0;
-  } else if (lform && a.ns2 && !a.kt) {
-    if (const char *e = getenv("KNNG_BULK2")) a.bulk = atoi(e) != 0;
   }
   if (a.bulk) {
     a.swz = 0;

@@ -244,14 +244,11 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   uint8_t *jwp = (uint8_t *)(qscr + (csr_metric(M) ? QSCR : 0));            // [32][JW_PTR] JW character pointers
   uint32_t *ebits = (uint32_t *)(jwp + (M == M_JW ? 32 * JW_PTR : 0));      // [e_bytes / 4] E bitmap (es)
   long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
-  // (BK) the warp's two bulk-copy barriers (barrier s serves chunk stage s; one-stage plans use 0), the
-  // phase parity of each (bit s) and the phases issued and not yet waited for (bit s)
-  uint64_t *mbar = (uint64_t *)(sched + WPC) + 2 * warp;
-  uint32_t bph = 0, bpend = 0;
+  uint64_t *mbar = (uint64_t *)(sched + WPC) + warp;                       // (BK) the warp's bulk-copy barrier
+  uint32_t bph = 0;                                                        // (BK) its phase
   if constexpr (BK != 0) {
     if (lane == 0) {
       mbar_init(mbar, 1);
-      mbar_init(mbar + 1, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -270,7 +267,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   int32_t *srw = nullptr;
   // KT: two key-table buffers -- insert it reads buffer it & 1 while warps 1.. (idle: the launch has one
   // task) stage row it + 1 of the key matrix into the other
-  uint8_t *ktbase = smem + (size_t)WPC * a.wbytes + 24 * WPC + fuse_bytes(a, csr_metric(M));
+  uint8_t *ktbase = smem + (size_t)WPC * a.wbytes + 16 * WPC + fuse_bytes(a, csr_metric(M));
   const size_t ktb = (size_t)(((a.n_t + nseq) * 4 + 15) & ~15ll);
   auto stage_kt = [&](int r, int t0, int nth) {
     uint32_t *dst = (uint32_t *)(ktbase + (r & 1) * ktb);
@@ -369,18 +366,6 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       const uint64_t idx = rng_index(h3, (uint64_t)j, (uint64_t)m);
       return make_int2((int32_t)idx, (int32_t)idx);
     };
-    // (BK) rows of node ids `id` (lane r: row r < nrows) into dst by bulk copies on barrier s_, and the
-    // wait for that barrier's pending phase
-    auto bulk_issue = [&](int s_, unsigned dst, int32_t id, int nrows) {
-      gather_bulk<NCK>(dst, pitch, vbase, id, nrows, mbar + s_);
-      bpend |= 1u << s_;
-    };
-    auto bulk_wait_s = [&](int s_) {
-      mbar_wait(mbar + s_, (bph >> s_) & 1u);
-      bph ^= 1u << s_;
-      bpend &= ~(1u << s_);
-    };
-    int cstg = 0;                                // (ns2) the stage of the chunk being processed
     // ---- the draw of a chunk: issue(d) copies the drawn rows into the stage (sets: each lane its token
     // range) and returns the E word of each draw, read in the same round trip.
     const unsigned sb0 = smem_u32(stage);
@@ -395,7 +380,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         if (nch <= slotch)
           for (int jj = 0; jj < nch; ++jj) cpa16(sb0 + lane * pitch + 16 * jj, a.st.tok + a0 + 4 * jj);
       } else if constexpr (LF) {
-        if constexpr (BK != 0) bulk_issue(0, sb0, d.y, 32);
+        if constexpr (BK != 0) gather_bulk<NCK>(sb0, pitch, vbase, d.y, 32, mbar);
         else gather_lf<NCK>(sb0, pitch, vbase, d.y, 32);
       } else {
         const uint8_t *base = vbase;
@@ -415,11 +400,10 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
     };
     auto e_smem_test = [&](int32_t i) -> bool { return ((ebits[i >> 5] >> (i & 31)) & 1u) != 0; };
     uint32_t *xbits = ebits + (a.e_bytes >> 2);  // xs: the X bitmap follows the E bitmap
-    auto issue_to = [&](uint8_t *dst, int2 d, int stg) {
+    auto issue_to = [&](uint8_t *dst, int2 d) {
       if constexpr (!csr_metric(M) && KT == 0) {
         if constexpr (LF) {
-          if constexpr (BK != 0) bulk_issue(stg, smem_u32(dst), d.y, 32);
-          else gather_lf<NCK>(smem_u32(dst), pitch, vbase, d.y, 32);
+          gather_lf<NCK>(smem_u32(dst), pitch, vbase, d.y, 32);
         } else {
           const unsigned sb = smem_u32(dst);
           for (int e = lane; e < 32 * nck; e += 32) {
@@ -490,14 +474,12 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           wl = infl.x;
           wnode = infl.y;
           cst = stage + (ch & 1) * 32 * pitch;
-          cstg = (int)(ch & 1);
-          issue_to(stage + ((ch + 1) & 1) * 32 * pitch, dnx, (int)((ch + 1) & 1));
+          issue_to(stage + ((ch + 1) & 1) * 32 * pitch, dnx);
           cp_async_commit();
           infl = dnx;
           dnx = dnx2;
           dnx2 = draw(ch + 3);
-          if constexpr (BK != 0) bulk_wait_s(cstg);
-          else cp_async_wait<1>();
+          cp_async_wait<1>();
         } else {
           wl = dnx.x;
           wnode = dnx.y;
@@ -507,7 +489,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           dnx = dnx2;
           if (M == M_JAC) offs(dnx, bnx, enx);
           dnx2 = draw(ch + 2);
-          if constexpr (BK != 0) bulk_wait_s(0);
+          if constexpr (BK != 0) bulk_wait(mbar, bph);
           cp_async_wait_all();
         }
         __syncwarp();
@@ -687,7 +669,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         if constexpr (KT != 0) {
           // keys from the table
         } else if constexpr (LF) {
-          if constexpr (BK != 0) bulk_issue(cstg, smem_u32(wvec), inpool ? v : -1, k);
+          if constexpr (BK != 0) gather_bulk<NCK>(smem_u32(wvec), pitch, vbase, inpool ? v : -1, k, mbar);
           else gather_lf<NCK>(smem_u32(wvec), pitch, vbase, inpool ? v : -1, k);
           if (row_pf) {
             const unsigned rb0 = smem_u32(rowbuf);
@@ -715,7 +697,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         if constexpr (KT != 0) {
           key = inpool ? kt[lv] : 0u;
         } else if constexpr (LF) {
-          if constexpr (BK != 0) bulk_wait_s(cstg);
+          if constexpr (BK != 0) bulk_wait(mbar, bph);
           cp_async_wait_all();
           __syncwarp();
           key = keys_of(wvec, k);
@@ -808,10 +790,6 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       a.out_ids[o] = lane < top.cnt ? (part ? a.members[pbase + top.id] : top.id) : -1;
       a.out_keys[o] = lane < top.cnt ? top.key : 0u;
     }
-    if constexpr (BK != 0) {   // a chunk stage still in flight when the task stopped (two-stage plans)
-      if (bpend & 1u) bulk_wait_s(0);
-      if (bpend & 2u) bulk_wait_s(1);
-    }
     cp_async_wait_all();
     __syncwarp();
     task = *(volatile long long *)(sched + warp);
@@ -819,7 +797,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   }
   if (a.fuse) {   // B = 1: one CTA, warp 0 ran the only task; it runs the insert's update
     if (gw == 0) {
-      uint8_t *us = smem + (size_t)WPC * a.wbytes + 24 * WPC;
+      uint8_t *us = smem + (size_t)WPC * a.wbytes + 16 * WPC;
       int32_t *usm = (int32_t *)(us + 16);
       uint32_t *uq = (uint32_t *)(us + 16 + update_one_smem(a.ub.hcap, a.ub.ballmax));
       BallArgs ub = a.ub;
@@ -891,7 +869,7 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   return (b + 15) & ~(size_t)15;
 }
 size_t search_smem_bytes(const SearchArgs &a, bool sets) {
-  return WPC * search_warp_bytes(a, sets) + 24 * WPC + fuse_bytes(a, sets) +
+  return WPC * search_warp_bytes(a, sets) + 16 * WPC + fuse_bytes(a, sets) +
          (a.kt ? 2 * (((a.n_t + (a.fuse ? a.nseq : 0)) * 4 + 15) & ~15ll) : 0) +
          (a.kt && a.srows ? (((a.n_t + (a.fuse ? a.nseq : 0)) * a.k * 4 + 15) & ~15ll) : 0);
 }

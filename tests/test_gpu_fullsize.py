@@ -96,7 +96,6 @@ _K1_PATHS = {
     # lane-form rows gathered by TMA bulk copies on the warp's mbarrier (one-stage plans)
     "bulk": {"KNNG_BULK": 1, "KNNG_ESMEM": 0},
     "bulk+smem-E+1stage": {"KNNG_BULK": 1, "KNNG_ESMEM": 1, "KNNG_NS2": 0},
-    "bulk+smem-E+2stages": {"KNNG_BULK2": 1, "KNNG_ESMEM": 1},
     "bulk+row-prefetch": {"KNNG_BULK": 1, "KNNG_ESMEM": 0, "KNNG_ROW_PF": 1},
     # sets: 4-chunk lane slots (most sets evaluated from global memory instead of the staged slot)
     "set-slots-4": {"KNNG_SET_SLOTCH": 4},
@@ -144,7 +143,6 @@ def test_long_walks_match_oracle(env, k, esmem, bulk):
     budget = pool (speedup 1); under every E-bit placement, with cp.async or bulk-copy gathers."""
     env("KNNG_ESMEM", esmem)
     env("KNNG_BULK", bulk)
-    env("KNNG_BULK2", bulk)
     X = _path_points(1500, 32)             # d = 32: a lane-form width (the bulk-copy gathers apply)
     g = _graph(X, k, 1600)
     o = O.OracleGraph(O.U8, X, k, capacity=1600)
