@@ -22,6 +22,9 @@
  *   or_key_of            pinned (closed forms, fp64 brute force)
  *   or_rng_draw          parity unpinned by the paper (Q4); pinned only by a
  *                        second, independent Python implementation (KAT)
+ *   or_rng_perm          (the restart draws, Q4) parity unpinned by the paper; pinned by an
+ *                        independent Python implementation (KAT), exhaustive bijection checks
+ *                        and a uniformity check of pi(0)
  *   or_exact_rows        pinned (hand examples, brute force in numpy)
  *   or_ignns_search      pinned (W3 hand traces, budget >= |pool| => linear search, a literal
  *                        re-derivation of the walk without the Q9 shortcut in tests/pyref.py);
@@ -274,6 +277,44 @@ uint64_t or_rng_draw(uint64_t seed, uint64_t pid, uint64_t part, uint64_t draw, 
   return (uint64_t)(prod >> 64);
 }
 
+/* Restart draws (reading Q4, round 2): the draws of one search are a pseudo-random PERMUTATION of the
+ * pool, pi(0), pi(1), ..., so a draw never repeats an earlier draw; a draw of a node a walk evaluated
+ * is still skipped for free.  pi is a 6-round (unbalanced) Feistel network on b = max(6, ceil(log2 m)) bits
+ * with cycle walking (apply F until the value is < m), keyed by the (seed, pid, part) prefix:
+ *   prefix = mix64(mix64(mix64(seed + G) ^ (pid + 2G)) ^ (part + 3G))
+ *   key_i  = (uint32)(prefix >> 16 (i mod 4)) ^ 0x9E3779B9 (i + 1)         (i = 0..5, 32-bit)
+ *   F(x):  L = x >> hr, R = x mod 2^hr (hl = b / 2, hr = b - hl bits);
+ *          round i: (L, R) <- (R, L ^ (lowbias32(R ^ key_i) mod 2^|L|))  (the halves swap widths)
+ * lowbias32(z): z ^= z >> 16; z *= 0x7feb352d; z ^= z >> 15; z *= 0x846ca68b; z ^= z >> 16. */
+static uint32_t lowbias32(uint32_t z) {
+  z ^= z >> 16; z *= 0x7feb352du; z ^= z >> 15; z *= 0x846ca68bu; z ^= z >> 16;
+  return z;
+}
+static uint32_t feistel(uint64_t prefix, uint32_t x, int hl, int hr) {
+  uint32_t L = x >> hr, R = x & ((1u << hr) - 1u);
+  int la = hl, ra = hr, i, t;
+  for (i = 0; i < 6; ++i) {
+    uint32_t key = (uint32_t)(prefix >> (16 * (i & 3))) ^ (0x9E3779B9u * (uint32_t)(i + 1));
+    uint32_t nR = L ^ (lowbias32(R ^ key) & ((1u << la) - 1u));
+    L = R; R = nR;
+    t = la; la = ra; ra = t;
+  }
+  return (L << ra) | R;
+}
+/* pi(j) for 0 <= j < m (m <= 2^31); -1 when j >= m (the pool is exhausted) */
+int64_t or_rng_perm(uint64_t seed, uint64_t pid, uint64_t part, uint64_t j, uint64_t m) {
+  uint64_t prefix = mix64(mix64(mix64(seed + 1ull * OR_GOLDEN) ^ (pid + 2ull * OR_GOLDEN)) ^ (part + 3ull * OR_GOLDEN));
+  int b = 0, hl, hr;
+  uint32_t x;
+  if (j >= m) return -1;
+  while ((1ull << b) < m) ++b;
+  if (b < 6) b = 6;                        /* tiny pools: walk down from 64 (a 4-bit Feistel mixes poorly) */
+  hl = b / 2; hr = b - hl;
+  x = (uint32_t)j;
+  do { x = feistel(prefix, x, hl, hr); } while (x >= m);
+  return (int64_t)x;
+}
+
 /* ------------------------------------------------------------------ */
 /* Neighbour list of capacity k, sorted by edge order.                 */
 /* ------------------------------------------------------------------ */
@@ -408,7 +449,8 @@ static void ignns(const or_search_cfg *C, or_point q, int64_t pid, int kr,
         if (j >= C->nstarts) goto done;    /* injected sequence exhausted */
         r = C->starts[j++];
       } else {
-        uint64_t idx = or_rng_draw(C->seed, (uint64_t)pid, (uint64_t)C->part, (uint64_t)j++, (uint64_t)C->m);
+        int64_t idx = or_rng_perm(C->seed, (uint64_t)pid, (uint64_t)C->part, (uint64_t)j++, (uint64_t)C->m);
+        if (idx < 0) goto done;            /* every pool node drawn (unreachable while c < m) */
         r = C->pool ? C->pool[idx] : (int32_t)idx;
       }
     } while (W->evaluated[r]);            /* Q4: redraw of an evaluated node is free */

@@ -46,6 +46,8 @@ def lib():
             L.or_rng_hash.argtypes = [u64, u64, u64, u64]
             L.or_rng_draw.restype = u64
             L.or_rng_draw.argtypes = [u64, u64, u64, u64, u64]
+            L.or_rng_perm.restype = C.c_int64
+            L.or_rng_perm.argtypes = [u64, u64, u64, u64, u64]
             L.or_budget.restype = i64
             L.or_budget.argtypes = [i64, i32, dbl]
             L.or_key.restype = C.c_uint32
@@ -151,6 +153,11 @@ def rng_hash(seed, pid, part, draw):
 
 def rng_draw(seed, pid, part, draw, m):
     return int(lib().or_rng_draw(seed, pid, part, draw, m))
+
+
+def rng_perm(seed, pid, part, j, m):
+    """Restart draw j of a search over a pool of m nodes (Q4: a pseudo-random permutation; -1 past m)."""
+    return int(lib().or_rng_perm(seed, pid, part, j, m))
 
 
 def budget(m, k, speedup):

@@ -433,6 +433,12 @@ static int plan_k1(knng_graph *g, SearchArgs &a, int64_t tasks, int64_t mmax) {
       }
     }
   }
+  // global E words: draws set no E bits and read their words only when the warp's W filter hits (perm_e;
+  // KNNG_PERM_E=0 restores E bits for every evaluation -- same results, measurement and tests)
+  // (vectors only: the set evaluators are ALU-bound and smem-limited, where the filter's 4 KB per warp and the
+  // pi^-1 per walk neighbour cost more than the E traffic saved -- C4 at 500k 24.1 vs 19.9 ms)
+  a.perm_e = !a.e_smem && !a.kt && a.starts == nullptr && !sets;
+  if (const char *e = getenv("KNNG_PERM_E")) a.perm_e = a.perm_e && atoi(e) != 0;
   // one-stage plans of the lane-form widths: the rows are gathered by the TMA engine (one bulk copy per row
   // on the warp's mbarrier instead of 16-byte cp.async per lane; measured C2 -3%, C3 at 2M -4.5%, C3 at 8M
   // equal: profiles/round2/k1_ab_bulk.txt); KNNG_BULK=0 restores the cp.async gathers (measurement, tests)

@@ -47,6 +47,78 @@ __device__ __forceinline__ uint64_t rng_index(uint64_t prefix, uint64_t draw, ui
   return __umul64hi(mix64(prefix ^ (draw + 4ull * GOLDEN)), m);
 }
 
+// Restart draws of a search (Q4, round 2): a pseudo-random permutation pi of the pool, so the draws of
+// one search never repeat each other.  6-round unbalanced Feistel network on b = max(6, ceil(log2 m))
+// bits (halves hl = b / 2 high, hr = b - hl low, swapping widths every round; round key i =
+// (uint32)(prefix >> 16 (i mod 4)) ^ 0x9E3779B9 (i + 1); round function lowbias32), cycle-walked into
+// [0, m).  Its inverse gives the draw position of a pool node, so a node's "drawn before" bit needs no
+// memory: pi^-1(v) <= the last draw processed.
+__device__ __forceinline__ uint32_t lowbias32(uint32_t z) {
+  z ^= z >> 16;
+  z *= 0x7feb352du;
+  z ^= z >> 15;
+  z *= 0x846ca68bu;
+  return z ^ (z >> 16);
+}
+struct Perm {
+  uint64_t pre;
+  uint32_t m;
+  int hl, hr;
+  __device__ __forceinline__ void init(uint64_t prefix, uint64_t m_) {
+    pre = prefix;
+    m = (uint32_t)m_;
+    int b = m_ > 1 ? 32 - __clz((unsigned)(m_ - 1)) : 0;
+    if (b < 6) b = 6;
+    hl = b >> 1;
+    hr = b - hl;
+  }
+  __device__ __forceinline__ uint32_t key(int i) const {
+    return (uint32_t)(pre >> (16 * (i & 3))) ^ (0x9E3779B9u * (uint32_t)(i + 1));
+  }
+  __device__ __forceinline__ uint32_t fwd(uint32_t x) const {
+    uint32_t L = x >> hr, R = x & ((1u << hr) - 1u);
+    int la = hl, ra = hr;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const uint32_t nR = L ^ (lowbias32(R ^ key(i)) & ((1u << la) - 1u));
+      L = R;
+      R = nR;
+      const int t = la;
+      la = ra;
+      ra = t;
+    }
+    return (L << ra) | R;
+  }
+  __device__ __forceinline__ uint32_t inv(uint32_t y) const {
+    uint32_t L = y >> hr, R = y & ((1u << hr) - 1u);
+    int la = hl, ra = hr;
+#pragma unroll
+    for (int i = 5; i >= 0; --i) {
+      const uint32_t R0 = L;
+      const uint32_t L0 = R ^ (lowbias32(R0 ^ key(i)) & ((1u << ra) - 1u));
+      L = L0;
+      R = R0;
+      const int t = la;
+      la = ra;
+      ra = t;
+    }
+    return (L << ra) | R;
+  }
+  // draw j (-1 past the pool)
+  __device__ __forceinline__ int32_t draw(int64_t j) const {
+    if (j >= (int64_t)m) return -1;
+    uint32_t x = (uint32_t)j;
+    do { x = fwd(x); } while (x >= m);
+    return (int32_t)x;
+  }
+  // the draw position of pool node v (< m)
+  __device__ __forceinline__ uint32_t pos(uint32_t v) const {
+    uint32_t y = v;
+    do { y = inv(y); } while (y >= m);
+    return y;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Key order.  U8: uint32 D; F32: fp32 D bits; JAC: (inter<<16)|union.
 // closer(a,b): a strictly more similar than b (metric value only).

@@ -113,6 +113,9 @@ struct SearchArgs {
   int x_smem;                  // (e_smem) 1: the X bitmap too (after E); KT launches always
   int ns2;                     // 1 (with e_smem): two chunk stages, chunk c + 1's rows in flight while c is processed
   int row_pf;                  // 1: a walk step copies the rows of all of cur's neighbours with their vectors
+  int perm_e;                  // 1 (global E words): draws set no E bits (the permutation draws never repeat and a
+                               // walk neighbour's "drawn before" is pi^-1(v) <= the last processed draw); the
+                               // words hold the walk evaluations, filtered per warp in shared memory
                                // (0: the chosen neighbour's row is loaded once the move is known)
   int full_scan;               // 1: the GNNS baseline walk (all k neighbours, move to the best)
   int bulk;                    // 1 (lane-form widths, one chunk stage): rows gathered by TMA bulk copies

@@ -68,6 +68,17 @@ __device__ __forceinline__ void cpa_n(unsigned sa, const void *gsrc, int bytes) 
   else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc) : "memory");
 }
 
+// W filter of a dsk task (shared, WFLT_WORDS words): one bit per hashed pool index of the walk evaluations
+constexpr int WFLT_WORDS = 1024;
+__device__ __forceinline__ uint32_t wflt_h(int32_t i) { return ((uint32_t)i * 0x9E3779B1u) >> 17; }   // 15 bits
+__device__ __forceinline__ bool wflt_test(const uint32_t *f, int32_t i) {
+  const uint32_t h = wflt_h(i);
+  return ((f[h >> 5] >> (h & 31)) & 1u) != 0;
+}
+__device__ __forceinline__ void wflt_set(uint32_t *f, int32_t i) {
+  const uint32_t h = wflt_h(i);
+  atomicOr(f + (h >> 5), 1u << (h & 31));
+}
 // E / X planes of a task: word w holds the evaluated bits (E) of pool nodes 16w..16w+15 in its low
 // half and their expanded bits (X) in its high half.
 __device__ __forceinline__ uint32_t pw(int32_t pidx) { return (uint32_t)pidx >> 4; }
@@ -231,6 +242,10 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   const bool es = KT || a.e_smem != 0;                                     // E bitmap in shared memory
   const bool ns2 = !KT && !csr_metric(M) && es && a.ns2 != 0;                  // two chunk stages (needs es)
   const bool xs = es && (KT || a.x_smem != 0);                             // X bitmap in shared memory too
+  // perm_e (global E words, permutation draws): draws set no E bits -- a walk neighbour's "drawn before" is
+  // pi^-1(v) <= the last processed draw -- so the words hold the WALK evaluations W only, and a draw reads
+  // its word only when the warp's shared filter of W (one bit per hashed pool index) says it may be in W
+  const bool dsk = !es && a.perm_e != 0 && a.starts == nullptr;
   // ---- this warp's shared memory (a.wbytes each; search_warp_bytes) ----
   uint8_t *wsm = smem + (size_t)warp * a.wbytes;
   uint8_t *stage = wsm;                                                   // [32][pitch] draw rows / set slots
@@ -243,6 +258,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
   uint32_t *qscr = (uint32_t *)(pid + 32);                                // [QSCR] query tokens + table (sets)
   uint8_t *jwp = (uint8_t *)(qscr + (csr_metric(M) ? QSCR : 0));            // [32][JW_PTR] JW character pointers
   uint32_t *ebits = (uint32_t *)(jwp + (M == M_JW ? 32 * JW_PTR : 0));      // [e_bytes / 4] E bitmap (es)
+  uint32_t *wflt = ebits;                                                  // [WFLT_WORDS] W filter (dsk; !es)
   long long *sched = (long long *)(smem + (size_t)WPC * a.wbytes);         // [WPC] next task per warp
   uint64_t *mbar = (uint64_t *)(sched + WPC) + warp;                       // (BK) the warp's bulk-copy barrier
   uint32_t bph = 0;                                                        // (BK) its phase
@@ -321,6 +337,10 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       uint4 *e4 = (uint4 *)ebits;
       for (int w = lane; w < (a.e_bytes >> (xs ? 3 : 4)); w += 32) e4[w] = make_uint4(0, 0, 0, 0);
     }
+    if (dsk) {
+      uint4 *f4 = (uint4 *)wflt;
+      for (int w = lane; w < WFLT_WORDS / 4; w += 32) f4[w] = make_uint4(0, 0, 0, 0);
+    }
     if (!xs) {
       const int64_t nw = (m + 15) >> 4;
       uint4 *p4 = (uint4 *)planes;
@@ -363,8 +383,10 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         const int32_t nd = j < a.nstarts ? a.starts[j] : -1;
         return make_int2(nd, nd);
       }
-      const uint64_t idx = rng_index(h3, (uint64_t)j, (uint64_t)m);
-      return make_int2((int32_t)idx, (int32_t)idx);
+      Perm pm;
+      pm.init(h3, (uint64_t)m);
+      const int32_t idx = pm.draw(j);
+      return make_int2(idx, idx);
     };
     // ---- the draw of a chunk: issue(d) copies the drawn rows into the stage (sets: each lane its token
     // range) and returns the E word of each draw, read in the same round trip.
@@ -391,7 +413,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           if (id >= 0) cpa16(sb0 + r * pitch + 16 * t, base + (size_t)id * stride + 16 * t);
         }
       }
-      return (!es && d.x >= 0) ? g_ld(planes + pw(d.x)) : 0u;
+      return (!es && d.x >= 0 && (!dsk || wflt_test(wflt, d.x))) ? g_ld(planes + pw(d.x)) : 0u;
     };
     // the E bit of pool node i: set / test (shared bitmap, or the low halves of the global words)
     auto e_set = [&](int32_t i) {
@@ -526,7 +548,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         thr_update();
         if (top.cnt > 0 && inv == 0 && c + __popc(fm) <= budget && !__any_sync(FULL, fr && !thr.skip(wkey))) {
           KPROF(const long long tq2 = clock64(); c_ph[4] += tq2 - tq1;)
-          if (fr) e_set(wl);
+          if (fr && !dsk) e_set(wl);
           top.insert(fr, wkey, wnode);             // Q5: skipped starts enter the top-k
           const int nf = __popc(fm);
           c += nf;
@@ -599,7 +621,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
       const int al = am ? __ffs(am) - 1 : -1;
       const unsigned commit = am ? (cm & (al == 31 ? FULL : ((2u << al) - 1u))) : cm;
       const bool cmt = (commit >> lane) & 1u;
-      if (cmt) e_set(wl);
+      if (cmt && !dsk) e_set(wl);
       top.insert(cmt, wkey, wnode);          // Q5: skipped starts enter the top-k too
       const int ncm = __popc(commit);
       c += ncm;
@@ -615,6 +637,7 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         continue;
       }
       wpos = al + 1;
+      const int64_t jw = (ch - 1) * 32 + al;   // (dsk) the accepted start's draw position: every draw up to it is processed
 
       // ------------------- hill climbing, eager first improvement -------------------
       // One memory round trip per step: the vectors (lane-form widths) and E / X words of cur's in-pool
@@ -706,7 +729,12 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
           cp_async_wait_all();
           __syncwarp();
         }
-        const bool evb2 = !inpool || (es ? e_smem_test(lv) : (xw & e_bit(lv)) != 0);
+        bool evb2 = !inpool || (es ? e_smem_test(lv) : (xw & e_bit(lv)) != 0);
+        if (dsk && !evb2) {   // drawn before: its draw position is at most the accepted start's
+          Perm pm;
+          pm.init(h3, (uint64_t)m);
+          evb2 = (int64_t)pm.pos((uint32_t)lv) <= jw;
+        }
         const bool imp = inpool && closer<M>(key, kcur);
         KPROF(long long ts2 = clock64(); c_ph[1] += ts2 - ts1;)
         const unsigned im = __ballot_sync(FULL, imp);
@@ -739,7 +767,10 @@ __global__ void __launch_bounds__(32 * WPC, MB) k_search(SearchArgs a) {
         if ((int64_t)__popc(fm2) > budget - c) { fm2 = first_bits(fm2, (int)(budget - c)); hit2 = true; }
         const bool cm2 = (fm2 >> lane) & 1u;
         const int nf2 = __popc(fm2);
-        if (cm2) e_set(lv);
+        if (cm2) {
+          e_set(lv);
+          if (dsk) wflt_set(wflt, lv);
+        }
         if (pn + nf2 > 32) flush();
         if (cm2) {
           const int q = pn + __popc(fm2 & lanemask_lt());
@@ -865,7 +896,8 @@ size_t search_warp_bytes(const SearchArgs &a, bool sets) {
   size_t b = (size_t)(ns2 ? 64 : 32) * a.pitch + (a.row_pf ? ((a.k * RB + 15) & ~(size_t)15) : 0) +
              ((WPF * RB + 15) & ~(size_t)15) + 512 + 2 * 32 * 4 + (sets ? QSCR * 4 : 0) +
              (a.metric == M_JW ? 32 * JW_PTR : 0) +
-             (a.e_smem ? (size_t)a.e_bytes * ((a.x_smem || a.kt) ? 2 : 1) : 0);
+             (a.e_smem ? (size_t)a.e_bytes * ((a.x_smem || a.kt) ? 2 : 1) : 0) +
+             (!a.e_smem && a.perm_e ? (size_t)WFLT_WORDS * 4 : 0);
   return (b + 15) & ~(size_t)15;
 }
 size_t search_smem_bytes(const SearchArgs &a, bool sets) {

@@ -44,6 +44,37 @@ def rng_draw(seed, pid, part, draw, m):
     return (rng_hash(seed, pid, part, draw) * m) >> 64
 
 
+def _lowbias32(z):
+    for sh, mul in ((16, 0x7FEB352D), (15, 0x846CA68B)):
+        z = ((z ^ (z >> sh)) * mul) % 2**32
+    return z ^ (z >> 16)
+
+
+def rng_perm(seed, pid, part, j, m):
+    """Restart draw j of a search over m pool nodes (reading Q4, round 2): a 6-round Feistel permutation
+    of the b-bit integers (b = max(6, bits of m - 1)), halves of b // 2 (high) and b - b // 2 (low) bits that
+    swap widths every round, cycle-walked into [0, m).  Written from DESIGN.md's statement, not from
+    the oracle's C."""
+    if j >= m:
+        return -1
+    b = max(6, (m - 1).bit_length())
+    h = mix64((seed + GOLDEN) & M64)
+    h = mix64(h ^ ((pid + 2 * GOLDEN) & M64))
+    pre = mix64(h ^ ((part + 3 * GOLDEN) & M64))
+    keys = [((pre >> (16 * (i % 4))) % 2**32) ^ ((0x9E3779B9 * (i + 1)) % 2**32) for i in range(6)]
+    widths = [b // 2, b - b // 2]           # [left, right]
+    x = j
+    while True:
+        left, right = divmod(x, 2 ** widths[1])
+        wl, wr = widths
+        for key in keys:
+            f = _lowbias32(right ^ key) % 2 ** wl
+            left, right, wl, wr = right, left ^ f, wr, wl
+        x = left * 2 ** wr + right
+        if x < m:
+            return x
+
+
 # ---------------------------------------------------------------------------
 # Exact metric values.  L2: D as an exact integer / Fraction (inputs are integer-valued, so the
 # fp32 canonical sum of the oracle is exact too); Jaccard: (inter, union).
@@ -131,7 +162,7 @@ def ignns_literal(metric, point, rows, q, kr, speedup, e_num, e_den, seed, pid, 
                     return _finish(metric, val, kr, st, c)
                 r = starts[j]
             else:
-                r = pool[rng_draw(seed, pid, part, j, m)]
+                r = pool[rng_perm(seed, pid, part, j, m)]
             j += 1
             if r not in val:
                 break

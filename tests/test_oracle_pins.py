@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
+from tests import pyref as R
 from datagen import line_points
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -221,6 +222,39 @@ def test_rng_uniformity():
         counts[O.rng_draw(2001, 12345, 0, j, m)] += 1
     chi2 = ((counts - N / m) ** 2 / (N / m)).sum()
     assert chi2 < 40  # 15 dof; p ~ 5e-4
+
+
+def test_rng_perm_known_answers_python_reimplementation():
+    """Restart draws (Q4, round 2): the oracle's Feistel permutation equals tests/pyref.py's
+    independent implementation of DESIGN.md's statement, including m = 1, powers of two and their
+    neighbours, and j >= m (-1)."""
+    rng = np.random.default_rng(11)
+    ms = [1, 2, 3, 4, 5, 7, 8, 9, 255, 256, 257, 4096, 4097, 62500, 1 << 20, 1050000, (1 << 31) - 1]
+    for t in range(600):
+        m = ms[t % len(ms)] if t < 200 else int(rng.integers(1, 1 << 31))
+        s, pid = (int(x) for x in rng.integers(0, 2 ** 62, 2))
+        part = int(rng.integers(0, 8))
+        j = int(rng.integers(0, m + 3))
+        assert O.rng_perm(s, pid, part, j, m) == R.rng_perm(s, pid, part, j, m)
+    assert O.rng_perm(1, 2, 3, 5, 5) == -1 and O.rng_perm(1, 2, 3, 0, 1) == 0
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 6, 64, 65, 127, 500, 549, 1000, 4097])
+def test_rng_perm_is_a_permutation(m):
+    """Every pool node is drawn exactly once in m draws (so a draw never repeats an earlier draw)."""
+    for s, pid, part in ((2000, 0, 0), (2003, 12345, 7)):
+        v = sorted(O.rng_perm(s, pid, part, j, m) for j in range(m))
+        assert v == list(range(m))
+
+
+def test_rng_perm_first_draw_uniform():
+    """The first draw pi(0) over many searches (pids) is uniform over the pool."""
+    m, N = 13, 26000
+    counts = np.zeros(m)
+    for pid in range(N):
+        counts[O.rng_perm(2001, pid, 0, 0, m)] += 1
+    chi2 = ((counts - N / m) ** 2 / (N / m)).sum()
+    assert chi2 < 40  # 12 dof; p ~ 1e-4
 
 
 # ---------------------------------------------------------------------------
